@@ -1,0 +1,351 @@
+#!/usr/bin/env python
+"""Benchmark of the sWLR per-iteration update (BASELINE.json metric: "WLR iterations/sec
+and achieved HBM GB/s at m x n = 19200 x 600, 1/2/4/8 B200").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 3]
+
+A "step" is one sWLR iteration (X1 half-step + (C, D) half-step) over
+the whole synthetic QVGA scene (BASELINE configs[2]: m=19200, n=600, k=30, r=32, fp32,
+uniform W1 = 100, GHS init).  Inputs are resident in HBM when the timed region starts; A
+(46 MB) is smaller than L2, so L2 is flushed (256 MB write) before every timed step and
+each step is timed alone with CUDA events on the library's stream.  For N > 1 the pixel
+rows are sharded across ranks (one process per GPU, torchrun) and the fp64 Gram
+increments are all-reduced with NCCL inside the library; the job-wide iteration rate is
+K / max over ranks of the summed step time.
+
+``--impl reference`` times the fp64 CPU oracle (``oracle/``, the literal Algorithm 1) on
+the host cores, on a bounded sample of the same workload (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import dataclasses
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12    # CUDA-core FP32
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def row_pass_flops(cfg):
+    k, r, nk, t = cfg.k, cfg.r, cfg.n - cfg.k, cfg.r - cfg.k
+    solve = 2 * k * k if cfg.uniform_w else k ** 3 // 3 + 2 * k * k
+    return cfg.m * (2 * nk * r + 4 * k * t + 3 * k + solve)
+
+
+def incr_flops(cfg):
+    k, nk = cfg.k, cfg.n - cfg.k
+    return cfg.m * 2 * k * (nk + 2 * k)
+
+
+def iteration_bytes(cfg):
+    s = 4 if cfg.dtype == "f32" else 8
+    return s * cfg.m * (cfg.n + 2 * cfg.k + (0 if cfg.uniform_w else cfg.k))
+
+
+def ncu_traffic(kernel_key):
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(kernel_key, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------------ reference arm
+def run_reference(args, cfg, world, rank):
+    if rank != 0:
+        return 0
+    sys.path.insert(0, ROOT)
+    import oracle
+    from threadpoolctl import threadpool_info
+    A = synth.make_A(cfg).astype(np.float64)
+    W1 = synth.dense_W1(cfg, synth.make_W1(cfg), cfg.m)
+    threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+    t_steps = []
+    # bounded sample: GHS init + iterations until ~20 s of CPU work (>= 1 iteration)
+    t0 = time.perf_counter()
+    a1, a2 = A[:, :cfg.k], A[:, cfg.k:]
+    c, d, _ = oracle.cd_step(a1.copy(), a2, cfg.r)
+    t_init = time.perf_counter() - t0
+    x1 = a1.copy()
+    budget = 20.0
+    while True:
+        ts = time.perf_counter()
+        x1 = oracle.x1_step(a1, a2, W1, c, d)
+        c, d, _ = oracle.cd_step(x1, a2, cfg.r)
+        t_steps.append(time.perf_counter() - ts)
+        if sum(t_steps) > budget or len(t_steps) >= max(args.steps, 1):
+            break
+    ms = 1e3 * statistics.mean(t_steps)
+    val = 1e3 / ms
+    line = {
+        "impl": "reference", "metric": "WLR iterations/sec", "value": val, "unit": "iter/s",
+        "n_gpus": world, "steps": len(t_steps), "warmup": 0, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": cfg.name + " (BASELINE configs[2])", "m": cfg.m,
+                                         "n": cfg.n, "k": cfg.k, "r": cfg.r, "init": "GHS"},
+        "cpu_baseline": {"value": val, "unit": "iter/s", "cores": threads, "kind": "oracle",
+                         "sample": f"GHS init ({t_init:.2f}s) + {len(t_steps)} literal Algorithm-1 "
+                                   f"iterations (QR + thin SVD + m row solves) of the full scene"},
+        "e2e": {"value": val, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline_sample(cfg, seconds=15.0):
+    """The oracle as it stands, timed on this host on a bounded sample (rank 0, N=1)."""
+    import oracle
+    from threadpoolctl import threadpool_info
+    A = synth.make_A(cfg).astype(np.float64)
+    W1 = synth.dense_W1(cfg, synth.make_W1(cfg), cfg.m)
+    a1, a2 = A[:, :cfg.k], A[:, cfg.k:]
+    c, d, _ = oracle.cd_step(a1.copy(), a2, cfg.r)
+    ts = []
+    while sum(ts) < seconds and len(ts) < 50:
+        t0 = time.perf_counter()
+        x1 = oracle.x1_step(a1, a2, W1, c, d)
+        c, d, _ = oracle.cd_step(x1, a2, cfg.r)
+        ts.append(time.perf_counter() - t0)
+    threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+    return {"value": 1.0 / statistics.mean(ts), "unit": "iter/s", "cores": threads, "kind": "oracle",
+            "sample": f"{len(ts)} literal Algorithm-1 iterations (fp64 QR + thin SVD + m row solves) "
+                      f"of the full {cfg.m}x{cfg.n} scene after the GHS step"}
+
+
+# ------------------------------------------------------------------------------ our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    cfg = synth.CONFIGS[args.config]
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, cfg, world, rank)
+
+    import torch
+    import paper_1703_06303_b200 as w
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.Stream()           # non-default stream shared by torch and libwlr
+    torch.cuda.set_stream(stream)
+
+    r0, r1 = synth.shard_rows(cfg.m, world, rank)
+    A = torch.from_numpy(synth.make_A(cfg, r0, r1)).cuda()
+    W1n = synth.make_W1(cfg, r0, r1)
+    W1 = None if W1n is None else torch.from_numpy(W1n).cuda()
+    nccl_id = None
+    if world > 1:
+        obj = [w.wlr_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    h = w.wlr_init(A, cfg.k, cfg.r, W1, w1=cfg.w_const or 1.0, m_global=cfg.m, row_offset=r0,
+                   nranks=world, rank=rank, nccl_id=nccl_id, stream=stream.cuda_stream)
+    torch.cuda.synchronize()
+    t_init = time.perf_counter() - t0
+
+    w.wlr_iterate_async(h, args.warmup)
+    w.wlr_sync(h)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    w.wlr_profile(h, enable=True, reset=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(K):
+            flush.fill_(float(i))                      # evict A from L2 (untimed)
+            ev[i][0].record(stream)
+            w.wlr_iterate_async(h, 1)
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    prof = w.wlr_profile(h, enable=False, reset=False)
+    w.wlr_sync(h)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    tot_ms = sum(step_ms)
+    if dist:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    ms_per_step = tot_ms / K
+    value = 1e3 / ms_per_step
+    F, step_norm, rel = w.wlr_objective(h)
+
+    # dominant kernel of the step and its roofline
+    iters = max(prof["iters"], 1)
+    kern_ms = {"row_pass": prof["row_pass"] / iters, "increments": prof["increments"] / iters,
+               "reduce": prof["reduce"] / iters, "small_step": prof["small_step"] / iters}
+    cfg_local = dataclasses.replace(cfg, m=r1 - r0)
+    flops = {"row_pass": row_pass_flops(cfg_local), "increments": incr_flops(cfg_local)}
+    dom = max(("row_pass", "increments"), key=lambda kk: kern_ms[kk])
+    peaks, peak_kind = measured_peaks()
+    achieved = flops[dom] / (kern_ms[dom] * 1e-3) / 1e12
+    roof = {"kernel": dom, "bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS,
+            "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS,
+            "peak_source": "derived CUDA-core FP32: 148 SM x 128 lanes x 2 x 1.965 GHz (DESIGN.md §6)",
+            "traffic": ncu_traffic(dom),
+            "kernel_ms": kern_ms,
+            "kernel_share_of_step": {kk: v / ms_per_step for kk, v in kern_ms.items()}}
+    alg_gbs = iteration_bytes(cfg_local) / (ms_per_step * 1e-3) / 1e9
+
+    # end-to-end through the C ABI with HOST buffers: H2D of A (pinned) + init +
+    # cfg.iters iterations + D2H of the result, per solve
+    e2e = None
+    if not args.no_e2e:
+        Ah = torch.from_numpy(synth.make_A(cfg, r0, r1)).pin_memory()
+        Wh = None if W1n is None else torch.from_numpy(W1n).pin_memory()
+        solves, its = 2, cfg.iters
+        e_ms = []
+        for s in range(solves + 1):
+            if dist:
+                dist.barrier()
+            torch.cuda.synchronize()
+            ts = time.perf_counter()
+            he = w.wlr_init(Ah, cfg.k, cfg.r, Wh, w1=cfg.w_const or 1.0, m_global=cfg.m, row_offset=r0,
+                            nranks=world, rank=rank, nccl_id=nccl_id, stream=stream.cuda_stream)
+            w.wlr_iterate_async(he, its)
+            res = w.wlr_result(he, x2=False)
+            torch.cuda.synchronize()
+            if s > 0:
+                e_ms.append((time.perf_counter() - ts) * 1e3)
+            w.wlr_destroy(he)
+        if dist:
+            t = torch.tensor([statistics.mean(e_ms)], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            emax = float(t.item())
+        else:
+            emax = statistics.mean(e_ms)
+        d2h = sum(v.nbytes for v in res.values() if v is not None)
+        e2e = {"value": its / (emax * 1e-3), "unit": "iter/s",
+               "h2d_bytes_per_step": int(Ah.numel() * Ah.element_size() + (0 if Wh is None else Wh.numel() * Wh.element_size())),
+               "d2h_bytes_per_step": int(d2h),
+               "step": f"one full solve from pinned host A: H2D + GHS init + {its} iterations + D2H(X1, C, B, D)",
+               "ms_per_solve": emax}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_sample(cfg)
+
+    if rank == 0:
+        line = {
+            "metric": "WLR iterations/sec", "value": value, "unit": "iter/s", "n_gpus": world,
+            "steps": K, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32" if cfg.dtype == "f32" else "f64",
+            "data": "synthetic (seeded scene generator, synth/)",
+            "config": {"workload": f"{cfg.name} (BASELINE configs[2]): m={cfg.m} (120x160), n={cfg.n}, "
+                                   f"k={cfg.k}, r={cfg.r}, W1={cfg.w_const}, GHS init",
+                       "l2": "flushed before every timed step (256 MB write); steps timed individually",
+                       "parallelism": f"row-sharded x{world}" if world > 1 else "1 GPU"},
+            "achieved_hbm_gbs_algorithmic": alg_gbs,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": prof["launches"],
+            "clocks": clk.summary(),
+            "init_ms": t_init * 1e3,
+            "final": {"F": F, "step": step_norm, "rel": rel},
+            "peaks_source": peak_kind,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

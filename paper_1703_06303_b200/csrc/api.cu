@@ -1,0 +1,813 @@
+// api.cu -- the C ABI of libwlr.so (include/wlr.h) and the host-side state machine.
+//
+// One wlr_init builds the initial canonical state X_0 (GHS / Theorem 1 when X1_0 = A1,
+// PAPER.md:56-65).  Every iteration then enqueues, on the handle's stream:
+//     K2a row pass  -> K2b Gram-increment GEMM -> K2c fixed-order reduce
+//     -> [ncclAllReduce of the packed fp64 increments when rows are sharded]
+//     -> K3 small step (one thread-block cluster)
+// optionally captured once per buffer parity as a CUDA graph and replayed.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/wlr.h"
+#include "kernels.h"
+
+using namespace wlr;
+
+namespace {
+
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*errStr)(ncclResult_t) = nullptr;
+  bool load(std::string& err) {
+    if (h) return true;
+    h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) { err = "cannot dlopen libnccl.so.2"; return false; }
+    getUniqueId = (decltype(getUniqueId))dlsym(h, "ncclGetUniqueId");
+    commInitRank = (decltype(commInitRank))dlsym(h, "ncclCommInitRank");
+    allReduce = (decltype(allReduce))dlsym(h, "ncclAllReduce");
+    commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
+    errStr = (decltype(errStr))dlsym(h, "ncclGetErrorString");
+    if (!getUniqueId || !commInitRank || !allReduce || !commDestroy) {
+      err = "libnccl is missing symbols";
+      return false;
+    }
+    return true;
+  }
+};
+NcclApi g_nccl;
+
+thread_local std::string g_err;
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+struct Profile {
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  double ms[4] = {0, 0, 0, 0};
+  int64_t launches = 0, iters = 0;
+};
+
+}  // namespace
+
+struct wlr_ctx {
+  // dimensions
+  int64_t m = 0, n = 0, k = 0, r = 0, t = 0, nk = 0, kp = 0, k0 = 0;
+  int64_t m_global = 0, row_offset = 0;
+  int dtype = WLR_F32;
+  size_t es = 4;
+  bool uniform = true;
+  double w1s = 1.0;
+  int b = 0, rp = 0, bm = 0, nz = 0, nsplit = 0, rp_grid = 0, CL = 0, ss_flags = 0;
+  int64_t rps = 0, xstride = 0;
+  size_t ss_smem = 0;
+  int nsm = 148;
+  wlr_opts opts;
+  // data
+  const void* A = nullptr; int64_t lda = 0;
+  const void* W1 = nullptr; int64_t ldw = 0;
+  void* X[2] = {nullptr, nullptr};
+  void *Wt = nullptr, *CVop = nullptr, *Kop = nullptr;
+  double *inc_part = nullptr, *fw_part = nullptr, *inc = nullptr, *fw0 = nullptr;
+  double* GA = nullptr;
+  double a2sq = 0.0;
+  double *G[2] = {nullptr, nullptr}, *M[2] = {nullptr, nullptr}, *C[2] = {nullptr, nullptr};
+  double *Vprev = nullptr, *CVprev = nullptr, *Y = nullptr, *Z = nullptr, *Y1 = nullptr,
+         *Y2 = nullptr, *theta = nullptr;
+  double *xchg = nullptr, *red = nullptr, *scal = nullptr, *trace = nullptr;
+  int trace_cap = 4096;
+  int* flags = nullptr;
+  int* h_flags = nullptr;
+  double* h_scal = nullptr;
+  cudaStream_t st = nullptr;
+  bool own_stream = false;
+  int par = 0;                 // parity of the current state (= p mod 2)
+  int64_t p = 0;               // index of the current canonical state
+  cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+  ncclComm_t comm = nullptr;
+  bool prof = false;
+  Profile pr;
+  std::string err;
+  std::vector<void*> allocs;
+};
+
+static wlr_status fail(wlr_ctx* h, wlr_status s, const std::string& msg) {
+  if (h) h->err = msg;
+  g_err = msg;
+  return s;
+}
+
+#define CUDA_TRY(h, x)                                                                       \
+  do {                                                                                       \
+    cudaError_t e_ = (x);                                                                    \
+    if (e_ != cudaSuccess)                                                                   \
+      return fail(h, e_ == cudaErrorMemoryAllocation ? WLR_ENOMEM : WLR_ECUDA,               \
+                  std::string(#x) + ": " + cudaGetErrorString(e_));                          \
+  } while (0)
+
+static wlr_status dalloc(wlr_ctx* h, void** p, size_t bytes) {
+  cudaError_t e = cudaMalloc(p, bytes ? bytes : 16);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(h, WLR_ENOMEM, std::string("cudaMalloc failed: ") + cudaGetErrorString(e));
+  }
+  h->allocs.push_back(*p);
+  e = cudaMemsetAsync(*p, 0, bytes ? bytes : 16, h->st);
+  if (e != cudaSuccess) return fail(h, WLR_ECUDA, cudaGetErrorString(e));
+  return WLR_OK;
+}
+template <typename P>
+static wlr_status dalloc_t(wlr_ctx* h, P** p, size_t count) {
+  return dalloc(h, reinterpret_cast<void**>(p), count * sizeof(P));
+}
+
+static wlr_status check_flags(wlr_ctx* h) {
+  CUDA_TRY(h, cudaMemcpyAsync(h->h_flags, h->flags, 8 * sizeof(int), cudaMemcpyDeviceToHost, h->st));
+  CUDA_TRY(h, cudaMemcpyAsync(h->h_scal, h->scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+  CUDA_TRY(h, cudaStreamSynchronize(h->st));
+  switch (h->h_flags[0]) {
+    case DF_OK: break;
+    case DF_RANK: return fail(h, WLR_ERANK, "X1 is numerically rank deficient (Cholesky of X1^T X1 failed)");
+    case DF_EIG: return fail(h, WLR_EEIG, "top-(r-k) eigensolver exceeded its iteration budget");
+    case DF_ROWSPD: return fail(h, WLR_EINTERNAL, "a row system diag(W1^2)+CC^T was not SPD");
+    case DF_NONFINITE: return fail(h, WLR_ENONFINITE, "non-finite objective");
+    default: return fail(h, WLR_EINTERNAL, "unknown device flag");
+  }
+  h->p = (int64_t)llround(h->h_scal[5]);
+  h->par = (int)(h->p & 1);
+  return WLR_OK;
+}
+
+// ------------------------------------------------------------------------ one iteration
+static cudaEvent_t prof_event(wlr_ctx* h) {
+  if (h->pr.used == h->pr.pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    h->pr.pool.push_back(e);
+  }
+  return h->pr.pool[h->pr.used++];
+}
+
+static wlr_status enqueue_iteration(wlr_ctx* h, int par) {
+  const int cur = par, nxt = par ^ 1;
+  cudaEvent_t ev[6] = {};
+  const bool prof = h->prof;
+  if (prof) {
+    for (int i = 0; i < 6; ++i) ev[i] = prof_event(h);
+    cudaEventRecord(ev[0], h->st);
+  }
+  cudaError_t e;
+  if (h->dtype == WLR_F32) {
+    RowPassArgs<float> a{};
+    a.A = (const float*)h->A; a.lda = h->lda; a.W1 = (const float*)h->W1; a.ldw = h->ldw;
+    a.w2s = (float)(h->w1s * h->w1s);
+    a.Xold = (const float*)h->X[cur]; a.Xnew = (float*)h->X[nxt];
+    a.Wt = (const float*)h->Wt; a.CV = (const float*)h->CVop; a.Kmat = (const float*)h->Kop;
+    a.fw_part = h->fw_part; a.flags = h->flags;
+    a.m = h->m; a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.k0 = (int)h->k0; a.t = (int)h->t;
+    a.vec_ok = (h->lda % 4 == 0) && ((uintptr_t)h->A % 16 == 0);
+    e = launch_row_pass<float>(a, h->rp, h->uniform, 0, h->rp_grid, h->st);
+  } else {
+    RowPassArgs<double> a{};
+    a.A = (const double*)h->A; a.lda = h->lda; a.W1 = (const double*)h->W1; a.ldw = h->ldw;
+    a.w2s = h->w1s * h->w1s;
+    a.Xold = (const double*)h->X[cur]; a.Xnew = (double*)h->X[nxt];
+    a.Wt = (const double*)h->Wt; a.CV = (const double*)h->CVop; a.Kmat = (const double*)h->Kop;
+    a.fw_part = h->fw_part; a.flags = h->flags;
+    a.m = h->m; a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.k0 = (int)h->k0; a.t = (int)h->t;
+    a.vec_ok = (h->lda % 4 == 0) && ((uintptr_t)h->A % 16 == 0);
+    e = launch_row_pass<double>(a, h->rp, h->uniform, 0, h->rp_grid, h->st);
+  }
+  if (e != cudaSuccess) return fail(h, WLR_ECUDA, std::string("row pass: ") + cudaGetErrorString(e));
+  if (prof) cudaEventRecord(ev[1], h->st);
+  if (h->dtype == WLR_F32) {
+    IncrArgs<float> a{};
+    a.A = (const float*)h->A; a.lda = h->lda;
+    a.Xold = (const float*)h->X[cur]; a.Xnew = (const float*)h->X[nxt];
+    a.part = h->inc_part; a.m = h->m; a.rows_per_split = h->rps;
+    a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.k0 = (int)h->k0; a.nz = h->nz; a.nsplit = h->nsplit;
+    a.vec_ok = (h->lda % 4 == 0) && ((uintptr_t)h->A % 16 == 0) && (h->n % 4 == 0);
+    e = launch_incr<float>(a, h->bm, h->st);
+  } else {
+    IncrArgs<double> a{};
+    a.A = (const double*)h->A; a.lda = h->lda;
+    a.Xold = (const double*)h->X[cur]; a.Xnew = (const double*)h->X[nxt];
+    a.part = h->inc_part; a.m = h->m; a.rows_per_split = h->rps;
+    a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.k0 = (int)h->k0; a.nz = h->nz; a.nsplit = h->nsplit;
+    a.vec_ok = (h->lda % 4 == 0) && ((uintptr_t)h->A % 16 == 0) && (h->n % 4 == 0);
+    e = launch_incr<double>(a, h->bm, h->st);
+  }
+  if (e != cudaSuccess) return fail(h, WLR_ECUDA, std::string("increments: ") + cudaGetErrorString(e));
+  if (prof) cudaEventRecord(ev[2], h->st);
+  launch_reduce_incr(h->inc_part, h->nsplit, (int)h->k, (int)h->nk, h->nz, (int)(h->k - h->k0),
+                     (int)(h->n - h->k0), (int)h->kp, h->fw_part, h->rp_grid, h->inc, h->st);
+  if (prof) cudaEventRecord(ev[3], h->st);
+  if (h->comm) {
+    const size_t cnt = (size_t)(h->k * h->nk + 2 * h->k * h->k + 1);
+    ncclResult_t nr = g_nccl.allReduce(h->inc, h->inc, cnt, ncclFloat64, ncclSum, h->comm, h->st);
+    if (nr != ncclSuccess) return fail(h, WLR_ENCCL, std::string("ncclAllReduce: ") + g_nccl.errStr(nr));
+  }
+  if (prof) cudaEventRecord(ev[4], h->st);
+  SmallArgs s{};
+  s.k = (int)h->k; s.nk = (int)h->nk; s.t = (int)h->t; s.b = h->b; s.kp = (int)h->kp;
+  s.k0 = (int)h->k0; s.rp = h->rp; s.mode = 1; s.dtype = h->dtype == WLR_F64 ? 1 : 0;
+  s.uniform = h->uniform ? 1 : 0; s.w2 = h->w1s * h->w1s;
+  s.GA = h->GA; s.a2sq = h->a2sq; s.inc = h->inc;
+  s.G_in = h->G[cur]; s.G_out = h->G[nxt]; s.M_in = h->M[cur]; s.M_out = h->M[nxt];
+  s.C_in = h->C[cur]; s.C_out = h->C[nxt];
+  s.Vprev = h->Vprev; s.CVprev = h->CVprev; s.Y = h->Y; s.Z = h->Z; s.Y1 = h->Y1; s.Y2 = h->Y2;
+  s.theta = h->theta; s.xchg = h->xchg; s.xchg_stride = h->xstride; s.red = h->red; s.scal = h->scal;
+  s.trace = h->trace; s.trace_cap = h->trace_cap; s.p = 0;
+  s.Wt = h->Wt; s.CVop = h->CVop; s.Kop = h->Kop; s.flags = h->flags;
+  s.eps = h->opts.eps; s.tol = h->opts.eig_tol; s.max_outer = h->opts.eig_max_outer; s.max_deg = 10;
+  s.cold = 0;
+  e = launch_small_step(s, h->CL, h->ss_smem, h->ss_flags, h->st);
+  if (e != cudaSuccess) return fail(h, WLR_ECUDA, std::string("small step: ") + cudaGetErrorString(e));
+  if (prof) {
+    cudaEventRecord(ev[5], h->st);
+    h->pr.iters++;
+  }
+  h->pr.launches += 4;
+  return WLR_OK;
+}
+
+static wlr_status build_graphs(wlr_ctx* h) {
+  for (int par = 0; par < 2; ++par) {
+    cudaGraph_t g;
+    CUDA_TRY(h, cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
+    const int64_t l0 = h->pr.launches;
+    wlr_status s = enqueue_iteration(h, par);
+    h->pr.launches = l0;
+    cudaError_t e = cudaStreamEndCapture(h->st, &g);
+    if (s != WLR_OK) return s;
+    CUDA_TRY(h, e);
+    CUDA_TRY(h, cudaGraphInstantiate(&h->gexec[par], g, 0));
+    cudaGraphDestroy(g);
+  }
+  return WLR_OK;
+}
+
+static wlr_status launch_iteration(wlr_ctx* h) {
+  wlr_status s;
+  if (h->opts.use_graph && !h->prof) {
+    if (!h->gexec[0]) {
+      s = build_graphs(h);
+      if (s != WLR_OK) return s;
+    }
+    CUDA_TRY(h, cudaGraphLaunch(h->gexec[h->par], h->st));
+    h->pr.launches += 4;
+  } else {
+    s = enqueue_iteration(h, h->par);
+    if (s != WLR_OK) return s;
+  }
+  h->par ^= 1;
+  h->p += 1;
+  return WLR_OK;
+}
+
+// ------------------------------------------------------------------------------- init
+extern "C" void wlr_opts_default(wlr_opts* o) {
+  std::memset(o, 0, sizeof(*o));
+  o->dtype = WLR_F32;
+  o->init = WLR_INIT_GHS;
+  o->w1_scalar = 1.0;
+  o->nranks = 1;
+  o->use_graph = 1;
+}
+
+static uint64_t splitmix(uint64_t& x) {
+  uint64_t z = (x += 0x9E3779B97F4A7C15ull);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+template <typename T>
+static void gram_launch(wlr_ctx* h, const void* L, int64_t ldl, int nl, const void* R, int64_t ldr,
+                        int nr, double* part, int nsplit, double* out) {
+  launch_gram64<T>((const T*)L, ldl, nl, (const T*)R, ldr, nr, h->m, part, nsplit, out, h->st);
+}
+
+static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
+  const wlr_opts& o = h->opts;
+  const size_t es = h->es;
+  // ---- stream
+  if (o.stream) h->st = (cudaStream_t)o.stream;
+  else {
+    CUDA_TRY(h, cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
+    h->own_stream = true;
+  }
+  int dev = 0;
+  CUDA_TRY(h, cudaGetDevice(&dev));
+  CUDA_TRY(h, cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, dev));
+  CUDA_TRY(h, cudaMallocHost(&h->h_flags, 8 * sizeof(int)));
+  CUDA_TRY(h, cudaMallocHost(&h->h_scal, 8 * sizeof(double)));
+  wlr_status s;
+  // ---- data: borrow device buffers, copy host buffers
+  if (is_device_ptr(A)) h->A = A;
+  else {
+    void* d = nullptr;
+    if ((s = dalloc(h, &d, (size_t)h->m * h->n * es)) != WLR_OK) return s;
+    CUDA_TRY(h, cudaMemcpy2DAsync(d, h->n * es, A, h->lda * es, h->n * es, h->m, cudaMemcpyHostToDevice, h->st));
+    h->A = d;
+    h->lda = h->n;
+  }
+  if (W1) {
+    if (is_device_ptr(W1)) h->W1 = W1;
+    else {
+      void* d = nullptr;
+      if ((s = dalloc(h, &d, (size_t)h->m * h->k * es)) != WLR_OK) return s;
+      CUDA_TRY(h, cudaMemcpy2DAsync(d, h->k * es, W1, h->ldw * es, h->k * es, h->m, cudaMemcpyHostToDevice, h->st));
+      h->W1 = d;
+      h->ldw = h->k;
+    }
+  }
+  if ((s = dalloc_t(h, &h->flags, 8)) != WLR_OK) return s;
+  // ---- validation on device: W1 > 0, finite data
+  if (h->dtype == WLR_F32) launch_validate<float>((const float*)h->A, h->lda, h->m, (int)h->n, (const float*)h->W1, h->ldw, (int)h->k, h->flags, h->st);
+  else launch_validate<double>((const double*)h->A, h->lda, h->m, (int)h->n, (const double*)h->W1, h->ldw, (int)h->k, h->flags, h->st);
+  CUDA_TRY(h, cudaMemcpyAsync(h->h_flags, h->flags, 8 * sizeof(int), cudaMemcpyDeviceToHost, h->st));
+  CUDA_TRY(h, cudaStreamSynchronize(h->st));
+  if (h->h_flags[1] & 2) return fail(h, WLR_ENONFINITE, "non-finite entry in A or W1");
+  if (h->h_flags[1] & 1) return fail(h, WLR_EINVAL, "W1 must be > 0 (PAPER.md:94)");
+  CUDA_TRY(h, cudaMemsetAsync(h->flags, 0, 8 * sizeof(int), h->st));
+
+  // ---- sizes of the per-iteration kernels
+  const int64_t k = h->k, n = h->n, nk = h->nk, t = h->t, kp = h->kp;
+  h->rp = row_pass_rp((int)(t + k));
+  if (h->rp < 0 || kp > 128) return fail(h, WLR_EINVAL, "this build supports r <= 128 and k <= 128");
+  const int tm = row_pass_tm(h->rp);
+  const size_t rsm = h->dtype == WLR_F32 ? row_pass_smem<float>(h->rp, h->uniform, (int)k, (int)t, (int)kp)
+                                         : row_pass_smem<double>(h->rp, h->uniform, (int)k, (int)t, (int)kp);
+  if (rsm > 227 * 1024) return fail(h, WLR_EINVAL, "row-pass shared memory exceeds 227 KB for this (k, r)");
+  const int64_t ntiles = ceil_div(h->m, tm);
+  const int per_sm = rsm > 113 * 1024 ? 1 : 2;
+  h->rp_grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)h->nsm * per_sm));
+  h->bm = incr_bm((int)kp);
+  const int bn = incr_bn(h->bm);
+  h->nz = (int)((n - h->k0) + 2 * kp);
+  const int ncol = (int)ceil_div(h->nz, bn);
+  int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(h->m, 256), ceil_div(2 * h->nsm, ncol)));
+  h->rps = round_up(ceil_div(h->m, nsplit), 32);
+  h->nsplit = (int)std::max<int64_t>(1, ceil_div(h->m, h->rps));
+  // eigen block width b
+  int b = o.eig_block > 0 ? o.eig_block : (int)std::max<int64_t>(2 * t, t + 2);
+  b = (int)std::min<int64_t>(std::max<int64_t>(b, t), nk);
+  if (b > 32) b = 32;
+  if (b < t) return fail(h, WLR_EINVAL, "r-k > 32 is not supported by this build");
+  h->b = b;
+
+  // ---- allocations
+  const int64_t wt_rows = round_up(n - h->k0, 32) + 32;
+  if ((s = dalloc(h, &h->X[0], (size_t)h->m * kp * es)) != WLR_OK) return s;
+  if ((s = dalloc(h, &h->X[1], (size_t)h->m * kp * es)) != WLR_OK) return s;
+  if ((s = dalloc(h, &h->Wt, (size_t)wt_rows * h->rp * es)) != WLR_OK) return s;
+  if ((s = dalloc(h, &h->CVop, (size_t)std::max<int64_t>(k * t, 1) * es)) != WLR_OK) return s;
+  if ((s = dalloc(h, &h->Kop, (size_t)k * k * es)) != WLR_OK) return s;
+  if ((s = dalloc_t(h, &h->inc_part, (size_t)h->nsplit * k * h->nz)) != WLR_OK) return s;
+  if ((s = dalloc_t(h, &h->fw_part, (size_t)std::max(h->rp_grid, 1184))) != WLR_OK) return s;
+  if ((s = dalloc_t(h, &h->inc, (size_t)(k * nk + 2 * k * k + 1))) != WLR_OK) return s;
+  if ((s = dalloc_t(h, &h->fw0, 2)) != WLR_OK) return s;
+  if ((s = dalloc_t(h, &h->GA, (size_t)nk * nk)) != WLR_OK) return s;
+  for (int i = 0; i < 2; ++i) {
+    if ((s = dalloc_t(h, &h->G[i], (size_t)k * k)) != WLR_OK) return s;
+    if ((s = dalloc_t(h, &h->M[i], (size_t)k * nk)) != WLR_OK) return s;
+    if ((s = dalloc_t(h, &h->C[i], (size_t)k * nk)) != WLR_OK) return s;
+  }
+  if ((s = dalloc_t(h, &h->Vprev, (size_t)nk * t)) != WLR_OK) return s;
+  if ((s = dalloc_t(h, &h->CVprev, (size_t)k * t)) != WLR_OK) return s;
+  if ((s = dalloc_t(h, &h->Y, (size_t)nk * b)) != WLR_OK) return s;
+  if ((s = dalloc_t(h, &h->Z, (size_t)nk * b)) != WLR_OK) return s;
+  if ((s = dalloc_t(h, &h->Y1, (size_t)nk * b)) != WLR_OK) return s;
+  if ((s = dalloc_t(h, &h->Y2, (size_t)nk * b)) != WLR_OK) return s;
+  if ((s = dalloc_t(h, &h->theta, 32)) != WLR_OK) return s;
+  h->xstride = small_step_xchg_stride((int)k, (int)nk, (int)t, b);
+  if ((s = dalloc_t(h, &h->xchg, (size_t)2 * 16 * h->xstride)) != WLR_OK) return s;
+  if ((s = dalloc_t(h, &h->red, (size_t)h->xstride + k * k + 2 * k * t + 64)) != WLR_OK) return s;
+  if ((s = dalloc_t(h, &h->scal, 8)) != WLR_OK) return s;
+  if ((s = dalloc_t(h, &h->trace, (size_t)h->trace_cap * 4)) != WLR_OK) return s;
+
+  // ---- NCCL communicator (rows sharded over ranks)
+  if (o.nranks > 1) {
+    if (!o.nccl_id) return fail(h, WLR_EINVAL, "nranks > 1 needs opts.nccl_id");
+    std::string e;
+    if (!g_nccl.load(e)) return fail(h, WLR_ENCCL, e);
+    ncclUniqueId id;
+    std::memcpy(&id, o.nccl_id, sizeof(id));
+    ncclResult_t nr = g_nccl.commInitRank(&h->comm, o.nranks, id, o.rank);
+    if (nr != ncclSuccess) return fail(h, WLR_ENCCL, std::string("ncclCommInitRank: ") + g_nccl.errStr(nr));
+  }
+
+  // ---- one-time Grams in fp64 (a0/a1): A^T A (or X1_0^T [X1_0 | A2] and A2^T A2)
+  const int gsplit = (int)std::max<int64_t>(1, std::min<int64_t>(8, ceil_div(h->m, 4096)));
+  double* part = nullptr;
+  double* gram = nullptr;
+  if ((s = dalloc_t(h, &part, (size_t)gsplit * n * n)) != WLR_OK) return s;
+  if ((s = dalloc_t(h, &gram, (size_t)n * n)) != WLR_OK) return s;
+  const char* A2 = (const char*)h->A + k * es;
+  if (h->dtype == WLR_F32) {
+    if (o.init == WLR_INIT_GIVEN) launch_init_x1<float>((const float*)h->opts.x1_0, k, h->m, (int)k, (int)kp, (float*)h->X[0], h->st);
+    else launch_init_x1<float>((const float*)h->A, h->lda, h->m, (int)k, (int)kp, (float*)h->X[0], h->st);
+  } else {
+    if (o.init == WLR_INIT_GIVEN) launch_init_x1<double>((const double*)h->opts.x1_0, k, h->m, (int)k, (int)kp, (double*)h->X[0], h->st);
+    else launch_init_x1<double>((const double*)h->A, h->lda, h->m, (int)k, (int)kp, (double*)h->X[0], h->st);
+  }
+  auto run_gram = [&](const void* L, int64_t ldl, int nl, const void* R, int64_t ldr, int nr, double* out) {
+    if (h->dtype == WLR_F32) gram_launch<float>(h, L, ldl, nl, R, ldr, nr, part, gsplit, out);
+    else gram_launch<double>(h, L, ldl, nl, R, ldr, nr, part, gsplit, out);
+  };
+  // gram buffer layout: n x n; for INIT_GIVEN rows [0,k) are X1_0^T [X1_0 | A2]
+  if (o.init == WLR_INIT_GIVEN) {
+    double* tmp = nullptr;
+    if ((s = dalloc_t(h, &tmp, (size_t)k * n)) != WLR_OK) return s;
+    run_gram(h->X[0], kp, (int)k, h->X[0], kp, (int)k, tmp);                 // k x k
+    CUDA_TRY(h, cudaMemcpy2DAsync(gram, n * 8, tmp, k * 8, k * 8, k, cudaMemcpyDeviceToDevice, h->st));
+    run_gram(h->X[0], kp, (int)k, A2, h->lda, (int)nk, tmp);                 // k x nk
+    CUDA_TRY(h, cudaMemcpy2DAsync(gram + k, n * 8, tmp, nk * 8, nk * 8, k, cudaMemcpyDeviceToDevice, h->st));
+    run_gram(A2, h->lda, (int)nk, A2, h->lda, (int)nk, h->GA);               // nk x nk
+  } else {
+    run_gram(h->A, h->lda, (int)n, h->A, h->lda, (int)n, gram);
+  }
+  if (h->comm) {
+    // sum the per-rank Grams (rows are sharded, Grams are additive over rows)
+    ncclResult_t nr = g_nccl.allReduce(gram, gram, (size_t)n * n, ncclFloat64, ncclSum, h->comm, h->st);
+    if (nr != ncclSuccess) return fail(h, WLR_ENCCL, "ncclAllReduce(init gram)");
+    if (o.init == WLR_INIT_GIVEN) {
+      nr = g_nccl.allReduce(h->GA, h->GA, (size_t)nk * nk, ncclFloat64, ncclSum, h->comm, h->st);
+      if (nr != ncclSuccess) return fail(h, WLR_ENCCL, "ncclAllReduce(init GA)");
+    }
+  }
+  CUDA_TRY(h, cudaMemcpy2DAsync(h->G[0], k * 8, gram, n * 8, k * 8, k, cudaMemcpyDeviceToDevice, h->st));
+  CUDA_TRY(h, cudaMemcpy2DAsync(h->M[0], nk * 8, gram + k, n * 8, nk * 8, k, cudaMemcpyDeviceToDevice, h->st));
+  if (o.init != WLR_INIT_GIVEN)
+    CUDA_TRY(h, cudaMemcpy2DAsync(h->GA, nk * 8, gram + k * n + k, n * 8, nk * 8, nk, cudaMemcpyDeviceToDevice, h->st));
+  // ||A2||_F^2 = tr(G_A)
+  {
+    std::vector<double> diag(nk);
+    CUDA_TRY(h, cudaMemcpy2DAsync(diag.data(), 8, h->GA, (nk + 1) * 8, 8, nk, cudaMemcpyDeviceToHost, h->st));
+    CUDA_TRY(h, cudaStreamSynchronize(h->st));
+    double a2 = 0.0;
+    for (double v : diag) a2 += v;
+    h->a2sq = a2;
+  }
+  // f_w(X1_0): 0 for the GHS start, otherwise computed
+  if (o.init == WLR_INIT_GIVEN) {
+    if (h->dtype == WLR_F32) launch_fw<float>((const float*)h->A, h->lda, (const float*)h->W1, h->ldw, h->w1s * h->w1s, (const float*)h->X[0], (int)kp, h->m, (int)k, h->fw_part, 1184, h->st);
+    else launch_fw<double>((const double*)h->A, h->lda, (const double*)h->W1, h->ldw, h->w1s * h->w1s, (const double*)h->X[0], (int)kp, h->m, (int)k, h->fw_part, 1184, h->st);
+    launch_reduce_incr(h->inc_part, 0, 0, 0, 1, 0, 0, 0, h->fw_part, 1184, h->fw0, h->st);
+    if (h->comm) {
+      ncclResult_t nr = g_nccl.allReduce(h->fw0, h->fw0, 1, ncclFloat64, ncclSum, h->comm, h->st);
+      if (nr != ncclSuccess) return fail(h, WLR_ENCCL, "ncclAllReduce(fw0)");
+    }
+  }
+  // cold-start block of the eigensolver: deterministic host PRNG (identical on all ranks)
+  {
+    std::vector<double> y((size_t)nk * b);
+    uint64_t st = 0x5eed0000ull + (uint64_t)(uint32_t)o.seed;
+    for (auto& v : y) v = (double)(splitmix(st) >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+    CUDA_TRY(h, cudaMemcpyAsync(h->Y, y.data(), y.size() * 8, cudaMemcpyHostToDevice, h->st));
+    CUDA_TRY(h, cudaStreamSynchronize(h->st));
+  }
+  // small step configuration
+  SmallArgs sa{};
+  sa.k = (int)k; sa.nk = (int)nk; sa.t = (int)t; sa.b = b; sa.kp = (int)kp; sa.k0 = (int)h->k0;
+  sa.rp = h->rp; sa.mode = 0; sa.dtype = h->dtype == WLR_F64 ? 1 : 0;
+  sa.uniform = h->uniform ? 1 : 0; sa.w2 = h->w1s * h->w1s;
+  sa.GA = h->GA; sa.a2sq = h->a2sq; sa.inc = h->fw0;
+  sa.G_in = h->G[0]; sa.G_out = h->G[0]; sa.M_in = h->M[0]; sa.M_out = h->M[0];
+  sa.C_in = h->C[0]; sa.C_out = h->C[0];
+  sa.Vprev = h->Vprev; sa.CVprev = h->CVprev; sa.Y = h->Y; sa.Z = h->Z; sa.Y1 = h->Y1; sa.Y2 = h->Y2;
+  sa.theta = h->theta; sa.xchg = h->xchg; sa.xchg_stride = h->xstride; sa.red = h->red; sa.scal = h->scal;
+  sa.trace = h->trace; sa.trace_cap = h->trace_cap; sa.p = 0;
+  sa.Wt = h->Wt; sa.CVop = h->CVop; sa.Kop = h->Kop; sa.flags = h->flags;
+  sa.eps = o.eps; sa.tol = o.eig_tol; sa.max_outer = 4 * o.eig_max_outer; sa.max_deg = 10; sa.cold = 1;
+  h->CL = small_step_cluster_size(sa, &h->ss_smem, &h->ss_flags);
+  if (h->CL <= 0) return fail(h, WLR_ECUDA, "no schedulable cluster configuration for the small step");
+  cudaError_t e = launch_small_step(sa, h->CL, h->ss_smem, h->ss_flags, h->st);
+  if (e != cudaSuccess) return fail(h, WLR_ECUDA, std::string("small step (init): ") + cudaGetErrorString(e));
+  h->pr.launches = 0;
+  s = check_flags(h);
+  if (s != WLR_OK) return s;
+  h->p = 0;
+  h->par = 0;
+  return WLR_OK;
+}
+
+extern "C" wlr_status wlr_init(wlr_handle* out, const void* A, int64_t lda, const void* W1,
+                               int64_t ldw, int64_t m_local, int64_t n, int64_t k, int64_t r,
+                               const wlr_opts* o) {
+  if (!out) return fail(nullptr, WLR_EINVAL, "null handle pointer");
+  *out = nullptr;
+  wlr_opts def;
+  wlr_opts_default(&def);
+  const wlr_opts& op = o ? *o : def;
+  if (!A) return fail(nullptr, WLR_EINVAL, "A is null");
+  if (m_local < 1 || n < 2) return fail(nullptr, WLR_EINVAL, "need m >= 1, n >= 2");
+  if (k < 1 || k >= n) return fail(nullptr, WLR_EINVAL, "need 1 <= k < n");
+  const int64_t mg = op.m_global > 0 ? op.m_global : m_local;
+  if (r <= k) return fail(nullptr, WLR_EINVAL, "need r > k (Theorem 2, PAPER.md:94)");
+  if (r > std::min(mg, n)) return fail(nullptr, WLR_EINVAL, "need r <= min(m, n)");
+  if (lda < n) return fail(nullptr, WLR_EINVAL, "lda < n");
+  if (W1 && ldw < k) return fail(nullptr, WLR_EINVAL, "ldw < k");
+  if (!W1 && !(op.w1_scalar > 0.0)) return fail(nullptr, WLR_EINVAL, "uniform weight must be > 0");
+  if (op.dtype != WLR_F32 && op.dtype != WLR_F64) return fail(nullptr, WLR_EINVAL, "bad dtype");
+  if (op.init == WLR_INIT_GIVEN && !op.x1_0) return fail(nullptr, WLR_EINVAL, "INIT_GIVEN needs x1_0");
+  if (op.nranks < 1 || op.rank < 0 || op.rank >= op.nranks) return fail(nullptr, WLR_EINVAL, "bad rank");
+  if (m_local < k && op.nranks == 1) return fail(nullptr, WLR_EINVAL, "need m >= k");
+  wlr_ctx* h = new wlr_ctx();
+  h->opts = op;
+  if (h->opts.eig_tol <= 0.0) h->opts.eig_tol = 1e-11;
+  if (h->opts.eig_max_outer <= 0) h->opts.eig_max_outer = 60;
+  h->m = m_local; h->n = n; h->k = k; h->r = r; h->t = r - k; h->nk = n - k;
+  h->kp = round_up(k, 4); h->k0 = k & ~3LL;
+  h->m_global = mg; h->row_offset = op.row_offset;
+  h->dtype = op.dtype; h->es = op.dtype == WLR_F64 ? 8 : 4;
+  h->uniform = W1 == nullptr; h->w1s = op.w1_scalar;
+  h->A = A; h->lda = lda; h->W1 = W1; h->ldw = ldw;
+  if (op.init == WLR_INIT_GIVEN && !is_device_ptr(op.x1_0)) {
+    void* d = nullptr;
+    if (cudaMalloc(&d, (size_t)m_local * k * h->es) != cudaSuccess) { delete h; return fail(nullptr, WLR_ENOMEM, "x1_0 copy"); }
+    h->allocs.push_back(d);
+    cudaMemcpy(d, op.x1_0, (size_t)m_local * k * h->es, cudaMemcpyHostToDevice);
+    h->opts.x1_0 = d;
+  }
+  wlr_status s = do_init(h, A, W1);
+  if (s != WLR_OK) {
+    g_err = h->err;
+    wlr_destroy(h);
+    return s;
+  }
+  *out = h;
+  return WLR_OK;
+}
+
+// --------------------------------------------------------------------------- iterate
+extern "C" wlr_status wlr_iterate_async(wlr_handle h, int32_t n_iters) {
+  if (!h) return fail(nullptr, WLR_EINVAL, "null handle");
+  for (int32_t i = 0; i < n_iters; ++i) {
+    wlr_status s = launch_iteration(h);
+    if (s != WLR_OK) return s;
+  }
+  return WLR_OK;
+}
+
+extern "C" wlr_status wlr_sync(wlr_handle h) {
+  if (!h) return fail(nullptr, WLR_EINVAL, "null handle");
+  return check_flags(h);
+}
+
+extern "C" wlr_status wlr_iterate(wlr_handle h, int32_t max_iters, int32_t* iters_done,
+                                  int32_t* converged) {
+  if (!h) return fail(nullptr, WLR_EINVAL, "null handle");
+  if (max_iters < 0) return fail(h, WLR_EINVAL, "max_iters < 0");
+  const int64_t p0 = h->p;
+  wlr_status s = WLR_OK;
+  int done = 0;
+  const int chunk = h->opts.eps > 0.0 ? 1 : 64;
+  while (done < max_iters) {
+    const int n = std::min(chunk, max_iters - done);
+    s = wlr_iterate_async(h, n);
+    if (s != WLR_OK) break;
+    done += n;
+    s = check_flags(h);
+    if (s != WLR_OK) break;
+    if (h->h_flags[2]) break;
+  }
+  if (iters_done) *iters_done = (int32_t)(h->p - p0);
+  if (converged) *converged = h->h_flags[2] ? 1 : 0;
+  return s;
+}
+
+extern "C" wlr_status wlr_objective(wlr_handle h, double* F, double* step_norm, double* rel_error) {
+  if (!h) return fail(nullptr, WLR_EINVAL, "null handle");
+  wlr_status s = check_flags(h);
+  if (s != WLR_OK) return s;
+  if (F) *F = h->h_scal[2];
+  if (step_norm) *step_norm = h->h_scal[3];
+  if (rel_error) *rel_error = h->h_scal[4];
+  return WLR_OK;
+}
+
+extern "C" wlr_status wlr_trace(wlr_handle h, double* out, int32_t cap, int32_t* count) {
+  if (!h || !out) return fail(h, WLR_EINVAL, "null argument");
+  wlr_status s = check_flags(h);
+  if (s != WLR_OK) return s;
+  std::vector<double> all((size_t)h->trace_cap * 4);
+  CUDA_TRY(h, cudaMemcpy(all.data(), h->trace, all.size() * 8, cudaMemcpyDeviceToHost));
+  const int64_t nstates = h->p + 1;
+  const int64_t avail = std::min<int64_t>(nstates, h->trace_cap);
+  const int64_t nout = std::min<int64_t>(avail, cap);
+  const int64_t first = nstates - nout;
+  for (int64_t i = 0; i < nout; ++i) {
+    const int64_t q = (first + i) % h->trace_cap;
+    for (int j = 0; j < 4; ++j) out[i * 4 + j] = all[q * 4 + j];
+  }
+  if (count) *count = (int32_t)nout;
+  return WLR_OK;
+}
+
+// copy a device buffer (rows x cols, ld_src) into dst (host or device, ld_dst)
+static wlr_status copy_out(wlr_ctx* h, void* dst, int64_t ldd, const void* src, int64_t lds,
+                           int64_t rows, int64_t cols, size_t es) {
+  const bool dev = is_device_ptr(dst);
+  CUDA_TRY(h, cudaMemcpy2DAsync(dst, ldd * es, src, lds * es, cols * es, rows,
+                                dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->st));
+  return WLR_OK;
+}
+
+extern "C" wlr_status wlr_result(wlr_handle h, void* X1, int64_t ldx1, void* C, void* B,
+                                 int64_t ldb, void* D, void* X2, int64_t ldx2) {
+  if (!h) return fail(nullptr, WLR_EINVAL, "null handle");
+  wlr_status s = check_flags(h);
+  if (s != WLR_OK) return s;
+  const int cur = h->par;
+  const size_t es = h->es;
+  if (X1) {
+    if (ldx1 < h->k) return fail(h, WLR_EINVAL, "ldx1 < k");
+    if ((s = copy_out(h, X1, ldx1, h->X[cur], h->kp, h->m, h->k, es)) != WLR_OK) return s;
+  }
+  if (C) {
+    if ((s = copy_out(h, C, h->nk, h->C[cur], h->nk, h->k, h->nk, 8)) != WLR_OK) return s;
+  }
+  if (D) {
+    std::vector<double> v((size_t)h->nk * h->t), d((size_t)h->nk * h->t);
+    CUDA_TRY(h, cudaMemcpyAsync(v.data(), h->Vprev, v.size() * 8, cudaMemcpyDeviceToHost, h->st));
+    CUDA_TRY(h, cudaStreamSynchronize(h->st));
+    for (int64_t c = 0; c < h->nk; ++c)
+      for (int64_t j = 0; j < h->t; ++j) d[j * h->nk + c] = v[c * h->t + j];
+    if (is_device_ptr(D)) CUDA_TRY(h, cudaMemcpy(D, d.data(), d.size() * 8, cudaMemcpyHostToDevice));
+    else std::memcpy(D, d.data(), d.size() * 8);
+  }
+  if (B || X2) {
+    void* Bd = nullptr;
+    CUDA_TRY(h, cudaMalloc(&Bd, (size_t)h->m * h->t * es + 16));
+    cudaError_t e;
+    if (h->dtype == WLR_F32) {
+      RowPassArgs<float> a{};
+      a.A = (const float*)h->A; a.lda = h->lda; a.W1 = (const float*)h->W1; a.ldw = h->ldw;
+      a.w2s = (float)(h->w1s * h->w1s); a.Xold = (const float*)h->X[cur]; a.Xnew = nullptr;
+      a.Wt = (const float*)h->Wt; a.CV = (const float*)h->CVop; a.Kmat = (const float*)h->Kop;
+      a.Bout = (float*)Bd; a.ldb = h->t; a.fw_part = h->fw_part; a.flags = h->flags;
+      a.m = h->m; a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.k0 = (int)h->k0; a.t = (int)h->t;
+      a.vec_ok = (h->lda % 4 == 0) && ((uintptr_t)h->A % 16 == 0);
+      e = launch_row_pass<float>(a, h->rp, h->uniform, 1, h->rp_grid, h->st);
+    } else {
+      RowPassArgs<double> a{};
+      a.A = (const double*)h->A; a.lda = h->lda; a.W1 = (const double*)h->W1; a.ldw = h->ldw;
+      a.w2s = h->w1s * h->w1s; a.Xold = (const double*)h->X[cur]; a.Xnew = nullptr;
+      a.Wt = (const double*)h->Wt; a.CV = (const double*)h->CVop; a.Kmat = (const double*)h->Kop;
+      a.Bout = (double*)Bd; a.ldb = h->t; a.fw_part = h->fw_part; a.flags = h->flags;
+      a.m = h->m; a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.k0 = (int)h->k0; a.t = (int)h->t;
+      a.vec_ok = (h->lda % 4 == 0) && ((uintptr_t)h->A % 16 == 0);
+      e = launch_row_pass<double>(a, h->rp, h->uniform, 1, h->rp_grid, h->st);
+    }
+    if (e != cudaSuccess) { cudaFree(Bd); return fail(h, WLR_ECUDA, std::string("result row pass: ") + cudaGetErrorString(e)); }
+    if (B) {
+      if (ldb < h->t) { cudaFree(Bd); return fail(h, WLR_EINVAL, "ldb < r-k"); }
+      if ((s = copy_out(h, B, ldb, Bd, h->t, h->m, h->t, es)) != WLR_OK) { cudaFree(Bd); return s; }
+    }
+    if (X2) {
+      if (ldx2 < h->nk) { cudaFree(Bd); return fail(h, WLR_EINVAL, "ldx2 < n-k"); }
+      void* X2d = nullptr;
+      const bool dev = is_device_ptr(X2);
+      if (dev) X2d = X2;
+      else if (cudaMalloc(&X2d, (size_t)h->m * h->nk * es) != cudaSuccess) { cudaFree(Bd); return fail(h, WLR_ENOMEM, "X2 staging"); }
+      const int64_t ldo = dev ? ldx2 : h->nk;
+      if (h->dtype == WLR_F32)
+        launch_assemble_x2<float>((const float*)h->X[cur], (int)h->kp, (const float*)Bd, h->t, h->C[cur], h->Vprev, h->m, (int)h->k, (int)h->nk, (int)h->t, (float*)X2d, ldo, h->st);
+      else
+        launch_assemble_x2<double>((const double*)h->X[cur], (int)h->kp, (const double*)Bd, h->t, h->C[cur], h->Vprev, h->m, (int)h->k, (int)h->nk, (int)h->t, (double*)X2d, ldo, h->st);
+      if (!dev) {
+        s = copy_out(h, X2, ldx2, X2d, h->nk, h->m, h->nk, es);
+        cudaStreamSynchronize(h->st);
+        cudaFree(X2d);
+        if (s != WLR_OK) { cudaFree(Bd); return s; }
+      }
+    }
+    CUDA_TRY(h, cudaStreamSynchronize(h->st));
+    cudaFree(Bd);
+  }
+  CUDA_TRY(h, cudaStreamSynchronize(h->st));
+  return WLR_OK;
+}
+
+extern "C" wlr_status wlr_debug_state(wlr_handle h, const char* name, double* out, int64_t cap,
+                                      int64_t* count) {
+  if (!h || !name) return fail(h, WLR_EINVAL, "null argument");
+  wlr_status s = check_flags(h);
+  if (s != WLR_OK) return s;
+  const int cur = h->par;
+  const double* src = nullptr;
+  int64_t cnt = 0;
+  std::string nm(name);
+  if (nm == "G") { src = h->G[cur]; cnt = h->k * h->k; }
+  else if (nm == "M") { src = h->M[cur]; cnt = h->k * h->nk; }
+  else if (nm == "C") { src = h->C[cur]; cnt = h->k * h->nk; }
+  else if (nm == "V") { src = h->Vprev; cnt = h->nk * h->t; }
+  else if (nm == "lam") { src = h->theta; cnt = h->t; }
+  else if (nm == "theta") { src = h->theta; cnt = h->b; }
+  else if (nm == "GA") { src = h->GA; cnt = h->nk * h->nk; }
+  else if (nm == "scal") { src = h->scal; cnt = 8; }
+  else return fail(h, WLR_EINVAL, "unknown state name");
+  if (count) *count = cnt;
+  if (out) CUDA_TRY(h, cudaMemcpy(out, src, (size_t)std::min(cap, cnt) * 8, cudaMemcpyDeviceToHost));
+  if (out && nm == "scal" && cap >= 8) {
+    // expose device flags too: scal[6] = eigensolver outer iterations of the last step
+    int fl[8];
+    CUDA_TRY(h, cudaMemcpy(fl, h->flags, sizeof(fl), cudaMemcpyDeviceToHost));
+    out[6] = fl[3];
+    out[7] = fl[2];
+  }
+  return WLR_OK;
+}
+
+extern "C" wlr_status wlr_profile(wlr_handle h, int32_t enable, int32_t reset, double* ms,
+                                  int32_t nms, int64_t* launches, int64_t* timed_iters) {
+  if (!h) return fail(nullptr, WLR_EINVAL, "null handle");
+  CUDA_TRY(h, cudaStreamSynchronize(h->st));
+  // fold recorded event groups (6 per iteration) into the per-kernel sums
+  for (size_t g = 0; g + 6 <= h->pr.used; g += 6) {
+    float t01 = 0, t12 = 0, t23 = 0, t45 = 0;
+    cudaEventElapsedTime(&t01, h->pr.pool[g], h->pr.pool[g + 1]);
+    cudaEventElapsedTime(&t12, h->pr.pool[g + 1], h->pr.pool[g + 2]);
+    cudaEventElapsedTime(&t23, h->pr.pool[g + 2], h->pr.pool[g + 3]);
+    cudaEventElapsedTime(&t45, h->pr.pool[g + 4], h->pr.pool[g + 5]);
+    h->pr.ms[0] += t01; h->pr.ms[1] += t12; h->pr.ms[2] += t23; h->pr.ms[3] += t45;
+  }
+  h->pr.used = 0;
+  if (ms)
+    for (int i = 0; i < nms && i < 4; ++i) ms[i] = h->pr.ms[i];
+  if (launches) *launches = h->pr.launches;
+  if (timed_iters) *timed_iters = h->pr.iters;
+  if (reset) {
+    for (double& v : h->pr.ms) v = 0.0;
+    h->pr.launches = 0;
+    h->pr.iters = 0;
+  }
+  h->prof = enable != 0;
+  return WLR_OK;
+}
+
+extern "C" wlr_status wlr_nccl_unique_id(void* out128) {
+  if (!out128) return fail(nullptr, WLR_EINVAL, "null output");
+  std::string e;
+  if (!g_nccl.load(e)) return fail(nullptr, WLR_ENCCL, e);
+  ncclUniqueId id;
+  ncclResult_t r = g_nccl.getUniqueId(&id);
+  if (r != ncclSuccess) return fail(nullptr, WLR_ENCCL, "ncclGetUniqueId failed");
+  std::memcpy(out128, &id, sizeof(id));
+  return WLR_OK;
+}
+
+extern "C" const char* wlr_last_error(wlr_handle h) { return h ? h->err.c_str() : g_err.c_str(); }
+
+extern "C" const char* wlr_status_string(int32_t s) {
+  switch (s) {
+    case WLR_OK: return "WLR_OK";
+    case WLR_EINVAL: return "WLR_EINVAL";
+    case WLR_ERANK: return "WLR_ERANK";
+    case WLR_EEIG: return "WLR_EEIG";
+    case WLR_EINTERNAL: return "WLR_EINTERNAL";
+    case WLR_ENONFINITE: return "WLR_ENONFINITE";
+    case WLR_ECUDA: return "WLR_ECUDA";
+    case WLR_ENCCL: return "WLR_ENCCL";
+    case WLR_ENOMEM: return "WLR_ENOMEM";
+  }
+  return "WLR_UNKNOWN";
+}
+
+extern "C" void wlr_destroy(wlr_handle h) {
+  if (!h) return;
+  if (h->st) cudaStreamSynchronize(h->st);
+  for (auto& g : h->gexec)
+    if (g) cudaGraphExecDestroy(g);
+  if (h->comm && g_nccl.commDestroy) g_nccl.commDestroy(h->comm);
+  for (void* p : h->allocs) cudaFree(p);
+  for (auto e : h->pr.pool) cudaEventDestroy(e);
+  if (h->h_flags) cudaFreeHost(h->h_flags);
+  if (h->h_scal) cudaFreeHost(h->h_scal);
+  if (h->own_stream && h->st) cudaStreamDestroy(h->st);
+  delete h;
+}
+
+extern "C" int32_t wlr_version(void) { return WLR_VERSION; }

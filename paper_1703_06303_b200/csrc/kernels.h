@@ -1,0 +1,101 @@
+// kernels.h -- internal launchers of libwlr (CUDA path only).
+#pragma once
+#include <algorithm>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace wlr {
+
+// ---------------------------------------------------------------- init (init_kernels.cu)
+template <typename T>
+void launch_gram64(const T* L, int64_t ldl, int nl, const T* R, int64_t ldr, int nr, int64_t m,
+                   double* part, int nsplit, double* out, cudaStream_t st);
+template <typename T>
+void launch_init_x1(const T* src, int64_t lds, int64_t m, int k, int kp, T* x, cudaStream_t st);
+template <typename T>
+void launch_fw(const T* A, int64_t lda, const T* W1, int64_t ldw, double w2s, const T* x, int kp,
+               int64_t m, int k, double* part, int nblk, cudaStream_t st);
+template <typename T>
+void launch_validate(const T* A, int64_t lda, int64_t m, int n, const T* W1, int64_t ldw, int k,
+                     int* flags, cudaStream_t st);
+
+// ---------------------------------------------------------------- row pass (rowpass.cu)
+template <typename T>
+struct RowPassArgs {
+  const T* A; int64_t lda;          // m x n (this rank's rows)
+  const T* W1; int64_t ldw;         // m x k or nullptr (uniform)
+  T w2s;                            // uniform weight squared
+  const T* Xold; T* Xnew;           // m x kp
+  const T* Wt;                      // (n-k0 padded to 32) x RP : rows c-k0 = [V(c-k,:) | C(:,c-k)^T | 0]
+  const T* CV;                      // k x t  = C V
+  const T* Kmat;                    // k x k  : K^{-1} (uniform) or C C^T
+  T* Bout; int64_t ldb;             // MODE_RESULT output
+  double* fw_part;                  // gridDim.x partials
+  int* flags;
+  int64_t m; int n, k, kp, k0, t;
+  int vec_ok;                       // A rows 16-byte aligned at multiples of 4 elements
+};
+int row_pass_rp(int r);
+int row_pass_tm(int rp);
+template <typename T> size_t row_pass_smem(int rp, bool uniform, int k, int t, int kp);
+template <typename T>
+cudaError_t launch_row_pass(const RowPassArgs<T>& a, int rp, bool uniform, int mode, int grid,
+                            cudaStream_t st);
+
+template <typename T>
+struct IncrArgs {
+  const T* A; int64_t lda;
+  const T* Xold; const T* Xnew;     // m x kp
+  double* part;                     // nsplit x k x nz
+  int64_t m; int64_t rows_per_split;
+  int n, k, kp, k0, nz, nsplit;
+  int vec_ok;
+};
+int incr_bm(int kp);
+int incr_bn(int bm);
+template <typename T> cudaError_t launch_incr(const IncrArgs<T>& a, int bm, cudaStream_t st);
+void launch_reduce_incr(const double* part, int nsplit, int k, int nk, int nz, int kshift, int nA,
+                        int kp, const double* fw_part, int nfw, double* inc, cudaStream_t st);
+
+// ---------------------------------------------------------------- small step (small_step.cu)
+struct SmallArgs {
+  int k, nk, t, b, kp, k0, rp;      // dims; b = eigen block width
+  int mode;                         // 0: init (G, M given), 1: iteration (apply increments)
+  int dtype;                        // 0 fp32 operands, 1 fp64 operands
+  int uniform; double w2;           // uniform weight squared
+  const double* GA; double a2sq;    // A2^T A2 ((nk)^2), ||A2||_F^2
+  const double* inc;                // [N | Gamma | Omega | f_w] (mode 1); f_w at [0] (mode 0)
+  const double* G_in; double* G_out;   // k x k
+  const double* M_in; double* M_out;   // k x nk
+  const double* C_in; double* C_out;   // k x nk
+  double* Vprev;                    // nk x t  (V of the previous state; updated in place)
+  double* CVprev;                   // k x t   (C V of the previous state; updated)
+  double* Y; double* Z; double* Y1; double* Y2;   // nk x b each (Ritz block + scratch)
+  double* theta;                    // b Ritz values (warm start)
+  double* xchg;                     // cluster exchange slots
+  int64_t xchg_stride;              // doubles per slot
+  double* red;                      // reduced exchange
+  double* scal;                     // persistent scalars (see small_step.cu)
+  double* trace; int trace_cap; int64_t p;   // trace ring (4 doubles per state)
+  void* Wt; void* CVop; void* Kop;  // row-pass operands (dtype)
+  int* flags;
+  double eps, tol; int max_outer, max_deg;
+  int cold;                         // 1: Y holds a random block (no Ritz values yet)
+};
+int small_step_cluster_size(const SmallArgs& a, size_t* smem_out, int* smem_flags);
+cudaError_t launch_small_step(const SmallArgs& a, int cluster, size_t smem, int smem_flags,
+                              cudaStream_t st);
+int small_step_bt(int b);
+int64_t small_step_xchg_stride(int k, int nk, int t, int b);
+
+// ---------------------------------------------------------------- result (result.cu)
+template <typename T>
+void launch_assemble_x2(const T* X1, int kp, const T* B, int64_t ldb, const double* C,
+                        const double* V, int64_t m, int k, int nk, int t, T* X2, int64_t ldx2,
+                        cudaStream_t st);
+template <typename T>
+void launch_copy_x1(const T* X, int kp, int64_t m, int k, T* out, int64_t ldo, cudaStream_t st);
+
+}  // namespace wlr

@@ -1,0 +1,131 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the same
+seeded inputs, same initialisation and same iteration count (BASELINE.json north_star
+tolerances, see tests/gpu_util.py)."""
+import dataclasses
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests import gpu_util as gu
+
+pytestmark = pytest.mark.gpu
+
+
+def test_config1_tiny_fp64_full_run():
+    cfg = synth.CONFIGS[1]
+    A, W1 = gu.inputs(cfg)
+    g = gu.run_gpu(cfg, A, W1, cfg.iters)
+    o = gu.run_oracle(cfg, A, W1, cfg.iters)
+    gu.compare(cfg, g, o)
+
+
+def test_config1_host_buffers_match_device_buffers():
+    """wlr_init with HOST A (copied by the library) == device A (borrowed)."""
+    cfg = synth.CONFIGS[1]
+    A, W1 = gu.inputs(cfg)
+    g_dev = gu.run_gpu(cfg, A, W1, 10, device=True)
+    g_host = gu.run_gpu(cfg, A, W1, 10, device=False)
+    np.testing.assert_array_equal(g_dev["X1"], g_host["X1"])
+    np.testing.assert_array_equal(g_dev["trace"], g_host["trace"])
+
+
+def test_config2_small_fp32_full_run():
+    cfg = synth.CONFIGS[2]
+    A, W1 = gu.inputs(cfg)
+    g = gu.run_gpu(cfg, A, W1, cfg.iters)
+    o = gu.run_oracle(cfg, A, W1, cfg.iters)
+    gu.compare(cfg, g, o)
+
+
+def test_step0_is_ghs_on_gpu():
+    """p = 0 is the Theorem 1 closed form on the GPU too (pin P1 path)."""
+    cfg = synth.CONFIGS[2]
+    A, W1 = gu.inputs(cfg)
+    g = gu.run_gpu(cfg, A, W1, 0)
+    o = gu.run_oracle(cfg, A, W1, 0)
+    gu.compare(cfg, g, o)
+    np.testing.assert_array_equal(g["X1"], A[:, : cfg.k])       # X1_0 = A1 exactly
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_ragged_odd_shapes(dtype):
+    """n not a multiple of 4 (scalar load paths), k not a multiple of 4, m ragged vs the
+    128-row tile, r - k = 1 (the paper's r = k + 1), non-uniform W1."""
+    g0 = np.random.default_rng(21)
+    m, n, k, r = 517, 37, 7, 8
+    A = (g0.standard_normal((m, 9)) @ g0.standard_normal((9, n)) + 0.05 * g0.standard_normal((m, n)))
+    W1 = g0.uniform(1.0, 30.0, size=(m, k))
+    dt = np.float64 if dtype == "f64" else np.float32
+    A, W1 = A.astype(dt), W1.astype(dt)
+    cfg = synth.Config("ragged", m, n, k, r, dtype, 12, "lowrank", w_const=None, w_logu=(1, 30))
+    g = gu.run_gpu(cfg, A, W1, 12)
+    o = gu.run_oracle(cfg, A, W1, 12)
+    gu.compare(cfg, g, o)
+
+
+def test_paper_rank_setting_k15_r16_uniform():
+    """k = 15, r = k + 1 (Basic sequence) on a small scene, uniform W1."""
+    cfg = dataclasses.replace(synth.scaled(synth.CONFIGS[3], 48, 64), k=15, r=16, n=120, iters=20)
+    A, W1 = gu.inputs(cfg)
+    g = gu.run_gpu(cfg, A, W1, cfg.iters)
+    o = gu.run_oracle(cfg, A, W1, cfg.iters)
+    gu.compare(cfg, g, o)
+
+
+def test_random_init_given_x1():
+    """INIT_GIVEN with a host-drawn Gaussian X1_0 (PAPER.md:234 random initialisation)."""
+    cfg = dataclasses.replace(synth.scaled(synth.CONFIGS[2], 30, 40), iters=15)
+    A, W1 = gu.inputs(cfg)
+    x0 = synth.random_x1(cfg.m, cfg.k, seed=5, dtype=np.float32)
+    g = gu.run_gpu(cfg, A, W1, cfg.iters, init="given", x1_0=x0)
+    o = gu.run_oracle(cfg, A, W1, cfg.iters, x1_0=x0.astype(np.float64))
+    gu.compare(cfg, g, o)
+
+
+def test_exactly_representable_gives_zero_objective():
+    """rank(A) <= r with full-rank A1 => F -> 0; S = 0 degenerate eigenproblem."""
+    g0 = np.random.default_rng(3)
+    A = (g0.standard_normal((300, 6)) @ g0.standard_normal((6, 40))).astype(np.float64)
+    cfg = synth.Config("rankr", 300, 40, 4, 6, "f64", 5, "lowrank", w_const=7.0)
+    g = gu.run_gpu(cfg, A, None, 5)
+    assert g["trace"][-1, 0] <= 1e-18 * np.sum(A * A)
+
+
+def test_errors_are_explicit():
+    w = gu.need_gpu()
+    import torch
+    A = torch.rand(200, 30, dtype=torch.float32, device="cuda")
+    with pytest.raises(w.WlrError) as e:
+        w.wlr_init(A, 5, 5)                                  # r = k
+    assert e.value.status == 1
+    W1 = torch.ones(200, 5, dtype=torch.float32, device="cuda")
+    W1[3, 2] = 0.0
+    with pytest.raises(w.WlrError) as e:
+        w.wlr_init(A, 5, 7, W1)                              # W1 > 0
+    assert e.value.status == 1
+    B = A.clone()
+    B[7, 9] = float("nan")
+    with pytest.raises(w.WlrError) as e:
+        w.wlr_init(B, 5, 7)
+    assert e.value.status == 5
+    C = A.clone()
+    C[:, 1] = C[:, 0]                                        # rank(A1) < k
+    with pytest.raises(w.WlrError) as e:
+        w.wlr_init(C, 5, 7)
+    assert e.value.status == 2
+
+
+def test_stopping_rule_eps():
+    """eps > 0 stops on Error_p < eps or rel < eps like the oracle."""
+    cfg = synth.CONFIGS[1]
+    A, W1 = gu.inputs(cfg)
+    eps = 1e-7
+    w = gu.need_gpu()
+    import torch
+    h = w.wlr_init(torch.from_numpy(A).cuda(), cfg.k, cfg.r, None, w1=cfg.w_const, eps=eps)
+    done, conv = w.wlr_iterate(h, 100)
+    o = oracle.swlr(A, synth.dense_W1(cfg, W1, cfg.m), cfg.k, cfg.r, iters=100, eps=eps)
+    assert conv and o.converged
+    assert abs(done - (len(o.trace) - 1)) <= 1
