@@ -70,8 +70,11 @@ WLR_DEVI void xchg_reduce(SSCtx& s, int len, double* out) {
 }
 
 // Cholesky of the n x n symmetric matrix in smem (row-major, lower result in place) by
-// warp 0.  Returns true iff every pivot is positive; result broadcast to the block.
-WLR_DEVI bool chol_warp0(double* A, int n, int ld, double shift) {
+// warp 0.  Returns true iff every pivot d_j > rel * A_jj (the original diagonal, after the
+// shift); result broadcast to the block.  rel > 0 is the numerical-rank test of the Gram
+// route (reading R6b): a pivot at rounding level of its column's squared norm
+// means that column lies in the span of the previous ones.
+WLR_DEVI bool chol_warp0(double* A, int n, int ld, double shift, double rel = 0.0) {
   __shared__ int ok_s;
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
@@ -79,9 +82,16 @@ WLR_DEVI bool chol_warp0(double* A, int n, int ld, double shift) {
     if (shift != 0.0)
       for (int i = lane; i < n; i += 32) A[i * ld + i] += shift;
     __syncwarp();
+    double od[4];                            // original diagonal, lane + 32q (n <= 128)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) od[q] = (lane + 32 * q < n) ? A[(lane + 32 * q) * (ld + 1)] : 0.0;
+    __syncwarp();
     for (int j = 0; j < n; ++j) {
       const double d = A[j * ld + j];
-      ok = ok && (d > 0.0) && isfinite(d);
+      const int q = j >> 5;
+      const double oq = q == 0 ? od[0] : q == 1 ? od[1] : q == 2 ? od[2] : od[3];
+      const double d0 = __shfl_sync(0xffffffffu, oq, j & 31);
+      ok = ok && (d > rel * d0) && (d > 0.0) && isfinite(d);
       const double r = sqrt(d > 0.0 ? d : 1.0);
       const double inv = 1.0 / r;
       __syncwarp();
@@ -403,7 +413,7 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(SmallArgs a, int sm
   if (s.c == 0 && a.mode)
     for (int idx = threadIdx.x; idx < k * k; idx += kSST) a.G_out[idx] = s.Ls[idx];
   __syncthreads();
-  if (!chol_warp0(s.Ls, k, k, 0.0)) {       // rank(X1) < k (R6)
+  if (!chol_warp0(s.Ls, k, k, 0.0, 256.0 * 2.220446049250313e-16)) {   // rank(X1) < k (R6)
     if (s.c == 0 && threadIdx.x == 0) raise_flag(a.flags, DF_RANK);
     return;                                  // every CTA takes this branch identically
   }
