@@ -78,9 +78,9 @@ struct wlr_ctx {
   size_t es = 4;
   bool uniform = true;
   double w1s = 1.0;
-  int b = 0, rp = 0, bm = 0, nz = 0, nsplit = 0, rp_grid = 0, CL = 0, ss_flags = 0;
-  int64_t rps = 0, xstride = 0;
-  size_t ss_smem = 0;
+  int b = 0, rp = 0, bm = 0, nz = 0, nsplit = 0, rp_grid = 0;
+  int64_t rps = 0;
+  SSPlan spl{};
   int nsm = 148;
   wlr_opts opts;
   // data
@@ -92,9 +92,12 @@ struct wlr_ctx {
   double* GA = nullptr;
   double a2sq = 0.0;
   double *G[2] = {nullptr, nullptr}, *M[2] = {nullptr, nullptr}, *C[2] = {nullptr, nullptr};
-  double *Vprev = nullptr, *CVprev = nullptr, *Y = nullptr, *Z = nullptr, *Y1 = nullptr,
-         *Y2 = nullptr, *theta = nullptr;
+  double *Gi[2] = {nullptr, nullptr}, *Ki = nullptr, *gws = nullptr;   // G^{-1}, K^{-1}, K3 workspace
+  double *Vprev = nullptr, *CVprev = nullptr, *Y = nullptr, *theta = nullptr;
   double *xchg = nullptr, *red = nullptr, *scal = nullptr, *trace = nullptr;
+  double* tdbg = nullptr;      // K3 phase timestamps (wlr_debug_state "ktime")
+  SmallArgs last_ss{};         // arguments of the last small-step launch (diagnostics)
+  bool ktime = false;
   int trace_cap = 4096;
   int* flags = nullptr;
   int* h_flags = nullptr;
@@ -235,13 +238,17 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int par) {
   s.GA = h->GA; s.a2sq = h->a2sq; s.inc = h->inc;
   s.G_in = h->G[cur]; s.G_out = h->G[nxt]; s.M_in = h->M[cur]; s.M_out = h->M[nxt];
   s.C_in = h->C[cur]; s.C_out = h->C[nxt];
-  s.Vprev = h->Vprev; s.CVprev = h->CVprev; s.Y = h->Y; s.Z = h->Z; s.Y1 = h->Y1; s.Y2 = h->Y2;
-  s.theta = h->theta; s.xchg = h->xchg; s.xchg_stride = h->xstride; s.red = h->red; s.scal = h->scal;
-  s.trace = h->trace; s.trace_cap = h->trace_cap; s.p = 0;
+  s.Vprev = h->Vprev; s.CVprev = h->CVprev; s.Y = h->Y;
+  s.Gi_in = h->Gi[cur]; s.Gi_out = h->Gi[nxt]; s.Ki = h->Ki; s.gws = h->gws;
+  s.theta = h->theta; s.xchg = h->xchg; s.red = h->red; s.scal = h->scal;
+  s.trace = h->trace; s.trace_cap = h->trace_cap;
   s.Wt = h->Wt; s.CVop = h->CVop; s.Kop = h->Kop; s.flags = h->flags;
-  s.eps = h->opts.eps; s.tol = h->opts.eig_tol; s.max_outer = h->opts.eig_max_outer; s.max_deg = 10;
+  s.eps = h->opts.eps; s.tol = h->opts.eig_tol; s.max_outer = h->opts.eig_max_outer; s.max_deg = 16;
   s.cold = 0;
-  e = launch_small_step(s, h->CL, h->ss_smem, h->ss_flags, h->st);
+  s.tdbg = h->ktime ? h->tdbg : nullptr;
+  s.pl = h->spl;
+  h->last_ss = s;
+  e = launch_small_step(s, h->st);
   if (e != cudaSuccess) return fail(h, WLR_ECUDA, std::string("small step: ") + cudaGetErrorString(e));
   if (prof) {
     cudaEventRecord(ev[5], h->st);
@@ -371,11 +378,19 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   h->rps = round_up(ceil_div(h->m, nsplit), 32);
   h->nsplit = (int)std::max<int64_t>(1, ceil_div(h->m, h->rps));
   // eigen block width b
-  int b = o.eig_block > 0 ? o.eig_block : (int)std::max<int64_t>(2 * t, t + 2);
+  int b = o.eig_block > 0 ? o.eig_block : (int)(t + 6);
   b = (int)std::min<int64_t>(std::max<int64_t>(b, t), nk);
   if (b > 32) b = 32;
   if (b < t) return fail(h, WLR_EINVAL, "r-k > 32 is not supported by this build");
   h->b = b;
+  // small-step (K3) cluster plan: depends on the dimensions only
+  {
+    SmallArgs pa{};
+    pa.k = (int)k; pa.nk = (int)nk; pa.t = (int)t; pa.b = b;
+    if (small_step_cluster_size(pa) <= 0)
+      return fail(h, WLR_ECUDA, "no schedulable cluster configuration for the small step");
+    h->spl = pa.pl;
+  }
 
   // ---- allocations
   const int64_t wt_rows = round_up(n - h->k0, 32) + 32;
@@ -393,18 +408,18 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
     if ((s = dalloc_t(h, &h->G[i], (size_t)k * k)) != WLR_OK) return s;
     if ((s = dalloc_t(h, &h->M[i], (size_t)k * nk)) != WLR_OK) return s;
     if ((s = dalloc_t(h, &h->C[i], (size_t)k * nk)) != WLR_OK) return s;
+    if ((s = dalloc_t(h, &h->Gi[i], (size_t)k * k)) != WLR_OK) return s;
   }
+  if ((s = dalloc_t(h, &h->Ki, (size_t)k * k)) != WLR_OK) return s;
+  if ((s = dalloc_t(h, &h->gws, (size_t)std::max<int64_t>(1, h->spl.CL * h->spl.gws_stride))) != WLR_OK) return s;
   if ((s = dalloc_t(h, &h->Vprev, (size_t)nk * t)) != WLR_OK) return s;
   if ((s = dalloc_t(h, &h->CVprev, (size_t)k * t)) != WLR_OK) return s;
   if ((s = dalloc_t(h, &h->Y, (size_t)nk * b)) != WLR_OK) return s;
-  if ((s = dalloc_t(h, &h->Z, (size_t)nk * b)) != WLR_OK) return s;
-  if ((s = dalloc_t(h, &h->Y1, (size_t)nk * b)) != WLR_OK) return s;
-  if ((s = dalloc_t(h, &h->Y2, (size_t)nk * b)) != WLR_OK) return s;
   if ((s = dalloc_t(h, &h->theta, 32)) != WLR_OK) return s;
-  h->xstride = small_step_xchg_stride((int)k, (int)nk, (int)t, b);
-  if ((s = dalloc_t(h, &h->xchg, (size_t)2 * 16 * h->xstride)) != WLR_OK) return s;
-  if ((s = dalloc_t(h, &h->red, (size_t)h->xstride + k * k + 2 * k * t + 64)) != WLR_OK) return s;
+  if ((s = dalloc_t(h, &h->xchg, (size_t)h->spl.CL * h->spl.flen)) != WLR_OK) return s;
+  if ((s = dalloc_t(h, &h->red, (size_t)h->spl.flen + 3 * k * t + 64)) != WLR_OK) return s;
   if ((s = dalloc_t(h, &h->scal, 8)) != WLR_OK) return s;
+  if ((s = dalloc_t(h, &h->tdbg, 64)) != WLR_OK) return s;
   if ((s = dalloc_t(h, &h->trace, (size_t)h->trace_cap * 4)) != WLR_OK) return s;
 
   // ---- NCCL communicator (rows sharded over ranks)
@@ -496,14 +511,15 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   sa.GA = h->GA; sa.a2sq = h->a2sq; sa.inc = h->fw0;
   sa.G_in = h->G[0]; sa.G_out = h->G[0]; sa.M_in = h->M[0]; sa.M_out = h->M[0];
   sa.C_in = h->C[0]; sa.C_out = h->C[0];
-  sa.Vprev = h->Vprev; sa.CVprev = h->CVprev; sa.Y = h->Y; sa.Z = h->Z; sa.Y1 = h->Y1; sa.Y2 = h->Y2;
-  sa.theta = h->theta; sa.xchg = h->xchg; sa.xchg_stride = h->xstride; sa.red = h->red; sa.scal = h->scal;
-  sa.trace = h->trace; sa.trace_cap = h->trace_cap; sa.p = 0;
+  sa.Vprev = h->Vprev; sa.CVprev = h->CVprev; sa.Y = h->Y;
+  sa.Gi_in = nullptr; sa.Gi_out = h->Gi[0]; sa.Ki = h->Ki; sa.gws = h->gws;
+  sa.theta = h->theta; sa.xchg = h->xchg; sa.red = h->red; sa.scal = h->scal;
+  sa.trace = h->trace; sa.trace_cap = h->trace_cap;
   sa.Wt = h->Wt; sa.CVop = h->CVop; sa.Kop = h->Kop; sa.flags = h->flags;
-  sa.eps = o.eps; sa.tol = o.eig_tol; sa.max_outer = 4 * o.eig_max_outer; sa.max_deg = 10; sa.cold = 1;
-  h->CL = small_step_cluster_size(sa, &h->ss_smem, &h->ss_flags);
-  if (h->CL <= 0) return fail(h, WLR_ECUDA, "no schedulable cluster configuration for the small step");
-  cudaError_t e = launch_small_step(sa, h->CL, h->ss_smem, h->ss_flags, h->st);
+  sa.eps = o.eps; sa.tol = o.eig_tol; sa.max_outer = 4 * o.eig_max_outer; sa.max_deg = 16; sa.cold = 1;
+  sa.pl = h->spl;
+  sa.tdbg = h->tdbg;
+  cudaError_t e = launch_small_step(sa, h->st);
   if (e != cudaSuccess) return fail(h, WLR_ECUDA, std::string("small step (init): ") + cudaGetErrorString(e));
   h->pr.launches = 0;
   s = check_flags(h);
@@ -536,7 +552,9 @@ extern "C" wlr_status wlr_init(wlr_handle* out, const void* A, int64_t lda, cons
   if (m_local < k && op.nranks == 1) return fail(nullptr, WLR_EINVAL, "need m >= k");
   wlr_ctx* h = new wlr_ctx();
   h->opts = op;
-  if (h->opts.eig_tol <= 0.0) h->opts.eig_tol = 1e-11;
+  // eigensolver target (relative to lambda_1; the S-product rounding floor is added in K3):
+  // fp64 mode 1e-12, fp32 mode 1e-8 (DESIGN.md §3 "eigensolver tolerance")
+  if (h->opts.eig_tol <= 0.0) h->opts.eig_tol = op.dtype == WLR_F64 ? 1e-12 : 1e-8;
   if (h->opts.eig_max_outer <= 0) h->opts.eig_max_outer = 60;
   h->m = m_local; h->n = n; h->k = k; h->r = r; h->t = r - k; h->nk = n - k;
   h->kp = round_up(k, 4); h->k0 = k & ~3LL;
@@ -728,16 +746,32 @@ extern "C" wlr_status wlr_debug_state(wlr_handle h, const char* name, double* ou
   else if (nm == "theta") { src = h->theta; cnt = h->b; }
   else if (nm == "GA") { src = h->GA; cnt = h->nk * h->nk; }
   else if (nm == "scal") { src = h->scal; cnt = 8; }
+  else if (nm == "ktime") { src = h->tdbg; cnt = 64; }
+  else if (nm == "ktime_on" || nm == "ktime_off") {   // enable/disable K3 phase timestamps
+    h->ktime = nm == "ktime_on";
+    for (auto& g : h->gexec)
+      if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+    if (count) *count = 0;
+    return WLR_OK;
+  }
+  else if (nm == "ss_rerun") {                 // relaunch the last small step twice (timing only;
+    SmallArgs s2 = h->last_ss;                  // leaves the state inconsistent)
+    s2.tdbg = h->tdbg;
+    for (int rep = 0; rep < 2; ++rep) CUDA_TRY(h, launch_small_step(s2, h->st));
+    CUDA_TRY(h, cudaStreamSynchronize(h->st));
+    if (count) *count = 0;
+    return WLR_OK;
+  }
+  else if (nm == "outer") {                    // eigensolver restarts of the last small step
+    int fl[8];
+    CUDA_TRY(h, cudaMemcpy(fl, h->flags, sizeof(fl), cudaMemcpyDeviceToHost));
+    if (count) *count = 1;
+    if (out && cap >= 1) out[0] = fl[3];
+    return WLR_OK;
+  }
   else return fail(h, WLR_EINVAL, "unknown state name");
   if (count) *count = cnt;
   if (out) CUDA_TRY(h, cudaMemcpy(out, src, (size_t)std::min(cap, cnt) * 8, cudaMemcpyDeviceToHost));
-  if (out && nm == "scal" && cap >= 8) {
-    // expose device flags too: scal[6] = eigensolver outer iterations of the last step
-    int fl[8];
-    CUDA_TRY(h, cudaMemcpy(fl, h->flags, sizeof(fl), cudaMemcpyDeviceToHost));
-    out[6] = fl[3];
-    out[7] = fl[2];
-  }
   return WLR_OK;
 }
 

@@ -60,35 +60,53 @@ void launch_reduce_incr(const double* part, int nsplit, int k, int nk, int nz, i
                         int kp, const double* fw_part, int nfw, double* inc, cudaStream_t st);
 
 // ---------------------------------------------------------------- small step (small_step.cu)
+// Shared-memory plan of the K3 cluster kernel (offsets in doubles; identical in every CTA
+// of the cluster so that DSMEM addresses of a peer's buffers equal the local ones).
+// Optional regions have offset -1 when they do not fit (then the code reads the global
+// originals, or the CTA's slot of the global workspace gws for the Newton-Schulz mats).
+struct SSPlan {
+  int CL, SL;                       // cluster size, columns per CTA (slice of the n-k index)
+  int KS, JS;                       // S-product split: KS reduction chunks x JS column groups
+  int PL;                           // DSMEM exchange length (doubles per bank)
+  int64_t oPart, oBuf, oVp, oE, oSE, oWk, oCinE, oSmall, oRed;            // always in smem
+  int64_t oCs, oMs, oCin, oXf, oMat3, oGsq, oTail;                         // optional
+  int64_t total;                    // doubles of dynamic smem
+  int64_t gws_stride;               // doubles of global workspace per CTA (Gsq fallback)
+  int64_t flen;                     // final partial length (global reduce-scatter)
+};
+
 struct SmallArgs {
-  int k, nk, t, b, kp, k0, rp;      // dims; b = eigen block width
+  int k, nk, t, b, kp, k0, rp;      // dims; b = eigen block width (t <= b <= 32)
   int mode;                         // 0: init (G, M given), 1: iteration (apply increments)
   int dtype;                        // 0 fp32 operands, 1 fp64 operands
   int uniform; double w2;           // uniform weight squared
-  const double* GA; double a2sq;    // A2^T A2 ((nk)^2), ||A2||_F^2
+  const double* GA; double a2sq;    // A2^T A2 ((nk)^2, symmetric), ||A2||_F^2
   const double* inc;                // [N | Gamma | Omega | f_w] (mode 1); f_w at [0] (mode 0)
   const double* G_in; double* G_out;   // k x k
   const double* M_in; double* M_out;   // k x nk
   const double* C_in; double* C_out;   // k x nk
   double* Vprev;                    // nk x t  (V of the previous state; updated in place)
   double* CVprev;                   // k x t   (C V of the previous state; updated)
-  double* Y; double* Z; double* Y1; double* Y2;   // nk x b each (Ritz block + scratch)
-  double* theta;                    // b Ritz values (warm start)
-  double* xchg;                     // cluster exchange slots
-  int64_t xchg_stride;              // doubles per slot
-  double* red;                      // reduced exchange
-  double* scal;                     // persistent scalars (see small_step.cu)
-  double* trace; int trace_cap; int64_t p;   // trace ring (4 doubles per state)
+  double* Y;                        // nk x b  warm-start Ritz block (updated)
+  const double* Gi_in; double* Gi_out;   // k x k  G^{-1} of the previous / current state
+  double* Ki;                       // k x k  (w^2 I + C C^T)^{-1} (uniform W1; updated)
+  double* gws;                      // CL x gws_stride global workspace
+  double* theta;                    // b Ritz values (updated; previous values read first)
+  double* xchg;                     // CL x flen global partial slots
+  double* red;                      // flen reduced partials
+  double* scal;                     // persistent scalars (see small_step.cuh)
+  double* trace; int trace_cap;     // trace ring (4 doubles per state)
   void* Wt; void* CVop; void* Kop;  // row-pass operands (dtype)
   int* flags;
   double eps, tol; int max_outer, max_deg;
   int cold;                         // 1: Y holds a random block (no Ritz values yet)
+  double* tdbg;                     // optional phase timestamps (64 doubles) or nullptr
+  SSPlan pl;
 };
-int small_step_cluster_size(const SmallArgs& a, size_t* smem_out, int* smem_flags);
-cudaError_t launch_small_step(const SmallArgs& a, int cluster, size_t smem, int smem_flags,
-                              cudaStream_t st);
+bool small_step_plan(SmallArgs& a, int CL);       // fills a.pl; false if it cannot fit
+int small_step_cluster_size(SmallArgs& a);        // picks CL and fills a.pl (0 = none)
+cudaError_t launch_small_step(const SmallArgs& a, cudaStream_t st);
 int small_step_bt(int b);
-int64_t small_step_xchg_stride(int k, int nk, int t, int b);
 
 // ---------------------------------------------------------------- result (result.cu)
 template <typename T>

@@ -1,30 +1,19 @@
-// small_step.cu -- dispatch of the K3 cluster kernel (templates in small_step.cuh, one
-// translation unit per eigen-block width BT so the build parallelises).
+// small_step.cu -- host side of K3: shared-memory plan, cluster-size choice and dispatch of
+// the cluster kernel (templates in small_step.cuh, one translation unit per eigen-block
+// width BT so the build parallelises).
 #include "small_step.cuh"
 
 namespace wlr {
 
-extern template cudaError_t launch_ss<4>(const SmallArgs&, int, size_t, int, cudaStream_t);
-extern template int ss_max_clusters<4>(int, size_t);
-extern template cudaError_t launch_ss<8>(const SmallArgs&, int, size_t, int, cudaStream_t);
-extern template int ss_max_clusters<8>(int, size_t);
-extern template cudaError_t launch_ss<12>(const SmallArgs&, int, size_t, int, cudaStream_t);
-extern template int ss_max_clusters<12>(int, size_t);
-extern template cudaError_t launch_ss<16>(const SmallArgs&, int, size_t, int, cudaStream_t);
-extern template int ss_max_clusters<16>(int, size_t);
-extern template cudaError_t launch_ss<24>(const SmallArgs&, int, size_t, int, cudaStream_t);
-extern template int ss_max_clusters<24>(int, size_t);
-extern template cudaError_t launch_ss<32>(const SmallArgs&, int, size_t, int, cudaStream_t);
-extern template int ss_max_clusters<32>(int, size_t);
-
-// exchange-slot payload (doubles) large enough for every round
-int64_t small_step_xchg_stride(int k, int nk, int t, int b) {
-  int64_t fin = 5 + 7LL * k * t + 4LL * t * t + (int64_t)k * k + 8;
-  int64_t prod = (int64_t)k * b;
-  int64_t gram = (int64_t)b * b + b;
-  int64_t s = std::max(fin, std::max(prod, gram));
-  return round_up(s, 32);
-}
+#define WLR_SS_EXTERN(B)                                                                   \
+  extern template cudaError_t launch_ss<B>(const SmallArgs&, cudaStream_t);                 \
+  extern template int ss_max_clusters<B>(int, size_t);
+WLR_SS_EXTERN(4)
+WLR_SS_EXTERN(8)
+WLR_SS_EXTERN(12)
+WLR_SS_EXTERN(16)
+WLR_SS_EXTERN(24)
+WLR_SS_EXTERN(32)
 
 static int bt_of(int b) { return b <= 4 ? 4 : b <= 8 ? 8 : b <= 12 ? 12 : b <= 16 ? 16 : b <= 24 ? 24 : 32; }
 int small_step_bt(int b) { return bt_of(b); }
@@ -40,34 +29,74 @@ static int max_clusters(int bt, int CL, size_t smem) {
   }
 }
 
-// Choose the cluster size (largest of 16, 8, 4, 2, 1 the device can co-schedule) and
-// whether G_A rows fit in shared memory.
-int small_step_cluster_size(const SmallArgs& a, size_t* smem_out, int* flags_out) {
-  const int bt = bt_of(a.b);
-  const int want = (int)std::max<int64_t>(1, std::min<int64_t>(16, ceil_div(a.nk, 24)));
-  for (int CL = 16; CL >= 1; CL /= 2) {
-    if (CL > want && CL > 1) continue;
-    for (int fl = 3; fl >= 0; --fl) {
-      const size_t smem = ss_smem_bytes(a, CL, fl);
-      if (smem > 220 * 1024) continue;
-      if (max_clusters(bt, CL, smem) >= 1) {
-        *smem_out = smem;
-        *flags_out = fl;
-        return CL;
-      }
-    }
+static constexpr int64_t kSmemLimit = 227 * 1024 / 8;   // doubles per CTA
+
+// Lay out the shared memory of one CTA for cluster size CL.  Required regions first, then
+// optional ones greedily in priority order (C' slice, Newton-Schulz mats, M' slice, gathered
+// S-product operand, staged G/Gamma/Omega, C_in slice, CTA-0 tail staging); an optional
+// region that does not fit gets offset -1 (the kernel then uses the global copy).
+bool small_step_plan(SmallArgs& a, int CL) {
+  SSPlan& p = a.pl;
+  const int k = a.k, nk = a.nk, t = a.t, b = a.b, bt = bt_of(b);
+  p.CL = CL;
+  p.SL = (int)ceil_div(nk, CL);
+  if (p.SL > 64 || p.SL < 1) return false;
+  p.JS = bt <= 8 ? 1 : bt <= 16 ? 2 : 4;
+  p.KS = 16 / p.JS;
+  const int64_t SL = p.SL, kt = (int64_t)k * t, kk = (int64_t)k * k;
+  int64_t pl = std::max<int64_t>({(int64_t)k * b, 2LL * b * b + 2LL * t * b, (int64_t)t + kt});
+  p.PL = (int)round_up(pl, 2);
+  const FinOff fo(k, t);
+  p.flen = fo.len;
+  const SmallOff so(b, t, k);
+  int64_t o = 0;
+  auto take = [&](int64_t n) { const int64_t r = o; o += round_up(n, 2); return r; };
+  p.oPart = take(2LL * p.PL);
+  p.oBuf = take(4 * SL * b);
+  p.oVp = take(SL * t);
+  p.oE = take(SL * t);
+  p.oSE = take(SL * t);
+  p.oWk = take((int64_t)k * b);
+  p.oCinE = take(t + kt);
+  p.oSmall = take(so.len);
+  p.oRed = take((int64_t)p.KS * SL * b);
+  if (o > kSmemLimit) return false;
+  auto opt = [&](int64_t n) -> int64_t {
+    if (o + round_up(n, 2) > kSmemLimit) return -1;
+    return take(n);
+  };
+  p.oCs = opt((int64_t)k * SL);
+  p.oGsq = opt(4 * kk);
+  p.oMs = opt((int64_t)k * SL);
+  p.oXf = opt((int64_t)nk * b);
+  p.oMat3 = opt(3 * kk + kt);
+  p.oCin = opt((int64_t)k * SL);
+  p.oTail = opt(p.flen + 3 * kt);
+  p.total = o;
+  p.gws_stride = p.oGsq >= 0 ? 0 : 4 * kk;
+  return true;
+}
+
+// Largest cluster (<= 16 CTAs, >= 24 columns per CTA where possible) whose plan fits and
+// which the device can co-schedule.
+int small_step_cluster_size(SmallArgs& a) {
+  const int lo = (int)std::max<int64_t>(1, ceil_div(a.nk, 64));
+  const int want = (int)std::max<int64_t>(lo, std::min<int64_t>(16, ceil_div(a.nk, 24)));
+  for (int CL = want; CL >= lo; --CL) {
+    if (!small_step_plan(a, CL)) continue;
+    if (max_clusters(bt_of(a.b), CL, (size_t)a.pl.total * 8) >= 1) return CL;
   }
   return 0;
 }
 
-cudaError_t launch_small_step(const SmallArgs& a, int CL, size_t smem, int fl, cudaStream_t st) {
+cudaError_t launch_small_step(const SmallArgs& a, cudaStream_t st) {
   switch (bt_of(a.b)) {
-    case 4: return launch_ss<4>(a, CL, smem, fl, st);
-    case 8: return launch_ss<8>(a, CL, smem, fl, st);
-    case 12: return launch_ss<12>(a, CL, smem, fl, st);
-    case 16: return launch_ss<16>(a, CL, smem, fl, st);
-    case 24: return launch_ss<24>(a, CL, smem, fl, st);
-    default: return launch_ss<32>(a, CL, smem, fl, st);
+    case 4: return launch_ss<4>(a, st);
+    case 8: return launch_ss<8>(a, st);
+    case 12: return launch_ss<12>(a, st);
+    case 16: return launch_ss<16>(a, st);
+    case 24: return launch_ss<24>(a, st);
+    default: return launch_ss<32>(a, st);
   }
 }
 

@@ -1,22 +1,30 @@
-// small_step.cu -- K3: the (C, D) half-step of Algorithm 1
+// small_step.cuh -- K3: the (C, D) half-step of Algorithm 1
 // on the Gram route, plus the objective and the convergence reduction.
 //
-// Runs as ONE thread-block cluster (CL CTAs, up to 16, one per SM) so that every
-// cross-CTA exchange is a hardware cluster barrier instead of a grid barrier.  Each CTA
-// owns a contiguous slice of the (n-k)-dimensional column index space and keeps its
-// rows of G_A = A2^T A2 resident in shared memory when they fit.
+// ONE thread-block cluster of CL CTAs (<= 16, one per SM).  CTA c owns the columns
+// [rs, rs + nl) of the (n-k)-dimensional index ("its slice"); per-slice vectors live in its
+// shared memory and every cross-CTA sum is a fixed-order DSMEM reduction behind one hardware
+// cluster barrier, so results are bitwise identical on every CTA (and on every rank of a
+// row-sharded run).  The kernel is latency-bound: every small dense step is
+// written as thread-per-output work or a parallel (round-robin) Jacobi, never as a long
+// single-thread chain, and inverses are Newton-Schulz refined from the previous iteration's.
 //
 //   Gram update   G' = G + Gamma + Gamma^T + Omega,  M' = M + N,  H = G + Gamma
-//   C             C' = G'^{-1} M'          (= R^{-1} Q^T A2 with X1 = QR)
-//   eigenpairs    top r-k of  S = G_A - M'^T C' = A2^T P^perp A2   (matrix-free S.Y)
-//                 -> V (right singular vectors of P^perp A2), lambda = sigma^2
-//                 so D = U Sigma_{r-k} V^T = (A2 - X1 C) V V^T
-//                 Chebyshev-filtered subspace iteration with Rayleigh-Ritz, warm-started
-//                 from the previous iteration's Ritz block.
+//   C             C' = G'^{-1} M'   (= R^{-1} Q^T A2); G'^{-1} by Newton-Schulz
+//                 from G_p^{-1} (fallback and init: symmetric Gauss-Jordan sweep)
+//   eigenpairs    top t = r-k of S = G_A - M'^T C' = A2^T P^perp A2 by matrix-free products
+//                 S X = G_A X - M'^T (C' X) (G_A streamed from L2): a Rayleigh-Ritz step on the
+//                 warm Ritz block and, only while the residual is above tolerance, Chebyshev-
+//                 filtered subspace iteration of adaptive degree.  V = right singular vectors of
+//                 P^perp A2, lambda = sigma^2, D = U Sigma_{r-k} V^T = (A2 - X1 C) V V^T
+//
 //   objective     F = f_w + ||A2||^2 - <M', C'> - sum(lambda)
 //   step norm     ||X_{p+1} - X_p||_F from small-side products only
-//   operands      Wt = [V | C^T], C V and K^{-1} = (w^2 I + C C^T)^{-1} (or C C^T) for
-//                 the next row pass, converted to the storage dtype.
+//   operands      Wt = [V | C^T], C V and K^{-1} = (w^2 I + C C^T)^{-1} (or C C^T) for the
+//                 next row pass, converted to the storage dtype.
+//
+// scal[] layout: 0 ||X2_p||^2, 1 ||X_p||^2, 2 F_p, 3 step, 4 rel, 5 p, 6 residual ratio
+// max_j ||S v_j - lambda_j v_j|| / lambda_1 of the last Rayleigh-Ritz, 7 S-products.
 #pragma once
 #include <cooperative_groups.h>
 
@@ -26,711 +34,974 @@ namespace cg = cooperative_groups;
 
 namespace wlr {
 
-
 constexpr int kSST = 512;            // threads per CTA
-constexpr int kSSW = kSST / 32;
+constexpr int kSSW = kSST / 32;      // warps per CTA
+constexpr double kEps = 2.220446049250313e-16;
 
-struct SSCtx {
-  SmallArgs a;
-  int c, CL, rs, re, nloc;
-  double* GAs;         // nloc x nk (smem) or nullptr
-  double* Ls;          // k x k
-  double* Hs;          // k x k
-  double* Wk;          // k x b
-  double* Tb;          // b x b (Gram / T)
-  double* Ub;          // b x b
-  double* vb;          // b (theta / scale)
-  double* Yst;         // nk x b staged transposed (smem) or nullptr
-  double* Xw;          // per-warp solve scratch (kSSW x k)
-  double* red;         // smem reduction scratch (kSSW)
-  int* bank;           // exchange bank parity (per-CTA, uniform)
+// Small-region layout (doubles, relative to pl.oSmall)
+struct SmallOff {
+  int Tb, Ub, Lb, Li, Qb, Wb, Gx, th, dsc, Rt, cs, d0, rb, len;
+  __host__ __device__ SmallOff(int b, int t, int k) {
+    const int bb = 32 * 32;             // b <= 32; fixed 32 x 32 tiles keep offsets simple
+    Tb = 0; Ub = Tb + bb; Lb = Ub + bb; Li = Lb + bb; Qb = Li + bb; Wb = Qb + bb;
+    Gx = Wb + bb;                       // reduced Gram exchange: Gyy | Gyz | VpY | VpZ
+    th = Gx + 2 * b * b + 2 * t * b + 8;
+    dsc = th + 32; Rt = dsc + 32; cs = Rt + t * t + 8; d0 = cs + 64; rb = d0 + k + 8;
+    len = rb + 2 * (k + 8);
+  }
 };
 
-WLR_DEVI void cl_sync() {
-  __threadfence();
-  cg::this_cluster().sync();
+// Final partial layout (global reduce-scatter)
+struct FinOff {
+  int CnV, CnVn, CVn, MnV, MVn, NV, CE, EE, ESE, CC, len;
+  __host__ __device__ FinOff(int k, int t) {
+    const int kt = k * t;
+    CnV = 5; CnVn = CnV + kt; CVn = CnVn + kt; MnV = CVn + kt; MVn = MnV + kt; NV = MVn + kt;
+    CE = NV + kt; EE = CE + kt; ESE = EE + t * t; CC = ESE + t * t; len = CC + k * k;
+  }
+};
+
+struct SS {
+  int c, CL, rs, nl, SL, k, nk, b, t;
+  double* sm;
+  int bank;
+  int nt;                // timestamps recorded (CTA 0, thread 0; a.tdbg != nullptr)
+};
+
+// Phase timestamps for profiling the latency-bound small step: CTA 0 /
+// thread 0 writes %globaltimer (ns) into a.tdbg[1..31] and clock64 into a.tdbg[32..].
+WLR_DEVI void tmark(SS& s, const SmallArgs& a) {
+  if (a.tdbg && s.c == 0 && threadIdx.x == 0 && s.nt < 31) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.tdbg[1 + s.nt] = (double)t;
+    a.tdbg[32 + s.nt] = (double)clock64();
+    a.tdbg[0] = (double)(s.nt + 1);
+  }
+  s.nt++;
 }
 
-WLR_DEVI double* slot(SSCtx& s, int cta) {
-  return s.a.xchg + ((int64_t)(*s.bank) * s.CL + cta) * s.a.xchg_stride;
-}
+WLR_DEVI double* xpart(SS& s, const SSPlan& p) { return s.sm + p.oPart + (int64_t)s.bank * p.PL; }
 
-// one exchange round: every CTA wrote its partial of length len into slot(c); after the
-// barrier, out[i] = sum_c slot(c)[i] in fixed CTA order (identical on every CTA).
-WLR_DEVI void xchg_reduce(SSCtx& s, int len, double* out) {
-  cl_sync();
+// Fixed-order cluster sum of the len-long partial every CTA wrote into xpart(); out is local.
+WLR_DEVI void xreduce(SS& s, const SSPlan& p, int len, double* out) {
+  cg::cluster_group cl = cg::this_cluster();
+  cl.sync();
+  const double* mine = xpart(s, p);
   for (int i = threadIdx.x; i < len; i += kSST) {
-    double v = 0.0;
-    for (int c = 0; c < s.CL; ++c) v += __ldcg(s.a.xchg + ((int64_t)(*s.bank) * s.CL + c) * s.a.xchg_stride + i);
-    out[i] = v;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) *s.bank ^= 1;
-  __syncthreads();
-}
-
-// Cholesky of the n x n symmetric matrix in smem (row-major, lower result in place) by
-// warp 0.  Returns true iff every pivot d_j > rel * A_jj (the original diagonal, after the
-// shift); result broadcast to the block.  rel > 0 is the numerical-rank test of the Gram
-// route (reading R6b): a pivot at rounding level of its column's squared norm
-// means that column lies in the span of the previous ones.
-WLR_DEVI bool chol_warp0(double* A, int n, int ld, double shift, double rel = 0.0) {
-  __shared__ int ok_s;
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    bool ok = true;
-    if (shift != 0.0)
-      for (int i = lane; i < n; i += 32) A[i * ld + i] += shift;
-    __syncwarp();
-    double od[4];                            // original diagonal, lane + 32q (n <= 128)
+    double v[16];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) od[q] = (lane + 32 * q < n) ? A[(lane + 32 * q) * (ld + 1)] : 0.0;
-    __syncwarp();
-    for (int j = 0; j < n; ++j) {
-      const double d = A[j * ld + j];
-      const int q = j >> 5;
-      const double oq = q == 0 ? od[0] : q == 1 ? od[1] : q == 2 ? od[2] : od[3];
-      const double d0 = __shfl_sync(0xffffffffu, oq, j & 31);
-      ok = ok && (d > rel * d0) && (d > 0.0) && isfinite(d);
-      const double r = sqrt(d > 0.0 ? d : 1.0);
-      const double inv = 1.0 / r;
-      __syncwarp();
-      if (lane == 0) A[j * ld + j] = r;
-      for (int i = j + 1 + lane; i < n; i += 32) A[i * ld + j] *= inv;
-      __syncwarp();
-      for (int i = j + 1 + lane; i < n; i += 32) {
-        const double lij = A[i * ld + j];
-        for (int l = j + 1; l <= i; ++l) A[i * ld + l] = fma(-lij, A[l * ld + j], A[i * ld + l]);
-      }
-      __syncwarp();
-    }
-    if (lane == 0) ok_s = ok ? 1 : 0;
+    for (int c = 0; c < 16; ++c) v[c] = c < s.CL ? cl.map_shared_rank(mine, c)[i] : 0.0;
+    double acc = 0.0;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) acc += v[c];
+    out[i] = acc;
   }
   __syncthreads();
-  return ok_s != 0;
+  s.bank ^= 1;
 }
 
-// x := L^{-T} L^{-1} x for one vector x in smem/global (stride sx), by one warp
-WLR_DEVI void chol_solve_warp(const double* L, int n, int ld, double* x, int sx, int lane) {
-  for (int j = 0; j < n; ++j) {
-    const double zj = x[j * sx] / L[j * ld + j];
-    for (int i = j + 1 + lane; i < n; i += 32) x[i * sx] = fma(-L[i * ld + j], zj, x[i * sx]);
-    __syncwarp();
-    if (lane == 0) x[j * sx] = zj;
-    __syncwarp();
-  }
-  for (int j = n - 1; j >= 0; --j) {
-    const double xj = x[j * sx] / L[j * ld + j];
-    for (int i = lane; i < j; i += 32) x[i * sx] = fma(-L[j * ld + i], xj, x[i * sx]);
-    __syncwarp();
-    if (lane == 0) x[j * sx] = xj;
-    __syncwarp();
-  }
-}
-
-// Cyclic Jacobi eigen-decomposition of the symmetric b x b matrix T (smem), by warp 0:
-// on exit theta = eigenvalues in DESCENDING order and U (b x b, columns) the matching
-// orthonormal eigenvectors.  Deterministic, so every CTA obtains identical results.
-WLR_DEVI void jacobi_warp0(double* T, double* U, double* theta, int b) {
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    for (int i = lane; i < b * b; i += 32) U[i] = (i / b == i % b) ? 1.0 : 0.0;
-    __syncwarp();
-    for (int sweep = 0; sweep < 60; ++sweep) {
-      bool rotated = false;
-      for (int p = 0; p < b - 1; ++p) {
-        for (int q = p + 1; q < b; ++q) {
-          const double apq = T[p * b + q];
-          const double app = T[p * b + p], aqq = T[q * b + q];
-          if (!(fabs(apq) > 1e-300) || fabs(apq) <= 1e-17 * sqrt(fabs(app * aqq))) continue;
-          rotated = true;
-          const double tau = (aqq - app) / (2.0 * apq);
-          const double tt = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-          const double c = 1.0 / sqrt(1.0 + tt * tt), s = tt * c;
-          __syncwarp();
-          if (lane < b && lane != p && lane != q) {
-            const double tip = T[lane * b + p], tiq = T[lane * b + q];
-            const double nip = c * tip - s * tiq, niq = s * tip + c * tiq;
-            T[lane * b + p] = nip; T[p * b + lane] = nip;
-            T[lane * b + q] = niq; T[q * b + lane] = niq;
-          }
-          if (lane < b) {
-            const double uip = U[lane * b + p], uiq = U[lane * b + q];
-            U[lane * b + p] = c * uip - s * uiq;
-            U[lane * b + q] = s * uip + c * uiq;
-          }
-          if (lane == 0) {
-            T[p * b + p] = app - tt * apq;
-            T[q * b + q] = aqq + tt * apq;
-            T[p * b + q] = 0.0;
-            T[q * b + p] = 0.0;
-          }
-          __syncwarp();
-        }
-      }
-      if (!rotated) break;
-    }
-    // sort descending (stable by index) and permute U's columns
-    double wj = lane < b ? T[lane * b + lane] : 0.0;
-    int rk = 0;
-    for (int i = 0; i < b; ++i) {
-      const double wi = T[i * b + i];
-      if (wi > wj || (wi == wj && i < lane)) ++rk;
-    }
-    double ucol[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) ucol[i] = (i < b && lane < b) ? U[i * b + lane] : 0.0;
-    __syncwarp();
-    if (lane < b) {
-      theta[rk] = wj;
-#pragma unroll
-      for (int i = 0; i < 32; ++i)
-        if (i < b) U[i * b + rk] = ucol[i];
-    }
-    __syncwarp();
-  }
-  __syncthreads();
-}
-
-// block reduction of one double per thread (result valid on all threads)
-WLR_DEVI double block_sum(double v, double* red) {
-  v = warp_sum(v);
+// block reduction of NV values per thread (sum; result valid on all threads)
+template <int NV>
+WLR_DEVI void block_sum_n(double (&v)[NV], double* red) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int u = 0; u < NV; ++u) v[u] = warp_sum(v[u]);
+  if (lane == 0)
+#pragma unroll
+    for (int u = 0; u < NV; ++u) red[u * kSSW + warp] = v[u];
   __syncthreads();
+#pragma unroll
+  for (int u = 0; u < NV; ++u) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kSSW; ++w) s += red[u * kSSW + w];
+    v[u] = s;
+  }
+  __syncthreads();
+}
+
+WLR_DEVI double block_max(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane == 0) red[warp] = v;
   __syncthreads();
-  double s = 0.0;
-  for (int w = 0; w < kSSW; ++w) s += red[w];
+  double m = 0.0;
+#pragma unroll
+  for (int w = 0; w < kSSW; ++w) m = fmax(m, red[w]);
   __syncthreads();
-  return s;
+  return m;
 }
 
-// Z[slice] = S . Yin[slice] = G_A[slice,:] Yin - M'[:,slice]^T (C' Yin)    (one product)
-template <int BT>
-WLR_DEVI void s_product(SSCtx& s, const double* Yin, double* Zout, const double* Mx = nullptr,
-                        const double* Cx = nullptr) {
-  constexpr int RG = BT <= 12 ? 4 : 2;       // rows per warp pass (register blocking)
-  const SmallArgs& a = s.a;
-  const int k = a.k, nk = a.nk, b = a.b;
-  if (!Mx) Mx = a.M_out;
-  if (!Cx) Cx = a.C_out;
-  // (1) partial W_c = C'[:, slice] . Yin[slice, :]
-  double* my = slot(s, s.c);
-  for (int idx = threadIdx.x; idx < k * b; idx += kSST) {
-    const int l = idx / b, j = idx % b;
-    double v = 0.0;
-    for (int i = s.rs; i < s.re; ++i) v = fma(Cx[(int64_t)l * nk + i], Yin[(int64_t)i * b + j], v);
-    my[idx] = v;
-  }
-  xchg_reduce(s, k * b, s.Wk);               // includes the cluster barrier (Yin complete)
-  if (s.Yst) {                               // stage Yin transposed: Yst[j][l]
-    for (int idx = threadIdx.x; idx < nk * b; idx += kSST) {
-      const int l = idx / b, j = idx % b;
-      s.Yst[(int64_t)j * nk + l] = Yin[idx];
+// C[r][c] = alpha * sum_q A[r*lda + q] B[q*ldb + c] (+ I if addI), thread per output.
+WLR_DEVI void gemm_nn(int m, int n, int kk, const double* A, int lda, const double* B, int ldb,
+                      double* C, int ldc, double alpha, bool addI) {
+  for (int o = threadIdx.x; o < m * n; o += kSST) {
+    const int r = o / n, c = o - r * n;
+    const double* pa = A + (int64_t)r * lda;
+    const double* pb = B + c;
+    double v0 = 0.0, v1 = 0.0;
+    int q = 0;
+    for (; q + 1 < kk; q += 2) {
+      v0 = fma(pa[q], pb[(int64_t)q * ldb], v0);
+      v1 = fma(pa[q + 1], pb[(int64_t)(q + 1) * ldb], v1);
     }
-    __syncthreads();
+    if (q < kk) v0 = fma(pa[q], pb[(int64_t)q * ldb], v0);
+    double v = alpha * (v0 + v1);
+    if (addI && r == c) v += 1.0;
+    C[(int64_t)r * ldc + c] = v;
   }
-  // (2) rows of the slice, RG rows per warp pass, lanes over the reduction index
+}
+
+// Segments of "transpose-NN" slice contractions: out[r*ncol + c] = sum_{i < nl}
+// A[r*ars + i*ais] B[c*bcs + i*bis]  (thread per output, all segments in one pass).
+struct TN {
+  const double* A; int ars, ais;
+  const double* B; int bcs, bis;
+  int nrow, ncol;
+  double* out;
+};
+template <int ND>
+WLR_DEVI void slice_tn(int nl, const TN (&d)[ND]) {
+  int tot = 0;
+#pragma unroll
+  for (int u = 0; u < ND; ++u) tot += d[u].nrow * d[u].ncol;
+  for (int o = threadIdx.x; o < tot; o += kSST) {
+    int u = 0, base = 0;
+#pragma unroll
+    for (int q = 0; q < ND - 1; ++q)
+      if (o >= base + d[u].nrow * d[u].ncol) { base += d[u].nrow * d[u].ncol; ++u; }
+    const TN& g = d[u];
+    const int oo = o - base, r = oo / g.ncol, c = oo - r * g.ncol;
+    const double* pa = g.A + (int64_t)r * g.ars;
+    const double* pb = g.B + (int64_t)c * g.bcs;
+    double v0 = 0.0, v1 = 0.0;
+    int i = 0;
+    for (; i + 1 < nl; i += 2) {
+      v0 = fma(pa[(int64_t)i * g.ais], pb[(int64_t)i * g.bis], v0);
+      v1 = fma(pa[(int64_t)(i + 1) * g.ais], pb[(int64_t)(i + 1) * g.bis], v1);
+    }
+    if (i < nl) v0 = fma(pa[(int64_t)i * g.ais], pb[(int64_t)i * g.bis], v0);
+    g.out[oo] = v0 + v1;
+  }
+}
+
+// In-place inverse of the SPD n x n matrix A (row-major) by the sweep operator (symmetric
+// Gauss-Jordan), whole CTA.  Returns false (uniformly) if a pivot is not > rel * its
+// original diagonal (numerical rank test, reading R6b).  Init / fallback only.
+WLR_DEVI bool sweep_inverse(double* A, int n, double rel, double* d0, double* rb) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int g0 = warp * RG; g0 < s.nloc; g0 += kSSW * RG) {
-    double acc[RG][BT];
-#pragma unroll
-    for (int r = 0; r < RG; ++r)
-#pragma unroll
-      for (int j = 0; j < BT; ++j) acc[r][j] = 0.0;
-    const double* grow[RG];
-#pragma unroll
-    for (int r = 0; r < RG; ++r) {
-      const int il = g0 + r < s.nloc ? g0 + r : g0;
-      grow[r] = s.GAs ? s.GAs + (int64_t)il * nk : a.GA + (int64_t)(s.rs + il) * nk;
-    }
-    for (int l = lane; l < nk; l += 32) {
-      double yv[BT];
-#pragma unroll
-      for (int j = 0; j < BT; ++j)
-        yv[j] = j < b ? (s.Yst ? s.Yst[(int64_t)j * nk + l] : Yin[(int64_t)l * b + j]) : 0.0;
-#pragma unroll
-      for (int r = 0; r < RG; ++r) {
-        const double gv = grow[r][l];
-#pragma unroll
-        for (int j = 0; j < BT; ++j) acc[r][j] = fma(gv, yv[j], acc[r][j]);
-      }
-    }
-    for (int l = lane; l < k; l += 32) {
-#pragma unroll
-      for (int r = 0; r < RG; ++r) {
-        const int i = s.rs + (g0 + r < s.nloc ? g0 + r : g0);
-        const double mli = Mx[(int64_t)l * nk + i];
-#pragma unroll
-        for (int j = 0; j < BT; ++j)
-          if (j < b) acc[r][j] = fma(-mli, s.Wk[l * b + j], acc[r][j]);
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < RG; ++r)
-#pragma unroll
-      for (int j = 0; j < BT; ++j) acc[r][j] = warp_sum(acc[r][j]);
-#pragma unroll
-    for (int r = 0; r < RG; ++r)
-#pragma unroll
-      for (int j = 0; j < BT; ++j)
-        if (j < b && lane == j && g0 + r < s.nloc) Zout[(int64_t)(s.rs + g0 + r) * b + j] = acc[r][j];
-  }
+  for (int i = threadIdx.x; i < n; i += kSST) d0[i] = A[(int64_t)i * n + i];
   __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    double* rj = rb + (j & 1) * (n + 8);       // double-buffered pivot row
+    for (int i = threadIdx.x; i < n; i += kSST) rj[i] = A[(int64_t)j * n + i];
+    __syncthreads();
+    const double p = rj[j];
+    if (!(p > rel * d0[j]) || !(p > 0.0) || !isfinite(p)) return false;
+    const double pinv = 1.0 / p;
+    for (int i = warp; i < n; i += kSSW) {
+      const double ri = rj[i] * pinv;
+      for (int l = lane; l < n; l += 32) {
+        double v;
+        if (i == j) v = (l == j) ? -pinv : rj[l] * pinv;
+        else if (l == j) v = ri;
+        else v = fma(-ri, rj[l], A[(int64_t)i * n + l]);
+        A[(int64_t)i * n + l] = v;
+      }
+    }
+    __syncthreads();
+  }
+  for (int idx = threadIdx.x; idx < n * n; idx += kSST) A[idx] = -A[idx];
+  __syncthreads();
+  return true;
 }
 
-// Y[slice] := Y[slice] R^{-1} with Gram = R^T R (CholQR pass).  scaled: Jacobi-scaled and
-// shifted first pass.  Returns false if the Gram is not numerically positive definite.
-template <int BT>
-WLR_DEVI bool cholqr_pass(SSCtx& s, double* Y, bool scaled) {
-  const SmallArgs& a = s.a;
-  const int b = a.b;
-  double* my = slot(s, s.c);
-  for (int idx = threadIdx.x; idx < b * b; idx += kSST) {
-    const int p = idx / b, q = idx % b;
-    double v = 0.0;
-    for (int i = s.rs; i < s.re; ++i) v = fma(Y[(int64_t)i * b + p], Y[(int64_t)i * b + q], v);
-    my[idx] = v;
-  }
-  xchg_reduce(s, b * b, s.Tb);
-  if (scaled) {
-    if (threadIdx.x < b) {
-      const double d = s.Tb[threadIdx.x * b + threadIdx.x];
-      s.vb[threadIdx.x] = d > 0.0 ? 1.0 / sqrt(d) : 1.0;
+// Newton-Schulz refinement of X ~ G^{-1} (n x n, row-major; R, P scratch n x n):
+// R = I - G X, X <- X + X R.  Returns false (uniformly) when max|I - G X| >= 3e-2 (the
+// warm start is too far: the caller falls back to the sweep).  The number of steps is
+// chosen from the initial residual so that delta^(2^steps) <= 1e-12.
+WLR_DEVI bool ns_inverse(const double* G, double* X, double* R, double* P, int n, double* red) {
+  gemm_nn(n, n, n, G, n, X, n, R, n, -1.0, true);
+  __syncthreads();
+  double dm = 0.0;
+  for (int idx = threadIdx.x; idx < n * n; idx += kSST) dm = fmax(dm, fabs(R[idx]));
+  const double delta = block_max(dm, red);
+  if (!(delta < 3e-2)) return false;
+  const int steps = delta < 1e-6 ? 1 : delta < 1e-3 ? 2 : 3;
+  for (int st = 0; st < steps; ++st) {
+    if (st > 0) {
+      gemm_nn(n, n, n, G, n, X, n, R, n, -1.0, true);
+      __syncthreads();
     }
+    gemm_nn(n, n, n, X, n, R, n, P, n, 1.0, false);
     __syncthreads();
-    for (int idx = threadIdx.x; idx < b * b; idx += kSST) s.Tb[idx] *= s.vb[idx / b] * s.vb[idx % b];
+    for (int idx = threadIdx.x; idx < n * n; idx += kSST) X[idx] += P[idx];
     __syncthreads();
   }
-  const bool ok = chol_warp0(s.Tb, b, b, scaled ? 1e-13 * b : 0.0);
-  if (!ok) return false;
-  // rows: y := (y .* scale) L^{-T}   i.e. solve x L^T = y'
-  for (int i = s.rs + threadIdx.x; i < s.re; i += kSST) {
-    double y[BT];
-#pragma unroll
-    for (int j = 0; j < BT; ++j) y[j] = j < b ? Y[(int64_t)i * b + j] * (scaled ? s.vb[j] : 1.0) : 0.0;
-#pragma unroll
-    for (int j = 0; j < BT; ++j) {
-      if (j < b) {
-        double v = y[j];
-#pragma unroll
-        for (int p = 0; p < BT; ++p)
-          if (p < j) v = fma(-s.Tb[j * b + p], y[p], v);
-        y[j] = v / s.Tb[j * b + j];
-      }
+  for (int idx = threadIdx.x; idx < n * n; idx += kSST) {   // symmetrise
+    const int i = idx / n, j = idx - i * n;
+    if (i < j) {
+      const double v = 0.5 * (X[idx] + X[(int64_t)j * n + i]);
+      X[idx] = v;
+      X[(int64_t)j * n + i] = v;
     }
-#pragma unroll
-    for (int j = 0; j < BT; ++j)
-      if (j < b) Y[(int64_t)i * b + j] = y[j];
   }
   __syncthreads();
   return true;
 }
 
-// rows of M := M U  (b x b rotation) on the slice
-template <int BT>
-WLR_DEVI void rotate_rows(SSCtx& s, double* Mx) {
-  const int b = s.a.b;
-  for (int i = s.rs + threadIdx.x; i < s.re; i += kSST) {
-    double y[BT], o[BT];
-#pragma unroll
-    for (int j = 0; j < BT; ++j) { y[j] = j < b ? Mx[(int64_t)i * b + j] : 0.0; o[j] = 0.0; }
-#pragma unroll
-    for (int p = 0; p < BT; ++p)
-#pragma unroll
-      for (int j = 0; j < BT; ++j)
-        if (p < b && j < b) o[j] = fma(y[p], s.Ub[p * b + j], o[j]);
-#pragma unroll
-    for (int j = 0; j < BT; ++j)
-      if (j < b) Mx[(int64_t)i * b + j] = o[j];
+// Cholesky of the small n x n SPD matrix A (smem, ld 32) by warp 0 (lower factor in place);
+// dinv[j] = 1 / L_jj.  Returns (uniformly, after a block barrier) true iff SPD.
+WLR_DEVI bool chol_small(double* A, int n, double* dinv, int* ok_s) {
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    bool ok = true;
+    for (int j = 0; j < n; ++j) {
+      const double d = A[j * 32 + j];
+      ok = ok && (d > 0.0) && isfinite(d);
+      const double r = rsqrt(d > 0.0 ? d : 1.0);
+      __syncwarp();
+      if (lane == 0) { A[j * 32 + j] = d * r; dinv[j] = r; }
+      const int i = j + 1 + lane;
+      double lij = 0.0;
+      if (i < n) { lij = A[i * 32 + j] * r; A[i * 32 + j] = lij; }
+      __syncwarp();
+      if (i < n)
+        for (int l = j + 1; l <= i; ++l) A[i * 32 + l] = fma(-lij, A[l * 32 + j], A[i * 32 + l]);
+      __syncwarp();
+    }
+    if (lane == 0) *ok_s = ok ? 1 : 0;
+  }
+  __syncthreads();
+  return *ok_s != 0;
+}
+
+// Li = L^{-1} (lower triangular, ld 32), column c by lane c of warp 0.
+WLR_DEVI void tri_inverse(const double* L, const double* dinv, int n, double* Li) {
+  if (threadIdx.x < 32) {
+    const int c = threadIdx.x;
+    if (c < n) {
+      for (int i = 0; i < c; ++i) Li[i * 32 + c] = 0.0;
+      Li[c * 32 + c] = dinv[c];
+      for (int i = c + 1; i < n; ++i) {
+        double v = 0.0;
+        for (int m = c; m < i; ++m) v = fma(L[i * 32 + m], Li[m * 32 + c], v);
+        Li[i * 32 + c] = -v * dinv[i];
+      }
+    }
   }
   __syncthreads();
 }
 
-template <int BT>
-__global__ void __launch_bounds__(kSST, 1) small_step_kernel(SmallArgs a, int smem_flags) {
-  extern __shared__ __align__(16) double ss_smem[];
-  __shared__ int bank_s;
-  __shared__ double red_s[kSSW];
-  __shared__ int flag_s;
-  SSCtx s;
-  s.a = a;
-  s.CL = gridDim.x;
-  s.c = blockIdx.x;
-  const int k = a.k, nk = a.nk, b = a.b, t = a.t;
-  const int SL = (int)ceil_div(nk, s.CL);
-  s.rs = std::min(nk, s.c * SL);
-  s.re = std::min(nk, s.rs + SL);
-  s.nloc = s.re - s.rs;
-  double* p = ss_smem;
-  s.GAs = nullptr;
-  s.Yst = nullptr;
-  if (smem_flags & 1) { s.GAs = p; p += (int64_t)SL * nk; }
-  if (smem_flags & 2) { s.Yst = p; p += (int64_t)nk * b; }
-  s.Ls = p; p += k * k;
-  s.Hs = p; p += k * k;
-  s.Wk = p; p += k * b;
-  s.Tb = p; p += b * b;
-  s.Ub = p; p += b * b;
-  s.vb = p; p += 32;
-  s.Xw = p; p += kSSW * k;
-  s.red = red_s;
-  s.bank = &bank_s;
-  if (threadIdx.x == 0) bank_s = 0;
+// Parallel (round-robin) cyclic Jacobi on the symmetric b x b matrix T (ld 32) by warp 0:
+// on exit th = eigenvalues in DESCENDING order and U (ld 32) the matching orthonormal
+// eigenvectors (columns).  b/2 disjoint rotations per round, b-1 rounds per sweep; stops
+// when every off-diagonal is at rounding level.  Deterministic.
+WLR_DEVI void jacobi_par(double* T, double* U, double* th, double* cs, int b) {
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    const int nb = (b + 1) & ~1;
+    const int np = nb / 2;
+    for (int i = lane; i < b; i += 32)
+      for (int j = 0; j < b; ++j) U[i * 32 + j] = (i == j) ? 1.0 : 0.0;
+    double dmax = 0.0;
+    for (int i = 0; i < b; ++i) dmax = fmax(dmax, fabs(T[i * 32 + i]));
+    const double tabs = 2e-15 * dmax;
+    __syncwarp();
+    for (int sweep = 0; sweep < 30 && nb > 1; ++sweep) {
+      for (int rnd = 0; rnd < nb - 1; ++rnd) {
+        // rotation parameters of pair (lane) from the current T
+        if (lane < np) {
+          int p, q;
+          if (lane == 0) { p = rnd; q = nb - 1; }
+          else { p = (rnd + lane) % (nb - 1); q = (rnd - lane + nb - 1) % (nb - 1); }
+          if (p > q) { const int x = p; p = q; q = x; }
+          double c = 1.0, sn = 0.0;
+          if (q < b) {
+            const double apq = T[p * 32 + q], app = T[p * 32 + p], aqq = T[q * 32 + q];
+            if (fabs(apq) > tabs && fabs(apq) > 1e-16 * sqrt(fabs(app * aqq))) {
+              const double tau = (aqq - app) / (2.0 * apq);
+              const double tt = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+              c = rsqrt(1.0 + tt * tt);
+              sn = tt * c;
+            }
+          }
+          cs[4 * lane + 0] = c; cs[4 * lane + 1] = sn;
+          cs[4 * lane + 2] = (double)p; cs[4 * lane + 3] = (double)(q < b && sn != 0.0 ? q : -1);
+        }
+        __syncwarp();
+        // rows:  T <- J^T T
+        for (int idx = lane; idx < np * b; idx += 32) {
+          const int kq = idx / b, j = idx - kq * b;
+          const int q = (int)cs[4 * kq + 3];
+          if (q >= 0) {
+            const int p = (int)cs[4 * kq + 2];
+            const double c = cs[4 * kq], sn = cs[4 * kq + 1];
+            const double tp = T[p * 32 + j], tq = T[q * 32 + j];
+            T[p * 32 + j] = c * tp - sn * tq;
+            T[q * 32 + j] = sn * tp + c * tq;
+          }
+        }
+        __syncwarp();
+        // columns: T <- T J, U <- U J
+        for (int idx = lane; idx < np * b; idx += 32) {
+          const int kq = idx / b, i = idx - kq * b;
+          const int q = (int)cs[4 * kq + 3];
+          if (q >= 0) {
+            const int p = (int)cs[4 * kq + 2];
+            const double c = cs[4 * kq], sn = cs[4 * kq + 1];
+            const double tp = T[i * 32 + p], tq = T[i * 32 + q];
+            T[i * 32 + p] = c * tp - sn * tq;
+            T[i * 32 + q] = sn * tp + c * tq;
+            const double up = U[i * 32 + p], uq = U[i * 32 + q];
+            U[i * 32 + p] = c * up - sn * uq;
+            U[i * 32 + q] = sn * up + c * uq;
+          }
+        }
+        __syncwarp();
+      }
+      // converged when every off-diagonal is at rounding level
+      bool big = false;
+      for (int idx = lane; idx < b * b; idx += 32) {
+        const int i = idx / b, j = idx - i * b;
+        if (i != j) {
+          const double v = fabs(T[i * 32 + j]);
+          big = big || (v > tabs && v > 1e-16 * sqrt(fabs(T[i * 32 + i] * T[j * 32 + j])));
+        }
+      }
+      if (!__any_sync(0xffffffffu, big)) break;
+    }
+    // sort descending (stable by index) and permute U's columns
+    double wj = lane < b ? T[lane * 32 + lane] : 0.0;
+    int rk = 0;
+    for (int i = 0; i < b; ++i) {
+      const double wi = T[i * 32 + i];
+      if (wi > wj || (wi == wj && i < lane)) ++rk;
+    }
+    __syncwarp();
+    if (lane < b) th[rk] = wj;
+    for (int i = lane; i < b; i += 32)                          // T is free now
+      for (int j = 0; j < b; ++j) T[i * 32 + j] = U[i * 32 + j];
+    __syncwarp();
+    if (lane < b)
+      for (int i = 0; i < b; ++i) U[i * 32 + rk] = T[i * 32 + lane];
+  }
+  __syncthreads();
+}
+
+// Z[slice] = S X[slice] = G_A[slice, :] X - M(:, slice)^T W   with W = C X (reduced, k x w).
+// X is distributed: row l lives in CTA l / SL at smem offset xoff (row stride ldx).  It is
+// gathered into Xf (local) when planned, else read through DSMEM.  Split: warp = (ks, js);
+// ks takes a chunk of the nk + k reduction index, js a group of columns; lanes own output
+// rows (i = lane, lane + 32; nl <= 64).  G_A is symmetric, so G_A[rs + i][l] is read as
+// G_A[l][rs + i] (coalesced).  Fixed-order sums.
+template <int PW>
+WLR_DEVI void s_product(SS& s, const SmallArgs& a, int64_t xoff, int ldx, int w,
+                        const double* Wk, const double* Mp, int ldm, double* Z, int ldz) {
+  const SSPlan& p = a.pl;
+  cg::cluster_group cl = cg::this_cluster();
+  double* Red = s.sm + p.oRed;
+  double* Xf = p.oXf >= 0 ? s.sm + p.oXf : nullptr;
+  if (Xf) {
+    for (int idx0 = threadIdx.x; idx0 < s.nk * w; idx0 += 4 * kSST) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int idx = idx0 + u * kSST;
+        v[u] = 0.0;
+        if (idx < s.nk * w) {
+          const int l = idx / w, j = idx - l * w;
+          const int owner = l / s.SL;
+          v[u] = cl.map_shared_rank(s.sm, owner)[xoff + (int64_t)(l - owner * s.SL) * ldx + j];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (idx0 + u * kSST < s.nk * w) Xf[idx0 + u * kSST] = v[u];
+    }
+    __syncthreads();
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ks = warp / p.JS, js = warp - ks * p.JS;
+  const int cw = (w + p.JS - 1) / p.JS;
+  const int j0 = js * cw;
+  const int wj = min(w - j0, cw);                 // columns of this warp (may be <= 0)
+  const int KT = s.nk + s.k;
+  const int kc = (KT + p.KS - 1) / p.KS;
+  const int l0 = ks * kc, l1 = min(KT, l0 + kc);
+  const bool has0 = lane < s.nl, has1 = lane + 32 < s.nl;
+  double acc0[PW], acc1[PW];
+#pragma unroll
+  for (int j = 0; j < PW; ++j) { acc0[j] = 0.0; acc1[j] = 0.0; }
+  if (wj > 0) {
+    const double* gcol = a.GA + s.rs;
+    const int lg = min(l1, s.nk);
+    constexpr int U = 8;                          // G_A loads in flight per lane
+    for (int lb = l0; lb < lg; lb += U) {
+      double g0[U], g1[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int l = lb + u;
+        const double* grow = gcol + (int64_t)l * s.nk;
+        g0[u] = (l < lg && has0) ? __ldg(grow + lane) : 0.0;
+        g1[u] = (l < lg && has1) ? __ldg(grow + lane + 32) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int l = lb + u;
+        if (l < lg) {
+          const double* xr;
+          if (Xf) {
+            xr = Xf + (int64_t)l * w + j0;
+          } else {
+            const int owner = l / s.SL;
+            xr = cl.map_shared_rank(s.sm, owner) + xoff + (int64_t)(l - owner * s.SL) * ldx + j0;
+          }
+#pragma unroll
+          for (int j = 0; j < PW; ++j) {
+            if (j < wj) {
+              const double x = xr[j];
+              acc0[j] = fma(g0[u], x, acc0[j]);
+              acc1[j] = fma(g1[u], x, acc1[j]);
+            }
+          }
+        }
+      }
+    }
+    for (int l = max(l0, s.nk); l < l1; ++l) {
+      const int q = l - s.nk;
+      const double m0 = has0 ? Mp[(int64_t)q * ldm + lane] : 0.0;
+      const double m1 = has1 ? Mp[(int64_t)q * ldm + lane + 32] : 0.0;
+#pragma unroll
+      for (int j = 0; j < PW; ++j) {
+        if (j < wj) {
+          const double x = Wk[q * w + j0 + j];
+          acc0[j] = fma(-m0, x, acc0[j]);
+          acc1[j] = fma(-m1, x, acc1[j]);
+        }
+      }
+    }
+  }
+  if (l0 < l1) {
+#pragma unroll
+    for (int j = 0; j < PW; ++j) {
+      if (j < wj) {
+        if (has0) Red[((int64_t)ks * s.SL + lane) * w + j0 + j] = acc0[j];
+        if (has1) Red[((int64_t)ks * s.SL + lane + 32) * w + j0 + j] = acc1[j];
+      }
+    }
+  }
+  __syncthreads();
+  const int nks = (KT + kc - 1) / kc;             // chunks that exist (ks >= nks are empty)
+  for (int idx = threadIdx.x; idx < s.nl * w; idx += kSST) {
+    const int i = idx / w, j = idx - i * w;
+    double v = 0.0;
+    for (int q = 0; q < nks; ++q) v += Red[((int64_t)q * s.SL + i) * w + j];
+    Z[i * ldz + j] = v;
+  }
+  __syncthreads();
+}
 
-  // ------------------------------------------------ stage G_A rows of the slice
-  if (s.GAs)
-    for (int64_t idx = threadIdx.x; idx < (int64_t)s.nloc * nk; idx += kSST)
-      s.GAs[idx] = a.GA[(int64_t)s.rs * nk + idx];
+// One S-product of the basis X (local slice at offset xoff, width w = row stride):
+// exchange of the C' X partials, then the distributed product into Z (local offset).
+template <int PW>
+WLR_DEVI void s_apply(SS& s, const SmallArgs& a, const double* Cs, int ldc, const double* Ms,
+                      int ldm, int64_t xoff, int w, int64_t zoff, int* nprod) {
+  const SSPlan& p = a.pl;
+  const double* X = s.sm + xoff;
+  double* part = xpart(s, p);
+  const TN d[1] = {{Cs, ldc, 1, X, 1, w, s.k, w, part}};
+  slice_tn<1>(s.nl, d);
+  double* Wk = s.sm + p.oWk;
+  xreduce(s, p, s.k * w, Wk);
+  s_product<PW>(s, a, xoff, w, w, Wk, Ms, ldm, s.sm + zoff, w);
+  ++*nprod;
+}
 
-  // ------------------------------------------------ A: Gram update, Cholesky, C
+template <int BT>
+__global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_constant__ SmallArgs a) {
+  constexpr int PW = BT <= 8 ? BT : (BT <= 16 ? (BT + 1) / 2 : (BT + 3) / 4);
+  extern __shared__ __align__(16) double ss_smem[];
+  __shared__ double red[8 * kSSW];
+  __shared__ int ok_s;
+  const SSPlan& p = a.pl;
+  SS s;
+  s.CL = p.CL;
+  s.c = (int)cg::this_cluster().block_rank();
+  s.SL = p.SL;
+  s.k = a.k; s.nk = a.nk; s.b = a.b; s.t = a.t;
+  s.rs = min(a.nk, s.c * s.SL);
+  s.nl = min(a.nk, s.rs + s.SL) - s.rs;
+  s.sm = ss_smem;
+  s.bank = 0;
+  s.nt = 0;
+  tmark(s, a);
+  const int k = a.k, nk = a.nk, b = a.b, t = a.t, kt = k * t, kk = k * k;
+  const SmallOff so(b, t, k);
+  double* sm = s.sm + p.oSmall;
+  const int64_t SLb = (int64_t)s.SL * b;
+  const int64_t buf[4] = {p.oBuf, p.oBuf + SLb, p.oBuf + 2 * SLb, p.oBuf + 3 * SLb};
+  int iY = 0, iZ = 1, iA = 2, iB = 3;          // roles of the four slice buffers
+  double* Vp = s.sm + p.oVp;                   // nl x t   V_p (previous V)
+  double* Es = s.sm + p.oE;                    // nl x t   E = V' - V_p R
+  double* SEs = s.sm + p.oSE;                  // nl x t   S_p E
+  // C', M', C_in slice accessors: smem (ld SL) or global (ld nk, offset rs)
+  double* Cs = p.oCs >= 0 ? s.sm + p.oCs : a.C_out + s.rs;
+  const int ldc = p.oCs >= 0 ? s.SL : nk;
+  double* Ms = p.oMs >= 0 ? s.sm + p.oMs : a.M_out + s.rs;
+  const int ldm = p.oMs >= 0 ? s.SL : nk;
+  const double* Cin = p.oCin >= 0 ? s.sm + p.oCin : a.C_in + s.rs;
+  const int ldci = p.oCin >= 0 ? s.SL : nk;
   const double* incN = a.inc;
   const double* incGam = a.inc + (int64_t)k * nk;
-  const double* incOm = incGam + (int64_t)k * k;
-  const double fw = a.mode ? incOm[(int64_t)k * k] : a.inc[0];
-  for (int idx = threadIdx.x; idx < k * k; idx += kSST) {
-    const int i = idx / k, j = idx % k;
-    if (a.mode) {
-      const double g = a.G_in[idx];
-      const double om = 0.5 * (incOm[i * k + j] + incOm[j * k + i]);
-      s.Ls[idx] = g + incGam[i * k + j] + incGam[j * k + i] + om;
-      s.Hs[idx] = g + incGam[i * k + j];
-    } else {
-      s.Ls[idx] = a.G_out[idx];
-      s.Hs[idx] = 0.0;
-    }
-  }
-  if (a.mode) {
-    for (int64_t idx = threadIdx.x; idx < (int64_t)k * s.nloc; idx += kSST) {
-      const int l = (int)(idx / s.nloc), c = s.rs + (int)(idx % s.nloc);
-      a.M_out[(int64_t)l * nk + c] = a.M_in[(int64_t)l * nk + c] + incN[(int64_t)l * nk + c];
-    }
-  }
-  __syncthreads();
-  double trG = 0.0;
-  for (int i = 0; i < k; ++i) trG += s.Ls[i * k + i];
-  if (s.c == 0 && a.mode)
-    for (int idx = threadIdx.x; idx < k * k; idx += kSST) a.G_out[idx] = s.Ls[idx];
-  __syncthreads();
-  if (!chol_warp0(s.Ls, k, k, 0.0, 256.0 * 2.220446049250313e-16)) {   // rank(X1) < k (R6)
-    if (s.c == 0 && threadIdx.x == 0) raise_flag(a.flags, DF_RANK);
-    return;                                  // every CTA takes this branch identically
-  }
-  // C'[:, c] = G'^{-1} M'[:, c] for the slice columns (warp per column)
-  for (int cl = warp; cl < s.nloc; cl += kSSW) {
-    const int c = s.rs + cl;
-    double* xw = s.Xw + warp * k;
-    for (int l = lane; l < k; l += 32) xw[l] = a.M_out[(int64_t)l * nk + c];
-    __syncwarp();
-    chol_solve_warp(s.Ls, k, k, xw, 1, lane);
-    for (int l = lane; l < k; l += 32) a.C_out[(int64_t)l * nk + c] = xw[l];
-    __syncwarp();
-  }
-  __syncthreads();
-  cl_sync();                                  // C', M' complete on every slice
+  const double* incOm = incGam + (int64_t)kk;
+  const double fw = a.mode ? incOm[(int64_t)kk] : a.inc[0];
+  // Newton-Schulz mats (G', X = inverse, R, P): smem or this CTA's global workspace
+  double* Gq = p.oGsq >= 0 ? s.sm + p.oGsq : a.gws + (int64_t)s.c * p.gws_stride;
+  double* Xq = Gq + kk;
+  double* Rq = Xq + kk;
+  double* Pq = Rq + kk;
+  int nprod = 0;
 
-  // ------------------------------------------------ B: eigenpairs of S (ChFSI + RR)
-  const double floor_abs = 8.0 * 2.220446049250313e-16 * a.a2sq;
-  double* Yb[3] = {a.Y, a.Y1, a.Y2};
-  int outer = 0;
-  const int max_outer = a.max_outer;
-  bool converged = false, failed = false;
-  while (true) {
-    // Rayleigh-Ritz on span(Y)
-    if (!cholqr_pass<BT>(s, a.Y, true) || !cholqr_pass<BT>(s, a.Y, false)) { failed = true; break; }
-    s_product<BT>(s, a.Y, a.Z);
-    {
-      double* my = slot(s, s.c);
-      for (int idx = threadIdx.x; idx < b * b; idx += kSST) {
-        const int pp = idx / b, q = idx % b;
-        double v = 0.0;
-        for (int i = s.rs; i < s.re; ++i) v = fma(a.Y[(int64_t)i * b + pp], a.Z[(int64_t)i * b + q], v);
-        my[idx] = v;
-      }
-      xchg_reduce(s, b * b, s.Tb);
-      for (int idx = threadIdx.x; idx < b * b; idx += kSST) {
-        const int pp = idx / b, q = idx % b;
-        if (pp < q) {
-          const double v = 0.5 * (s.Tb[pp * b + q] + s.Tb[q * b + pp]);
-          s.Tb[pp * b + q] = v;
-          s.Tb[q * b + pp] = v;
-        }
-      }
-      __syncthreads();
-      jacobi_warp0(s.Tb, s.Ub, s.vb, b);
+  // ------------------------------------------------ A: Gram update, G'^{-1}, C', slices
+  // stage G_p, Gamma, Omega, C_p V_p (used again by the final phase) when planned
+  const bool ms3 = p.oMat3 >= 0 && a.mode;
+  double* mats = s.sm + (p.oMat3 >= 0 ? p.oMat3 : 0);
+  if (ms3) {
+    for (int idx = threadIdx.x; idx < kk; idx += kSST) {
+      mats[idx] = a.G_in[idx];
+      mats[kk + idx] = incGam[idx];
+      mats[2 * kk + idx] = incOm[idx];
     }
-    rotate_rows<BT>(s, a.Y);
-    rotate_rows<BT>(s, a.Z);
-    {   // residual norms of the wanted pairs
-      double* my = slot(s, s.c);
-      for (int j = threadIdx.x; j < b; j += kSST) {
-        double v = 0.0;
-        for (int i = s.rs; i < s.re; ++i) {
-          const double r = a.Z[(int64_t)i * b + j] - s.vb[j] * a.Y[(int64_t)i * b + j];
-          v = fma(r, r, v);
-        }
-        my[j] = v;
-      }
-      xchg_reduce(s, b, s.Tb);    // Tb[j] = ||S y_j - theta_j y_j||^2
-    }
-    double rmax = 0.0;
-    for (int j = 0; j < t; ++j) rmax = fmax(rmax, sqrt(fmax(s.Tb[j], 0.0)));
-    const double theta0 = s.vb[0];
-    if (rmax <= a.tol * fabs(theta0) + floor_abs) { converged = true; break; }
-    if (++outer > max_outer) break;
-    // Chebyshev filter of degree d damping [0, theta_{b-1}]
-    const double beta = s.vb[b - 1];
-    int d = a.max_deg;
-    double cc = 0.5 * beta, ee = 0.5 * beta;
-    if (!(beta > 1e-300 * fabs(theta0)) || beta >= theta0) {
-      cc = 0.0; ee = 1.0; d = 1;                // plain power step
+    for (int idx = threadIdx.x; idx < kt; idx += kSST) mats[3 * kk + idx] = a.CVprev[idx];
+  }
+  const double* Gm = ms3 ? mats : a.G_in;
+  const double* Gam = ms3 ? mats + kk : incGam;
+  const double* Om = ms3 ? mats + 2 * kk : incOm;
+  const double* CVp = ms3 ? mats + 3 * kk : a.CVprev;
+  for (int idx = threadIdx.x; idx < k * s.nl; idx += kSST) {
+    const int q = idx / s.nl, i = idx - q * s.nl;
+    const int64_t gi = (int64_t)q * nk + s.rs + i;
+    const double mv = a.mode ? a.M_in[gi] + incN[gi] : a.M_out[gi];
+    if (p.oMs >= 0) Ms[q * ldm + i] = mv;
+    if (a.mode) a.M_out[gi] = mv;
+    if (p.oCin >= 0 && a.mode) s.sm[p.oCin + q * s.SL + i] = a.C_in[gi];
+  }
+  for (int idx = threadIdx.x; idx < s.nl * b; idx += kSST) s.sm[buf[iY] + idx] = a.Y[(int64_t)s.rs * b + idx];
+  if (a.mode) {
+    for (int idx = threadIdx.x; idx < s.nl * t; idx += kSST) Vp[idx] = a.Vprev[(int64_t)s.rs * t + idx];
+    for (int idx = threadIdx.x; idx < kk; idx += kSST) Xq[idx] = a.Gi_in[idx];
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < kk; idx += kSST) {
+    const int i = idx / k, j = idx - i * k;
+    double g;
+    if (a.mode) {
+      g = Gm[idx] + Gam[i * k + j] + Gam[j * k + i] + 0.5 * (Om[i * k + j] + Om[j * k + i]);
+      if (s.c == 0) a.G_out[idx] = g;
     } else {
-      const double x0 = (theta0 - cc) / ee, xt = (s.vb[t - 1] - cc) / ee;
-      const double gap = acosh(fmax(x0, 1.0)) - acosh(fmax(xt, 1.0));
-      if (gap > 0.0) d = std::max(1, std::min(d, (int)(11.5 / gap)));   // amplification <= 1e5
+      g = a.G_out[idx];
     }
-    // Y1 = (Z - c Y)/e
-    double* Yp = Yb[0];
-    double* Yc = Yb[1];
-    double* Yn = Yb[2];
-    for (int64_t idx = (int64_t)s.rs * b + threadIdx.x; idx < (int64_t)s.re * b; idx += kSST)
-      Yc[idx] = (a.Z[idx] - cc * Yp[idx]) / ee;
+    Gq[idx] = g;
+  }
+  __syncthreads();
+  bool okinv = a.mode ? ns_inverse(Gq, Xq, Rq, Pq, k, red) : false;
+  if (!okinv) {
+    for (int idx = threadIdx.x; idx < kk; idx += kSST) Xq[idx] = Gq[idx];
     __syncthreads();
+    if (!sweep_inverse(Xq, k, 256.0 * kEps, sm + so.d0, sm + so.rb)) {   // rank(X1) < k (R6)
+      if (s.c == 0 && threadIdx.x == 0) raise_flag(a.flags, DF_RANK);
+      return;                                  // uniform on every CTA; no barrier issued yet
+    }
+  }
+  if (s.c == 0)
+    for (int idx = threadIdx.x; idx < kk; idx += kSST) a.Gi_out[idx] = Xq[idx];
+  tmark(s, a);                                 // [1] Gram update + G'^{-1}
+  // C'[:, slice] = G'^{-1} M'[:, slice]
+  gemm_nn(k, s.nl, k, Xq, k, Ms, ldm, Cs, ldc, 1.0, false);
+  __syncthreads();
+  if (p.oCs >= 0)
+    for (int idx = threadIdx.x; idx < k * s.nl; idx += kSST) {
+      const int q = idx / s.nl, i = idx - q * s.nl;
+      a.C_out[(int64_t)q * nk + s.rs + i] = Cs[q * ldc + i];
+    }
+  tmark(s, a);                                 // [2] C'
+
+  // ------------------------------------------------ B: eigenpairs of S
+  const double floor_abs = 4.0 * kEps * sqrt((double)nk) * a.a2sq;   // S-product rounding floor
+  bool converged = false, failed = false;
+  int outer = 0;
+  double rmax = 0.0;
+  double* Gx = sm + so.Gx;
+  double* th = sm + so.th;
+  double* Rt = sm + so.Rt;
+  double* dsc = sm + so.dsc;
+  double* rres = s.sm + p.oCinE;               // [res (t) | C_in E (k x t)]
+  bool ortho = !a.cold;                        // Y expected orthonormal (warm Ritz block)
+  while (true) {
+    // ---- Rayleigh-Ritz on span(Y):  Z = S Y;  Gyy = Y^T Y, Gyz = Y^T Z (generalised RR)
+    s_apply<PW>(s, a, Cs, ldc, Ms, ldm, buf[iY], b, buf[iZ], &nprod);
+    tmark(s, a);                               // product
+    {
+      const double* Y = s.sm + buf[iY];
+      const double* Z = s.sm + buf[iZ];
+      double* part = xpart(s, p);
+      const int tb = a.mode ? t : 0;
+      const TN d[4] = {{Y, 1, b, Y, 1, b, b, b, part},
+                       {Y, 1, b, Z, 1, b, b, b, part + b * b},
+                       {Vp, 1, t, Y, 1, b, tb, b, part + 2 * b * b},
+                       {Vp, 1, t, Z, 1, b, tb, b, part + 2 * b * b + t * b}};
+      slice_tn<4>(s.nl, d);
+      xreduce(s, p, 2 * b * b + 2 * tb * b, Gx);
+    }
+    tmark(s, a);                               // Gram exchange
+    // ---- local (every CTA identically): D = diag(Gyy)^-1/2; if D Gyy D = I to rounding
+    //      the block is orthonormal: T = D Gyz D, Q = D U.  Otherwise L L^T = D Gyy D,
+    //      T = L^-1 (D Gyz D) L^-T, Q = D L^-T U.
+    bool gen;
+    {
+      double* Lb = sm + so.Lb;
+      double* Li = sm + so.Li;
+      double* Tb = sm + so.Tb;
+      double* Ub = sm + so.Ub;
+      double* Qb = sm + so.Qb;
+      double* Wb = sm + so.Wb;
+      if (threadIdx.x < b) {
+        const double d = Gx[threadIdx.x * b + threadIdx.x];
+        dsc[threadIdx.x] = d > 0.0 ? rsqrt(d) : 1.0;
+      }
+      __syncthreads();
+      double dev = 0.0;
+      for (int idx = threadIdx.x; idx < b * b; idx += kSST) {
+        const int i = idx / b, j = idx - i * b;
+        const double di = dsc[i] * dsc[j];
+        const double g = 0.5 * (Gx[i * b + j] + Gx[j * b + i]) * di;
+        Lb[i * 32 + j] = g;
+        Wb[i * 32 + j] = 0.5 * (Gx[b * b + i * b + j] + Gx[b * b + j * b + i]) * di;
+        if (i != j) dev = fmax(dev, fabs(g));
+      }
+      dev = block_max(dev, red);
+      gen = !(ortho && dev < 1e-13);
+      if (gen) {
+        if (!chol_small(Lb, b, sm + so.rb, &ok_s)) { failed = true; break; }
+        tri_inverse(Lb, sm + so.rb, b, Li);
+        // Tb = Li Wb Li^T   (two small products; Ub as scratch)
+        for (int idx = threadIdx.x; idx < b * b; idx += kSST) {
+          const int i = idx / b, j = idx - i * b;
+          double v = 0.0;
+          for (int q = 0; q <= i; ++q) v = fma(Li[i * 32 + q], Wb[q * 32 + j], v);
+          Ub[i * 32 + j] = v;
+        }
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < b * b; idx += kSST) {
+          const int i = idx / b, j = idx - i * b;
+          double v = 0.0;
+          for (int q = 0; q <= j; ++q) v = fma(Ub[i * 32 + q], Li[j * 32 + q], v);
+          Tb[i * 32 + j] = v;
+        }
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < b * b; idx += kSST) {
+          const int i = idx / b, j = idx - i * b;
+          if (i < j) {
+            const double v = 0.5 * (Tb[i * 32 + j] + Tb[j * 32 + i]);
+            Tb[i * 32 + j] = v;
+            Tb[j * 32 + i] = v;
+          }
+        }
+      } else {
+        for (int idx = threadIdx.x; idx < b * b; idx += kSST) {
+          const int i = idx / b, j = idx - i * b;
+          Tb[i * 32 + j] = Wb[i * 32 + j];
+        }
+      }
+      __syncthreads();
+      jacobi_par(Tb, Ub, th, sm + so.cs, b);
+      // Qb = D (Li^T U)  or  D U
+      for (int idx = threadIdx.x; idx < b * b; idx += kSST) {
+        const int i = idx / b, j = idx - i * b;
+        double v;
+        if (gen) {
+          v = 0.0;
+          for (int q = i; q < b; ++q) v = fma(Li[q * 32 + i], Ub[q * 32 + j], v);
+        } else {
+          v = Ub[i * 32 + j];
+        }
+        Qb[i * b + j] = v * dsc[i];
+      }
+      __syncthreads();
+    }
+    tmark(s, a);                               // local RR
+    const double* Qb = sm + so.Qb;
+    // ---- rotate: Y' = Y Q, Z' = Z Q  (into the free buffers)
+    gemm_nn(s.nl, b, b, s.sm + buf[iY], b, Qb, b, s.sm + buf[iA], b, 1.0, false);
+    gemm_nn(s.nl, b, b, s.sm + buf[iZ], b, Qb, b, s.sm + buf[iB], b, 1.0, false);
+    {
+      const int oy = iY, oz = iZ;
+      iY = iA; iZ = iB; iA = oy; iB = oz;
+    }
+    if (a.mode)   // R = Vp^T V' = (Vp^T Y) Q[:, :t]
+      gemm_nn(t, t, b, Gx + 2 * b * b, b, Qb, b, Rt, t, 1.0, false);
+    __syncthreads();
+    // ---- residuals of the wanted pairs; E = V' - Vp R and its C_in E partial (final phase)
+    {
+      const double* Y = s.sm + buf[iY];
+      const double* Z = s.sm + buf[iZ];
+      double* part = xpart(s, p);
+      if (a.mode) {
+        for (int idx = threadIdx.x; idx < s.nl * t; idx += kSST) {
+          const int r = idx / t, j = idx - r * t;
+          double v = Y[r * b + j];
+          for (int q = 0; q < t; ++q) v = fma(-Vp[r * t + q], Rt[q * t + j], v);
+          Es[idx] = v;
+        }
+        __syncthreads();
+      }
+      for (int j = threadIdx.x; j < t; j += kSST) {
+        double v = 0.0;
+        for (int r = 0; r < s.nl; ++r) {
+          const double d = Z[r * b + j] - th[j] * Y[r * b + j];
+          v = fma(d, d, v);
+        }
+        part[j] = v;
+      }
+      if (a.mode) {
+        const TN d[1] = {{Cin, ldci, 1, Es, 1, t, k, t, part + t}};
+        slice_tn<1>(s.nl, d);
+      }
+      xreduce(s, p, t + (a.mode ? kt : 0), rres);
+    }
+    tmark(s, a);                               // residual exchange
+    rmax = 0.0;
+    for (int j = 0; j < t; ++j) rmax = fmax(rmax, sqrt(fmax(rres[j], 0.0)));
+    const double theta0 = th[0];
+    const double target = fmax(a.tol * fabs(theta0), floor_abs);
+    if (rmax <= target) { converged = true; break; }
+    if (++outer > a.max_outer) break;
+    // ---- Chebyshev filter of adaptive degree damping [0, theta_{b-1}]
+    const double beta = th[b - 1];
+    double cc = 0.5 * beta, ee = 0.5 * beta;
+    int d = 1;
+    if (!(beta > 1e-300 * fabs(theta0)) || beta >= th[t - 1]) {
+      cc = 0.0; ee = 1.0; d = 1;                // no gap inside the block: plain power step
+    } else {
+      const double x0 = (theta0 - cc) / ee, xt = (th[t - 1] - cc) / ee;
+      const double at = acosh(fmax(xt, 1.0)), a0 = acosh(fmax(x0, 1.0));
+      const double need = log(fmax(rmax / target, 1.0)) / fmax(at, 1e-6);
+      d = (int)ceil(need) + 1;
+      const int dcap = max(1, (int)(9.9 / fmax(a0, 1e-6)));   // amplification <= ~1e4
+      d = max(1, min(d, min(a.max_deg, dcap)));
+    }
+    const double einv = 1.0 / ee;
+    int i0 = iY, i1 = iA, iz = iZ, i3 = iB;     // P0 = Y, P1 = (Z - c Y)/e, scratch z, free
+    {
+      double* P1 = s.sm + buf[i1];
+      const double* Y = s.sm + buf[i0];
+      const double* Z = s.sm + buf[iz];
+      for (int idx = threadIdx.x; idx < s.nl * b; idx += kSST) P1[idx] = (Z[idx] - cc * Y[idx]) * einv;
+      __syncthreads();
+    }
     for (int j = 2; j <= d; ++j) {
-      s_product<BT>(s, Yc, a.Z);
-      for (int64_t idx = (int64_t)s.rs * b + threadIdx.x; idx < (int64_t)s.re * b; idx += kSST)
-        Yn[idx] = 2.0 * (a.Z[idx] - cc * Yc[idx]) / ee - Yp[idx];
+      s_apply<PW>(s, a, Cs, ldc, Ms, ldm, buf[i1], b, buf[iz], &nprod);
+      double* pn = s.sm + buf[i0];             // P2 = 2 (S P1 - c P1)/e - P0, in place of P0
+      const double* pz = s.sm + buf[iz];
+      const double* p1 = s.sm + buf[i1];
+      for (int idx = threadIdx.x; idx < s.nl * b; idx += kSST)
+        pn[idx] = 2.0 * (pz[idx] - cc * p1[idx]) * einv - pn[idx];
       __syncthreads();
-      double* tmp = Yp; Yp = Yc; Yc = Yn; Yn = tmp;
+      const int tmp = i0; i0 = i1; i1 = tmp;
     }
-    if (Yc != a.Y) {
-      for (int64_t idx = (int64_t)s.rs * b + threadIdx.x; idx < (int64_t)s.re * b; idx += kSST)
-        a.Y[idx] = Yc[idx];
-      __syncthreads();
-    }
+    iY = i1; iZ = iz; iA = i0; iB = i3;
+    ortho = false;                             // filtered block: generalised Rayleigh-Ritz
   }
-  if (failed || !converged) {
-    if (s.c == 0 && threadIdx.x == 0) raise_flag(a.flags, DF_EIG);
+  if ((failed || !converged) && s.c == 0 && threadIdx.x == 0) raise_flag(a.flags, DF_EIG);
+  if (failed) {            // every CTA took the same decision; keep peers' smem alive
+    cg::this_cluster().sync();
+    return;
   }
-  if (failed) return;
 
   // ------------------------------------------------ C: objective, step norm, operands
-  // Step norm: ||X_{p+1}-X_p||^2 = tr(Omega) + ||X2'-X2||^2.  Two
-  // evaluations: the exact Gram identity (accurate while the relative step is >= 1e-4)
-  // and, below that, the first-order expansion ||T1||^2 + ||T2||^2 + 2<T1,T2> with
-  //   T1 = (X1'C' - X1 C)(I - Q'),  T2 = P^perp A2 (Q' - Q),  Q = V V^T,
-  //   V' = V R + E (R = V^T V', E orthogonal to V): every term is a product of O(step)
-  //   factors, so no second-order cancellation.
-  const int kt = k * t;
-  double* Rt = s.Tb;                               // R = V^T V' (t x t), all CTAs
-  if (a.mode) {
-    double* my = slot(s, s.c);
-    for (int idx = threadIdx.x; idx < t * t; idx += kSST) {
-      const int i = idx / t, j = idx % t;
-      double v = 0.0;
-      for (int c = s.rs; c < s.re; ++c) v = fma(a.Vprev[(int64_t)c * t + i], a.Y[(int64_t)c * b + j], v);
-      my[idx] = v;
-    }
-    xchg_reduce(s, t * t, Rt);
-    // E = V' - V R into Y1 (first t columns, stride b; other columns zero)
-    for (int64_t idx = threadIdx.x; idx < (int64_t)s.nloc * b; idx += kSST) {
-      const int c = s.rs + (int)(idx / b), j = (int)(idx % b);
-      double v = 0.0;
-      if (j < t) {
-        v = a.Y[(int64_t)c * b + j];
-        for (int q = 0; q < t; ++q) v = fma(-a.Vprev[(int64_t)c * t + q], Rt[q * t + j], v);
-      }
-      a.Y1[(int64_t)c * b + j] = v;
-    }
-    __syncthreads();
-    s_product<BT>(s, a.Y1, a.Y2, a.M_in, a.C_in);   // S_p E  (old S)
-  }
-  // partial layout of the final round:
-  //   [0] <M',C'> [1] <C',H C> [2] <C',Om C'> [3] <C',Gam dC> [4] <dC, G dC>
-  //   | CnV | CnVn | CVn | MnV | MVn | NV | CE  (k x t each)
-  //   | VnV | ZnV | EE | ESE (t x t each) | C'C'^T (k x k)
-  const int oCnV = 5, oCnVn = oCnV + kt, oCVn = oCnVn + kt, oMnV = oCVn + kt, oMVn = oMnV + kt;
-  const int oNV = oMVn + kt, oCE = oNV + kt;
-  const int oVnV = oCE + kt, oZnV = oVnV + t * t, oEE = oZnV + t * t, oESE = oEE + t * t;
-  const int oCC = oESE + t * t, flen = oCC + k * k;
+  const double* Y = s.sm + buf[iY];            // V' = Y[:, :t]
+  const double* CinE = rres + t;               // reduced C_in E (k x t)
+  if (a.mode)   // S_p E = G_A E - M_in^T (C_in E)   (old S; E distributed at offset oE, stride t)
+    s_product<PW>(s, a, p.oE, t, t, CinE, a.M_in + s.rs, nk, SEs, t);
+  tmark(s, a);                                 // old-S product
+  const FinOff fo(k, t);
+  double* my = a.xchg + (int64_t)s.c * p.flen;
   {
-    double* my = slot(s, s.c);
-    double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0, v4 = 0.0;
-    for (int64_t idx = threadIdx.x; idx < (int64_t)k * s.nloc; idx += kSST) {
-      const int l = (int)(idx / s.nloc), c = s.rs + (int)(idx % s.nloc);
-      const double cn = a.C_out[(int64_t)l * nk + c];
-      v0 = fma(a.M_out[(int64_t)l * nk + c], cn, v0);
+    // [0] <M',C'> [1] <C', H C_in> [2] <C', Om C'> [3] <C', Gam dC> [4] <dC, G dC>
+    double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int idx = threadIdx.x; idx < k * s.nl; idx += kSST) {
+      const int l = idx / s.nl, i = idx - l * s.nl;
+      const double cn = Cs[(int64_t)l * ldc + i];
+      v[0] = fma(Ms[(int64_t)l * ldm + i], cn, v[0]);
       if (a.mode) {
         double hc = 0.0, omc = 0.0, gdc = 0.0, ggdc = 0.0;
         for (int q = 0; q < k; ++q) {
-          const double co = a.C_in[(int64_t)q * nk + c], cq = a.C_out[(int64_t)q * nk + c];
+          const double co = Cin[(int64_t)q * ldci + i], cq = Cs[(int64_t)q * ldc + i];
           const double dq = cq - co;
-          hc = fma(s.Hs[l * k + q], co, hc);
-          omc = fma(0.5 * (incOm[l * k + q] + incOm[q * k + l]), cq, omc);
-          gdc = fma(incGam[l * k + q], dq, gdc);
-          ggdc = fma(a.G_in[l * k + q], dq, ggdc);
+          const double gam = Gam[l * k + q], gm = Gm[l * k + q];
+          hc = fma(gm + gam, co, hc);
+          omc = fma(0.5 * (Om[l * k + q] + Om[q * k + l]), cq, omc);
+          gdc = fma(gam, dq, gdc);
+          ggdc = fma(gm, dq, ggdc);
         }
-        const double dl = cn - a.C_in[(int64_t)l * nk + c];
-        v1 = fma(cn, hc, v1);
-        v2 = fma(cn, omc, v2);
-        v3 = fma(cn, gdc, v3);
-        v4 = fma(dl, ggdc, v4);
+        const double dl = cn - Cin[(int64_t)l * ldci + i];
+        v[1] = fma(cn, hc, v[1]);
+        v[2] = fma(cn, omc, v[2]);
+        v[3] = fma(cn, gdc, v[3]);
+        v[4] = fma(dl, ggdc, v[4]);
       }
     }
-    v0 = block_sum(v0, s.red);
-    v1 = block_sum(v1, s.red);
-    v2 = block_sum(v2, s.red);
-    v3 = block_sum(v3, s.red);
-    v4 = block_sum(v4, s.red);
-    if (threadIdx.x == 0) { my[0] = v0; my[1] = v1; my[2] = v2; my[3] = v3; my[4] = v4; }
-    for (int idx = threadIdx.x; idx < kt; idx += kSST) {
-      const int l = idx / t, j = idx % t;
-      double cnv = 0.0, cnvn = 0.0, cvn = 0.0, mnv = 0.0, mvn = 0.0, nv = 0.0, ce = 0.0;
-      for (int c = s.rs; c < s.re; ++c) {
-        const double cn = a.C_out[(int64_t)l * nk + c], mn = a.M_out[(int64_t)l * nk + c];
-        const double vn = a.Y[(int64_t)c * b + j];
-        cnvn = fma(cn, vn, cnvn);
-        if (a.mode) {
-          const double vp = a.Vprev[(int64_t)c * t + j];
-          cnv = fma(cn, vp, cnv);
-          cvn = fma(a.C_in[(int64_t)l * nk + c], vn, cvn);
-          mnv = fma(mn, vp, mnv);
-          mvn = fma(a.M_in[(int64_t)l * nk + c], vn, mvn);
-          nv = fma(incN[(int64_t)l * nk + c], vp, nv);
-          ce = fma(cn, a.Y1[(int64_t)c * b + j], ce);
-        }
-      }
-      my[oCnV + idx] = cnv; my[oCnVn + idx] = cnvn; my[oCVn + idx] = cvn;
-      my[oMnV + idx] = mnv; my[oMVn + idx] = mvn; my[oNV + idx] = nv; my[oCE + idx] = ce;
-    }
-    for (int idx = threadIdx.x; idx < t * t; idx += kSST) {
-      const int i = idx / t, j = idx % t;
-      double vv = 0.0, zv = 0.0, ee = 0.0, ese = 0.0;
-      if (a.mode)
-        for (int c = s.rs; c < s.re; ++c) {
-          const double vp = a.Vprev[(int64_t)c * t + j];
-          vv = fma(a.Y[(int64_t)c * b + i], vp, vv);
-          zv = fma(a.Z[(int64_t)c * b + i], vp, zv);
-          const double ei = a.Y1[(int64_t)c * b + i];
-          ee = fma(ei, a.Y1[(int64_t)c * b + j], ee);
-          ese = fma(ei, a.Y2[(int64_t)c * b + j], ese);
-        }
-      my[oVnV + idx] = vv; my[oZnV + idx] = zv; my[oEE + idx] = ee; my[oESE + idx] = ese;
-    }
-    for (int idx = threadIdx.x; idx < k * k; idx += kSST) {
-      const int i = idx / k, j = idx % k;
-      double v = 0.0;
-      for (int c = s.rs; c < s.re; ++c) v = fma(a.C_out[(int64_t)i * nk + c], a.C_out[(int64_t)j * nk + c], v);
-      my[oCC + idx] = v;
-    }
-    __syncthreads();
-    // slice-local outputs: Wt rows, Vprev <- Vn (own slice only; read above by this CTA only)
+    block_sum_n<5>(v, red);
+    if (threadIdx.x == 0)
+      for (int u = 0; u < 5; ++u) my[u] = v[u];
+  }
+  {
+    // k x t, t x t and k x k slice contractions in one pass (zero rows when mode == 0)
+    const int km = a.mode ? k : 0, tm = a.mode ? t : 0;
+    const TN d[10] = {{Cs, ldc, 1, Vp, 1, t, km, t, my + fo.CnV},
+                      {Cs, ldc, 1, Y, 1, b, k, t, my + fo.CnVn},
+                      {Cin, ldci, 1, Y, 1, b, km, t, my + fo.CVn},
+                      {Ms, ldm, 1, Vp, 1, t, km, t, my + fo.MnV},
+                      {a.M_in + s.rs, nk, 1, Y, 1, b, km, t, my + fo.MVn},
+                      {incN + s.rs, nk, 1, Vp, 1, t, km, t, my + fo.NV},
+                      {Cs, ldc, 1, Es, 1, t, km, t, my + fo.CE},
+                      {Es, 1, t, Es, 1, t, tm, t, my + fo.EE},
+                      {Es, 1, t, SEs, 1, t, tm, t, my + fo.ESE},
+                      {Cs, ldc, 1, Cs, ldc, 1, k, k, my + fo.CC}};
+    slice_tn<10>(s.nl, d);
+    if (!a.mode)
+      for (int idx = threadIdx.x; idx < fo.CC; idx += kSST)
+        if (idx >= fo.CnV && (idx < fo.CnVn || idx >= fo.CnVn + kt)) my[idx] = 0.0;
+  }
+  // slice-local outputs: Wt rows [V' | C'^T | 0], V' into Vprev, Ritz block into Y
+  {
     const int RP = a.rp;
-    for (int64_t idx = threadIdx.x; idx < (int64_t)s.nloc * RP; idx += kSST) {
+    for (int64_t idx = threadIdx.x; idx < (int64_t)s.nl * RP; idx += kSST) {
       const int cl = (int)(idx / RP), j = (int)(idx % RP);
-      const int c = s.rs + cl;
       double v = 0.0;
-      if (j < t) v = a.Y[(int64_t)c * b + j];
-      else if (j < t + k) v = a.C_out[(int64_t)(j - t) * nk + c];
-      const int64_t o = (int64_t)(k + c - a.k0) * RP + j;
+      if (j < t) v = Y[cl * b + j];
+      else if (j < t + k) v = Cs[(int64_t)(j - t) * ldc + cl];
+      const int64_t o = (int64_t)(k + s.rs + cl - a.k0) * RP + j;
       if (a.dtype) reinterpret_cast<double*>(a.Wt)[o] = v;
       else reinterpret_cast<float*>(a.Wt)[o] = (float)v;
     }
-    for (int64_t idx = threadIdx.x; idx < (int64_t)s.nloc * t; idx += kSST) {
-      const int cl = (int)(idx / t), j = (int)(idx % t);
-      const int c = s.rs + cl;
-      a.Vprev[(int64_t)c * t + j] = a.Y[(int64_t)c * b + j];
+    for (int idx = threadIdx.x; idx < s.nl * t; idx += kSST) {
+      const int r = idx / t, j = idx - r * t;
+      a.Vprev[(int64_t)(s.rs + r) * t + j] = Y[r * b + j];
+    }
+    for (int idx = threadIdx.x; idx < s.nl * b; idx += kSST) a.Y[(int64_t)s.rs * b + idx] = Y[idx];
+  }
+  tmark(s, a);                                 // final partials
+  cg::this_cluster().sync();                   // partials in global memory (cluster scope)
+  {   // reduce-scatter: CTA c sums its chunk of the flen partials over the CL slots
+    const int64_t fc = (p.flen + s.CL - 1) / s.CL;
+    const int64_t f0 = (int64_t)s.c * fc, f1 = min((int64_t)p.flen, f0 + fc);
+    for (int64_t i = f0 + threadIdx.x; i < f1; i += kSST) {
+      double v[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) v[c] = c < s.CL ? __ldcg(a.xchg + (int64_t)c * p.flen + i) : 0.0;
+      double acc = 0.0;
+#pragma unroll
+      for (int c = 0; c < 16; ++c) acc += v[c];
+      a.red[i] = acc;
     }
   }
-  cl_sync();
+  cg::this_cluster().sync();
+  tmark(s, a);                                 // reduce-scatter
   if (s.c != 0) return;
 
-  // ---- CTA 0: reduce the final partials (fixed order) and finish
-  double* R = a.red;
-  for (int i = threadIdx.x; i < flen; i += kSST) {
-    double v = 0.0;
-    for (int c = 0; c < s.CL; ++c) v += __ldcg(a.xchg + ((int64_t)bank_s * s.CL + c) * a.xchg_stride + i);
-    R[i] = v;
-  }
+  // ---- CTA 0: finish from the reduced partials (fixed order)
+  const bool rsm = p.oTail >= 0;
+  double* R = rsm ? s.sm + p.oTail : a.red;    // reduced partials (staged in smem if room)
+  if (rsm)
+    for (int i = threadIdx.x; i < p.flen; i += kSST) R[i] = __ldcg(a.red + i);
+  double* HCV = R + p.flen;                    // k x t
+  double* HCVn = HCV + kt;                     // k x t
+  double* Wm = HCVn + kt;                      // k x t
   __syncthreads();
   double sum_theta = 0.0;
-  for (int j = 0; j < t; ++j) sum_theta += s.vb[j];
+  for (int j = 0; j < t; ++j) sum_theta += th[j];
+  double trG = 0.0;
+  for (int i = 0; i < k; ++i) trG += Gq[i * k + i];
   const double x2sq_new = R[0] + sum_theta;
   const double F = fw + a.a2sq - R[0] - sum_theta;
   double step = -1.0, rel = -1.0;
   if (a.mode) {
-    double* HCV = R + flen + (int64_t)k * k;     // global scratch after Kinv
-    double* HCVn = HCV + kt;
+    // VnV = V'^T Vp = R^T;  ZnV = (S V')^T Vp = ((Vp^T Z) Q)[:, :t]^T
+    double* ZnV = sm + so.Tb;                  // t x t scratch (Tb is free now)
+    for (int idx = threadIdx.x; idx < t * t; idx += kSST) {
+      const int i = idx / t, j = idx - i * t;
+      double v = 0.0;
+      for (int q = 0; q < b; ++q) v = fma(Gx[2 * b * b + t * b + j * b + q], sm[so.Qb + q * b + i], v);
+      ZnV[idx] = v;
+    }
     for (int idx = threadIdx.x; idx < kt; idx += kSST) {
-      const int l = idx / t, j = idx % t;
+      const int l = idx / t, j = idx - l * t;
       double h1 = 0.0, h2 = 0.0;
       for (int q = 0; q < k; ++q) {
-        h1 = fma(s.Hs[l * k + q], a.CVprev[q * t + j], h1);
-        h2 = fma(s.Hs[l * k + q], R[oCVn + q * t + j], h2);
+        const double hq = Gm[l * k + q] + Gam[l * k + q];
+        h1 = fma(hq, CVp[q * t + j], h1);
+        h2 = fma(hq, R[fo.CVn + q * t + j], h2);
       }
       HCV[idx] = h1;
       HCVn[idx] = h2;
     }
     __syncthreads();
-    // (a) exact Gram identity
-    double v = 0.0;
+    // (a) exact Gram identity   (b) first-order expansion (small steps; no cancellation)
+    double v[2] = {0.0, 0.0};
     for (int idx = threadIdx.x; idx < kt; idx += kSST) {
-      // t1: - <CnV, HCV> - <CnVn, HCVn>;  t3: + <MVn, CVn>;  t2+t4: + <MnV, CnV>
-      v -= R[oCnV + idx] * HCV[idx] + R[oCnVn + idx] * HCVn[idx];
-      v += R[oMVn + idx] * R[oCVn + idx] + R[oMnV + idx] * R[oCnV + idx];
-    }
-    for (int idx = threadIdx.x; idx < t * t; idx += kSST) {
-      const int aa = idx / t, bb = idx % t;     // VnV[aa][bb] = (Vn^T V)[aa][bb]
-      double x1 = 0.0, x3 = 0.0;
-      for (int l = 0; l < k; ++l) {
-        x1 = fma(R[oCnVn + l * t + aa], HCV[l * t + bb], x1);             // (CnVn^T HCV)[aa][bb]
-        x3 = fma(a.CVprev[l * t + bb], R[oMVn + l * t + aa], x3);         // (CVprev^T MVn)[bb][aa]
-      }
-      v += R[oVnV + idx] * (x1 + R[oZnV + idx]) - R[oVnV + idx] * x3;
-    }
-    v = block_sum(v, s.red);
-    const double cross = R[1] + v;
-    double trOm = 0.0;
-    for (int i = 0; i < k; ++i) trOm += incOm[i * k + i];
-    const double x2sq_old = a.scal[0], xn2_old = a.scal[1];
-    const double st2_big = trOm + x2sq_new + x2sq_old - 2.0 * cross;
-    // (b) first-order expansion (small steps)
-    double u = 0.0;
-    for (int idx = threadIdx.x; idx < kt; idx += kSST) {
-      const int l = idx / t, j = idx % t;
+      v[0] -= R[fo.CnV + idx] * HCV[idx] + R[fo.CnVn + idx] * HCVn[idx];
+      v[0] += R[fo.MVn + idx] * R[fo.CVn + idx] + R[fo.MnV + idx] * R[fo.CnV + idx];
+      const int l = idx / t, j = idx - l * t;
       double om = 0.0, gd = 0.0, gg = 0.0, gcv = 0.0;
       for (int q = 0; q < k; ++q) {
-        const double cvq = R[oCnVn + q * t + j];
-        const double dq = cvq - R[oCVn + q * t + j];                      // (dC V')[q][j]
-        om = fma(0.5 * (incOm[l * k + q] + incOm[q * k + l]), cvq, om);
-        gd = fma(incGam[l * k + q], dq, gd);
-        gg = fma(a.G_in[l * k + q], dq, gg);
-        gcv = fma(incGam[l * k + q], a.CVprev[q * t + j], gcv);
+        const double cvq = R[fo.CnVn + q * t + j];
+        const double dq = cvq - R[fo.CVn + q * t + j];
+        om = fma(0.5 * (Om[l * k + q] + Om[q * k + l]), cvq, om);
+        gd = fma(Gam[l * k + q], dq, gd);
+        gg = fma(Gm[l * k + q], dq, gg);
+        gcv = fma(Gam[l * k + q], CVp[q * t + j], gcv);
       }
-      const double cvl = R[oCnVn + idx], dl = cvl - R[oCVn + idx];
-      u -= cvl * om + 2.0 * cvl * gd + dl * gg;                          // -||Z V'||^2
-      HCV[idx] = R[oNV + idx] - gcv;                                     // W = N V - Gam C V
+      const double cvl = R[fo.CnVn + idx], dl = cvl - R[fo.CVn + idx];
+      v[1] -= cvl * om + 2.0 * cvl * gd + dl * gg;
+      Wm[idx] = R[fo.NV + idx] - gcv;
     }
     __syncthreads();
     for (int idx = threadIdx.x; idx < t * t; idx += kSST) {
-      const int i = idx / t, j = idx % t;
+      const int aa = idx / t, bb = idx - aa * t;
+      const double vnv = Rt[bb * t + aa];      // (V'^T Vp)[aa][bb]
+      double x1 = 0.0, x3 = 0.0;
+      for (int l = 0; l < k; ++l) {
+        x1 = fma(R[fo.CnVn + l * t + aa], HCV[l * t + bb], x1);
+        x3 = fma(CVp[l * t + bb], R[fo.MVn + l * t + aa], x3);
+      }
+      v[0] += vnv * (x1 + ZnV[idx]) - vnv * x3;
+      const int i = aa, j = bb;
       double rlr = 0.0, rr = 0.0, xw = 0.0;
       for (int q = 0; q < t; ++q) {
-        rlr = fma(Rt[q * t + i] * a.theta[q], Rt[q * t + j], rlr);       // (R^T Lam R)[i][j]
-        rr = fma(Rt[q * t + i], Rt[q * t + j], rr);                       // (R^T R)[i][j]
+        rlr = fma(Rt[q * t + i] * a.theta[q], Rt[q * t + j], rlr);   // previous Ritz values
+        rr = fma(Rt[q * t + i], Rt[q * t + j], rr);
       }
-      for (int l = 0; l < k; ++l) xw = fma(R[oCE + l * t + i], HCV[l * t + j], xw);   // ((CE)^T W)[i][j]
-      u += rlr * R[oEE + j * t + i] + rr * R[oESE + j * t + i] + 2.0 * xw * Rt[j * t + i];
+      for (int l = 0; l < k; ++l) xw = fma(R[fo.CE + l * t + i], Wm[l * t + j], xw);
+      v[1] += rlr * R[fo.EE + j * t + i] + rr * R[fo.ESE + j * t + i] + 2.0 * xw * Rt[j * t + i];
     }
-    u = block_sum(u, s.red);
-    const double st2_small = trOm + R[2] + 2.0 * R[3] + R[4] + u;
+    block_sum_n<2>(v, red);
+    const double cross = R[1] + v[0];
+    double trOm = 0.0;
+    for (int i = 0; i < k; ++i) trOm += Om[i * k + i];
+    const double x2sq_old = a.scal[0], xn2_old = a.scal[1];
+    const double st2_big = trOm + x2sq_new + x2sq_old - 2.0 * cross;
+    const double st2_small = trOm + R[2] + 2.0 * R[3] + R[4] + v[1];
     const double st2 = st2_big > 1e-8 * xn2_old ? st2_big : st2_small;
     step = sqrt(fmax(st2, 0.0));
     rel = step / sqrt(xn2_old);
   }
-  for (int j = threadIdx.x; j < b; j += kSST) a.theta[j] = s.vb[j];
+  tmark(s, a);                                 // objective + step norm
   __syncthreads();
+  for (int j = threadIdx.x; j < b; j += kSST) a.theta[j] = th[j];
   if (threadIdx.x == 0) {
     const int64_t pnew = a.mode ? (int64_t)llround(a.scal[5]) + 1 : 0;   // canonical state index
     a.scal[0] = x2sq_new;
@@ -739,6 +1010,8 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(SmallArgs a, int sm
     a.scal[3] = step;
     a.scal[4] = rel;
     a.scal[5] = (double)pnew;
+    a.scal[6] = rmax / fabs(th[0]);
+    a.scal[7] = (double)nprod;
     const int64_t slotp = pnew % a.trace_cap;
     a.trace[slotp * 4 + 0] = F;
     a.trace[slotp * 4 + 1] = step;
@@ -750,53 +1023,46 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(SmallArgs a, int sm
   }
   // operands: CV (k x t), K (k x k)
   for (int idx = threadIdx.x; idx < kt; idx += kSST) {
-    const double v = R[oCnVn + idx];
+    const double v = R[fo.CnVn + idx];
     a.CVprev[idx] = v;
     if (a.dtype) reinterpret_cast<double*>(a.CVop)[idx] = v;
     else reinterpret_cast<float*>(a.CVop)[idx] = (float)v;
   }
   if (!a.uniform) {
-    for (int idx = threadIdx.x; idx < k * k; idx += kSST) {
-      const double v = R[oCC + idx];
+    for (int idx = threadIdx.x; idx < kk; idx += kSST) {
+      const int i = idx / k, j = idx - i * k;
+      const double v = 0.5 * (R[fo.CC + idx] + R[fo.CC + j * k + i]);
       if (a.dtype) reinterpret_cast<double*>(a.Kop)[idx] = v;
       else reinterpret_cast<float*>(a.Kop)[idx] = (float)v;
     }
+    tmark(s, a);
     return;
   }
-  // uniform W1: K = w^2 I + C'C'^T, K^{-1} by Cholesky + k column solves (Ls as scratch)
-  double* Kf = s.Ls;
-  for (int idx = threadIdx.x; idx < k * k; idx += kSST)
-    Kf[idx] = R[oCC + idx] + ((idx / k == idx % k) ? a.w2 : 0.0);
+  // uniform W1: K^{-1} = (w^2 I + C'C'^T)^{-1}: Newton-Schulz from the previous K^{-1}
+  // (the NS mats are free now), sweep-operator inverse at init or as fallback
   __syncthreads();
-  if (!chol_warp0(Kf, k, k, 0.0)) {
-    if (threadIdx.x == 0) raise_flag(a.flags, DF_ROWSPD);
-    return;
-  }
-  double* Kinv = R + flen;             // scratch after the reduced partials (k x k)
-  for (int col = warp; col < k; col += kSSW) {
-    double* xw = s.Xw + warp * k;
-    for (int i = lane; i < k; i += 32) xw[i] = (i == col) ? 1.0 : 0.0;
-    __syncwarp();
-    chol_solve_warp(Kf, k, k, xw, 1, lane);
-    for (int i = lane; i < k; i += 32) Kinv[(int64_t)i * k + col] = xw[i];
-    __syncwarp();
+  for (int idx = threadIdx.x; idx < kk; idx += kSST) {
+    const int i = idx / k, j = idx - i * k;
+    Gq[idx] = 0.5 * (R[fo.CC + idx] + R[fo.CC + j * k + i]) + (i == j ? a.w2 : 0.0);
+    if (a.mode) Xq[idx] = a.Ki[idx];
   }
   __syncthreads();
-  for (int idx = threadIdx.x; idx < k * k; idx += kSST) {
-    const int i = idx / k, j = idx % k;
-    const double v = 0.5 * (Kinv[i * k + j] + Kinv[j * k + i]);
+  bool okk = a.mode ? ns_inverse(Gq, Xq, Rq, Pq, k, red) : false;
+  if (!okk) {
+    for (int idx = threadIdx.x; idx < kk; idx += kSST) Xq[idx] = Gq[idx];
+    __syncthreads();
+    if (!sweep_inverse(Xq, k, 0.0, sm + so.d0, sm + so.rb)) {
+      if (threadIdx.x == 0) raise_flag(a.flags, DF_ROWSPD);
+      return;
+    }
+  }
+  for (int idx = threadIdx.x; idx < kk; idx += kSST) {
+    const double v = Xq[idx];
+    a.Ki[idx] = v;
     if (a.dtype) reinterpret_cast<double*>(a.Kop)[idx] = v;
     else reinterpret_cast<float*>(a.Kop)[idx] = (float)v;
   }
-}
-
-inline size_t ss_smem_bytes(const SmallArgs& a, int CL, int flags) {
-  const int SL = (int)ceil_div(a.nk, CL);
-  size_t d = (size_t)2 * a.k * a.k + (size_t)a.k * a.b + 2 * (size_t)a.b * a.b + 32 +
-             (size_t)kSSW * a.k;
-  if (flags & 1) d += (size_t)SL * a.nk;
-  if (flags & 2) d += (size_t)a.nk * a.b;
-  return d * sizeof(double);
+  tmark(s, a);                                 // K^{-1}
 }
 
 template <int BT>
@@ -836,21 +1102,21 @@ int ss_max_clusters(int CL, size_t smem) {
 }
 
 template <int BT>
-cudaError_t launch_ss(const SmallArgs& a, int CL, size_t smem, int fl, cudaStream_t st) {
-  cudaError_t e = ss_configure<BT>(CL, smem);
+cudaError_t launch_ss(const SmallArgs& a, cudaStream_t st) {
+  const size_t smem = (size_t)a.pl.total * sizeof(double);
+  cudaError_t e = ss_configure<BT>(a.pl.CL, smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(CL);
+  cfg.gridDim = dim3(a.pl.CL);
   cfg.blockDim = dim3(kSST);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = CL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  at[0].val.clusterDim.x = a.pl.CL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, small_step_kernel<BT>, a, fl);
+  return cudaLaunchKernelEx(&cfg, small_step_kernel<BT>, a);
 }
-
 
 }  // namespace wlr
