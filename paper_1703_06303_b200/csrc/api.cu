@@ -64,8 +64,9 @@ bool is_device_ptr(const void* p) {
 struct Profile {
   std::vector<cudaEvent_t> pool;
   size_t used = 0;
-  double ms[4] = {0, 0, 0, 0};
+  double ms[5] = {0, 0, 0, 0, 0};   // row pass, increments, reduce, small step (K3a), deferred K3b
   int64_t launches = 0, iters = 0;
+  std::vector<int> groups;           // per profiled iteration: 1 if it launched a deferred K3b
 };
 
 }  // namespace
@@ -87,13 +88,16 @@ struct wlr_ctx {
   const void* A = nullptr; int64_t lda = 0;
   const void* W1 = nullptr; int64_t ldw = 0;
   void* X[2] = {nullptr, nullptr};
+  void* Dl = nullptr;          // Delta = X1_{p+1} - X1_p (m x kp, written by the row pass)
+  int nwc = 8;                 // row-pass warps running per-row Cholesky
   void *Wt = nullptr, *CVop = nullptr, *Kop = nullptr;
   double *inc_part = nullptr, *fw_part = nullptr, *inc = nullptr, *fw0 = nullptr;
   double* GA = nullptr;
   double a2sq = 0.0;
   double *G[2] = {nullptr, nullptr}, *M[2] = {nullptr, nullptr}, *C[2] = {nullptr, nullptr};
   double *Gi[2] = {nullptr, nullptr}, *Ki = nullptr, *gws = nullptr;   // G^{-1}, K^{-1}, K3 workspace
-  double *Vprev = nullptr, *CVprev = nullptr, *Y = nullptr, *theta = nullptr;
+  double *V[2] = {nullptr, nullptr}, *CV[2] = {nullptr, nullptr}, *th[2] = {nullptr, nullptr};
+  double *Y = nullptr, *k3x = nullptr;
   double *xchg = nullptr, *red = nullptr, *scal = nullptr, *trace = nullptr;
   double* tdbg = nullptr;      // K3 phase timestamps (wlr_debug_state "ktime")
   SmallArgs last_ss{};         // arguments of the last small-step launch (diagnostics)
@@ -106,7 +110,11 @@ struct wlr_ctx {
   bool own_stream = false;
   int par = 0;                 // parity of the current state (= p mod 2)
   int64_t p = 0;               // index of the current canonical state
-  cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+  cudaGraphExec_t gexec[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};   // [parity][deferred pending]
+  cudaStream_t st2 = nullptr;  // side stream of the deferred small-step half
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool pending = false;        // deferred half of the last small step not launched yet
+  SmallArgs pend{};
   ncclComm_t comm = nullptr;
   bool prof = false;
   Profile pr;
@@ -144,7 +152,12 @@ static wlr_status dalloc_t(wlr_ctx* h, P** p, size_t count) {
   return dalloc(h, reinterpret_cast<void**>(p), count * sizeof(P));
 }
 
+static wlr_status flush_pending(wlr_ctx* h);
 static wlr_status check_flags(wlr_ctx* h) {
+  {
+    wlr_status fs = flush_pending(h);
+    if (fs != WLR_OK) return fs;
+  }
   CUDA_TRY(h, cudaMemcpyAsync(h->h_flags, h->flags, 8 * sizeof(int), cudaMemcpyDeviceToHost, h->st));
   CUDA_TRY(h, cudaMemcpyAsync(h->h_scal, h->scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, h->st));
   CUDA_TRY(h, cudaStreamSynchronize(h->st));
@@ -171,34 +184,96 @@ static cudaEvent_t prof_event(wlr_ctx* h) {
   return h->pr.pool[h->pr.used++];
 }
 
+// L2 prefetch list for the row pass: the inputs the following small step reads first
+static void set_prefetch(wlr_ctx* h, int cur, const void** ptr, int64_t* bytes) {
+  const int64_t k = h->k, nk = h->nk;
+  ptr[0] = h->GA;       bytes[0] = nk * nk * 8;
+  ptr[1] = h->M[cur];   bytes[1] = k * nk * 8;
+  ptr[2] = h->C[cur];   bytes[2] = k * nk * 8;
+  ptr[3] = h->Y;        bytes[3] = nk * h->b * 8;
+  ptr[4] = h->V[cur];   bytes[4] = nk * h->t * 8;
+  ptr[5] = h->Gi[cur];  bytes[5] = k * k * 8;
+}
+
+static SmallArgs small_args(wlr_ctx* h, int par, int mode) {
+  const int cur = par, nxt = par ^ 1;
+  SmallArgs s{};
+  s.k = (int)h->k; s.nk = (int)h->nk; s.t = (int)h->t; s.b = h->b; s.kp = (int)h->kp;
+  s.k0 = (int)h->k0; s.rp = h->rp; s.mode = mode; s.dtype = h->dtype == WLR_F64 ? 1 : 0;
+  s.uniform = h->uniform ? 1 : 0; s.w2 = h->w1s * h->w1s;
+  s.GA = h->GA; s.a2sq = h->a2sq; s.inc = mode ? h->inc : h->fw0;
+  s.G_in = h->G[cur]; s.G_out = h->G[nxt]; s.M_in = h->M[cur]; s.M_out = h->M[nxt];
+  s.C_in = h->C[cur]; s.C_out = h->C[nxt];
+  s.V_in = h->V[cur]; s.V_out = h->V[nxt]; s.CV_in = h->CV[cur]; s.CV_out = h->CV[nxt];
+  s.th_in = h->th[cur]; s.th_out = h->th[nxt]; s.k3x = h->k3x;
+  s.Y = h->Y;
+  s.Gi_in = h->Gi[cur]; s.Gi_out = h->Gi[nxt]; s.Ki = h->Ki; s.gws = h->gws;
+  s.xchg = h->xchg; s.red = h->red; s.scal = h->scal;
+  s.trace = h->trace; s.trace_cap = h->trace_cap;
+  s.Wt = h->Wt; s.CVop = h->CVop; s.Kop = h->Kop; s.flags = h->flags;
+  s.eps = h->opts.eps; s.tol = h->opts.eig_tol; s.max_outer = h->opts.eig_max_outer; s.max_deg = 16;
+  s.cold = 0;
+  s.tdbg = h->ktime ? h->tdbg : nullptr;
+  s.pl = h->spl;
+  return s;
+}
+
+// Launch the deferred half of the previous small step (objective, step norm, trace) on the
+// main stream: needed before the host reads F / the trace / the stopping flag.
+static wlr_status flush_pending(wlr_ctx* h) {
+  if (!h->pending) return WLR_OK;
+  cudaError_t e = launch_small_step(h->pend, 2, h->st);
+  if (e != cudaSuccess) return fail(h, WLR_ECUDA, std::string("small step (deferred): ") + cudaGetErrorString(e));
+  h->pending = false;
+  h->pr.launches += 1;
+  return WLR_OK;
+}
+
+// One iteration.  Stream order:
+//   st : row pass(p) -> increments(p) -> [join] -> reduce(p) -> allreduce -> K3a(p)
+//   st2: [fork at the start] K3b(p-1)       (objective/step norm of the previous state)
+// K3b(p-1) only reads state the row pass / increments of iteration p do not write; reduce(p)
+// (which rewrites the increments K3b reads) waits for it.
 static wlr_status enqueue_iteration(wlr_ctx* h, int par) {
   const int cur = par, nxt = par ^ 1;
-  cudaEvent_t ev[6] = {};
+  cudaEvent_t ev[8] = {};
   const bool prof = h->prof;
+  const bool pend = h->pending;
   if (prof) {
-    for (int i = 0; i < 6; ++i) ev[i] = prof_event(h);
+    for (int i = 0; i < 8; ++i) ev[i] = prof_event(h);
     cudaEventRecord(ev[0], h->st);
   }
   cudaError_t e;
+  if (pend) {                                  // fork: deferred half of the previous step
+    CUDA_TRY(h, cudaEventRecord(h->ev_fork, h->st));
+    CUDA_TRY(h, cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
+    if (prof) cudaEventRecord(ev[6], h->st2);
+    e = launch_small_step(h->pend, 2, h->st2);
+    if (e != cudaSuccess) return fail(h, WLR_ECUDA, std::string("small step (deferred): ") + cudaGetErrorString(e));
+    if (prof) cudaEventRecord(ev[7], h->st2);
+    CUDA_TRY(h, cudaEventRecord(h->ev_join, h->st2));
+  }
   if (h->dtype == WLR_F32) {
     RowPassArgs<float> a{};
     a.A = (const float*)h->A; a.lda = h->lda; a.W1 = (const float*)h->W1; a.ldw = h->ldw;
     a.w2s = (float)(h->w1s * h->w1s);
-    a.Xold = (const float*)h->X[cur]; a.Xnew = (float*)h->X[nxt];
+    a.Xold = (const float*)h->X[cur]; a.Xnew = (float*)h->X[nxt]; a.Dnew = (float*)h->Dl; a.nwc = h->nwc;
     a.Wt = (const float*)h->Wt; a.CV = (const float*)h->CVop; a.Kmat = (const float*)h->Kop;
     a.fw_part = h->fw_part; a.flags = h->flags;
     a.m = h->m; a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.k0 = (int)h->k0; a.t = (int)h->t;
     a.vec_ok = (h->lda % 4 == 0) && ((uintptr_t)h->A % 16 == 0);
+    set_prefetch(h, cur, a.pf_ptr, a.pf_bytes);
     e = launch_row_pass<float>(a, h->rp, h->uniform, 0, h->rp_grid, h->st);
   } else {
     RowPassArgs<double> a{};
     a.A = (const double*)h->A; a.lda = h->lda; a.W1 = (const double*)h->W1; a.ldw = h->ldw;
     a.w2s = h->w1s * h->w1s;
-    a.Xold = (const double*)h->X[cur]; a.Xnew = (double*)h->X[nxt];
+    a.Xold = (const double*)h->X[cur]; a.Xnew = (double*)h->X[nxt]; a.Dnew = (double*)h->Dl; a.nwc = h->nwc;
     a.Wt = (const double*)h->Wt; a.CV = (const double*)h->CVop; a.Kmat = (const double*)h->Kop;
     a.fw_part = h->fw_part; a.flags = h->flags;
     a.m = h->m; a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.k0 = (int)h->k0; a.t = (int)h->t;
     a.vec_ok = (h->lda % 4 == 0) && ((uintptr_t)h->A % 16 == 0);
+    set_prefetch(h, cur, a.pf_ptr, a.pf_bytes);
     e = launch_row_pass<double>(a, h->rp, h->uniform, 0, h->rp_grid, h->st);
   }
   if (e != cudaSuccess) return fail(h, WLR_ECUDA, std::string("row pass: ") + cudaGetErrorString(e));
@@ -206,7 +281,7 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int par) {
   if (h->dtype == WLR_F32) {
     IncrArgs<float> a{};
     a.A = (const float*)h->A; a.lda = h->lda;
-    a.Xold = (const float*)h->X[cur]; a.Xnew = (const float*)h->X[nxt];
+    a.Xold = (const float*)h->X[cur]; a.Dnew = (const float*)h->Dl;
     a.part = h->inc_part; a.m = h->m; a.rows_per_split = h->rps;
     a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.k0 = (int)h->k0; a.nz = h->nz; a.nsplit = h->nsplit;
     a.vec_ok = (h->lda % 4 == 0) && ((uintptr_t)h->A % 16 == 0) && (h->n % 4 == 0);
@@ -214,7 +289,7 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int par) {
   } else {
     IncrArgs<double> a{};
     a.A = (const double*)h->A; a.lda = h->lda;
-    a.Xold = (const double*)h->X[cur]; a.Xnew = (const double*)h->X[nxt];
+    a.Xold = (const double*)h->X[cur]; a.Dnew = (const double*)h->Dl;
     a.part = h->inc_part; a.m = h->m; a.rows_per_split = h->rps;
     a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.k0 = (int)h->k0; a.nz = h->nz; a.nsplit = h->nsplit;
     a.vec_ok = (h->lda % 4 == 0) && ((uintptr_t)h->A % 16 == 0) && (h->n % 4 == 0);
@@ -222,6 +297,7 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int par) {
   }
   if (e != cudaSuccess) return fail(h, WLR_ECUDA, std::string("increments: ") + cudaGetErrorString(e));
   if (prof) cudaEventRecord(ev[2], h->st);
+  if (pend) CUDA_TRY(h, cudaStreamWaitEvent(h->st, h->ev_join, 0));   // join
   launch_reduce_incr(h->inc_part, h->nsplit, (int)h->k, (int)h->nk, h->nz, (int)(h->k - h->k0),
                      (int)(h->n - h->k0), (int)h->kp, h->fw_part, h->rp_grid, h->inc, h->st);
   if (prof) cudaEventRecord(ev[3], h->st);
@@ -231,58 +307,53 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int par) {
     if (nr != ncclSuccess) return fail(h, WLR_ENCCL, std::string("ncclAllReduce: ") + g_nccl.errStr(nr));
   }
   if (prof) cudaEventRecord(ev[4], h->st);
-  SmallArgs s{};
-  s.k = (int)h->k; s.nk = (int)h->nk; s.t = (int)h->t; s.b = h->b; s.kp = (int)h->kp;
-  s.k0 = (int)h->k0; s.rp = h->rp; s.mode = 1; s.dtype = h->dtype == WLR_F64 ? 1 : 0;
-  s.uniform = h->uniform ? 1 : 0; s.w2 = h->w1s * h->w1s;
-  s.GA = h->GA; s.a2sq = h->a2sq; s.inc = h->inc;
-  s.G_in = h->G[cur]; s.G_out = h->G[nxt]; s.M_in = h->M[cur]; s.M_out = h->M[nxt];
-  s.C_in = h->C[cur]; s.C_out = h->C[nxt];
-  s.Vprev = h->Vprev; s.CVprev = h->CVprev; s.Y = h->Y;
-  s.Gi_in = h->Gi[cur]; s.Gi_out = h->Gi[nxt]; s.Ki = h->Ki; s.gws = h->gws;
-  s.theta = h->theta; s.xchg = h->xchg; s.red = h->red; s.scal = h->scal;
-  s.trace = h->trace; s.trace_cap = h->trace_cap;
-  s.Wt = h->Wt; s.CVop = h->CVop; s.Kop = h->Kop; s.flags = h->flags;
-  s.eps = h->opts.eps; s.tol = h->opts.eig_tol; s.max_outer = h->opts.eig_max_outer; s.max_deg = 16;
-  s.cold = 0;
-  s.tdbg = h->ktime ? h->tdbg : nullptr;
-  s.pl = h->spl;
+  SmallArgs s = small_args(h, par, 1);
   h->last_ss = s;
-  e = launch_small_step(s, h->st);
+  e = launch_small_step(s, 1, h->st);
   if (e != cudaSuccess) return fail(h, WLR_ECUDA, std::string("small step: ") + cudaGetErrorString(e));
   if (prof) {
     cudaEventRecord(ev[5], h->st);
     h->pr.iters++;
+    h->pr.groups.push_back(pend ? 1 : 0);
   }
-  h->pr.launches += 4;
+  h->pend = s;
+  h->pending = true;
+  h->pr.launches += pend ? 5 : 4;
   return WLR_OK;
 }
 
-static wlr_status build_graphs(wlr_ctx* h) {
-  for (int par = 0; par < 2; ++par) {
-    cudaGraph_t g;
-    CUDA_TRY(h, cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
-    const int64_t l0 = h->pr.launches;
-    wlr_status s = enqueue_iteration(h, par);
-    h->pr.launches = l0;
-    cudaError_t e = cudaStreamEndCapture(h->st, &g);
-    if (s != WLR_OK) return s;
-    CUDA_TRY(h, e);
-    CUDA_TRY(h, cudaGraphInstantiate(&h->gexec[par], g, 0));
-    cudaGraphDestroy(g);
-  }
+static wlr_status build_graph(wlr_ctx* h, int par, int pend) {
+  cudaGraph_t g;
+  const bool keep_pend = h->pending;
+  const SmallArgs keep_args = h->pend;
+  h->pending = pend != 0;
+  if (pend) h->pend = small_args(h, par ^ 1, 1);   // the previous iteration's step
+  CUDA_TRY(h, cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
+  const int64_t l0 = h->pr.launches;
+  wlr_status s = enqueue_iteration(h, par);
+  h->pr.launches = l0;
+  cudaError_t e = cudaStreamEndCapture(h->st, &g);
+  h->pending = keep_pend;
+  h->pend = keep_args;
+  if (s != WLR_OK) return s;
+  CUDA_TRY(h, e);
+  CUDA_TRY(h, cudaGraphInstantiate(&h->gexec[par][pend], g, 0));
+  cudaGraphDestroy(g);
   return WLR_OK;
 }
 
 static wlr_status launch_iteration(wlr_ctx* h) {
   wlr_status s;
   if (h->opts.use_graph && !h->prof) {
-    if (!h->gexec[0]) {
-      s = build_graphs(h);
+    const int pend = h->pending ? 1 : 0;
+    if (!h->gexec[h->par][pend]) {
+      s = build_graph(h, h->par, pend);
       if (s != WLR_OK) return s;
     }
-    CUDA_TRY(h, cudaGraphLaunch(h->gexec[h->par], h->st));
-    h->pr.launches += 4;
+    CUDA_TRY(h, cudaGraphLaunch(h->gexec[h->par][pend], h->st));
+    h->pend = small_args(h, h->par, 1);
+    h->pending = true;
+    h->pr.launches += pend ? 5 : 4;
   } else {
     s = enqueue_iteration(h, h->par);
     if (s != WLR_OK) return s;
@@ -366,15 +437,20 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   const int tm = row_pass_tm(h->rp);
   const size_t rsm = h->dtype == WLR_F32 ? row_pass_smem<float>(h->rp, h->uniform, (int)k, (int)t, (int)kp)
                                          : row_pass_smem<double>(h->rp, h->uniform, (int)k, (int)t, (int)kp);
-  if (rsm > 227 * 1024) return fail(h, WLR_EINVAL, "row-pass shared memory exceeds 227 KB for this (k, r)");
+  h->nwc = h->dtype == WLR_F32 ? row_pass_chol_warps<float>(h->rp, h->uniform, (int)k, (int)t, (int)kp)
+                               : row_pass_chol_warps<double>(h->rp, h->uniform, (int)k, (int)t, (int)kp);
+  if (rsm > 227 * 1024 || h->nwc < 1)
+    return fail(h, WLR_EINVAL, "row-pass shared memory exceeds 227 KB for this (k, r)");
   const int64_t ntiles = ceil_div(h->m, tm);
-  const int per_sm = rsm > 113 * 1024 ? 1 : 2;
+  // row pass: one tile per CTA when the whole grid is co-resident (3 CTAs/SM fit at the
+  // metric's config), else a persistent grid of co-resident CTAs
+  const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(3, (227 * 1024) / std::max<size_t>(rsm, 1)));
   h->rp_grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)h->nsm * per_sm));
   h->bm = incr_bm((int)kp);
   const int bn = incr_bn(h->bm);
   h->nz = (int)((n - h->k0) + 2 * kp);
   const int ncol = (int)ceil_div(h->nz, bn);
-  int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(h->m, 256), ceil_div(2 * h->nsm, ncol)));
+  int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(h->m, 128), ceil_div(4 * h->nsm, ncol)));
   h->rps = round_up(ceil_div(h->m, nsplit), 32);
   h->nsplit = (int)std::max<int64_t>(1, ceil_div(h->m, h->rps));
   // eigen block width b
@@ -396,6 +472,7 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   const int64_t wt_rows = round_up(n - h->k0, 32) + 32;
   if ((s = dalloc(h, &h->X[0], (size_t)h->m * kp * es)) != WLR_OK) return s;
   if ((s = dalloc(h, &h->X[1], (size_t)h->m * kp * es)) != WLR_OK) return s;
+  if ((s = dalloc(h, &h->Dl, (size_t)h->m * kp * es)) != WLR_OK) return s;
   if ((s = dalloc(h, &h->Wt, (size_t)wt_rows * h->rp * es)) != WLR_OK) return s;
   if ((s = dalloc(h, &h->CVop, (size_t)std::max<int64_t>(k * t, 1) * es)) != WLR_OK) return s;
   if ((s = dalloc(h, &h->Kop, (size_t)k * k * es)) != WLR_OK) return s;
@@ -412,10 +489,20 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   }
   if ((s = dalloc_t(h, &h->Ki, (size_t)k * k)) != WLR_OK) return s;
   if ((s = dalloc_t(h, &h->gws, (size_t)std::max<int64_t>(1, h->spl.CL * h->spl.gws_stride))) != WLR_OK) return s;
-  if ((s = dalloc_t(h, &h->Vprev, (size_t)nk * t)) != WLR_OK) return s;
-  if ((s = dalloc_t(h, &h->CVprev, (size_t)k * t)) != WLR_OK) return s;
+  for (int i = 0; i < 2; ++i) {
+    if ((s = dalloc_t(h, &h->V[i], (size_t)nk * t)) != WLR_OK) return s;
+    if ((s = dalloc_t(h, &h->CV[i], (size_t)k * t)) != WLR_OK) return s;
+    if ((s = dalloc_t(h, &h->th[i], 32)) != WLR_OK) return s;
+  }
+  if ((s = dalloc_t(h, &h->k3x, (size_t)2 * t * t + 8)) != WLR_OK) return s;
   if ((s = dalloc_t(h, &h->Y, (size_t)nk * b)) != WLR_OK) return s;
-  if ((s = dalloc_t(h, &h->theta, 32)) != WLR_OK) return s;
+  {
+    int lo = 0, hi = 0;
+    CUDA_TRY(h, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CUDA_TRY(h, cudaStreamCreateWithPriority(&h->st2, cudaStreamNonBlocking, hi));
+    CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+    CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+  }
   if ((s = dalloc_t(h, &h->xchg, (size_t)h->spl.CL * h->spl.flen)) != WLR_OK) return s;
   if ((s = dalloc_t(h, &h->red, (size_t)h->spl.flen + 3 * k * t + 64)) != WLR_OK) return s;
   if ((s = dalloc_t(h, &h->scal, 8)) != WLR_OK) return s;
@@ -504,22 +591,15 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
     CUDA_TRY(h, cudaStreamSynchronize(h->st));
   }
   // small step configuration
-  SmallArgs sa{};
-  sa.k = (int)k; sa.nk = (int)nk; sa.t = (int)t; sa.b = b; sa.kp = (int)kp; sa.k0 = (int)h->k0;
-  sa.rp = h->rp; sa.mode = 0; sa.dtype = h->dtype == WLR_F64 ? 1 : 0;
-  sa.uniform = h->uniform ? 1 : 0; sa.w2 = h->w1s * h->w1s;
-  sa.GA = h->GA; sa.a2sq = h->a2sq; sa.inc = h->fw0;
-  sa.G_in = h->G[0]; sa.G_out = h->G[0]; sa.M_in = h->M[0]; sa.M_out = h->M[0];
-  sa.C_in = h->C[0]; sa.C_out = h->C[0];
-  sa.Vprev = h->Vprev; sa.CVprev = h->CVprev; sa.Y = h->Y;
-  sa.Gi_in = nullptr; sa.Gi_out = h->Gi[0]; sa.Ki = h->Ki; sa.gws = h->gws;
-  sa.theta = h->theta; sa.xchg = h->xchg; sa.red = h->red; sa.scal = h->scal;
-  sa.trace = h->trace; sa.trace_cap = h->trace_cap;
-  sa.Wt = h->Wt; sa.CVop = h->CVop; sa.Kop = h->Kop; sa.flags = h->flags;
-  sa.eps = o.eps; sa.tol = o.eig_tol; sa.max_outer = 4 * o.eig_max_outer; sa.max_deg = 16; sa.cold = 1;
-  sa.pl = h->spl;
+  // initial (C, D) half-step: outputs into buffer 0 (small_args with par = 1 maps out -> 0)
+  SmallArgs sa = small_args(h, 1, 0);
+  sa.G_in = nullptr; sa.M_in = nullptr; sa.C_in = nullptr; sa.Gi_in = nullptr;
+  sa.V_in = nullptr; sa.CV_in = nullptr; sa.th_in = nullptr;
+  sa.G_out = h->G[0]; sa.M_out = h->M[0];        // mode 0 reads the init Grams from here
+  sa.max_outer = 4 * o.eig_max_outer; sa.cold = 1;
   sa.tdbg = h->tdbg;
-  cudaError_t e = launch_small_step(sa, h->st);
+  cudaError_t e = launch_small_step(sa, 1, h->st);
+  if (e == cudaSuccess) e = launch_small_step(sa, 2, h->st);
   if (e != cudaSuccess) return fail(h, WLR_ECUDA, std::string("small step (init): ") + cudaGetErrorString(e));
   h->pr.launches = 0;
   s = check_flags(h);
@@ -669,7 +749,7 @@ extern "C" wlr_status wlr_result(wlr_handle h, void* X1, int64_t ldx1, void* C, 
   }
   if (D) {
     std::vector<double> v((size_t)h->nk * h->t), d((size_t)h->nk * h->t);
-    CUDA_TRY(h, cudaMemcpyAsync(v.data(), h->Vprev, v.size() * 8, cudaMemcpyDeviceToHost, h->st));
+    CUDA_TRY(h, cudaMemcpyAsync(v.data(), h->V[cur], v.size() * 8, cudaMemcpyDeviceToHost, h->st));
     CUDA_TRY(h, cudaStreamSynchronize(h->st));
     for (int64_t c = 0; c < h->nk; ++c)
       for (int64_t j = 0; j < h->t; ++j) d[j * h->nk + c] = v[c * h->t + j];
@@ -683,7 +763,7 @@ extern "C" wlr_status wlr_result(wlr_handle h, void* X1, int64_t ldx1, void* C, 
     if (h->dtype == WLR_F32) {
       RowPassArgs<float> a{};
       a.A = (const float*)h->A; a.lda = h->lda; a.W1 = (const float*)h->W1; a.ldw = h->ldw;
-      a.w2s = (float)(h->w1s * h->w1s); a.Xold = (const float*)h->X[cur]; a.Xnew = nullptr;
+      a.w2s = (float)(h->w1s * h->w1s); a.Xold = (const float*)h->X[cur]; a.Xnew = nullptr; a.nwc = h->nwc;
       a.Wt = (const float*)h->Wt; a.CV = (const float*)h->CVop; a.Kmat = (const float*)h->Kop;
       a.Bout = (float*)Bd; a.ldb = h->t; a.fw_part = h->fw_part; a.flags = h->flags;
       a.m = h->m; a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.k0 = (int)h->k0; a.t = (int)h->t;
@@ -692,7 +772,7 @@ extern "C" wlr_status wlr_result(wlr_handle h, void* X1, int64_t ldx1, void* C, 
     } else {
       RowPassArgs<double> a{};
       a.A = (const double*)h->A; a.lda = h->lda; a.W1 = (const double*)h->W1; a.ldw = h->ldw;
-      a.w2s = h->w1s * h->w1s; a.Xold = (const double*)h->X[cur]; a.Xnew = nullptr;
+      a.w2s = h->w1s * h->w1s; a.Xold = (const double*)h->X[cur]; a.Xnew = nullptr; a.nwc = h->nwc;
       a.Wt = (const double*)h->Wt; a.CV = (const double*)h->CVop; a.Kmat = (const double*)h->Kop;
       a.Bout = (double*)Bd; a.ldb = h->t; a.fw_part = h->fw_part; a.flags = h->flags;
       a.m = h->m; a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.k0 = (int)h->k0; a.t = (int)h->t;
@@ -712,9 +792,9 @@ extern "C" wlr_status wlr_result(wlr_handle h, void* X1, int64_t ldx1, void* C, 
       else if (cudaMalloc(&X2d, (size_t)h->m * h->nk * es) != cudaSuccess) { cudaFree(Bd); return fail(h, WLR_ENOMEM, "X2 staging"); }
       const int64_t ldo = dev ? ldx2 : h->nk;
       if (h->dtype == WLR_F32)
-        launch_assemble_x2<float>((const float*)h->X[cur], (int)h->kp, (const float*)Bd, h->t, h->C[cur], h->Vprev, h->m, (int)h->k, (int)h->nk, (int)h->t, (float*)X2d, ldo, h->st);
+        launch_assemble_x2<float>((const float*)h->X[cur], (int)h->kp, (const float*)Bd, h->t, h->C[cur], h->V[cur], h->m, (int)h->k, (int)h->nk, (int)h->t, (float*)X2d, ldo, h->st);
       else
-        launch_assemble_x2<double>((const double*)h->X[cur], (int)h->kp, (const double*)Bd, h->t, h->C[cur], h->Vprev, h->m, (int)h->k, (int)h->nk, (int)h->t, (double*)X2d, ldo, h->st);
+        launch_assemble_x2<double>((const double*)h->X[cur], (int)h->kp, (const double*)Bd, h->t, h->C[cur], h->V[cur], h->m, (int)h->k, (int)h->nk, (int)h->t, (double*)X2d, ldo, h->st);
       if (!dev) {
         s = copy_out(h, X2, ldx2, X2d, h->nk, h->m, h->nk, es);
         cudaStreamSynchronize(h->st);
@@ -741,23 +821,24 @@ extern "C" wlr_status wlr_debug_state(wlr_handle h, const char* name, double* ou
   if (nm == "G") { src = h->G[cur]; cnt = h->k * h->k; }
   else if (nm == "M") { src = h->M[cur]; cnt = h->k * h->nk; }
   else if (nm == "C") { src = h->C[cur]; cnt = h->k * h->nk; }
-  else if (nm == "V") { src = h->Vprev; cnt = h->nk * h->t; }
-  else if (nm == "lam") { src = h->theta; cnt = h->t; }
-  else if (nm == "theta") { src = h->theta; cnt = h->b; }
+  else if (nm == "V") { src = h->V[cur]; cnt = h->nk * h->t; }
+  else if (nm == "lam") { src = h->th[cur]; cnt = h->t; }
+  else if (nm == "theta") { src = h->th[cur]; cnt = h->b; }
   else if (nm == "GA") { src = h->GA; cnt = h->nk * h->nk; }
   else if (nm == "scal") { src = h->scal; cnt = 8; }
   else if (nm == "ktime") { src = h->tdbg; cnt = 64; }
   else if (nm == "ktime_on" || nm == "ktime_off") {   // enable/disable K3 phase timestamps
     h->ktime = nm == "ktime_on";
-    for (auto& g : h->gexec)
-      if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+    for (auto& gp : h->gexec)
+      for (auto& g : gp)
+        if (g) { cudaGraphExecDestroy(g); g = nullptr; }
     if (count) *count = 0;
     return WLR_OK;
   }
   else if (nm == "ss_rerun") {                 // relaunch the last small step twice (timing only;
     SmallArgs s2 = h->last_ss;                  // leaves the state inconsistent)
     s2.tdbg = h->tdbg;
-    for (int rep = 0; rep < 2; ++rep) CUDA_TRY(h, launch_small_step(s2, h->st));
+    for (int rep = 0; rep < 2; ++rep) CUDA_TRY(h, launch_small_step(s2, 1, h->st));
     CUDA_TRY(h, cudaStreamSynchronize(h->st));
     if (count) *count = 0;
     return WLR_OK;
@@ -779,18 +860,21 @@ extern "C" wlr_status wlr_profile(wlr_handle h, int32_t enable, int32_t reset, d
                                   int32_t nms, int64_t* launches, int64_t* timed_iters) {
   if (!h) return fail(nullptr, WLR_EINVAL, "null handle");
   CUDA_TRY(h, cudaStreamSynchronize(h->st));
-  // fold recorded event groups (6 per iteration) into the per-kernel sums
-  for (size_t g = 0; g + 6 <= h->pr.used; g += 6) {
-    float t01 = 0, t12 = 0, t23 = 0, t45 = 0;
+  CUDA_TRY(h, cudaStreamSynchronize(h->st2));
+  // fold recorded event groups (8 per iteration; 6, 7 = deferred K3b on the side stream)
+  for (size_t g = 0, it = 0; g + 8 <= h->pr.used; g += 8, ++it) {
+    float t01 = 0, t12 = 0, t23 = 0, t45 = 0, t67 = 0;
     cudaEventElapsedTime(&t01, h->pr.pool[g], h->pr.pool[g + 1]);
     cudaEventElapsedTime(&t12, h->pr.pool[g + 1], h->pr.pool[g + 2]);
     cudaEventElapsedTime(&t23, h->pr.pool[g + 2], h->pr.pool[g + 3]);
     cudaEventElapsedTime(&t45, h->pr.pool[g + 4], h->pr.pool[g + 5]);
-    h->pr.ms[0] += t01; h->pr.ms[1] += t12; h->pr.ms[2] += t23; h->pr.ms[3] += t45;
+    if (it < h->pr.groups.size() && h->pr.groups[it]) cudaEventElapsedTime(&t67, h->pr.pool[g + 6], h->pr.pool[g + 7]);
+    h->pr.ms[0] += t01; h->pr.ms[1] += t12; h->pr.ms[2] += t23; h->pr.ms[3] += t45; h->pr.ms[4] += t67;
   }
+  h->pr.groups.clear();
   h->pr.used = 0;
   if (ms)
-    for (int i = 0; i < nms && i < 4; ++i) ms[i] = h->pr.ms[i];
+    for (int i = 0; i < nms && i < 5; ++i) ms[i] = h->pr.ms[i];
   if (launches) *launches = h->pr.launches;
   if (timed_iters) *timed_iters = h->pr.iters;
   if (reset) {
@@ -833,8 +917,13 @@ extern "C" const char* wlr_status_string(int32_t s) {
 extern "C" void wlr_destroy(wlr_handle h) {
   if (!h) return;
   if (h->st) cudaStreamSynchronize(h->st);
-  for (auto& g : h->gexec)
-    if (g) cudaGraphExecDestroy(g);
+  if (h->st2) cudaStreamSynchronize(h->st2);
+  for (auto& gp : h->gexec)
+    for (auto& g : gp)
+      if (g) cudaGraphExecDestroy(g);
+  if (h->st2) cudaStreamDestroy(h->st2);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
   if (h->comm && g_nccl.commDestroy) g_nccl.commDestroy(h->comm);
   for (void* p : h->allocs) cudaFree(p);
   for (auto e : h->pr.pool) cudaEventDestroy(e);

@@ -28,18 +28,22 @@ struct RowPassArgs {
   const T* W1; int64_t ldw;         // m x k or nullptr (uniform)
   T w2s;                            // uniform weight squared
   const T* Xold; T* Xnew;           // m x kp
+  T* Dnew;                          // m x kp  Delta = Xnew - Xold (stored values)
+  int nwc;                          // warps running per-row Cholesky (non-uniform W1)
   const T* Wt;                      // (n-k0 padded to 32) x RP : rows c-k0 = [V(c-k,:) | C(:,c-k)^T | 0]
   const T* CV;                      // k x t  = C V
   const T* Kmat;                    // k x k  : K^{-1} (uniform) or C C^T
   T* Bout; int64_t ldb;             // MODE_RESULT output
   double* fw_part;                  // gridDim.x partials
   int* flags;
+  const void* pf_ptr[6]; int64_t pf_bytes[6];   // L2 prefetch of the next small step's inputs
   int64_t m; int n, k, kp, k0, t;
   int vec_ok;                       // A rows 16-byte aligned at multiples of 4 elements
 };
 int row_pass_rp(int r);
 int row_pass_tm(int rp);
 template <typename T> size_t row_pass_smem(int rp, bool uniform, int k, int t, int kp);
+template <typename T> int row_pass_chol_warps(int rp, bool uniform, int k, int t, int kp);
 template <typename T>
 cudaError_t launch_row_pass(const RowPassArgs<T>& a, int rp, bool uniform, int mode, int grid,
                             cudaStream_t st);
@@ -47,7 +51,7 @@ cudaError_t launch_row_pass(const RowPassArgs<T>& a, int rp, bool uniform, int m
 template <typename T>
 struct IncrArgs {
   const T* A; int64_t lda;
-  const T* Xold; const T* Xnew;     // m x kp
+  const T* Xold; const T* Dnew;     // m x kp  X1_p and Delta
   double* part;                     // nsplit x k x nz
   int64_t m; int64_t rows_per_split;
   int n, k, kp, k0, nz, nsplit;
@@ -85,13 +89,14 @@ struct SmallArgs {
   const double* G_in; double* G_out;   // k x k
   const double* M_in; double* M_out;   // k x nk
   const double* C_in; double* C_out;   // k x nk
-  double* Vprev;                    // nk x t  (V of the previous state; updated in place)
-  double* CVprev;                   // k x t   (C V of the previous state; updated)
+  const double* V_in; double* V_out;     // nk x t  V_p (previous state) / V_{p+1}
+  const double* CV_in; double* CV_out;   // k x t   C_p V_p / C_{p+1} V_{p+1}
+  const double* th_in; double* th_out;   // b       Ritz values of S_p / S_{p+1}
+  double* k3x;                      // small results K3a -> K3b: R (t x t), ZnV (t x t)
   double* Y;                        // nk x b  warm-start Ritz block (updated)
   const double* Gi_in; double* Gi_out;   // k x k  G^{-1} of the previous / current state
   double* Ki;                       // k x k  (w^2 I + C C^T)^{-1} (uniform W1; updated)
   double* gws;                      // CL x gws_stride global workspace
-  double* theta;                    // b Ritz values (updated; previous values read first)
   double* xchg;                     // CL x flen global partial slots
   double* red;                      // flen reduced partials
   double* scal;                     // persistent scalars (see small_step.cuh)
@@ -105,7 +110,9 @@ struct SmallArgs {
 };
 bool small_step_plan(SmallArgs& a, int CL);       // fills a.pl; false if it cannot fit
 int small_step_cluster_size(SmallArgs& a);        // picks CL and fills a.pl (0 = none)
-cudaError_t launch_small_step(const SmallArgs& a, cudaStream_t st);
+// part 1: critical half (C', eigenpairs, next row-pass operands); part 2: deferred half
+// (objective, step norm, trace), which may run concurrently with the next row pass
+cudaError_t launch_small_step(const SmallArgs& a, int part, cudaStream_t st);
 int small_step_bt(int b);
 
 // ---------------------------------------------------------------- result (result.cu)

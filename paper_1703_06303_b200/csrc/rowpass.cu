@@ -6,39 +6,34 @@
 //        e   = A1(i,:) . W1(i,:)^2 + y_C - b (C_p V_p)^T   (= E_p(i,:) = [A1.W1.W1 + (A2-D_p)C_p^T](i,:))
 //        x'  = e (diag(W1(i,:)^2) + C_p C_p^T)^{-1}        (uniform W1: one shared inverse;
 //                                                           otherwise warp-per-row Cholesky)
-//      writes X1_{p+1}(i,:) and an fp64 partial of f_w = sum W1^2 (A1 - X1_{p+1})^2.
+//      writes X1_{p+1}(i,:), Delta(i,:) = X1_{p+1}(i,:) - X1_p(i,:) (from the stored values) and
+//      an fp64 partial of f_w = sum W1^2 (A1 - X1_{p+1})^2.
 //      MODE_RESULT writes b (row of B) instead of solving (wlr_result).
-// K2b  incr_kernel : Gram increments with Delta = X1_{p+1} - X1_p (fp32, from the stored
-//        values):  N = Delta^T A2,  Gamma = Delta^T X1_p,  Omega = Delta^T Delta.
-//        fp32 inside 256-row super-chunks, fp64 across them and across CTAs.
+// K2b  incr_kernel : Gram increments  N = Delta^T A2,  Gamma = Delta^T X1_p,  Omega = Delta^T Delta.
+//        fp32 inside <= 256-row chunks, fp64 across them and across CTAs.
 // K2c  reduce_incr_kernel : fixed-order fp64 sum of the K2b/K2a partials into the packed
 //        increment vector [N | Gamma | Omega | f_w] that is all-reduced across ranks.
+//
+// Mainloops: operands stream global -> shared with cp.async (LDGSTS) into
+// double-buffered stages, so no registers hold in-flight tiles; each thread owns an
+// 8 x TC register tile fed by 128-bit shared loads (row pass: A rows read 4 k at a time, rows
+// interleaved by 8 so a warp's A loads hit distinct banks).  The row pass splits the
+// reduction over KG = 4 thread groups (in-CTA split-K, fixed-order sum).  Its epilogue runs
+// from shared memory (X1_p and A1 of the tile are staged with the first chunk), as
+// thread-per-output small products.  A is streamed once from HBM by the row pass; the
+// increment pass re-reads it from L2 (46 MB at the metric's config fits the 126 MB L2).
 #include "kernels.h"
 
 namespace wlr {
 
-// ------------------------------------------------------------------------------ K2a
-template <int RP> struct RowPassShape;
-template <> struct RowPassShape<16>  { static constexpr int TM = 128, TR = 4, TC = 2; };
-template <> struct RowPassShape<32>  { static constexpr int TM = 128, TR = 4, TC = 4; };
-template <> struct RowPassShape<64>  { static constexpr int TM = 128, TR = 8, TC = 4; };
-template <> struct RowPassShape<128> { static constexpr int TM = 64,  TR = 4, TC = 8; };
-
-constexpr int kRowKC = 32;        // reduction chunk (columns of A2)
-constexpr int kRowThreads = 256;
-
-template <typename T, int RP>
-struct RowPassSmem {
-  using S = RowPassShape<RP>;
-  static constexpr int TMP = S::TM + 4;                         // padded row count (As)
-  static constexpr int kAsBs = kRowKC * TMP + kRowKC * RP;      // GEMM phase
-  static constexpr int kYs = S::TM * (RP + 1);                  // epilogue y tile
-  static constexpr int kUnion = kAsBs > kYs ? kAsBs : kYs;
-};
-
-// Per-warp scratch for the epilogue: b (t values), e / solution (kp values), and for
-// non-uniform W1 the packed lower triangle of the row matrix.
-__host__ __device__ inline int chol_packed(int kp) { return kp * (kp + 1) / 2; }
+// ------------------------------------------------------------------------- cp.async
+WLR_DEVI void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+WLR_DEVI void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+WLR_DEVI void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 template <typename T>
 WLR_DEVI void load_vec4_or_scalar(const T* p, bool vec, T out[4], int valid) {
@@ -51,175 +46,299 @@ WLR_DEVI void load_vec4_or_scalar(const T* p, bool vec, T out[4], int valid) {
   }
 }
 
+// N consecutive T from shared memory with 128-bit loads where possible
+template <typename T, int N>
+WLR_DEVI void lds_vec(const T* p, T (&o)[N]) {
+  if constexpr (sizeof(T) == 4 && N % 4 == 0) {
+#pragma unroll
+    for (int q = 0; q < N; q += 4) {
+      const float4 v = *reinterpret_cast<const float4*>(p + q);
+      o[q] = v.x; o[q + 1] = v.y; o[q + 2] = v.z; o[q + 3] = v.w;
+    }
+  } else if constexpr (N % 2 == 0) {
+#pragma unroll
+    for (int q = 0; q < N; q += 2) {
+      if constexpr (sizeof(T) == 4) {
+        const float2 v = *reinterpret_cast<const float2*>(p + q);
+        o[q] = v.x; o[q + 1] = v.y;
+      } else {
+        const double2 v = *reinterpret_cast<const double2*>(p + q);
+        o[q] = v.x; o[q + 1] = v.y;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < N; ++q) o[q] = p[q];
+  }
+}
+
+// ------------------------------------------------------------------------------ K2a
+template <int RP> struct RowPassShape;   // BM rows per tile, TC columns per thread (TR = 8)
+template <> struct RowPassShape<16>  { static constexpr int BM = 64, TC = 2; };
+template <> struct RowPassShape<32>  { static constexpr int BM = 64, TC = 4; };
+template <> struct RowPassShape<64>  { static constexpr int BM = 64, TC = 8; };
+template <> struct RowPassShape<128> { static constexpr int BM = 32, TC = 8; };
+
+constexpr int kRowKC = 32;        // reduction chunk (columns of A2)
+constexpr int kRowKG = 4;         // k-groups (in-CTA split-K); each takes 8 k of a chunk
+constexpr int kRowTR = 8;         // rows per thread (interleaved by BM / 8)
+constexpr int kRowThreads = 256;
+
+// Per-warp scratch for the non-uniform epilogue: the packed lower triangle of the row matrix.
+__host__ __device__ inline int chol_packed(int kp) { return kp * (kp + 1) / 2; }
+
+template <typename T, int RP>
+struct RowPassLayout {            // shared memory layout (elements of T)
+  using S = RowPassShape<RP>;
+  static constexpr int BM = S::BM;
+  static constexpr int ALD = kRowKC + 16 / (int)sizeof(T);      // padded A row (16 B)
+  static constexpr int kA = BM * ALD;                           // one A stage
+  static constexpr int kB = kRowKC * RP;                        // one Wt stage
+  static constexpr int YLD = RP + 1;
+  static constexpr int oA = 0, oB = 2 * kA, oY = oB + 2 * kB, oX = oY + BM * YLD;
+  // then: X1_p tile [BM][kp], A1 tile [BM][kp], e tile [BM][kp], b tile [BM][32],
+  //       K^{-1} or C C^T [k][k], C V [k][t], per-warp packed L (non-uniform)
+};
+
+template <typename T, int RP>
+size_t row_pass_smem_elems(bool uniform, int k, int t, int kp, int nwc) {
+  using L = RowPassLayout<T, RP>;
+  size_t n = (size_t)L::oX + 3 * (size_t)L::BM * kp + (size_t)L::BM * 32 + (size_t)k * kp + (size_t)k * t;
+  if (!uniform) n += (size_t)nwc * chol_packed(kp);
+  return n;
+}
+
+// warps that can hold a packed k x k factor in the remaining shared memory (<= 8)
+template <typename T, int RP>
+int row_pass_nwc(bool uniform, int k, int t, int kp) {
+  if (uniform) return 8;
+  const size_t base = row_pass_smem_elems<T, RP>(true, k, t, kp, 0);
+  const size_t cap = 227 * 1024 / sizeof(T);
+  if (base >= cap) return 0;
+  return (int)std::min<size_t>(8, (cap - base) / chol_packed(kp));
+}
+
 template <typename T, int RP, bool UNIFORM, int MODE>
 __global__ void __launch_bounds__(kRowThreads)
 row_pass_kernel(RowPassArgs<T> a) {
   using S = RowPassShape<RP>;
-  constexpr int TM = S::TM, TR = S::TR, TC = S::TC;
-  constexpr int TMP = RowPassSmem<T, RP>::TMP;
-  constexpr int THC = RP / TC;                 // threads along columns
-  static_assert((TM / TR) * THC == kRowThreads, "thread tile");
-  constexpr int AV = TM * kRowKC / 4 / kRowThreads;     // vec4 loads of A per thread
-  constexpr int BVN = kRowKC * RP / 4;                  // vec4 of one Wt chunk
-  constexpr int BV = (BVN + kRowThreads - 1) / kRowThreads;   // per thread (guarded)
-  constexpr int BVc = BV;
+  using L = RowPassLayout<T, RP>;
+  constexpr int BM = S::BM, TC = S::TC, TR = kRowTR, KG = kRowKG, ALD = L::ALD;
+  constexpr int THC = RP / TC;                 // threads along columns (per k-group)
+  constexpr int GT = (BM / TR) * THC;          // threads per k-group
+  static_assert(GT * KG == kRowThreads, "thread tile");
+  constexpr int KPG = kRowKC / KG;             // k per group per chunk (8)
+  constexpr int VE = 16 / (int)sizeof(T);      // elements per 16-byte copy
+  constexpr int RS = BM / TR;                  // row interleave stride
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
-  T* As = sm;                                   // [KC][TMP]
-  T* Bs = sm + kRowKC * TMP;                    // [KC][RP]
-  T* Ys = sm;                                   // [TM][RP+1] (aliases As/Bs after the GEMM)
-  T* sK = sm + RowPassSmem<T, RP>::kUnion;      // uniform: K^{-1} (k x k); else C C^T (k x k)
-  T* sCV = sK + (UNIFORM ? a.k * a.k : 0);      // C V (k x t)
-  T* sW = sCV + a.k * a.t;                      // per-warp scratch
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kp = a.kp, k = a.k, t = a.t;
-  const int wstride = 32 + kp + (UNIFORM ? 0 : chol_packed(kp));
-  T* wb = sW + warp * wstride;                  // b   [32]
-  T* we = wb + 32;                              // e   [kp]
-  T* wL = we + kp;                              // packed L (non-uniform)
+  T* As = sm + L::oA;                          // [2][BM][ALD]
+  T* Bs = sm + L::oB;                          // [2][KC][RP]
+  T* Ys = sm + L::oY;                          // [BM][RP+1]
+  T* Xs = sm + L::oX;                          // [BM][kp]  X1_p rows of the tile
+  T* A1s = Xs + BM * kp;                       // [BM][kp]  A1 columns of the tile
+  T* Es = A1s + BM * kp;                       // [BM][kp]  e, then the solution
+  T* Bt = Es + BM * kp;                        // [BM][32]  b
+  T* sK = Bt + BM * 32;                        // [k][k]    K^{-1} (uniform) or C C^T
+  T* sCV = sK + k * kp;                        // [k][t]
+  T* sL = sCV + k * t;                         // per-warp packed L (non-uniform)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  for (int i = threadIdx.x; i < (UNIFORM ? k * k : 0); i += kRowThreads) sK[i] = a.Kmat[i];
+  // K^{-1} (uniform; leading dimension kp, zero-padded) or C C^T (leading dimension k)
+  if (UNIFORM) {
+    for (int i = threadIdx.x; i < k * kp; i += kRowThreads) {
+      const int r = i / kp, c = i - r * kp;
+      sK[i] = c < k ? a.Kmat[r * k + c] : T(0);
+    }
+  } else {
+    for (int i = threadIdx.x; i < k * k; i += kRowThreads) sK[i] = a.Kmat[i];
+  }
   for (int i = threadIdx.x; i < k * t; i += kRowThreads) sCV[i] = a.CV[i];
+  // The small step that follows is latency-bound and reads G_A and its previous state:
+  // pull them into L2 while this pass streams A (bulk L2 prefetch, 64 KB per request).
+  if (MODE == 0 && threadIdx.x < 32) {
+    for (int r = 0; r < 6; ++r) {
+      const char* base = reinterpret_cast<const char*>(a.pf_ptr[r]);
+      const int64_t nb = a.pf_bytes[r] & ~(int64_t)15;
+      if (!base || nb <= 0) continue;
+      const int64_t chunk = 65536;
+      const int64_t nchunk = ceil_div(nb, chunk);
+      for (int64_t c = blockIdx.x * 32 + threadIdx.x; c < nchunk; c += (int64_t)gridDim.x * 32) {
+        const int64_t off = c * chunk;
+        const unsigned sz = (unsigned)(nb - off < chunk ? nb - off : chunk);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(base + off), "r"(sz) : "memory");
+      }
+    }
+  }
 
-  const int ty = threadIdx.x / THC, tx = threadIdx.x % THC;
+  const int kg = threadIdx.x / GT, gt = threadIdx.x - kg * GT;
+  const int ty = gt / THC, tx = gt - ty * THC;
   const int nch = (int)ceil_div(a.n - a.k0, kRowKC);
   double fw = 0.0;
-  const int64_t ntiles = ceil_div(a.m, TM);
+  const int64_t ntiles = ceil_div(a.m, BM);
+  const bool vec = a.vec_ok;
+
+  // issue the async copies of chunk ch of the tile starting at row r0 into stage st
+  auto issue = [&](int64_t r0, int ch, int st) {
+    const int cb = a.k0 + ch * kRowKC;
+    T* as = As + st * L::kA;
+    for (int idx = threadIdx.x; idx < BM * (kRowKC / VE); idx += kRowThreads) {
+      const int rr = idx / (kRowKC / VE), cv = (idx % (kRowKC / VE)) * VE;
+      const int64_t row = r0 + rr;
+      const int col = cb + cv;
+      T* dst = as + rr * ALD + cv;
+      if (vec) {
+        int valid = a.n - col;
+        valid = valid > VE ? VE : (valid < 0 ? 0 : valid);
+        if (row >= a.m) valid = 0;
+        const T* src = valid > 0 ? a.A + row * a.lda + col : a.A;
+        cp_async16(dst, src, valid * (int)sizeof(T));
+      } else {
+#pragma unroll
+        for (int q = 0; q < VE; ++q)
+          dst[q] = (row < a.m && col + q < a.n) ? a.A[row * a.lda + col + q] : T(0);
+      }
+    }
+    T* bs = Bs + st * L::kB;
+    for (int idx = threadIdx.x; idx < kRowKC * RP / VE; idx += kRowThreads) {
+      const int rr = idx / (RP / VE), cv = (idx % (RP / VE)) * VE;
+      cp_async16(bs + rr * RP + cv, a.Wt + (int64_t)(ch * kRowKC + rr) * RP + cv, 16);   // padded
+    }
+  };
 
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t r0 = tile * TM;
-    // ---------------- GEMM  Y[TM x RP] = A2_tile . Wt  (register-prefetched chunks)
+    const int64_t r0 = tile * BM;
+    __syncthreads();                           // previous tile's epilogue done with the stages
+    // epilogue operands of this tile (X1_p rows, A1 columns) ride with chunk 0
+    for (int idx = threadIdx.x; idx < BM * (kp / VE); idx += kRowThreads) {
+      const int rr = idx / (kp / VE), cv = (idx % (kp / VE)) * VE;
+      const int64_t row = r0 + rr;
+      const bool in = row < a.m;
+      cp_async16(Xs + rr * kp + cv, in ? a.Xold + row * kp + cv : a.Xold, in ? 16 : 0);
+      if (vec && cv + VE <= a.n) {
+        cp_async16(A1s + rr * kp + cv, in ? a.A + row * a.lda + cv : a.A, in ? 16 : 0);
+      } else {
+#pragma unroll
+        for (int q = 0; q < VE; ++q) A1s[rr * kp + cv + q] = (in && cv + q < a.n) ? a.A[row * a.lda + cv + q] : T(0);
+      }
+    }
+    issue(r0, 0, 0);
+    cp_async_commit();
+
     T acc[TR][TC];
 #pragma unroll
     for (int i = 0; i < TR; ++i)
 #pragma unroll
       for (int j = 0; j < TC; ++j) acc[i][j] = T(0);
-    T ra[AV][4];
-    T rb[BVc][4];
-    auto gload = [&](int ch) {
-      const int cb = a.k0 + ch * kRowKC;       // absolute first column of the chunk
-#pragma unroll
-      for (int e = 0; e < AV; ++e) {
-        const int idx = threadIdx.x + e * kRowThreads;
-        const int rr = idx / (kRowKC / 4), c4 = (idx % (kRowKC / 4)) * 4;
-        const int64_t row = r0 + rr;
-        const int col = cb + c4;
-        int valid = a.n - col;
-        valid = valid > 4 ? 4 : (valid < 0 ? 0 : valid);
-        if (row >= a.m) valid = 0;
-        load_vec4_or_scalar<T>(a.A + row * a.lda + col, a.vec_ok, ra[e], row < a.m ? valid : 0);
-      }
-#pragma unroll
-      for (int e = 0; e < BV; ++e) {
-        const int idx = threadIdx.x + e * kRowThreads;
-        if (idx < BVN) {
-          const int rr = idx / (RP / 4), c4 = (idx % (RP / 4)) * 4;
-          const T* p = a.Wt + (int64_t)(ch * kRowKC + rr) * RP + c4;   // Wt padded: no bounds
-          auto v = ldg4<T>(p);
-          rb[e][0] = v.x; rb[e][1] = v.y; rb[e][2] = v.z; rb[e][3] = v.w;
-        }
-      }
-    };
-    auto sstore = [&]() {
-#pragma unroll
-      for (int e = 0; e < AV; ++e) {
-        const int idx = threadIdx.x + e * kRowThreads;
-        const int rr = idx / (kRowKC / 4), c4 = (idx % (kRowKC / 4)) * 4;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) As[(c4 + q) * TMP + rr] = ra[e][q];
-      }
-#pragma unroll
-      for (int e = 0; e < BV; ++e) {
-        const int idx = threadIdx.x + e * kRowThreads;
-        if (idx < BVN) {
-          const int rr = idx / (RP / 4), c4 = (idx % (RP / 4)) * 4;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) Bs[rr * RP + c4 + q] = rb[e][q];
-        }
-      }
-    };
-    gload(0);
-    __syncthreads();            // previous tile's epilogue finished with Ys (aliases As)
-    sstore();
-    __syncthreads();
+
     for (int ch = 0; ch < nch; ++ch) {
-      if (ch + 1 < nch) gload(ch + 1);
-#pragma unroll 8
-      for (int kk = 0; kk < kRowKC; ++kk) {
-        T av[TR], bv[TC];
+      const int st = ch & 1;
+      if (ch + 1 < nch) issue(r0, ch + 1, st ^ 1);
+      cp_async_commit();
+      cp_async_wait<1>();
+      __syncthreads();
+      const T* as = As + st * L::kA;
+      const T* bs = Bs + st * L::kB;
 #pragma unroll
-        for (int i = 0; i < TR; ++i) av[i] = As[kk * TMP + ty * TR + i];
+      for (int k4 = 0; k4 < KPG; k4 += VE) {
+        const int kk0 = kg * KPG + k4;
+        T av[TR][VE];
 #pragma unroll
-        for (int j = 0; j < TC; ++j) bv[j] = Bs[kk * RP + tx * TC + j];
+        for (int i = 0; i < TR; ++i) {
+          T tmp[VE];
+          lds_vec<T, VE>(as + (ty + i * RS) * ALD + kk0, tmp);
+#pragma unroll
+          for (int q = 0; q < VE; ++q) av[i][q] = tmp[q];
+        }
+#pragma unroll
+        for (int q = 0; q < VE; ++q) {
+          T bv[TC];
+          lds_vec<T, TC>(bs + (kk0 + q) * RP + tx * TC, bv);
+#pragma unroll
+          for (int i = 0; i < TR; ++i)
+#pragma unroll
+            for (int j = 0; j < TC; ++j) acc[i][j] = fma(av[i][q], bv[j], acc[i][j]);
+        }
+      }
+      __syncthreads();                         // stage st may be overwritten next iteration
+    }
+    // fixed-order sum of the KG partial tiles into Ys
+#pragma unroll 1
+    for (int g = 0; g < KG; ++g) {
+      if (kg == g) {
 #pragma unroll
         for (int i = 0; i < TR; ++i)
 #pragma unroll
-          for (int j = 0; j < TC; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+          for (int j = 0; j < TC; ++j) {
+            T* y = Ys + (ty + i * RS) * L::YLD + tx * TC + j;
+            *y = g == 0 ? acc[i][j] : *y + acc[i][j];
+          }
       }
       __syncthreads();
-      if (ch + 1 < nch) {
-        sstore();
-        __syncthreads();
-      }
     }
-#pragma unroll
-    for (int i = 0; i < TR; ++i)
-#pragma unroll
-      for (int j = 0; j < TC; ++j) Ys[(ty * TR + i) * (RP + 1) + tx * TC + j] = acc[i][j];
-    __syncthreads();
+    const int nrow = (int)((a.m - r0) < BM ? (a.m - r0) : BM);
 
-    // ---------------- epilogue: warp per row
-    for (int rl = warp; rl < TM; rl += kRowThreads / 32) {
-      const int64_t g = r0 + rl;
-      if (g >= a.m) break;
-      const T* yr = Ys + rl * (RP + 1);
-      const T* xo = a.Xold + g * kp;
-      // b_j = y_V[j] - sum_l x_l (CV)_{lj}
-      for (int j = 0; j < t; ++j) {
-        T part = T(0);
-        for (int l = lane; l < k; l += 32) part = fma(xo[l], sCV[l * t + j], part);
-        part = warp_sum(part);
-        if (lane == 0) wb[j] = yr[j] - part;
-      }
-      __syncwarp();
-      if (MODE == 1) {                       // wlr_result: B(i,:) = b
-        for (int j = lane; j < t; j += 32) a.Bout[g * a.ldb + j] = wb[j];
-        __syncwarp();
-        continue;
-      }
-      // e_l = a1_l w_l^2 + y_C[l] - sum_j b_j (CV)_{lj}
-      for (int l = lane; l < kp; l += 32) {
-        T e = T(0);
-        if (l < k) {
-          const T a1 = a.A[g * a.lda + l];
-          const T w2 = UNIFORM ? a.w2s : a.W1[g * a.ldw + l] * a.W1[g * a.ldw + l];
-          e = fma(a1, w2, yr[t + l]);
-          for (int j = 0; j < t; ++j) e = fma(-wb[j], sCV[l * t + j], e);
+    // ---------------- epilogue (shared memory only; thread per output)
+    // b[r][j] = y_V[r][j] - sum_l X1_p[r][l] (CV)[l][j]
+    for (int o = threadIdx.x; o < nrow * t; o += kRowThreads) {
+      const int r = o / t, j = o - r * t;
+      T v = Ys[r * L::YLD + j];
+      for (int l = 0; l < k; ++l) v = fma(-Xs[r * kp + l], sCV[l * t + j], v);
+      Bt[r * 32 + j] = v;
+      if (MODE == 1) a.Bout[(r0 + r) * a.ldb + j] = v;
+    }
+    if (MODE == 1) continue;
+    __syncthreads();
+    // e[r][l] = a1 w^2 + y_C[r][l] - sum_j b[r][j] (CV)[l][j]
+    for (int o = threadIdx.x; o < nrow * k; o += kRowThreads) {
+      const int r = o / k, l = o - r * k;
+      const T w2 = UNIFORM ? a.w2s : a.W1[(r0 + r) * a.ldw + l] * a.W1[(r0 + r) * a.ldw + l];
+      T e = fma(A1s[r * kp + l], w2, Ys[r * L::YLD + t + l]);
+      for (int j = 0; j < t; ++j) e = fma(-Bt[r * 32 + j], sCV[l * t + j], e);
+      Es[r * kp + l] = e;
+    }
+    __syncthreads();
+    if (UNIFORM) {
+      // x'[r][l..l+3] = sum_m e[r][m] (K^{-1})[m][l..l+3];  Delta = x' - x;  f_w
+      // (thread per row and 4 consecutive outputs: one broadcast e load per 4 FMA)
+      const int kq = kp / 4;
+      for (int o = threadIdx.x; o < nrow * kq; o += kRowThreads) {
+        const int r = o / kq, l0 = (o - r * kq) * 4;
+        T x[4] = {T(0), T(0), T(0), T(0)};
+        const T* er = Es + r * kp;
+        for (int mm = 0; mm < k; ++mm) {
+          const T e = er[mm];
+          const T* kr = sK + mm * kp + l0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) x[q] = fma(e, kr[q], x[q]);
         }
-        we[l] = e;
-      }
-      __syncwarp();
-      if (UNIFORM) {
-        // x'_l = sum_m e_m (K^{-1})_{ml}
-        for (int l = lane; l < kp; l += 32) {
-          T x = T(0);
-          if (l < k)
-            for (int mm = 0; mm < k; ++mm) x = fma(we[mm], sK[mm * k + l], x);
-          a.Xnew[g * kp + l] = x;
+        const int64_t gi = (r0 + r) * kp + l0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int l = l0 + q;
+          const T xv = l < k ? x[q] : T(0);
+          a.Xnew[gi + q] = xv;
+          a.Dnew[gi + q] = xv - Xs[r * kp + l];
           if (l < k) {
-            const double d = (double)a.A[g * a.lda + l] - (double)x;
+            const double d = (double)A1s[r * kp + l] - (double)xv;
             fw += (double)a.w2s * d * d;
           }
         }
-      } else {
-        // K = C C^T + diag(w^2), packed lower triangle P(i,j) = i(i+1)/2 + j
+      }
+    } else {
+      // K = C C^T + diag(w^2): warp per row, packed lower triangle P(i,j) = i(i+1)/2 + j
+      T* wL = sL + warp * chol_packed(kp);
+      for (int rl = warp; rl < (warp < a.nwc ? nrow : 0); rl += a.nwc) {
+        const int64_t g = r0 + rl;
+        T* we = Es + rl * kp;
         for (int idx = lane; idx < chol_packed(k); idx += 32) {
           int i = (int)((sqrtf(8.f * idx + 1.f) - 1.f) * 0.5f);
           while ((i + 1) * (i + 2) / 2 <= idx) ++i;
           while (i * (i + 1) / 2 > idx) --i;
           const int j = idx - i * (i + 1) / 2;
-          T v = a.Kmat[i * k + j];
+          T v = sK[i * k + j];
           if (i == j) v += a.W1[g * a.ldw + i] * a.W1[g * a.ldw + i];
           wL[idx] = v;
         }
@@ -242,16 +361,14 @@ row_pass_kernel(RowPassArgs<T> a) {
           __syncwarp();
         }
         if (!spd && lane == 0) raise_flag(a.flags, DF_ROWSPD);
-        // forward: L z = e
-        for (int j = 0; j < k; ++j) {
+        for (int j = 0; j < k; ++j) {          // forward: L z = e
           const T zj = we[j] / wL[j * (j + 1) / 2 + j];
           for (int i = j + 1 + lane; i < k; i += 32) we[i] = fma(-wL[i * (i + 1) / 2 + j], zj, we[i]);
           __syncwarp();
           if (lane == 0) we[j] = zj;
           __syncwarp();
         }
-        // backward: L^T x = z
-        for (int j = k - 1; j >= 0; --j) {
+        for (int j = k - 1; j >= 0; --j) {     // backward: L^T x = z
           const T xj = we[j] / wL[j * (j + 1) / 2 + j];
           const T* rowj = wL + j * (j + 1) / 2;
           for (int i = lane; i < j; i += 32) we[i] = fma(-rowj[i], xj, we[i]);
@@ -262,14 +379,15 @@ row_pass_kernel(RowPassArgs<T> a) {
         for (int l = lane; l < kp; l += 32) {
           const T x = l < k ? we[l] : T(0);
           a.Xnew[g * kp + l] = x;
+          a.Dnew[g * kp + l] = x - Xs[rl * kp + l];
           if (l < k) {
             const double w = (double)a.W1[g * a.ldw + l];
-            const double d = (double)a.A[g * a.lda + l] - (double)x;
+            const double d = (double)A1s[rl * kp + l] - (double)x;
             fw += w * w * d * d;
           }
         }
+        __syncwarp();
       }
-      __syncwarp();
     }
   }
   if (MODE == 0) {
@@ -285,17 +403,10 @@ row_pass_kernel(RowPassArgs<T> a) {
   }
 }
 
-template <typename T, int RP, bool UNIFORM>
-size_t row_pass_smem_bytes(int k, int t, int kp) {
-  const int wstride = 32 + kp + (UNIFORM ? 0 : chol_packed(kp));
-  return sizeof(T) * ((size_t)RowPassSmem<T, RP>::kUnion + (UNIFORM ? (size_t)k * k : 0) +
-                      (size_t)k * t + (size_t)(kRowThreads / 32) * wstride);
-}
-
 template <typename T, int RP, bool UNIFORM, int MODE>
 static cudaError_t launch_rp(const RowPassArgs<T>& a, int grid, cudaStream_t st) {
   auto kern = row_pass_kernel<T, RP, UNIFORM, MODE>;
-  const size_t smem = row_pass_smem_bytes<T, RP, UNIFORM>(a.k, a.t, a.kp);
+  const size_t smem = sizeof(T) * row_pass_smem_elems<T, RP>(UNIFORM, a.k, a.t, a.kp, a.nwc);
   static size_t configured = 0;            // cudaFuncSetAttribute once per size increase
   if (smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -314,17 +425,28 @@ static cudaError_t dispatch_rp(const RowPassArgs<T>& a, bool uniform, int mode, 
 }
 
 int row_pass_rp(int r) { return r <= 16 ? 16 : r <= 32 ? 32 : r <= 64 ? 64 : r <= 128 ? 128 : -1; }
-int row_pass_tm(int rp) { return rp == 128 ? RowPassShape<128>::TM : 128; }
+int row_pass_tm(int rp) { return rp == 128 ? RowPassShape<128>::BM : RowPassShape<32>::BM; }
 
 template <typename T>
 size_t row_pass_smem(int rp, bool uniform, int k, int t, int kp) {
   switch (rp) {
-    case 16: return uniform ? row_pass_smem_bytes<T, 16, true>(k, t, kp) : row_pass_smem_bytes<T, 16, false>(k, t, kp);
-    case 32: return uniform ? row_pass_smem_bytes<T, 32, true>(k, t, kp) : row_pass_smem_bytes<T, 32, false>(k, t, kp);
-    case 64: return uniform ? row_pass_smem_bytes<T, 64, true>(k, t, kp) : row_pass_smem_bytes<T, 64, false>(k, t, kp);
-    default: return uniform ? row_pass_smem_bytes<T, 128, true>(k, t, kp) : row_pass_smem_bytes<T, 128, false>(k, t, kp);
+    case 16: return sizeof(T) * row_pass_smem_elems<T, 16>(uniform, k, t, kp, row_pass_nwc<T, 16>(uniform, k, t, kp));
+    case 32: return sizeof(T) * row_pass_smem_elems<T, 32>(uniform, k, t, kp, row_pass_nwc<T, 32>(uniform, k, t, kp));
+    case 64: return sizeof(T) * row_pass_smem_elems<T, 64>(uniform, k, t, kp, row_pass_nwc<T, 64>(uniform, k, t, kp));
+    default: return sizeof(T) * row_pass_smem_elems<T, 128>(uniform, k, t, kp, row_pass_nwc<T, 128>(uniform, k, t, kp));
   }
 }
+template <typename T>
+int row_pass_chol_warps(int rp, bool uniform, int k, int t, int kp) {
+  switch (rp) {
+    case 16: return row_pass_nwc<T, 16>(uniform, k, t, kp);
+    case 32: return row_pass_nwc<T, 32>(uniform, k, t, kp);
+    case 64: return row_pass_nwc<T, 64>(uniform, k, t, kp);
+    default: return row_pass_nwc<T, 128>(uniform, k, t, kp);
+  }
+}
+template int row_pass_chol_warps<float>(int, bool, int, int, int);
+template int row_pass_chol_warps<double>(int, bool, int, int, int);
 template size_t row_pass_smem<float>(int, bool, int, int, int);
 template size_t row_pass_smem<double>(int, bool, int, int, int);
 
@@ -343,156 +465,221 @@ template cudaError_t launch_row_pass<float>(const RowPassArgs<float>&, int, bool
 template cudaError_t launch_row_pass<double>(const RowPassArgs<double>&, int, bool, int, int, cudaStream_t);
 
 // ------------------------------------------------------------------------------ K2b
-template <int BM> struct IncrShape;
-template <> struct IncrShape<16>  { static constexpr int BN = 128, TR = 2, TC = 4; };
-template <> struct IncrShape<32>  { static constexpr int BN = 128, TR = 4, TC = 4; };
-template <> struct IncrShape<64>  { static constexpr int BN = 64,  TR = 4, TC = 4; };
-template <> struct IncrShape<128> { static constexpr int BN = 64,  TR = 8, TC = 4; };
-constexpr int kIncRC = 32;          // rows per smem stage
-constexpr int kIncSuper = 8;        // stages per fp32 super-chunk (256 rows)
+// Thread tile 8 (q) x 4 (columns); warp w owns q in [8w, 8w+8) and lanes 32 column groups,
+// so the Delta operand is a warp broadcast and the Z operand one LDS.128 per lane.
+// Z = [A(:, k0:n) | X1_p | Delta]; stages arrive by cp.async (double-buffered).
+constexpr int kIncRC = 32;          // rows per stage
+constexpr int kIncBN = 128;         // columns per CTA
+constexpr int kIncFlush = 8;        // stages per fp32 chunk (256 rows), then fp64
 
-int incr_bm(int kp) { return kp <= 16 ? 16 : kp <= 32 ? 32 : kp <= 64 ? 64 : kp <= 128 ? 128 : -1; }
-int incr_bn(int bm) { return bm <= 32 ? 128 : 64; }
+int incr_bm(int kp) { return kp <= 32 ? 32 : kp <= 64 ? 64 : kp <= 128 ? 128 : -1; }
+int incr_bn(int) { return kIncBN; }
 
 template <typename T, int BM>
-__global__ void __launch_bounds__(256) incr_kernel(IncrArgs<T> a) {
-  using S = IncrShape<BM>;
-  constexpr int BN = S::BN, TR = S::TR, TC = S::TC;
-  constexpr int THC = BN / TC;
-  static_assert((BM / TR) * THC == 256, "thread tile");
-  __shared__ __align__(16) T Ds[kIncRC][BM];
-  __shared__ __align__(16) T Zs[kIncRC][BN];
-  const int ty = threadIdx.x / THC, tx = threadIdx.x % THC;
+size_t incr_smem_bytes() { return sizeof(T) * 2 * (size_t)kIncRC * (BM + kIncBN); }
+
+template <typename T, int BM>
+__global__ void __launch_bounds__(BM * 4) incr_kernel(IncrArgs<T> a) {
+  constexpr int NT = BM * 4;                    // threads: BM/8 warps
+  constexpr int BN = kIncBN;
+  constexpr int VE = 16 / (int)sizeof(T);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* Ds = reinterpret_cast<T*>(smem_raw);       // [2][RC][BM]
+  T* Zs = Ds + 2 * kIncRC * BM;                 // [2][RC][BN]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q0 = warp * 8, c0 = lane * 4;
   const int j0 = blockIdx.x * BN;
   const int64_t rb0 = (int64_t)blockIdx.y * a.rows_per_split;
   const int64_t re = rb0 + a.rows_per_split < a.m ? rb0 + a.rows_per_split : a.m;
   const int kp = a.kp;
   const int nA = a.n - a.k0;
-  float acc32[TR][TC];
-  double acc64[TR][TC];
+  const bool vec = a.vec_ok;
+
+  // per-thread copy slots of the Z stage: fixed column -> fixed source base and row stride
+  constexpr int ZS = kIncRC * (BN / VE) / NT;
+  const T* zsrc[ZS];
+  int64_t zld[ZS];
 #pragma unroll
-  for (int i = 0; i < TR; ++i)
-#pragma unroll
-    for (int j = 0; j < TC; ++j) { acc32[i][j] = 0.f; acc64[i][j] = 0.0; }
-  int stage = 0;
-  for (int64_t rb = rb0; rb < re; rb += kIncRC) {
-    // Delta rows (BM wide; columns >= kp are zero)
-    for (int idx = threadIdx.x; idx < kIncRC * BM; idx += 256) {
-      const int rr = idx / BM, l = idx % BM;
+  for (int e = 0; e < ZS; ++e) {
+    const int idx = threadIdx.x + e * NT;
+    const int zc = j0 + (idx % (BN / VE)) * VE;
+    zsrc[e] = nullptr;
+    zld[e] = 0;
+    if (zc < nA) { zsrc[e] = a.A + a.k0 + zc; zld[e] = a.lda; }
+    else if (zc < nA + kp) { zsrc[e] = a.Xold + (zc - nA); zld[e] = kp; }
+    else if (zc < nA + 2 * kp) { zsrc[e] = a.Dnew + (zc - nA - kp); zld[e] = kp; }
+  }
+  auto issue = [&](int64_t rb, int st) {
+    T* ds = Ds + st * kIncRC * BM;
+    for (int idx = threadIdx.x; idx < kIncRC * (BM / VE); idx += NT) {
+      const int rr = idx / (BM / VE), lv = (idx % (BM / VE)) * VE;
       const int64_t row = rb + rr;
-      T d = T(0);
-      if (row < re && l < kp) d = a.Xnew[row * kp + l] - a.Xold[row * kp + l];
-      Ds[rr][l] = d;
+      const bool in = row < re && lv < kp;
+      cp_async16(ds + rr * BM + lv, in ? a.Dnew + row * kp + lv : a.Dnew, in ? 16 : 0);
     }
-    // Z = [A(:, k0:n) | X1_p | Delta] columns j0 .. j0+BN
-    for (int idx = threadIdx.x; idx < kIncRC * (BN / 4); idx += 256) {
-      const int rr = idx / (BN / 4), c4 = (idx % (BN / 4)) * 4;
-      const int64_t row = rb + rr;
-      const int zc = j0 + c4;
-      T v[4] = {T(0), T(0), T(0), T(0)};
-      if (row < re) {
-        if (a.vec_ok && zc + 4 <= nA) {
-          load_vec4_or_scalar<T>(a.A + row * a.lda + a.k0 + zc, true, v, 4);
-        } else {
+    T* zs = Zs + st * kIncRC * BN;
+    if (vec) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int c = zc + q;
-            if (c < nA) v[q] = a.A[row * a.lda + a.k0 + c];
-            else if (c < nA + kp) v[q] = a.Xold[row * kp + (c - nA)];
-            else if (c < nA + 2 * kp) v[q] = a.Xnew[row * kp + (c - nA - kp)] - a.Xold[row * kp + (c - nA - kp)];
+      for (int e = 0; e < ZS; ++e) {
+        const int idx = threadIdx.x + e * NT;
+        const int rr = idx / (BN / VE), cv = (idx % (BN / VE)) * VE;
+        const int64_t row = rb + rr;
+        const bool in = zsrc[e] != nullptr && row < re;
+        cp_async16(zs + rr * BN + cv, in ? zsrc[e] + row * zld[e] : a.A, in ? 16 : 0);
+      }
+    } else {
+      for (int idx = threadIdx.x; idx < kIncRC * (BN / VE); idx += NT) {
+        const int rr = idx / (BN / VE), cv = (idx % (BN / VE)) * VE;
+        const int64_t row = rb + rr;
+        const int zc = j0 + cv;
+        T* dst = zs + rr * BN + cv;
+#pragma unroll
+        for (int q = 0; q < VE; ++q) {
+          const int c = zc + q;
+          T v = T(0);
+          if (row < re) {
+            if (c < nA) v = a.A[row * a.lda + a.k0 + c];
+            else if (c < nA + kp) v = a.Xold[row * kp + (c - nA)];
+            else if (c < nA + 2 * kp) v = a.Dnew[row * kp + (c - nA - kp)];
           }
+          dst[q] = v;
         }
       }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) Zs[rr][c4 + q] = v[q];
     }
-    __syncthreads();
-#pragma unroll 4
-    for (int rr = 0; rr < kIncRC; ++rr) {
-      T dv[TR], zv[TC];
+  };
+
+  T acc[8][4];
 #pragma unroll
-      for (int i = 0; i < TR; ++i) dv[i] = Ds[rr][ty * TR + i];
+  for (int i = 0; i < 8; ++i)
 #pragma unroll
-      for (int j = 0; j < TC; ++j) zv[j] = Zs[rr][tx * TC + j];
-      if constexpr (sizeof(T) == 8) {
+    for (int j = 0; j < 4; ++j) acc[i][j] = T(0);
+  double* out = a.part + (int64_t)blockIdx.y * a.k * a.nz;
+  bool first = true;
+  // fp32 chunk sums are added into this CTA's fp64 partial (fixed order)
+  auto flush = [&]() {
 #pragma unroll
-        for (int i = 0; i < TR; ++i)
+    for (int i = 0; i < 8; ++i) {
+      const int l = q0 + i;
 #pragma unroll
-          for (int j = 0; j < TC; ++j) acc64[i][j] = fma((double)dv[i], (double)zv[j], acc64[i][j]);
-      } else {
-#pragma unroll
-        for (int i = 0; i < TR; ++i)
-#pragma unroll
-          for (int j = 0; j < TC; ++j) acc32[i][j] = fmaf((float)dv[i], (float)zv[j], acc32[i][j]);
+      for (int j = 0; j < 4; ++j) {
+        const int zc = j0 + c0 + j;
+        if (l < a.k && zc < a.nz) {
+          double* o = out + (int64_t)l * a.nz + zc;
+          *o = first ? (double)acc[i][j] : *o + (double)acc[i][j];
+        }
+        acc[i][j] = T(0);
       }
     }
+    first = false;
+  };
+  const int nst = (int)ceil_div(re - rb0, kIncRC);
+  if (nst > 0) {
+    issue(rb0, 0);
+    cp_async_commit();
+  }
+  int stage = 0;
+  for (int s = 0; s < nst; ++s) {
+    const int st = s & 1;
+    if (s + 1 < nst) issue(rb0 + (int64_t)(s + 1) * kIncRC, st ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
     __syncthreads();
-    if (++stage == kIncSuper) {
+    const T* ds = Ds + st * kIncRC * BM;
+    const T* zs = Zs + st * kIncRC * BN;
+#pragma unroll 4
+    for (int rr = 0; rr < kIncRC; ++rr) {
+      T dv[8], zv[4];
+      lds_vec<T, 8>(ds + rr * BM + q0, dv);
+      lds_vec<T, 4>(zs + rr * BN + c0, zv);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(dv[i], zv[j], acc[i][j]);
+    }
+    if (sizeof(T) == 4 && ++stage == kIncFlush && s + 1 < nst) {
       stage = 0;
-#pragma unroll
-      for (int i = 0; i < TR; ++i)
-#pragma unroll
-        for (int j = 0; j < TC; ++j) { acc64[i][j] += (double)acc32[i][j]; acc32[i][j] = 0.f; }
+      flush();
     }
+    __syncthreads();
   }
-  double* out = a.part + (int64_t)blockIdx.y * a.k * a.nz;
-#pragma unroll
-  for (int i = 0; i < TR; ++i) {
-    const int l = ty * TR + i;
-    if (l >= a.k) continue;
-#pragma unroll
-    for (int j = 0; j < TC; ++j) {
-      const int zc = j0 + tx * TC + j;
-      if (zc < a.nz) out[(int64_t)l * a.nz + zc] = acc64[i][j] + (double)acc32[i][j];
-    }
+  flush();
+}
+
+template <typename T, int BM>
+static cudaError_t launch_incr_bm(const IncrArgs<T>& a, cudaStream_t st) {
+  auto kern = incr_kernel<T, BM>;
+  const size_t smem = incr_smem_bytes<T, BM>();
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
   }
+  dim3 grid((unsigned)ceil_div(a.nz, kIncBN), (unsigned)a.nsplit);
+  kern<<<grid, BM * 4, smem, st>>>(a);
+  return cudaGetLastError();
 }
 
 template <typename T>
 cudaError_t launch_incr(const IncrArgs<T>& a, int bm, cudaStream_t st) {
-  const int bn = incr_bn(bm);
-  dim3 grid((unsigned)ceil_div(a.nz, bn), (unsigned)a.nsplit);
   switch (bm) {
-    case 16: incr_kernel<T, 16><<<grid, 256, 0, st>>>(a); break;
-    case 32: incr_kernel<T, 32><<<grid, 256, 0, st>>>(a); break;
-    case 64: incr_kernel<T, 64><<<grid, 256, 0, st>>>(a); break;
-    case 128: incr_kernel<T, 128><<<grid, 256, 0, st>>>(a); break;
+    case 32: return launch_incr_bm<T, 32>(a, st);
+    case 64: return launch_incr_bm<T, 64>(a, st);
+    case 128: return launch_incr_bm<T, 128>(a, st);
     default: return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
 }
 template cudaError_t launch_incr<float>(const IncrArgs<float>&, int, cudaStream_t);
 template cudaError_t launch_incr<double>(const IncrArgs<double>&, int, cudaStream_t);
 
 // ------------------------------------------------------------------------------ K2c
-// inc = [N (k x nk) | Gamma (k x k) | Omega (k x k) | f_w]
+// inc = [N (k x nk) | Gamma (k x k) | Omega (k x k) | f_w]; thread per output, the split
+// partials summed in fixed order with 8 independent loads in flight.
 __global__ void reduce_incr_kernel(const double* __restrict__ part, int nsplit, int k, int nk,
                                    int nz, int kshift, int nA, int kp,
                                    const double* __restrict__ fw_part, int nfw,
                                    double* __restrict__ inc) {
+  // 8 lanes per output: lane g sums the splits p = g (mod 8) in order, then a fixed
+  // shuffle tree combines the 8 sums (deterministic)
   const int64_t nN = (int64_t)k * nk, nG = (int64_t)k * k;
   const int64_t tot = nN + 2 * nG;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int l, zc;
-    if (i < nN) { l = (int)(i / nk); zc = (int)(i % nk) + kshift; }
-    else if (i < nN + nG) { const int64_t q = i - nN; l = (int)(q / k); zc = nA + (int)(q % k); }
-    else { const int64_t q = i - nN - nG; l = (int)(q / k); zc = nA + kp + (int)(q % k); }
+  const int64_t stride = (int64_t)k * nz;
+  const int g = threadIdx.x & 7;
+  const int64_t per_block = blockDim.x / 8;
+  for (int64_t i0 = blockIdx.x * per_block; i0 < tot; i0 += (int64_t)gridDim.x * per_block) {
+    const int64_t i = i0 + threadIdx.x / 8;
     double s = 0.0;
-    for (int p = 0; p < nsplit; ++p) s += part[((int64_t)p * k + l) * nz + zc];
-    inc[i] = s;
+    if (i < tot) {
+      int l, zc;
+      if (i < nN) { l = (int)(i / nk); zc = (int)(i % nk) + kshift; }
+      else if (i < nN + nG) { const int64_t q = i - nN; l = (int)(q / k); zc = nA + (int)(q % k); }
+      else { const int64_t q = i - nN - nG; l = (int)(q / k); zc = nA + kp + (int)(q % k); }
+      const double* src = part + (int64_t)l * nz + zc;
+      int p = g;
+      for (; p + 24 < nsplit; p += 32) {
+        const double v0 = __ldg(src + (int64_t)p * stride), v1 = __ldg(src + (int64_t)(p + 8) * stride);
+        const double v2 = __ldg(src + (int64_t)(p + 16) * stride), v3 = __ldg(src + (int64_t)(p + 24) * stride);
+        s += v0; s += v1; s += v2; s += v3;
+      }
+      for (; p < nsplit; p += 8) s += __ldg(src + (int64_t)p * stride);
+    }
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    if (g == 0 && i < tot) inc[i] = s;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
     double s = 0.0;
-    for (int p = 0; p < nfw; ++p) s += fw_part[p];
-    inc[tot] = s;
+    for (int p = threadIdx.x; p < nfw; p += 32) s += fw_part[p];
+    s = warp_sum(s);                      // fixed lane order -> deterministic
+    if (threadIdx.x == 0) inc[tot] = s;
   }
 }
 
 void launch_reduce_incr(const double* part, int nsplit, int k, int nk, int nz, int kshift, int nA,
                         int kp, const double* fw_part, int nfw, double* inc, cudaStream_t st) {
   const int64_t tot = (int64_t)k * nk + 2LL * k * k;
-  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(tot, 256), 1184));
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(tot, 32), 4096));
   reduce_incr_kernel<<<blocks, 256, 0, st>>>(part, nsplit, k, nk, nz, kshift, nA, kp, fw_part, nfw, inc);
 }
 

@@ -6,7 +6,7 @@
 namespace wlr {
 
 #define WLR_SS_EXTERN(B)                                                                   \
-  extern template cudaError_t launch_ss<B>(const SmallArgs&, cudaStream_t);                 \
+  extern template cudaError_t launch_ss<B>(const SmallArgs&, int, cudaStream_t);            \
   extern template int ss_max_clusters<B>(int, size_t);
 WLR_SS_EXTERN(4)
 WLR_SS_EXTERN(8)
@@ -89,14 +89,14 @@ int small_step_cluster_size(SmallArgs& a) {
   return 0;
 }
 
-cudaError_t launch_small_step(const SmallArgs& a, cudaStream_t st) {
+cudaError_t launch_small_step(const SmallArgs& a, int part, cudaStream_t st) {
   switch (bt_of(a.b)) {
-    case 4: return launch_ss<4>(a, st);
-    case 8: return launch_ss<8>(a, st);
-    case 12: return launch_ss<12>(a, st);
-    case 16: return launch_ss<16>(a, st);
-    case 24: return launch_ss<24>(a, st);
-    default: return launch_ss<32>(a, st);
+    case 4: return launch_ss<4>(a, part, st);
+    case 8: return launch_ss<8>(a, part, st);
+    case 12: return launch_ss<12>(a, part, st);
+    case 16: return launch_ss<16>(a, part, st);
+    case 24: return launch_ss<24>(a, part, st);
+    default: return launch_ss<32>(a, part, st);
   }
 }
 

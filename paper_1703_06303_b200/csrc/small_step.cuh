@@ -34,6 +34,8 @@ namespace cg = cooperative_groups;
 
 namespace wlr {
 
+#define WLR_NOINL static __device__ __noinline__
+
 constexpr int kSST = 512;            // threads per CTA
 constexpr int kSSW = kSST / 32;      // warps per CTA
 constexpr double kEps = 2.220446049250313e-16;
@@ -83,27 +85,31 @@ WLR_DEVI void tmark(SS& s, const SmallArgs& a) {
 
 WLR_DEVI double* xpart(SS& s, const SSPlan& p) { return s.sm + p.oPart + (int64_t)s.bank * p.PL; }
 
-// Fixed-order cluster sum of the len-long partial every CTA wrote into xpart(); out is local.
-WLR_DEVI void xreduce(SS& s, const SSPlan& p, int len, double* out) {
+// Fixed-order cluster sum of the len-long partial every CTA wrote into its exchange bank;
+// out is local.  (Arguments by value: this is a shared, non-inlined routine.)
+WLR_NOINL void xreduce_impl(const double* mine, int CL, int len, double* out) {
   cg::cluster_group cl = cg::this_cluster();
   cl.sync();
-  const double* mine = xpart(s, p);
+#pragma unroll 1
   for (int i = threadIdx.x; i < len; i += kSST) {
     double v[16];
 #pragma unroll
-    for (int c = 0; c < 16; ++c) v[c] = c < s.CL ? cl.map_shared_rank(mine, c)[i] : 0.0;
+    for (int c = 0; c < 16; ++c) v[c] = c < CL ? cl.map_shared_rank(mine, c)[i] : 0.0;
     double acc = 0.0;
 #pragma unroll
     for (int c = 0; c < 16; ++c) acc += v[c];
     out[i] = acc;
   }
   __syncthreads();
+}
+WLR_DEVI void xreduce(SS& s, const SSPlan& p, int len, double* out) {
+  xreduce_impl(xpart(s, p), s.CL, len, out);
   s.bank ^= 1;
 }
 
 // block reduction of NV values per thread (sum; result valid on all threads)
 template <int NV>
-WLR_DEVI void block_sum_n(double (&v)[NV], double* red) {
+WLR_NOINL void block_sum_n(double (&v)[NV], double* red) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
   for (int u = 0; u < NV; ++u) v[u] = warp_sum(v[u]);
@@ -121,7 +127,7 @@ WLR_DEVI void block_sum_n(double (&v)[NV], double* red) {
   __syncthreads();
 }
 
-WLR_DEVI double block_max(double v, double* red) {
+WLR_NOINL double block_max(double v, double* red) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -135,14 +141,16 @@ WLR_DEVI double block_max(double v, double* red) {
 }
 
 // C[r][c] = alpha * sum_q A[r*lda + q] B[q*ldb + c] (+ I if addI), thread per output.
-WLR_DEVI void gemm_nn(int m, int n, int kk, const double* A, int lda, const double* B, int ldb,
+WLR_NOINL void gemm_nn(int m, int n, int kk, const double* A, int lda, const double* B, int ldb,
                       double* C, int ldc, double alpha, bool addI) {
+  #pragma unroll 1
   for (int o = threadIdx.x; o < m * n; o += kSST) {
     const int r = o / n, c = o - r * n;
     const double* pa = A + (int64_t)r * lda;
     const double* pb = B + c;
     double v0 = 0.0, v1 = 0.0;
     int q = 0;
+    #pragma unroll 1
     for (; q + 1 < kk; q += 2) {
       v0 = fma(pa[q], pb[(int64_t)q * ldb], v0);
       v1 = fma(pa[q + 1], pb[(int64_t)(q + 1) * ldb], v1);
@@ -163,10 +171,11 @@ struct TN {
   double* out;
 };
 template <int ND>
-WLR_DEVI void slice_tn(int nl, const TN (&d)[ND]) {
+WLR_NOINL void slice_tn(int nl, const TN (&d)[ND]) {
   int tot = 0;
 #pragma unroll
   for (int u = 0; u < ND; ++u) tot += d[u].nrow * d[u].ncol;
+  #pragma unroll 1
   for (int o = threadIdx.x; o < tot; o += kSST) {
     int u = 0, base = 0;
 #pragma unroll
@@ -178,6 +187,7 @@ WLR_DEVI void slice_tn(int nl, const TN (&d)[ND]) {
     const double* pb = g.B + (int64_t)c * g.bcs;
     double v0 = 0.0, v1 = 0.0;
     int i = 0;
+    #pragma unroll 1
     for (; i + 1 < nl; i += 2) {
       v0 = fma(pa[(int64_t)i * g.ais], pb[(int64_t)i * g.bis], v0);
       v1 = fma(pa[(int64_t)(i + 1) * g.ais], pb[(int64_t)(i + 1) * g.bis], v1);
@@ -190,19 +200,24 @@ WLR_DEVI void slice_tn(int nl, const TN (&d)[ND]) {
 // In-place inverse of the SPD n x n matrix A (row-major) by the sweep operator (symmetric
 // Gauss-Jordan), whole CTA.  Returns false (uniformly) if a pivot is not > rel * its
 // original diagonal (numerical rank test, reading R6b).  Init / fallback only.
-WLR_DEVI bool sweep_inverse(double* A, int n, double rel, double* d0, double* rb) {
+WLR_NOINL bool sweep_inverse(double* A, int n, double rel, double* d0, double* rb) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  #pragma unroll 1
   for (int i = threadIdx.x; i < n; i += kSST) d0[i] = A[(int64_t)i * n + i];
   __syncthreads();
+  #pragma unroll 1
   for (int j = 0; j < n; ++j) {
     double* rj = rb + (j & 1) * (n + 8);       // double-buffered pivot row
+    #pragma unroll 1
     for (int i = threadIdx.x; i < n; i += kSST) rj[i] = A[(int64_t)j * n + i];
     __syncthreads();
     const double p = rj[j];
     if (!(p > rel * d0[j]) || !(p > 0.0) || !isfinite(p)) return false;
     const double pinv = 1.0 / p;
+    #pragma unroll 1
     for (int i = warp; i < n; i += kSSW) {
       const double ri = rj[i] * pinv;
+      #pragma unroll 1
       for (int l = lane; l < n; l += 32) {
         double v;
         if (i == j) v = (l == j) ? -pinv : rj[l] * pinv;
@@ -213,6 +228,7 @@ WLR_DEVI bool sweep_inverse(double* A, int n, double rel, double* d0, double* rb
     }
     __syncthreads();
   }
+  #pragma unroll 1
   for (int idx = threadIdx.x; idx < n * n; idx += kSST) A[idx] = -A[idx];
   __syncthreads();
   return true;
@@ -222,14 +238,16 @@ WLR_DEVI bool sweep_inverse(double* A, int n, double rel, double* d0, double* rb
 // R = I - G X, X <- X + X R.  Returns false (uniformly) when max|I - G X| >= 3e-2 (the
 // warm start is too far: the caller falls back to the sweep).  The number of steps is
 // chosen from the initial residual so that delta^(2^steps) <= 1e-12.
-WLR_DEVI bool ns_inverse(const double* G, double* X, double* R, double* P, int n, double* red) {
+WLR_NOINL bool ns_inverse(const double* G, double* X, double* R, double* P, int n, double* red) {
   gemm_nn(n, n, n, G, n, X, n, R, n, -1.0, true);
   __syncthreads();
   double dm = 0.0;
+  #pragma unroll 1
   for (int idx = threadIdx.x; idx < n * n; idx += kSST) dm = fmax(dm, fabs(R[idx]));
   const double delta = block_max(dm, red);
   if (!(delta < 3e-2)) return false;
   const int steps = delta < 1e-6 ? 1 : delta < 1e-3 ? 2 : 3;
+  #pragma unroll 1
   for (int st = 0; st < steps; ++st) {
     if (st > 0) {
       gemm_nn(n, n, n, G, n, X, n, R, n, -1.0, true);
@@ -237,9 +255,11 @@ WLR_DEVI bool ns_inverse(const double* G, double* X, double* R, double* P, int n
     }
     gemm_nn(n, n, n, X, n, R, n, P, n, 1.0, false);
     __syncthreads();
+    #pragma unroll 1
     for (int idx = threadIdx.x; idx < n * n; idx += kSST) X[idx] += P[idx];
     __syncthreads();
   }
+  #pragma unroll 1
   for (int idx = threadIdx.x; idx < n * n; idx += kSST) {   // symmetrise
     const int i = idx / n, j = idx - i * n;
     if (i < j) {
@@ -254,10 +274,11 @@ WLR_DEVI bool ns_inverse(const double* G, double* X, double* R, double* P, int n
 
 // Cholesky of the small n x n SPD matrix A (smem, ld 32) by warp 0 (lower factor in place);
 // dinv[j] = 1 / L_jj.  Returns (uniformly, after a block barrier) true iff SPD.
-WLR_DEVI bool chol_small(double* A, int n, double* dinv, int* ok_s) {
+WLR_NOINL bool chol_small(double* A, int n, double* dinv, int* ok_s) {
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
     bool ok = true;
+    #pragma unroll 1
     for (int j = 0; j < n; ++j) {
       const double d = A[j * 32 + j];
       ok = ok && (d > 0.0) && isfinite(d);
@@ -269,6 +290,7 @@ WLR_DEVI bool chol_small(double* A, int n, double* dinv, int* ok_s) {
       if (i < n) { lij = A[i * 32 + j] * r; A[i * 32 + j] = lij; }
       __syncwarp();
       if (i < n)
+        #pragma unroll 1
         for (int l = j + 1; l <= i; ++l) A[i * 32 + l] = fma(-lij, A[l * 32 + j], A[i * 32 + l]);
       __syncwarp();
     }
@@ -279,14 +301,17 @@ WLR_DEVI bool chol_small(double* A, int n, double* dinv, int* ok_s) {
 }
 
 // Li = L^{-1} (lower triangular, ld 32), column c by lane c of warp 0.
-WLR_DEVI void tri_inverse(const double* L, const double* dinv, int n, double* Li) {
+WLR_NOINL void tri_inverse(const double* L, const double* dinv, int n, double* Li) {
   if (threadIdx.x < 32) {
     const int c = threadIdx.x;
     if (c < n) {
+      #pragma unroll 1
       for (int i = 0; i < c; ++i) Li[i * 32 + c] = 0.0;
       Li[c * 32 + c] = dinv[c];
+      #pragma unroll 1
       for (int i = c + 1; i < n; ++i) {
         double v = 0.0;
+        #pragma unroll 1
         for (int m = c; m < i; ++m) v = fma(L[i * 32 + m], Li[m * 32 + c], v);
         Li[i * 32 + c] = -v * dinv[i];
       }
@@ -299,18 +324,23 @@ WLR_DEVI void tri_inverse(const double* L, const double* dinv, int n, double* Li
 // on exit th = eigenvalues in DESCENDING order and U (ld 32) the matching orthonormal
 // eigenvectors (columns).  b/2 disjoint rotations per round, b-1 rounds per sweep; stops
 // when every off-diagonal is at rounding level.  Deterministic.
-WLR_DEVI void jacobi_par(double* T, double* U, double* th, double* cs, int b) {
+WLR_NOINL void jacobi_par(double* T, double* U, double* th, double* cs, int b) {
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
     const int nb = (b + 1) & ~1;
     const int np = nb / 2;
+    #pragma unroll 1
     for (int i = lane; i < b; i += 32)
+      #pragma unroll 1
       for (int j = 0; j < b; ++j) U[i * 32 + j] = (i == j) ? 1.0 : 0.0;
     double dmax = 0.0;
+    #pragma unroll 1
     for (int i = 0; i < b; ++i) dmax = fmax(dmax, fabs(T[i * 32 + i]));
     const double tabs = 2e-15 * dmax;
     __syncwarp();
+    #pragma unroll 1
     for (int sweep = 0; sweep < 30 && nb > 1; ++sweep) {
+      #pragma unroll 1
       for (int rnd = 0; rnd < nb - 1; ++rnd) {
         // rotation parameters of pair (lane) from the current T
         if (lane < np) {
@@ -333,6 +363,7 @@ WLR_DEVI void jacobi_par(double* T, double* U, double* th, double* cs, int b) {
         }
         __syncwarp();
         // rows:  T <- J^T T
+        #pragma unroll 1
         for (int idx = lane; idx < np * b; idx += 32) {
           const int kq = idx / b, j = idx - kq * b;
           const int q = (int)cs[4 * kq + 3];
@@ -346,6 +377,7 @@ WLR_DEVI void jacobi_par(double* T, double* U, double* th, double* cs, int b) {
         }
         __syncwarp();
         // columns: T <- T J, U <- U J
+        #pragma unroll 1
         for (int idx = lane; idx < np * b; idx += 32) {
           const int kq = idx / b, i = idx - kq * b;
           const int q = (int)cs[4 * kq + 3];
@@ -364,6 +396,7 @@ WLR_DEVI void jacobi_par(double* T, double* U, double* th, double* cs, int b) {
       }
       // converged when every off-diagonal is at rounding level
       bool big = false;
+      #pragma unroll 1
       for (int idx = lane; idx < b * b; idx += 32) {
         const int i = idx / b, j = idx - i * b;
         if (i != j) {
@@ -376,16 +409,20 @@ WLR_DEVI void jacobi_par(double* T, double* U, double* th, double* cs, int b) {
     // sort descending (stable by index) and permute U's columns
     double wj = lane < b ? T[lane * 32 + lane] : 0.0;
     int rk = 0;
+    #pragma unroll 1
     for (int i = 0; i < b; ++i) {
       const double wi = T[i * 32 + i];
       if (wi > wj || (wi == wj && i < lane)) ++rk;
     }
     __syncwarp();
     if (lane < b) th[rk] = wj;
+    #pragma unroll 1
     for (int i = lane; i < b; i += 32)                          // T is free now
+      #pragma unroll 1
       for (int j = 0; j < b; ++j) T[i * 32 + j] = U[i * 32 + j];
     __syncwarp();
     if (lane < b)
+      #pragma unroll 1
       for (int i = 0; i < b; ++i) U[i * 32 + rk] = T[i * 32 + lane];
   }
   __syncthreads();
@@ -398,13 +435,17 @@ WLR_DEVI void jacobi_par(double* T, double* U, double* th, double* cs, int b) {
 // rows (i = lane, lane + 32; nl <= 64).  G_A is symmetric, so G_A[rs + i][l] is read as
 // G_A[l][rs + i] (coalesced).  Fixed-order sums.
 template <int PW>
-WLR_DEVI void s_product(SS& s, const SmallArgs& a, int64_t xoff, int ldx, int w,
-                        const double* Wk, const double* Mp, int ldm, double* Z, int ldz) {
-  const SSPlan& p = a.pl;
+WLR_DEVI void s_product_impl(double* smb, int rs, int nl, int SL, int k, int nk, int KS, int JS,
+                              int64_t oRed, int64_t oXf, const double* GA, int64_t xoff, int ldx,
+                              int w, const double* Wk, const double* Mp, int ldm, double* Z,
+                              int ldz) {
+  struct { int rs, nl, SL, k, nk; double* sm; } s = {rs, nl, SL, k, nk, smb};
+  struct { int KS, JS; } p = {KS, JS};
   cg::cluster_group cl = cg::this_cluster();
-  double* Red = s.sm + p.oRed;
-  double* Xf = p.oXf >= 0 ? s.sm + p.oXf : nullptr;
+  double* Red = s.sm + oRed;
+  double* Xf = oXf >= 0 ? s.sm + oXf : nullptr;
   if (Xf) {
+    #pragma unroll 1
     for (int idx0 = threadIdx.x; idx0 < s.nk * w; idx0 += 4 * kSST) {
       double v[4];
 #pragma unroll
@@ -436,9 +477,10 @@ WLR_DEVI void s_product(SS& s, const SmallArgs& a, int64_t xoff, int ldx, int w,
 #pragma unroll
   for (int j = 0; j < PW; ++j) { acc0[j] = 0.0; acc1[j] = 0.0; }
   if (wj > 0) {
-    const double* gcol = a.GA + s.rs;
+    const double* gcol = GA + s.rs;
     const int lg = min(l1, s.nk);
     constexpr int U = 8;                          // G_A loads in flight per lane
+    #pragma unroll 1
     for (int lb = l0; lb < lg; lb += U) {
       double g0[U], g1[U];
 #pragma unroll
@@ -470,6 +512,7 @@ WLR_DEVI void s_product(SS& s, const SmallArgs& a, int64_t xoff, int ldx, int w,
         }
       }
     }
+    #pragma unroll 1
     for (int l = max(l0, s.nk); l < l1; ++l) {
       const int q = l - s.nk;
       const double m0 = has0 ? Mp[(int64_t)q * ldm + lane] : 0.0;
@@ -495,13 +538,22 @@ WLR_DEVI void s_product(SS& s, const SmallArgs& a, int64_t xoff, int ldx, int w,
   }
   __syncthreads();
   const int nks = (KT + kc - 1) / kc;             // chunks that exist (ks >= nks are empty)
+  #pragma unroll 1
   for (int idx = threadIdx.x; idx < s.nl * w; idx += kSST) {
     const int i = idx / w, j = idx - i * w;
     double v = 0.0;
+    #pragma unroll 1
     for (int q = 0; q < nks; ++q) v += Red[((int64_t)q * s.SL + i) * w + j];
     Z[i * ldz + j] = v;
   }
   __syncthreads();
+}
+
+template <int PW>
+WLR_DEVI void s_product(SS& s, const SmallArgs& a, int64_t xoff, int ldx, int w,
+                        const double* Wk, const double* Mp, int ldm, double* Z, int ldz) {
+  s_product_impl<PW>(s.sm, s.rs, s.nl, s.SL, s.k, s.nk, a.pl.KS, a.pl.JS, a.pl.oRed, a.pl.oXf,
+                     a.GA, xoff, ldx, w, Wk, Mp, ldm, Z, ldz);
 }
 
 // One S-product of the basis X (local slice at offset xoff, width w = row stride):
@@ -520,7 +572,15 @@ WLR_DEVI void s_apply(SS& s, const SmallArgs& a, const double* Cs, int ldc, cons
   ++*nprod;
 }
 
-template <int BT>
+// ---------------------------------------------------------------------------------------
+// The kernel, in two parts (template PART):
+//   PART 1 (K3a, critical path): Gram update, G'^{-1}, C', eigenpairs of S, and the next row
+//          pass's operands (Wt, C V, K^{-1} or C C^T).  Writes V_{p+1}, Ritz values, R = V_p^T
+//          V_{p+1} and (V_p^T S V_{p+1})^T for PART 2.
+//   PART 2 (K3b, deferred): objective F_{p+1}, step norm, trace and stopping flag.  It only
+//          reads state that the next iteration's row pass and increment pass do not touch, so
+//          the library runs it on a second stream concurrently with them.
+template <int BT, int PART>
 __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_constant__ SmallArgs a) {
   constexpr int PW = BT <= 8 ? BT : (BT <= 16 ? (BT + 1) / 2 : (BT + 3) / 4);
   extern __shared__ __align__(16) double ss_smem[];
@@ -543,7 +603,6 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
   double* sm = s.sm + p.oSmall;
   const int64_t SLb = (int64_t)s.SL * b;
   const int64_t buf[4] = {p.oBuf, p.oBuf + SLb, p.oBuf + 2 * SLb, p.oBuf + 3 * SLb};
-  int iY = 0, iZ = 1, iA = 2, iB = 3;          // roles of the four slice buffers
   double* Vp = s.sm + p.oVp;                   // nl x t   V_p (previous V)
   double* Es = s.sm + p.oE;                    // nl x t   E = V' - V_p R
   double* SEs = s.sm + p.oSE;                  // nl x t   S_p E
@@ -557,520 +616,562 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
   const double* incN = a.inc;
   const double* incGam = a.inc + (int64_t)k * nk;
   const double* incOm = incGam + (int64_t)kk;
-  const double fw = a.mode ? incOm[(int64_t)kk] : a.inc[0];
-  // Newton-Schulz mats (G', X = inverse, R, P): smem or this CTA's global workspace
   double* Gq = p.oGsq >= 0 ? s.sm + p.oGsq : a.gws + (int64_t)s.c * p.gws_stride;
   double* Xq = Gq + kk;
   double* Rq = Xq + kk;
   double* Pq = Rq + kk;
-  int nprod = 0;
-
-  // ------------------------------------------------ A: Gram update, G'^{-1}, C', slices
-  // stage G_p, Gamma, Omega, C_p V_p (used again by the final phase) when planned
-  const bool ms3 = p.oMat3 >= 0 && a.mode;
-  double* mats = s.sm + (p.oMat3 >= 0 ? p.oMat3 : 0);
-  if (ms3) {
-    for (int idx = threadIdx.x; idx < kk; idx += kSST) {
-      mats[idx] = a.G_in[idx];
-      mats[kk + idx] = incGam[idx];
-      mats[2 * kk + idx] = incOm[idx];
-    }
-    for (int idx = threadIdx.x; idx < kt; idx += kSST) mats[3 * kk + idx] = a.CVprev[idx];
-  }
-  const double* Gm = ms3 ? mats : a.G_in;
-  const double* Gam = ms3 ? mats + kk : incGam;
-  const double* Om = ms3 ? mats + 2 * kk : incOm;
-  const double* CVp = ms3 ? mats + 3 * kk : a.CVprev;
-  for (int idx = threadIdx.x; idx < k * s.nl; idx += kSST) {
-    const int q = idx / s.nl, i = idx - q * s.nl;
-    const int64_t gi = (int64_t)q * nk + s.rs + i;
-    const double mv = a.mode ? a.M_in[gi] + incN[gi] : a.M_out[gi];
-    if (p.oMs >= 0) Ms[q * ldm + i] = mv;
-    if (a.mode) a.M_out[gi] = mv;
-    if (p.oCin >= 0 && a.mode) s.sm[p.oCin + q * s.SL + i] = a.C_in[gi];
-  }
-  for (int idx = threadIdx.x; idx < s.nl * b; idx += kSST) s.sm[buf[iY] + idx] = a.Y[(int64_t)s.rs * b + idx];
-  if (a.mode) {
-    for (int idx = threadIdx.x; idx < s.nl * t; idx += kSST) Vp[idx] = a.Vprev[(int64_t)s.rs * t + idx];
-    for (int idx = threadIdx.x; idx < kk; idx += kSST) Xq[idx] = a.Gi_in[idx];
-  }
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < kk; idx += kSST) {
-    const int i = idx / k, j = idx - i * k;
-    double g;
-    if (a.mode) {
-      g = Gm[idx] + Gam[i * k + j] + Gam[j * k + i] + 0.5 * (Om[i * k + j] + Om[j * k + i]);
-      if (s.c == 0) a.G_out[idx] = g;
-    } else {
-      g = a.G_out[idx];
-    }
-    Gq[idx] = g;
-  }
-  __syncthreads();
-  bool okinv = a.mode ? ns_inverse(Gq, Xq, Rq, Pq, k, red) : false;
-  if (!okinv) {
-    for (int idx = threadIdx.x; idx < kk; idx += kSST) Xq[idx] = Gq[idx];
-    __syncthreads();
-    if (!sweep_inverse(Xq, k, 256.0 * kEps, sm + so.d0, sm + so.rb)) {   // rank(X1) < k (R6)
-      if (s.c == 0 && threadIdx.x == 0) raise_flag(a.flags, DF_RANK);
-      return;                                  // uniform on every CTA; no barrier issued yet
-    }
-  }
-  if (s.c == 0)
-    for (int idx = threadIdx.x; idx < kk; idx += kSST) a.Gi_out[idx] = Xq[idx];
-  tmark(s, a);                                 // [1] Gram update + G'^{-1}
-  // C'[:, slice] = G'^{-1} M'[:, slice]
-  gemm_nn(k, s.nl, k, Xq, k, Ms, ldm, Cs, ldc, 1.0, false);
-  __syncthreads();
-  if (p.oCs >= 0)
-    for (int idx = threadIdx.x; idx < k * s.nl; idx += kSST) {
-      const int q = idx / s.nl, i = idx - q * s.nl;
-      a.C_out[(int64_t)q * nk + s.rs + i] = Cs[q * ldc + i];
-    }
-  tmark(s, a);                                 // [2] C'
-
-  // ------------------------------------------------ B: eigenpairs of S
-  const double floor_abs = 4.0 * kEps * sqrt((double)nk) * a.a2sq;   // S-product rounding floor
-  bool converged = false, failed = false;
-  int outer = 0;
-  double rmax = 0.0;
   double* Gx = sm + so.Gx;
   double* th = sm + so.th;
   double* Rt = sm + so.Rt;
-  double* dsc = sm + so.dsc;
-  double* rres = s.sm + p.oCinE;               // [res (t) | C_in E (k x t)]
-  bool ortho = !a.cold;                        // Y expected orthonormal (warm Ritz block)
-  while (true) {
-    // ---- Rayleigh-Ritz on span(Y):  Z = S Y;  Gyy = Y^T Y, Gyz = Y^T Z (generalised RR)
-    s_apply<PW>(s, a, Cs, ldc, Ms, ldm, buf[iY], b, buf[iZ], &nprod);
-    tmark(s, a);                               // product
-    {
-      const double* Y = s.sm + buf[iY];
-      const double* Z = s.sm + buf[iZ];
-      double* part = xpart(s, p);
-      const int tb = a.mode ? t : 0;
-      const TN d[4] = {{Y, 1, b, Y, 1, b, b, b, part},
-                       {Y, 1, b, Z, 1, b, b, b, part + b * b},
-                       {Vp, 1, t, Y, 1, b, tb, b, part + 2 * b * b},
-                       {Vp, 1, t, Z, 1, b, tb, b, part + 2 * b * b + t * b}};
-      slice_tn<4>(s.nl, d);
-      xreduce(s, p, 2 * b * b + 2 * tb * b, Gx);
-    }
-    tmark(s, a);                               // Gram exchange
-    // ---- local (every CTA identically): D = diag(Gyy)^-1/2; if D Gyy D = I to rounding
-    //      the block is orthonormal: T = D Gyz D, Q = D U.  Otherwise L L^T = D Gyy D,
-    //      T = L^-1 (D Gyz D) L^-T, Q = D L^-T U.
-    bool gen;
-    {
-      double* Lb = sm + so.Lb;
-      double* Li = sm + so.Li;
-      double* Tb = sm + so.Tb;
-      double* Ub = sm + so.Ub;
-      double* Qb = sm + so.Qb;
-      double* Wb = sm + so.Wb;
-      if (threadIdx.x < b) {
-        const double d = Gx[threadIdx.x * b + threadIdx.x];
-        dsc[threadIdx.x] = d > 0.0 ? rsqrt(d) : 1.0;
-      }
-      __syncthreads();
-      double dev = 0.0;
-      for (int idx = threadIdx.x; idx < b * b; idx += kSST) {
-        const int i = idx / b, j = idx - i * b;
-        const double di = dsc[i] * dsc[j];
-        const double g = 0.5 * (Gx[i * b + j] + Gx[j * b + i]) * di;
-        Lb[i * 32 + j] = g;
-        Wb[i * 32 + j] = 0.5 * (Gx[b * b + i * b + j] + Gx[b * b + j * b + i]) * di;
-        if (i != j) dev = fmax(dev, fabs(g));
-      }
-      dev = block_max(dev, red);
-      gen = !(ortho && dev < 1e-13);
-      if (gen) {
-        if (!chol_small(Lb, b, sm + so.rb, &ok_s)) { failed = true; break; }
-        tri_inverse(Lb, sm + so.rb, b, Li);
-        // Tb = Li Wb Li^T   (two small products; Ub as scratch)
-        for (int idx = threadIdx.x; idx < b * b; idx += kSST) {
-          const int i = idx / b, j = idx - i * b;
-          double v = 0.0;
-          for (int q = 0; q <= i; ++q) v = fma(Li[i * 32 + q], Wb[q * 32 + j], v);
-          Ub[i * 32 + j] = v;
-        }
-        __syncthreads();
-        for (int idx = threadIdx.x; idx < b * b; idx += kSST) {
-          const int i = idx / b, j = idx - i * b;
-          double v = 0.0;
-          for (int q = 0; q <= j; ++q) v = fma(Ub[i * 32 + q], Li[j * 32 + q], v);
-          Tb[i * 32 + j] = v;
-        }
-        __syncthreads();
-        for (int idx = threadIdx.x; idx < b * b; idx += kSST) {
-          const int i = idx / b, j = idx - i * b;
-          if (i < j) {
-            const double v = 0.5 * (Tb[i * 32 + j] + Tb[j * 32 + i]);
-            Tb[i * 32 + j] = v;
-            Tb[j * 32 + i] = v;
-          }
-        }
-      } else {
-        for (int idx = threadIdx.x; idx < b * b; idx += kSST) {
-          const int i = idx / b, j = idx - i * b;
-          Tb[i * 32 + j] = Wb[i * 32 + j];
-        }
-      }
-      __syncthreads();
-      jacobi_par(Tb, Ub, th, sm + so.cs, b);
-      // Qb = D (Li^T U)  or  D U
-      for (int idx = threadIdx.x; idx < b * b; idx += kSST) {
-        const int i = idx / b, j = idx - i * b;
-        double v;
-        if (gen) {
-          v = 0.0;
-          for (int q = i; q < b; ++q) v = fma(Li[q * 32 + i], Ub[q * 32 + j], v);
-        } else {
-          v = Ub[i * 32 + j];
-        }
-        Qb[i * b + j] = v * dsc[i];
-      }
-      __syncthreads();
-    }
-    tmark(s, a);                               // local RR
-    const double* Qb = sm + so.Qb;
-    // ---- rotate: Y' = Y Q, Z' = Z Q  (into the free buffers)
-    gemm_nn(s.nl, b, b, s.sm + buf[iY], b, Qb, b, s.sm + buf[iA], b, 1.0, false);
-    gemm_nn(s.nl, b, b, s.sm + buf[iZ], b, Qb, b, s.sm + buf[iB], b, 1.0, false);
-    {
-      const int oy = iY, oz = iZ;
-      iY = iA; iZ = iB; iA = oy; iB = oz;
-    }
-    if (a.mode)   // R = Vp^T V' = (Vp^T Y) Q[:, :t]
-      gemm_nn(t, t, b, Gx + 2 * b * b, b, Qb, b, Rt, t, 1.0, false);
-    __syncthreads();
-    // ---- residuals of the wanted pairs; E = V' - Vp R and its C_in E partial (final phase)
-    {
-      const double* Y = s.sm + buf[iY];
-      const double* Z = s.sm + buf[iZ];
-      double* part = xpart(s, p);
-      if (a.mode) {
-        for (int idx = threadIdx.x; idx < s.nl * t; idx += kSST) {
-          const int r = idx / t, j = idx - r * t;
-          double v = Y[r * b + j];
-          for (int q = 0; q < t; ++q) v = fma(-Vp[r * t + q], Rt[q * t + j], v);
-          Es[idx] = v;
-        }
-        __syncthreads();
-      }
-      for (int j = threadIdx.x; j < t; j += kSST) {
-        double v = 0.0;
-        for (int r = 0; r < s.nl; ++r) {
-          const double d = Z[r * b + j] - th[j] * Y[r * b + j];
-          v = fma(d, d, v);
-        }
-        part[j] = v;
-      }
-      if (a.mode) {
-        const TN d[1] = {{Cin, ldci, 1, Es, 1, t, k, t, part + t}};
-        slice_tn<1>(s.nl, d);
-      }
-      xreduce(s, p, t + (a.mode ? kt : 0), rres);
-    }
-    tmark(s, a);                               // residual exchange
-    rmax = 0.0;
-    for (int j = 0; j < t; ++j) rmax = fmax(rmax, sqrt(fmax(rres[j], 0.0)));
-    const double theta0 = th[0];
-    const double target = fmax(a.tol * fabs(theta0), floor_abs);
-    if (rmax <= target) { converged = true; break; }
-    if (++outer > a.max_outer) break;
-    // ---- Chebyshev filter of adaptive degree damping [0, theta_{b-1}]
-    const double beta = th[b - 1];
-    double cc = 0.5 * beta, ee = 0.5 * beta;
-    int d = 1;
-    if (!(beta > 1e-300 * fabs(theta0)) || beta >= th[t - 1]) {
-      cc = 0.0; ee = 1.0; d = 1;                // no gap inside the block: plain power step
-    } else {
-      const double x0 = (theta0 - cc) / ee, xt = (th[t - 1] - cc) / ee;
-      const double at = acosh(fmax(xt, 1.0)), a0 = acosh(fmax(x0, 1.0));
-      const double need = log(fmax(rmax / target, 1.0)) / fmax(at, 1e-6);
-      d = (int)ceil(need) + 1;
-      const int dcap = max(1, (int)(9.9 / fmax(a0, 1e-6)));   // amplification <= ~1e4
-      d = max(1, min(d, min(a.max_deg, dcap)));
-    }
-    const double einv = 1.0 / ee;
-    int i0 = iY, i1 = iA, iz = iZ, i3 = iB;     // P0 = Y, P1 = (Z - c Y)/e, scratch z, free
-    {
-      double* P1 = s.sm + buf[i1];
-      const double* Y = s.sm + buf[i0];
-      const double* Z = s.sm + buf[iz];
-      for (int idx = threadIdx.x; idx < s.nl * b; idx += kSST) P1[idx] = (Z[idx] - cc * Y[idx]) * einv;
-      __syncthreads();
-    }
-    for (int j = 2; j <= d; ++j) {
-      s_apply<PW>(s, a, Cs, ldc, Ms, ldm, buf[i1], b, buf[iz], &nprod);
-      double* pn = s.sm + buf[i0];             // P2 = 2 (S P1 - c P1)/e - P0, in place of P0
-      const double* pz = s.sm + buf[iz];
-      const double* p1 = s.sm + buf[i1];
-      for (int idx = threadIdx.x; idx < s.nl * b; idx += kSST)
-        pn[idx] = 2.0 * (pz[idx] - cc * p1[idx]) * einv - pn[idx];
-      __syncthreads();
-      const int tmp = i0; i0 = i1; i1 = tmp;
-    }
-    iY = i1; iZ = iz; iA = i0; iB = i3;
-    ortho = false;                             // filtered block: generalised Rayleigh-Ritz
-  }
-  if ((failed || !converged) && s.c == 0 && threadIdx.x == 0) raise_flag(a.flags, DF_EIG);
-  if (failed) {            // every CTA took the same decision; keep peers' smem alive
-    cg::this_cluster().sync();
-    return;
-  }
 
-  // ------------------------------------------------ C: objective, step norm, operands
-  const double* Y = s.sm + buf[iY];            // V' = Y[:, :t]
-  const double* CinE = rres + t;               // reduced C_in E (k x t)
-  if (a.mode)   // S_p E = G_A E - M_in^T (C_in E)   (old S; E distributed at offset oE, stride t)
-    s_product<PW>(s, a, p.oE, t, t, CinE, a.M_in + s.rs, nk, SEs, t);
-  tmark(s, a);                                 // old-S product
-  const FinOff fo(k, t);
-  double* my = a.xchg + (int64_t)s.c * p.flen;
-  {
-    // [0] <M',C'> [1] <C', H C_in> [2] <C', Om C'> [3] <C', Gam dC> [4] <dC, G dC>
-    double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  if constexpr (PART == 1) {
+    int iY = 0, iZ = 1, iA = 2, iB = 3;        // roles of the four slice buffers
+    int nprod = 0;
+    // ---------------------------------------------- A: Gram update, G'^{-1}, C', slices
     for (int idx = threadIdx.x; idx < k * s.nl; idx += kSST) {
-      const int l = idx / s.nl, i = idx - l * s.nl;
-      const double cn = Cs[(int64_t)l * ldc + i];
-      v[0] = fma(Ms[(int64_t)l * ldm + i], cn, v[0]);
-      if (a.mode) {
-        double hc = 0.0, omc = 0.0, gdc = 0.0, ggdc = 0.0;
-        for (int q = 0; q < k; ++q) {
-          const double co = Cin[(int64_t)q * ldci + i], cq = Cs[(int64_t)q * ldc + i];
-          const double dq = cq - co;
-          const double gam = Gam[l * k + q], gm = Gm[l * k + q];
-          hc = fma(gm + gam, co, hc);
-          omc = fma(0.5 * (Om[l * k + q] + Om[q * k + l]), cq, omc);
-          gdc = fma(gam, dq, gdc);
-          ggdc = fma(gm, dq, ggdc);
-        }
-        const double dl = cn - Cin[(int64_t)l * ldci + i];
-        v[1] = fma(cn, hc, v[1]);
-        v[2] = fma(cn, omc, v[2]);
-        v[3] = fma(cn, gdc, v[3]);
-        v[4] = fma(dl, ggdc, v[4]);
-      }
+      const int q = idx / s.nl, i = idx - q * s.nl;
+      const int64_t gi = (int64_t)q * nk + s.rs + i;
+      const double mv = a.mode ? a.M_in[gi] + incN[gi] : a.M_out[gi];
+      if (p.oMs >= 0) Ms[q * ldm + i] = mv;
+      if (a.mode) a.M_out[gi] = mv;
     }
-    block_sum_n<5>(v, red);
-    if (threadIdx.x == 0)
-      for (int u = 0; u < 5; ++u) my[u] = v[u];
-  }
-  {
-    // k x t, t x t and k x k slice contractions in one pass (zero rows when mode == 0)
-    const int km = a.mode ? k : 0, tm = a.mode ? t : 0;
-    const TN d[10] = {{Cs, ldc, 1, Vp, 1, t, km, t, my + fo.CnV},
-                      {Cs, ldc, 1, Y, 1, b, k, t, my + fo.CnVn},
-                      {Cin, ldci, 1, Y, 1, b, km, t, my + fo.CVn},
-                      {Ms, ldm, 1, Vp, 1, t, km, t, my + fo.MnV},
-                      {a.M_in + s.rs, nk, 1, Y, 1, b, km, t, my + fo.MVn},
-                      {incN + s.rs, nk, 1, Vp, 1, t, km, t, my + fo.NV},
-                      {Cs, ldc, 1, Es, 1, t, km, t, my + fo.CE},
-                      {Es, 1, t, Es, 1, t, tm, t, my + fo.EE},
-                      {Es, 1, t, SEs, 1, t, tm, t, my + fo.ESE},
-                      {Cs, ldc, 1, Cs, ldc, 1, k, k, my + fo.CC}};
-    slice_tn<10>(s.nl, d);
-    if (!a.mode)
-      for (int idx = threadIdx.x; idx < fo.CC; idx += kSST)
-        if (idx >= fo.CnV && (idx < fo.CnVn || idx >= fo.CnVn + kt)) my[idx] = 0.0;
-  }
-  // slice-local outputs: Wt rows [V' | C'^T | 0], V' into Vprev, Ritz block into Y
-  {
-    const int RP = a.rp;
-    for (int64_t idx = threadIdx.x; idx < (int64_t)s.nl * RP; idx += kSST) {
-      const int cl = (int)(idx / RP), j = (int)(idx % RP);
-      double v = 0.0;
-      if (j < t) v = Y[cl * b + j];
-      else if (j < t + k) v = Cs[(int64_t)(j - t) * ldc + cl];
-      const int64_t o = (int64_t)(k + s.rs + cl - a.k0) * RP + j;
-      if (a.dtype) reinterpret_cast<double*>(a.Wt)[o] = v;
-      else reinterpret_cast<float*>(a.Wt)[o] = (float)v;
+    for (int idx = threadIdx.x; idx < s.nl * b; idx += kSST) s.sm[buf[iY] + idx] = a.Y[(int64_t)s.rs * b + idx];
+    if (a.mode) {
+      for (int idx = threadIdx.x; idx < s.nl * t; idx += kSST) Vp[idx] = a.V_in[(int64_t)s.rs * t + idx];
+      for (int idx = threadIdx.x; idx < kk; idx += kSST) Xq[idx] = a.Gi_in[idx];
     }
-    for (int idx = threadIdx.x; idx < s.nl * t; idx += kSST) {
-      const int r = idx / t, j = idx - r * t;
-      a.Vprev[(int64_t)(s.rs + r) * t + j] = Y[r * b + j];
-    }
-    for (int idx = threadIdx.x; idx < s.nl * b; idx += kSST) a.Y[(int64_t)s.rs * b + idx] = Y[idx];
-  }
-  tmark(s, a);                                 // final partials
-  cg::this_cluster().sync();                   // partials in global memory (cluster scope)
-  {   // reduce-scatter: CTA c sums its chunk of the flen partials over the CL slots
-    const int64_t fc = (p.flen + s.CL - 1) / s.CL;
-    const int64_t f0 = (int64_t)s.c * fc, f1 = min((int64_t)p.flen, f0 + fc);
-    for (int64_t i = f0 + threadIdx.x; i < f1; i += kSST) {
-      double v[16];
-#pragma unroll
-      for (int c = 0; c < 16; ++c) v[c] = c < s.CL ? __ldcg(a.xchg + (int64_t)c * p.flen + i) : 0.0;
-      double acc = 0.0;
-#pragma unroll
-      for (int c = 0; c < 16; ++c) acc += v[c];
-      a.red[i] = acc;
-    }
-  }
-  cg::this_cluster().sync();
-  tmark(s, a);                                 // reduce-scatter
-  if (s.c != 0) return;
-
-  // ---- CTA 0: finish from the reduced partials (fixed order)
-  const bool rsm = p.oTail >= 0;
-  double* R = rsm ? s.sm + p.oTail : a.red;    // reduced partials (staged in smem if room)
-  if (rsm)
-    for (int i = threadIdx.x; i < p.flen; i += kSST) R[i] = __ldcg(a.red + i);
-  double* HCV = R + p.flen;                    // k x t
-  double* HCVn = HCV + kt;                     // k x t
-  double* Wm = HCVn + kt;                      // k x t
-  __syncthreads();
-  double sum_theta = 0.0;
-  for (int j = 0; j < t; ++j) sum_theta += th[j];
-  double trG = 0.0;
-  for (int i = 0; i < k; ++i) trG += Gq[i * k + i];
-  const double x2sq_new = R[0] + sum_theta;
-  const double F = fw + a.a2sq - R[0] - sum_theta;
-  double step = -1.0, rel = -1.0;
-  if (a.mode) {
-    // VnV = V'^T Vp = R^T;  ZnV = (S V')^T Vp = ((Vp^T Z) Q)[:, :t]^T
-    double* ZnV = sm + so.Tb;                  // t x t scratch (Tb is free now)
-    for (int idx = threadIdx.x; idx < t * t; idx += kSST) {
-      const int i = idx / t, j = idx - i * t;
-      double v = 0.0;
-      for (int q = 0; q < b; ++q) v = fma(Gx[2 * b * b + t * b + j * b + q], sm[so.Qb + q * b + i], v);
-      ZnV[idx] = v;
-    }
-    for (int idx = threadIdx.x; idx < kt; idx += kSST) {
-      const int l = idx / t, j = idx - l * t;
-      double h1 = 0.0, h2 = 0.0;
-      for (int q = 0; q < k; ++q) {
-        const double hq = Gm[l * k + q] + Gam[l * k + q];
-        h1 = fma(hq, CVp[q * t + j], h1);
-        h2 = fma(hq, R[fo.CVn + q * t + j], h2);
-      }
-      HCV[idx] = h1;
-      HCVn[idx] = h2;
-    }
-    __syncthreads();
-    // (a) exact Gram identity   (b) first-order expansion (small steps; no cancellation)
-    double v[2] = {0.0, 0.0};
-    for (int idx = threadIdx.x; idx < kt; idx += kSST) {
-      v[0] -= R[fo.CnV + idx] * HCV[idx] + R[fo.CnVn + idx] * HCVn[idx];
-      v[0] += R[fo.MVn + idx] * R[fo.CVn + idx] + R[fo.MnV + idx] * R[fo.CnV + idx];
-      const int l = idx / t, j = idx - l * t;
-      double om = 0.0, gd = 0.0, gg = 0.0, gcv = 0.0;
-      for (int q = 0; q < k; ++q) {
-        const double cvq = R[fo.CnVn + q * t + j];
-        const double dq = cvq - R[fo.CVn + q * t + j];
-        om = fma(0.5 * (Om[l * k + q] + Om[q * k + l]), cvq, om);
-        gd = fma(Gam[l * k + q], dq, gd);
-        gg = fma(Gm[l * k + q], dq, gg);
-        gcv = fma(Gam[l * k + q], CVp[q * t + j], gcv);
-      }
-      const double cvl = R[fo.CnVn + idx], dl = cvl - R[fo.CVn + idx];
-      v[1] -= cvl * om + 2.0 * cvl * gd + dl * gg;
-      Wm[idx] = R[fo.NV + idx] - gcv;
-    }
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < t * t; idx += kSST) {
-      const int aa = idx / t, bb = idx - aa * t;
-      const double vnv = Rt[bb * t + aa];      // (V'^T Vp)[aa][bb]
-      double x1 = 0.0, x3 = 0.0;
-      for (int l = 0; l < k; ++l) {
-        x1 = fma(R[fo.CnVn + l * t + aa], HCV[l * t + bb], x1);
-        x3 = fma(CVp[l * t + bb], R[fo.MVn + l * t + aa], x3);
-      }
-      v[0] += vnv * (x1 + ZnV[idx]) - vnv * x3;
-      const int i = aa, j = bb;
-      double rlr = 0.0, rr = 0.0, xw = 0.0;
-      for (int q = 0; q < t; ++q) {
-        rlr = fma(Rt[q * t + i] * a.theta[q], Rt[q * t + j], rlr);   // previous Ritz values
-        rr = fma(Rt[q * t + i], Rt[q * t + j], rr);
-      }
-      for (int l = 0; l < k; ++l) xw = fma(R[fo.CE + l * t + i], Wm[l * t + j], xw);
-      v[1] += rlr * R[fo.EE + j * t + i] + rr * R[fo.ESE + j * t + i] + 2.0 * xw * Rt[j * t + i];
-    }
-    block_sum_n<2>(v, red);
-    const double cross = R[1] + v[0];
-    double trOm = 0.0;
-    for (int i = 0; i < k; ++i) trOm += Om[i * k + i];
-    const double x2sq_old = a.scal[0], xn2_old = a.scal[1];
-    const double st2_big = trOm + x2sq_new + x2sq_old - 2.0 * cross;
-    const double st2_small = trOm + R[2] + 2.0 * R[3] + R[4] + v[1];
-    const double st2 = st2_big > 1e-8 * xn2_old ? st2_big : st2_small;
-    step = sqrt(fmax(st2, 0.0));
-    rel = step / sqrt(xn2_old);
-  }
-  tmark(s, a);                                 // objective + step norm
-  __syncthreads();
-  for (int j = threadIdx.x; j < b; j += kSST) a.theta[j] = th[j];
-  if (threadIdx.x == 0) {
-    const int64_t pnew = a.mode ? (int64_t)llround(a.scal[5]) + 1 : 0;   // canonical state index
-    a.scal[0] = x2sq_new;
-    a.scal[1] = trG + x2sq_new;
-    a.scal[2] = F;
-    a.scal[3] = step;
-    a.scal[4] = rel;
-    a.scal[5] = (double)pnew;
-    a.scal[6] = rmax / fabs(th[0]);
-    a.scal[7] = (double)nprod;
-    const int64_t slotp = pnew % a.trace_cap;
-    a.trace[slotp * 4 + 0] = F;
-    a.trace[slotp * 4 + 1] = step;
-    a.trace[slotp * 4 + 2] = rel;
-    a.trace[slotp * 4 + 3] = (double)pnew;
-    if (!isfinite(F)) raise_flag(a.flags, DF_NONFINITE);
-    if (a.mode && a.eps > 0.0 && (step < a.eps || rel < a.eps)) a.flags[2] = 1;   // converged
-    a.flags[3] = outer;
-  }
-  // operands: CV (k x t), K (k x k)
-  for (int idx = threadIdx.x; idx < kt; idx += kSST) {
-    const double v = R[fo.CnVn + idx];
-    a.CVprev[idx] = v;
-    if (a.dtype) reinterpret_cast<double*>(a.CVop)[idx] = v;
-    else reinterpret_cast<float*>(a.CVop)[idx] = (float)v;
-  }
-  if (!a.uniform) {
     for (int idx = threadIdx.x; idx < kk; idx += kSST) {
       const int i = idx / k, j = idx - i * k;
-      const double v = 0.5 * (R[fo.CC + idx] + R[fo.CC + j * k + i]);
+      double g;
+      if (a.mode) {
+        g = a.G_in[idx] + incGam[i * k + j] + incGam[j * k + i] + 0.5 * (incOm[i * k + j] + incOm[j * k + i]);
+        if (s.c == 0) a.G_out[idx] = g;
+      } else {
+        g = a.G_out[idx];
+      }
+      Gq[idx] = g;
+    }
+    __syncthreads();
+    bool okinv = a.mode ? ns_inverse(Gq, Xq, Rq, Pq, k, red) : false;
+    if (!okinv) {
+      for (int idx = threadIdx.x; idx < kk; idx += kSST) Xq[idx] = Gq[idx];
+      __syncthreads();
+      if (!sweep_inverse(Xq, k, 256.0 * kEps, sm + so.d0, sm + so.rb)) {   // rank(X1) < k (R6)
+        if (s.c == 0 && threadIdx.x == 0) raise_flag(a.flags, DF_RANK);
+        return;                                // uniform on every CTA; no barrier issued yet
+      }
+    }
+    if (s.c == 0)
+      for (int idx = threadIdx.x; idx < kk; idx += kSST) a.Gi_out[idx] = Xq[idx];
+    tmark(s, a);                               // [1] Gram update + G'^{-1}
+    // C'[:, slice] = G'^{-1} M'[:, slice]
+    gemm_nn(k, s.nl, k, Xq, k, Ms, ldm, Cs, ldc, 1.0, false);
+    __syncthreads();
+    if (p.oCs >= 0)
+      for (int idx = threadIdx.x; idx < k * s.nl; idx += kSST) {
+        const int q = idx / s.nl, i = idx - q * s.nl;
+        a.C_out[(int64_t)q * nk + s.rs + i] = Cs[q * ldc + i];
+      }
+    tmark(s, a);                               // [2] C'
+
+    // ---------------------------------------------- B: eigenpairs of S
+    const double floor_abs = 4.0 * kEps * sqrt((double)nk) * a.a2sq;   // S-product rounding floor
+    bool converged = false, failed = false;
+    int outer = 0;
+    double rmax = 0.0;
+    double* dsc = sm + so.dsc;
+    double* rres = s.sm + p.oCinE;             // residuals (t)
+    bool ortho = !a.cold;                      // Y expected orthonormal (warm Ritz block)
+    while (true) {
+      // ---- Rayleigh-Ritz on span(Y):  Z = S Y;  Gyy = Y^T Y, Gyz = Y^T Z (generalised RR)
+      s_apply<PW>(s, a, Cs, ldc, Ms, ldm, buf[iY], b, buf[iZ], &nprod);
+      tmark(s, a);                             // product
+      {
+        const double* Y = s.sm + buf[iY];
+        const double* Z = s.sm + buf[iZ];
+        double* part = xpart(s, p);
+        const int tb = a.mode ? t : 0;
+        const TN d[4] = {{Y, 1, b, Y, 1, b, b, b, part},
+                         {Y, 1, b, Z, 1, b, b, b, part + b * b},
+                         {Vp, 1, t, Y, 1, b, tb, b, part + 2 * b * b},
+                         {Vp, 1, t, Z, 1, b, tb, b, part + 2 * b * b + t * b}};
+        slice_tn<4>(s.nl, d);
+        xreduce(s, p, 2 * b * b + 2 * tb * b, Gx);
+      }
+      tmark(s, a);                             // Gram exchange
+      // ---- local (every CTA identically): D = diag(Gyy)^-1/2; if D Gyy D = I to rounding
+      //      the block is orthonormal: T = D Gyz D, Q = D U.  Otherwise L L^T = D Gyy D,
+      //      T = L^-1 (D Gyz D) L^-T, Q = D L^-T U.
+      bool gen;
+      {
+        double* Lb = sm + so.Lb;
+        double* Li = sm + so.Li;
+        double* Tb = sm + so.Tb;
+        double* Ub = sm + so.Ub;
+        double* Qb = sm + so.Qb;
+        double* Wb = sm + so.Wb;
+        if (threadIdx.x < b) {
+          const double d = Gx[threadIdx.x * b + threadIdx.x];
+          dsc[threadIdx.x] = d > 0.0 ? rsqrt(d) : 1.0;
+        }
+        __syncthreads();
+        double dev = 0.0;
+        for (int idx = threadIdx.x; idx < b * b; idx += kSST) {
+          const int i = idx / b, j = idx - i * b;
+          const double di = dsc[i] * dsc[j];
+          const double g = 0.5 * (Gx[i * b + j] + Gx[j * b + i]) * di;
+          Lb[i * 32 + j] = g;
+          Wb[i * 32 + j] = 0.5 * (Gx[b * b + i * b + j] + Gx[b * b + j * b + i]) * di;
+          if (i != j) dev = fmax(dev, fabs(g));
+        }
+        dev = block_max(dev, red);
+        gen = !(ortho && dev < 1e-13);
+        if (gen) {
+          if (!chol_small(Lb, b, sm + so.rb, &ok_s)) { failed = true; break; }
+          tri_inverse(Lb, sm + so.rb, b, Li);
+          for (int idx = threadIdx.x; idx < b * b; idx += kSST) {   // Ub = Li Wb
+            const int i = idx / b, j = idx - i * b;
+            double v = 0.0;
+            for (int q = 0; q <= i; ++q) v = fma(Li[i * 32 + q], Wb[q * 32 + j], v);
+            Ub[i * 32 + j] = v;
+          }
+          __syncthreads();
+          for (int idx = threadIdx.x; idx < b * b; idx += kSST) {   // Tb = Ub Li^T
+            const int i = idx / b, j = idx - i * b;
+            double v = 0.0;
+            for (int q = 0; q <= j; ++q) v = fma(Ub[i * 32 + q], Li[j * 32 + q], v);
+            Tb[i * 32 + j] = v;
+          }
+          __syncthreads();
+          for (int idx = threadIdx.x; idx < b * b; idx += kSST) {
+            const int i = idx / b, j = idx - i * b;
+            if (i < j) {
+              const double v = 0.5 * (Tb[i * 32 + j] + Tb[j * 32 + i]);
+              Tb[i * 32 + j] = v;
+              Tb[j * 32 + i] = v;
+            }
+          }
+        } else {
+          for (int idx = threadIdx.x; idx < b * b; idx += kSST) {
+            const int i = idx / b, j = idx - i * b;
+            Tb[i * 32 + j] = Wb[i * 32 + j];
+          }
+        }
+        __syncthreads();
+        jacobi_par(Tb, Ub, th, sm + so.cs, b);
+        for (int idx = threadIdx.x; idx < b * b; idx += kSST) {     // Qb = D (Li^T U) or D U
+          const int i = idx / b, j = idx - i * b;
+          double v;
+          if (gen) {
+            v = 0.0;
+            for (int q = i; q < b; ++q) v = fma(Li[q * 32 + i], Ub[q * 32 + j], v);
+          } else {
+            v = Ub[i * 32 + j];
+          }
+          Qb[i * b + j] = v * dsc[i];
+        }
+        __syncthreads();
+      }
+      tmark(s, a);                             // local RR
+      const double* Qb = sm + so.Qb;
+      // ---- rotate: Y' = Y Q, Z' = Z Q  (into the free buffers)
+      gemm_nn(s.nl, b, b, s.sm + buf[iY], b, Qb, b, s.sm + buf[iA], b, 1.0, false);
+      gemm_nn(s.nl, b, b, s.sm + buf[iZ], b, Qb, b, s.sm + buf[iB], b, 1.0, false);
+      {
+        const int oy = iY, oz = iZ;
+        iY = iA; iZ = iB; iA = oy; iB = oz;
+      }
+      __syncthreads();
+      // ---- residuals of the wanted pairs
+      {
+        const double* Y = s.sm + buf[iY];
+        const double* Z = s.sm + buf[iZ];
+        double* part = xpart(s, p);
+        for (int j = threadIdx.x; j < t; j += kSST) {
+          double v = 0.0;
+          for (int r = 0; r < s.nl; ++r) {
+            const double d = Z[r * b + j] - th[j] * Y[r * b + j];
+            v = fma(d, d, v);
+          }
+          part[j] = v;
+        }
+        xreduce(s, p, t, rres);
+      }
+      tmark(s, a);                             // residual exchange
+      rmax = 0.0;
+      for (int j = 0; j < t; ++j) rmax = fmax(rmax, sqrt(fmax(rres[j], 0.0)));
+      const double theta0 = th[0];
+      const double target = fmax(a.tol * fabs(theta0), floor_abs);
+      if (rmax <= target) { converged = true; break; }
+      if (++outer > a.max_outer) break;
+      // ---- Chebyshev filter of adaptive degree damping [0, theta_{b-1}]
+      const double beta = th[b - 1];
+      double cc = 0.5 * beta, ee = 0.5 * beta;
+      int d = 1;
+      if (!(beta > 1e-300 * fabs(theta0)) || beta >= th[t - 1]) {
+        cc = 0.0; ee = 1.0; d = 1;              // no gap inside the block: plain power step
+      } else {
+        const double x0 = (theta0 - cc) / ee, xt = (th[t - 1] - cc) / ee;
+        // acosh(x) = log(x + sqrt(x^2 - 1)) for x >= 1
+        const double xtc = fmax(xt, 1.0), x0c = fmax(x0, 1.0);
+        const double at = log(xtc + sqrt(xtc * xtc - 1.0)), a0 = log(x0c + sqrt(x0c * x0c - 1.0));
+        const double need = log(fmax(rmax / target, 1.0)) / fmax(at, 1e-6);
+        d = (int)ceil(need) + 1;
+        const int dcap = max(1, (int)(9.9 / fmax(a0, 1e-6)));   // amplification <= ~1e4
+        d = max(1, min(d, min(a.max_deg, dcap)));
+      }
+      const double einv = 1.0 / ee;
+      int i0 = iY, i1 = iA, iz = iZ, i3 = iB;   // P0 = Y, P1 = (Z - c Y)/e, scratch z, free
+      {
+        double* P1 = s.sm + buf[i1];
+        const double* Y = s.sm + buf[i0];
+        const double* Z = s.sm + buf[iz];
+        for (int idx = threadIdx.x; idx < s.nl * b; idx += kSST) P1[idx] = (Z[idx] - cc * Y[idx]) * einv;
+        __syncthreads();
+      }
+      for (int j = 2; j <= d; ++j) {
+        s_apply<PW>(s, a, Cs, ldc, Ms, ldm, buf[i1], b, buf[iz], &nprod);
+        double* pn = s.sm + buf[i0];           // P2 = 2 (S P1 - c P1)/e - P0, in place of P0
+        const double* pz = s.sm + buf[iz];
+        const double* p1 = s.sm + buf[i1];
+        for (int idx = threadIdx.x; idx < s.nl * b; idx += kSST)
+          pn[idx] = 2.0 * (pz[idx] - cc * p1[idx]) * einv - pn[idx];
+        __syncthreads();
+        const int tmp = i0; i0 = i1; i1 = tmp;
+      }
+      iY = i1; iZ = iz; iA = i0; iB = i3;
+      ortho = false;                           // filtered block: generalised Rayleigh-Ritz
+    }
+    if ((failed || !converged) && s.c == 0 && threadIdx.x == 0) raise_flag(a.flags, DF_EIG);
+    if (failed) {          // every CTA took the same decision; keep peers' smem alive
+      cg::this_cluster().sync();
+      return;
+    }
+    // ---------------------------------------------- C: operands of the next row pass
+    const double* Y = s.sm + buf[iY];          // V' = Y[:, :t]
+    double* my = a.xchg + (int64_t)s.c * p.flen;
+    {   // slice partials of C' C'^T (k x k) and C' V' (k x t)
+      const TN d[2] = {{Cs, ldc, 1, Cs, ldc, 1, k, k, my},
+                       {Cs, ldc, 1, Y, 1, b, k, t, my + kk}};
+      slice_tn<2>(s.nl, d);
+    }
+    {
+      const int RP = a.rp;
+      for (int64_t idx = threadIdx.x; idx < (int64_t)s.nl * RP; idx += kSST) {   // Wt rows
+        const int cl = (int)(idx / RP), j = (int)(idx % RP);
+        double v = 0.0;
+        if (j < t) v = Y[cl * b + j];
+        else if (j < t + k) v = Cs[(int64_t)(j - t) * ldc + cl];
+        const int64_t o = (int64_t)(k + s.rs + cl - a.k0) * RP + j;
+        if (a.dtype) reinterpret_cast<double*>(a.Wt)[o] = v;
+        else reinterpret_cast<float*>(a.Wt)[o] = (float)v;
+      }
+      for (int idx = threadIdx.x; idx < s.nl * t; idx += kSST) {
+        const int r = idx / t, j = idx - r * t;
+        a.V_out[(int64_t)(s.rs + r) * t + j] = Y[r * b + j];
+      }
+      for (int idx = threadIdx.x; idx < s.nl * b; idx += kSST) a.Y[(int64_t)s.rs * b + idx] = Y[idx];
+    }
+    tmark(s, a);                               // operand partials
+    cg::this_cluster().sync();                 // partials in global memory (cluster scope)
+    const int flen = kk + kt;
+    {   // reduce-scatter of the k^2 + kt partials
+      const int fc = (flen + s.CL - 1) / s.CL;
+      const int f0 = s.c * fc, f1 = min(flen, f0 + fc);
+      for (int i = f0 + threadIdx.x; i < f1; i += kSST) {
+        double v[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) v[c] = c < s.CL ? __ldcg(a.xchg + (int64_t)c * p.flen + i) : 0.0;
+        double acc = 0.0;
+#pragma unroll
+        for (int c = 0; c < 16; ++c) acc += v[c];
+        a.red[i] = acc;
+      }
+    }
+    cg::this_cluster().sync();
+    if (s.c != 0) return;
+    // ---- CTA 0: small results for the deferred half, C V, K^{-1}
+    if (a.mode) {
+      const double* Qb = sm + so.Qb;
+      for (int idx = threadIdx.x; idx < t * t; idx += kSST) {
+        const int i = idx / t, j = idx - i * t;
+        double r = 0.0, z = 0.0;     // R = (Vp^T Y) Q[:, :t];  ZnV[i][j] = sum_q VpZ[j][q] Q[q][i]
+        for (int q = 0; q < b; ++q) {
+          r = fma(Gx[2 * b * b + i * b + q], Qb[q * b + j], r);
+          z = fma(Gx[2 * b * b + t * b + j * b + q], Qb[q * b + i], z);
+        }
+        a.k3x[idx] = r;
+        a.k3x[t * t + idx] = z;
+      }
+    }
+    for (int j = threadIdx.x; j < b; j += kSST) a.th_out[j] = th[j];
+    if (threadIdx.x == 0) {
+      a.scal[6] = rmax / fabs(th[0]);
+      a.scal[7] = (double)nprod;
+      a.flags[3] = outer;
+    }
+    for (int idx = threadIdx.x; idx < kt; idx += kSST) {
+      const double v = __ldcg(a.red + kk + idx);
+      a.CV_out[idx] = v;
+      if (a.dtype) reinterpret_cast<double*>(a.CVop)[idx] = v;
+      else reinterpret_cast<float*>(a.CVop)[idx] = (float)v;
+    }
+    if (!a.uniform) {
+      for (int idx = threadIdx.x; idx < kk; idx += kSST) {
+        const int i = idx / k, j = idx - i * k;
+        const double v = 0.5 * (__ldcg(a.red + idx) + __ldcg(a.red + j * k + i));
+        if (a.dtype) reinterpret_cast<double*>(a.Kop)[idx] = v;
+        else reinterpret_cast<float*>(a.Kop)[idx] = (float)v;
+      }
+      tmark(s, a);
+      return;
+    }
+    // uniform W1: K^{-1} = (w^2 I + C'C'^T)^{-1}: Newton-Schulz from the previous K^{-1},
+    // sweep-operator inverse at init or as fallback
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < kk; idx += kSST) {
+      const int i = idx / k, j = idx - i * k;
+      Gq[idx] = 0.5 * (__ldcg(a.red + idx) + __ldcg(a.red + j * k + i)) + (i == j ? a.w2 : 0.0);
+      if (a.mode) Xq[idx] = a.Ki[idx];
+    }
+    __syncthreads();
+    bool okk = a.mode ? ns_inverse(Gq, Xq, Rq, Pq, k, red) : false;
+    if (!okk) {
+      for (int idx = threadIdx.x; idx < kk; idx += kSST) Xq[idx] = Gq[idx];
+      __syncthreads();
+      if (!sweep_inverse(Xq, k, 0.0, sm + so.d0, sm + so.rb)) {
+        if (threadIdx.x == 0) raise_flag(a.flags, DF_ROWSPD);
+        return;
+      }
+    }
+    for (int idx = threadIdx.x; idx < kk; idx += kSST) {
+      const double v = Xq[idx];
+      a.Ki[idx] = v;
       if (a.dtype) reinterpret_cast<double*>(a.Kop)[idx] = v;
       else reinterpret_cast<float*>(a.Kop)[idx] = (float)v;
     }
-    tmark(s, a);
-    return;
-  }
-  // uniform W1: K^{-1} = (w^2 I + C'C'^T)^{-1}: Newton-Schulz from the previous K^{-1}
-  // (the NS mats are free now), sweep-operator inverse at init or as fallback
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < kk; idx += kSST) {
-    const int i = idx / k, j = idx - i * k;
-    Gq[idx] = 0.5 * (R[fo.CC + idx] + R[fo.CC + j * k + i]) + (i == j ? a.w2 : 0.0);
-    if (a.mode) Xq[idx] = a.Ki[idx];
-  }
-  __syncthreads();
-  bool okk = a.mode ? ns_inverse(Gq, Xq, Rq, Pq, k, red) : false;
-  if (!okk) {
-    for (int idx = threadIdx.x; idx < kk; idx += kSST) Xq[idx] = Gq[idx];
-    __syncthreads();
-    if (!sweep_inverse(Xq, k, 0.0, sm + so.d0, sm + so.rb)) {
-      if (threadIdx.x == 0) raise_flag(a.flags, DF_ROWSPD);
-      return;
+    tmark(s, a);                               // K^{-1}
+  } else {
+    // ================================== PART 2: objective, step norm, trace (deferred)
+    const double fw = a.mode ? incOm[(int64_t)kk] : a.inc[0];
+    double* Vn = s.sm + p.oBuf;                // nl x t  V_{p+1} (buffer 0)
+    const bool ms3 = p.oMat3 >= 0 && a.mode;
+    double* mats = s.sm + (p.oMat3 >= 0 ? p.oMat3 : 0);
+    if (ms3) {
+      for (int idx = threadIdx.x; idx < kk; idx += kSST) {
+        mats[idx] = a.G_in[idx];
+        mats[kk + idx] = incGam[idx];
+        mats[2 * kk + idx] = incOm[idx];
+      }
+      for (int idx = threadIdx.x; idx < kt; idx += kSST) mats[3 * kk + idx] = a.CV_in[idx];
     }
+    const double* Gm = ms3 ? mats : a.G_in;
+    const double* Gam = ms3 ? mats + kk : incGam;
+    const double* Om = ms3 ? mats + 2 * kk : incOm;
+    const double* CVp = ms3 ? mats + 3 * kk : a.CV_in;
+    for (int idx = threadIdx.x; idx < k * s.nl; idx += kSST) {
+      const int q = idx / s.nl, i = idx - q * s.nl;
+      const int64_t gi = (int64_t)q * nk + s.rs + i;
+      if (p.oCs >= 0) Cs[q * ldc + i] = a.C_out[gi];
+      if (p.oMs >= 0) Ms[q * ldm + i] = a.M_out[gi];
+      if (p.oCin >= 0 && a.mode) s.sm[p.oCin + q * s.SL + i] = a.C_in[gi];
+    }
+    for (int idx = threadIdx.x; idx < s.nl * t; idx += kSST) {
+      Vn[idx] = a.V_out[(int64_t)s.rs * t + idx];
+      if (a.mode) Vp[idx] = a.V_in[(int64_t)s.rs * t + idx];
+    }
+    if (threadIdx.x < t * t && a.mode) Rt[threadIdx.x] = a.k3x[threadIdx.x];
+    __syncthreads();
+    if (a.mode) {
+      // E = V' - Vp R (slice), C_in E partial -> exchange -> S_p E = G_A E - M_in^T (C_in E)
+      for (int idx = threadIdx.x; idx < s.nl * t; idx += kSST) {
+        const int r = idx / t, j = idx - r * t;
+        double v = Vn[idx];
+        for (int q = 0; q < t; ++q) v = fma(-Vp[r * t + q], Rt[q * t + j], v);
+        Es[idx] = v;
+      }
+      __syncthreads();
+      double* part = xpart(s, p);
+      const TN d[1] = {{Cin, ldci, 1, Es, 1, t, k, t, part}};
+      slice_tn<1>(s.nl, d);
+      double* CinE = s.sm + p.oCinE;
+      xreduce(s, p, kt, CinE);
+      s_product<PW>(s, a, p.oE, t, t, CinE, a.M_in + s.rs, nk, SEs, t);
+    }
+    tmark(s, a);                               // old-S product
+    const FinOff fo(k, t);
+    double* my = a.xchg + (int64_t)s.c * p.flen;
+    {
+      // [0] <M',C'> [1] <C', H C_in> [2] <C', Om C'> [3] <C', Gam dC> [4] <dC, G dC>
+      double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+      for (int idx = threadIdx.x; idx < k * s.nl; idx += kSST) {
+        const int l = idx / s.nl, i = idx - l * s.nl;
+        const double cn = Cs[(int64_t)l * ldc + i];
+        v[0] = fma(Ms[(int64_t)l * ldm + i], cn, v[0]);
+        if (a.mode) {
+          double hc = 0.0, omc = 0.0, gdc = 0.0, ggdc = 0.0;
+          for (int q = 0; q < k; ++q) {
+            const double co = Cin[(int64_t)q * ldci + i], cq = Cs[(int64_t)q * ldc + i];
+            const double dq = cq - co;
+            const double gam = Gam[l * k + q], gm = Gm[l * k + q];
+            hc = fma(gm + gam, co, hc);
+            omc = fma(0.5 * (Om[l * k + q] + Om[q * k + l]), cq, omc);
+            gdc = fma(gam, dq, gdc);
+            ggdc = fma(gm, dq, ggdc);
+          }
+          const double dl = cn - Cin[(int64_t)l * ldci + i];
+          v[1] = fma(cn, hc, v[1]);
+          v[2] = fma(cn, omc, v[2]);
+          v[3] = fma(cn, gdc, v[3]);
+          v[4] = fma(dl, ggdc, v[4]);
+        }
+      }
+      block_sum_n<5>(v, red);
+      if (threadIdx.x == 0)
+        for (int u = 0; u < 5; ++u) my[u] = v[u];
+    }
+    {
+      const int km = a.mode ? k : 0, tm = a.mode ? t : 0;
+      const TN d[9] = {{Cs, ldc, 1, Vp, 1, t, km, t, my + fo.CnV},
+                       {Cs, ldc, 1, Vn, 1, t, k, t, my + fo.CnVn},
+                       {Cin, ldci, 1, Vn, 1, t, km, t, my + fo.CVn},
+                       {Ms, ldm, 1, Vp, 1, t, km, t, my + fo.MnV},
+                       {a.M_in + s.rs, nk, 1, Vn, 1, t, km, t, my + fo.MVn},
+                       {incN + s.rs, nk, 1, Vp, 1, t, km, t, my + fo.NV},
+                       {Cs, ldc, 1, Es, 1, t, km, t, my + fo.CE},
+                       {Es, 1, t, Es, 1, t, tm, t, my + fo.EE},
+                       {Es, 1, t, SEs, 1, t, tm, t, my + fo.ESE}};
+      slice_tn<9>(s.nl, d);
+      if (!a.mode)
+        for (int idx = threadIdx.x; idx < fo.CC; idx += kSST)
+          if (idx >= fo.CnV && (idx < fo.CnVn || idx >= fo.CnVn + kt)) my[idx] = 0.0;
+    }
+    tmark(s, a);                               // final partials
+    cg::this_cluster().sync();
+    {   // reduce-scatter of the 5 + 7kt + 2t^2 partials
+      const int flen = fo.CC;
+      const int fc = (flen + s.CL - 1) / s.CL;
+      const int f0 = s.c * fc, f1 = min(flen, f0 + fc);
+      for (int i = f0 + threadIdx.x; i < f1; i += kSST) {
+        double v[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) v[c] = c < s.CL ? __ldcg(a.xchg + (int64_t)c * p.flen + i) : 0.0;
+        double acc = 0.0;
+#pragma unroll
+        for (int c = 0; c < 16; ++c) acc += v[c];
+        a.red[i] = acc;
+      }
+    }
+    cg::this_cluster().sync();
+    tmark(s, a);                               // reduce-scatter
+    if (s.c != 0) return;
+    // ---- CTA 0: F, step norm, trace
+    const bool rsm = p.oTail >= 0;
+    double* R = rsm ? s.sm + p.oTail : a.red;
+    if (rsm)
+      for (int i = threadIdx.x; i < fo.CC; i += kSST) R[i] = __ldcg(a.red + i);
+    double* HCV = R + p.flen;                  // k x t
+    double* HCVn = HCV + kt;                   // k x t
+    double* Wm = HCVn + kt;                    // k x t
+    double* ZnV = sm + so.Tb;                  // t x t
+    if (threadIdx.x < t * t && a.mode) ZnV[threadIdx.x] = a.k3x[t * t + threadIdx.x];
+    __syncthreads();
+    double sum_theta = 0.0;
+    for (int j = 0; j < t; ++j) sum_theta += a.th_out[j];
+    double trG = 0.0;
+    for (int i = 0; i < k; ++i) trG += a.G_out[i * k + i];
+    const double x2sq_new = R[0] + sum_theta;
+    const double F = fw + a.a2sq - R[0] - sum_theta;
+    double step = -1.0, rel = -1.0;
+    if (a.mode) {
+      for (int idx = threadIdx.x; idx < kt; idx += kSST) {
+        const int l = idx / t, j = idx - l * t;
+        double h1 = 0.0, h2 = 0.0;
+        for (int q = 0; q < k; ++q) {
+          const double hq = Gm[l * k + q] + Gam[l * k + q];
+          h1 = fma(hq, CVp[q * t + j], h1);
+          h2 = fma(hq, R[fo.CVn + q * t + j], h2);
+        }
+        HCV[idx] = h1;
+        HCVn[idx] = h2;
+      }
+      __syncthreads();
+      // (a) exact Gram identity   (b) first-order expansion (small steps; no cancellation)
+      double v[2] = {0.0, 0.0};
+      for (int idx = threadIdx.x; idx < kt; idx += kSST) {
+        v[0] -= R[fo.CnV + idx] * HCV[idx] + R[fo.CnVn + idx] * HCVn[idx];
+        v[0] += R[fo.MVn + idx] * R[fo.CVn + idx] + R[fo.MnV + idx] * R[fo.CnV + idx];
+        const int l = idx / t, j = idx - l * t;
+        double om = 0.0, gd = 0.0, gg = 0.0, gcv = 0.0;
+        for (int q = 0; q < k; ++q) {
+          const double cvq = R[fo.CnVn + q * t + j];
+          const double dq = cvq - R[fo.CVn + q * t + j];
+          om = fma(0.5 * (Om[l * k + q] + Om[q * k + l]), cvq, om);
+          gd = fma(Gam[l * k + q], dq, gd);
+          gg = fma(Gm[l * k + q], dq, gg);
+          gcv = fma(Gam[l * k + q], CVp[q * t + j], gcv);
+        }
+        const double cvl = R[fo.CnVn + idx], dl = cvl - R[fo.CVn + idx];
+        v[1] -= cvl * om + 2.0 * cvl * gd + dl * gg;
+        Wm[idx] = R[fo.NV + idx] - gcv;
+      }
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < t * t; idx += kSST) {
+        const int aa = idx / t, bb = idx - aa * t;
+        const double vnv = Rt[bb * t + aa];    // (V'^T Vp)[aa][bb]
+        double x1 = 0.0, x3 = 0.0;
+        for (int l = 0; l < k; ++l) {
+          x1 = fma(R[fo.CnVn + l * t + aa], HCV[l * t + bb], x1);
+          x3 = fma(CVp[l * t + bb], R[fo.MVn + l * t + aa], x3);
+        }
+        v[0] += vnv * (x1 + ZnV[idx]) - vnv * x3;
+        const int i = aa, j = bb;
+        double rlr = 0.0, rr = 0.0, xw = 0.0;
+        for (int q = 0; q < t; ++q) {
+          rlr = fma(Rt[q * t + i] * a.th_in[q], Rt[q * t + j], rlr);   // previous Ritz values
+          rr = fma(Rt[q * t + i], Rt[q * t + j], rr);
+        }
+        for (int l = 0; l < k; ++l) xw = fma(R[fo.CE + l * t + i], Wm[l * t + j], xw);
+        v[1] += rlr * R[fo.EE + j * t + i] + rr * R[fo.ESE + j * t + i] + 2.0 * xw * Rt[j * t + i];
+      }
+      block_sum_n<2>(v, red);
+      const double cross = R[1] + v[0];
+      double trOm = 0.0;
+      for (int i = 0; i < k; ++i) trOm += Om[i * k + i];
+      const double x2sq_old = a.scal[0], xn2_old = a.scal[1];
+      const double st2_big = trOm + x2sq_new + x2sq_old - 2.0 * cross;
+      const double st2_small = trOm + R[2] + 2.0 * R[3] + R[4] + v[1];
+      const double st2 = st2_big > 1e-8 * xn2_old ? st2_big : st2_small;
+      step = sqrt(fmax(st2, 0.0));
+      rel = step / sqrt(xn2_old);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int64_t pnew = a.mode ? (int64_t)llround(a.scal[5]) + 1 : 0;   // canonical state index
+      a.scal[0] = x2sq_new;
+      a.scal[1] = trG + x2sq_new;
+      a.scal[2] = F;
+      a.scal[3] = step;
+      a.scal[4] = rel;
+      a.scal[5] = (double)pnew;
+      const int64_t slotp = pnew % a.trace_cap;
+      a.trace[slotp * 4 + 0] = F;
+      a.trace[slotp * 4 + 1] = step;
+      a.trace[slotp * 4 + 2] = rel;
+      a.trace[slotp * 4 + 3] = (double)pnew;
+      if (!isfinite(F)) raise_flag(a.flags, DF_NONFINITE);
+      if (a.mode && a.eps > 0.0 && (step < a.eps || rel < a.eps)) a.flags[2] = 1;   // converged
+    }
+    tmark(s, a);                               // objective + step norm
   }
-  for (int idx = threadIdx.x; idx < kk; idx += kSST) {
-    const double v = Xq[idx];
-    a.Ki[idx] = v;
-    if (a.dtype) reinterpret_cast<double*>(a.Kop)[idx] = v;
-    else reinterpret_cast<float*>(a.Kop)[idx] = (float)v;
-  }
-  tmark(s, a);                                 // K^{-1}
 }
 
-template <int BT>
+template <int BT, int PART>
 cudaError_t ss_configure(int CL, size_t smem) {
   static size_t done_smem = 0;
   static int done_cl = 0;
   if (smem <= done_smem && (CL <= 8 || done_cl > 8)) return cudaSuccess;
-  auto kern = small_step_kernel<BT>;
+  auto kern = small_step_kernel<BT, PART>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (CL > 8) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -1083,7 +1184,10 @@ cudaError_t ss_configure(int CL, size_t smem) {
 
 template <int BT>
 int ss_max_clusters(int CL, size_t smem) {
-  if (ss_configure<BT>(CL, smem) != cudaSuccess) { cudaGetLastError(); return 0; }
+  if (ss_configure<BT, 1>(CL, smem) != cudaSuccess || ss_configure<BT, 2>(CL, smem) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(CL);
   cfg.blockDim = dim3(kSST);
@@ -1093,18 +1197,19 @@ int ss_max_clusters(int CL, size_t smem) {
   at[0].val.clusterDim.x = CL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, small_step_kernel<BT>, &cfg) != cudaSuccess) {
+  int n1 = 0, n2 = 0;
+  if (cudaOccupancyMaxActiveClusters(&n1, small_step_kernel<BT, 1>, &cfg) != cudaSuccess ||
+      cudaOccupancyMaxActiveClusters(&n2, small_step_kernel<BT, 2>, &cfg) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }
-  return n;
+  return std::min(n1, n2);
 }
 
 template <int BT>
-cudaError_t launch_ss(const SmallArgs& a, cudaStream_t st) {
+cudaError_t launch_ss(const SmallArgs& a, int part, cudaStream_t st) {
   const size_t smem = (size_t)a.pl.total * sizeof(double);
-  cudaError_t e = ss_configure<BT>(a.pl.CL, smem);
+  cudaError_t e = part == 1 ? ss_configure<BT, 1>(a.pl.CL, smem) : ss_configure<BT, 2>(a.pl.CL, smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(a.pl.CL);
@@ -1116,7 +1221,8 @@ cudaError_t launch_ss(const SmallArgs& a, cudaStream_t st) {
   at[0].val.clusterDim.x = a.pl.CL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, small_step_kernel<BT>, a);
+  if (part == 1) return cudaLaunchKernelEx(&cfg, small_step_kernel<BT, 1>, a);
+  return cudaLaunchKernelEx(&cfg, small_step_kernel<BT, 2>, a);
 }
 
 }  // namespace wlr

@@ -2,6 +2,6 @@
 #include "small_step.cuh"
 
 namespace wlr {
-template cudaError_t launch_ss<24>(const SmallArgs&, cudaStream_t);
+template cudaError_t launch_ss<24>(const SmallArgs&, int, cudaStream_t);
 template int ss_max_clusters<24>(int, size_t);
 }  // namespace wlr
