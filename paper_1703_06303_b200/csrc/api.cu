@@ -79,7 +79,7 @@ struct wlr_ctx {
   size_t es = 4;
   bool uniform = true;
   double w1s = 1.0;
-  int b = 0, rp = 0, bm = 0, nz = 0, nsplit = 0, rp_grid = 0;
+  int b = 0, rp = 0, bm = 0, nz = 0, nsplit = 0, rp_grid = 0, KA = 0;
   int64_t rps = 0;
   SSPlan spl{};
   int nsm = 148;
@@ -89,6 +89,7 @@ struct wlr_ctx {
   const void* W1 = nullptr; int64_t ldw = 0;
   void* X[2] = {nullptr, nullptr};
   void* Dl = nullptr;          // Delta = X1_{p+1} - X1_p (m x kp, written by the row pass)
+  CUtensorMap tmA{}, tmX[2]{}, tmW{};   // TMA descriptors of A, X1 (per buffer) and Wt
   int nwc = 8;                 // row-pass warps running per-row Cholesky
   void *Wt = nullptr, *CVop = nullptr, *Kop = nullptr;
   double *inc_part = nullptr, *fw_part = nullptr, *inc = nullptr, *fw0 = nullptr;
@@ -199,7 +200,7 @@ static SmallArgs small_args(wlr_ctx* h, int par, int mode) {
   const int cur = par, nxt = par ^ 1;
   SmallArgs s{};
   s.k = (int)h->k; s.nk = (int)h->nk; s.t = (int)h->t; s.b = h->b; s.kp = (int)h->kp;
-  s.k0 = (int)h->k0; s.rp = h->rp; s.mode = mode; s.dtype = h->dtype == WLR_F64 ? 1 : 0;
+  s.k0 = (int)h->k0; s.rp = h->rp; s.KA = h->KA; s.mode = mode; s.dtype = h->dtype == WLR_F64 ? 1 : 0;
   s.uniform = h->uniform ? 1 : 0; s.w2 = h->w1s * h->w1s;
   s.GA = h->GA; s.a2sq = h->a2sq; s.inc = mode ? h->inc : h->fw0;
   s.G_in = h->G[cur]; s.G_out = h->G[nxt]; s.M_in = h->M[cur]; s.M_out = h->M[nxt];
@@ -258,9 +259,10 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int par) {
     a.A = (const float*)h->A; a.lda = h->lda; a.W1 = (const float*)h->W1; a.ldw = h->ldw;
     a.w2s = (float)(h->w1s * h->w1s);
     a.Xold = (const float*)h->X[cur]; a.Xnew = (float*)h->X[nxt]; a.Dnew = (float*)h->Dl; a.nwc = h->nwc;
-    a.Wt = (const float*)h->Wt; a.CV = (const float*)h->CVop; a.Kmat = (const float*)h->Kop;
+    a.Wt = (const float*)h->Wt; a.KA = h->KA; a.Kmat = (const float*)h->Kop;
+    a.tmA = h->tmA; a.tmX = h->tmX[cur]; a.tmW = h->tmW;
     a.fw_part = h->fw_part; a.flags = h->flags;
-    a.m = h->m; a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.k0 = (int)h->k0; a.t = (int)h->t;
+    a.m = h->m; a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.no = (int)h->kp;
     a.vec_ok = (h->lda % 4 == 0) && ((uintptr_t)h->A % 16 == 0);
     set_prefetch(h, cur, a.pf_ptr, a.pf_bytes);
     e = launch_row_pass<float>(a, h->rp, h->uniform, 0, h->rp_grid, h->st);
@@ -269,9 +271,10 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int par) {
     a.A = (const double*)h->A; a.lda = h->lda; a.W1 = (const double*)h->W1; a.ldw = h->ldw;
     a.w2s = h->w1s * h->w1s;
     a.Xold = (const double*)h->X[cur]; a.Xnew = (double*)h->X[nxt]; a.Dnew = (double*)h->Dl; a.nwc = h->nwc;
-    a.Wt = (const double*)h->Wt; a.CV = (const double*)h->CVop; a.Kmat = (const double*)h->Kop;
+    a.Wt = (const double*)h->Wt; a.KA = h->KA; a.Kmat = (const double*)h->Kop;
+    a.tmA = h->tmA; a.tmX = h->tmX[cur]; a.tmW = h->tmW;
     a.fw_part = h->fw_part; a.flags = h->flags;
-    a.m = h->m; a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.k0 = (int)h->k0; a.t = (int)h->t;
+    a.m = h->m; a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.no = (int)h->kp;
     a.vec_ok = (h->lda % 4 == 0) && ((uintptr_t)h->A % 16 == 0);
     set_prefetch(h, cur, a.pf_ptr, a.pf_bytes);
     e = launch_row_pass<double>(a, h->rp, h->uniform, 0, h->rp_grid, h->st);
@@ -402,13 +405,19 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   CUDA_TRY(h, cudaMallocHost(&h->h_scal, 8 * sizeof(double)));
   wlr_status s;
   // ---- data: borrow device buffers, copy host buffers
-  if (is_device_ptr(A)) h->A = A;
-  else {
+  // The streaming kernels read A through TMA: rows must start 16-byte aligned.  A borrowed
+  // device A that is not (odd n) and every host A are copied into a padded buffer.
+  const bool dev_a = is_device_ptr(A);
+  if (dev_a && (h->lda * es) % 16 == 0 && (uintptr_t)A % 16 == 0) {
+    h->A = A;
+  } else {
+    const int64_t ldp = round_up(h->n, (int64_t)(16 / es));
     void* d = nullptr;
-    if ((s = dalloc(h, &d, (size_t)h->m * h->n * es)) != WLR_OK) return s;
-    CUDA_TRY(h, cudaMemcpy2DAsync(d, h->n * es, A, h->lda * es, h->n * es, h->m, cudaMemcpyHostToDevice, h->st));
+    if ((s = dalloc(h, &d, (size_t)h->m * ldp * es)) != WLR_OK) return s;
+    CUDA_TRY(h, cudaMemcpy2DAsync(d, ldp * es, A, h->lda * es, h->n * es, h->m,
+                                  dev_a ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->st));
     h->A = d;
-    h->lda = h->n;
+    h->lda = ldp;
   }
   if (W1) {
     if (is_device_ptr(W1)) h->W1 = W1;
@@ -432,13 +441,14 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
 
   // ---- sizes of the per-iteration kernels
   const int64_t k = h->k, n = h->n, nk = h->nk, t = h->t, kp = h->kp;
-  h->rp = row_pass_rp((int)(t + k));
-  if (h->rp < 0 || kp > 128) return fail(h, WLR_EINVAL, "this build supports r <= 128 and k <= 128");
+  h->rp = row_pass_rp((int)kp);                  // row pass output: the k (padded) columns of X1
+  if (h->rp < 0 || kp > 128 || t > 32) return fail(h, WLR_EINVAL, "this build supports k <= 128 and r - k <= 32");
+  h->KA = (int)round_up(n, 32);
   const int tm = row_pass_tm(h->rp);
-  const size_t rsm = h->dtype == WLR_F32 ? row_pass_smem<float>(h->rp, h->uniform, (int)k, (int)t, (int)kp)
-                                         : row_pass_smem<double>(h->rp, h->uniform, (int)k, (int)t, (int)kp);
-  h->nwc = h->dtype == WLR_F32 ? row_pass_chol_warps<float>(h->rp, h->uniform, (int)k, (int)t, (int)kp)
-                               : row_pass_chol_warps<double>(h->rp, h->uniform, (int)k, (int)t, (int)kp);
+  const size_t rsm = h->dtype == WLR_F32 ? row_pass_smem<float>(h->rp, h->uniform, (int)k, (int)kp)
+                                         : row_pass_smem<double>(h->rp, h->uniform, (int)k, (int)kp);
+  h->nwc = h->dtype == WLR_F32 ? row_pass_chol_warps<float>(h->rp, h->uniform, (int)k, (int)kp)
+                               : row_pass_chol_warps<double>(h->rp, h->uniform, (int)k, (int)kp);
   if (rsm > 227 * 1024 || h->nwc < 1)
     return fail(h, WLR_EINVAL, "row-pass shared memory exceeds 227 KB for this (k, r)");
   const int64_t ntiles = ceil_div(h->m, tm);
@@ -469,11 +479,20 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   }
 
   // ---- allocations
-  const int64_t wt_rows = round_up(n - h->k0, 32) + 32;
+  const int64_t wt_rows = h->KA + round_up(kp, 32);    // [A | X1_p] rows of the linear update
   if ((s = dalloc(h, &h->X[0], (size_t)h->m * kp * es)) != WLR_OK) return s;
   if ((s = dalloc(h, &h->X[1], (size_t)h->m * kp * es)) != WLR_OK) return s;
   if ((s = dalloc(h, &h->Dl, (size_t)h->m * kp * es)) != WLR_OK) return s;
   if ((s = dalloc(h, &h->Wt, (size_t)wt_rows * h->rp * es)) != WLR_OK) return s;
+  {   // TMA tensor maps: 128-byte x BM boxes (SWIZZLE_128B) of A and X1, 32-row boxes of Wt
+    const uint32_t pe = (uint32_t)(128 / es), bm = (uint32_t)row_pass_tm(h->rp);
+    bool ok = make_tmap_2d(&h->tmA, h->A, (int)es, (uint64_t)n, (uint64_t)h->m, (uint64_t)h->lda * es, pe, bm, true);
+    for (int i = 0; i < 2; ++i)
+      ok = ok && make_tmap_2d(&h->tmX[i], h->X[i], (int)es, (uint64_t)kp, (uint64_t)h->m, (uint64_t)kp * es, pe, bm, true);
+    ok = ok && make_tmap_2d(&h->tmW, h->Wt, (int)es, (uint64_t)h->rp, (uint64_t)wt_rows, (uint64_t)h->rp * es,
+                            (uint32_t)h->rp, 32u, false);
+    if (!ok) return fail(h, WLR_ECUDA, "cuTensorMapEncodeTiled failed (TMA descriptors)");
+  }
   if ((s = dalloc(h, &h->CVop, (size_t)std::max<int64_t>(k * t, 1) * es)) != WLR_OK) return s;
   if ((s = dalloc(h, &h->Kop, (size_t)k * k * es)) != WLR_OK) return s;
   if ((s = dalloc_t(h, &h->inc_part, (size_t)h->nsplit * k * h->nz)) != WLR_OK) return s;
@@ -759,26 +778,55 @@ extern "C" wlr_status wlr_result(wlr_handle h, void* X1, int64_t ldx1, void* C, 
   if (B || X2) {
     void* Bd = nullptr;
     CUDA_TRY(h, cudaMalloc(&Bd, (size_t)h->m * h->t * es + 16));
+    // B = A2 V - X1 (C V) as the same streaming GEMM: Wb = [0; V; -C V]  (host-built, small)
+    const int rpb = row_pass_rp((int)h->t);
+    const int64_t wrows = h->KA + round_up(h->kp, 32);
+    std::vector<double> v((size_t)h->nk * h->t), cv((size_t)h->k * h->t);
+    CUDA_TRY(h, cudaMemcpyAsync(v.data(), h->V[cur], v.size() * 8, cudaMemcpyDeviceToHost, h->st));
+    CUDA_TRY(h, cudaMemcpyAsync(cv.data(), h->CV[cur], cv.size() * 8, cudaMemcpyDeviceToHost, h->st));
+    CUDA_TRY(h, cudaStreamSynchronize(h->st));
+    std::vector<double> wb((size_t)wrows * rpb, 0.0);
+    for (int64_t c = 0; c < h->nk; ++c)
+      for (int64_t j = 0; j < h->t; ++j) wb[(size_t)(h->k + c) * rpb + j] = v[(size_t)c * h->t + j];
+    for (int64_t q = 0; q < h->k; ++q)
+      for (int64_t j = 0; j < h->t; ++j) wb[(size_t)(h->KA + q) * rpb + j] = -cv[(size_t)q * h->t + j];
+    void* Wbd = nullptr;
+    CUDA_TRY(h, cudaMalloc(&Wbd, wb.size() * es));
+    if (h->dtype == WLR_F32) {
+      std::vector<float> wf(wb.begin(), wb.end());
+      CUDA_TRY(h, cudaMemcpy(Wbd, wf.data(), wf.size() * 4, cudaMemcpyHostToDevice));
+    } else {
+      CUDA_TRY(h, cudaMemcpy(Wbd, wb.data(), wb.size() * 8, cudaMemcpyHostToDevice));
+    }
+    CUtensorMap tmB{};
+    if (!make_tmap_2d(&tmB, Wbd, (int)es, (uint64_t)rpb, (uint64_t)wrows, (uint64_t)rpb * es, (uint32_t)rpb, 32u, false)) {
+      cudaFree(Wbd); cudaFree(Bd);
+      return fail(h, WLR_ECUDA, "cuTensorMapEncodeTiled failed (result)");
+    }
     cudaError_t e;
     if (h->dtype == WLR_F32) {
       RowPassArgs<float> a{};
+      a.tmA = h->tmA; a.tmX = h->tmX[cur]; a.tmW = tmB;
       a.A = (const float*)h->A; a.lda = h->lda; a.W1 = (const float*)h->W1; a.ldw = h->ldw;
-      a.w2s = (float)(h->w1s * h->w1s); a.Xold = (const float*)h->X[cur]; a.Xnew = nullptr; a.nwc = h->nwc;
-      a.Wt = (const float*)h->Wt; a.CV = (const float*)h->CVop; a.Kmat = (const float*)h->Kop;
+      a.Xold = (const float*)h->X[cur]; a.nwc = h->nwc;
+      a.Wt = (const float*)Wbd; a.KA = h->KA;
       a.Bout = (float*)Bd; a.ldb = h->t; a.fw_part = h->fw_part; a.flags = h->flags;
-      a.m = h->m; a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.k0 = (int)h->k0; a.t = (int)h->t;
+      a.m = h->m; a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.no = (int)h->t;
       a.vec_ok = (h->lda % 4 == 0) && ((uintptr_t)h->A % 16 == 0);
-      e = launch_row_pass<float>(a, h->rp, h->uniform, 1, h->rp_grid, h->st);
+      e = launch_row_pass<float>(a, rpb, true, 1, h->rp_grid, h->st);
     } else {
       RowPassArgs<double> a{};
+      a.tmA = h->tmA; a.tmX = h->tmX[cur]; a.tmW = tmB;
       a.A = (const double*)h->A; a.lda = h->lda; a.W1 = (const double*)h->W1; a.ldw = h->ldw;
-      a.w2s = h->w1s * h->w1s; a.Xold = (const double*)h->X[cur]; a.Xnew = nullptr; a.nwc = h->nwc;
-      a.Wt = (const double*)h->Wt; a.CV = (const double*)h->CVop; a.Kmat = (const double*)h->Kop;
+      a.Xold = (const double*)h->X[cur]; a.nwc = h->nwc;
+      a.Wt = (const double*)Wbd; a.KA = h->KA;
       a.Bout = (double*)Bd; a.ldb = h->t; a.fw_part = h->fw_part; a.flags = h->flags;
-      a.m = h->m; a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.k0 = (int)h->k0; a.t = (int)h->t;
+      a.m = h->m; a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.no = (int)h->t;
       a.vec_ok = (h->lda % 4 == 0) && ((uintptr_t)h->A % 16 == 0);
-      e = launch_row_pass<double>(a, h->rp, h->uniform, 1, h->rp_grid, h->st);
+      e = launch_row_pass<double>(a, rpb, true, 1, h->rp_grid, h->st);
     }
+    cudaStreamSynchronize(h->st);
+    cudaFree(Wbd);
     if (e != cudaSuccess) { cudaFree(Bd); return fail(h, WLR_ECUDA, std::string("result row pass: ") + cudaGetErrorString(e)); }
     if (B) {
       if (ldb < h->t) { cudaFree(Bd); return fail(h, WLR_EINVAL, "ldb < r-k"); }
@@ -812,6 +860,12 @@ extern "C" wlr_status wlr_result(wlr_handle h, void* X1, int64_t ldx1, void* C, 
 extern "C" wlr_status wlr_debug_state(wlr_handle h, const char* name, double* out, int64_t cap,
                                       int64_t* count) {
   if (!h || !name) return fail(h, WLR_EINVAL, "null argument");
+  if (std::string(name) == "ktime") {          // timestamps of the last launched K3 half,
+    CUDA_TRY(h, cudaStreamSynchronize(h->st)); // read without launching a pending one
+    if (count) *count = 64;
+    if (out) CUDA_TRY(h, cudaMemcpy(out, h->tdbg, (size_t)std::min<int64_t>(cap, 64) * 8, cudaMemcpyDeviceToHost));
+    return WLR_OK;
+  }
   wlr_status s = check_flags(h);
   if (s != WLR_OK) return s;
   const int cur = h->par;

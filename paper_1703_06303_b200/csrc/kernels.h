@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace wlr {
 
@@ -24,26 +25,34 @@ void launch_validate(const T* A, int64_t lda, int64_t m, int n, const T* W1, int
 // ---------------------------------------------------------------- row pass (rowpass.cu)
 template <typename T>
 struct RowPassArgs {
+  // TMA tensor maps (SWIZZLE_128B for A and X1_p boxes of 128 B x BM rows; Wt plain)
+  CUtensorMap tmA, tmX, tmW;
   const T* A; int64_t lda;          // m x n (this rank's rows)
   const T* W1; int64_t ldw;         // m x k or nullptr (uniform)
   T w2s;                            // uniform weight squared
   const T* Xold; T* Xnew;           // m x kp
   T* Dnew;                          // m x kp  Delta = Xnew - Xold (stored values)
   int nwc;                          // warps running per-row Cholesky (non-uniform W1)
-  const T* Wt;                      // (n-k0 padded to 32) x RP : rows c-k0 = [V(c-k,:) | C(:,c-k)^T | 0]
-  const T* CV;                      // k x t  = C V
-  const T* Kmat;                    // k x k  : K^{-1} (uniform) or C C^T
-  T* Bout; int64_t ldb;             // MODE_RESULT output
+  // Linear row update: out = [A | X1_p] Wt, Wt is (KA + KX) x RP with rows
+  // [0, n) for the columns of A and [KA, KA + kp) for X1_p (KA = n rounded up to 32):
+  //   uniform W1    : Wt = [w^2 K^{-1}; U K^{-1}; P K^{-1}]  -> out = X1_{p+1} rows
+  //   non-uniform   : Wt = [0; U; P]                        -> out = e - A1 . W1^2
+  //   MODE_RESULT   : Wt = [0; V; -C V]                      -> out = B rows
+  // with U = C^T - V (C V)^T ((n-k) x k), P = (C V)(C V)^T, K = w^2 I + C C^T.
+  const T* Wt;
+  int KA;                           // row offset of the X1_p block in Wt
+  const T* Kmat;                    // k x k C C^T (non-uniform) or unused
+  T* Bout; int64_t ldb;             // MODE_RESULT output (m x t)
   double* fw_part;                  // gridDim.x partials
   int* flags;
   const void* pf_ptr[6]; int64_t pf_bytes[6];   // L2 prefetch of the next small step's inputs
-  int64_t m; int n, k, kp, k0, t;
+  int64_t m; int n, k, kp, no;      // no = output columns (kp, or t for MODE_RESULT)
   int vec_ok;                       // A rows 16-byte aligned at multiples of 4 elements
 };
 int row_pass_rp(int r);
 int row_pass_tm(int rp);
-template <typename T> size_t row_pass_smem(int rp, bool uniform, int k, int t, int kp);
-template <typename T> int row_pass_chol_warps(int rp, bool uniform, int k, int t, int kp);
+template <typename T> size_t row_pass_smem(int rp, bool uniform, int k, int kp);
+template <typename T> int row_pass_chol_warps(int rp, bool uniform, int k, int kp);
 template <typename T>
 cudaError_t launch_row_pass(const RowPassArgs<T>& a, int rp, bool uniform, int mode, int grid,
                             cudaStream_t st);
@@ -81,6 +90,7 @@ struct SSPlan {
 
 struct SmallArgs {
   int k, nk, t, b, kp, k0, rp;      // dims; b = eigen block width (t <= b <= 32)
+  int KA;                           // row offset of the X1_p block of the row-pass Wt
   int mode;                         // 0: init (G, M given), 1: iteration (apply increments)
   int dtype;                        // 0 fp32 operands, 1 fp64 operands
   int uniform; double w2;           // uniform weight squared

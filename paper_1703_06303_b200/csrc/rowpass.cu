@@ -79,7 +79,7 @@ template <> struct RowPassShape<32>  { static constexpr int BM = 64, TC = 4; };
 template <> struct RowPassShape<64>  { static constexpr int BM = 64, TC = 8; };
 template <> struct RowPassShape<128> { static constexpr int BM = 32, TC = 8; };
 
-constexpr int kRowKC = 32;        // reduction chunk (columns of A2)
+constexpr int kRowKC = 32;        // reduction chunk (columns of [A | X1_p])
 constexpr int kRowKG = 4;         // k-groups (in-CTA split-K); each takes 8 k of a chunk
 constexpr int kRowTR = 8;         // rows per thread (interleaved by BM / 8)
 constexpr int kRowThreads = 256;
@@ -88,74 +88,95 @@ constexpr int kRowThreads = 256;
 __host__ __device__ inline int chol_packed(int kp) { return kp * (kp + 1) / 2; }
 
 template <typename T, int RP>
-struct RowPassLayout {            // shared memory layout (elements of T)
+struct RowPassLayout {            // shared memory layout (elements of T; base 1024-byte aligned)
   using S = RowPassShape<RP>;
   static constexpr int BM = S::BM;
-  static constexpr int ALD = kRowKC + 16 / (int)sizeof(T);      // padded A row (16 B)
-  static constexpr int kA = BM * ALD;                           // one A stage
+  static constexpr int PE = 128 / (int)sizeof(T);               // elements per 128-byte panel row
+  static constexpr int NP = kRowKC / PE;                        // panels per A chunk (1 fp32, 2 fp64)
+  static constexpr int kA = NP * BM * PE;                       // one A stage (SWIZZLE_128B panels)
   static constexpr int kB = kRowKC * RP;                        // one Wt stage
   static constexpr int YLD = RP + 1;
-  static constexpr int oA = 0, oB = 2 * kA, oY = oB + 2 * kB, oX = oY + BM * YLD;
-  // then: X1_p tile [BM][kp], A1 tile [BM][kp], e tile [BM][kp], b tile [BM][32],
-  //       K^{-1} or C C^T [k][k], C V [k][t], per-warp packed L (non-uniform)
+  static constexpr int NST = 4;                                 // TMA pipeline stages
+  static constexpr int oA = 0, oB = NST * kA, oStEnd = oB + NST * kB;
+  // epilogue buffers alias the stages (free once the mainloop is done): Ys [BM][RP+1] at 0,
+  // then the e tile [BM][kp] (non-uniform)
+  static constexpr int oY = 0, oE = BM * YLD;
+  static constexpr int ALIGN = 1024 / (int)sizeof(T);           // SWIZZLE_128B destinations
+};
+
+__host__ __device__ inline int64_t align_up_i(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+// offsets (elements) of the X1_p / A1 staging panels and of the tail buffers
+template <typename T, int RP>
+struct RowPassTail {
+  int64_t oXs, oA1s, oK, oL, end;
+  __host__ __device__ RowPassTail(bool uniform, int k, int kp, int nwc) {
+    using L = RowPassLayout<T, RP>;
+    const int npk = (kp + L::PE - 1) / L::PE;
+    const int64_t alias = (int64_t)L::oE + (uniform ? 0 : (int64_t)L::BM * kp);
+    oXs = align_up_i(alias > L::oStEnd ? alias : L::oStEnd, L::ALIGN);
+    oA1s = oXs + (int64_t)npk * L::BM * L::PE;
+    oK = oA1s + (int64_t)npk * L::BM * L::PE;
+    oL = oK + (uniform ? 0 : (int64_t)k * k);
+    end = oL + (uniform ? 0 : (int64_t)nwc * chol_packed(kp));
+  }
 };
 
 template <typename T, int RP>
-size_t row_pass_smem_elems(bool uniform, int k, int t, int kp, int nwc) {
-  using L = RowPassLayout<T, RP>;
-  size_t n = (size_t)L::oX + 3 * (size_t)L::BM * kp + (size_t)L::BM * 32 + (size_t)k * kp + (size_t)k * t;
-  if (!uniform) n += (size_t)nwc * chol_packed(kp);
-  return n;
+size_t row_pass_smem_elems(bool uniform, int k, int kp, int nwc) {
+  return (size_t)RowPassTail<T, RP>(uniform, k, kp, nwc).end + RowPassLayout<T, RP>::ALIGN;
 }
 
 // warps that can hold a packed k x k factor in the remaining shared memory (<= 8)
 template <typename T, int RP>
-int row_pass_nwc(bool uniform, int k, int t, int kp) {
+int row_pass_nwc(bool uniform, int k, int kp) {
   if (uniform) return 8;
-  const size_t base = row_pass_smem_elems<T, RP>(true, k, t, kp, 0);
+  const size_t base = row_pass_smem_elems<T, RP>(false, k, kp, 0);
   const size_t cap = 227 * 1024 / sizeof(T);
   if (base >= cap) return 0;
   return (int)std::min<size_t>(8, (cap - base) / chol_packed(kp));
 }
 
 template <typename T, int RP, bool UNIFORM, int MODE>
-__global__ void __launch_bounds__(kRowThreads)
-row_pass_kernel(RowPassArgs<T> a) {
+__global__ void __launch_bounds__(kRowThreads, RP <= 32 ? 3 : 1)
+row_pass_kernel(const __grid_constant__ RowPassArgs<T> a) {
   using S = RowPassShape<RP>;
   using L = RowPassLayout<T, RP>;
-  constexpr int BM = S::BM, TC = S::TC, TR = kRowTR, KG = kRowKG, ALD = L::ALD;
+  constexpr int BM = S::BM, TC = S::TC, TR = kRowTR, KG = kRowKG, PE = L::PE, NST = L::NST;
   constexpr int THC = RP / TC;                 // threads along columns (per k-group)
   constexpr int GT = (BM / TR) * THC;          // threads per k-group
   static_assert(GT * KG == kRowThreads, "thread tile");
   constexpr int KPG = kRowKC / KG;             // k per group per chunk (8)
-  constexpr int VE = 16 / (int)sizeof(T);      // elements per 16-byte copy
+  constexpr int VE = 16 / (int)sizeof(T);      // elements per 16-byte chunk
   constexpr int RS = BM / TR;                  // row interleave stride
 
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* sm = reinterpret_cast<T*>(smem_raw);
-  const int kp = a.kp, k = a.k, t = a.t;
-  T* As = sm + L::oA;                          // [2][BM][ALD]
-  T* Bs = sm + L::oB;                          // [2][KC][RP]
-  T* Ys = sm + L::oY;                          // [BM][RP+1]
-  T* Xs = sm + L::oX;                          // [BM][kp]  X1_p rows of the tile
-  T* A1s = Xs + BM * kp;                       // [BM][kp]  A1 columns of the tile
-  T* Es = A1s + BM * kp;                       // [BM][kp]  e, then the solution
-  T* Bt = Es + BM * kp;                        // [BM][32]  b
-  T* sK = Bt + BM * 32;                        // [k][k]    K^{-1} (uniform) or C C^T
-  T* sCV = sK + k * kp;                        // [k][t]
-  T* sL = sCV + k * t;                         // per-warp packed L (non-uniform)
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  T* sm = reinterpret_cast<T*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t full[NST];
+  __shared__ __align__(8) uint64_t epb;
+  const int kp = a.kp, k = a.k;
+  const RowPassTail<T, RP> tl(UNIFORM || MODE == 1, k, kp, a.nwc);
+  T* As = sm + L::oA;                          // [NST][NP][BM][PE]  (swizzled panels)
+  T* Bs = sm + L::oB;                          // [NST][KC][RP]
+  T* Ys = sm + L::oY;                          // [BM][RP+1]   (aliases the stages)
+  T* Es = sm + L::oE;                          // [BM][kp]     (aliases; non-uniform)
+  T* Xs = sm + tl.oXs;                         // [npk][BM][PE] X1_p rows (swizzled)
+  T* A1s = sm + tl.oA1s;                       // [npk][BM][PE] A1 columns (swizzled)
+  T* sK = sm + tl.oK;                          // [k][k]    C C^T (non-uniform)
+  T* sL = sm + tl.oL;                          // per-warp packed L (non-uniform)
+  const int npk = (kp + PE - 1) / PE;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  auto pan = [&](const T* base, int r, int c) -> T {   // staged X1_p / A1 element (r, c)
+    return base[(c / PE) * (BM * PE) + swz128<T>(r, c % PE)];
+  };
 
-  // K^{-1} (uniform; leading dimension kp, zero-padded) or C C^T (leading dimension k)
-  if (UNIFORM) {
-    for (int i = threadIdx.x; i < k * kp; i += kRowThreads) {
-      const int r = i / kp, c = i - r * kp;
-      sK[i] = c < k ? a.Kmat[r * k + c] : T(0);
-    }
-  } else {
-    for (int i = threadIdx.x; i < k * k; i += kRowThreads) sK[i] = a.Kmat[i];
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NST; ++s) mbar_init(&full[s], 1);
+    mbar_init(&epb, 1);
+    mbar_init_fence();
   }
-  for (int i = threadIdx.x; i < k * t; i += kRowThreads) sCV[i] = a.CV[i];
+  if (!UNIFORM && MODE == 0)
+    for (int i = threadIdx.x; i < k * k; i += kRowThreads) sK[i] = a.Kmat[i];
   // The small step that follows is latency-bound and reads G_A and its previous state:
   // pull them into L2 while this pass streams A (bulk L2 prefetch, 64 KB per request).
   if (MODE == 0 && threadIdx.x < 32) {
@@ -172,60 +193,43 @@ row_pass_kernel(RowPassArgs<T> a) {
       }
     }
   }
+  __syncthreads();
 
   const int kg = threadIdx.x / GT, gt = threadIdx.x - kg * GT;
   const int ty = gt / THC, tx = gt - ty * THC;
-  const int nch = (int)ceil_div(a.n - a.k0, kRowKC);
+  const int nchA = a.KA / kRowKC;              // chunks over the columns of A
+  const int nch = nchA + (kp + kRowKC - 1) / kRowKC;   // + chunks over X1_p
   double fw = 0.0;
   const int64_t ntiles = ceil_div(a.m, BM);
-  const bool vec = a.vec_ok;
+  constexpr uint32_t kStageBytes = (uint32_t)((L::kA + L::kB) * sizeof(T));
 
-  // issue the async copies of chunk ch of the tile starting at row r0 into stage st
-  auto issue = [&](int64_t r0, int ch, int st) {
-    const int cb = a.k0 + ch * kRowKC;
-    T* as = As + st * L::kA;
-    for (int idx = threadIdx.x; idx < BM * (kRowKC / VE); idx += kRowThreads) {
-      const int rr = idx / (kRowKC / VE), cv = (idx % (kRowKC / VE)) * VE;
-      const int64_t row = r0 + rr;
-      const int col = cb + cv;
-      T* dst = as + rr * ALD + cv;
-      if (vec) {
-        int valid = a.n - col;
-        valid = valid > VE ? VE : (valid < 0 ? 0 : valid);
-        if (row >= a.m) valid = 0;
-        const T* src = valid > 0 ? a.A + row * a.lda + col : a.A;
-        cp_async16(dst, src, valid * (int)sizeof(T));
-      } else {
+  // thread 0: TMA loads of chunk c of the tile at row r0 into stage st
+  auto load_chunk = [&](int64_t r0, int c, int st) {
+    const bool isA = c < nchA;
+    const int cb = (isA ? c : c - nchA) * kRowKC;
+    mbar_expect_tx(&full[st], kStageBytes);
 #pragma unroll
-        for (int q = 0; q < VE; ++q)
-          dst[q] = (row < a.m && col + q < a.n) ? a.A[row * a.lda + col + q] : T(0);
-      }
-    }
-    T* bs = Bs + st * L::kB;
-    for (int idx = threadIdx.x; idx < kRowKC * RP / VE; idx += kRowThreads) {
-      const int rr = idx / (RP / VE), cv = (idx % (RP / VE)) * VE;
-      cp_async16(bs + rr * RP + cv, a.Wt + (int64_t)(ch * kRowKC + rr) * RP + cv, 16);   // padded
-    }
+    for (int p = 0; p < L::NP; ++p)
+      tma_load_2d(As + st * L::kA + p * BM * PE, isA ? &a.tmA : &a.tmX, &full[st], cb + p * PE, (int)r0);
+    tma_load_2d(Bs + st * L::kB, &a.tmW, &full[st], 0, isA ? cb : a.KA + cb);
   };
 
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  int64_t G = 0;                               // chunks consumed so far (stage / parity)
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
     const int64_t r0 = tile * BM;
-    __syncthreads();                           // previous tile's epilogue done with the stages
-    // epilogue operands of this tile (X1_p rows, A1 columns) ride with chunk 0
-    for (int idx = threadIdx.x; idx < BM * (kp / VE); idx += kRowThreads) {
-      const int rr = idx / (kp / VE), cv = (idx % (kp / VE)) * VE;
-      const int64_t row = r0 + rr;
-      const bool in = row < a.m;
-      cp_async16(Xs + rr * kp + cv, in ? a.Xold + row * kp + cv : a.Xold, in ? 16 : 0);
-      if (vec && cv + VE <= a.n) {
-        cp_async16(A1s + rr * kp + cv, in ? a.A + row * a.lda + cv : a.A, in ? 16 : 0);
-      } else {
-#pragma unroll
-        for (int q = 0; q < VE; ++q) A1s[rr * kp + cv + q] = (in && cv + q < a.n) ? a.A[row * a.lda + cv + q] : T(0);
+    __syncthreads();                           // previous tile's epilogue done with the smem
+    if (threadIdx.x == 0) {
+      fence_proxy_async();
+      if (MODE == 0) {   // epilogue operands of this tile: X1_p rows and A1 columns
+        mbar_expect_tx(&epb, (uint32_t)(2 * npk * BM * PE * sizeof(T)));
+        for (int pp = 0; pp < npk; ++pp) {
+          tma_load_2d(Xs + pp * BM * PE, &a.tmX, &epb, pp * PE, (int)r0);
+          tma_load_2d(A1s + pp * BM * PE, &a.tmA, &epb, pp * PE, (int)r0);
+        }
       }
+      for (int q = 0; q < NST - 1 && q < nch; ++q) load_chunk(r0, q, (int)((G + q) % NST));
     }
-    issue(r0, 0, 0);
-    cp_async_commit();
 
     T acc[TR][TC];
 #pragma unroll
@@ -234,21 +238,24 @@ row_pass_kernel(RowPassArgs<T> a) {
       for (int j = 0; j < TC; ++j) acc[i][j] = T(0);
 
     for (int ch = 0; ch < nch; ++ch) {
-      const int st = ch & 1;
-      if (ch + 1 < nch) issue(r0, ch + 1, st ^ 1);
-      cp_async_commit();
-      cp_async_wait<1>();
-      __syncthreads();
+      const int64_t g = G + ch;
+      const int st = (int)(g % NST);
+      if (threadIdx.x == 0 && ch + NST - 1 < nch) {   // refill the stage freed last iteration
+        fence_proxy_async();
+        load_chunk(r0, ch + NST - 1, (int)((g + NST - 1) % NST));
+      }
+      mbar_wait(&full[st], (uint32_t)((g / NST) & 1));
       const T* as = As + st * L::kA;
       const T* bs = Bs + st * L::kB;
 #pragma unroll
       for (int k4 = 0; k4 < KPG; k4 += VE) {
         const int kk0 = kg * KPG + k4;
+        const T* ap = as + (kk0 / PE) * (BM * PE);
         T av[TR][VE];
 #pragma unroll
         for (int i = 0; i < TR; ++i) {
           T tmp[VE];
-          lds_vec<T, VE>(as + (ty + i * RS) * ALD + kk0, tmp);
+          lds_vec<T, VE>(ap + swz128<T>(ty + i * RS, kk0 % PE), tmp);
 #pragma unroll
           for (int q = 0; q < VE; ++q) av[i][q] = tmp[q];
         }
@@ -262,73 +269,59 @@ row_pass_kernel(RowPassArgs<T> a) {
             for (int j = 0; j < TC; ++j) acc[i][j] = fma(av[i][q], bv[j], acc[i][j]);
         }
       }
-      __syncthreads();                         // stage st may be overwritten next iteration
+      __syncthreads();                         // stage st is free for the next refill
     }
+    G += nch;
     // fixed-order sum of the KG partial tiles into Ys
 #pragma unroll 1
-    for (int g = 0; g < KG; ++g) {
-      if (kg == g) {
+    for (int gg = 0; gg < KG; ++gg) {
+      if (kg == gg) {
 #pragma unroll
         for (int i = 0; i < TR; ++i)
 #pragma unroll
           for (int j = 0; j < TC; ++j) {
             T* y = Ys + (ty + i * RS) * L::YLD + tx * TC + j;
-            *y = g == 0 ? acc[i][j] : *y + acc[i][j];
+            *y = gg == 0 ? acc[i][j] : *y + acc[i][j];
           }
       }
       __syncthreads();
     }
     const int nrow = (int)((a.m - r0) < BM ? (a.m - r0) : BM);
 
-    // ---------------- epilogue (shared memory only; thread per output)
-    // b[r][j] = y_V[r][j] - sum_l X1_p[r][l] (CV)[l][j]
-    for (int o = threadIdx.x; o < nrow * t; o += kRowThreads) {
-      const int r = o / t, j = o - r * t;
-      T v = Ys[r * L::YLD + j];
-      for (int l = 0; l < k; ++l) v = fma(-Xs[r * kp + l], sCV[l * t + j], v);
-      Bt[r * 32 + j] = v;
-      if (MODE == 1) a.Bout[(r0 + r) * a.ldb + j] = v;
+    // ---------------- epilogue (shared memory; thread per output)
+    if (MODE == 1) {                           // wlr_result: B rows
+      for (int o = threadIdx.x; o < nrow * a.no; o += kRowThreads) {
+        const int r = o / a.no, j = o - r * a.no;
+        a.Bout[(r0 + r) * a.ldb + j] = Ys[r * L::YLD + j];
+      }
+      continue;
     }
-    if (MODE == 1) continue;
-    __syncthreads();
-    // e[r][l] = a1 w^2 + y_C[r][l] - sum_j b[r][j] (CV)[l][j]
-    for (int o = threadIdx.x; o < nrow * k; o += kRowThreads) {
-      const int r = o / k, l = o - r * k;
-      const T w2 = UNIFORM ? a.w2s : a.W1[(r0 + r) * a.ldw + l] * a.W1[(r0 + r) * a.ldw + l];
-      T e = fma(A1s[r * kp + l], w2, Ys[r * L::YLD + t + l]);
-      for (int j = 0; j < t; ++j) e = fma(-Bt[r * 32 + j], sCV[l * t + j], e);
-      Es[r * kp + l] = e;
-    }
-    __syncthreads();
-    if (UNIFORM) {
-      // x'[r][l..l+3] = sum_m e[r][m] (K^{-1})[m][l..l+3];  Delta = x' - x;  f_w
-      // (thread per row and 4 consecutive outputs: one broadcast e load per 4 FMA)
-      const int kq = kp / 4;
-      for (int o = threadIdx.x; o < nrow * kq; o += kRowThreads) {
-        const int r = o / kq, l0 = (o - r * kq) * 4;
-        T x[4] = {T(0), T(0), T(0), T(0)};
-        const T* er = Es + r * kp;
-        for (int mm = 0; mm < k; ++mm) {
-          const T e = er[mm];
-          const T* kr = sK + mm * kp + l0;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) x[q] = fma(e, kr[q], x[q]);
-        }
-        const int64_t gi = (r0 + r) * kp + l0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int l = l0 + q;
-          const T xv = l < k ? x[q] : T(0);
-          a.Xnew[gi + q] = xv;
-          a.Dnew[gi + q] = xv - Xs[r * kp + l];
-          if (l < k) {
-            const double d = (double)A1s[r * kp + l] - (double)xv;
-            fw += (double)a.w2s * d * d;
-          }
+    mbar_wait(&epb, (uint32_t)(it & 1));
+    if (UNIFORM) {                             // out = X1_{p+1} rows; Delta; f_w
+      for (int o = threadIdx.x; o < nrow * kp; o += kRowThreads) {
+        const int r = o / kp, l = o - r * kp;
+        const T x = l < k ? Ys[r * L::YLD + l] : T(0);
+        const int64_t gi = (r0 + r) * kp + l;
+        a.Xnew[gi] = x;
+        a.Dnew[gi] = x - pan(Xs, r, l);
+        if (l < k) {
+          const double d = (double)pan(A1s, r, l) - (double)x;
+          fw += (double)a.w2s * d * d;
         }
       }
     } else {
-      // K = C C^T + diag(w^2): warp per row, packed lower triangle P(i,j) = i(i+1)/2 + j
+      // e = out + A1 . W1^2, then x' = e (diag(W1^2) + C C^T)^{-1}: warp per row, packed
+      // lower triangle P(i,j) = i(i+1)/2 + j
+      for (int o = threadIdx.x; o < nrow * kp; o += kRowThreads) {
+        const int r = o / kp, l = o - r * kp;
+        T e = T(0);
+        if (l < k) {
+          const T w = a.W1[(r0 + r) * a.ldw + l];
+          e = fma(pan(A1s, r, l), w * w, Ys[r * L::YLD + l]);
+        }
+        Es[r * kp + l] = e;
+      }
+      __syncthreads();
       T* wL = sL + warp * chol_packed(kp);
       for (int rl = warp; rl < (warp < a.nwc ? nrow : 0); rl += a.nwc) {
         const int64_t g = r0 + rl;
@@ -379,10 +372,10 @@ row_pass_kernel(RowPassArgs<T> a) {
         for (int l = lane; l < kp; l += 32) {
           const T x = l < k ? we[l] : T(0);
           a.Xnew[g * kp + l] = x;
-          a.Dnew[g * kp + l] = x - Xs[rl * kp + l];
+          a.Dnew[g * kp + l] = x - pan(Xs, rl, l);
           if (l < k) {
             const double w = (double)a.W1[g * a.ldw + l];
-            const double d = (double)A1s[rl * kp + l] - (double)x;
+            const double d = (double)pan(A1s, rl, l) - (double)x;
             fw += w * w * d * d;
           }
         }
@@ -406,10 +399,13 @@ row_pass_kernel(RowPassArgs<T> a) {
 template <typename T, int RP, bool UNIFORM, int MODE>
 static cudaError_t launch_rp(const RowPassArgs<T>& a, int grid, cudaStream_t st) {
   auto kern = row_pass_kernel<T, RP, UNIFORM, MODE>;
-  const size_t smem = sizeof(T) * row_pass_smem_elems<T, RP>(UNIFORM, a.k, a.t, a.kp, a.nwc);
+  const size_t smem = sizeof(T) * row_pass_smem_elems<T, RP>(UNIFORM || MODE == 1, a.k, a.kp, a.nwc);
   static size_t configured = 0;            // cudaFuncSetAttribute once per size increase
   if (smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    // all of the unified L1/shared storage as shared memory, so 3 CTAs/SM fit
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     configured = smem;
   }
@@ -420,35 +416,35 @@ static cudaError_t launch_rp(const RowPassArgs<T>& a, int grid, cudaStream_t st)
 template <typename T, int RP>
 static cudaError_t dispatch_rp(const RowPassArgs<T>& a, bool uniform, int mode, int grid,
                                cudaStream_t st) {
-  if (uniform) return mode ? launch_rp<T, RP, true, 1>(a, grid, st) : launch_rp<T, RP, true, 0>(a, grid, st);
-  return mode ? launch_rp<T, RP, false, 1>(a, grid, st) : launch_rp<T, RP, false, 0>(a, grid, st);
+  if (mode) return launch_rp<T, RP, true, 1>(a, grid, st);
+  return uniform ? launch_rp<T, RP, true, 0>(a, grid, st) : launch_rp<T, RP, false, 0>(a, grid, st);
 }
 
 int row_pass_rp(int r) { return r <= 16 ? 16 : r <= 32 ? 32 : r <= 64 ? 64 : r <= 128 ? 128 : -1; }
 int row_pass_tm(int rp) { return rp == 128 ? RowPassShape<128>::BM : RowPassShape<32>::BM; }
 
 template <typename T>
-size_t row_pass_smem(int rp, bool uniform, int k, int t, int kp) {
+size_t row_pass_smem(int rp, bool uniform, int k, int kp) {
   switch (rp) {
-    case 16: return sizeof(T) * row_pass_smem_elems<T, 16>(uniform, k, t, kp, row_pass_nwc<T, 16>(uniform, k, t, kp));
-    case 32: return sizeof(T) * row_pass_smem_elems<T, 32>(uniform, k, t, kp, row_pass_nwc<T, 32>(uniform, k, t, kp));
-    case 64: return sizeof(T) * row_pass_smem_elems<T, 64>(uniform, k, t, kp, row_pass_nwc<T, 64>(uniform, k, t, kp));
-    default: return sizeof(T) * row_pass_smem_elems<T, 128>(uniform, k, t, kp, row_pass_nwc<T, 128>(uniform, k, t, kp));
+    case 16: return sizeof(T) * row_pass_smem_elems<T, 16>(uniform, k, kp, row_pass_nwc<T, 16>(uniform, k, kp));
+    case 32: return sizeof(T) * row_pass_smem_elems<T, 32>(uniform, k, kp, row_pass_nwc<T, 32>(uniform, k, kp));
+    case 64: return sizeof(T) * row_pass_smem_elems<T, 64>(uniform, k, kp, row_pass_nwc<T, 64>(uniform, k, kp));
+    default: return sizeof(T) * row_pass_smem_elems<T, 128>(uniform, k, kp, row_pass_nwc<T, 128>(uniform, k, kp));
   }
 }
+template size_t row_pass_smem<float>(int, bool, int, int);
+template size_t row_pass_smem<double>(int, bool, int, int);
 template <typename T>
-int row_pass_chol_warps(int rp, bool uniform, int k, int t, int kp) {
+int row_pass_chol_warps(int rp, bool uniform, int k, int kp) {
   switch (rp) {
-    case 16: return row_pass_nwc<T, 16>(uniform, k, t, kp);
-    case 32: return row_pass_nwc<T, 32>(uniform, k, t, kp);
-    case 64: return row_pass_nwc<T, 64>(uniform, k, t, kp);
-    default: return row_pass_nwc<T, 128>(uniform, k, t, kp);
+    case 16: return row_pass_nwc<T, 16>(uniform, k, kp);
+    case 32: return row_pass_nwc<T, 32>(uniform, k, kp);
+    case 64: return row_pass_nwc<T, 64>(uniform, k, kp);
+    default: return row_pass_nwc<T, 128>(uniform, k, kp);
   }
 }
-template int row_pass_chol_warps<float>(int, bool, int, int, int);
-template int row_pass_chol_warps<double>(int, bool, int, int, int);
-template size_t row_pass_smem<float>(int, bool, int, int, int);
-template size_t row_pass_smem<double>(int, bool, int, int, int);
+template int row_pass_chol_warps<float>(int, bool, int, int);
+template int row_pass_chol_warps<double>(int, bool, int, int);
 
 template <typename T>
 cudaError_t launch_row_pass(const RowPassArgs<T>& a, int rp, bool uniform, int mode, int grid,
@@ -468,15 +464,16 @@ template cudaError_t launch_row_pass<double>(const RowPassArgs<double>&, int, bo
 // Thread tile 8 (q) x 4 (columns); warp w owns q in [8w, 8w+8) and lanes 32 column groups,
 // so the Delta operand is a warp broadcast and the Z operand one LDS.128 per lane.
 // Z = [A(:, k0:n) | X1_p | Delta]; stages arrive by cp.async (double-buffered).
-constexpr int kIncRC = 32;          // rows per stage
+constexpr int kIncRC = 16;          // rows per stage
+constexpr int kIncNST = 4;          // cp.async pipeline stages
 constexpr int kIncBN = 128;         // columns per CTA
-constexpr int kIncFlush = 8;        // stages per fp32 chunk (256 rows), then fp64
+constexpr int kIncFlush = 16;       // stages per fp32 chunk (256 rows), then fp64
 
 int incr_bm(int kp) { return kp <= 32 ? 32 : kp <= 64 ? 64 : kp <= 128 ? 128 : -1; }
 int incr_bn(int) { return kIncBN; }
 
 template <typename T, int BM>
-size_t incr_smem_bytes() { return sizeof(T) * 2 * (size_t)kIncRC * (BM + kIncBN); }
+size_t incr_smem_bytes() { return sizeof(T) * kIncNST * (size_t)kIncRC * (BM + kIncBN); }
 
 template <typename T, int BM>
 __global__ void __launch_bounds__(BM * 4) incr_kernel(IncrArgs<T> a) {
@@ -485,7 +482,7 @@ __global__ void __launch_bounds__(BM * 4) incr_kernel(IncrArgs<T> a) {
   constexpr int VE = 16 / (int)sizeof(T);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* Ds = reinterpret_cast<T*>(smem_raw);       // [2][RC][BM]
-  T* Zs = Ds + 2 * kIncRC * BM;                 // [2][RC][BN]
+  T* Zs = Ds + kIncNST * kIncRC * BM;           // [NST][RC][BN]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q0 = warp * 8, c0 = lane * 4;
   const int j0 = blockIdx.x * BN;
@@ -573,16 +570,17 @@ __global__ void __launch_bounds__(BM * 4) incr_kernel(IncrArgs<T> a) {
     first = false;
   };
   const int nst = (int)ceil_div(re - rb0, kIncRC);
-  if (nst > 0) {
-    issue(rb0, 0);
+#pragma unroll
+  for (int q = 0; q < kIncNST - 1; ++q) {
+    if (q < nst) issue(rb0 + (int64_t)q * kIncRC, q);
     cp_async_commit();
   }
   int stage = 0;
   for (int s = 0; s < nst; ++s) {
-    const int st = s & 1;
-    if (s + 1 < nst) issue(rb0 + (int64_t)(s + 1) * kIncRC, st ^ 1);
+    const int st = s % kIncNST;
+    if (s + kIncNST - 1 < nst) issue(rb0 + (int64_t)(s + kIncNST - 1) * kIncRC, (s + kIncNST - 1) % kIncNST);
     cp_async_commit();
-    cp_async_wait<1>();
+    cp_async_wait<kIncNST - 1>();
     __syncthreads();
     const T* ds = Ds + st * kIncRC * BM;
     const T* zs = Zs + st * kIncRC * BN;
@@ -612,6 +610,8 @@ static cudaError_t launch_incr_bm(const IncrArgs<T>& a, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     configured = true;
   }

@@ -59,7 +59,7 @@ bool small_step_plan(SmallArgs& a, int CL) {
   p.oWk = take((int64_t)k * b);
   p.oCinE = take(t + kt);
   p.oSmall = take(so.len);
-  p.oRed = take((int64_t)p.KS * SL * b);
+  p.oRed = take(std::max<int64_t>((int64_t)p.KS * SL * b, SL * (int64_t)k));   // also U rows
   if (o > kSmemLimit) return false;
   auto opt = [&](int64_t n) -> int64_t {
     if (o + round_up(n, 2) > kSmemLimit) return -1;

@@ -848,6 +848,8 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
       return;
     }
     // ---------------------------------------------- C: operands of the next row pass
+    // Linear row update: Wt = [w^2 K^{-1}; U K^{-1}; P K^{-1}] for uniform W1,
+    // [0; U; P] otherwise, with U = C'^T - V' (C'V')^T, P = (C'V')(C'V')^T, K = w^2 I + C'C'^T.
     const double* Y = s.sm + buf[iY];          // V' = Y[:, :t]
     double* my = a.xchg + (int64_t)s.c * p.flen;
     {   // slice partials of C' C'^T (k x k) and C' V' (k x t)
@@ -855,42 +857,115 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
                        {Cs, ldc, 1, Y, 1, b, k, t, my + kk}};
       slice_tn<2>(s.nl, d);
     }
-    {
-      const int RP = a.rp;
-      for (int64_t idx = threadIdx.x; idx < (int64_t)s.nl * RP; idx += kSST) {   // Wt rows
-        const int cl = (int)(idx / RP), j = (int)(idx % RP);
-        double v = 0.0;
-        if (j < t) v = Y[cl * b + j];
-        else if (j < t + k) v = Cs[(int64_t)(j - t) * ldc + cl];
-        const int64_t o = (int64_t)(k + s.rs + cl - a.k0) * RP + j;
-        if (a.dtype) reinterpret_cast<double*>(a.Wt)[o] = v;
-        else reinterpret_cast<float*>(a.Wt)[o] = (float)v;
-      }
-      for (int idx = threadIdx.x; idx < s.nl * t; idx += kSST) {
-        const int r = idx / t, j = idx - r * t;
-        a.V_out[(int64_t)(s.rs + r) * t + j] = Y[r * b + j];
-      }
-      for (int idx = threadIdx.x; idx < s.nl * b; idx += kSST) a.Y[(int64_t)s.rs * b + idx] = Y[idx];
+    for (int idx = threadIdx.x; idx < s.nl * t; idx += kSST) {
+      const int r = idx / t, j = idx - r * t;
+      a.V_out[(int64_t)(s.rs + r) * t + j] = Y[r * b + j];
     }
+    for (int idx = threadIdx.x; idx < s.nl * b; idx += kSST) a.Y[(int64_t)s.rs * b + idx] = Y[idx];
     tmark(s, a);                               // operand partials
     cg::this_cluster().sync();                 // partials in global memory (cluster scope)
-    const int flen = kk + kt;
-    {   // reduce-scatter of the k^2 + kt partials
-      const int fc = (flen + s.CL - 1) / s.CL;
-      const int f0 = s.c * fc, f1 = min(flen, f0 + fc);
-      for (int i = f0 + threadIdx.x; i < f1; i += kSST) {
-        double v[16];
+    // every CTA sums all k^2 + kt partials in the same fixed order: CC' into Gq (+ w^2 I when
+    // uniform, for the inverse), C'V' into cvs
+    double* cvs = s.sm + p.oCinE;              // k x t (the residual region is free now)
+#pragma unroll 1
+    for (int i = threadIdx.x; i < kk + kt; i += kSST) {
+      double v[16];
 #pragma unroll
-        for (int c = 0; c < 16; ++c) v[c] = c < s.CL ? __ldcg(a.xchg + (int64_t)c * p.flen + i) : 0.0;
-        double acc = 0.0;
+      for (int c = 0; c < 16; ++c) v[c] = c < s.CL ? __ldcg(a.xchg + (int64_t)c * p.flen + i) : 0.0;
+      double acc = 0.0;
 #pragma unroll
-        for (int c = 0; c < 16; ++c) acc += v[c];
-        a.red[i] = acc;
+      for (int c = 0; c < 16; ++c) acc += v[c];
+      if (i < kk) Gq[i] = acc;
+      else cvs[i - kk] = acc;
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int idx = threadIdx.x; idx < kk; idx += kSST) {   // symmetrise C'C'^T; K = w^2 I + CC'
+      const int i = idx / k, j = idx - i * k;
+      if (i < j) {
+        const double v = 0.5 * (Gq[idx] + Gq[j * k + i]);
+        Gq[idx] = v;
+        Gq[j * k + i] = v;
       }
     }
-    cg::this_cluster().sync();
+    __syncthreads();
+    if (s.c == 0) {
+      for (int idx = threadIdx.x; idx < kk; idx += kSST) {
+        if (!a.uniform) {
+          if (a.dtype) reinterpret_cast<double*>(a.Kop)[idx] = Gq[idx];
+          else reinterpret_cast<float*>(a.Kop)[idx] = (float)Gq[idx];
+        }
+      }
+      for (int idx = threadIdx.x; idx < kt; idx += kSST) a.CV_out[idx] = cvs[idx];
+    }
+    if (a.uniform) {
+      for (int i = threadIdx.x; i < k; i += kSST) Gq[i * k + i] += a.w2;
+      for (int idx = threadIdx.x; idx < kk && a.mode; idx += kSST) Xq[idx] = a.Ki[idx];
+      __syncthreads();
+      // K^{-1}: Newton-Schulz from the previous K^{-1}; sweep at init or as fallback
+      bool okk = a.mode ? ns_inverse(Gq, Xq, Rq, Pq, k, red) : false;
+      if (!okk) {
+        for (int idx = threadIdx.x; idx < kk; idx += kSST) Xq[idx] = Gq[idx];
+        __syncthreads();
+        if (!sweep_inverse(Xq, k, 0.0, sm + so.d0, sm + so.rb)) {
+          if (s.c == 0 && threadIdx.x == 0) raise_flag(a.flags, DF_ROWSPD);
+          cg::this_cluster().sync();
+          return;
+        }
+      }
+      if (s.c == 0)
+        for (int idx = threadIdx.x; idx < kk; idx += kSST) a.Ki[idx] = Xq[idx];
+    }
+    // U rows of this slice: u[c][q] = C'[q][c] - sum_j V'[c][j] (C'V')[q][j]   (into Red)
+    double* Us = s.sm + p.oRed;                // nl x k
+#pragma unroll 1
+    for (int idx = threadIdx.x; idx < s.nl * k; idx += kSST) {
+      const int c = idx / k, q = idx - c * k;
+      double v = Cs[(int64_t)q * ldc + c];
+      for (int j = 0; j < t; ++j) v = fma(-Y[c * b + j], cvs[q * t + j], v);
+      Us[idx] = v;
+    }
+    __syncthreads();
+    const int RP = a.rp;
+    auto put = [&](int64_t row, int l, double v) {
+      const int64_t o = row * RP + l;
+      if (a.dtype) reinterpret_cast<double*>(a.Wt)[o] = v;
+      else reinterpret_cast<float*>(a.Wt)[o] = (float)v;
+    };
+    // Wt rows k + rs + c (columns of A2 in this slice): u K^{-1} or u
+#pragma unroll 1
+    for (int idx = threadIdx.x; idx < s.nl * k; idx += kSST) {
+      const int c = idx / k, l = idx - c * k;
+      double v;
+      if (a.uniform) {
+        v = 0.0;
+        for (int q = 0; q < k; ++q) v = fma(Us[c * k + q], Xq[q * k + l], v);
+      } else {
+        v = Us[idx];
+      }
+      put(k + s.rs + c, l, v);
+    }
+    if (s.c == 0) {
+      // A1 rows (uniform: w^2 K^{-1}) and X1_p rows (P K^{-1} or P), P = (C'V')(C'V')^T
+#pragma unroll 1
+      for (int idx = threadIdx.x; idx < kk; idx += kSST) {
+        const int j = idx / k, l = idx - j * k;
+        if (a.uniform) put(j, l, a.w2 * Xq[idx]);
+        double v = 0.0;
+        if (a.uniform) {
+          for (int q = 0; q < k; ++q) {
+            double pjq = 0.0;
+            for (int i = 0; i < t; ++i) pjq = fma(cvs[j * t + i], cvs[q * t + i], pjq);
+            v = fma(pjq, Xq[q * k + l], v);
+          }
+        } else {
+          for (int i = 0; i < t; ++i) v = fma(cvs[j * t + i], cvs[l * t + i], v);
+        }
+        put(a.KA + j, l, v);
+      }
+    }
     if (s.c != 0) return;
-    // ---- CTA 0: small results for the deferred half, C V, K^{-1}
+    // ---- CTA 0: small results for the deferred half
     if (a.mode) {
       const double* Qb = sm + so.Qb;
       for (int idx = threadIdx.x; idx < t * t; idx += kSST) {
@@ -910,47 +985,7 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
       a.scal[7] = (double)nprod;
       a.flags[3] = outer;
     }
-    for (int idx = threadIdx.x; idx < kt; idx += kSST) {
-      const double v = __ldcg(a.red + kk + idx);
-      a.CV_out[idx] = v;
-      if (a.dtype) reinterpret_cast<double*>(a.CVop)[idx] = v;
-      else reinterpret_cast<float*>(a.CVop)[idx] = (float)v;
-    }
-    if (!a.uniform) {
-      for (int idx = threadIdx.x; idx < kk; idx += kSST) {
-        const int i = idx / k, j = idx - i * k;
-        const double v = 0.5 * (__ldcg(a.red + idx) + __ldcg(a.red + j * k + i));
-        if (a.dtype) reinterpret_cast<double*>(a.Kop)[idx] = v;
-        else reinterpret_cast<float*>(a.Kop)[idx] = (float)v;
-      }
-      tmark(s, a);
-      return;
-    }
-    // uniform W1: K^{-1} = (w^2 I + C'C'^T)^{-1}: Newton-Schulz from the previous K^{-1},
-    // sweep-operator inverse at init or as fallback
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < kk; idx += kSST) {
-      const int i = idx / k, j = idx - i * k;
-      Gq[idx] = 0.5 * (__ldcg(a.red + idx) + __ldcg(a.red + j * k + i)) + (i == j ? a.w2 : 0.0);
-      if (a.mode) Xq[idx] = a.Ki[idx];
-    }
-    __syncthreads();
-    bool okk = a.mode ? ns_inverse(Gq, Xq, Rq, Pq, k, red) : false;
-    if (!okk) {
-      for (int idx = threadIdx.x; idx < kk; idx += kSST) Xq[idx] = Gq[idx];
-      __syncthreads();
-      if (!sweep_inverse(Xq, k, 0.0, sm + so.d0, sm + so.rb)) {
-        if (threadIdx.x == 0) raise_flag(a.flags, DF_ROWSPD);
-        return;
-      }
-    }
-    for (int idx = threadIdx.x; idx < kk; idx += kSST) {
-      const double v = Xq[idx];
-      a.Ki[idx] = v;
-      if (a.dtype) reinterpret_cast<double*>(a.Kop)[idx] = v;
-      else reinterpret_cast<float*>(a.Kop)[idx] = (float)v;
-    }
-    tmark(s, a);                               // K^{-1}
+    tmark(s, a);                               // operands
   } else {
     // ================================== PART 2: objective, step norm, trace (deferred)
     const double fw = a.mode ? incOm[(int64_t)kk] : a.inc[0];
@@ -1216,11 +1251,16 @@ cudaError_t launch_ss(const SmallArgs& a, int part, cudaStream_t st) {
   cfg.blockDim = dim3(kSST);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = a.pl.CL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  // the deferred half competes with the next row pass for SMs: schedule its cluster first
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  at[1].id = cudaLaunchAttributePriority;
+  at[1].val.priority = hi;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = part == 2 ? 2 : 1;
   if (part == 1) return cudaLaunchKernelEx(&cfg, small_step_kernel<BT, 1>, a);
   return cudaLaunchKernelEx(&cfg, small_step_kernel<BT, 2>, a);
 }

@@ -1,0 +1,60 @@
+// tma.cuh -- TMA (cp.async.bulk.tensor) + mbarrier helpers for the streaming kernels.
+// Device side: raw PTX (sm_90+/sm_100a).  Host side: tensor-map encoding through the driver
+// entry point (no libcuda link needed; cudart is static).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace wlr {
+
+WLR_DEVI uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+WLR_DEVI void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+WLR_DEVI void mbar_init_fence() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+WLR_DEVI void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+WLR_DEVI void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+// generic-proxy accesses to smem before this point are ordered before later async-proxy
+// (TMA) writes to it
+WLR_DEVI void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+// 2D tile load global -> shared, completion signalled on bar (complete_tx bytes)
+WLR_DEVI void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c_inner, int c_outer) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c_inner), "r"(c_outer)
+      : "memory");
+}
+
+// element offset of (row r, column c) in a [rows][PE] panel written by TMA with
+// SWIZZLE_128B (PE = 128 / sizeof(T) elements per row; 16-byte chunks XOR row % 8)
+template <typename T>
+__host__ __device__ inline int swz128(int r, int c) {
+  constexpr int PE = 128 / (int)sizeof(T), CE = 16 / (int)sizeof(T);
+  return r * PE + ((((c / CE) ^ (r & 7))) * CE) + (c % CE);
+}
+
+// host: encode a 2D row-major tensor map (inner dim contiguous) -- returns false on failure
+bool make_tmap_2d(CUtensorMap* map, const void* base, int elem_bytes, uint64_t inner,
+                  uint64_t outer, uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer,
+                  bool swizzle128);
+
+}  // namespace wlr
