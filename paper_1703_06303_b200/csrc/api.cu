@@ -79,7 +79,7 @@ struct wlr_ctx {
   size_t es = 4;
   bool uniform = true;
   double w1s = 1.0;
-  int b = 0, rp = 0, bm = 0, nz = 0, nsplit = 0, rp_grid = 0, KA = 0;
+  int b = 0, rp = 0, rp_tr = 8, bm = 0, nz = 0, nsplit = 0, rp_grid = 0, KA = 0;
   int64_t rps = 0;
   SSPlan spl{};
   int nsm = 148;
@@ -92,14 +92,17 @@ struct wlr_ctx {
   CUtensorMap tmA{}, tmX[2]{}, tmW{};   // TMA descriptors of A, X1 (per buffer) and Wt
   int nwc = 8;                 // row-pass warps running per-row Cholesky
   void *Wt = nullptr, *CVop = nullptr, *Kop = nullptr;
-  double *inc_part = nullptr, *fw_part = nullptr, *inc = nullptr, *fw0 = nullptr;
+  double *inc_part = nullptr, *fw_part = nullptr, *fw0 = nullptr;
+  double* inc[2] = {nullptr, nullptr};   // packed increments, by iteration parity
   double* GA = nullptr;
   double a2sq = 0.0;
-  double *G[2] = {nullptr, nullptr}, *M[2] = {nullptr, nullptr}, *C[2] = {nullptr, nullptr};
-  double *Gi[2] = {nullptr, nullptr}, *Ki = nullptr, *gws = nullptr;   // G^{-1}, K^{-1}, K3 workspace
-  double *V[2] = {nullptr, nullptr}, *CV[2] = {nullptr, nullptr}, *th[2] = {nullptr, nullptr};
-  double *Y = nullptr, *k3x = nullptr;
-  double *xchg = nullptr, *red = nullptr, *scal = nullptr, *trace = nullptr;
+  // small-step state S_p (Grams, C, G^{-1}, Ritz block) in slot p mod 3: K3a(p) writes slot
+  // (p+1) mod 3 while the deferred K3b(p-1) still reads slots (p-1) and p mod 3
+  double *G[3] = {}, *M[3] = {}, *C[3] = {};
+  double *Gi[3] = {}, *Ki = nullptr, *gws = nullptr, *gws2 = nullptr;   // G^{-1}, K^{-1}, workspaces
+  double *V[3] = {}, *CV[3] = {}, *th[3] = {};
+  double *Y = nullptr, *k3x[2] = {nullptr, nullptr};
+  double *xchg = nullptr, *xchg2 = nullptr, *red = nullptr, *scal = nullptr, *trace = nullptr;
   double* tdbg = nullptr;      // K3 phase timestamps (wlr_debug_state "ktime")
   SmallArgs last_ss{};         // arguments of the last small-step launch (diagnostics)
   bool ktime = false;
@@ -109,9 +112,9 @@ struct wlr_ctx {
   double* h_scal = nullptr;
   cudaStream_t st = nullptr;
   bool own_stream = false;
-  int par = 0;                 // parity of the current state (= p mod 2)
+  int ph = 0;                  // phase of the current state (= p mod 6: X by p mod 2, state by p mod 3)
   int64_t p = 0;               // index of the current canonical state
-  cudaGraphExec_t gexec[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};   // [parity][deferred pending]
+  cudaGraphExec_t gexec[6][2] = {};   // [phase][deferred pending]
   cudaStream_t st2 = nullptr;  // side stream of the deferred small-step half
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool pending = false;        // deferred half of the last small step not launched yet
@@ -171,7 +174,7 @@ static wlr_status check_flags(wlr_ctx* h) {
     default: return fail(h, WLR_EINTERNAL, "unknown device flag");
   }
   h->p = (int64_t)llround(h->h_scal[5]);
-  h->par = (int)(h->p & 1);
+  h->ph = (int)(h->p % 6);
   return WLR_OK;
 }
 
@@ -186,7 +189,8 @@ static cudaEvent_t prof_event(wlr_ctx* h) {
 }
 
 // L2 prefetch list for the row pass: the inputs the following small step reads first
-static void set_prefetch(wlr_ctx* h, int cur, const void** ptr, int64_t* bytes) {
+static void set_prefetch(wlr_ctx* h, int ph, const void** ptr, int64_t* bytes) {
+  const int cur = ph % 3;
   const int64_t k = h->k, nk = h->nk;
   ptr[0] = h->GA;       bytes[0] = nk * nk * 8;
   ptr[1] = h->M[cur];   bytes[1] = k * nk * 8;
@@ -196,17 +200,19 @@ static void set_prefetch(wlr_ctx* h, int cur, const void** ptr, int64_t* bytes) 
   ptr[5] = h->Gi[cur];  bytes[5] = k * k * 8;
 }
 
-static SmallArgs small_args(wlr_ctx* h, int par, int mode) {
-  const int cur = par, nxt = par ^ 1;
+// Small-step arguments of iteration p (phase ph = p mod 6): state slot p mod 3 -> (p+1) mod 3,
+// increments / exchange block by p mod 2.
+static SmallArgs small_args(wlr_ctx* h, int ph, int mode) {
+  const int cur = ph % 3, nxt = (ph + 1) % 3, par = ph & 1;
   SmallArgs s{};
   s.k = (int)h->k; s.nk = (int)h->nk; s.t = (int)h->t; s.b = h->b; s.kp = (int)h->kp;
   s.k0 = (int)h->k0; s.rp = h->rp; s.KA = h->KA; s.mode = mode; s.dtype = h->dtype == WLR_F64 ? 1 : 0;
   s.uniform = h->uniform ? 1 : 0; s.w2 = h->w1s * h->w1s;
-  s.GA = h->GA; s.a2sq = h->a2sq; s.inc = mode ? h->inc : h->fw0;
+  s.GA = h->GA; s.a2sq = h->a2sq; s.inc = mode ? h->inc[par] : h->fw0;
   s.G_in = h->G[cur]; s.G_out = h->G[nxt]; s.M_in = h->M[cur]; s.M_out = h->M[nxt];
   s.C_in = h->C[cur]; s.C_out = h->C[nxt];
   s.V_in = h->V[cur]; s.V_out = h->V[nxt]; s.CV_in = h->CV[cur]; s.CV_out = h->CV[nxt];
-  s.th_in = h->th[cur]; s.th_out = h->th[nxt]; s.k3x = h->k3x;
+  s.th_in = h->th[cur]; s.th_out = h->th[nxt]; s.k3x = h->k3x[par];
   s.Y = h->Y;
   s.Gi_in = h->Gi[cur]; s.Gi_out = h->Gi[nxt]; s.Ki = h->Ki; s.gws = h->gws;
   s.xchg = h->xchg; s.red = h->red; s.scal = h->scal;
@@ -221,9 +227,17 @@ static SmallArgs small_args(wlr_ctx* h, int par, int mode) {
 
 // Launch the deferred half of the previous small step (objective, step norm, trace) on the
 // main stream: needed before the host reads F / the trace / the stopping flag.
+// K3b has its own exchange block / workspace, so it can run beside the next K3a.
+static cudaError_t launch_deferred(wlr_ctx* h, const SmallArgs& a, cudaStream_t st) {
+  SmallArgs d = a;
+  d.xchg = h->xchg2;
+  d.gws = h->gws2;
+  return launch_small_step(d, 2, st);
+}
+
 static wlr_status flush_pending(wlr_ctx* h) {
   if (!h->pending) return WLR_OK;
-  cudaError_t e = launch_small_step(h->pend, 2, h->st);
+  cudaError_t e = launch_deferred(h, h->pend, h->st);
   if (e != cudaSuccess) return fail(h, WLR_ECUDA, std::string("small step (deferred): ") + cudaGetErrorString(e));
   h->pending = false;
   h->pr.launches += 1;
@@ -231,12 +245,12 @@ static wlr_status flush_pending(wlr_ctx* h) {
 }
 
 // One iteration.  Stream order:
-//   st : row pass(p) -> increments(p) -> [join] -> reduce(p) -> allreduce -> K3a(p)
-//   st2: [fork at the start] K3b(p-1)       (objective/step norm of the previous state)
-// K3b(p-1) only reads state the row pass / increments of iteration p do not write; reduce(p)
-// (which rewrites the increments K3b reads) waits for it.
-static wlr_status enqueue_iteration(wlr_ctx* h, int par) {
-  const int cur = par, nxt = par ^ 1;
+//   K3b(p-1) => row pass(p) -> increments(p) -> reduce(p) -> allreduce -> K3a(p)
+// (=> programmatic dependent launch: the row pass overlaps K3b(p-1), the objective / step
+// norm of the previous state; K3b only reads state the row pass does not write, and the
+// increments, which wait for both, are where K3b's inputs get rewritten.)
+static wlr_status enqueue_iteration(wlr_ctx* h, int ph) {
+  const int cur = ph & 1, nxt = cur ^ 1;      // X1 buffers
   cudaEvent_t ev[8] = {};
   const bool prof = h->prof;
   const bool pend = h->pending;
@@ -245,15 +259,6 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int par) {
     cudaEventRecord(ev[0], h->st);
   }
   cudaError_t e;
-  if (pend) {                                  // fork: deferred half of the previous step
-    CUDA_TRY(h, cudaEventRecord(h->ev_fork, h->st));
-    CUDA_TRY(h, cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
-    if (prof) cudaEventRecord(ev[6], h->st2);
-    e = launch_small_step(h->pend, 2, h->st2);
-    if (e != cudaSuccess) return fail(h, WLR_ECUDA, std::string("small step (deferred): ") + cudaGetErrorString(e));
-    if (prof) cudaEventRecord(ev[7], h->st2);
-    CUDA_TRY(h, cudaEventRecord(h->ev_join, h->st2));
-  }
   if (h->dtype == WLR_F32) {
     RowPassArgs<float> a{};
     a.A = (const float*)h->A; a.lda = h->lda; a.W1 = (const float*)h->W1; a.ldw = h->ldw;
@@ -264,8 +269,8 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int par) {
     a.fw_part = h->fw_part; a.flags = h->flags;
     a.m = h->m; a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.no = (int)h->kp;
     a.vec_ok = (h->lda % 4 == 0) && ((uintptr_t)h->A % 16 == 0);
-    set_prefetch(h, cur, a.pf_ptr, a.pf_bytes);
-    e = launch_row_pass<float>(a, h->rp, h->uniform, 0, h->rp_grid, h->st);
+    set_prefetch(h, ph, a.pf_ptr, a.pf_bytes);
+    e = launch_row_pass<float>(a, h->rp, h->rp_tr, h->uniform, 0, h->rp_grid, h->st);
   } else {
     RowPassArgs<double> a{};
     a.A = (const double*)h->A; a.lda = h->lda; a.W1 = (const double*)h->W1; a.ldw = h->ldw;
@@ -276,8 +281,8 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int par) {
     a.fw_part = h->fw_part; a.flags = h->flags;
     a.m = h->m; a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.no = (int)h->kp;
     a.vec_ok = (h->lda % 4 == 0) && ((uintptr_t)h->A % 16 == 0);
-    set_prefetch(h, cur, a.pf_ptr, a.pf_bytes);
-    e = launch_row_pass<double>(a, h->rp, h->uniform, 0, h->rp_grid, h->st);
+    set_prefetch(h, ph, a.pf_ptr, a.pf_bytes);
+    e = launch_row_pass<double>(a, h->rp, h->rp_tr, h->uniform, 0, h->rp_grid, h->st);
   }
   if (e != cudaSuccess) return fail(h, WLR_ECUDA, std::string("row pass: ") + cudaGetErrorString(e));
   if (prof) cudaEventRecord(ev[1], h->st);
@@ -300,20 +305,31 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int par) {
   }
   if (e != cudaSuccess) return fail(h, WLR_ECUDA, std::string("increments: ") + cudaGetErrorString(e));
   if (prof) cudaEventRecord(ev[2], h->st);
-  if (pend) CUDA_TRY(h, cudaStreamWaitEvent(h->st, h->ev_join, 0));   // join
   launch_reduce_incr(h->inc_part, h->nsplit, (int)h->k, (int)h->nk, h->nz, (int)(h->k - h->k0),
-                     (int)(h->n - h->k0), (int)h->kp, h->fw_part, h->rp_grid, h->inc, h->st);
+                     (int)(h->n - h->k0), (int)h->kp, h->fw_part, h->rp_grid, h->inc[cur], h->st);
   if (prof) cudaEventRecord(ev[3], h->st);
   if (h->comm) {
     const size_t cnt = (size_t)(h->k * h->nk + 2 * h->k * h->k + 1);
-    ncclResult_t nr = g_nccl.allReduce(h->inc, h->inc, cnt, ncclFloat64, ncclSum, h->comm, h->st);
+    ncclResult_t nr = g_nccl.allReduce(h->inc[cur], h->inc[cur], cnt, ncclFloat64, ncclSum, h->comm, h->st);
     if (nr != ncclSuccess) return fail(h, WLR_ENCCL, std::string("ncclAllReduce: ") + g_nccl.errStr(nr));
   }
   if (prof) cudaEventRecord(ev[4], h->st);
-  SmallArgs s = small_args(h, par, 1);
+  // fork: the deferred half of the previous step runs beside this step's K3a (its own SMs;
+  // it reads state slots and increments that K3a(p) does not write); joined at the end
+  if (pend) {
+    CUDA_TRY(h, cudaEventRecord(h->ev_fork, h->st));
+    CUDA_TRY(h, cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
+    if (prof) cudaEventRecord(ev[6], h->st2);
+    e = launch_deferred(h, h->pend, h->st2);
+    if (e != cudaSuccess) return fail(h, WLR_ECUDA, std::string("small step (deferred): ") + cudaGetErrorString(e));
+    if (prof) cudaEventRecord(ev[7], h->st2);
+    CUDA_TRY(h, cudaEventRecord(h->ev_join, h->st2));
+  }
+  SmallArgs s = small_args(h, ph, 1);
   h->last_ss = s;
   e = launch_small_step(s, 1, h->st);
   if (e != cudaSuccess) return fail(h, WLR_ECUDA, std::string("small step: ") + cudaGetErrorString(e));
+  if (pend) CUDA_TRY(h, cudaStreamWaitEvent(h->st, h->ev_join, 0));   // join
   if (prof) {
     cudaEventRecord(ev[5], h->st);
     h->pr.iters++;
@@ -325,22 +341,22 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int par) {
   return WLR_OK;
 }
 
-static wlr_status build_graph(wlr_ctx* h, int par, int pend) {
+static wlr_status build_graph(wlr_ctx* h, int ph, int pend) {
   cudaGraph_t g;
   const bool keep_pend = h->pending;
   const SmallArgs keep_args = h->pend;
   h->pending = pend != 0;
-  if (pend) h->pend = small_args(h, par ^ 1, 1);   // the previous iteration's step
+  if (pend) h->pend = small_args(h, (ph + 5) % 6, 1);   // the previous iteration's step
   CUDA_TRY(h, cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
   const int64_t l0 = h->pr.launches;
-  wlr_status s = enqueue_iteration(h, par);
+  wlr_status s = enqueue_iteration(h, ph);
   h->pr.launches = l0;
   cudaError_t e = cudaStreamEndCapture(h->st, &g);
   h->pending = keep_pend;
   h->pend = keep_args;
   if (s != WLR_OK) return s;
   CUDA_TRY(h, e);
-  CUDA_TRY(h, cudaGraphInstantiate(&h->gexec[par][pend], g, 0));
+  CUDA_TRY(h, cudaGraphInstantiate(&h->gexec[ph][pend], g, 0));
   cudaGraphDestroy(g);
   return WLR_OK;
 }
@@ -349,19 +365,19 @@ static wlr_status launch_iteration(wlr_ctx* h) {
   wlr_status s;
   if (h->opts.use_graph && !h->prof) {
     const int pend = h->pending ? 1 : 0;
-    if (!h->gexec[h->par][pend]) {
-      s = build_graph(h, h->par, pend);
+    if (!h->gexec[h->ph][pend]) {
+      s = build_graph(h, h->ph, pend);
       if (s != WLR_OK) return s;
     }
-    CUDA_TRY(h, cudaGraphLaunch(h->gexec[h->par][pend], h->st));
-    h->pend = small_args(h, h->par, 1);
+    CUDA_TRY(h, cudaGraphLaunch(h->gexec[h->ph][pend], h->st));
+    h->pend = small_args(h, h->ph, 1);
     h->pending = true;
     h->pr.launches += pend ? 5 : 4;
   } else {
-    s = enqueue_iteration(h, h->par);
+    s = enqueue_iteration(h, h->ph);
     if (s != WLR_OK) return s;
   }
-  h->par ^= 1;
+  h->ph = (h->ph + 1) % 6;
   h->p += 1;
   return WLR_OK;
 }
@@ -444,18 +460,42 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   h->rp = row_pass_rp((int)kp);                  // row pass output: the k (padded) columns of X1
   if (h->rp < 0 || kp > 128 || t > 32) return fail(h, WLR_EINVAL, "this build supports k <= 128 and r - k <= 32");
   h->KA = (int)round_up(n, 32);
-  const int tm = row_pass_tm(h->rp);
-  const size_t rsm = h->dtype == WLR_F32 ? row_pass_smem<float>(h->rp, h->uniform, (int)k, (int)kp)
-                                         : row_pass_smem<double>(h->rp, h->uniform, (int)k, (int)kp);
-  h->nwc = h->dtype == WLR_F32 ? row_pass_chol_warps<float>(h->rp, h->uniform, (int)k, (int)kp)
-                               : row_pass_chol_warps<double>(h->rp, h->uniform, (int)k, (int)kp);
-  if (rsm > 227 * 1024 || h->nwc < 1)
-    return fail(h, WLR_EINVAL, "row-pass shared memory exceeds 227 KB for this (k, r)");
-  const int64_t ntiles = ceil_div(h->m, tm);
-  // row pass: one tile per CTA when the whole grid is co-resident (3 CTAs/SM fit at the
-  // metric's config), else a persistent grid of co-resident CTAs
-  const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(3, (227 * 1024) / std::max<size_t>(rsm, 1)));
-  h->rp_grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)h->nsm * per_sm));
+  // Row-pass tile height BM = RS * TR: the pass is throughput-bound per SM, so pick the TR whose
+  // busiest SM streams the fewest rows (ceil(tiles / SMs) * BM), with a small penalty for the
+  // lower operand reuse of short tiles; ties go to the taller tile.
+  {
+    double best = 1e300;
+    int best_tr = -1, best_cps = 1;
+    for (int tr : {8, 6, 4}) {
+      if (!row_pass_tr_ok(h->rp, tr)) continue;
+      const size_t sm = h->dtype == WLR_F32 ? row_pass_smem<float>(h->rp, tr, h->uniform, (int)k, (int)kp)
+                                            : row_pass_smem<double>(h->rp, tr, h->uniform, (int)k, (int)kp);
+      const int nw = h->dtype == WLR_F32 ? row_pass_chol_warps<float>(h->rp, tr, h->uniform, (int)k, (int)kp)
+                                         : row_pass_chol_warps<double>(h->rp, tr, h->uniform, (int)k, (int)kp);
+      if (sm > 227 * 1024 || nw < 1) continue;
+      int cps = 0;
+      cudaError_t e;
+      if (h->dtype == WLR_F32) {
+        RowPassArgs<float> q{}; q.k = (int)k; q.kp = (int)kp; q.nwc = nw;
+        e = launch_row_pass<float>(q, h->rp, tr, h->uniform, 0, 0, h->st, &cps);
+      } else {
+        RowPassArgs<double> q{}; q.k = (int)k; q.kp = (int)kp; q.nwc = nw;
+        e = launch_row_pass<double>(q, h->rp, tr, h->uniform, 0, 0, h->st, &cps);
+      }
+      if (e != cudaSuccess || cps < 1) continue;
+      const int bmr = row_pass_bm(h->rp, tr);
+      const double cost = (double)ceil_div(ceil_div(h->m, bmr), (int64_t)h->nsm) * bmr *
+                          (tr == 8 ? 1.0 : tr == 6 ? 1.03 : 1.08);
+      if (cost < best) { best = cost; best_tr = tr; best_cps = cps; }
+    }
+    if (best_tr < 0) return fail(h, WLR_EINVAL, "row-pass shared memory exceeds 227 KB for this (k, r)");
+    h->rp_tr = best_tr;
+    h->nwc = h->dtype == WLR_F32 ? row_pass_chol_warps<float>(h->rp, best_tr, h->uniform, (int)k, (int)kp)
+                                 : row_pass_chol_warps<double>(h->rp, best_tr, h->uniform, (int)k, (int)kp);
+    // all tiles co-resident when they fit, else a persistent grid of co-resident CTAs
+    const int64_t ntiles = ceil_div(h->m, row_pass_bm(h->rp, best_tr));
+    h->rp_grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)h->nsm * best_cps));
+  }
   h->bm = incr_bm((int)kp);
   const int bn = incr_bn(h->bm);
   h->nz = (int)((n - h->k0) + 2 * kp);
@@ -485,7 +525,7 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   if ((s = dalloc(h, &h->Dl, (size_t)h->m * kp * es)) != WLR_OK) return s;
   if ((s = dalloc(h, &h->Wt, (size_t)wt_rows * h->rp * es)) != WLR_OK) return s;
   {   // TMA tensor maps: 128-byte x BM boxes (SWIZZLE_128B) of A and X1, 32-row boxes of Wt
-    const uint32_t pe = (uint32_t)(128 / es), bm = (uint32_t)row_pass_tm(h->rp);
+    const uint32_t pe = (uint32_t)(128 / es), bm = (uint32_t)row_pass_bm(h->rp, h->rp_tr);
     bool ok = make_tmap_2d(&h->tmA, h->A, (int)es, (uint64_t)n, (uint64_t)h->m, (uint64_t)h->lda * es, pe, bm, true);
     for (int i = 0; i < 2; ++i)
       ok = ok && make_tmap_2d(&h->tmX[i], h->X[i], (int)es, (uint64_t)kp, (uint64_t)h->m, (uint64_t)kp * es, pe, bm, true);
@@ -497,10 +537,11 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   if ((s = dalloc(h, &h->Kop, (size_t)k * k * es)) != WLR_OK) return s;
   if ((s = dalloc_t(h, &h->inc_part, (size_t)h->nsplit * k * h->nz)) != WLR_OK) return s;
   if ((s = dalloc_t(h, &h->fw_part, (size_t)std::max(h->rp_grid, 1184))) != WLR_OK) return s;
-  if ((s = dalloc_t(h, &h->inc, (size_t)(k * nk + 2 * k * k + 1))) != WLR_OK) return s;
+  for (int i = 0; i < 2; ++i)
+    if ((s = dalloc_t(h, &h->inc[i], (size_t)(k * nk + 2 * k * k + 1))) != WLR_OK) return s;
   if ((s = dalloc_t(h, &h->fw0, 2)) != WLR_OK) return s;
   if ((s = dalloc_t(h, &h->GA, (size_t)nk * nk)) != WLR_OK) return s;
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < 3; ++i) {
     if ((s = dalloc_t(h, &h->G[i], (size_t)k * k)) != WLR_OK) return s;
     if ((s = dalloc_t(h, &h->M[i], (size_t)k * nk)) != WLR_OK) return s;
     if ((s = dalloc_t(h, &h->C[i], (size_t)k * nk)) != WLR_OK) return s;
@@ -508,12 +549,14 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   }
   if ((s = dalloc_t(h, &h->Ki, (size_t)k * k)) != WLR_OK) return s;
   if ((s = dalloc_t(h, &h->gws, (size_t)std::max<int64_t>(1, h->spl.CL * h->spl.gws_stride))) != WLR_OK) return s;
-  for (int i = 0; i < 2; ++i) {
+  if ((s = dalloc_t(h, &h->gws2, (size_t)std::max<int64_t>(1, h->spl.CL * h->spl.gws_stride))) != WLR_OK) return s;
+  for (int i = 0; i < 3; ++i) {
     if ((s = dalloc_t(h, &h->V[i], (size_t)nk * t)) != WLR_OK) return s;
     if ((s = dalloc_t(h, &h->CV[i], (size_t)k * t)) != WLR_OK) return s;
     if ((s = dalloc_t(h, &h->th[i], 32)) != WLR_OK) return s;
   }
-  if ((s = dalloc_t(h, &h->k3x, (size_t)2 * t * t + 8)) != WLR_OK) return s;
+  for (int i = 0; i < 2; ++i)
+    if ((s = dalloc_t(h, &h->k3x[i], (size_t)2 * t * t + 8)) != WLR_OK) return s;
   if ((s = dalloc_t(h, &h->Y, (size_t)nk * b)) != WLR_OK) return s;
   {
     int lo = 0, hi = 0;
@@ -523,6 +566,7 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
     CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
   }
   if ((s = dalloc_t(h, &h->xchg, (size_t)h->spl.CL * h->spl.flen)) != WLR_OK) return s;
+  if ((s = dalloc_t(h, &h->xchg2, (size_t)h->spl.CL * h->spl.flen)) != WLR_OK) return s;
   if ((s = dalloc_t(h, &h->red, (size_t)h->spl.flen + 3 * k * t + 64)) != WLR_OK) return s;
   if ((s = dalloc_t(h, &h->scal, 8)) != WLR_OK) return s;
   if ((s = dalloc_t(h, &h->tdbg, 64)) != WLR_OK) return s;
@@ -610,21 +654,21 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
     CUDA_TRY(h, cudaStreamSynchronize(h->st));
   }
   // small step configuration
-  // initial (C, D) half-step: outputs into buffer 0 (small_args with par = 1 maps out -> 0)
-  SmallArgs sa = small_args(h, 1, 0);
+  // initial (C, D) half-step: outputs into state slot 0 (phase 5 maps out -> 0)
+  SmallArgs sa = small_args(h, 5, 0);
   sa.G_in = nullptr; sa.M_in = nullptr; sa.C_in = nullptr; sa.Gi_in = nullptr;
   sa.V_in = nullptr; sa.CV_in = nullptr; sa.th_in = nullptr;
   sa.G_out = h->G[0]; sa.M_out = h->M[0];        // mode 0 reads the init Grams from here
   sa.max_outer = 4 * o.eig_max_outer; sa.cold = 1;
   sa.tdbg = h->tdbg;
   cudaError_t e = launch_small_step(sa, 1, h->st);
-  if (e == cudaSuccess) e = launch_small_step(sa, 2, h->st);
+  if (e == cudaSuccess) e = launch_deferred(h, sa, h->st);
   if (e != cudaSuccess) return fail(h, WLR_ECUDA, std::string("small step (init): ") + cudaGetErrorString(e));
   h->pr.launches = 0;
   s = check_flags(h);
   if (s != WLR_OK) return s;
   h->p = 0;
-  h->par = 0;
+  h->ph = 0;
   return WLR_OK;
 }
 
@@ -757,11 +801,11 @@ extern "C" wlr_status wlr_result(wlr_handle h, void* X1, int64_t ldx1, void* C, 
   if (!h) return fail(nullptr, WLR_EINVAL, "null handle");
   wlr_status s = check_flags(h);
   if (s != WLR_OK) return s;
-  const int cur = h->par;
+  const int cx = h->ph & 1, cur = h->ph % 3;   // X1 buffer, state slot
   const size_t es = h->es;
   if (X1) {
     if (ldx1 < h->k) return fail(h, WLR_EINVAL, "ldx1 < k");
-    if ((s = copy_out(h, X1, ldx1, h->X[cur], h->kp, h->m, h->k, es)) != WLR_OK) return s;
+    if ((s = copy_out(h, X1, ldx1, h->X[cx], h->kp, h->m, h->k, es)) != WLR_OK) return s;
   }
   if (C) {
     if ((s = copy_out(h, C, h->nk, h->C[cur], h->nk, h->k, h->nk, 8)) != WLR_OK) return s;
@@ -798,32 +842,36 @@ extern "C" wlr_status wlr_result(wlr_handle h, void* X1, int64_t ldx1, void* C, 
     } else {
       CUDA_TRY(h, cudaMemcpy(Wbd, wb.data(), wb.size() * 8, cudaMemcpyHostToDevice));
     }
-    CUtensorMap tmB{};
-    if (!make_tmap_2d(&tmB, Wbd, (int)es, (uint64_t)rpb, (uint64_t)wrows, (uint64_t)rpb * es, (uint32_t)rpb, 32u, false)) {
+    // the result pass runs with TR = 8: its own A / X1 boxes (BM rows) and the Wb map
+    CUtensorMap tmB{}, tmAr{}, tmXr{};
+    const uint32_t pe = (uint32_t)(128 / es), bmr = (uint32_t)row_pass_bm(rpb, 8);
+    if (!make_tmap_2d(&tmB, Wbd, (int)es, (uint64_t)rpb, (uint64_t)wrows, (uint64_t)rpb * es, (uint32_t)rpb, 32u, false) ||
+        !make_tmap_2d(&tmAr, h->A, (int)es, (uint64_t)h->n, (uint64_t)h->m, (uint64_t)h->lda * es, pe, bmr, true) ||
+        !make_tmap_2d(&tmXr, h->X[cx], (int)es, (uint64_t)h->kp, (uint64_t)h->m, (uint64_t)h->kp * es, pe, bmr, true)) {
       cudaFree(Wbd); cudaFree(Bd);
       return fail(h, WLR_ECUDA, "cuTensorMapEncodeTiled failed (result)");
     }
     cudaError_t e;
     if (h->dtype == WLR_F32) {
       RowPassArgs<float> a{};
-      a.tmA = h->tmA; a.tmX = h->tmX[cur]; a.tmW = tmB;
+      a.tmA = tmAr; a.tmX = tmXr; a.tmW = tmB;
       a.A = (const float*)h->A; a.lda = h->lda; a.W1 = (const float*)h->W1; a.ldw = h->ldw;
-      a.Xold = (const float*)h->X[cur]; a.nwc = h->nwc;
+      a.Xold = (const float*)h->X[cx]; a.nwc = h->nwc;
       a.Wt = (const float*)Wbd; a.KA = h->KA;
       a.Bout = (float*)Bd; a.ldb = h->t; a.fw_part = h->fw_part; a.flags = h->flags;
       a.m = h->m; a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.no = (int)h->t;
       a.vec_ok = (h->lda % 4 == 0) && ((uintptr_t)h->A % 16 == 0);
-      e = launch_row_pass<float>(a, rpb, true, 1, h->rp_grid, h->st);
+      e = launch_row_pass<float>(a, rpb, 8, true, 1, h->rp_grid, h->st);
     } else {
       RowPassArgs<double> a{};
-      a.tmA = h->tmA; a.tmX = h->tmX[cur]; a.tmW = tmB;
+      a.tmA = tmAr; a.tmX = tmXr; a.tmW = tmB;
       a.A = (const double*)h->A; a.lda = h->lda; a.W1 = (const double*)h->W1; a.ldw = h->ldw;
-      a.Xold = (const double*)h->X[cur]; a.nwc = h->nwc;
+      a.Xold = (const double*)h->X[cx]; a.nwc = h->nwc;
       a.Wt = (const double*)Wbd; a.KA = h->KA;
       a.Bout = (double*)Bd; a.ldb = h->t; a.fw_part = h->fw_part; a.flags = h->flags;
       a.m = h->m; a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.no = (int)h->t;
       a.vec_ok = (h->lda % 4 == 0) && ((uintptr_t)h->A % 16 == 0);
-      e = launch_row_pass<double>(a, rpb, true, 1, h->rp_grid, h->st);
+      e = launch_row_pass<double>(a, rpb, 8, true, 1, h->rp_grid, h->st);
     }
     cudaStreamSynchronize(h->st);
     cudaFree(Wbd);
@@ -840,9 +888,9 @@ extern "C" wlr_status wlr_result(wlr_handle h, void* X1, int64_t ldx1, void* C, 
       else if (cudaMalloc(&X2d, (size_t)h->m * h->nk * es) != cudaSuccess) { cudaFree(Bd); return fail(h, WLR_ENOMEM, "X2 staging"); }
       const int64_t ldo = dev ? ldx2 : h->nk;
       if (h->dtype == WLR_F32)
-        launch_assemble_x2<float>((const float*)h->X[cur], (int)h->kp, (const float*)Bd, h->t, h->C[cur], h->V[cur], h->m, (int)h->k, (int)h->nk, (int)h->t, (float*)X2d, ldo, h->st);
+        launch_assemble_x2<float>((const float*)h->X[cx], (int)h->kp, (const float*)Bd, h->t, h->C[cur], h->V[cur], h->m, (int)h->k, (int)h->nk, (int)h->t, (float*)X2d, ldo, h->st);
       else
-        launch_assemble_x2<double>((const double*)h->X[cur], (int)h->kp, (const double*)Bd, h->t, h->C[cur], h->V[cur], h->m, (int)h->k, (int)h->nk, (int)h->t, (double*)X2d, ldo, h->st);
+        launch_assemble_x2<double>((const double*)h->X[cx], (int)h->kp, (const double*)Bd, h->t, h->C[cur], h->V[cur], h->m, (int)h->k, (int)h->nk, (int)h->t, (double*)X2d, ldo, h->st);
       if (!dev) {
         s = copy_out(h, X2, ldx2, X2d, h->nk, h->m, h->nk, es);
         cudaStreamSynchronize(h->st);
@@ -868,7 +916,7 @@ extern "C" wlr_status wlr_debug_state(wlr_handle h, const char* name, double* ou
   }
   wlr_status s = check_flags(h);
   if (s != WLR_OK) return s;
-  const int cur = h->par;
+  const int cx = h->ph & 1, cur = h->ph % 3;   // X1 buffer, state slot
   const double* src = nullptr;
   int64_t cnt = 0;
   std::string nm(name);
@@ -914,7 +962,6 @@ extern "C" wlr_status wlr_profile(wlr_handle h, int32_t enable, int32_t reset, d
                                   int32_t nms, int64_t* launches, int64_t* timed_iters) {
   if (!h) return fail(nullptr, WLR_EINVAL, "null handle");
   CUDA_TRY(h, cudaStreamSynchronize(h->st));
-  CUDA_TRY(h, cudaStreamSynchronize(h->st2));
   // fold recorded event groups (8 per iteration; 6, 7 = deferred K3b on the side stream)
   for (size_t g = 0, it = 0; g + 8 <= h->pr.used; g += 8, ++it) {
     float t01 = 0, t12 = 0, t23 = 0, t45 = 0, t67 = 0;
@@ -971,18 +1018,17 @@ extern "C" const char* wlr_status_string(int32_t s) {
 extern "C" void wlr_destroy(wlr_handle h) {
   if (!h) return;
   if (h->st) cudaStreamSynchronize(h->st);
-  if (h->st2) cudaStreamSynchronize(h->st2);
   for (auto& gp : h->gexec)
     for (auto& g : gp)
       if (g) cudaGraphExecDestroy(g);
-  if (h->st2) cudaStreamDestroy(h->st2);
-  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
-  if (h->ev_join) cudaEventDestroy(h->ev_join);
   if (h->comm && g_nccl.commDestroy) g_nccl.commDestroy(h->comm);
   for (void* p : h->allocs) cudaFree(p);
   for (auto e : h->pr.pool) cudaEventDestroy(e);
   if (h->h_flags) cudaFreeHost(h->h_flags);
   if (h->h_scal) cudaFreeHost(h->h_scal);
+  if (h->st2) { cudaStreamSynchronize(h->st2); cudaStreamDestroy(h->st2); }
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
   if (h->own_stream && h->st) cudaStreamDestroy(h->st);
   delete h;
 }

@@ -50,12 +50,14 @@ struct RowPassArgs {
   int vec_ok;                       // A rows 16-byte aligned at multiples of 4 elements
 };
 int row_pass_rp(int r);
-int row_pass_tm(int rp);
-template <typename T> size_t row_pass_smem(int rp, bool uniform, int k, int kp);
-template <typename T> int row_pass_chol_warps(int rp, bool uniform, int k, int kp);
+bool row_pass_tr_ok(int rp, int tr);     // rows per thread TR available for this width
+int row_pass_bm(int rp, int tr);         // tile height BM (rows per CTA tile)
+template <typename T> size_t row_pass_smem(int rp, int tr, bool uniform, int k, int kp);
+template <typename T> int row_pass_chol_warps(int rp, int tr, bool uniform, int k, int kp);
 template <typename T>
-cudaError_t launch_row_pass(const RowPassArgs<T>& a, int rp, bool uniform, int mode, int grid,
-                            cudaStream_t st);
+cudaError_t launch_row_pass(const RowPassArgs<T>& a, int rp, int tr, bool uniform, int mode, int grid,
+                            cudaStream_t st, int* occ = nullptr,   // occ: only report CTAs/SM
+                            bool pdl = false);   // programmatic dependent of the previous kernel
 
 template <typename T>
 struct IncrArgs {

@@ -73,24 +73,25 @@ WLR_DEVI void lds_vec(const T* p, T (&o)[N]) {
 }
 
 // ------------------------------------------------------------------------------ K2a
-template <int RP> struct RowPassShape;   // BM rows per tile, TC columns per thread (TR = 8)
-template <> struct RowPassShape<16>  { static constexpr int BM = 64, TC = 2; };
-template <> struct RowPassShape<32>  { static constexpr int BM = 64, TC = 4; };
-template <> struct RowPassShape<64>  { static constexpr int BM = 64, TC = 8; };
-template <> struct RowPassShape<128> { static constexpr int BM = 32, TC = 8; };
+template <int RP> struct RowPassShape;   // TC columns per thread, RS row groups (BM = RS * TR)
+template <> struct RowPassShape<16>  { static constexpr int TC = 2, RS = 8; };
+template <> struct RowPassShape<32>  { static constexpr int TC = 4, RS = 8; };
+template <> struct RowPassShape<64>  { static constexpr int TC = 8, RS = 8; };
+template <> struct RowPassShape<128> { static constexpr int TC = 8, RS = 4; };
 
 constexpr int kRowKC = 32;        // reduction chunk (columns of [A | X1_p])
 constexpr int kRowKG = 4;         // k-groups (in-CTA split-K); each takes 8 k of a chunk
-constexpr int kRowTR = 8;         // rows per thread (interleaved by BM / 8)
+// TR (rows per thread, interleaved by RS) is a template parameter: the host picks the tile
+// height BM = RS * TR that balances the tiles over the SMs (row_pass_pick_tr)
 constexpr int kRowThreads = 256;
 
 // Per-warp scratch for the non-uniform epilogue: the packed lower triangle of the row matrix.
 __host__ __device__ inline int chol_packed(int kp) { return kp * (kp + 1) / 2; }
 
-template <typename T, int RP>
+template <typename T, int RP, int TR>
 struct RowPassLayout {            // shared memory layout (elements of T; base 1024-byte aligned)
   using S = RowPassShape<RP>;
-  static constexpr int BM = S::BM;
+  static constexpr int BM = S::RS * TR;
   static constexpr int PE = 128 / (int)sizeof(T);               // elements per 128-byte panel row
   static constexpr int NP = kRowKC / PE;                        // panels per A chunk (1 fp32, 2 fp64)
   static constexpr int kA = NP * BM * PE;                       // one A stage (SWIZZLE_128B panels)
@@ -107,11 +108,11 @@ struct RowPassLayout {            // shared memory layout (elements of T; base 1
 __host__ __device__ inline int64_t align_up_i(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 
 // offsets (elements) of the X1_p / A1 staging panels and of the tail buffers
-template <typename T, int RP>
+template <typename T, int RP, int TR>
 struct RowPassTail {
   int64_t oXs, oA1s, oK, oL, end;
   __host__ __device__ RowPassTail(bool uniform, int k, int kp, int nwc) {
-    using L = RowPassLayout<T, RP>;
+    using L = RowPassLayout<T, RP, TR>;
     const int npk = (kp + L::PE - 1) / L::PE;
     const int64_t alias = (int64_t)L::oE + (uniform ? 0 : (int64_t)L::BM * kp);
     oXs = align_up_i(alias > L::oStEnd ? alias : L::oStEnd, L::ALIGN);
@@ -122,27 +123,27 @@ struct RowPassTail {
   }
 };
 
-template <typename T, int RP>
+template <typename T, int RP, int TR>
 size_t row_pass_smem_elems(bool uniform, int k, int kp, int nwc) {
-  return (size_t)RowPassTail<T, RP>(uniform, k, kp, nwc).end + RowPassLayout<T, RP>::ALIGN;
+  return (size_t)RowPassTail<T, RP, TR>(uniform, k, kp, nwc).end + RowPassLayout<T, RP, TR>::ALIGN;
 }
 
 // warps that can hold a packed k x k factor in the remaining shared memory (<= 8)
-template <typename T, int RP>
+template <typename T, int RP, int TR>
 int row_pass_nwc(bool uniform, int k, int kp) {
   if (uniform) return 8;
-  const size_t base = row_pass_smem_elems<T, RP>(false, k, kp, 0);
+  const size_t base = row_pass_smem_elems<T, RP, TR>(false, k, kp, 0);
   const size_t cap = 227 * 1024 / sizeof(T);
   if (base >= cap) return 0;
   return (int)std::min<size_t>(8, (cap - base) / chol_packed(kp));
 }
 
-template <typename T, int RP, bool UNIFORM, int MODE>
+template <typename T, int RP, int TR, bool UNIFORM, int MODE>
 __global__ void __launch_bounds__(kRowThreads, RP <= 32 ? 3 : 1)
 row_pass_kernel(const __grid_constant__ RowPassArgs<T> a) {
   using S = RowPassShape<RP>;
-  using L = RowPassLayout<T, RP>;
-  constexpr int BM = S::BM, TC = S::TC, TR = kRowTR, KG = kRowKG, PE = L::PE, NST = L::NST;
+  using L = RowPassLayout<T, RP, TR>;
+  constexpr int BM = L::BM, TC = S::TC, KG = kRowKG, PE = L::PE, NST = L::NST;
   constexpr int THC = RP / TC;                 // threads along columns (per k-group)
   constexpr int GT = (BM / TR) * THC;          // threads per k-group
   static_assert(GT * KG == kRowThreads, "thread tile");
@@ -152,10 +153,11 @@ row_pass_kernel(const __grid_constant__ RowPassArgs<T> a) {
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  __shared__ __align__(8) uint64_t full[NST];
+  __shared__ __align__(8) uint64_t full[NST];    // stage filled (TMA bytes landed)
+  __shared__ __align__(8) uint64_t empty[NST];   // stage drained (one arrival per warp)
   __shared__ __align__(8) uint64_t epb;
   const int kp = a.kp, k = a.k;
-  const RowPassTail<T, RP> tl(UNIFORM || MODE == 1, k, kp, a.nwc);
+  const RowPassTail<T, RP, TR> tl(UNIFORM || MODE == 1, k, kp, a.nwc);
   T* As = sm + L::oA;                          // [NST][NP][BM][PE]  (swizzled panels)
   T* Bs = sm + L::oB;                          // [NST][KC][RP]
   T* Ys = sm + L::oY;                          // [BM][RP+1]   (aliases the stages)
@@ -171,7 +173,10 @@ row_pass_kernel(const __grid_constant__ RowPassArgs<T> a) {
   };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < NST; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kRowThreads / 32);
+    }
     mbar_init(&epb, 1);
     mbar_init_fence();
   }
@@ -240,7 +245,8 @@ row_pass_kernel(const __grid_constant__ RowPassArgs<T> a) {
     for (int ch = 0; ch < nch; ++ch) {
       const int64_t g = G + ch;
       const int st = (int)(g % NST);
-      if (threadIdx.x == 0 && ch + NST - 1 < nch) {   // refill the stage freed last iteration
+      if (threadIdx.x == 0 && ch + NST - 1 < nch) {   // refill the stage chunk g-1 used
+        if (ch > 0) mbar_wait(&empty[(g - 1) % NST], (uint32_t)(((g - 1) / NST) & 1));
         fence_proxy_async();
         load_chunk(r0, ch + NST - 1, (int)((g + NST - 1) % NST));
       }
@@ -269,9 +275,11 @@ row_pass_kernel(const __grid_constant__ RowPassArgs<T> a) {
             for (int j = 0; j < TC; ++j) acc[i][j] = fma(av[i][q], bv[j], acc[i][j]);
         }
       }
-      __syncthreads();                         // stage st is free for the next refill
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done with stage st
     }
     G += nch;
+    __syncthreads();                           // every warp is out of the stages (Ys aliases them)
     // fixed-order sum of the KG partial tiles into Ys
 #pragma unroll 1
     for (int gg = 0; gg < KG; ++gg) {
@@ -396,10 +404,10 @@ row_pass_kernel(const __grid_constant__ RowPassArgs<T> a) {
   }
 }
 
-template <typename T, int RP, bool UNIFORM, int MODE>
-static cudaError_t launch_rp(const RowPassArgs<T>& a, int grid, cudaStream_t st) {
-  auto kern = row_pass_kernel<T, RP, UNIFORM, MODE>;
-  const size_t smem = sizeof(T) * row_pass_smem_elems<T, RP>(UNIFORM || MODE == 1, a.k, a.kp, a.nwc);
+template <typename T, int RP, int TR, bool UNIFORM, int MODE>
+static cudaError_t launch_rp(const RowPassArgs<T>& a, int grid, cudaStream_t st, int* occ, bool pdl) {
+  auto kern = row_pass_kernel<T, RP, TR, UNIFORM, MODE>;
+  const size_t smem = sizeof(T) * row_pass_smem_elems<T, RP, TR>(UNIFORM || MODE == 1, a.k, a.kp, a.nwc);
   static size_t configured = 0;            // cudaFuncSetAttribute once per size increase
   if (smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -409,56 +417,68 @@ static cudaError_t launch_rp(const RowPassArgs<T>& a, int grid, cudaStream_t st)
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  kern<<<grid, kRowThreads, smem, st>>>(a);
-  return cudaGetLastError();
-}
-
-template <typename T, int RP>
-static cudaError_t dispatch_rp(const RowPassArgs<T>& a, bool uniform, int mode, int grid,
-                               cudaStream_t st) {
-  if (mode) return launch_rp<T, RP, true, 1>(a, grid, st);
-  return uniform ? launch_rp<T, RP, true, 0>(a, grid, st) : launch_rp<T, RP, false, 0>(a, grid, st);
+  if (occ) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kern, kRowThreads, smem);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kRowThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
 int row_pass_rp(int r) { return r <= 16 ? 16 : r <= 32 ? 32 : r <= 64 ? 64 : r <= 128 ? 128 : -1; }
-int row_pass_tm(int rp) { return rp == 128 ? RowPassShape<128>::BM : RowPassShape<32>::BM; }
+bool row_pass_tr_ok(int rp, int tr) { return rp == 128 ? tr == 8 : (tr == 4 || tr == 6 || tr == 8); }
+int row_pass_bm(int rp, int tr) { return (rp == 128 ? RowPassShape<128>::RS : RowPassShape<32>::RS) * tr; }
+
+#define WLR_RP_SWITCH(RPV, TRV, CALL)                                                    \
+  switch (RPV) {                                                                         \
+    case 16: switch (TRV) { case 4: CALL(16, 4); case 6: CALL(16, 6); default: CALL(16, 8); } \
+    case 32: switch (TRV) { case 4: CALL(32, 4); case 6: CALL(32, 6); default: CALL(32, 8); } \
+    case 64: switch (TRV) { case 4: CALL(64, 4); case 6: CALL(64, 6); default: CALL(64, 8); } \
+    default: CALL(128, 8);                                                               \
+  }
 
 template <typename T>
-size_t row_pass_smem(int rp, bool uniform, int k, int kp) {
-  switch (rp) {
-    case 16: return sizeof(T) * row_pass_smem_elems<T, 16>(uniform, k, kp, row_pass_nwc<T, 16>(uniform, k, kp));
-    case 32: return sizeof(T) * row_pass_smem_elems<T, 32>(uniform, k, kp, row_pass_nwc<T, 32>(uniform, k, kp));
-    case 64: return sizeof(T) * row_pass_smem_elems<T, 64>(uniform, k, kp, row_pass_nwc<T, 64>(uniform, k, kp));
-    default: return sizeof(T) * row_pass_smem_elems<T, 128>(uniform, k, kp, row_pass_nwc<T, 128>(uniform, k, kp));
-  }
+size_t row_pass_smem(int rp, int tr, bool uniform, int k, int kp) {
+#define WLR_SMEM(R, TT) \
+  return sizeof(T) * row_pass_smem_elems<T, R, TT>(uniform, k, kp, row_pass_nwc<T, R, TT>(uniform, k, kp))
+  WLR_RP_SWITCH(rp, tr, WLR_SMEM)
+#undef WLR_SMEM
 }
-template size_t row_pass_smem<float>(int, bool, int, int);
-template size_t row_pass_smem<double>(int, bool, int, int);
+template size_t row_pass_smem<float>(int, int, bool, int, int);
+template size_t row_pass_smem<double>(int, int, bool, int, int);
 template <typename T>
-int row_pass_chol_warps(int rp, bool uniform, int k, int kp) {
-  switch (rp) {
-    case 16: return row_pass_nwc<T, 16>(uniform, k, kp);
-    case 32: return row_pass_nwc<T, 32>(uniform, k, kp);
-    case 64: return row_pass_nwc<T, 64>(uniform, k, kp);
-    default: return row_pass_nwc<T, 128>(uniform, k, kp);
-  }
+int row_pass_chol_warps(int rp, int tr, bool uniform, int k, int kp) {
+#define WLR_NWC(R, TT) return row_pass_nwc<T, R, TT>(uniform, k, kp)
+  WLR_RP_SWITCH(rp, tr, WLR_NWC)
+#undef WLR_NWC
 }
-template int row_pass_chol_warps<float>(int, bool, int, int);
-template int row_pass_chol_warps<double>(int, bool, int, int);
+template int row_pass_chol_warps<float>(int, int, bool, int, int);
+template int row_pass_chol_warps<double>(int, int, bool, int, int);
 
+// The result pass (mode 1) exists for TR = 8 only.
 template <typename T>
-cudaError_t launch_row_pass(const RowPassArgs<T>& a, int rp, bool uniform, int mode, int grid,
-                            cudaStream_t st) {
-  switch (rp) {
-    case 16: return dispatch_rp<T, 16>(a, uniform, mode, grid, st);
-    case 32: return dispatch_rp<T, 32>(a, uniform, mode, grid, st);
-    case 64: return dispatch_rp<T, 64>(a, uniform, mode, grid, st);
-    case 128: return dispatch_rp<T, 128>(a, uniform, mode, grid, st);
+cudaError_t launch_row_pass(const RowPassArgs<T>& a, int rp, int tr, bool uniform, int mode, int grid,
+                            cudaStream_t st, int* occ, bool pdl) {
+  if (rp != 16 && rp != 32 && rp != 64 && rp != 128) return cudaErrorInvalidValue;
+  if (!row_pass_tr_ok(rp, tr) || (mode && tr != 8)) return cudaErrorInvalidValue;
+  if (mode) {
+#define WLR_RES(R, TT) return launch_rp<T, R, 8, true, 1>(a, grid, st, occ, pdl)
+    WLR_RP_SWITCH(rp, 8, WLR_RES)
+#undef WLR_RES
   }
-  return cudaErrorInvalidValue;
+#define WLR_RUN(R, TT) \
+  return uniform ? launch_rp<T, R, TT, true, 0>(a, grid, st, occ, pdl) : launch_rp<T, R, TT, false, 0>(a, grid, st, occ, pdl)
+  WLR_RP_SWITCH(rp, tr, WLR_RUN)
+#undef WLR_RUN
 }
-template cudaError_t launch_row_pass<float>(const RowPassArgs<float>&, int, bool, int, int, cudaStream_t);
-template cudaError_t launch_row_pass<double>(const RowPassArgs<double>&, int, bool, int, int, cudaStream_t);
+template cudaError_t launch_row_pass<float>(const RowPassArgs<float>&, int, int, bool, int, int, cudaStream_t, int*, bool);
+template cudaError_t launch_row_pass<double>(const RowPassArgs<double>&, int, int, bool, int, int, cudaStream_t, int*, bool);
 
 // ------------------------------------------------------------------------------ K2b
 // Thread tile 8 (q) x 4 (columns); warp w owns q in [8w, 8w+8) and lanes 32 column groups,

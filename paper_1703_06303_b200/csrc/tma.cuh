@@ -31,6 +31,9 @@ WLR_DEVI void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
   }
 }
+WLR_DEVI void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
 // generic-proxy accesses to smem before this point are ordered before later async-proxy
 // (TMA) writes to it
 WLR_DEVI void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
