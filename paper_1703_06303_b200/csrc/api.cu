@@ -232,6 +232,7 @@ static cudaError_t launch_deferred(wlr_ctx* h, const SmallArgs& a, cudaStream_t 
   SmallArgs d = a;
   d.xchg = h->xchg2;
   d.gws = h->gws2;
+  if (d.tdbg) d.tdbg += 64;                  // its own timestamp block
   return launch_small_step(d, 2, st);
 }
 
@@ -569,7 +570,7 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   if ((s = dalloc_t(h, &h->xchg2, (size_t)h->spl.CL * h->spl.flen)) != WLR_OK) return s;
   if ((s = dalloc_t(h, &h->red, (size_t)h->spl.flen + 3 * k * t + 64)) != WLR_OK) return s;
   if ((s = dalloc_t(h, &h->scal, 8)) != WLR_OK) return s;
-  if ((s = dalloc_t(h, &h->tdbg, 64)) != WLR_OK) return s;
+  if ((s = dalloc_t(h, &h->tdbg, 128)) != WLR_OK) return s;   // K3a marks, then K3b marks
   if ((s = dalloc_t(h, &h->trace, (size_t)h->trace_cap * 4)) != WLR_OK) return s;
 
   // ---- NCCL communicator (rows sharded over ranks)
@@ -910,8 +911,8 @@ extern "C" wlr_status wlr_debug_state(wlr_handle h, const char* name, double* ou
   if (!h || !name) return fail(h, WLR_EINVAL, "null argument");
   if (std::string(name) == "ktime") {          // timestamps of the last launched K3 half,
     CUDA_TRY(h, cudaStreamSynchronize(h->st)); // read without launching a pending one
-    if (count) *count = 64;
-    if (out) CUDA_TRY(h, cudaMemcpy(out, h->tdbg, (size_t)std::min<int64_t>(cap, 64) * 8, cudaMemcpyDeviceToHost));
+    if (count) *count = 128;
+    if (out) CUDA_TRY(h, cudaMemcpy(out, h->tdbg, (size_t)std::min<int64_t>(cap, 128) * 8, cudaMemcpyDeviceToHost));
     return WLR_OK;
   }
   wlr_status s = check_flags(h);
@@ -928,7 +929,7 @@ extern "C" wlr_status wlr_debug_state(wlr_handle h, const char* name, double* ou
   else if (nm == "theta") { src = h->th[cur]; cnt = h->b; }
   else if (nm == "GA") { src = h->GA; cnt = h->nk * h->nk; }
   else if (nm == "scal") { src = h->scal; cnt = 8; }
-  else if (nm == "ktime") { src = h->tdbg; cnt = 64; }
+  else if (nm == "ktime") { src = h->tdbg; cnt = 128; }
   else if (nm == "ktime_on" || nm == "ktime_off") {   // enable/disable K3 phase timestamps
     h->ktime = nm == "ktime_on";
     for (auto& gp : h->gexec)

@@ -83,6 +83,7 @@ struct SSPlan {
   int CL, SL;                       // cluster size, columns per CTA (slice of the n-k index)
   int KS, JS;                       // S-product split: KS reduction chunks x JS column groups
   int PL;                           // DSMEM exchange length (doubles per bank)
+  int ccx;                          // C'C'^T partials ride in the DSMEM exchange (else global)
   int64_t oPart, oBuf, oVp, oE, oSE, oWk, oCinE, oSmall, oRed;            // always in smem
   int64_t oCs, oMs, oCin, oXf, oMat3, oGsq, oTail;                         // optional
   int64_t total;                    // doubles of dynamic smem

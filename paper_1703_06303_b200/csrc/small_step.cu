@@ -35,7 +35,7 @@ static constexpr int64_t kSmemLimit = 227 * 1024 / 8;   // doubles per CTA
 // optional ones greedily in priority order (C' slice, Newton-Schulz mats, M' slice, gathered
 // S-product operand, staged G/Gamma/Omega, C_in slice, CTA-0 tail staging); an optional
 // region that does not fit gets offset -1 (the kernel then uses the global copy).
-bool small_step_plan(SmallArgs& a, int CL) {
+static bool plan_once(SmallArgs& a, int CL, int ccx) {
   SSPlan& p = a.pl;
   const int k = a.k, nk = a.nk, t = a.t, b = a.b, bt = bt_of(b);
   p.CL = CL;
@@ -44,7 +44,9 @@ bool small_step_plan(SmallArgs& a, int CL) {
   p.JS = bt <= 8 ? 1 : bt <= 16 ? 2 : 4;
   p.KS = 16 / p.JS;
   const int64_t SL = p.SL, kt = (int64_t)k * t, kk = (int64_t)k * k;
-  int64_t pl = std::max<int64_t>({(int64_t)k * b, 2LL * b * b + 2LL * t * b, (int64_t)t + kt});
+  // exchange bank: C X (k b), the Rayleigh-Ritz Grams (+ C'C'^T on the first pass), C'V' (k t)
+  int64_t pl = std::max<int64_t>({(int64_t)k * b, 2LL * b * b + 2LL * t * b + (ccx ? kk : 0), (int64_t)t + kt});
+  p.ccx = ccx;
   p.PL = (int)round_up(pl, 2);
   const FinOff fo(k, t);
   p.flen = fo.len;
@@ -59,23 +61,25 @@ bool small_step_plan(SmallArgs& a, int CL) {
   p.oWk = take((int64_t)k * b);
   p.oCinE = take(t + kt);
   p.oSmall = take(so.len);
-  p.oRed = take(std::max<int64_t>((int64_t)p.KS * SL * b, SL * (int64_t)k));   // also U rows
+  p.oRed = take(std::max<int64_t>((int64_t)p.KS * SL * b, (SL + t) * (int64_t)k));   // also U rows, Qt
   if (o > kSmemLimit) return false;
   auto opt = [&](int64_t n) -> int64_t {
     if (o + round_up(n, 2) > kSmemLimit) return -1;
     return take(n);
   };
-  p.oCs = opt((int64_t)k * SL);
+  p.oCs = opt((int64_t)k * (SL | 1));
   p.oGsq = opt(4 * kk);
-  p.oMs = opt((int64_t)k * SL);
+  p.oMs = opt((int64_t)k * (SL | 1));
   p.oXf = opt((int64_t)nk * b);
   p.oMat3 = opt(3 * kk + kt);
-  p.oCin = opt((int64_t)k * SL);
+  p.oCin = opt((int64_t)k * (SL | 1));
   p.oTail = opt(p.flen + 3 * kt);
   p.total = o;
   p.gws_stride = p.oGsq >= 0 ? 0 : 4 * kk;
   return true;
 }
+
+bool small_step_plan(SmallArgs& a, int CL) { return plan_once(a, CL, 1) || plan_once(a, CL, 0); }
 
 // Largest cluster (<= 16 CTAs, >= 24 columns per CTA where possible) whose plan fits and
 // which the device can co-schedule.

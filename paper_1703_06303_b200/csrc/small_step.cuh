@@ -87,23 +87,25 @@ WLR_DEVI double* xpart(SS& s, const SSPlan& p) { return s.sm + p.oPart + (int64_
 
 // Fixed-order cluster sum of the len-long partial every CTA wrote into its exchange bank;
 // out is local.  (Arguments by value: this is a shared, non-inlined routine.)
-WLR_NOINL void xreduce_impl(const double* mine, int CL, int len, double* out) {
+WLR_NOINL void xreduce_impl(const double* mine, int CL, int len, double* out, int len2, double* out2) {
   cg::cluster_group cl = cg::this_cluster();
   cl.sync();
 #pragma unroll 1
-  for (int i = threadIdx.x; i < len; i += kSST) {
+  for (int i = threadIdx.x; i < len + len2; i += kSST) {
     double v[16];
 #pragma unroll
     for (int c = 0; c < 16; ++c) v[c] = c < CL ? cl.map_shared_rank(mine, c)[i] : 0.0;
     double acc = 0.0;
 #pragma unroll
     for (int c = 0; c < 16; ++c) acc += v[c];
-    out[i] = acc;
+    if (i < len) out[i] = acc;
+    else out2[i - len] = acc;
   }
   __syncthreads();
 }
-WLR_DEVI void xreduce(SS& s, const SSPlan& p, int len, double* out) {
-  xreduce_impl(xpart(s, p), s.CL, len, out);
+// (a second segment of len2 values, if any, lands in out2)
+WLR_DEVI void xreduce(SS& s, const SSPlan& p, int len, double* out, int len2 = 0, double* out2 = nullptr) {
+  xreduce_impl(xpart(s, p), s.CL, len, out, len2, out2);
   s.bank ^= 1;
 }
 
@@ -127,36 +129,44 @@ WLR_NOINL void block_sum_n(double (&v)[NV], double* red) {
   __syncthreads();
 }
 
-WLR_NOINL double block_max(double v, double* red) {
+// barrier over the nt threads of named barrier `bar` (bar 0 with nt = kSST: __syncthreads)
+WLR_DEVI void bar_sync(int bar, int nt) { asm volatile("bar.sync %0, %1;\n" ::"r"(bar), "r"(nt) : "memory"); }
+
+// max over the threads [t0, t0 + nt) (whole warps), valid on all of them
+WLR_NOINL double block_max(double v, double* red, int t0 = 0, int nt = kSST, int bar = 0) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = (threadIdx.x - t0) >> 5, lane = threadIdx.x & 31;
   if (lane == 0) red[warp] = v;
-  __syncthreads();
+  bar_sync(bar, nt);
   double m = 0.0;
-#pragma unroll
-  for (int w = 0; w < kSSW; ++w) m = fmax(m, red[w]);
-  __syncthreads();
+  #pragma unroll 1
+  for (int w = 0; w < (nt >> 5); ++w) m = fmax(m, red[w]);
+  bar_sync(bar, nt);
   return m;
 }
 
-// C[r][c] = alpha * sum_q A[r*lda + q] B[q*ldb + c] (+ I if addI), thread per output.
+// C[r][c] = alpha * sum_q A[r*lda + q] B[q*ldb + c] (+ I if addI), thread per output, on the
+// threads [t0, t0 + nt) of the block (no barrier inside).
 WLR_NOINL void gemm_nn(int m, int n, int kk, const double* A, int lda, const double* B, int ldb,
-                      double* C, int ldc, double alpha, bool addI) {
+                      double* C, int ldc, double alpha, bool addI, int t0 = 0, int nt = kSST) {
   #pragma unroll 1
-  for (int o = threadIdx.x; o < m * n; o += kSST) {
+  for (int o = threadIdx.x - t0; o < m * n; o += nt) {
     const int r = o / n, c = o - r * n;
     const double* pa = A + (int64_t)r * lda;
     const double* pb = B + c;
-    double v0 = 0.0, v1 = 0.0;
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
     int q = 0;
     #pragma unroll 1
-    for (; q + 1 < kk; q += 2) {
+    for (; q + 3 < kk; q += 4) {
       v0 = fma(pa[q], pb[(int64_t)q * ldb], v0);
       v1 = fma(pa[q + 1], pb[(int64_t)(q + 1) * ldb], v1);
+      v2 = fma(pa[q + 2], pb[(int64_t)(q + 2) * ldb], v2);
+      v3 = fma(pa[q + 3], pb[(int64_t)(q + 3) * ldb], v3);
     }
-    if (q < kk) v0 = fma(pa[q], pb[(int64_t)q * ldb], v0);
-    double v = alpha * (v0 + v1);
+    #pragma unroll 1
+    for (; q < kk; ++q) v0 = fma(pa[q], pb[(int64_t)q * ldb], v0);
+    double v = alpha * ((v0 + v1) + (v2 + v3));
     if (addI && r == c) v += 1.0;
     C[(int64_t)r * ldc + c] = v;
   }
@@ -238,29 +248,31 @@ WLR_NOINL bool sweep_inverse(double* A, int n, double rel, double* d0, double* r
 // R = I - G X, X <- X + X R.  Returns false (uniformly) when max|I - G X| >= 3e-2 (the
 // warm start is too far: the caller falls back to the sweep).  The number of steps is
 // chosen from the initial residual so that delta^(2^steps) <= 1e-12.
-WLR_NOINL bool ns_inverse(const double* G, double* X, double* R, double* P, int n, double* red) {
-  gemm_nn(n, n, n, G, n, X, n, R, n, -1.0, true);
-  __syncthreads();
+// Runs on the threads [t0, t0 + nt) with named barrier `bar` (defaults: the whole block).
+WLR_NOINL bool ns_inverse(const double* G, double* X, double* R, double* P, int n, double* red,
+                          int t0 = 0, int nt = kSST, int bar = 0) {
+  gemm_nn(n, n, n, G, n, X, n, R, n, -1.0, true, t0, nt);
+  bar_sync(bar, nt);
   double dm = 0.0;
   #pragma unroll 1
-  for (int idx = threadIdx.x; idx < n * n; idx += kSST) dm = fmax(dm, fabs(R[idx]));
-  const double delta = block_max(dm, red);
+  for (int idx = threadIdx.x - t0; idx < n * n; idx += nt) dm = fmax(dm, fabs(R[idx]));
+  const double delta = block_max(dm, red, t0, nt, bar);
   if (!(delta < 3e-2)) return false;
   const int steps = delta < 1e-6 ? 1 : delta < 1e-3 ? 2 : 3;
   #pragma unroll 1
   for (int st = 0; st < steps; ++st) {
     if (st > 0) {
-      gemm_nn(n, n, n, G, n, X, n, R, n, -1.0, true);
-      __syncthreads();
+      gemm_nn(n, n, n, G, n, X, n, R, n, -1.0, true, t0, nt);
+      bar_sync(bar, nt);
     }
-    gemm_nn(n, n, n, X, n, R, n, P, n, 1.0, false);
-    __syncthreads();
+    gemm_nn(n, n, n, X, n, R, n, P, n, 1.0, false, t0, nt);
+    bar_sync(bar, nt);
     #pragma unroll 1
-    for (int idx = threadIdx.x; idx < n * n; idx += kSST) X[idx] += P[idx];
-    __syncthreads();
+    for (int idx = threadIdx.x - t0; idx < n * n; idx += nt) X[idx] += P[idx];
+    bar_sync(bar, nt);
   }
   #pragma unroll 1
-  for (int idx = threadIdx.x; idx < n * n; idx += kSST) {   // symmetrise
+  for (int idx = threadIdx.x - t0; idx < n * n; idx += nt) {   // symmetrise
     const int i = idx / n, j = idx - i * n;
     if (i < j) {
       const double v = 0.5 * (X[idx] + X[(int64_t)j * n + i]);
@@ -268,7 +280,7 @@ WLR_NOINL bool ns_inverse(const double* G, double* X, double* R, double* P, int 
       X[(int64_t)j * n + i] = v;
     }
   }
-  __syncthreads();
+  bar_sync(bar, nt);
   return true;
 }
 
@@ -320,12 +332,12 @@ WLR_NOINL void tri_inverse(const double* L, const double* dinv, int n, double* L
   __syncthreads();
 }
 
-// Parallel (round-robin) cyclic Jacobi on the symmetric b x b matrix T (ld 32) by warp 0:
+// Parallel (round-robin) cyclic Jacobi on the symmetric b x b matrix T (ld 32), called by warp 0:
 // on exit th = eigenvalues in DESCENDING order and U (ld 32) the matching orthonormal
 // eigenvectors (columns).  b/2 disjoint rotations per round, b-1 rounds per sweep; stops
 // when every off-diagonal is at rounding level.  Deterministic.
 WLR_NOINL void jacobi_par(double* T, double* U, double* th, double* cs, int b) {
-  if (threadIdx.x < 32) {
+  {   // warp 0 only (the caller branches); no block barrier inside
     const int lane = threadIdx.x;
     const int nb = (b + 1) & ~1;
     const int np = nb / 2;
@@ -425,7 +437,6 @@ WLR_NOINL void jacobi_par(double* T, double* U, double* th, double* cs, int b) {
       #pragma unroll 1
       for (int i = 0; i < b; ++i) U[i * 32 + rk] = T[i * 32 + lane];
   }
-  __syncthreads();
 }
 
 // Z[slice] = S X[slice] = G_A[slice, :] X - M(:, slice)^T W   with W = C X (reduced, k x w).
@@ -588,6 +599,7 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
   extern __shared__ __align__(16) double ss_smem[];
   __shared__ double red[8 * kSSW];
   __shared__ int ok_s;
+  __shared__ int kok_s;                        // K^{-1} refined during the first Rayleigh-Ritz
   const SSPlan& p = a.pl;
   SS s;
   s.CL = p.CL;
@@ -610,11 +622,11 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
   double* SEs = s.sm + p.oSE;                  // nl x t   S_p E
   // C', M', C_in slice accessors: smem (ld SL) or global (ld nk, offset rs)
   double* Cs = p.oCs >= 0 ? s.sm + p.oCs : a.C_out + s.rs;
-  const int ldc = p.oCs >= 0 ? s.SL : nk;
+  const int ldc = p.oCs >= 0 ? (s.SL | 1) : nk;   // odd: conflict-free column walks
   double* Ms = p.oMs >= 0 ? s.sm + p.oMs : a.M_out + s.rs;
-  const int ldm = p.oMs >= 0 ? s.SL : nk;
+  const int ldm = p.oMs >= 0 ? (s.SL | 1) : nk;
   const double* Cin = p.oCin >= 0 ? s.sm + p.oCin : a.C_in + s.rs;
-  const int ldci = p.oCin >= 0 ? s.SL : nk;
+  const int ldci = p.oCin >= 0 ? (s.SL | 1) : nk;
   const double* incN = a.inc;
   const double* incGam = a.inc + (int64_t)k * nk;
   const double* incOm = incGam + (int64_t)kk;
@@ -654,6 +666,7 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
       Gq[idx] = g;
     }
     __syncthreads();
+    tmark(s, a);                               // [1a] Gram update loads
     bool okinv = a.mode ? ns_inverse(Gq, Xq, Rq, Pq, k, red) : false;
     if (!okinv) {
       for (int idx = threadIdx.x; idx < kk; idx += kSST) Xq[idx] = Gq[idx];
@@ -665,6 +678,7 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
     }
     if (s.c == 0)
       for (int idx = threadIdx.x; idx < kk; idx += kSST) a.Gi_out[idx] = Xq[idx];
+    if (threadIdx.x == 0) kok_s = 0;
     tmark(s, a);                               // [1] Gram update + G'^{-1}
     // C'[:, slice] = G'^{-1} M'[:, slice]
     gemm_nn(k, s.nl, k, Xq, k, Ms, ldm, Cs, ldc, 1.0, false);
@@ -693,12 +707,46 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
         const double* Z = s.sm + buf[iZ];
         double* part = xpart(s, p);
         const int tb = a.mode ? t : 0;
-        const TN d[4] = {{Y, 1, b, Y, 1, b, b, b, part},
+        // first pass: C'C'^T rides along (K = w^2 I + C'C'^T of the next row update) into Gq
+        // (through global memory when the exchange bank cannot hold it)
+        const int kc = outer == 0 ? k : 0;
+        const int lg = 2 * b * b + 2 * tb * b;
+        const TN d[5] = {{Y, 1, b, Y, 1, b, b, b, part},
                          {Y, 1, b, Z, 1, b, b, b, part + b * b},
                          {Vp, 1, t, Y, 1, b, tb, b, part + 2 * b * b},
-                         {Vp, 1, t, Z, 1, b, tb, b, part + 2 * b * b + t * b}};
-        slice_tn<4>(s.nl, d);
-        xreduce(s, p, 2 * b * b + 2 * tb * b, Gx);
+                         {Vp, 1, t, Z, 1, b, tb, b, part + 2 * b * b + t * b},
+                         {Cs, ldc, 1, Cs, ldc, 1, kc, k, p.ccx ? part + lg : a.xchg + (int64_t)s.c * p.flen}};
+        slice_tn<5>(s.nl, d);
+        tmark(s, a);                           // [4a] Gram partials
+        xreduce(s, p, lg, Gx, p.ccx ? kc * k : 0, Gq);
+        tmark(s, a);                           // [4b] exchange
+        if (kc) {
+          #pragma unroll 1
+          for (int idx = threadIdx.x; idx < kk; idx += kSST) {
+            const int i = idx / k, j = idx - i * k;
+            double v = 0.0;
+            if (p.ccx) {
+              v = 0.5 * (Gq[idx] + Gq[j * k + i]);
+            } else {
+              for (int c = 0; c < s.CL; ++c)
+                v += 0.5 * (__ldcg(a.xchg + (int64_t)c * p.flen + idx) + __ldcg(a.xchg + (int64_t)c * p.flen + j * k + i));
+            }
+            Rq[idx] = v;                       // symmetrised C'C'^T
+          }
+          __syncthreads();
+          #pragma unroll 1
+          for (int idx = threadIdx.x; idx < kk; idx += kSST) {
+            const int i = idx / k, j = idx - i * k;
+            const double v = Rq[idx];
+            if (!a.uniform && s.c == 0) {
+              if (a.dtype) reinterpret_cast<double*>(a.Kop)[idx] = v;
+              else reinterpret_cast<float*>(a.Kop)[idx] = (float)v;
+            }
+            Gq[idx] = v + (i == j ? a.w2 : 0.0);
+            if (a.mode && a.uniform) Xq[idx] = a.Ki[idx];
+          }
+          __syncthreads();
+        }
       }
       tmark(s, a);                             // Gram exchange
       // ---- local (every CTA identically): D = diag(Gyy)^-1/2; if D Gyy D = I to rounding
@@ -760,7 +808,15 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
           }
         }
         __syncthreads();
-        jacobi_par(Tb, Ub, th, sm + so.cs, b);
+        // warp 0: Jacobi; warps 1..: K^{-1} by Newton-Schulz from the previous one (first pass)
+        if (threadIdx.x < 32) {
+          jacobi_par(Tb, Ub, th, sm + so.cs, b);
+        } else if (outer == 0 && a.uniform && a.mode) {
+          // warps 1..: K^{-1} by Newton-Schulz from the previous one
+          const bool okk = ns_inverse(Gq, Xq, Rq, Pq, k, red + 32, 32, kSST - 32, 1);
+          if (threadIdx.x == 32) kok_s = okk ? 1 : 0;
+        }
+        __syncthreads();
         for (int idx = threadIdx.x; idx < b * b; idx += kSST) {     // Qb = D (Li^T U) or D U
           const int i = idx / b, j = idx - i * b;
           double v;
@@ -853,11 +909,10 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
     // Linear row update: Wt = [w^2 K^{-1}; U K^{-1}; P K^{-1}] for uniform W1,
     // [0; U; P] otherwise, with U = C'^T - V' (C'V')^T, P = (C'V')(C'V')^T, K = w^2 I + C'C'^T.
     const double* Y = s.sm + buf[iY];          // V' = Y[:, :t]
-    double* my = a.xchg + (int64_t)s.c * p.flen;
-    {   // slice partials of C' C'^T (k x k) and C' V' (k x t)
-      const TN d[2] = {{Cs, ldc, 1, Cs, ldc, 1, k, k, my},
-                       {Cs, ldc, 1, Y, 1, b, k, t, my + kk}};
-      slice_tn<2>(s.nl, d);
+    double* cvs = s.sm + p.oCinE;              // k x t (the residual region is free now)
+    {   // C'V' (k x t): slice partials, cluster sum
+      const TN d[1] = {{Cs, ldc, 1, Y, 1, b, k, t, xpart(s, p)}};
+      slice_tn<1>(s.nl, d);
     }
     for (int idx = threadIdx.x; idx < s.nl * t; idx += kSST) {
       const int r = idx / t, j = idx - r * t;
@@ -865,48 +920,12 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
     }
     for (int idx = threadIdx.x; idx < s.nl * b; idx += kSST) a.Y[(int64_t)s.rs * b + idx] = Y[idx];
     tmark(s, a);                               // operand partials
-    cg::this_cluster().sync();                 // partials in global memory (cluster scope)
-    // every CTA sums all k^2 + kt partials in the same fixed order: CC' into Gq (+ w^2 I when
-    // uniform, for the inverse), C'V' into cvs
-    double* cvs = s.sm + p.oCinE;              // k x t (the residual region is free now)
-#pragma unroll 1
-    for (int i = threadIdx.x; i < kk + kt; i += kSST) {
-      double v[16];
-#pragma unroll
-      for (int c = 0; c < 16; ++c) v[c] = c < s.CL ? __ldcg(a.xchg + (int64_t)c * p.flen + i) : 0.0;
-      double acc = 0.0;
-#pragma unroll
-      for (int c = 0; c < 16; ++c) acc += v[c];
-      if (i < kk) Gq[i] = acc;
-      else cvs[i - kk] = acc;
-    }
-    __syncthreads();
-#pragma unroll 1
-    for (int idx = threadIdx.x; idx < kk; idx += kSST) {   // symmetrise C'C'^T; K = w^2 I + CC'
-      const int i = idx / k, j = idx - i * k;
-      if (i < j) {
-        const double v = 0.5 * (Gq[idx] + Gq[j * k + i]);
-        Gq[idx] = v;
-        Gq[j * k + i] = v;
-      }
-    }
-    __syncthreads();
-    if (s.c == 0) {
-      for (int idx = threadIdx.x; idx < kk; idx += kSST) {
-        if (!a.uniform) {
-          if (a.dtype) reinterpret_cast<double*>(a.Kop)[idx] = Gq[idx];
-          else reinterpret_cast<float*>(a.Kop)[idx] = (float)Gq[idx];
-        }
-      }
+    xreduce(s, p, kt, cvs);
+    if (s.c == 0)
       for (int idx = threadIdx.x; idx < kt; idx += kSST) a.CV_out[idx] = cvs[idx];
-    }
+    tmark(s, a);                               // [8a] C'V' summed
     if (a.uniform) {
-      for (int i = threadIdx.x; i < k; i += kSST) Gq[i * k + i] += a.w2;
-      for (int idx = threadIdx.x; idx < kk && a.mode; idx += kSST) Xq[idx] = a.Ki[idx];
-      __syncthreads();
-      // K^{-1}: Newton-Schulz from the previous K^{-1}; sweep at init or as fallback
-      bool okk = a.mode ? ns_inverse(Gq, Xq, Rq, Pq, k, red) : false;
-      if (!okk) {
+      if (!kok_s) {   // init, or the warm start was too far: sweep K^{-1} from K (still in Gq)
         for (int idx = threadIdx.x; idx < kk; idx += kSST) Xq[idx] = Gq[idx];
         __syncthreads();
         if (!sweep_inverse(Xq, k, 0.0, sm + so.d0, sm + so.rb)) {
@@ -918,8 +937,11 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
       if (s.c == 0)
         for (int idx = threadIdx.x; idx < kk; idx += kSST) a.Ki[idx] = Xq[idx];
     }
-    // U rows of this slice: u[c][q] = C'[q][c] - sum_j V'[c][j] (C'V')[q][j]   (into Red)
+    tmark(s, a);                               // [8b] K^{-1} (fallback only)
+    // U rows of this slice: u[c][q] = C'[q][c] - sum_j V'[c][j] (C'V')[q][j]   (into Red);
+    // Qt = (C'V')^T K^{-1} (t x k, uniform) for the X1_p rows, after Us
     double* Us = s.sm + p.oRed;                // nl x k
+    double* Qt = Us + (int64_t)s.nl * k;       // t x k
 #pragma unroll 1
     for (int idx = threadIdx.x; idx < s.nl * k; idx += kSST) {
       const int c = idx / k, q = idx - c * k;
@@ -927,6 +949,19 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
       for (int j = 0; j < t; ++j) v = fma(-Y[c * b + j], cvs[q * t + j], v);
       Us[idx] = v;
     }
+    if (a.uniform)
+#pragma unroll 1
+      for (int idx = threadIdx.x; idx < kt; idx += kSST) {
+        const int i = idx / k, l = idx - i * k;
+        double v0 = 0.0, v1 = 0.0;
+        int q = 0;
+        for (; q + 1 < k; q += 2) {
+          v0 = fma(cvs[q * t + i], Xq[q * k + l], v0);
+          v1 = fma(cvs[(q + 1) * t + i], Xq[(q + 1) * k + l], v1);
+        }
+        if (q < k) v0 = fma(cvs[q * t + i], Xq[q * k + l], v0);
+        Qt[idx] = v0 + v1;
+      }
     __syncthreads();
     const int RP = a.rp;
     auto put = [&](int64_t row, int l, double v) {
@@ -940,32 +975,36 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
       const int c = idx / k, l = idx - c * k;
       double v;
       if (a.uniform) {
-        v = 0.0;
-        for (int q = 0; q < k; ++q) v = fma(Us[c * k + q], Xq[q * k + l], v);
+        const double* ur = Us + c * k;
+        double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+        int q = 0;
+        for (; q + 3 < k; q += 4) {
+          v0 = fma(ur[q], Xq[q * k + l], v0);
+          v1 = fma(ur[q + 1], Xq[(q + 1) * k + l], v1);
+          v2 = fma(ur[q + 2], Xq[(q + 2) * k + l], v2);
+          v3 = fma(ur[q + 3], Xq[(q + 3) * k + l], v3);
+        }
+        for (; q < k; ++q) v0 = fma(ur[q], Xq[q * k + l], v0);
+        v = (v0 + v1) + (v2 + v3);
       } else {
         v = Us[idx];
       }
       put(k + s.rs + c, l, v);
     }
-    if (s.c == 0) {
-      // A1 rows (uniform: w^2 K^{-1}) and X1_p rows (P K^{-1} or P), P = (C'V')(C'V')^T
+    // A1 rows (uniform: w^2 K^{-1}) and X1_p rows (P K^{-1} = (C'V') Qt, or P = (C'V')(C'V')^T),
+    // spread over the cluster: output o of [0, 2 k^2) on CTA o mod CL
 #pragma unroll 1
-      for (int idx = threadIdx.x; idx < kk; idx += kSST) {
-        const int j = idx / k, l = idx - j * k;
+    for (int o = s.c + s.CL * threadIdx.x; o < 2 * kk; o += s.CL * kSST) {
+      const int blk = o / kk, idx = o - blk * kk, j = idx / k, l = idx - j * k;
+      if (blk == 0) {
         if (a.uniform) put(j, l, a.w2 * Xq[idx]);
+      } else {
         double v = 0.0;
-        if (a.uniform) {
-          for (int q = 0; q < k; ++q) {
-            double pjq = 0.0;
-            for (int i = 0; i < t; ++i) pjq = fma(cvs[j * t + i], cvs[q * t + i], pjq);
-            v = fma(pjq, Xq[q * k + l], v);
-          }
-        } else {
-          for (int i = 0; i < t; ++i) v = fma(cvs[j * t + i], cvs[l * t + i], v);
-        }
+        for (int i = 0; i < t; ++i) v = fma(cvs[j * t + i], a.uniform ? Qt[i * k + l] : cvs[l * t + i], v);
         put(a.KA + j, l, v);
       }
     }
+    tmark(s, a);                               // [8c] Wt rows
     if (s.c != 0) return;
     // ---- CTA 0: small results for the deferred half
     if (a.mode) {
@@ -1011,7 +1050,7 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
       const int64_t gi = (int64_t)q * nk + s.rs + i;
       if (p.oCs >= 0) Cs[q * ldc + i] = a.C_out[gi];
       if (p.oMs >= 0) Ms[q * ldm + i] = a.M_out[gi];
-      if (p.oCin >= 0 && a.mode) s.sm[p.oCin + q * s.SL + i] = a.C_in[gi];
+      if (p.oCin >= 0 && a.mode) s.sm[p.oCin + q * ldci + i] = a.C_in[gi];
     }
     for (int idx = threadIdx.x; idx < s.nl * t; idx += kSST) {
       Vn[idx] = a.V_out[(int64_t)s.rs * t + idx];

@@ -21,15 +21,20 @@ def run(ci, warm=8, H=None, Wd=None):
     for rep in range(2):
         w.wlr_iterate_async(h, 1)
         torch.cuda.synchronize()
-        for name in ("K3a", "K3b"):
-            kt = w.wlr_debug_state(h, "ktime")       # K3a marks (debug_state flushes K3b after reading? no)
-            n = int(kt[0])
-            ts = kt[1:1 + n]
-            ck = kt[32:32 + n]
+        kt = w.wlr_debug_state(h, "ktime")   # [0:64] K3a(p), [64:128] K3b(p-1) (ran beside it)
+        for name, off in (("K3a", 0), ("K3b", 64)):
+            n = int(kt[off])
+            ts = kt[off + 1:off + 1 + n]
+            ck = kt[off + 32:off + 32 + n]
+            if n < 2:
+                continue
             d = np.diff(ts) / 1e3
             mhz = (ck[-1] - ck[0]) / max(ts[-1] - ts[0], 1) * 1e3
             print(f"cfg{ci} {name} total={(ts[-1]-ts[0])/1e3:.1f}us clk={mhz:.0f}MHz phases(us)=" + " ".join(f"{x:.1f}" for x in d))
-            w.wlr_sync(h)                            # runs the deferred half (records its marks)
+        t0a, t0b = kt[1], kt[65]
+        if int(kt[64]) > 1:
+            print(f"   K3b start - K3a start = {(t0b - t0a)/1e3:.1f}us")
+
 
 run(1)
 run(2)
