@@ -170,6 +170,16 @@ def wlr_result(h: Handle, x2: bool = False, b: bool = True):
     return dict(X1=X1, C=C, B=B, D=D, X2=X2)
 
 
+def wlr_row_path(h: Handle, tensor_cores: bool) -> bool:
+    """Select the row-pass implementation for uniform-weight fp32 problems: the tcgen05 3xTF32
+    kernel (default) or the CUDA-core FP32 kernel.  Returns whether the tensor-core path is
+    active afterwards (it is only available for uniform W1 with fp32 data)."""
+    cnt = ctypes.c_int64()
+    name = b"rowtc_on" if tensor_cores else b"rowtc_off"
+    check(lib.wlr_debug_state(h.raw, name, None, 0, ctypes.byref(cnt)), h.raw)
+    return bool(cnt.value)
+
+
 def wlr_debug_state(h: Handle, name: str) -> np.ndarray:
     cnt = ctypes.c_int64()
     check(lib.wlr_debug_state(h.raw, name.encode(), None, 0, ctypes.byref(cnt)), h.raw)

@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -90,6 +91,13 @@ struct wlr_ctx {
   void* X[2] = {nullptr, nullptr};
   void* Dl = nullptr;          // Delta = X1_{p+1} - X1_p (m x kp, written by the row pass)
   CUtensorMap tmA{}, tmX[2]{}, tmW{};   // TMA descriptors of A, X1 (per buffer) and Wt
+  // tensor-core row pass (uniform W1, fp32): 128-row boxes of A / X1 and the K-major W'^T
+  bool tc_ok = false, tc_on = false;
+  int tc_dbg = 0;                       // diagnostics only (WLR_TC_DBG)
+  unsigned long long* tc_tstamp = nullptr;   // per-CTA timestamps (WLR_TC_DBG & 16)
+  int tc_grid = 0;
+  void* WtT = nullptr; int KW = 0;
+  CUtensorMap tmA_tc{}, tmX_tc[2]{}, tmWT{};
   int nwc = 8;                 // row-pass warps running per-row Cholesky
   void *Wt = nullptr, *CVop = nullptr, *Kop = nullptr;
   double *inc_part = nullptr, *fw_part = nullptr, *fw0 = nullptr;
@@ -218,6 +226,7 @@ static SmallArgs small_args(wlr_ctx* h, int ph, int mode) {
   s.xchg = h->xchg; s.red = h->red; s.scal = h->scal;
   s.trace = h->trace; s.trace_cap = h->trace_cap;
   s.Wt = h->Wt; s.CVop = h->CVop; s.Kop = h->Kop; s.flags = h->flags;
+  s.WtT = h->WtT; s.KW = h->KW;
   s.eps = h->opts.eps; s.tol = h->opts.eig_tol; s.max_outer = h->opts.eig_max_outer; s.max_deg = 16;
   s.cold = 0;
   s.tdbg = h->ktime ? h->tdbg : nullptr;
@@ -271,7 +280,19 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int ph) {
     a.m = h->m; a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.no = (int)h->kp;
     a.vec_ok = (h->lda % 4 == 0) && ((uintptr_t)h->A % 16 == 0);
     set_prefetch(h, ph, a.pf_ptr, a.pf_bytes);
-    e = launch_row_pass<float>(a, h->rp, h->rp_tr, h->uniform, 0, h->rp_grid, h->st);
+    if (h->tc_on) {
+      RowPassTcArgs q{};
+      q.tmA = h->tmA_tc; q.tmX = h->tmX_tc[cur]; q.tmW = h->tmWT;
+      q.A = a.A; q.lda = a.lda; q.Xold = a.Xold; q.Xnew = a.Xnew; q.Dnew = a.Dnew;
+      q.w2s = a.w2s; q.fw_part = h->fw_part;
+      for (int i = 0; i < 6; ++i) { q.pf_ptr[i] = a.pf_ptr[i]; q.pf_bytes[i] = a.pf_bytes[i]; }
+      q.m = h->m; q.KA = h->KA; q.k = (int)h->k; q.kp = (int)h->kp;
+      q.dbg = h->tc_dbg;
+      q.tstamp = h->tc_tstamp;
+      e = launch_row_pass_tc(q, h->rp, h->tc_grid, h->st);
+    } else {
+      e = launch_row_pass<float>(a, h->rp, h->rp_tr, h->uniform, 0, h->rp_grid, h->st);
+    }
   } else {
     RowPassArgs<double> a{};
     a.A = (const double*)h->A; a.lda = h->lda; a.W1 = (const double*)h->W1; a.ldw = h->ldw;
@@ -307,7 +328,8 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int ph) {
   if (e != cudaSuccess) return fail(h, WLR_ECUDA, std::string("increments: ") + cudaGetErrorString(e));
   if (prof) cudaEventRecord(ev[2], h->st);
   launch_reduce_incr(h->inc_part, h->nsplit, (int)h->k, (int)h->nk, h->nz, (int)(h->k - h->k0),
-                     (int)(h->n - h->k0), (int)h->kp, h->fw_part, h->rp_grid, h->inc[cur], h->st);
+                     (int)(h->n - h->k0), (int)h->kp, h->fw_part, h->tc_on ? h->tc_grid : h->rp_grid,
+                     h->inc[cur], h->st);
   if (prof) cudaEventRecord(ev[3], h->st);
   if (h->comm) {
     const size_t cnt = (size_t)(h->k * h->nk + 2 * h->k * h->k + 1);
@@ -533,6 +555,31 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
     ok = ok && make_tmap_2d(&h->tmW, h->Wt, (int)es, (uint64_t)h->rp, (uint64_t)wt_rows, (uint64_t)h->rp * es,
                             (uint32_t)h->rp, 32u, false);
     if (!ok) return fail(h, WLR_ECUDA, "cuTensorMapEncodeTiled failed (TMA descriptors)");
+  }
+  // tensor-core row pass (uniform W1, fp32): K-major W'^T written by the small step
+  h->tc_ok = h->dtype == WLR_F32 && h->uniform;
+  if (const char* dbg = std::getenv("WLR_TC_DBG")) h->tc_dbg = std::atoi(dbg);
+  if (h->tc_dbg & 16) {
+    void* p = nullptr;
+    if ((s = dalloc(h, &p, 8 * 8 * 2048)) != WLR_OK) return s;
+    h->tc_tstamp = (unsigned long long*)p;
+  }
+  if (h->tc_ok) {
+    h->KW = (int)wt_rows;
+    if ((s = dalloc(h, &h->WtT, (size_t)2 * h->rp * wt_rows * es)) != WLR_OK) return s;   // W'^T | W'^T_lo
+    bool ok = make_tmap_2d(&h->tmA_tc, h->A, 4, (uint64_t)n, (uint64_t)h->m, (uint64_t)h->lda * 4, 32u, (uint32_t)kTcBM, true);
+    for (int i = 0; i < 2; ++i)
+      ok = ok && make_tmap_2d(&h->tmX_tc[i], h->X[i], 4, (uint64_t)kp, (uint64_t)h->m, (uint64_t)kp * 4, 32u, (uint32_t)kTcBM, true);
+    ok = ok && make_tmap_2d(&h->tmWT, h->WtT, 4, (uint64_t)wt_rows, (uint64_t)(2 * h->rp), (uint64_t)wt_rows * 4, 32u, (uint32_t)h->rp, true);
+    int occ = 0;
+    RowPassTcArgs q{};
+    if (ok && launch_row_pass_tc(q, h->rp, 0, h->st, &occ) == cudaSuccess && occ > 0) {
+      occ = std::max(occ, row_pass_tc_ctas_per_sm(h->rp));   // shared-memory bound (carveout 100)
+      h->tc_grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(h->m, kTcBM), (int64_t)h->nsm * occ));
+      h->tc_on = true;
+    } else {
+      h->tc_ok = false;
+    }
   }
   if ((s = dalloc(h, &h->CVop, (size_t)std::max<int64_t>(k * t, 1) * es)) != WLR_OK) return s;
   if ((s = dalloc(h, &h->Kop, (size_t)k * k * es)) != WLR_OK) return s;
@@ -930,12 +977,21 @@ extern "C" wlr_status wlr_debug_state(wlr_handle h, const char* name, double* ou
   else if (nm == "GA") { src = h->GA; cnt = h->nk * h->nk; }
   else if (nm == "scal") { src = h->scal; cnt = 8; }
   else if (nm == "ktime") { src = h->tdbg; cnt = 128; }
+  else if (nm == "tctime") { src = (const double*)h->tc_tstamp; cnt = h->tc_tstamp ? 8 * h->tc_grid : 0; }
   else if (nm == "ktime_on" || nm == "ktime_off") {   // enable/disable K3 phase timestamps
     h->ktime = nm == "ktime_on";
     for (auto& gp : h->gexec)
       for (auto& g : gp)
         if (g) { cudaGraphExecDestroy(g); g = nullptr; }
     if (count) *count = 0;
+    return WLR_OK;
+  }
+  else if (nm == "rowtc_on" || nm == "rowtc_off") {   // tensor-core / CUDA-core row pass (A/B)
+    h->tc_on = h->tc_ok && nm == "rowtc_on";
+    for (auto& gp : h->gexec)
+      for (auto& g : gp)
+        if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+    if (count) *count = h->tc_on ? 1 : 0;
     return WLR_OK;
   }
   else if (nm == "ss_rerun") {                 // relaunch the last small step twice (timing only;

@@ -59,6 +59,25 @@ cudaError_t launch_row_pass(const RowPassArgs<T>& a, int rp, int tr, bool unifor
                             cudaStream_t st, int* occ = nullptr,   // occ: only report CTAs/SM
                             bool pdl = false);   // programmatic dependent of the previous kernel
 
+// ------------------------------------------------- row pass on tcgen05 (rowpass_tc.cu)
+// Uniform-weight fp32 row update X1_{p+1} = [A | X1_p] W' on the 5th-generation tensor cores
+// with 3xTF32: 128-row tiles, TMEM accumulator, K-major W'^T.
+struct RowPassTcArgs {
+  CUtensorMap tmA, tmX;             // boxes 32 columns (128 B, SWIZZLE_128B) x 128 rows
+  CUtensorMap tmW;                  // W'^T (RP x KW, K-major): boxes 32 x RP, SWIZZLE_128B
+  const float* A; int64_t lda;
+  const float* Xold; float* Xnew; float* Dnew;   // m x kp
+  float w2s;
+  double* fw_part;                  // gridDim.x partials of f_w
+  const void* pf_ptr[6]; int64_t pf_bytes[6];
+  int64_t m; int KA, k, kp;
+  unsigned long long* tstamp;       // diagnostics: 8 globaltimer stamps per CTA, or nullptr
+  int dbg;                          // diagnostics: bit 0 skip the lo conversion, bit 1 skip the MMAs, bit 2 skip W loads, bit 3 skip epilogue
+};
+constexpr int kTcBM = 64;           // rows per tile (UMMA M)
+cudaError_t launch_row_pass_tc(const RowPassTcArgs& a, int rp, int grid, cudaStream_t st, int* occ = nullptr);
+int row_pass_tc_ctas_per_sm(int rp);   // co-resident CTAs by shared memory (228 KB per SM)
+
 template <typename T>
 struct IncrArgs {
   const T* A; int64_t lda;
@@ -94,6 +113,7 @@ struct SSPlan {
 struct SmallArgs {
   int k, nk, t, b, kp, k0, rp;      // dims; b = eigen block width (t <= b <= 32)
   int KA;                           // row offset of the X1_p block of the row-pass Wt
+  void* WtT; int KW;                // fp32 W'^T (RP x KW, K-major) for the tensor-core row pass
   int mode;                         // 0: init (G, M given), 1: iteration (apply increments)
   int dtype;                        // 0 fp32 operands, 1 fp64 operands
   int uniform; double w2;           // uniform weight squared

@@ -968,6 +968,13 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
       const int64_t o = row * RP + l;
       if (a.dtype) reinterpret_cast<double*>(a.Wt)[o] = v;
       else reinterpret_cast<float*>(a.Wt)[o] = (float)v;
+      if (a.WtT) {   // K-major fp32 copy W'^T and its 3xTF32 low part (tensor-core row pass)
+        const float f = (float)v;
+        const float hi = __uint_as_float(__float_as_uint(f) & 0xFFFFE000u);
+        float* wt = reinterpret_cast<float*>(a.WtT) + (int64_t)l * a.KW + row;
+        wt[0] = f;
+        wt[(int64_t)RP * a.KW] = f - hi;
+      }
     };
     // Wt rows k + rs + c (columns of A2 in this slice): u K^{-1} or u
 #pragma unroll 1

@@ -1,0 +1,21 @@
+"""Timeline of the tensor-core row pass: per-CTA globaltimer stamps (WLR_TC_DBG=16)."""
+import sys
+import numpy as np
+sys.path.insert(0, ".")
+import torch
+import synth
+import paper_1703_06303_b200 as w
+cfg = synth.CONFIGS[3]
+A = torch.from_numpy(synth.make_A(cfg)).cuda()
+flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+h = w.wlr_init(A, cfg.k, cfg.r, None, w1=cfg.w_const)
+w.wlr_iterate(h, 5)
+flush.fill_(1.0)
+w.wlr_iterate_async(h, 1)
+torch.cuda.synchronize()
+t = w.wlr_debug_state(h, "tctime").view(np.uint64).astype(np.int64).reshape(-1, 8)
+t0 = t[:, 0].min()
+names = ["start", "first_full", "first_tma", "epi_wait", "accfull", "epi_done", "end"]
+for i, nm in enumerate(names):
+    v = (t[:, i] - t0) / 1e3
+    print(f"{nm:11s} min {v.min():7.2f} med {np.median(v):7.2f} max {v.max():7.2f} us")

@@ -27,7 +27,7 @@ def inputs(cfg):
     return A, W1
 
 
-def run_gpu(cfg, A, W1, iters, device=True, **kw):
+def run_gpu(cfg, A, W1, iters, device=True, tensor_cores=True, **kw):
     import torch
     w = need_gpu()
     if device:
@@ -36,6 +36,7 @@ def run_gpu(cfg, A, W1, iters, device=True, **kw):
     else:
         At, Wt = A, W1
     h = w.wlr_init(At, cfg.k, cfg.r, Wt, w1=cfg.w_const or 1.0, **kw)
+    tc = w.wlr_row_path(h, tensor_cores)
     tr0 = w.wlr_trace(h)
     if iters:
         done, conv = w.wlr_iterate(h, iters)
@@ -44,6 +45,7 @@ def run_gpu(cfg, A, W1, iters, device=True, **kw):
     res["trace0"] = tr0
     res["handle"] = h
     res["keep"] = (At, Wt)
+    res["tensor_cores"] = tc
     return res
 
 

@@ -39,6 +39,32 @@ def test_config2_small_fp32_full_run():
     gu.compare(cfg, g, o)
 
 
+@pytest.mark.parametrize("tensor_cores", [True, False])
+def test_config2_row_pass_paths(tensor_cores):
+    """Uniform-weight fp32: the tcgen05 3xTF32 row pass (default) and the CUDA-core FP32 row
+    pass each meet the parity bar; the tensor-core path is the one active by default."""
+    cfg = synth.CONFIGS[2]
+    A, W1 = gu.inputs(cfg)
+    g = gu.run_gpu(cfg, A, W1, cfg.iters, tensor_cores=tensor_cores)
+    assert g["tensor_cores"] == tensor_cores
+    o = gu.run_oracle(cfg, A, W1, cfg.iters)
+    gu.compare(cfg, g, o)
+
+
+def test_row_pass_tensor_core_ragged_tail():
+    """m not a multiple of the 64-row tensor-core tile, k = r - 1 < 32, n ragged vs the
+    32-column chunk: tensor-core path against the oracle."""
+    g0 = np.random.default_rng(5)
+    m, n, k, r = 1000 + 37, 75, 13, 15
+    A = (g0.standard_normal((m, 16)) @ g0.standard_normal((16, n)) + 0.02 * g0.standard_normal((m, n)))
+    cfg = dataclasses.replace(synth.CONFIGS[2], m=m, n=n, k=k, r=r, w_const=30.0, iters=12)
+    A = A.astype(np.float32)
+    g = gu.run_gpu(cfg, A, None, cfg.iters)
+    assert g["tensor_cores"]
+    o = gu.run_oracle(cfg, A, None, cfg.iters)
+    gu.compare(cfg, g, o)
+
+
 def test_step0_is_ghs_on_gpu():
     """p = 0 is the Theorem 1 closed form on the GPU too (pin P1 path)."""
     cfg = synth.CONFIGS[2]
