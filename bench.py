@@ -111,6 +111,14 @@ def incr_flops(cfg):
     return cfg.m * 2 * k * (nk + 2 * k)
 
 
+def row_pass_bytes(cfg):
+    """Algorithmic HBM bytes of one row pass: A read, X1_p read, X1_{p+1} and Delta written
+    (kp = k rounded up to 4 columns; W' and the small operands are L2-resident)."""
+    s = 4 if cfg.dtype == "f32" else 8
+    kp = (cfg.k + 3) // 4 * 4
+    return s * cfg.m * (cfg.n + 3 * kp + (0 if cfg.uniform_w else cfg.k))
+
+
 def iteration_bytes(cfg):
     s = 4 if cfg.dtype == "f32" else 8
     return s * cfg.m * (cfg.n + 2 * cfg.k + (0 if cfg.uniform_w else cfg.k))
@@ -234,6 +242,7 @@ def main():
                    nranks=world, rank=rank, nccl_id=nccl_id, stream=stream.cuda_stream)
     torch.cuda.synchronize()
     t_init = time.perf_counter() - t0
+    tensor_cores = w.wlr_row_path(h, True)     # tcgen05 row pass when eligible (uniform fp32)
 
     w.wlr_iterate_async(h, args.warmup)
     w.wlr_sync(h)
@@ -265,21 +274,40 @@ def main():
     value = 1e3 / ms_per_step
     F, step_norm, rel = w.wlr_objective(h)
 
-    # dominant kernel of the step and its roofline
+    # per-kernel rooflines; the roofline object is the dominant m-scaled (streaming) kernel
     iters = max(prof["iters"], 1)
     kern_ms = {"row_pass": prof["row_pass"] / iters, "increments": prof["increments"] / iters,
-               "reduce": prof["reduce"] / iters, "small_step": prof["small_step"] / iters}
+               "reduce": prof["reduce"] / iters, "small_step": prof["small_step"] / iters,
+               "deferred_small_step": prof["deferred"] / iters}
     cfg_local = dataclasses.replace(cfg, m=r1 - r0)
-    flops = {"row_pass": row_pass_flops(cfg_local), "increments": incr_flops(cfg_local)}
-    dom = max(("row_pass", "increments"), key=lambda kk: kern_ms[kk])
     peaks, peak_kind = measured_peaks()
-    achieved = flops[dom] / (kern_ms[dom] * 1e-3) / 1e12
-    roof = {"kernel": dom, "bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS,
-            "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS,
-            "peak_source": "derived CUDA-core FP32: 148 SM x 128 lanes x 2 x 1.965 GHz (DESIGN.md §6)",
-            "traffic": ncu_traffic(dom),
-            "kernel_ms": kern_ms,
-            "kernel_share_of_step": {kk: v / ms_per_step for kk, v in kern_ms.items()}}
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    kernels = {}
+    if tensor_cores:
+        a = row_pass_bytes(cfg_local) / (kern_ms["row_pass"] * 1e-3) / 1e9
+        kernels["row_pass"] = {"bound": "hbm", "achieved": a, "peak": hbm_peak, "unit": "GB/s",
+                               "frac": a / hbm_peak, "impl": "tcgen05 3xTF32",
+                               "per_unit": "4 (n + 3 kp) bytes per pixel row"}
+    else:
+        a = row_pass_flops(cfg_local) / (kern_ms["row_pass"] * 1e-3) / 1e12
+        kernels["row_pass"] = {"bound": "alu", "achieved": a, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
+                               "frac": a / FP32_PEAK_TFLOPS, "impl": "CUDA-core FP32"}
+    a = incr_flops(cfg_local) / (kern_ms["increments"] * 1e-3) / 1e12
+    kernels["increments"] = {"bound": "alu", "achieved": a, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
+                             "frac": a / FP32_PEAK_TFLOPS, "impl": "CUDA-core FP32",
+                             "per_unit": "2 k (n - k + 2 k) flops per pixel row"}
+    kernels["small_step"] = {"bound": "latency", "ms": kern_ms["small_step"],
+                             "note": "one 16-CTA cluster, fp64, dependent chain (DESIGN.md §5.3)"}
+    dom = max(("row_pass", "increments"), key=lambda kk: kern_ms[kk])
+    roof = dict(kernels[dom])
+    roof.update({"kernel": dom,
+                 "peak_source": (f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, burst)" if roof["unit"] == "GB/s"
+                                 else "derived CUDA-core FP32: 148 SM x 128 lanes x 2 x 1.965 GHz (DESIGN.md §6)"),
+                 "traffic": ncu_traffic(dom),
+                 "kernel_ms": kern_ms,
+                 "kernel_share_of_step": {kk: v / ms_per_step for kk, v in kern_ms.items()},
+                 "dominant_of_step": max(("row_pass", "increments", "small_step"), key=lambda kk: kern_ms[kk]),
+                 "kernels": kernels})
     alg_gbs = iteration_bytes(cfg_local) / (ms_per_step * 1e-3) / 1e9
 
     # end-to-end through the C ABI with HOST buffers: H2D of A (pinned) + init +

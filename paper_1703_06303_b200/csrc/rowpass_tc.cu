@@ -3,15 +3,17 @@
 // The uniform-weight row update is one dense contraction over every pixel row
 // (Algorithm 1 lines 7-9, as the linear update of DESIGN.md §2):
 //     X1_{p+1}(i,:) = [A(i,:) | X1_p(i,:)] W',   W' = [w^2 K^{-1}; U K^{-1}; P K^{-1}]
-// so a tile of 128 rows is a 128 x RP x (KA + kp) GEMM.  The CUDA-core version is bound by
-// FP32 issue; here it runs as tcgen05.mma kind::tf32 with the 3xTF32 split
-//     a b ~ a_hi b_hi + a_hi b_lo + a_lo b_hi,   a_hi = tf32(a) (the tensor core truncates),
-// which keeps fp32-level accuracy.  Data path per 32-column chunk:
-//   TMA (SWIZZLE_128B) -> smem  Z = [A | X1_p] chunk (128 x 32) and W'^T chunk (RP x 32)
-//   all threads: Z_lo = Z - tf32(Z), W_lo likewise (generic proxy), fence.proxy.async
-//   thread 0: 4 k-steps x 3 MMAs into the TMEM accumulator, tcgen05.commit -> stage free
-// Epilogue: warp w reads TMEM lanes [32w, 32w+32) (its 32 rows), writes X1_{p+1}, Delta and
-// an fp64 partial of f_w, exactly as the CUDA-core kernel does.
+// so a tile of 64 rows is a 64 x RP x (KA + KX) GEMM.  It runs as tcgen05.mma kind::tf32 with the
+// 3xTF32 split
+//     z w ~ z_hi w_hi + z_hi w_lo + z_lo w_hi,   z_hi = tf32(z) (the tensor core truncates),
+// W'^T and W'^T_lo are written K-major by the small step; Z_lo is made here.  Per 32-column chunk:
+//   warp 4 (1 thread)  : TMA (SWIZZLE_128B) Z = [A | X1_p] chunk (64 x 32), W'^T, W'^T_lo
+//   warps 0-3          : Z_lo = Z - tf32(Z) into the lo ring (generic proxy), fence.proxy.async
+//   warp 5 (1 thread)  : 4 k-steps x 3 MMAs into the TMEM accumulator; tcgen05.commit frees
+//                        the raw and lo stages (and signals the epilogue after the last chunk)
+// Epilogue (warps 0-3): TMEM lanes 32w..32w+15 hold rows 16w..16w+15 of the M = 64 tile
+// (measured, profiles/r01_ubench_umma_m64_layout.log); writes X1_{p+1}, Delta and an fp64
+// partial of f_w.  A1 and X1_p of the row are captured from the stream (chunks 0 and KA/32).
 #include "kernels.h"
 #include "umma.cuh"
 
