@@ -231,11 +231,15 @@ def main():
     A = torch.from_numpy(synth.make_A(cfg, r0, r1)).cuda()
     W1n = synth.make_W1(cfg, r0, r1)
     W1 = None if W1n is None else torch.from_numpy(W1n).cuda()
-    nccl_id = None
-    if world > 1:
+    def fresh_nccl_id():
+        # one ncclUniqueId per communicator (every handle owns its own), broadcast from rank 0
+        if world == 1:
+            return None
         obj = [w.wlr_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+        return obj[0]
+
+    nccl_id = fresh_nccl_id()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     h = w.wlr_init(A, cfg.k, cfg.r, W1, w1=cfg.w_const or 1.0, m_global=cfg.m, row_offset=r0,
@@ -319,12 +323,13 @@ def main():
         solves, its = 2, cfg.iters
         e_ms = []
         for s in range(solves + 1):
+            idn = fresh_nccl_id()
             if dist:
                 dist.barrier()
             torch.cuda.synchronize()
             ts = time.perf_counter()
             he = w.wlr_init(Ah, cfg.k, cfg.r, Wh, w1=cfg.w_const or 1.0, m_global=cfg.m, row_offset=r0,
-                            nranks=world, rank=rank, nccl_id=nccl_id, stream=stream.cuda_stream)
+                            nranks=world, rank=rank, nccl_id=idn, stream=stream.cuda_stream)
             w.wlr_iterate_async(he, its)
             res = w.wlr_result(he, x2=False)
             torch.cuda.synchronize()
@@ -344,6 +349,28 @@ def main():
                "step": f"one full solve from pinned host A: H2D + GHS init + {its} iterations + D2H(X1, C, B, D)",
                "ms_per_solve": emax}
 
+    # time to tolerance (north_star): GHS init, eps = 1e-7 stopping rule (R3/R14),
+    # inputs resident in HBM; the iterations' wall time (init reported separately)
+    ttt = None
+    if not args.no_e2e:
+        if dist:
+            dist.barrier()
+        idt = fresh_nccl_id()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ht = w.wlr_init(A, cfg.k, cfg.r, W1, w1=cfg.w_const or 1.0, m_global=cfg.m, row_offset=r0, eps=1e-7,
+                        nranks=world, rank=rank, nccl_id=idt, stream=stream.cuda_stream)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        done, conv = w.wlr_iterate(ht, 1000)
+        t2 = time.perf_counter()
+        Ft, st_, rl_ = w.wlr_objective(ht)
+        w.wlr_destroy(ht)
+        ttt = {"eps": 1e-7, "iters": done, "converged": conv, "ms": (t2 - t1) * 1e3,
+               "ms_incl_init": (t2 - t0) * 1e3, "final_rel_step": rl_}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_sample(cfg)
@@ -362,6 +389,7 @@ def main():
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "time_to_tolerance": ttt,
             "gpu_launches": prof["launches"],
             "clocks": clk.summary(),
             "init_ms": t_init * 1e3,

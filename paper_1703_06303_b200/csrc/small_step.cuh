@@ -449,7 +449,7 @@ template <int PW>
 WLR_DEVI void s_product_impl(double* smb, int rs, int nl, int SL, int k, int nk, int KS, int JS,
                               int64_t oRed, int64_t oXf, const double* GA, int64_t xoff, int ldx,
                               int w, const double* Wk, const double* Mp, int ldm, double* Z,
-                              int ldz) {
+                              int ldz, SS* ms = nullptr, const SmallArgs* ma = nullptr) {
   struct { int rs, nl, SL, k, nk; double* sm; } s = {rs, nl, SL, k, nk, smb};
   struct { int KS, JS; } p = {KS, JS};
   cg::cluster_group cl = cg::this_cluster();
@@ -475,6 +475,7 @@ WLR_DEVI void s_product_impl(double* smb, int rs, int nl, int SL, int k, int nk,
     }
     __syncthreads();
   }
+  if (ms) tmark(*ms, *ma);                        // [p3] X gathered
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ks = warp / p.JS, js = warp - ks * p.JS;
   const int cw = (w + p.JS - 1) / p.JS;
@@ -538,6 +539,7 @@ WLR_DEVI void s_product_impl(double* smb, int rs, int nl, int SL, int k, int nk,
       }
     }
   }
+  if (ms) tmark(*ms, *ma);                        // [p4] main loop (warp 0's share)
   if (l0 < l1) {
 #pragma unroll
     for (int j = 0; j < PW; ++j) {
@@ -564,7 +566,7 @@ template <int PW>
 WLR_DEVI void s_product(SS& s, const SmallArgs& a, int64_t xoff, int ldx, int w,
                         const double* Wk, const double* Mp, int ldm, double* Z, int ldz) {
   s_product_impl<PW>(s.sm, s.rs, s.nl, s.SL, s.k, s.nk, a.pl.KS, a.pl.JS, a.pl.oRed, a.pl.oXf,
-                     a.GA, xoff, ldx, w, Wk, Mp, ldm, Z, ldz);
+                     a.GA, xoff, ldx, w, Wk, Mp, ldm, Z, ldz, &s, &a);
 }
 
 // One S-product of the basis X (local slice at offset xoff, width w = row stride):
@@ -577,8 +579,10 @@ WLR_DEVI void s_apply(SS& s, const SmallArgs& a, const double* Cs, int ldc, cons
   double* part = xpart(s, p);
   const TN d[1] = {{Cs, ldc, 1, X, 1, w, s.k, w, part}};
   slice_tn<1>(s.nl, d);
+  tmark(s, a);                                 // [p1] C X partials
   double* Wk = s.sm + p.oWk;
   xreduce(s, p, s.k * w, Wk);
+  tmark(s, a);                                 // [p2] C X exchange
   s_product<PW>(s, a, xoff, w, w, Wk, Ms, ldm, s.sm + zoff, w);
   ++*nprod;
 }

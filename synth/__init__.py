@@ -171,6 +171,17 @@ def make_A(cfg: Config, r0: int = 0, r1: Optional[int] = None) -> np.ndarray:
     return _scene_rows(cfg, r0, r1, _scene_params(cfg))
 
 
+def make_background(cfg: Config, r0: int = 0, r1: Optional[int] = None) -> np.ndarray:
+    """Rows [r0, r1) of the clean background of a scene config: the rank-q illumination-
+    modulated part of make_A before the foreground block, the noise, the clipping and the
+    salt-and-pepper (the ground truth of SURVEY.md §8(f4) / SPEC.md's generate_scene)."""
+    if cfg.kind == "lowrank":
+        raise ValueError("the low-rank config has no background ground truth")
+    r1 = cfg.m if r1 is None else r1
+    c = _scene_params(cfg)[0]
+    return (_basis(cfg, np.arange(r0, r1)) @ c).astype(np.float64)
+
+
 def make_W1(cfg: Config, r0: int = 0, r1: Optional[int] = None) -> Optional[np.ndarray]:
     """Rows [r0, r1) of W1 (m x k, entries > 0), or None when W1 is uniform
     (then ``cfg.w_const`` is the scalar weight)."""
