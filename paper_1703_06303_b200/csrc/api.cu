@@ -527,7 +527,9 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   h->rps = round_up(ceil_div(h->m, nsplit), 32);
   h->nsplit = (int)std::max<int64_t>(1, ceil_div(h->m, h->rps));
   // eigen block width b
-  int b = o.eig_block > 0 ? o.eig_block : (int)(t + 6);
+  // warm block: 2 spare Ritz vectors for r-k <= 4 (one product per iteration at steady state,
+  // profiles/r01_v7_eigblock.log), 6 otherwise (narrow gaps at configs 4-5)
+  int b = o.eig_block > 0 ? o.eig_block : (int)(t + (t <= 4 ? 2 : 6));
   b = (int)std::min<int64_t>(std::max<int64_t>(b, t), nk);
   if (b > 32) b = 32;
   if (b < t) return fail(h, WLR_EINVAL, "r-k > 32 is not supported by this build");
