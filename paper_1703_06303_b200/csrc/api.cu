@@ -100,7 +100,8 @@ struct wlr_ctx {
   CUtensorMap tmA_tc{}, tmX_tc[2]{}, tmWT{};
   int nwc = 8;                 // row-pass warps running per-row Cholesky
   void *Wt = nullptr, *CVop = nullptr, *Kop = nullptr;
-  double *inc_part = nullptr, *fw_part = nullptr, *fw0 = nullptr;
+  double *inc_part = nullptr, *inc_part2 = nullptr, *fw_part = nullptr, *fw0 = nullptr;
+  int ics = 1, ncl = 0;        // increment row splits per cluster, cluster partials
   double* inc[2] = {nullptr, nullptr};   // packed increments, by iteration parity
   double* GA = nullptr;
   double a2sq = 0.0;
@@ -312,7 +313,7 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int ph) {
     IncrArgs<float> a{};
     a.A = (const float*)h->A; a.lda = h->lda;
     a.Xold = (const float*)h->X[cur]; a.Dnew = (const float*)h->Dl;
-    a.part = h->inc_part; a.m = h->m; a.rows_per_split = h->rps;
+    a.part = h->inc_part; a.part2 = h->inc_part2; a.cs = h->ics; a.m = h->m; a.rows_per_split = h->rps;
     a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.k0 = (int)h->k0; a.nz = h->nz; a.nsplit = h->nsplit;
     a.vec_ok = (h->lda % 4 == 0) && ((uintptr_t)h->A % 16 == 0) && (h->n % 4 == 0);
     e = launch_incr<float>(a, h->bm, h->st);
@@ -320,14 +321,14 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int ph) {
     IncrArgs<double> a{};
     a.A = (const double*)h->A; a.lda = h->lda;
     a.Xold = (const double*)h->X[cur]; a.Dnew = (const double*)h->Dl;
-    a.part = h->inc_part; a.m = h->m; a.rows_per_split = h->rps;
+    a.part = h->inc_part; a.part2 = h->inc_part2; a.cs = h->ics; a.m = h->m; a.rows_per_split = h->rps;
     a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.k0 = (int)h->k0; a.nz = h->nz; a.nsplit = h->nsplit;
     a.vec_ok = (h->lda % 4 == 0) && ((uintptr_t)h->A % 16 == 0) && (h->n % 4 == 0);
     e = launch_incr<double>(a, h->bm, h->st);
   }
   if (e != cudaSuccess) return fail(h, WLR_ECUDA, std::string("increments: ") + cudaGetErrorString(e));
   if (prof) cudaEventRecord(ev[2], h->st);
-  launch_reduce_incr(h->inc_part, h->nsplit, (int)h->k, (int)h->nk, h->nz, (int)(h->k - h->k0),
+  launch_reduce_incr(h->ics > 1 ? h->inc_part2 : h->inc_part, h->ics > 1 ? h->ncl : h->nsplit, (int)h->k, (int)h->nk, h->nz, (int)(h->k - h->k0),
                      (int)(h->n - h->k0), (int)h->kp, h->fw_part, h->tc_on ? h->tc_grid : h->rp_grid,
                      h->inc[cur], h->st);
   if (prof) cudaEventRecord(ev[3], h->st);
@@ -520,12 +521,15 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
     h->rp_grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)h->nsm * best_cps));
   }
   h->bm = incr_bm((int)kp);
-  const int bn = incr_bn(h->bm);
+  const int bn = incr_bn(h->bm, (int)es);
   h->nz = (int)((n - h->k0) + 2 * kp);
   const int ncol = (int)ceil_div(h->nz, bn);
   int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(h->m, 128), ceil_div(4 * h->nsm, ncol)));
   h->rps = round_up(ceil_div(h->m, nsplit), 32);
   h->nsplit = (int)std::max<int64_t>(1, ceil_div(h->m, h->rps));
+  // clusters of 8 row splits pre-reduce their partials through DSMEM (8x fewer for K2c)
+  h->ics = h->nsplit >= 8 && incr_cluster_ok() ? 8 : 1;
+  h->ncl = (int)ceil_div(h->nsplit, h->ics);
   // eigen block width b
   // warm block: 2 spare Ritz vectors for r-k <= 4 (one product per iteration at steady state,
   // profiles/r01_v7_eigblock.log), 6 otherwise (narrow gaps at configs 4-5)
@@ -586,6 +590,7 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   if ((s = dalloc(h, &h->CVop, (size_t)std::max<int64_t>(k * t, 1) * es)) != WLR_OK) return s;
   if ((s = dalloc(h, &h->Kop, (size_t)k * k * es)) != WLR_OK) return s;
   if ((s = dalloc_t(h, &h->inc_part, (size_t)h->nsplit * k * h->nz)) != WLR_OK) return s;
+  if ((s = dalloc_t(h, &h->inc_part2, (size_t)h->ncl * k * h->nz)) != WLR_OK) return s;
   if ((s = dalloc_t(h, &h->fw_part, (size_t)std::max(h->rp_grid, 1184))) != WLR_OK) return s;
   for (int i = 0; i < 2; ++i)
     if ((s = dalloc_t(h, &h->inc[i], (size_t)(k * nk + 2 * k * k + 1))) != WLR_OK) return s;

@@ -82,13 +82,16 @@ template <typename T>
 struct IncrArgs {
   const T* A; int64_t lda;
   const T* Xold; const T* Dnew;     // m x kp  X1_p and Delta
-  double* part;                     // nsplit x k x nz
+  double* part;                     // nsplit x k x nz (per-CTA fp64 chunk sums, rows > 256 only)
+  double* part2;                    // (grid.y / cs) x k x nz: one fp64 partial per cluster
   int64_t m; int64_t rows_per_split;
   int n, k, kp, k0, nz, nsplit;
+  int cs;                           // row splits per thread-block cluster (DSMEM pre-reduction)
   int vec_ok;
 };
 int incr_bm(int kp);
-int incr_bn(int bm);
+inline bool incr_cluster_ok() { return true; }   // 8-CTA clusters of 128-512 threads (portable)
+int incr_bn(int bm, int elem_bytes);   // columns per CTA
 template <typename T> cudaError_t launch_incr(const IncrArgs<T>& a, int bm, cudaStream_t st);
 void launch_reduce_incr(const double* part, int nsplit, int k, int nk, int nz, int kshift, int nA,
                         int kp, const double* fw_part, int nfw, double* inc, cudaStream_t st);

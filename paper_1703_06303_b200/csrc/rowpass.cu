@@ -24,6 +24,9 @@
 // increment pass re-reads it from L2 (46 MB at the metric's config fits the 126 MB L2).
 #include "kernels.h"
 
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
+
 namespace wlr {
 
 // ------------------------------------------------------------------------- cp.async
@@ -481,51 +484,53 @@ template cudaError_t launch_row_pass<float>(const RowPassArgs<float>&, int, int,
 template cudaError_t launch_row_pass<double>(const RowPassArgs<double>&, int, int, bool, int, int, cudaStream_t, int*, bool);
 
 // ------------------------------------------------------------------------------ K2b
-// Thread tile 8 (q) x 4 (columns); warp w owns q in [8w, 8w+8) and lanes 32 column groups,
-// so the Delta operand is a warp broadcast and the Z operand one LDS.128 per lane.
-// Z = [A(:, k0:n) | X1_p | Delta]; stages arrive by cp.async (double-buffered).
+// Thread tile 8 (q) x TW (columns); warp w owns q in [8w, 8w+8) and lane l the columns
+// [l TW, l TW + TW) of the CTA's BN-wide block (BN = 32 TW), so the Delta operand is a warp
+// broadcast and the Z operand TW/4 LDS.128 per lane.  Z = [A(:, k0:n) | X1_p | Delta] arrives by
+// cp.async (4-stage ring of 16-row stages); every thread copies ONE fixed 16-byte column of Z
+// (its source pointer and row stride are set once).  fp32 inside 256-row chunks, then fp64.
+// BN = 128 (8 x 4 tiles).  A BN = 256 variant (8 x 8 tiles, 64 FFMA per 4 LDS.128) needed 168
+// registers and ran 1.7x slower at config 3 (3 CTAs/SM, a second wave).
 constexpr int kIncRC = 16;          // rows per stage
 constexpr int kIncNST = 4;          // cp.async pipeline stages
-constexpr int kIncBN = 128;         // columns per CTA
 constexpr int kIncFlush = 16;       // stages per fp32 chunk (256 rows), then fp64
 
 int incr_bm(int kp) { return kp <= 32 ? 32 : kp <= 64 ? 64 : kp <= 128 ? 128 : -1; }
-int incr_bn(int) { return kIncBN; }
+int incr_bn(int, int) { return 128; }   // (BN = 256 with 8 x 8 tiles measured slower: 168 regs)
 
-template <typename T, int BM>
-size_t incr_smem_bytes() { return sizeof(T) * kIncNST * (size_t)kIncRC * (BM + kIncBN); }
+template <typename T, int BM, int BN>
+size_t incr_smem_bytes() {   // stages; after the mainloop the fp64 BM x BN tile of the cluster sum
+  return std::max(sizeof(T) * kIncNST * (size_t)kIncRC * (BM + BN), sizeof(double) * BM * BN);
+}
 
-template <typename T, int BM>
+template <typename T, int BM, int BN>
 __global__ void __launch_bounds__(BM * 4) incr_kernel(IncrArgs<T> a) {
   constexpr int NT = BM * 4;                    // threads: BM/8 warps
-  constexpr int BN = kIncBN;
+  constexpr int TW = BN / 32;                   // columns per lane
   constexpr int VE = 16 / (int)sizeof(T);
+  constexpr int CPR = BN / VE;                  // 16-byte copies per Z row
+  static_assert(NT % CPR == 0 || CPR % NT == 0, "copy mapping");
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* Ds = reinterpret_cast<T*>(smem_raw);       // [2][RC][BM]
+  T* Ds = reinterpret_cast<T*>(smem_raw);       // [NST][RC][BM]
   T* Zs = Ds + kIncNST * kIncRC * BM;           // [NST][RC][BN]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int q0 = warp * 8, c0 = lane * 4;
+  const int q0 = warp * 8, c0 = lane * TW;
   const int j0 = blockIdx.x * BN;
   const int64_t rb0 = (int64_t)blockIdx.y * a.rows_per_split;
-  const int64_t re = rb0 + a.rows_per_split < a.m ? rb0 + a.rows_per_split : a.m;
+  const int64_t re = rb0 + a.rows_per_split < a.m ? rb0 + a.rows_per_split : (rb0 < a.m ? a.m : rb0);
   const int kp = a.kp;
   const int nA = a.n - a.k0;
   const bool vec = a.vec_ok;
 
-  // per-thread copy slots of the Z stage: fixed column -> fixed source base and row stride
-  constexpr int ZS = kIncRC * (BN / VE) / NT;
-  const T* zsrc[ZS];
-  int64_t zld[ZS];
-#pragma unroll
-  for (int e = 0; e < ZS; ++e) {
-    const int idx = threadIdx.x + e * NT;
-    const int zc = j0 + (idx % (BN / VE)) * VE;
-    zsrc[e] = nullptr;
-    zld[e] = 0;
-    if (zc < nA) { zsrc[e] = a.A + a.k0 + zc; zld[e] = a.lda; }
-    else if (zc < nA + kp) { zsrc[e] = a.Xold + (zc - nA); zld[e] = kp; }
-    else if (zc < nA + 2 * kp) { zsrc[e] = a.Dnew + (zc - nA - kp); zld[e] = kp; }
-  }
+  // Z copy slot of this thread: column cv (fixed), rows rr0, rr0 + RS, ...
+  constexpr int RS = NT >= CPR ? NT / CPR : 1;  // rows per pass of all threads
+  const int cv = (threadIdx.x % CPR) * VE, rr0 = threadIdx.x / CPR;
+  const int zc = j0 + cv;
+  const T* zsrc = nullptr;
+  int64_t zld = 0;
+  if (zc < nA) { zsrc = a.A + a.k0 + zc; zld = a.lda; }
+  else if (zc < nA + kp) { zsrc = a.Xold + (zc - nA); zld = kp; }
+  else if (zc < nA + 2 * kp) { zsrc = a.Dnew + (zc - nA - kp); zld = kp; }
   auto issue = [&](int64_t rb, int st) {
     T* ds = Ds + st * kIncRC * BM;
     for (int idx = threadIdx.x; idx < kIncRC * (BM / VE); idx += NT) {
@@ -537,22 +542,20 @@ __global__ void __launch_bounds__(BM * 4) incr_kernel(IncrArgs<T> a) {
     T* zs = Zs + st * kIncRC * BN;
     if (vec) {
 #pragma unroll
-      for (int e = 0; e < ZS; ++e) {
-        const int idx = threadIdx.x + e * NT;
-        const int rr = idx / (BN / VE), cv = (idx % (BN / VE)) * VE;
+      for (int rr = rr0; rr < kIncRC; rr += RS) {
         const int64_t row = rb + rr;
-        const bool in = zsrc[e] != nullptr && row < re;
-        cp_async16(zs + rr * BN + cv, in ? zsrc[e] + row * zld[e] : a.A, in ? 16 : 0);
+        const bool in = zsrc != nullptr && row < re;
+        cp_async16(zs + rr * BN + cv, in ? zsrc + row * zld : a.A, in ? 16 : 0);
       }
     } else {
-      for (int idx = threadIdx.x; idx < kIncRC * (BN / VE); idx += NT) {
-        const int rr = idx / (BN / VE), cv = (idx % (BN / VE)) * VE;
+      for (int idx = threadIdx.x; idx < kIncRC * CPR; idx += NT) {
+        const int rr = idx / CPR, cc = (idx % CPR) * VE;
         const int64_t row = rb + rr;
-        const int zc = j0 + cv;
-        T* dst = zs + rr * BN + cv;
+        const int zcc = j0 + cc;
+        T* dst = zs + rr * BN + cc;
 #pragma unroll
         for (int q = 0; q < VE; ++q) {
-          const int c = zc + q;
+          const int c = zcc + q;
           T v = T(0);
           if (row < re) {
             if (c < nA) v = a.A[row * a.lda + a.k0 + c];
@@ -565,11 +568,11 @@ __global__ void __launch_bounds__(BM * 4) incr_kernel(IncrArgs<T> a) {
     }
   };
 
-  T acc[8][4];
+  T acc[8][TW];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = T(0);
+    for (int j = 0; j < TW; ++j) acc[i][j] = T(0);
   double* out = a.part + (int64_t)blockIdx.y * a.k * a.nz;
   bool first = true;
   // fp32 chunk sums are added into this CTA's fp64 partial (fixed order)
@@ -578,10 +581,10 @@ __global__ void __launch_bounds__(BM * 4) incr_kernel(IncrArgs<T> a) {
     for (int i = 0; i < 8; ++i) {
       const int l = q0 + i;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int zc = j0 + c0 + j;
-        if (l < a.k && zc < a.nz) {
-          double* o = out + (int64_t)l * a.nz + zc;
+      for (int j = 0; j < TW; ++j) {
+        const int zcol = j0 + c0 + j;
+        if (l < a.k && zcol < a.nz) {
+          double* o = out + (int64_t)l * a.nz + zcol;
           *o = first ? (double)acc[i][j] : *o + (double)acc[i][j];
         }
         acc[i][j] = T(0);
@@ -589,7 +592,7 @@ __global__ void __launch_bounds__(BM * 4) incr_kernel(IncrArgs<T> a) {
     }
     first = false;
   };
-  const int nst = (int)ceil_div(re - rb0, kIncRC);
+  const int nst = (int)ceil_div(re - rb0, (int64_t)kIncRC);   // 0 for padding CTAs of a cluster
 #pragma unroll
   for (int q = 0; q < kIncNST - 1; ++q) {
     if (q < nst) issue(rb0 + (int64_t)q * kIncRC, q);
@@ -606,13 +609,13 @@ __global__ void __launch_bounds__(BM * 4) incr_kernel(IncrArgs<T> a) {
     const T* zs = Zs + st * kIncRC * BN;
 #pragma unroll 4
     for (int rr = 0; rr < kIncRC; ++rr) {
-      T dv[8], zv[4];
+      T dv[8], zv[TW];
       lds_vec<T, 8>(ds + rr * BM + q0, dv);
-      lds_vec<T, 4>(zs + rr * BN + c0, zv);
+      lds_vec<T, TW>(zs + rr * BN + c0, zv);
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(dv[i], zv[j], acc[i][j]);
+        for (int j = 0; j < TW; ++j) acc[i][j] = fma(dv[i], zv[j], acc[i][j]);
     }
     if (sizeof(T) == 4 && ++stage == kIncFlush && s + 1 < nst) {
       stage = 0;
@@ -620,13 +623,39 @@ __global__ void __launch_bounds__(BM * 4) incr_kernel(IncrArgs<T> a) {
     }
     __syncthreads();
   }
-  flush();
+  if (a.cs <= 1) {
+    flush();
+    return;
+  }
+  // cluster pre-reduction: the cs row splits of this cluster sum their fp64 tiles through DSMEM
+  // in rank order; rank r writes rows [r BM / cs, (r+1) BM / cs) of the cluster's partial
+  double* tile = reinterpret_cast<double*>(smem_raw);         // BM x BN (the stages are free)
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < TW; ++j) {
+      const int l = q0 + i, zcol = j0 + c0 + j;
+      double v = (double)acc[i][j];
+      if (!first && l < a.k && zcol < a.nz) v += out[(int64_t)l * a.nz + zcol];
+      tile[l * BN + c0 + j] = v;
+    }
+  cg::cluster_group cl = cg::this_cluster();
+  cl.sync();
+  const int rk = (int)cl.block_rank(), rows = BM / a.cs;
+  double* o2 = a.part2 + (int64_t)(blockIdx.y / a.cs) * a.k * a.nz;
+  for (int idx = threadIdx.x; idx < rows * BN; idx += NT) {
+    const int q = rk * rows + idx / BN, c = idx % BN;
+    double v = 0.0;
+    for (int r = 0; r < a.cs; ++r) v += cl.map_shared_rank(tile, r)[q * BN + c];
+    if (q < a.k && j0 + c < a.nz) o2[(int64_t)q * a.nz + j0 + c] = v;
+  }
+  cl.sync();                                                  // peers' tiles stay alive until read
 }
 
-template <typename T, int BM>
+template <typename T, int BM, int BN>
 static cudaError_t launch_incr_bm(const IncrArgs<T>& a, cudaStream_t st) {
-  auto kern = incr_kernel<T, BM>;
-  const size_t smem = incr_smem_bytes<T, BM>();
+  auto kern = incr_kernel<T, BM, BN>;
+  const size_t smem = incr_smem_bytes<T, BM, BN>();
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -635,17 +664,27 @@ static cudaError_t launch_incr_bm(const IncrArgs<T>& a, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  dim3 grid((unsigned)ceil_div(a.nz, kIncBN), (unsigned)a.nsplit);
-  kern<<<grid, BM * 4, smem, st>>>(a);
-  return cudaGetLastError();
+  const int cs = a.cs > 1 ? a.cs : 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)ceil_div(a.nz, BN), (unsigned)(ceil_div(a.nsplit, cs) * cs));
+  cfg.blockDim = dim3(BM * 4);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 1; at[0].val.clusterDim.y = cs; at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = cs > 1 ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
 template <typename T>
 cudaError_t launch_incr(const IncrArgs<T>& a, int bm, cudaStream_t st) {
   switch (bm) {
-    case 32: return launch_incr_bm<T, 32>(a, st);
-    case 64: return launch_incr_bm<T, 64>(a, st);
-    case 128: return launch_incr_bm<T, 128>(a, st);
+    case 32:
+      return launch_incr_bm<T, 32, 128>(a, st);
+    case 64: return launch_incr_bm<T, 64, 128>(a, st);
+    case 128: return launch_incr_bm<T, 128, 128>(a, st);
     default: return cudaErrorInvalidValue;
   }
 }
