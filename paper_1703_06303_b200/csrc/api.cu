@@ -329,7 +329,8 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int ph) {
   if (e != cudaSuccess) return fail(h, WLR_ECUDA, std::string("increments: ") + cudaGetErrorString(e));
   if (prof) cudaEventRecord(ev[2], h->st);
   launch_reduce_incr(h->ics > 1 ? h->inc_part2 : h->inc_part, h->ics > 1 ? h->ncl : h->nsplit, (int)h->k, (int)h->nk, h->nz, (int)(h->k - h->k0),
-                     (int)(h->n - h->k0), (int)h->kp, h->fw_part, h->tc_on ? h->tc_grid : h->rp_grid,
+                     (int)(h->n - h->k0), (int)h->kp, h->fw_part,
+                     h->tc_on ? h->tc_grid : h->rp_grid,
                      h->inc[cur], h->st);
   if (prof) cudaEventRecord(ev[3], h->st);
   if (h->comm) {
@@ -984,7 +985,7 @@ extern "C" wlr_status wlr_debug_state(wlr_handle h, const char* name, double* ou
   else if (nm == "GA") { src = h->GA; cnt = h->nk * h->nk; }
   else if (nm == "scal") { src = h->scal; cnt = 8; }
   else if (nm == "ktime") { src = h->tdbg; cnt = 128; }
-  else if (nm == "tctime") { src = (const double*)h->tc_tstamp; cnt = h->tc_tstamp ? 8 * h->tc_grid : 0; }
+  else if (nm == "tctime") { src = (const double*)h->tc_tstamp; cnt = h->tc_tstamp ? 16 * h->tc_grid : 0; }
   else if (nm == "ktime_on" || nm == "ktime_off") {   // enable/disable K3 phase timestamps
     h->ktime = nm == "ktime_on";
     for (auto& gp : h->gexec)

@@ -72,11 +72,12 @@ struct RowPassTcArgs {
   const void* pf_ptr[6]; int64_t pf_bytes[6];
   int64_t m; int KA, k, kp;
   unsigned long long* tstamp;       // diagnostics: 8 globaltimer stamps per CTA, or nullptr
-  int dbg;                          // diagnostics: bit 0 skip the lo conversion, bit 1 skip the MMAs, bit 2 skip W loads, bit 3 skip epilogue
+  int dbg;                          // diagnostics: bit 2 skip W loads, bit 3 skip epilogue
 };
-constexpr int kTcBM = 64;           // rows per tile (UMMA M)
+constexpr int kTcBM = 128;          // rows per tile (UMMA M)
 cudaError_t launch_row_pass_tc(const RowPassTcArgs& a, int rp, int grid, cudaStream_t st, int* occ = nullptr);
 int row_pass_tc_ctas_per_sm(int rp);   // co-resident CTAs by shared memory (228 KB per SM)
+
 
 template <typename T>
 struct IncrArgs {

@@ -504,7 +504,7 @@ size_t incr_smem_bytes() {   // stages; after the mainloop the fp64 BM x BN tile
 }
 
 template <typename T, int BM, int BN>
-__global__ void __launch_bounds__(BM * 4) incr_kernel(IncrArgs<T> a) {
+__global__ void __launch_bounds__(BM * 4, BM == 32 ? 5 : 1) incr_kernel(IncrArgs<T> a) {
   constexpr int NT = BM * 4;                    // threads: BM/8 warps
   constexpr int TW = BN / 32;                   // columns per lane
   constexpr int VE = 16 / (int)sizeof(T);

@@ -19,32 +19,53 @@
 
 namespace wlr {
 
-// Warp roles (192 threads): warps 0-3 convert (lo parts) and run the epilogue (TMEM lanes
-// 32w..32w+15 hold rows 16w..16w+15 of an M = 64 tile), warp 4 lane 0 issues TMA, warp 5
-// lane 0 issues the MMAs.  Rings: NR raw stages (TMA -> smem) and NL lo stages.
+// Warp roles (192 threads): warps 0-3 convert (lo parts) and run the epilogue (warp w reads TMEM
+// lanes 32w.. : rows 32w..32w+31 of an M = 128 tile; rows 16w..16w+15 of an M = 64 tile), warp 4
+// lane 0 issues TMA, warp 5 lane 0 issues the MMAs.  Rings: NR raw stages (TMA -> smem) and NL
+// lo stages.  M = 128: a TF32 MMA with N = 32, K = 8 costs ~44 cycles whether M is 64 or 128
+// (profiles/r01_ubench_umma_rate.log), so the 128-row tile halves the per-row MMA time.
 constexpr int kTcThreads = 192;
-constexpr int kTcNR = 3, kTcNL = 3;
+// The A operand lives in TMEM: each converter thread owns one row of the tile, reads its 32
+// values of the chunk from the swizzled stage and writes Z_hi, Z_lo into TMEM (tcgen05.st);
+// the MMAs read A from TMEM (the "TS" form) and only W'^T from shared memory.  Shared-memory
+// traffic per chunk drops from ~100 KB (Z_lo staged in smem, Z read twice by the tensor core)
+// to ~52 KB, which was the binding limit (profiles/r01_v7_rowpass_tc_roles.log).
+// (Separate Z / W' rings with a polling producer were measured no faster: the MMA issue rate,
+// ~90 cycles per N <= 64 MMA in situ, and the converter -> MMA handoff bound the chunk rate.)
+constexpr int kTcNR = 4, kTcNL = 3;
+constexpr int kTcRPW = kTcBM / 4;                  // epilogue rows per warp
 
 template <int RP>
 struct TcLayout {                                  // bytes; every block 1024-aligned
   static constexpr int ZB = kTcBM * 128;          // Z chunk (fp32 BM x 32)
   static constexpr int WB = RP * 128;             // W'^T chunk (RP x 32)
   static constexpr int STAGE = ZB + 2 * WB;       // raw stage = Z | W'^T | W'^T_lo (all TMA)
-  static constexpr int TOTAL = kTcNR * STAGE + kTcNL * ZB;   // + lo ring of Z_lo
-  static constexpr int NCOL = RP < 32 ? 32 : RP;  // TMEM columns (power of 2 >= 32)
+  static constexpr int TOTAL = kTcNR * STAGE;
+  // TMEM columns: accumulator [0, RP) z_hi w_hi + z_lo w_hi, [RP, 2 RP) z_hi w_lo; then NL slots
+  // of 64 columns (Z_hi chunk | Z_lo chunk, 32 fp32 each)
+  static constexpr int ACC = 2 * RP < 64 ? 64 : 2 * RP;
+  static constexpr int NCOL = ACC + 64 * kTcNL <= 256 ? 256 : 512;
 };
 
 template <int RP>
-__global__ void __launch_bounds__(kTcThreads, 3) row_pass_tc_kernel(const __grid_constant__ RowPassTcArgs a) {
+__global__ void __launch_bounds__(kTcThreads, 2) row_pass_tc_kernel(const __grid_constant__ RowPassTcArgs a) {
   using L = TcLayout<RP>;
   extern __shared__ __align__(1024) unsigned char tc_raw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tc_raw) + 1023) & ~(uintptr_t)1023);
   unsigned char* rawst = sm;                               // [NR][Z | W | W_lo]
-  unsigned char* lost = sm + kTcNR * L::STAGE;             // [NL][Z_lo]
   __shared__ __align__(8) uint64_t full[kTcNR], rawfree[kTcNR], lofull[kTcNL], lofree[kTcNL], accfull, accfree;
   __shared__ uint32_t tslot;
   __shared__ double wsum[4];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  auto twait = [&](uint64_t* bar, uint32_t par, unsigned long long& acc) {
+    if (a.tstamp) {
+      const unsigned long long t0 = clock64();
+      mbar_wait(bar, par);
+      acc += clock64() - t0;
+    } else {
+      mbar_wait(bar, par);
+    }
+  };
   auto stamp = [&](int i) {
     if (a.tstamp) {
       unsigned long long t;
@@ -73,47 +94,50 @@ __global__ void __launch_bounds__(kTcThreads, 3) row_pass_tc_kernel(const __grid
 
   if (warp == 4) {
     // ---------------- TMA producer
+    unsigned long long w_prod = 0;
     if (lane == 0) {
       int s = 0, c = 0;
       uint32_t ph = 0;
       int64_t tile = blockIdx.x;
       for (int64_t g = 0; g < total; ++g) {
-        if (g >= kTcNR) mbar_wait(&rawfree[s], ph ^ 1);
+        if (g >= kTcNR) twait(&rawfree[s], ph ^ 1, w_prod);
         if (g == 0) stamp(2);
         const int r0 = (int)(tile * kTcBM);
         unsigned char* st = rawst + s * L::STAGE;
-        mbar_expect_tx(&full[s], (uint32_t)((a.dbg & 4) ? L::ZB : L::STAGE));
+        mbar_expect_tx(&full[s], (uint32_t)L::STAGE);
         if (c < nchA) tma_load_2d(st, &a.tmA, &full[s], c * 32, r0);
         else tma_load_2d(st, &a.tmX, &full[s], (c - nchA) * 32, r0);
         const int kw = c < nchA ? c * 32 : a.KA + (c - nchA) * 32;
-        if (!(a.dbg & 4)) {
-          tma_load_2d(st + L::ZB, &a.tmW, &full[s], kw, 0);
-          tma_load_2d(st + L::ZB + L::WB, &a.tmW, &full[s], kw, RP);
-        }
+        tma_load_2d(st + L::ZB, &a.tmW, &full[s], kw, 0);
+        tma_load_2d(st + L::ZB + L::WB, &a.tmW, &full[s], kw, RP);
         if (++s == kTcNR) { s = 0; ph ^= 1; }
         if (++c == nch) { c = 0; tile += gridDim.x; }
       }
     }
+    if (lane == 0 && a.tstamp) a.tstamp[(int64_t)gridDim.x * 8 + blockIdx.x * 8 + 0] = w_prod;
   } else if (warp == 5) {
     // ---------------- MMA issuer
+    unsigned long long w_lof = 0, w_accf = 0;
     if (lane == 0) {
-      const uint32_t idesc = umma_idesc_tf32<kTcBM, RP>();
+      // per k-step two MMAs: Z_hi against [W_hi; W_lo] (N = 2 RP, the two halves are adjacent in
+      // the stage) and Z_lo against W_hi (N = RP) -- Z_hi is read once and the fixed per-MMA
+      // cost (~44 cycles at N <= 64) is paid twice instead of three times
+      const uint32_t idesc2 = umma_idesc_tf32<kTcBM, 2 * RP>();
+      const uint32_t idesc1 = umma_idesc_tf32<kTcBM, RP>();
       int r = 0, l = 0, c = 0;
       uint32_t phl = 0, pht = 0;
       int64_t tl = 0;
       for (int64_t g = 0; g < total; ++g) {
-        if (c == 0 && tl > 0) { mbar_wait(&accfree, pht); pht ^= 1; }   // epilogue drained TMEM
-        mbar_wait(&lofull[l], phl);
+        if (c == 0 && tl > 0) { twait(&accfree, pht, w_accf); pht ^= 1; }   // epilogue drained TMEM
+        twait(&lofull[l], phl, w_lof);
         tc_fence_after();
-        const uint32_t zs = smem_u32(rawst + r * L::STAGE), ws = zs + L::ZB, wl = ws + L::WB;
-        const uint32_t zl = smem_u32(lost + l * L::ZB);
+        const uint32_t ws = smem_u32(rawst + r * L::STAGE) + L::ZB;
+        const uint32_t ta = tmem + (uint32_t)(L::ACC + 64 * l);   // Z_hi | Z_lo of this chunk
 #pragma unroll
-        for (int kk = 0; kk < ((a.dbg & 2) ? 0 : 4); ++kk) {   // K = 8 tf32 (32 bytes) per MMA
-          const uint64_t dzh = umma_desc_k_sw128(zs + kk * 32), dzl = umma_desc_k_sw128(zl + kk * 32);
-          const uint64_t dwh = umma_desc_k_sw128(ws + kk * 32), dwl = umma_desc_k_sw128(wl + kk * 32);
-          umma_tf32(tmem, dzh, dwh, idesc, c > 0 || kk > 0);
-          umma_tf32(tmem, dzh, dwl, idesc, true);
-          umma_tf32(tmem, dzl, dwh, idesc, true);
+        for (int kk = 0; kk < 4; ++kk) {           // K = 8 tf32 (8 TMEM columns) per MMA
+          const uint64_t dw = umma_desc_k_sw128(ws + kk * 32);
+          umma_tf32_ts(tmem, ta + 8 * kk, dw, idesc2, c > 0 || kk > 0);
+          umma_tf32_ts(tmem, ta + 32 + 8 * kk, dw, idesc1, true);
         }
         umma_commit(&rawfree[r]);
         umma_commit(&lofree[l]);
@@ -121,6 +145,10 @@ __global__ void __launch_bounds__(kTcThreads, 3) row_pass_tc_kernel(const __grid
         if (++r == kTcNR) r = 0;
         if (++l == kTcNL) { l = 0; phl ^= 1; }
         if (++c == nch) { c = 0; ++tl; }
+      }
+      if (a.tstamp) {
+        a.tstamp[(int64_t)gridDim.x * 8 + blockIdx.x * 8 + 1] = w_lof;
+        a.tstamp[(int64_t)gridDim.x * 8 + blockIdx.x * 8 + 2] = w_accf;
       }
     }
   } else {
@@ -130,44 +158,46 @@ __global__ void __launch_bounds__(kTcThreads, 3) row_pass_tc_kernel(const __grid
     int r = 0, l = 0, c = 0;
     uint32_t phr = 0, phl = 0;
     int64_t tl = 0;
+    unsigned long long w_full = 0, w_lofree = 0, w_acc = 0, t_conv = 0;
     for (int64_t g = 0; g < total; ++g) {
-      mbar_wait(&full[r], phr);
+      twait(&full[r], phr, w_full);
       if (g == 0 && tid == 0) stamp(1);
-      if (g >= kTcNL) mbar_wait(&lofree[l], phl ^ 1);
-      const float4* src = reinterpret_cast<const float4*>(rawst + r * L::STAGE);
-      float4* dst = reinterpret_cast<float4*>(lost + l * L::ZB);
-      if (RP <= 32 && lane < 16 && (c == 0 || c == nchA)) {
-        // this thread's epilogue row (16 warp + lane): A1 = chunk 0, X1_p = chunk nchA
-        const int rr = 16 * warp + lane;
+      if (g >= kTcNL) twait(&lofree[l], phl ^ 1, w_lofree);
+      const unsigned long long tc0 = a.tstamp ? clock64() : 0;
+      {   // this thread's row (32 warp + lane) of the chunk: 8 swizzled 16-byte units
+        const int rr = 32 * warp + lane;
+        const float4* src = reinterpret_cast<const float4*>(rawst + r * L::STAGE) + rr * 8;
+        float hi[32], lo[32];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          const float4 v = src[rr * 8 + (q ^ (rr & 7))];   // SWIZZLE_128B: 16-byte unit q of row rr
-          if (c == 0) a1r[q] = v;
-          else xor_[q] = v;
+          const float4 v = src[q ^ (rr & 7)];
+          if (RP <= 32 && c == 0) a1r[q] = v;            // A1 (epilogue operand)
+          if (RP <= 32 && c == nchA) xor_[q] = v;        // X1_p
+          tf32_split(v.x, hi[4 * q], lo[4 * q]);
+          tf32_split(v.y, hi[4 * q + 1], lo[4 * q + 1]);
+          tf32_split(v.z, hi[4 * q + 2], lo[4 * q + 2]);
+          tf32_split(v.w, hi[4 * q + 3], lo[4 * q + 3]);
         }
+        const uint32_t ta = tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(L::ACC + 64 * l);
+        tmem_st32(ta, hi);
+        tmem_st32(ta + 32, lo);
+        tmem_st_wait();
       }
-#pragma unroll
-      for (int i = tid; i < ((a.dbg & 1) ? 0 : L::ZB / 16); i += 128) {
-        const float4 v = src[i];
-        float4 o;
-        float h;
-        tf32_split(v.x, h, o.x); tf32_split(v.y, h, o.y); tf32_split(v.z, h, o.z); tf32_split(v.w, h, o.w);
-        dst[i] = o;
-      }
-      fence_proxy_async();                         // generic-proxy writes -> tensor core reads
+      tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&lofull[l]);
+      if (a.tstamp) t_conv += clock64() - tc0;
       if (++r == kTcNR) { r = 0; phr ^= 1; }
       if (++l == kTcNL) { l = 0; phl ^= 1; }
       if (c == nch - 1) {
-        // ---- epilogue of tile tl: row 16 warp + lane (lanes < 16) of the M = 64 tile
+        // ---- epilogue of tile tl: row kTcRPW warp + lane of the tile
         const int64_t r0 = (blockIdx.x + tl * gridDim.x) * kTcBM;
         if (tid == 0) stamp(3);
-        mbar_wait(&accfull, (uint32_t)(tl & 1));
+        twait(&accfull, (uint32_t)(tl & 1), w_acc);
         if (tid == 0) stamp(4);
         tc_fence_after();
-        const int64_t row = r0 + 16 * warp + lane;
-        const bool live = lane < 16 && row < a.m && !(a.dbg & 8);
+        const int64_t row = r0 + kTcRPW * warp + lane;
+        const bool live = lane < kTcRPW && row < a.m && !(a.dbg & 8);
 #pragma unroll 1
         for (int c0 = 0; c0 < RP && c0 < a.kp; c0 += 32) {
           // operands first (kp and lda are multiples of 4: 16-byte vectors), then the TMEM tile
@@ -184,7 +214,13 @@ __global__ void __launch_bounds__(kTcThreads, 3) row_pass_tc_kernel(const __grid
               if (q < nv) { xo[q] = __ldg(xp + q); ar[q] = __ldg(ap + q); }
           }
           float v[32];
-          tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)c0, v);
+          {
+            float vl[32];
+            tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)c0, v);
+            tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(RP + c0), vl);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += vl[j];
+          }
           if (live) {
             float4* xn = reinterpret_cast<float4*>(a.Xnew + row * a.kp + c0);
             float4* dn = reinterpret_cast<float4*>(a.Dnew + row * a.kp + c0);
@@ -217,6 +253,12 @@ __global__ void __launch_bounds__(kTcThreads, 3) row_pass_tc_kernel(const __grid
         if (tid == 0) stamp(5);
       }
       if (++c == nch) { c = 0; ++tl; }
+    }
+    if (a.tstamp && tid == 0) {
+      a.tstamp[(int64_t)gridDim.x * 8 + blockIdx.x * 8 + 3] = w_full;
+      a.tstamp[(int64_t)gridDim.x * 8 + blockIdx.x * 8 + 4] = w_lofree;
+      a.tstamp[(int64_t)gridDim.x * 8 + blockIdx.x * 8 + 5] = w_acc;
+      a.tstamp[(int64_t)gridDim.x * 8 + blockIdx.x * 8 + 6] = t_conv;
     }
     fw = warp_sum(fw);
     if (lane == 0) wsum[warp] = fw;
@@ -270,7 +312,7 @@ int row_pass_tc_ctas_per_sm(int rp) {
     case 64: bytes = TcLayout<64>::TOTAL; break;
     default: bytes = TcLayout<128>::TOTAL; break;
   }
-  return std::max(1, std::min(3, (228 * 1024) / (bytes + 1024 + 1024)));   // + align pad + reserve
+  return std::max(1, std::min(2, (227 * 1024) / (bytes + 1024 + 1024)));   // + align pad + reserve
 }
 
 cudaError_t launch_row_pass_tc(const RowPassTcArgs& a, int rp, int grid, cudaStream_t st, int* occ) {

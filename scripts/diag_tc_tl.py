@@ -13,9 +13,16 @@ w.wlr_iterate(h, 5)
 flush.fill_(1.0)
 w.wlr_iterate_async(h, 1)
 torch.cuda.synchronize()
-t = w.wlr_debug_state(h, "tctime").view(np.uint64).astype(np.int64).reshape(-1, 8)
+tt = w.wlr_debug_state(h, "tctime").view(np.uint64).astype(np.int64)
+t = tt[: tt.size // 2].reshape(-1, 8)
+wc = tt[tt.size // 2:].reshape(-1, 8)
 t0 = t[:, 0].min()
 names = ["start", "first_full", "first_tma", "epi_wait", "accfull", "epi_done", "end"]
 for i, nm in enumerate(names):
     v = (t[:, i] - t0) / 1e3
     print(f"{nm:11s} min {v.min():7.2f} med {np.median(v):7.2f} max {v.max():7.2f} us")
+wnames = ["prod wait rawfree", "mma wait lofull", "mma wait accfree", "conv wait full", "conv wait lofree",
+          "epi wait accfull", "conv busy"]
+for i, nm in enumerate(wnames):
+    v = wc[:, i] / 1.965e3
+    print(f"{nm:18s} min {v.min():7.2f} med {np.median(v):7.2f} max {v.max():7.2f} us (cycles / 1965)")
