@@ -102,6 +102,11 @@ struct wlr_ctx {
   void *Wt = nullptr, *CVop = nullptr, *Kop = nullptr;
   double *inc_part = nullptr, *inc_part2 = nullptr, *fw_part = nullptr, *fw0 = nullptr;
   int ics = 1, ncl = 0;        // increment row splits per cluster, cluster partials
+  // tensor-core increments (fp32, kp <= 32): own column layout (A part padded to 32)
+  bool itc_ok = false, itc_on = false;
+  int itc_nsplit = 0, itc_nA32 = 0, itc_nz = 0;
+  int64_t itc_rps = 0;
+  CUtensorMap tmA32{}, tmX32[2]{}, tmD32{};
   double* inc[2] = {nullptr, nullptr};   // packed increments, by iteration parity
   double* GA = nullptr;
   double a2sq = 0.0;
@@ -316,7 +321,18 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int ph) {
     a.part = h->inc_part; a.part2 = h->inc_part2; a.cs = h->ics; a.m = h->m; a.rows_per_split = h->rps;
     a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.k0 = (int)h->k0; a.nz = h->nz; a.nsplit = h->nsplit;
     a.vec_ok = (h->lda % 4 == 0) && ((uintptr_t)h->A % 16 == 0) && (h->n % 4 == 0);
+    // both increment kernels are enqueued; the small step's gate (flags[5]) decides on the
+    // device which one works: tensor cores once the X1 step is small
+    a.gate = h->itc_on ? h->flags + 5 : nullptr;
     e = launch_incr<float>(a, h->bm, h->st);
+    if (e == cudaSuccess && h->itc_on) {
+      IncrTcArgs q{};
+      q.tmA = h->tmA32; q.tmX = h->tmX32[cur]; q.tmD = h->tmD32;
+      q.part = h->inc_part; q.m = h->m; q.rows_per_split = h->itc_rps;
+      q.k = (int)h->k; q.k0 = (int)h->k0; q.nA32 = h->itc_nA32; q.nz = h->itc_nz;
+      q.gate = h->flags + 5;
+      e = launch_incr_tc(q, h->itc_nsplit, h->st);
+    }
   } else {
     IncrArgs<double> a{};
     a.A = (const double*)h->A; a.lda = h->lda;
@@ -328,10 +344,11 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int ph) {
   }
   if (e != cudaSuccess) return fail(h, WLR_ECUDA, std::string("increments: ") + cudaGetErrorString(e));
   if (prof) cudaEventRecord(ev[2], h->st);
-  launch_reduce_incr(h->ics > 1 ? h->inc_part2 : h->inc_part, h->ics > 1 ? h->ncl : h->nsplit, (int)h->k, (int)h->nk, h->nz, (int)(h->k - h->k0),
-                     (int)(h->n - h->k0), (int)h->kp, h->fw_part,
-                     h->tc_on ? h->tc_grid : h->rp_grid,
-                     h->inc[cur], h->st);
+  launch_reduce_incr(h->ics > 1 ? h->inc_part2 : h->inc_part, h->ics > 1 ? h->ncl : h->nsplit, (int)h->k,
+                     (int)h->nk, h->nz, (int)(h->k - h->k0), (int)(h->n - h->k0), (int)h->kp, h->fw_part,
+                     h->tc_on ? h->tc_grid : h->rp_grid, h->inc[cur], h->st,
+                     h->itc_on ? h->flags + 5 : nullptr,   // tensor-core layout: A part padded to nA32
+                     ReduceLayout{h->inc_part, h->itc_nsplit, h->itc_nz, h->itc_nA32, 32});
   if (prof) cudaEventRecord(ev[3], h->st);
   if (h->comm) {
     const size_t cnt = (size_t)(h->k * h->nk + 2 * h->k * h->k + 1);
@@ -531,6 +548,16 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   // clusters of 8 row splits pre-reduce their partials through DSMEM (8x fewer for K2c)
   h->ics = h->nsplit >= 8 && incr_cluster_ok() ? 8 : 1;
   h->ncl = (int)ceil_div(h->nsplit, h->ics);
+  // tensor-core increments: 128-column blocks x row splits, one wave at 2 CTAs/SM
+  h->itc_ok = h->dtype == WLR_F32 && kp <= 32;
+  if (h->itc_ok) {
+    h->itc_nA32 = (int)round_up(n - h->k0, 32);
+    h->itc_nz = h->itc_nA32 + 64;
+    const int64_t ncb = ceil_div(h->itc_nz, 128);
+    const int64_t want = std::max<int64_t>(1, (2 * h->nsm) / ncb);
+    h->itc_rps = round_up(ceil_div(h->m, want), 32);
+    h->itc_nsplit = (int)ceil_div(h->m, h->itc_rps);
+  }
   // eigen block width b
   // warm block: 2 spare Ritz vectors for r-k <= 4 (one product per iteration at steady state,
   // profiles/r01_v7_eigblock.log), 6 otherwise (narrow gaps at configs 4-5)
@@ -588,9 +615,17 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
       h->tc_ok = false;
     }
   }
+  if (h->itc_ok) {   // 32 x 32 boxes of A, X1 (per buffer) and Delta for the tensor-core increments
+    bool ok = make_tmap_2d(&h->tmA32, h->A, 4, (uint64_t)n, (uint64_t)h->m, (uint64_t)h->lda * 4, 32u, 32u, true);
+    for (int i = 0; i < 2; ++i)
+      ok = ok && make_tmap_2d(&h->tmX32[i], h->X[i], 4, (uint64_t)kp, (uint64_t)h->m, (uint64_t)kp * 4, 32u, 32u, true);
+    ok = ok && make_tmap_2d(&h->tmD32, h->Dl, 4, (uint64_t)kp, (uint64_t)h->m, (uint64_t)kp * 4, 32u, 32u, true);
+    h->itc_ok = h->itc_on = ok;
+  }
   if ((s = dalloc(h, &h->CVop, (size_t)std::max<int64_t>(k * t, 1) * es)) != WLR_OK) return s;
   if ((s = dalloc(h, &h->Kop, (size_t)k * k * es)) != WLR_OK) return s;
-  if ((s = dalloc_t(h, &h->inc_part, (size_t)h->nsplit * k * h->nz)) != WLR_OK) return s;
+  if ((s = dalloc_t(h, &h->inc_part, std::max((size_t)h->nsplit * k * h->nz,
+                                                (size_t)h->itc_nsplit * k * h->itc_nz))) != WLR_OK) return s;
   if ((s = dalloc_t(h, &h->inc_part2, (size_t)h->ncl * k * h->nz)) != WLR_OK) return s;
   if ((s = dalloc_t(h, &h->fw_part, (size_t)std::max(h->rp_grid, 1184))) != WLR_OK) return s;
   for (int i = 0; i < 2; ++i)
@@ -992,6 +1027,14 @@ extern "C" wlr_status wlr_debug_state(wlr_handle h, const char* name, double* ou
       for (auto& g : gp)
         if (g) { cudaGraphExecDestroy(g); g = nullptr; }
     if (count) *count = 0;
+    return WLR_OK;
+  }
+  else if (nm == "incrtc_on" || nm == "incrtc_off") {   // tensor-core / CUDA-core increments (A/B)
+    h->itc_on = h->itc_ok && nm == "incrtc_on";
+    for (auto& gp : h->gexec)
+      for (auto& g : gp)
+        if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+    if (count) *count = h->itc_on ? 1 : 0;
     return WLR_OK;
   }
   else if (nm == "rowtc_on" || nm == "rowtc_off") {   // tensor-core / CUDA-core row pass (A/B)

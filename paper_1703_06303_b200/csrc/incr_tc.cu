@@ -1,0 +1,180 @@
+// incr_tc.cu -- K2b on the 5th-generation tensor cores (fp32 data, kp <= 32).
+//
+// The Gram increments are one contraction over the pixel rows:
+//     [N | Gamma | Omega](l, j) = sum_i Delta(i, l) Z(i, j),   Z = [A(:, k0:n) | X1_p | Delta]
+// computed here as D = Z^T Delta on tcgen05 with 3xTF32, one CTA per (128-column block of Z,
+// row split):
+//   warp 4 (lane 0): TMA per 32-row chunk: 4 boxes of Z (32 columns each, SWIZZLE_128B) + Delta
+//   warps 0-3: thread c owns Z column c of the block: it reads its column of the chunk (32 rows,
+//     conflict-free across the warp), splits it into tf32 hi / lo and stores both into TMEM
+//     (tcgen05.st; the A operand, M = 128 columns x K = 32 rows, K-major); the four warps also
+//     write Delta^T hi / lo (K-major, SWIZZLE_128B) into shared memory (the B operand)
+//   warp 5 (lane 0): per 8-row k-step, Z_hi x [Delta_hi; Delta_lo] (N = 64) and
+//     Z_lo x Delta_hi (N = 32) into the TMEM accumulator
+// Epilogue: thread c reads its accumulator lane and writes the fp64 partial of column c for all
+// l < k.  The column layout pads the A part to a multiple of 32 (nA32) so that no 32-column TMA
+// box straddles two sources; the reduce kernel reads that layout (nz' = nA32 + 64, kp' = 32).
+#include "kernels.h"
+#include "umma.cuh"
+
+namespace wlr {
+
+constexpr int kItThreads = 192;
+constexpr int kItNR = 3, kItNL = 3;
+constexpr int kItZB = 4 * 32 * 128;     // Z chunk: 4 boxes of 32 rows x 128 B (16 KB)
+constexpr int kItDB = 32 * 128;         // Delta chunk: 32 rows x 32 fp32 (4 KB)
+constexpr int kItST = kItZB + kItDB;    // raw stage
+constexpr int kItBT = 2 * 32 * 128;     // B operand slot: Delta^T hi | lo (64 rows x 128 B)
+constexpr int kItSmem = kItNR * kItST + kItNL * kItBT;
+
+__global__ void __launch_bounds__(kItThreads, 2) incr_tc_kernel(const __grid_constant__ IncrTcArgs a) {
+  if (!*a.gate) return;                           // large step: the CUDA-core FP32 kernel runs
+  extern __shared__ __align__(1024) unsigned char it_raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(it_raw) + 1023) & ~(uintptr_t)1023);
+  unsigned char* rawst = sm;                               // [NR][Z boxes | Delta]
+  unsigned char* bst = sm + kItNR * kItST;                 // [NL][Delta^T hi | Delta^T lo]
+  __shared__ __align__(8) uint64_t full[kItNR], rawfree[kItNR], lofull[kItNL], lofree[kItNL], accfull;
+  __shared__ uint32_t tslot;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int ACC = 64;                                  // accumulator columns
+  if (warp == 0) tmem_alloc<256>(&tslot);                  // ACC + NL x 64 (Z_hi | Z_lo) <= 256
+  if (tid == 32) {
+    for (int s = 0; s < kItNR; ++s) { mbar_init(&full[s], 1); mbar_init(&rawfree[s], 1); }
+    for (int s = 0; s < kItNL; ++s) { mbar_init(&lofull[s], 4); mbar_init(&lofree[s], 1); }
+    mbar_init(&accfull, 1);
+    mbar_init_fence();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  const int j0 = blockIdx.x * 128;                         // first Z column of this block
+  const int64_t r0 = (int64_t)blockIdx.y * a.rows_per_split;
+  const int64_t r1 = r0 + a.rows_per_split < a.m ? r0 + a.rows_per_split : a.m;
+  const int nch = r1 > r0 ? (int)ceil_div(r1 - r0, (int64_t)32) : 0;
+
+  if (warp == 4) {
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int ch = 0; ch < nch; ++ch) {
+        if (ch >= kItNR) mbar_wait(&rawfree[s], ph ^ 1);
+        unsigned char* st = rawst + s * kItST;
+        const int row = (int)(r0 + 32 * ch);
+        mbar_expect_tx(&full[s], (uint32_t)kItST);
+        for (int b = 0; b < 4; ++b) {                      // Z column boxes
+          const int zc = j0 + 32 * b;
+          if (zc < a.nA32) tma_load_2d(st + b * 4096, &a.tmA, &full[s], a.k0 + zc, row);
+          else if (zc < a.nA32 + 32) tma_load_2d(st + b * 4096, &a.tmX, &full[s], 0, row);
+          else if (zc < a.nA32 + 64) tma_load_2d(st + b * 4096, &a.tmD, &full[s], 0, row);
+          else tma_load_2d(st + b * 4096, &a.tmD, &full[s], 0, row);   // beyond nz': ignored lanes
+        }
+        tma_load_2d(st + kItZB, &a.tmD, &full[s], 0, row);
+        if (++s == kItNR) { s = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0) {
+      const uint32_t id2 = umma_idesc_tf32<128, 64>(), id1 = umma_idesc_tf32<128, 32>();
+      int r = 0, l = 0;
+      uint32_t phl = 0;
+      for (int ch = 0; ch < nch; ++ch) {
+        mbar_wait(&lofull[l], phl);
+        tc_fence_after();
+        const uint32_t ta = tmem + (uint32_t)(ACC + 64 * l);
+        const uint32_t bs = smem_u32(bst + l * kItBT);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const uint64_t db = umma_desc_k_sw128(bs + kk * 32);   // [Delta_hi^T; Delta_lo^T], N = 64
+          umma_tf32_ts(tmem, ta + 8 * kk, db, id2, ch > 0 || kk > 0);
+          umma_tf32_ts(tmem, ta + 32 + 8 * kk, db, id1, true);
+        }
+        umma_commit(&rawfree[r]);
+        umma_commit(&lofree[l]);
+        if (ch == nch - 1) umma_commit(&accfull);
+        if (++r == kItNR) r = 0;
+        if (++l == kItNL) { l = 0; phl ^= 1; }
+      }
+    }
+  } else {
+    // ---------------- warps 0-3: Z column c = 32 warp + lane -> TMEM; Delta^T -> smem
+    const int c = 32 * warp + lane;
+    int r = 0, l = 0;
+    uint32_t phr = 0, phl = 0;
+    for (int ch = 0; ch < nch; ++ch) {
+      mbar_wait(&full[r], phr);
+      if (ch >= kItNL) mbar_wait(&lofree[l], phl ^ 1);
+      const unsigned char* st = rawst + r * kItST;
+      {   // column c: box warp, 16-byte unit (lane / 4) ^ (row & 7), word lane % 4
+        const float* box = reinterpret_cast<const float*>(st + warp * 4096);
+        float hi[32], lo[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float v = box[i * 32 + ((((lane >> 2) ^ (i & 7)) << 2) | (lane & 3))];
+          tf32_split(v, hi[i], lo[i]);
+        }
+        const uint32_t ta = tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(ACC + 64 * l);
+        tmem_st32(ta, hi);
+        tmem_st32(ta + 32, lo);
+        tmem_st_wait();
+      }
+      {   // Delta^T hi (rows 0-31) | lo (rows 32-63) of the B slot: element (n, k) = Delta(k, n)
+        const float* dl = reinterpret_cast<const float*>(st + kItZB);
+        float* bt = reinterpret_cast<float*>(bst + l * kItBT);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int e = tid + 128 * q;                    // 1024 elements
+          const int k = e >> 5, n = e & 31;               // read row k of Delta (coalesced)
+          const float v = dl[k * 32 + ((((n >> 2) ^ (k & 7)) << 2) | (n & 3))];
+          float h, lo;
+          tf32_split(v, h, lo);
+          const int off = n * 32 + ((((k >> 2) ^ (n & 7)) << 2) | (k & 3));
+          bt[off] = h;
+          bt[32 * 32 + off] = lo;                         // rows 32.. : (n + 32) & 7 == n & 7
+        }
+      }
+      fence_proxy_async();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&lofull[l]);
+      if (++r == kItNR) { r = 0; phr ^= 1; }
+      if (++l == kItNL) { l = 0; phl ^= 1; }
+    }
+    // ---------------- epilogue: Z column c, Delta columns l < k
+    double* out = a.part + (int64_t)blockIdx.y * a.k * a.nz;
+    const int zc = j0 + c;
+    if (nch > 0) {
+      mbar_wait(&accfull, 0);
+      tc_fence_after();
+      float v[32], v2[32];
+      tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16), v);
+      tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + 32, v2);
+      if (zc < a.nz)
+        for (int q = 0; q < a.k; ++q) out[(int64_t)q * a.nz + zc] = (double)v[q] + (double)v2[q];
+    } else if (zc < a.nz) {
+      for (int q = 0; q < a.k; ++q) out[(int64_t)q * a.nz + zc] = 0.0;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<256>(tmem);
+  }
+}
+
+cudaError_t launch_incr_tc(const IncrTcArgs& a, int nsplit, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(incr_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kItSmem + 1024);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(incr_tc_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  dim3 grid((unsigned)ceil_div(a.nz, 128), (unsigned)nsplit);
+  incr_tc_kernel<<<grid, kItThreads, kItSmem + 1024, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace wlr

@@ -89,13 +89,27 @@ struct IncrArgs {
   int n, k, kp, k0, nz, nsplit;
   int cs;                           // row splits per thread-block cluster (DSMEM pre-reduction)
   int vec_ok;
+  const int* gate;                  // non-null and *gate != 0: the tensor-core kernel runs instead
 };
+// tensor-core increments (incr_tc.cu): fp32, kp <= 32; partial layout nz' = nA32 + 64 columns
+struct IncrTcArgs {
+  CUtensorMap tmA, tmX, tmD;        // boxes 32 columns x 32 rows (SWIZZLE_128B): A, X1_p, Delta
+  double* part;                     // nsplit x k x nz'
+  int64_t m, rows_per_split;
+  int k, k0, nA32, nz;              // nz = nA32 + 64
+  const int* gate;                  // runs only when *gate != 0 (set by the small step)
+};
+cudaError_t launch_incr_tc(const IncrTcArgs& a, int nsplit, cudaStream_t st);
 int incr_bm(int kp);
 inline bool incr_cluster_ok() { return true; }   // 8-CTA clusters of 128-512 threads (portable)
 int incr_bn(int bm, int elem_bytes);   // columns per CTA
 template <typename T> cudaError_t launch_incr(const IncrArgs<T>& a, int bm, cudaStream_t st);
+// Partial layouts: (part, nsplit, nz, nA, kp), or -- when gate && *gate -- the tensor-core layout
+// (part_t, nsplit_t, nz_t, nA_t, kp_t).
+struct ReduceLayout { const double* part; int nsplit, nz, nA, kp; };
 void launch_reduce_incr(const double* part, int nsplit, int k, int nk, int nz, int kshift, int nA,
-                        int kp, const double* fw_part, int nfw, double* inc, cudaStream_t st);
+                        int kp, const double* fw_part, int nfw, double* inc, cudaStream_t st,
+                        const int* gate = nullptr, ReduceLayout alt = {nullptr, 0, 0, 0, 0});
 
 // ---------------------------------------------------------------- small step (small_step.cu)
 // Shared-memory plan of the K3 cluster kernel (offsets in doubles; identical in every CTA

@@ -505,6 +505,7 @@ size_t incr_smem_bytes() {   // stages; after the mainloop the fp64 BM x BN tile
 
 template <typename T, int BM, int BN>
 __global__ void __launch_bounds__(BM * 4, BM == 32 ? 5 : 1) incr_kernel(IncrArgs<T> a) {
+  if (a.gate && *a.gate) return;                // the tensor-core kernel computes this iteration
   constexpr int NT = BM * 4;                    // threads: BM/8 warps
   constexpr int TW = BN / 32;                   // columns per lane
   constexpr int VE = 16 / (int)sizeof(T);
@@ -697,7 +698,10 @@ template cudaError_t launch_incr<double>(const IncrArgs<double>&, int, cudaStrea
 __global__ void reduce_incr_kernel(const double* __restrict__ part, int nsplit, int k, int nk,
                                    int nz, int kshift, int nA, int kp,
                                    const double* __restrict__ fw_part, int nfw,
-                                   double* __restrict__ inc) {
+                                   double* __restrict__ inc, const int* gate, ReduceLayout alt) {
+  if (gate && *gate) {   // tensor-core partial layout this iteration
+    part = alt.part; nsplit = alt.nsplit; nz = alt.nz; nA = alt.nA; kp = alt.kp;
+  }
   // 8 lanes per output: lane g sums the splits p = g (mod 8) in order, then a fixed
   // shuffle tree combines the 8 sums (deterministic)
   const int64_t nN = (int64_t)k * nk, nG = (int64_t)k * k;
@@ -736,10 +740,12 @@ __global__ void reduce_incr_kernel(const double* __restrict__ part, int nsplit, 
 }
 
 void launch_reduce_incr(const double* part, int nsplit, int k, int nk, int nz, int kshift, int nA,
-                        int kp, const double* fw_part, int nfw, double* inc, cudaStream_t st) {
+                        int kp, const double* fw_part, int nfw, double* inc, cudaStream_t st,
+                        const int* gate, ReduceLayout alt) {
   const int64_t tot = (int64_t)k * nk + 2LL * k * k;
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(tot, 32), 4096));
-  reduce_incr_kernel<<<blocks, 256, 0, st>>>(part, nsplit, k, nk, nz, kshift, nA, kp, fw_part, nfw, inc);
+  reduce_incr_kernel<<<blocks, 256, 0, st>>>(part, nsplit, k, nk, nz, kshift, nA, kp, fw_part, nfw, inc,
+                                             gate, alt);
 }
 
 }  // namespace wlr

@@ -664,6 +664,11 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
       if (a.mode) {
         g = a.G_in[idx] + incGam[i * k + j] + incGam[j * k + i] + 0.5 * (incOm[i * k + j] + incOm[j * k + i]);
         if (s.c == 0) a.G_out[idx] = g;
+        if (s.c == 0 && idx == 0) {   // gate of the next increments: tensor cores when ||dX1|| <= 1e-3 ||X1||
+          double tom = 0.0, tg = 0.0;
+          for (int q = 0; q < k; ++q) { tom += incOm[q * k + q]; tg += a.G_in[q * k + q] + 2.0 * incGam[q * k + q] + incOm[q * k + q]; }
+          a.flags[5] = tom <= 1e-6 * tg ? 1 : 0;
+        }
       } else {
         g = a.G_out[idx];
       }
