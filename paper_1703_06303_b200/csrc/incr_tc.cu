@@ -17,6 +17,9 @@
 #include "kernels.h"
 #include "umma.cuh"
 
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
+
 namespace wlr {
 
 constexpr int kItThreads = 192;
@@ -140,23 +143,46 @@ __global__ void __launch_bounds__(kItThreads, 2) incr_tc_kernel(const __grid_con
       if (++r == kItNR) { r = 0; phr ^= 1; }
       if (++l == kItNL) { l = 0; phl ^= 1; }
     }
-    // ---------------- epilogue: Z column c, Delta columns l < k
-    double* out = a.part + (int64_t)blockIdx.y * a.k * a.nz;
-    const int zc = j0 + c;
+  }
+  // ---------------- epilogue: Z column c = tid (< 128), Delta columns l < 32, into an fp64 tile
+  // [32][128] (the stages are free); the cs row splits of a cluster sum their tiles in rank order
+  double* tile = reinterpret_cast<double*>(sm);
+  if (warp < 4) {
+    const int c = tid;
+    float v[32], v2[32];
     if (nch > 0) {
       mbar_wait(&accfull, 0);
       tc_fence_after();
-      float v[32], v2[32];
       tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16), v);
       tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + 32, v2);
-      if (zc < a.nz)
-        for (int q = 0; q < a.k; ++q) out[(int64_t)q * a.nz + zc] = (double)v[q] + (double)v2[q];
-    } else if (zc < a.nz) {
-      for (int q = 0; q < a.k; ++q) out[(int64_t)q * a.nz + zc] = 0.0;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 32; ++q) { v[q] = 0.f; v2[q] = 0.f; }
     }
+#pragma unroll
+    for (int q = 0; q < 32; ++q) tile[q * 128 + c] = (double)v[q] + (double)v2[q];
   }
   tc_fence_before();
   __syncthreads();
+  if (a.cs <= 1) {
+    double* out = a.part + (int64_t)blockIdx.y * a.k * a.nz;
+    for (int idx = tid; idx < a.k * 128; idx += kItThreads) {
+      const int q = idx >> 7, c = idx & 127;
+      if (j0 + c < a.nz) out[(int64_t)q * a.nz + j0 + c] = tile[q * 128 + c];
+    }
+  } else {
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    const int rk = (int)cl.block_rank(), rows = 32 / a.cs;        // Delta columns per rank
+    double* out = a.part + (int64_t)(blockIdx.y / a.cs) * a.k * a.nz;
+    for (int idx = tid; idx < rows * 128; idx += kItThreads) {
+      const int q = rk * rows + (idx >> 7), c = idx & 127;
+      double s = 0.0;
+      for (int r = 0; r < a.cs; ++r) s += cl.map_shared_rank(tile, r)[q * 128 + c];
+      if (q < a.k && j0 + c < a.nz) out[(int64_t)q * a.nz + j0 + c] = s;
+    }
+    cl.sync();
+  }
   if (warp == 0) {
     tc_fence_after();
     tmem_dealloc<256>(tmem);
@@ -172,9 +198,18 @@ cudaError_t launch_incr_tc(const IncrTcArgs& a, int nsplit, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  dim3 grid((unsigned)ceil_div(a.nz, 128), (unsigned)nsplit);
-  incr_tc_kernel<<<grid, kItThreads, kItSmem + 1024, st>>>(a);
-  return cudaGetLastError();
+  const int cs = a.cs > 1 ? a.cs : 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)ceil_div(a.nz, 128), (unsigned)(ceil_div(nsplit, cs) * cs));
+  cfg.blockDim = dim3(kItThreads);
+  cfg.dynamicSmemBytes = kItSmem + 1024;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 1; at[0].val.clusterDim.y = cs; at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = cs > 1 ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, incr_tc_kernel, a);
 }
 
 }  // namespace wlr

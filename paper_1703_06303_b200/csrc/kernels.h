@@ -94,8 +94,9 @@ struct IncrArgs {
 // tensor-core increments (incr_tc.cu): fp32, kp <= 32; partial layout nz' = nA32 + 64 columns
 struct IncrTcArgs {
   CUtensorMap tmA, tmX, tmD;        // boxes 32 columns x 32 rows (SWIZZLE_128B): A, X1_p, Delta
-  double* part;                     // nsplit x k x nz'
+  double* part;                     // nsplit x k x nz' (cs == 1) or (nsplit / cs) x k x nz' (clusters)
   int64_t m, rows_per_split;
+  int cs;                           // row splits per thread-block cluster (DSMEM pre-reduction)
   int k, k0, nA32, nz;              // nz = nA32 + 64
   const int* gate;                  // runs only when *gate != 0 (set by the small step)
 };
