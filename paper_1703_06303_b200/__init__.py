@@ -180,6 +180,16 @@ def wlr_row_path(h: Handle, tensor_cores: bool) -> bool:
     return bool(cnt.value)
 
 
+def wlr_incr_path(h: Handle, tensor_cores: bool) -> bool:
+    """Select the Gram-increment implementation for fp32 problems with k <= 32: the tcgen05
+    3xTF32 kernel (default; used on the device only while the X1 step is small, R20)
+    or always the CUDA-core FP32 kernel.  Returns whether the tensor-core kernel is enabled."""
+    cnt = ctypes.c_int64()
+    name = b"incrtc_on" if tensor_cores else b"incrtc_off"
+    check(lib.wlr_debug_state(h.raw, name, None, 0, ctypes.byref(cnt)), h.raw)
+    return bool(cnt.value)
+
+
 def wlr_debug_state(h: Handle, name: str) -> np.ndarray:
     cnt = ctypes.c_int64()
     check(lib.wlr_debug_state(h.raw, name.encode(), None, 0, ctypes.byref(cnt)), h.raw)

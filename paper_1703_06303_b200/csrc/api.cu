@@ -380,7 +380,7 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int ph) {
   }
   h->pend = s;
   h->pending = true;
-  h->pr.launches += pend ? 5 : 4;
+  h->pr.launches += (pend ? 5 : 4) + (h->itc_on ? 1 : 0);   // + the gated tensor-core increments
   return WLR_OK;
 }
 
@@ -415,7 +415,7 @@ static wlr_status launch_iteration(wlr_ctx* h) {
     CUDA_TRY(h, cudaGraphLaunch(h->gexec[h->ph][pend], h->st));
     h->pend = small_args(h, h->ph, 1);
     h->pending = true;
-    h->pr.launches += pend ? 5 : 4;
+    h->pr.launches += (pend ? 5 : 4) + (h->itc_on ? 1 : 0);
   } else {
     s = enqueue_iteration(h, h->ph);
     if (s != WLR_OK) return s;

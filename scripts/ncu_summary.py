@@ -18,12 +18,24 @@ def val(d, name):
     return v * UNIT.get(units[i], 1.0)
 
 
-fam = {"row_pass_tc_kernel": "row_pass", "row_pass_kernel": "row_pass", "incr_kernel": "increments",
-       "reduce_incr_kernel": "reduce", "small_step_kernel<8, 1>": "small_step", "small_step_kernel<8, 2>": "deferred_small_step"}
+def family(name):
+    if "reduce_incr_kernel" in name:
+        return "reduce"
+    if "incr_tc_kernel" in name:
+        return "increments"
+    if "incr_kernel" in name:
+        return "increments_cuda_core"
+    if "row_pass_tc_kernel" in name or "row_pass_kernel" in name:
+        return "row_pass"
+    if "small_step_kernel" in name:
+        return "small_step" if ", 1>" in name else "deferred_small_step"
+    return None
+
+
 out = {}
 for d in rows[2:]:
     name = d[idx["Kernel Name"]]
-    key = next((v for k, v in fam.items() if k in name), None)
+    key = family(name)
     if key is None or key in out:
         continue
     dur = val(d, "gpu__time_duration.sum")
