@@ -104,7 +104,7 @@ struct wlr_ctx {
   int ics = 1, ncl = 0;        // increment row splits per cluster, cluster partials
   // tensor-core increments (fp32, kp <= 32): own column layout (A part padded to 32)
   bool itc_ok = false, itc_on = false;
-  int itc_nsplit = 0, itc_nA32 = 0, itc_nz = 0;
+  int itc_nsplit = 0, itc_nA32 = 0, itc_nz = 0, itc_cs = 1;
   int64_t itc_rps = 0;
   CUtensorMap tmA32{}, tmX32[2]{}, tmD32{};
   double* inc[2] = {nullptr, nullptr};   // packed increments, by iteration parity
@@ -331,7 +331,7 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int ph) {
       q.part = h->inc_part; q.m = h->m; q.rows_per_split = h->itc_rps;
       q.k = (int)h->k; q.k0 = (int)h->k0; q.nA32 = h->itc_nA32; q.nz = h->itc_nz;
       q.gate = h->flags + 5;
-      q.cs = 1;   // (8-CTA clusters measured 1.5x slower here: cluster placement at 2 CTAs/SM)
+      q.cs = h->itc_cs;
       e = launch_incr_tc(q, h->itc_nsplit, h->st);
     }
   } else {
@@ -349,7 +349,7 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int ph) {
                      (int)h->nk, h->nz, (int)(h->k - h->k0), (int)(h->n - h->k0), (int)h->kp, h->fw_part,
                      h->tc_on ? h->tc_grid : h->rp_grid, h->inc[cur], h->st,
                      h->itc_on ? h->flags + 5 : nullptr,   // tensor-core layout: A part padded to nA32
-                     ReduceLayout{h->inc_part, h->itc_nsplit, h->itc_nz, h->itc_nA32, 32});
+                     ReduceLayout{h->inc_part, (int)ceil_div(h->itc_nsplit, h->itc_cs), h->itc_nz, h->itc_nA32, 32});
   if (prof) cudaEventRecord(ev[3], h->st);
   if (h->comm) {
     const size_t cnt = (size_t)(h->k * h->nk + 2 * h->k * h->k + 1);
@@ -558,6 +558,7 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
     const int64_t want = std::max<int64_t>(1, (2 * h->nsm) / ncb);
     h->itc_rps = round_up(ceil_div(h->m, want), 32);
     h->itc_nsplit = (int)ceil_div(h->m, h->itc_rps);
+    // (2/4/8-CTA clusters pre-reducing the partials were measured no faster: profiles/r01_v10_itc_cs.log)
   }
   // eigen block width b
   // warm block: 2 spare Ritz vectors for r-k <= 4 (one product per iteration at steady state,
