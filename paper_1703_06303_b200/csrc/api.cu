@@ -324,6 +324,7 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int ph) {
     // both increment kernels are enqueued; the small step's gate (flags[5]) decides on the
     // device which one works: tensor cores once the X1 step is small
     a.gate = h->itc_on ? h->flags + 5 : nullptr;
+    a.pdl = prof ? 0 : 1;
     e = launch_incr<float>(a, h->bm, h->st);
     if (e == cudaSuccess && h->itc_on) {
       IncrTcArgs q{};
@@ -345,20 +346,9 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int ph) {
   }
   if (e != cudaSuccess) return fail(h, WLR_ECUDA, std::string("increments: ") + cudaGetErrorString(e));
   if (prof) cudaEventRecord(ev[2], h->st);
-  launch_reduce_incr(h->ics > 1 ? h->inc_part2 : h->inc_part, h->ics > 1 ? h->ncl : h->nsplit, (int)h->k,
-                     (int)h->nk, h->nz, (int)(h->k - h->k0), (int)(h->n - h->k0), (int)h->kp, h->fw_part,
-                     h->tc_on ? h->tc_grid : h->rp_grid, h->inc[cur], h->st,
-                     h->itc_on ? h->flags + 5 : nullptr,   // tensor-core layout: A part padded to nA32
-                     ReduceLayout{h->inc_part, (int)ceil_div(h->itc_nsplit, h->itc_cs), h->itc_nz, h->itc_nA32, 32});
-  if (prof) cudaEventRecord(ev[3], h->st);
-  if (h->comm) {
-    const size_t cnt = (size_t)(h->k * h->nk + 2 * h->k * h->k + 1);
-    ncclResult_t nr = g_nccl.allReduce(h->inc[cur], h->inc[cur], cnt, ncclFloat64, ncclSum, h->comm, h->st);
-    if (nr != ncclSuccess) return fail(h, WLR_ENCCL, std::string("ncclAllReduce: ") + g_nccl.errStr(nr));
-  }
-  if (prof) cudaEventRecord(ev[4], h->st);
-  // fork: the deferred half of the previous step runs beside this step's K3a (its own SMs;
-  // it reads state slots and increments that K3a(p) does not write); joined at the end
+  // fork (before the reduce, so that K3a can be the reduce's programmatic dependent): the
+  // deferred half of the previous step runs beside reduce(p) and K3a(p) on its own SMs; it reads
+  // state slots and increments that neither writes (inc[p-1 mod 2]); joined at the end
   if (pend) {
     CUDA_TRY(h, cudaEventRecord(h->ev_fork, h->st));
     CUDA_TRY(h, cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
@@ -368,7 +358,21 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int ph) {
     if (prof) cudaEventRecord(ev[7], h->st2);
     CUDA_TRY(h, cudaEventRecord(h->ev_join, h->st2));
   }
+  launch_reduce_incr(h->ics > 1 ? h->inc_part2 : h->inc_part, h->ics > 1 ? h->ncl : h->nsplit, (int)h->k,
+                     (int)h->nk, h->nz, (int)(h->k - h->k0), (int)(h->n - h->k0), (int)h->kp, h->fw_part,
+                     h->tc_on ? h->tc_grid : h->rp_grid, h->inc[cur], h->st,
+                     h->itc_on ? h->flags + 5 : nullptr,   // tensor-core layout: A part padded to nA32
+                     ReduceLayout{h->inc_part, (int)ceil_div(h->itc_nsplit, h->itc_cs), h->itc_nz, h->itc_nA32, 32},
+                     !prof && !pend);
+  if (prof) cudaEventRecord(ev[3], h->st);
+  if (h->comm) {
+    const size_t cnt = (size_t)(h->k * h->nk + 2 * h->k * h->k + 1);
+    ncclResult_t nr = g_nccl.allReduce(h->inc[cur], h->inc[cur], cnt, ncclFloat64, ncclSum, h->comm, h->st);
+    if (nr != ncclSuccess) return fail(h, WLR_ENCCL, std::string("ncclAllReduce: ") + g_nccl.errStr(nr));
+  }
+  if (prof) cudaEventRecord(ev[4], h->st);
   SmallArgs s = small_args(h, ph, 1);
+  s.pdl = (!h->comm && !prof) ? 1 : 0;   // right behind the reduce kernel (no allreduce between)
   h->last_ss = s;
   e = launch_small_step(s, 1, h->st);
   if (e != cudaSuccess) return fail(h, WLR_ECUDA, std::string("small step: ") + cudaGetErrorString(e));
@@ -1050,6 +1054,7 @@ extern "C" wlr_status wlr_debug_state(wlr_handle h, const char* name, double* ou
   else if (nm == "ss_rerun") {                 // relaunch the last small step twice (timing only;
     SmallArgs s2 = h->last_ss;                  // leaves the state inconsistent)
     s2.tdbg = h->tdbg;
+    s2.pdl = 0;
     for (int rep = 0; rep < 2; ++rep) CUDA_TRY(h, launch_small_step(s2, 1, h->st));
     CUDA_TRY(h, cudaStreamSynchronize(h->st));
     if (count) *count = 0;

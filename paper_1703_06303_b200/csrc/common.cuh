@@ -49,4 +49,10 @@ WLR_DEVI double4 ldg4<double>(const double* p) {
 
 template <typename V> WLR_DEVI auto vx(const V& v) { return v.x; }
 
+// Programmatic dependent launch (the per-iteration kernel chain): a dependent
+// waits for its predecessor grid (completion + memory flush) before touching its outputs; every
+// kernel of the chain waits before it exits, so the ordering stays transitive.
+WLR_DEVI void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+WLR_DEVI void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 }  // namespace wlr

@@ -31,6 +31,8 @@ constexpr int kItBT = 2 * 32 * 128;     // B operand slot: Delta^T hi | lo (64 r
 constexpr int kItSmem = kItNR * kItST + kItNL * kItBT;
 
 __global__ void __launch_bounds__(kItThreads, 2) incr_tc_kernel(const __grid_constant__ IncrTcArgs a) {
+  pdl_wait();                                     // the CUDA-core increments kernel (and the row pass)
+  pdl_trigger();
   if (!*a.gate) return;                           // large step: the CUDA-core FP32 kernel runs
   extern __shared__ __align__(1024) unsigned char it_raw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(it_raw) + 1023) & ~(uintptr_t)1023);
@@ -207,8 +209,13 @@ cudaError_t launch_incr_tc(const IncrTcArgs& a, int nsplit, cudaStream_t st) {
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = 1; at[0].val.clusterDim.y = cs; at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = cs > 1 ? 1 : 0;
+  cudaLaunchAttribute atp[2] = {at[0], {}};
+  int na = cs > 1 ? 1 : 0;
+  atp[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  atp[na].val.programmaticStreamSerializationAllowed = 1;
+  ++na;
+  cfg.attrs = atp;
+  cfg.numAttrs = na;
   return cudaLaunchKernelEx(&cfg, incr_tc_kernel, a);
 }
 

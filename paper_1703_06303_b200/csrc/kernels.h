@@ -90,6 +90,7 @@ struct IncrArgs {
   int cs;                           // row splits per thread-block cluster (DSMEM pre-reduction)
   int vec_ok;
   const int* gate;                  // non-null and *gate != 0: the tensor-core kernel runs instead
+  int pdl;                          // launched as a programmatic dependent of the row pass
 };
 // tensor-core increments (incr_tc.cu): fp32, kp <= 32; partial layout nz' = nA32 + 64 columns
 struct IncrTcArgs {
@@ -110,7 +111,8 @@ template <typename T> cudaError_t launch_incr(const IncrArgs<T>& a, int bm, cuda
 struct ReduceLayout { const double* part; int nsplit, nz, nA, kp; };
 void launch_reduce_incr(const double* part, int nsplit, int k, int nk, int nz, int kshift, int nA,
                         int kp, const double* fw_part, int nfw, double* inc, cudaStream_t st,
-                        const int* gate = nullptr, ReduceLayout alt = {nullptr, 0, 0, 0, 0});
+                        const int* gate = nullptr, ReduceLayout alt = {nullptr, 0, 0, 0, 0},
+                        bool pdl = false);
 
 // ---------------------------------------------------------------- small step (small_step.cu)
 // Shared-memory plan of the K3 cluster kernel (offsets in doubles; identical in every CTA
@@ -131,6 +133,7 @@ struct SSPlan {
 
 struct SmallArgs {
   int k, nk, t, b, kp, k0, rp;      // dims; b = eigen block width (t <= b <= 32)
+  int pdl;                          // host only: launch as a programmatic dependent (part 1)
   int KA;                           // row offset of the X1_p block of the row-pass Wt
   void* WtT; int KW;                // fp32 W'^T (RP x KW, K-major) for the tensor-core row pass
   int mode;                         // 0: init (G, M given), 1: iteration (apply increments)

@@ -144,6 +144,7 @@ int row_pass_nwc(bool uniform, int k, int kp) {
 template <typename T, int RP, int TR, bool UNIFORM, int MODE>
 __global__ void __launch_bounds__(kRowThreads, RP <= 32 ? 3 : 1)
 row_pass_kernel(const __grid_constant__ RowPassArgs<T> a) {
+  pdl_trigger();                               // the increments may be scheduled (they wait)
   using S = RowPassShape<RP>;
   using L = RowPassLayout<T, RP, TR>;
   constexpr int BM = L::BM, TC = S::TC, KG = kRowKG, PE = L::PE, NST = L::NST;
@@ -505,6 +506,8 @@ size_t incr_smem_bytes() {   // stages; after the mainloop the fp64 BM x BN tile
 
 template <typename T, int BM, int BN>
 __global__ void __launch_bounds__(BM * 4, BM == 32 ? 5 : 1) incr_kernel(IncrArgs<T> a) {
+  pdl_wait();                                   // Delta / X1_{p+1} of the row pass
+  pdl_trigger();
   if (a.gate && *a.gate) return;                // the tensor-core kernel computes this iteration
   constexpr int NT = BM * 4;                    // threads: BM/8 warps
   constexpr int TW = BN / 32;                   // columns per lane
@@ -674,8 +677,15 @@ static cudaError_t launch_incr_bm(const IncrArgs<T>& a, cudaStream_t st) {
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = 1; at[0].val.clusterDim.y = cs; at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = cs > 1 ? 1 : 0;
+  cudaLaunchAttribute atp[2] = {at[0], {}};
+  int na = cs > 1 ? 1 : 0;
+  if (a.pdl) {
+    atp[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    atp[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = atp;
+  cfg.numAttrs = na;
   return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
@@ -699,6 +709,8 @@ __global__ void reduce_incr_kernel(const double* __restrict__ part, int nsplit, 
                                    int nz, int kshift, int nA, int kp,
                                    const double* __restrict__ fw_part, int nfw,
                                    double* __restrict__ inc, const int* gate, ReduceLayout alt) {
+  pdl_wait();
+  pdl_trigger();
   if (gate && *gate) {   // tensor-core partial layout this iteration
     part = alt.part; nsplit = alt.nsplit; nz = alt.nz; nA = alt.nA; kp = alt.kp;
   }
@@ -741,11 +753,20 @@ __global__ void reduce_incr_kernel(const double* __restrict__ part, int nsplit, 
 
 void launch_reduce_incr(const double* part, int nsplit, int k, int nk, int nz, int kshift, int nA,
                         int kp, const double* fw_part, int nfw, double* inc, cudaStream_t st,
-                        const int* gate, ReduceLayout alt) {
+                        const int* gate, ReduceLayout alt, bool pdl) {
   const int64_t tot = (int64_t)k * nk + 2LL * k * k;
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(tot, 32), 4096));
-  reduce_incr_kernel<<<blocks, 256, 0, st>>>(part, nsplit, k, nk, nz, kshift, nA, kp, fw_part, nfw, inc,
-                                             gate, alt);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, reduce_incr_kernel, part, nsplit, k, nk, nz, kshift, nA, kp, fw_part, nfw, inc,
+                     gate, alt);
 }
 
 }  // namespace wlr

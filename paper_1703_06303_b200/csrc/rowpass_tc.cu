@@ -49,6 +49,7 @@ struct TcLayout {                                  // bytes; every block 1024-al
 
 template <int RP>
 __global__ void __launch_bounds__(kTcThreads, 2) row_pass_tc_kernel(const __grid_constant__ RowPassTcArgs a) {
+  pdl_trigger();                               // the increments may be scheduled (they wait)
   using L = TcLayout<RP>;
   extern __shared__ __align__(1024) unsigned char tc_raw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tc_raw) + 1023) & ~(uintptr_t)1023);

@@ -597,8 +597,7 @@ WLR_DEVI void s_apply(SS& s, const SmallArgs& a, const double* Cs, int ldc, cons
 //          the library runs it on a second stream concurrently with them.
 template <int BT, int PART>
 __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_constant__ SmallArgs a) {
-  // deferred half: let the programmatic dependent (the next row pass) launch now
-  if (PART == 2) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  pdl_wait();                                  // part 1: the increments of the reduce kernel
   constexpr int PW = BT <= 8 ? BT : (BT <= 16 ? (BT + 1) / 2 : (BT + 3) / 4);
   extern __shared__ __align__(16) double ss_smem[];
   __shared__ double red[8 * kSSW];
@@ -1313,9 +1312,13 @@ cudaError_t launch_ss(const SmallArgs& a, int part, cudaStream_t st) {
   at[0].val.clusterDim.x = a.pl.CL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  if (part == 1 && a.pdl) {
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.numAttrs = 2;
+  }
   if (part == 2) {
-    // the deferred half overlaps the next row pass (its programmatic dependent): schedule its
-    // cluster first
+    // the deferred half runs beside the next critical half: schedule its cluster first
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
     at[1].id = cudaLaunchAttributePriority;
