@@ -105,6 +105,8 @@ struct wlr_ctx {
   // tensor-core increments (fp32, kp <= 32): own column layout (A part padded to 32)
   bool itc_ok = false, itc_on = false;
   int itc_nsplit = 0, itc_nA32 = 0, itc_nz = 0, itc_cs = 1;
+  // non-uniform fp32: e rows -> warp-per-row shared-memory Cholesky (rowsolve.cu)
+  void* Ebuf = nullptr; int rs_grid = 0;
   int64_t itc_rps = 0;
   CUtensorMap tmA32{}, tmX32[2]{}, tmD32{};
   double* inc[2] = {nullptr, nullptr};   // packed increments, by iteration parity
@@ -285,6 +287,7 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int ph) {
     a.fw_part = h->fw_part; a.flags = h->flags;
     a.m = h->m; a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.no = (int)h->kp;
     a.vec_ok = (h->lda % 4 == 0) && ((uintptr_t)h->A % 16 == 0);
+    a.Ebuf = (float*)h->Ebuf;
     set_prefetch(h, ph, a.pf_ptr, a.pf_bytes);
     if (h->tc_on) {
       RowPassTcArgs q{};
@@ -298,6 +301,14 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int ph) {
       e = launch_row_pass_tc(q, h->rp, h->tc_grid, h->st);
     } else {
       e = launch_row_pass<float>(a, h->rp, h->rp_tr, h->uniform, 0, h->rp_grid, h->st);
+      if (e == cudaSuccess && h->Ebuf) {
+        RowSolveArgs q{};
+        q.E = (const float*)h->Ebuf; q.S = (const float*)h->Kop;
+        q.W1 = (const float*)h->W1; q.ldw = h->ldw; q.A = (const float*)h->A; q.lda = h->lda;
+        q.Xold = a.Xold; q.Xnew = a.Xnew; q.Dnew = a.Dnew; q.fw_part = h->fw_part; q.flags = h->flags;
+        q.m = h->m; q.k = (int)h->k; q.kp = (int)h->kp;
+        e = launch_row_solve(q, h->rs_grid, h->st);
+      }
     }
   } else {
     RowPassArgs<double> a{};
@@ -360,7 +371,7 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int ph) {
   }
   launch_reduce_incr(h->ics > 1 ? h->inc_part2 : h->inc_part, h->ics > 1 ? h->ncl : h->nsplit, (int)h->k,
                      (int)h->nk, h->nz, (int)(h->k - h->k0), (int)(h->n - h->k0), (int)h->kp, h->fw_part,
-                     h->tc_on ? h->tc_grid : h->rp_grid, h->inc[cur], h->st,
+                     h->tc_on ? h->tc_grid : (h->Ebuf ? h->rs_grid : h->rp_grid), h->inc[cur], h->st,
                      h->itc_on ? h->flags + 5 : nullptr,   // tensor-core layout: A part padded to nA32
                      ReduceLayout{h->inc_part, (int)ceil_div(h->itc_nsplit, h->itc_cs), h->itc_nz, h->itc_nA32, 32},
                      !prof && !pend);
@@ -586,6 +597,10 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   if ((s = dalloc(h, &h->X[0], (size_t)h->m * kp * es)) != WLR_OK) return s;
   if ((s = dalloc(h, &h->X[1], (size_t)h->m * kp * es)) != WLR_OK) return s;
   if ((s = dalloc(h, &h->Dl, (size_t)h->m * kp * es)) != WLR_OK) return s;
+  if (h->dtype == WLR_F32 && !h->uniform && row_solve_ok((int)k)) {
+    if ((s = dalloc(h, &h->Ebuf, (size_t)h->m * kp * es)) != WLR_OK) return s;
+    h->rs_grid = row_solve_grid((int)k, h->nsm);
+  }
   if ((s = dalloc(h, &h->Wt, (size_t)wt_rows * h->rp * es)) != WLR_OK) return s;
   {   // TMA tensor maps: 128-byte x BM boxes (SWIZZLE_128B) of A and X1, 32-row boxes of Wt
     const uint32_t pe = (uint32_t)(128 / es), bm = (uint32_t)row_pass_bm(h->rp, h->rp_tr);

@@ -43,6 +43,7 @@ struct RowPassArgs {
   int KA;                           // row offset of the X1_p block in Wt
   const T* Kmat;                    // k x k C C^T (non-uniform) or unused
   T* Bout; int64_t ldb;             // MODE_RESULT output (m x t)
+  T* Ebuf;                          // non-uniform: write e rows here and skip the per-row solve
   double* fw_part;                  // gridDim.x partials
   int* flags;
   const void* pf_ptr[6]; int64_t pf_bytes[6];   // L2 prefetch of the next small step's inputs
@@ -92,6 +93,23 @@ struct IncrArgs {
   const int* gate;                  // non-null and *gate != 0: the tensor-core kernel runs instead
   int pdl;                          // launched as a programmatic dependent of the row pass
 };
+// per-row SPD solves of the non-uniform X1 half-step (rowsolve.cu), fp32: warp per row,
+// reverse-packed shared-memory Cholesky
+struct RowSolveArgs {
+  const float* E;                   // m x kp  e_i (written by the row pass)
+  const float* S;                   // k x k   C C^T
+  const float* W1; int64_t ldw;
+  const float* A; int64_t lda;      // A1 = A(:, 0:k) for f_w
+  const float* Xold; float* Xnew; float* Dnew;   // m x kp
+  double* fw_part;                  // gridDim.x partials of f_w
+  int* flags;
+  int64_t m; int k, kp;
+};
+bool row_solve_ok(int k);
+size_t row_solve_smem(int k);
+int row_solve_grid(int k, int nsm);
+cudaError_t launch_row_solve(const RowSolveArgs& a, int grid, cudaStream_t st);
+
 // tensor-core increments (incr_tc.cu): fp32, kp <= 32; partial layout nz' = nA32 + 64 columns
 struct IncrTcArgs {
   CUtensorMap tmA, tmX, tmD;        // boxes 32 columns x 32 rows (SWIZZLE_128B): A, X1_p, Delta

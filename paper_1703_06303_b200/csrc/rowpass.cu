@@ -332,8 +332,10 @@ row_pass_kernel(const __grid_constant__ RowPassArgs<T> a) {
           e = fma(pan(A1s, r, l), w * w, Ys[r * L::YLD + l]);
         }
         Es[r * kp + l] = e;
+        if (a.Ebuf) a.Ebuf[(r0 + r) * kp + l] = e;    // the warp-per-row solver takes over
       }
       __syncthreads();
+      if (a.Ebuf) continue;
       T* wL = sL + warp * chol_packed(kp);
       for (int rl = warp; rl < (warp < a.nwc ? nrow : 0); rl += a.nwc) {
         const int64_t g = r0 + rl;
@@ -361,7 +363,17 @@ row_pass_kernel(const __grid_constant__ RowPassArgs<T> a) {
           for (int i = j + 1 + lane; i < k; i += 32) {
             const T lij = wL[i * (i + 1) / 2 + j];
             T* rowi = wL + i * (i + 1) / 2;
-            for (int l = j + 1; l <= i; ++l) rowi[l] = fma(-lij, wL[l * (l + 1) / 2 + j], rowi[l]);
+            int l = j + 1;
+            for (; l + 3 <= i; l += 4) {           // 4 independent element updates in flight
+              const T c0 = wL[l * (l + 1) / 2 + j], c1 = wL[(l + 1) * (l + 2) / 2 + j];
+              const T c2 = wL[(l + 2) * (l + 3) / 2 + j], c3 = wL[(l + 3) * (l + 4) / 2 + j];
+              const T r0 = rowi[l], r1 = rowi[l + 1], r2 = rowi[l + 2], r3 = rowi[l + 3];
+              rowi[l] = fma(-lij, c0, r0);
+              rowi[l + 1] = fma(-lij, c1, r1);
+              rowi[l + 2] = fma(-lij, c2, r2);
+              rowi[l + 3] = fma(-lij, c3, r3);
+            }
+            for (; l <= i; ++l) rowi[l] = fma(-lij, wL[l * (l + 1) / 2 + j], rowi[l]);
           }
           __syncwarp();
         }
