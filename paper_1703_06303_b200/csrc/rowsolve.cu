@@ -18,6 +18,11 @@ namespace wlr {
 
 constexpr int kRsWarps = 4;                      // warps (row problems in flight) per CTA
 
+// floats of one warp's workspace: factor (rounded to 16 B) | vector | float4 panel rows
+__host__ __device__ inline int rs_warp_floats(int k) {
+  return ((k * (k + 1) / 2 + 3) & ~3) + ((k + 3) & ~3) + 4 * k;
+}
+
 __global__ void __launch_bounds__(32 * kRsWarps) row_solve_kernel(const __grid_constant__ RowSolveArgs a) {
   extern __shared__ __align__(16) unsigned char rs_raw[];
   const int k = a.k, kp = a.kp;
@@ -26,8 +31,10 @@ __global__ void __launch_bounds__(32 * kRsWarps) row_solve_kernel(const __grid_c
   uint16_t* tab = reinterpret_cast<uint16_t*>(rs_raw);              // ntri entries: r | c << 8
   float* wbase = reinterpret_cast<float*>(tab + ((ntri + 7) & ~7));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float* Lp = wbase + (size_t)warp * (ntri + 2 * (k + 4));           // this warp's factor
-  float* v = Lp + ntri;                                             // e -> z -> x
+  const int stride = rs_warp_floats(k);                             // multiple of 4 floats
+  float* Lp = wbase + (size_t)warp * stride;                        // this warp's factor
+  float* v = Lp + ((ntri + 3) & ~3);                                // e -> z -> x
+  float4* P = reinterpret_cast<float4*>(v + ((k + 3) & ~3));        // panel: 4 columns per row r
   for (int c = warp; c < k; c += kRsWarps)
     for (int r = lane; r <= c; r += 32) tab[c * (c + 1) / 2 + r] = (uint16_t)(r | (c << 8));
   __syncthreads();
@@ -46,17 +53,46 @@ __global__ void __launch_bounds__(32 * kRsWarps) row_solve_kernel(const __grid_c
     for (int l = lane; l < k; l += 32) v[l] = a.E[row * kp + l];
     __syncwarp();
     bool spd = true;
-    for (int j = 0; j < k; ++j) {
-      const int M = k - 1 - j, cb = M * (M + 1) / 2;
-      const float djj = Lp[cb + M];
-      spd = spd && (djj > 0.f);
-      const float d = sqrtf(djj > 0.f ? djj : 1.f), inv = 1.f / d;
-      for (int r = lane; r < M; r += 32) Lp[cb + r] *= inv;          // column j below the diagonal
+    // blocked right-looking Cholesky: panels of 4 columns, then one rank-4 update of the
+    // trailing triangle (a storage prefix) with the panel staged as float4 per row
+    for (int j0 = 0; j0 < k; j0 += 4) {
+      const int nb = min(4, k - j0);
+      for (int q = 0; q < nb; ++q) {                                // panel factorisation
+        const int j = j0 + q, M = k - 1 - j, cb = M * (M + 1) / 2;
+        const float djj = Lp[cb + M];
+        spd = spd && (djj > 0.f);
+        const float d = sqrtf(djj > 0.f ? djj : 1.f), inv = 1.f / d;
+        for (int r = lane; r < M; r += 32) Lp[cb + r] *= inv;
+        __syncwarp();
+        if (lane == 0) Lp[cb + M] = d;
+        for (int q2 = q + 1; q2 < nb; ++q2) {                       // later panel columns
+          const int M2 = k - 1 - (j0 + q2), cb2 = M2 * (M2 + 1) / 2;
+          const float ljj2 = Lp[cb + M2];                           // L(j0+q2, j)
+          for (int r = lane; r <= M2; r += 32) Lp[cb2 + r] = fmaf(-Lp[cb + r], ljj2, Lp[cb2 + r]);
+        }
+        __syncwarp();
+      }
+      const int Mt = k - 1 - (j0 + nb - 1);                         // trailing rows r < Mt
+      for (int r = lane; r < Mt; r += 32) {
+        float c4[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int M = k - 1 - (j0 + q);
+          c4[q] = q < nb ? Lp[M * (M + 1) / 2 + r] : 0.f;
+        }
+        P[r] = make_float4(c4[0], c4[1], c4[2], c4[3]);
+      }
       __syncwarp();
-      if (lane == 0) Lp[cb + M] = d;
-      for (int e = lane; e < cb; e += 32) {                         // trailing triangle = prefix
+      const int tt = Mt * (Mt + 1) / 2;
+      for (int e = lane; e < tt; e += 32) {
         const int rc = tab[e], r = rc & 255, c = rc >> 8;
-        Lp[e] = fmaf(-Lp[cb + r], Lp[cb + c], Lp[e]);
+        const float4 pr = P[r], pc = P[c];
+        float x = Lp[e];
+        x = fmaf(-pr.x, pc.x, x);
+        x = fmaf(-pr.y, pc.y, x);
+        x = fmaf(-pr.z, pc.z, x);
+        x = fmaf(-pr.w, pc.w, x);
+        Lp[e] = x;
       }
       __syncwarp();
     }
@@ -105,7 +141,7 @@ __global__ void __launch_bounds__(32 * kRsWarps) row_solve_kernel(const __grid_c
 size_t row_solve_smem(int k) {
   const int ntri = k * (k + 1) / 2;
   return sizeof(uint16_t) * (size_t)((ntri + 7) & ~7) +
-         sizeof(float) * (size_t)kRsWarps * (ntri + 2 * (k + 4));
+         sizeof(float) * (size_t)kRsWarps * rs_warp_floats(k);
 }
 
 bool row_solve_ok(int k) { return k >= 1 && k <= 255 && row_solve_smem(k) <= 220 * 1024; }
