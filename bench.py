@@ -216,6 +216,10 @@ def main():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--flush", default="write", choices=["clean", "write"],
+                    help="L2 flush before each timed step: 'write' = 256 MB write; 'clean' = the same "
+                         "write followed by a read of the buffer, so no dirty flush lines are "
+                         "written back inside the timed step")
     args = ap.parse_args()
     cfg = synth.CONFIGS[args.config]
 
@@ -260,6 +264,7 @@ def main():
     w.wlr_iterate_async(h, args.warmup)
     w.wlr_sync(h)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    flush_sink = torch.zeros((), dtype=torch.float32, device="cuda")
     K = args.steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     w.wlr_profile(h, enable=True, reset=True)
@@ -269,6 +274,8 @@ def main():
     with ClockSampler(local) as clk:
         for i in range(K):
             flush.fill_(float(i))                      # evict A from L2 (untimed)
+            if args.flush == "clean":
+                flush_sink += flush.sum()              # ... and leave only clean lines behind
             ev[i][0].record(stream)
             w.wlr_iterate_async(h, 1)
             ev[i][1].record(stream)
@@ -399,7 +406,9 @@ def main():
             "data": "synthetic (seeded scene generator, synth/)",
             "config": {"workload": f"{cfg.name} (BASELINE configs[2]): m={cfg.m} (120x160), n={cfg.n}, "
                                    f"k={cfg.k}, r={cfg.r}, W1={cfg.w_const}, GHS init",
-                       "l2": "flushed before every timed step (256 MB write); steps timed individually",
+                       "l2": ("flushed before every timed step (256 MB write, then a read of it: no dirty lines left); "
+                              "steps timed individually" if args.flush == "clean" else
+                              "flushed before every timed step (256 MB write); steps timed individually"),
                        "parallelism": f"row-sharded x{world}" if world > 1 else "1 GPU"},
             "achieved_hbm_gbs_algorithmic": alg_gbs,
             "roofline": roof,

@@ -19,7 +19,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 SOURCES = ["api.cu", "init_kernels.cu", "rowpass.cu", "small_step.cu", "result.cu", "tma_host.cu", "rowpass_tc.cu", "incr_tc.cu", "rowsolve.cu"] + [
     f"small_step_bt{b}.cu" for b in (4, 8, 12, 16, 24, 32)]
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
+# WLR_NVCC_EXTRA: extra nvcc flags for experiments (e.g. "-DWLR_IT_NR=4"); empty in normal builds
+FLAGS = [*os.environ.get("WLR_NVCC_EXTRA", "").split(), "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
          "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 
 

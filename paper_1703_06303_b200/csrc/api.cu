@@ -332,12 +332,12 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int ph) {
     a.part = h->inc_part; a.part2 = h->inc_part2; a.cs = h->ics; a.m = h->m; a.rows_per_split = h->rps;
     a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.k0 = (int)h->k0; a.nz = h->nz; a.nsplit = h->nsplit;
     a.vec_ok = (h->lda % 4 == 0) && ((uintptr_t)h->A % 16 == 0) && (h->n % 4 == 0);
-    // both increment kernels are enqueued; the small step's gate (flags[5]) decides on the
-    // device which one works: tensor cores once the X1 step is small
-    a.gate = h->itc_on ? h->flags + 5 : nullptr;
+    // tensor-core layout: one kernel; the small step's gate (flags[5]) decides on the device
+    // whether its pipeline feeds the tensor cores (small X1 step) or CUDA-core FMAs
+    a.gate = nullptr;
     a.pdl = prof ? 0 : 1;
-    e = launch_incr<float>(a, h->bm, h->st);
-    if (e == cudaSuccess && h->itc_on) {
+    if (!h->itc_on) e = launch_incr<float>(a, h->bm, h->st);
+    else {
       IncrTcArgs q{};
       q.tmA = h->tmA32; q.tmX = h->tmX32[cur]; q.tmD = h->tmD32;
       q.part = h->inc_part; q.m = h->m; q.rows_per_split = h->itc_rps;
@@ -369,12 +369,15 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int ph) {
     if (prof) cudaEventRecord(ev[7], h->st2);
     CUDA_TRY(h, cudaEventRecord(h->ev_join, h->st2));
   }
-  launch_reduce_incr(h->ics > 1 ? h->inc_part2 : h->inc_part, h->ics > 1 ? h->ncl : h->nsplit, (int)h->k,
-                     (int)h->nk, h->nz, (int)(h->k - h->k0), (int)(h->n - h->k0), (int)h->kp, h->fw_part,
-                     h->tc_on ? h->tc_grid : (h->Ebuf ? h->rs_grid : h->rp_grid), h->inc[cur], h->st,
-                     h->itc_on ? h->flags + 5 : nullptr,   // tensor-core layout: A part padded to nA32
-                     ReduceLayout{h->inc_part, (int)ceil_div(h->itc_nsplit, h->itc_cs), h->itc_nz, h->itc_nA32, 32},
-                     !prof && !pend);
+  const int nfw = h->tc_on ? h->tc_grid : (h->Ebuf ? h->rs_grid : h->rp_grid);
+  if (h->itc_on)   // tensor-core layout: A part padded to nA32, kp' = 32
+    launch_reduce_incr(h->inc_part, (int)ceil_div(h->itc_nsplit, h->itc_cs), (int)h->k, (int)h->nk, h->itc_nz,
+                       (int)(h->k - h->k0), h->itc_nA32, 32, h->fw_part, nfw, h->inc[cur], h->st, nullptr,
+                       ReduceLayout{nullptr, 0, 0, 0, 0}, !prof && !pend);
+  else
+    launch_reduce_incr(h->ics > 1 ? h->inc_part2 : h->inc_part, h->ics > 1 ? h->ncl : h->nsplit, (int)h->k,
+                       (int)h->nk, h->nz, (int)(h->k - h->k0), (int)(h->n - h->k0), (int)h->kp, h->fw_part,
+                       nfw, h->inc[cur], h->st, nullptr, ReduceLayout{nullptr, 0, 0, 0, 0}, !prof && !pend);
   if (prof) cudaEventRecord(ev[3], h->st);
   if (h->comm) {
     const size_t cnt = (size_t)(h->k * h->nk + 2 * h->k * h->k + 1);
@@ -395,7 +398,7 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int ph) {
   }
   h->pend = s;
   h->pending = true;
-  h->pr.launches += (pend ? 5 : 4) + (h->itc_on ? 1 : 0);   // + the gated tensor-core increments
+  h->pr.launches += pend ? 5 : 4;
   return WLR_OK;
 }
 
@@ -430,7 +433,7 @@ static wlr_status launch_iteration(wlr_ctx* h) {
     CUDA_TRY(h, cudaGraphLaunch(h->gexec[h->ph][pend], h->st));
     h->pend = small_args(h, h->ph, 1);
     h->pending = true;
-    h->pr.launches += (pend ? 5 : 4) + (h->itc_on ? 1 : 0);
+    h->pr.launches += pend ? 5 : 4;
   } else {
     s = enqueue_iteration(h, h->ph);
     if (s != WLR_OK) return s;

@@ -23,7 +23,13 @@ namespace cg = cooperative_groups;
 namespace wlr {
 
 constexpr int kItThreads = 192;
-constexpr int kItNR = 3, kItNL = 3;
+#ifndef WLR_IT_NR
+#define WLR_IT_NR 3
+#endif
+#ifndef WLR_IT_NL
+#define WLR_IT_NL 3
+#endif
+constexpr int kItNR = WLR_IT_NR, kItNL = WLR_IT_NL;
 constexpr int kItZB = 4 * 32 * 128;     // Z chunk: 4 boxes of 32 rows x 128 B (16 KB)
 constexpr int kItDB = 32 * 128;         // Delta chunk: 32 rows x 32 fp32 (4 KB)
 constexpr int kItST = kItZB + kItDB;    // raw stage
@@ -31,9 +37,11 @@ constexpr int kItBT = 2 * 32 * 128;     // B operand slot: Delta^T hi | lo (64 r
 constexpr int kItSmem = kItNR * kItST + kItNL * kItBT;
 
 __global__ void __launch_bounds__(kItThreads, 2) incr_tc_kernel(const __grid_constant__ IncrTcArgs a) {
-  pdl_wait();                                     // the CUDA-core increments kernel (and the row pass)
+  pdl_wait();                                     // the row pass
   pdl_trigger();
-  if (!*a.gate) return;                           // large step: the CUDA-core FP32 kernel runs
+  // gate: tensor cores once the X1 step is small; otherwise the same pipeline
+  // feeds plain FP32 FMAs on the CUDA cores (fp32 sums over 32-row chunks, fp64 across chunks)
+  const bool tc = *a.gate != 0;
   extern __shared__ __align__(1024) unsigned char it_raw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(it_raw) + 1023) & ~(uintptr_t)1023);
   unsigned char* rawst = sm;                               // [NR][Z boxes | Delta]
@@ -44,7 +52,7 @@ __global__ void __launch_bounds__(kItThreads, 2) incr_tc_kernel(const __grid_con
   constexpr int ACC = 64;                                  // accumulator columns
   if (warp == 0) tmem_alloc<256>(&tslot);                  // ACC + NL x 64 (Z_hi | Z_lo) <= 256
   if (tid == 32) {
-    for (int s = 0; s < kItNR; ++s) { mbar_init(&full[s], 1); mbar_init(&rawfree[s], 1); }
+    for (int s = 0; s < kItNR; ++s) { mbar_init(&full[s], 1); mbar_init(&rawfree[s], tc ? 1 : 4); }
     for (int s = 0; s < kItNL; ++s) { mbar_init(&lofull[s], 4); mbar_init(&lofree[s], 1); }
     mbar_init(&accfull, 1);
     mbar_init_fence();
@@ -53,6 +61,7 @@ __global__ void __launch_bounds__(kItThreads, 2) incr_tc_kernel(const __grid_con
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tslot;
+  double acc64[32];                                        // CUDA-core path accumulators
   const int j0 = blockIdx.x * 128;                         // first Z column of this block
   const int64_t r0 = (int64_t)blockIdx.y * a.rows_per_split;
   const int64_t r1 = r0 + a.rows_per_split < a.m ? r0 + a.rows_per_split : a.m;
@@ -79,7 +88,7 @@ __global__ void __launch_bounds__(kItThreads, 2) incr_tc_kernel(const __grid_con
       }
     }
   } else if (warp == 5) {
-    if (lane == 0) {
+    if (lane == 0 && tc) {
       const uint32_t id2 = umma_idesc_tf32<128, 64>(), id1 = umma_idesc_tf32<128, 32>();
       int r = 0, l = 0;
       uint32_t phl = 0;
@@ -100,6 +109,39 @@ __global__ void __launch_bounds__(kItThreads, 2) incr_tc_kernel(const __grid_con
         if (++r == kItNR) r = 0;
         if (++l == kItNL) { l = 0; phl ^= 1; }
       }
+    }
+  } else if (!tc) {
+    // ---------------- warps 0-3, CUDA cores: thread c owns Z column c = 32 warp + lane;
+    // per 32-row chunk acc32[l] = sum_i Delta(i, l) Z(i, c) in fp32, then added into fp64
+    int r = 0;
+    uint32_t phr = 0;
+#pragma unroll
+    for (int q = 0; q < 32; ++q) acc64[q] = 0.0;
+    for (int ch = 0; ch < nch; ++ch) {
+      mbar_wait(&full[r], phr);
+      const unsigned char* st = rawst + r * kItST;
+      const float* box = reinterpret_cast<const float*>(st + warp * 4096);
+      const float4* dl = reinterpret_cast<const float4*>(st + kItZB);
+      float acc32[32];
+#pragma unroll
+      for (int q = 0; q < 32; ++q) acc32[q] = 0.f;
+#pragma unroll 4
+      for (int i = 0; i < 32; ++i) {
+        const float z = box[i * 32 + ((((lane >> 2) ^ (i & 7)) << 2) | (lane & 3))];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {           // Delta(i, 4q..4q+3): unit q of row i (broadcast)
+          const float4 d = dl[i * 8 + (q ^ (i & 7))];
+          acc32[4 * q] = fmaf(d.x, z, acc32[4 * q]);
+          acc32[4 * q + 1] = fmaf(d.y, z, acc32[4 * q + 1]);
+          acc32[4 * q + 2] = fmaf(d.z, z, acc32[4 * q + 2]);
+          acc32[4 * q + 3] = fmaf(d.w, z, acc32[4 * q + 3]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 32; ++q) acc64[q] += (double)acc32[q];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&rawfree[r]);
+      if (++r == kItNR) { r = 0; phr ^= 1; }
     }
   } else {
     // ---------------- warps 0-3: Z column c = 32 warp + lane -> TMEM; Delta^T -> smem
@@ -149,7 +191,12 @@ __global__ void __launch_bounds__(kItThreads, 2) incr_tc_kernel(const __grid_con
   // ---------------- epilogue: Z column c = tid (< 128), Delta columns l < 32, into an fp64 tile
   // [32][128] (the stages are free); the cs row splits of a cluster sum their tiles in rank order
   double* tile = reinterpret_cast<double*>(sm);
-  if (warp < 4) {
+  if (!tc) {
+    __syncthreads();                                       // every stage consumed
+    if (warp < 4)
+#pragma unroll
+      for (int q = 0; q < 32; ++q) tile[q * 128 + tid] = acc64[q];
+  } else if (warp < 4) {
     const int c = tid;
     float v[32], v2[32];
     if (nch > 0) {

@@ -32,7 +32,10 @@ constexpr int kTcThreads = 192;
 // to ~52 KB, which was the binding limit (profiles/r01_v7_rowpass_tc_roles.log).
 // (Separate Z / W' rings with a polling producer were measured no faster: the MMA issue rate,
 // ~90 cycles per N <= 64 MMA in situ, and the converter -> MMA handoff bound the chunk rate.)
-constexpr int kTcNR = 4, kTcNL = 3;
+#ifndef WLR_TC_NR
+#define WLR_TC_NR 4
+#endif
+constexpr int kTcNR = WLR_TC_NR, kTcNL = 3;
 constexpr int kTcRPW = kTcBM / 4;                  // epilogue rows per warp
 
 template <int RP>

@@ -38,6 +38,12 @@ __global__ void stream(const __grid_constant__ CUtensorMap tm, float* sink) {
     sink[blockIdx.x] = acc;
   }
 }
+__global__ void readall(const float4* p, size_t n, float* sink) {
+  float acc = 0.f;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) acc += p[i].x;
+  if (acc == 12345.f) sink[0] = acc;
+}
+static int g_flush = 0;   // 0: 256 MB memset (dirty L2); 1: memset + read of it (clean L2); 2: read only
 template <int BR, int NB, int NS, bool LIN = false>
 void run(const CUtensorMap& tm, float* sink) {
   const size_t smem = NS * NB * BR * 128 + 1024;
@@ -50,12 +56,13 @@ void run(const CUtensorMap& tm, float* sink) {
   static void* fl = nullptr; if (!fl) cudaMalloc(&fl, 256 << 20);
   float best = 1e9;
   for (int rep = 0; rep < 5; ++rep) {
-    cudaMemset(fl, rep, 256 << 20);
+    if (g_flush != 2) cudaMemset(fl, rep, 256 << 20);
+    if (g_flush >= 1) readall<<<148 * 8, 512>>>((const float4*)fl, (256 << 20) / 16, sink);
     cudaEventRecord(a); k<<<grid, 64, smem>>>(tm, sink); cudaEventRecord(b); cudaEventSynchronize(b);
     float ms; cudaEventElapsedTime(&ms, a, b); if (rep) best = fminf(best, ms);
   }
   int occ = 0; cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 64, smem);
-  printf("BR=%3d NB=%d NS=%d smem=%6zu occ=%d grid=%d: %.1f us  %.2f TB/s  (%s)\n", BR, NB, NS, smem, occ, grid, best * 1e3,
+  printf("flush=%d BR=%3d NB=%d NS=%d smem=%6zu occ=%d grid=%d: %.1f us  %.2f TB/s  (%s)\n", g_flush, BR, NB, NS, smem, occ, grid, best * 1e3,
          (double)M * N * 4 / (best * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
 }
 int main() {
@@ -68,7 +75,14 @@ int main() {
   CUtensorMap t16, tlin;
   make_tmap_2d(&t16, A, 4, N, M, N * 4, 32, 16, true);
   make_tmap_2d(&tlin, A, 4, 32, (uint64_t)M * N / 32, 128, 32, 64, true);   // contiguous 8 KB boxes
+  for (g_flush = 0; g_flush < 3; ++g_flush) {
   run<64, 1, 4>(t64, sink);
+  run<128, 1, 4>(t128, sink);
+  run<128, 1, 8>(t128, sink);
+  run<128, 2, 4>(t128, sink);
+  run<64, 1, 4, true>(tlin, sink);
+  }
+  g_flush = 0;
   run<16, 19, 2>(t16, sink); run<16, 19, 3>(t16, sink); run<16, 10, 4>(t16, sink); run<16, 5, 6>(t16, sink);
   run<32, 10, 2>(t32, sink); run<32, 5, 4>(t32, sink);
   printf("contiguous 1-D stream (same bytes):\n");
