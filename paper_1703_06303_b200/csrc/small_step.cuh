@@ -146,30 +146,75 @@ WLR_NOINL double block_max(double v, double* red, int t0 = 0, int nt = kSST, int
   return m;
 }
 
-// C[r][c] = alpha * sum_q A[r*lda + q] B[q*ldb + c] (+ I if addI), thread per output, on the
-// threads [t0, t0 + nt) of the block (no barrier inside).
-WLR_NOINL void gemm_nn(int m, int n, int kk, const double* A, int lda, const double* B, int ldb,
-                      double* C, int ldc, double alpha, bool addI, int t0 = 0, int nt = kSST) {
+// One fp64 tensor-core step (mma.sync m8n8k4, FP64 DMMA): d (8 x 8, two values per lane) +=
+// a (8 x 4, one value per lane: row lane / 4, column lane % 4) . b (4 x 8: row lane % 4,
+// column lane / 4); d holds row lane / 4, columns 2 (lane % 4) + {0, 1}.
+WLR_DEVI void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// This lane's two outputs of the 8 x 8 tile (r0, c0) of sum_q A(r, q) B(q, c), A(r, q) =
+// A[r*ars + q*aqs], B(q, c) = B[q*bqs + c*bcs] (m x kk . kk x n): k-steps of 4 on the FP64
+// tensor cores, two accumulator chains.  Row r0 + lane / 4, columns c0 + 2 (lane % 4) + {0, 1}.
+WLR_DEVI void tc_tile(int m, int n, int kk, const double* A, int ars, int aqs, const double* B, int bqs, int bcs,
+                      int r0, int c0, double& v0, double& v1) {
+  const int lane = threadIdx.x & 31, ra = lane >> 2, qa = lane & 3;
+  const int ar = r0 + ra, bc = c0 + ra;                    // A: row ra, k qa; B: k qa, column ra
+  const bool aok = ar < m, bok = bc < n;
+  const double* pa = A + (int64_t)ar * ars + (int64_t)qa * aqs;
+  const double* pb = B + (int64_t)bc * bcs + (int64_t)qa * bqs;
+  const int64_t sa = 4LL * aqs, sb = 4LL * bqs;
+  double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
+  int q = 0;
   #pragma unroll 1
-  for (int o = threadIdx.x - t0; o < m * n; o += nt) {
-    const int r = o / n, c = o - r * n;
-    const double* pa = A + (int64_t)r * lda;
-    const double* pb = B + c;
-    double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
-    int q = 0;
-    #pragma unroll 1
-    for (; q + 3 < kk; q += 4) {
-      v0 = fma(pa[q], pb[(int64_t)q * ldb], v0);
-      v1 = fma(pa[q + 1], pb[(int64_t)(q + 1) * ldb], v1);
-      v2 = fma(pa[q + 2], pb[(int64_t)(q + 2) * ldb], v2);
-      v3 = fma(pa[q + 3], pb[(int64_t)(q + 3) * ldb], v3);
-    }
-    #pragma unroll 1
-    for (; q < kk; ++q) v0 = fma(pa[q], pb[(int64_t)q * ldb], v0);
-    double v = alpha * ((v0 + v1) + (v2 + v3));
-    if (addI && r == c) v += 1.0;
-    C[(int64_t)r * ldc + c] = v;
+  for (; q + 8 <= kk; q += 8) {
+    const double a0 = aok ? pa[0] : 0.0, b0 = bok ? pb[0] : 0.0;
+    const double a1 = aok ? pa[sa] : 0.0, b1 = bok ? pb[sb] : 0.0;
+    dmma884(d0, d1, a0, b0);
+    dmma884(e0, e1, a1, b1);
+    pa += 2 * sa; pb += 2 * sb;
   }
+  #pragma unroll 1
+  for (; q < kk; q += 4) {
+    const bool kin = q + qa < kk;
+    const double a0 = aok && kin ? pa[0] : 0.0, b0 = bok && kin ? pb[0] : 0.0;
+    dmma884(d0, d1, a0, b0);
+    pa += sa; pb += sb;
+  }
+  v0 = d0 + e0;
+  v1 = d1 + e1;
+}
+
+// C(r, c) = alpha * sum_q A(r, q) B(q, c) (+ I if addI) with A(r, q) = A[r*ars + q*aqs],
+// B(q, c) = B[q*bqs + c*bcs], C(r, c) = C[r*ldc + c]: one 8 x 8 output tile per warp step, on
+// the warps of the threads [t0, t0 + nt) (whole warps; no barrier inside).  C must not alias
+// A or B.
+WLR_NOINL void gemm_tc(int m, int n, int kk, const double* A, int ars, int aqs, const double* B, int bqs, int bcs,
+                       double* C, int ldc, double alpha, bool addI, int t0 = 0, int nt = kSST) {
+  const int lane = threadIdx.x & 31, w = (threadIdx.x - t0) >> 5, nw = nt >> 5;
+  const int tn = (n + 7) >> 3, tt = ((m + 7) >> 3) * tn;
+  #pragma unroll 1
+  for (int tile = w; tile < tt; tile += nw) {
+    const int r0 = (tile / tn) << 3, c0 = (tile - (tile / tn) * tn) << 3;
+    double v0, v1;
+    tc_tile(m, n, kk, A, ars, aqs, B, bqs, bcs, r0, c0, v0, v1);
+    const int cr = r0 + (lane >> 2), cc = c0 + 2 * (lane & 3);
+    if (cr < m) {
+      v0 *= alpha; v1 *= alpha;
+      if (addI) { if (cr == cc) v0 += 1.0; if (cr == cc + 1) v1 += 1.0; }
+      if (cc < n) C[(int64_t)cr * ldc + cc] = v0;
+      if (cc + 1 < n) C[(int64_t)cr * ldc + cc + 1] = v1;
+    }
+  }
+}
+
+// C[r][c] = alpha * sum_q A[r*lda + q] B[q*ldb + c] (+ I if addI) on the threads [t0, t0 + nt)
+// of the block (no barrier inside)
+WLR_DEVI void gemm_nn(int m, int n, int kk, const double* A, int lda, const double* B, int ldb,
+                      double* C, int ldc, double alpha, bool addI, int t0 = 0, int nt = kSST) {
+  gemm_tc(m, n, kk, A, lda, 1, B, ldb, 1, C, ldc, alpha, addI, t0, nt);
 }
 
 // Segments of "transpose-NN" slice contractions: out[r*ncol + c] = sum_{i < nl}
@@ -182,28 +227,29 @@ struct TN {
 };
 template <int ND>
 WLR_NOINL void slice_tn(int nl, const TN (&d)[ND]) {
+  // one combined space of 8 x 8 output tiles over the segments, a tile per warp step
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int tot = 0;
 #pragma unroll
-  for (int u = 0; u < ND; ++u) tot += d[u].nrow * d[u].ncol;
+  for (int u = 0; u < ND; ++u) tot += ((d[u].nrow + 7) >> 3) * ((d[u].ncol + 7) >> 3);
   #pragma unroll 1
-  for (int o = threadIdx.x; o < tot; o += kSST) {
+  for (int tile = w; tile < tot; tile += kSSW) {
     int u = 0, base = 0;
 #pragma unroll
-    for (int q = 0; q < ND - 1; ++q)
-      if (o >= base + d[u].nrow * d[u].ncol) { base += d[u].nrow * d[u].ncol; ++u; }
-    const TN& g = d[u];
-    const int oo = o - base, r = oo / g.ncol, c = oo - r * g.ncol;
-    const double* pa = g.A + (int64_t)r * g.ars;
-    const double* pb = g.B + (int64_t)c * g.bcs;
-    double v0 = 0.0, v1 = 0.0;
-    int i = 0;
-    #pragma unroll 1
-    for (; i + 1 < nl; i += 2) {
-      v0 = fma(pa[(int64_t)i * g.ais], pb[(int64_t)i * g.bis], v0);
-      v1 = fma(pa[(int64_t)(i + 1) * g.ais], pb[(int64_t)(i + 1) * g.bis], v1);
+    for (int q = 0; q < ND - 1; ++q) {
+      const int nt = ((d[u].nrow + 7) >> 3) * ((d[u].ncol + 7) >> 3);
+      if (tile >= base + nt) { base += nt; ++u; }
     }
-    if (i < nl) v0 = fma(pa[(int64_t)i * g.ais], pb[(int64_t)i * g.bis], v0);
-    g.out[oo] = v0 + v1;
+    const TN& g = d[u];
+    const int tn = (g.ncol + 7) >> 3, tl = tile - base;
+    const int r0 = (tl / tn) << 3, c0 = (tl - (tl / tn) * tn) << 3;
+    double v0, v1;
+    tc_tile(g.nrow, g.ncol, nl, g.A, g.ars, g.ais, g.B, g.bis, g.bcs, r0, c0, v0, v1);
+    const int cr = r0 + (lane >> 2), cc = c0 + 2 * (lane & 3);
+    if (cr < g.nrow) {
+      if (cc < g.ncol) g.out[cr * g.ncol + cc] = v0;
+      if (cc + 1 < g.ncol) g.out[cr * g.ncol + cc + 1] = v1;
+    }
   }
 }
 
@@ -663,17 +709,22 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
       if (a.mode) {
         g = a.G_in[idx] + incGam[i * k + j] + incGam[j * k + i] + 0.5 * (incOm[i * k + j] + incOm[j * k + i]);
         if (s.c == 0) a.G_out[idx] = g;
-        if (s.c == 0 && idx == 0) {   // gate of the next increments: tensor cores when ||dX1|| <= 1e-3 ||X1||
-          double tom = 0.0, tg = 0.0;
-          for (int q = 0; q < k; ++q) { tom += incOm[q * k + q]; tg += a.G_in[q * k + q] + 2.0 * incGam[q * k + q] + incOm[q * k + q]; }
-          a.flags[5] = tom <= 1e-6 * tg ? 1 : 0;
-        }
+        if (s.c == 0 && i == j) sm[so.d0 + i] = incOm[idx];   // diag(Omega) for the gate below
       } else {
         g = a.G_out[idx];
       }
       Gq[idx] = g;
     }
     __syncthreads();
+    if (a.mode && s.c == 0 && threadIdx.x >= kSST - 32) {
+      // gate of the next increments: tensor cores when ||dX1||^2 = tr(Omega)
+      // <= 1e-6 tr(G') (one warp, beside the inverse)
+      double tom = 0.0, tg = 0.0;
+      for (int q = threadIdx.x & 31; q < k; q += 32) { tom += sm[so.d0 + q]; tg += Gq[q * k + q]; }
+      tom = warp_sum(tom);
+      tg = warp_sum(tg);
+      if ((threadIdx.x & 31) == 0) a.flags[5] = tom <= 1e-6 * tg ? 1 : 0;
+    }
     tmark(s, a);                               // [1a] Gram update loads
     bool okinv = a.mode ? ns_inverse(Gq, Xq, Rq, Pq, k, red) : false;
     if (!okinv) {
