@@ -684,7 +684,7 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   if ((s = dalloc_t(h, &h->xchg2, (size_t)h->spl.CL * h->spl.flen)) != WLR_OK) return s;
   if ((s = dalloc_t(h, &h->red, (size_t)h->spl.flen + 3 * k * t + 64)) != WLR_OK) return s;
   if ((s = dalloc_t(h, &h->scal, 8)) != WLR_OK) return s;
-  if ((s = dalloc_t(h, &h->tdbg, 128)) != WLR_OK) return s;   // K3a marks, then K3b marks
+  if ((s = dalloc_t(h, &h->tdbg, 256)) != WLR_OK) return s;   // K3a marks, K3b marks, exchange stamps
   if ((s = dalloc_t(h, &h->trace, (size_t)h->trace_cap * 4)) != WLR_OK) return s;
 
   // ---- NCCL communicator (rows sharded over ranks)
@@ -1025,8 +1025,8 @@ extern "C" wlr_status wlr_debug_state(wlr_handle h, const char* name, double* ou
   if (!h || !name) return fail(h, WLR_EINVAL, "null argument");
   if (std::string(name) == "ktime") {          // timestamps of the last launched K3 half,
     CUDA_TRY(h, cudaStreamSynchronize(h->st)); // read without launching a pending one
-    if (count) *count = 128;
-    if (out) CUDA_TRY(h, cudaMemcpy(out, h->tdbg, (size_t)std::min<int64_t>(cap, 128) * 8, cudaMemcpyDeviceToHost));
+    if (count) *count = 256;
+    if (out) CUDA_TRY(h, cudaMemcpy(out, h->tdbg, (size_t)std::min<int64_t>(cap, 256) * 8, cudaMemcpyDeviceToHost));
     return WLR_OK;
   }
   wlr_status s = check_flags(h);
@@ -1043,7 +1043,7 @@ extern "C" wlr_status wlr_debug_state(wlr_handle h, const char* name, double* ou
   else if (nm == "theta") { src = h->th[cur]; cnt = h->b; }
   else if (nm == "GA") { src = h->GA; cnt = h->nk * h->nk; }
   else if (nm == "scal") { src = h->scal; cnt = 8; }
-  else if (nm == "ktime") { src = h->tdbg; cnt = 128; }
+  else if (nm == "ktime") { src = h->tdbg; cnt = 256; }
   else if (nm == "tctime") { src = (const double*)h->tc_tstamp; cnt = h->tc_tstamp ? 16 * h->tc_grid : 0; }
   else if (nm == "ktime_on" || nm == "ktime_off") {   // enable/disable K3 phase timestamps
     h->ktime = nm == "ktime_on";

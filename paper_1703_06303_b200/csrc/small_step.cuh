@@ -68,6 +68,8 @@ struct SS {
   double* sm;
   int bank;
   int nt;                // timestamps recorded (CTA 0, thread 0; a.tdbg != nullptr)
+  double* tb;            // cluster-barrier release stamps of the exchanges (a.tdbg + 128)
+  int nx;
 };
 
 // Phase timestamps for profiling the latency-bound small step: CTA 0 /
@@ -87,9 +89,15 @@ WLR_DEVI double* xpart(SS& s, const SSPlan& p) { return s.sm + p.oPart + (int64_
 
 // Fixed-order cluster sum of the len-long partial every CTA wrote into its exchange bank;
 // out is local.  (Arguments by value: this is a shared, non-inlined routine.)
-WLR_NOINL void xreduce_impl(const double* mine, int CL, int len, double* out, int len2, double* out2) {
+WLR_NOINL void xreduce_impl(const double* mine, int CL, int len, double* out, int len2, double* out2,
+                            double* stamp) {
   cg::cluster_group cl = cg::this_cluster();
   cl.sync();
+  if (stamp && threadIdx.x == 0) {             // profiling: when the cluster barrier released
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    *stamp = (double)t;
+  }
 #pragma unroll 1
   for (int i = threadIdx.x; i < len + len2; i += kSST) {
     double v[16];
@@ -103,9 +111,42 @@ WLR_NOINL void xreduce_impl(const double* mine, int CL, int len, double* out, in
   }
   __syncthreads();
 }
+// The same sum as a reduce-scatter + all-gather: CTA c sums the c-th block of the values over the
+// cluster and stores the results into every CTA's out / out2 (remote shared-memory stores), then
+// a second cluster barrier.  Each CTA moves ~2 len values through the cluster network instead of
+// CL len: the long exchanges are bandwidth-bound.  out / out2 in shared memory.
+WLR_NOINL void xreduce_rs_impl(const double* mine, int CL, int c, int len, double* out, int len2, double* out2,
+                               double* stamp) {
+  cg::cluster_group cl = cg::this_cluster();
+  cl.sync();
+  if (stamp && threadIdx.x == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    *stamp = (double)t;
+  }
+  const int L = len + len2, chunk = (L + CL - 1) / CL, i1 = min(L, (c + 1) * chunk);
+#pragma unroll 1
+  for (int i = c * chunk + threadIdx.x; i < i1; i += kSST) {
+    double v[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = q < CL ? cl.map_shared_rank(mine, q)[i] : 0.0;
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) acc += v[q];
+    double* dst = i < len ? out + i : out2 + (i - len);
+#pragma unroll 1
+    for (int d = 0; d < CL; ++d) *cl.map_shared_rank(dst, d) = acc;
+  }
+  cl.sync();
+}
 // (a second segment of len2 values, if any, lands in out2)
 WLR_DEVI void xreduce(SS& s, const SSPlan& p, int len, double* out, int len2 = 0, double* out2 = nullptr) {
-  xreduce_impl(xpart(s, p), s.CL, len, out, len2, out2);
+  double* stamp = s.tb && s.c == 0 && s.nx < 32 ? s.tb + s.nx : nullptr;
+  if (len + len2 >= 256 && s.CL > 1 && __isShared(out) && (len2 == 0 || __isShared(out2)))
+    xreduce_rs_impl(xpart(s, p), s.CL, s.c, len, out, len2, out2, stamp);
+  else
+    xreduce_impl(xpart(s, p), s.CL, len, out, len2, out2, stamp);
+  s.nx++;
   s.bank ^= 1;
 }
 
@@ -660,6 +701,8 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
   s.sm = ss_smem;
   s.bank = 0;
   s.nt = 0;
+  s.tb = a.tdbg ? a.tdbg + 128 : nullptr;
+  s.nx = 0;
   tmark(s, a);
   const int k = a.k, nk = a.nk, b = a.b, t = a.t, kt = k * t, kk = k * k;
   const SmallOff so(b, t, k);
@@ -834,6 +877,7 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
           if (i != j) dev = fmax(dev, fabs(g));
         }
         dev = block_max(dev, red);
+        tmark(s, a);                           // (RR: scaled Grams)
         gen = !(ortho && dev < 1e-13);
         if (gen) {
           if (!chol_small(Lb, b, sm + so.rb, &ok_s)) { failed = true; break; }
@@ -876,6 +920,7 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
           if (threadIdx.x == 32) kok_s = okk ? 1 : 0;
         }
         __syncthreads();
+        tmark(s, a);                           // (RR: Jacobi || K^{-1})
         for (int idx = threadIdx.x; idx < b * b; idx += kSST) {     // Qb = D (Li^T U) or D U
           const int i = idx / b, j = idx - i * b;
           double v;

@@ -31,12 +31,21 @@ def run(ci, warm=8, H=None, Wd=None):
             d = np.diff(ts) / 1e3
             mhz = (ck[-1] - ck[0]) / max(ts[-1] - ts[0], 1) * 1e3
             print(f"cfg{ci} {name} total={(ts[-1]-ts[0])/1e3:.1f}us clk={mhz:.0f}MHz phases(us)=" + " ".join(f"{x:.1f}" for x in d))
+            xb = kt[128 + off: 128 + off + 32]
+            xb = xb[xb > 0]
+            if len(xb):
+                print(f"   {name} exchange barrier releases (us from start): " +
+                      " ".join(f"{(x - ts[0]) / 1e3:.1f}" for x in xb) +
+                      " | marks: " + " ".join(f"{(x - ts[0]) / 1e3:.1f}" for x in ts))
+        if kt[167] > 0:
+            print("   EXP NS#1 start %.1f end %.1f restore %.1f (us from K3a start)" % tuple((kt[i] - kt[1]) / 1e3 for i in (167, 168, 169)))
         t0a, t0b = kt[1], kt[65]
         if int(kt[64]) > 1:
             print(f"   K3b start - K3a start = {(t0b - t0a)/1e3:.1f}us")
 
 
-run(1)
-run(2)
-run(3)
-run(4, H=120, Wd=160)
+for c in (sys.argv[1:] or ["1", "2", "3", "4"]):
+    if c == "4":
+        run(4, H=120, Wd=160)
+    else:
+        run(int(c))

@@ -1,0 +1,87 @@
+// Latency of one small fp64 GEMM (n x n x n, operands in shared memory) inside a 512-thread CTA:
+// (a) FP64 DMMA m8n8k4 tiles (one 8 x 8 tile per warp step), generic pointers
+// (b) the same with shared-space pointers (ld.shared)
+// (c) thread-per-output CUDA-core FMAs (4 chains)
+// Each measured as the clock64 span of 20 back-to-back GEMMs separated by __syncthreads.
+#include <cstdio>
+#include <cstdint>
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+template <bool UNROLL>
+__device__ __noinline__ void gemm_tc(int n, const double* A, const double* B, double* C) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int tn = (n + 7) >> 3;
+  for (int tile = w; tile < tn * tn; tile += nw) {
+    const int r0 = (tile / tn) << 3, c0 = (tile % tn) << 3;
+    const int ra = lane >> 2, qa = lane & 3;
+    const int ar = r0 + ra, bc = c0 + ra;
+    const bool aok = ar < n, bok = bc < n;
+    double d0 = 0, d1 = 0, e0 = 0, e1 = 0;
+    if (UNROLL) {
+      double a[8], b[8];
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        const int q = 4 * s + qa;
+        a[s] = aok && q < n ? A[ar * n + q] : 0.0;
+        b[s] = bok && q < n ? B[q * n + bc] : 0.0;
+      }
+#pragma unroll
+      for (int s = 0; s < 8; s += 2) { dmma884(d0, d1, a[s], b[s]); dmma884(e0, e1, a[s + 1], b[s + 1]); }
+    } else {
+#pragma unroll 1
+      for (int q0 = 0; q0 < n; q0 += 4) {
+        const int q = q0 + qa;
+        dmma884(d0, d1, aok && q < n ? A[ar * n + q] : 0.0, bok && q < n ? B[q * n + bc] : 0.0);
+      }
+    }
+    const int cr = r0 + ra, cc = c0 + 2 * qa;
+    if (cr < n && cc < n) C[cr * n + cc] = d0 + e0;
+    if (cr < n && cc + 1 < n) C[cr * n + cc + 1] = d1 + e1;
+  }
+}
+__device__ __noinline__ void gemm_cc(int n, const double* A, const double* B, double* C) {
+  for (int o = threadIdx.x; o < n * n; o += blockDim.x) {
+    const int r = o / n, c = o % n;
+    double v0 = 0, v1 = 0, v2 = 0, v3 = 0;
+    int q = 0;
+#pragma unroll 1
+    for (; q + 3 < n; q += 4) {
+      v0 = fma(A[r * n + q], B[q * n + c], v0);
+      v1 = fma(A[r * n + q + 1], B[(q + 1) * n + c], v1);
+      v2 = fma(A[r * n + q + 2], B[(q + 2) * n + c], v2);
+      v3 = fma(A[r * n + q + 3], B[(q + 3) * n + c], v3);
+    }
+    for (; q < n; ++q) v0 = fma(A[r * n + q], B[q * n + c], v0);
+    C[o] = (v0 + v1) + (v2 + v3);
+  }
+}
+template <int MODE>
+__global__ void k(int n, unsigned long long* out, double* sink) {
+  __shared__ double A[1024], B[1024], C[1024];
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x) { A[i] = 1.0 / (1 + i); B[i] = 0.5 / (2 + i); C[i] = 0; }
+  __syncthreads();
+  unsigned long long t0 = 0;
+  for (int r = 0; r < 21; ++r) {
+    if (r == 1) t0 = clock64();
+    if (MODE == 0) gemm_tc<false>(n, A, B, C);
+    if (MODE == 1) gemm_tc<true>(n, A, B, C);
+    if (MODE == 2) gemm_cc(n, A, B, C);
+    __syncthreads();
+    if (MODE == 0 || MODE == 1) { if (threadIdx.x < 1024) {} }
+  }
+  if (threadIdx.x == 0) { out[0] = (clock64() - t0) / 20; sink[0] = C[7]; }
+}
+int main() {
+  unsigned long long* d; double* s; cudaMalloc(&d, 64); cudaMalloc(&s, 64);
+  for (int n : {16, 30, 32}) {
+    unsigned long long h[3];
+    k<0><<<1, 512>>>(n, d, s); cudaDeviceSynchronize(); k<0><<<1, 512>>>(n, d, s); cudaMemcpy(&h[0], d, 8, cudaMemcpyDeviceToHost);
+    k<1><<<1, 512>>>(n, d, s); cudaDeviceSynchronize(); k<1><<<1, 512>>>(n, d, s); cudaMemcpy(&h[1], d, 8, cudaMemcpyDeviceToHost);
+    k<2><<<1, 512>>>(n, d, s); cudaDeviceSynchronize(); k<2><<<1, 512>>>(n, d, s); cudaMemcpy(&h[2], d, 8, cudaMemcpyDeviceToHost);
+    printf("n=%2d: DMMA loop %llu cyc | DMMA unrolled loads %llu cyc | CUDA-core %llu cyc  [%s]\n", n, h[0], h[1], h[2],
+           cudaGetErrorString(cudaGetLastError()));
+  }
+  return 0;
+}
