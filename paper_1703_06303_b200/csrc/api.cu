@@ -573,7 +573,9 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
     h->itc_nA32 = (int)round_up(n - h->k0, 32);
     h->itc_nz = h->itc_nA32 + 64;
     const int64_t ncb = ceil_div(h->itc_nz, 128);
-    const int64_t want = std::max<int64_t>(1, (2 * h->nsm) / ncb);
+    const char* cps_env = getenv("WLR_ITC_CPS");    // (experiments: CTAs per SM of the split grid)
+    const int cps = cps_env ? std::max(1, atoi(cps_env)) : 2;
+    const int64_t want = std::max<int64_t>(1, (cps * h->nsm) / ncb);
     h->itc_rps = round_up(ceil_div(h->m, want), 32);
     h->itc_nsplit = (int)ceil_div(h->m, h->itc_rps);
     // (2/4/8-CTA clusters pre-reducing the partials were measured no faster: profiles/r01_v10_itc_cs.log)

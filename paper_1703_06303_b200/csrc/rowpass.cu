@@ -742,13 +742,17 @@ __global__ void reduce_incr_kernel(const double* __restrict__ part, int nsplit, 
       else if (i < nN + nG) { const int64_t q = i - nN; l = (int)(q / k); zc = nA + (int)(q % k); }
       else { const int64_t q = i - nN - nG; l = (int)(q / k); zc = nA + kp + (int)(q % k); }
       const double* src = part + (int64_t)l * nz + zc;
-      int p = g;
-      for (; p + 24 < nsplit; p += 32) {
-        const double v0 = __ldg(src + (int64_t)p * stride), v1 = __ldg(src + (int64_t)(p + 8) * stride);
-        const double v2 = __ldg(src + (int64_t)(p + 16) * stride), v3 = __ldg(src + (int64_t)(p + 24) * stride);
-        s += v0; s += v1; s += v2; s += v3;
+      // batches of 8 splits per lane (64 per output), every load of a batch in flight at once
+      for (int p0 = 0; p0 < nsplit; p0 += 64) {
+        double v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int p = p0 + g + 8 * j;
+          v[j] = p < nsplit ? __ldg(src + (int64_t)p * stride) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s += v[j];
       }
-      for (; p < nsplit; p += 8) s += __ldg(src + (int64_t)p * stride);
     }
     s += __shfl_xor_sync(0xffffffffu, s, 1);
     s += __shfl_xor_sync(0xffffffffu, s, 2);

@@ -78,23 +78,43 @@ __global__ void __launch_bounds__(kTcThreads, 2) row_pass_tc_kernel(const __grid
     }
   };
   if (tid == 0) stamp(0);
-  if (warp == 0) tmem_alloc<L::NCOL>(&tslot);
-  if (tid == 32) {
-    for (int s = 0; s < kTcNR; ++s) { mbar_init(&full[s], 1); mbar_init(&rawfree[s], 1); }
-    for (int s = 0; s < kTcNL; ++s) { mbar_init(&lofull[s], 4); mbar_init(&lofree[s], 1); }
-    mbar_init(&accfull, 1);
-    mbar_init(&accfree, 4);
-    mbar_init_fence();
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = tslot;
   const int nchA = a.KA / 32;
   const int nch = nchA + (a.kp + 31) / 32;
   const int64_t ntiles = ceil_div(a.m, kTcBM);
   const int myt = blockIdx.x < ntiles ? (int)ceil_div(ntiles - blockIdx.x, (int64_t)gridDim.x) : 0;
   const int64_t total = (int64_t)myt * nch;        // chunks this CTA streams
+  // the producer thread initialises the barriers and puts the first stages in flight before the
+  // block-wide barrier (the loads do not wait for the TMEM allocation)
+  auto issue = [&](int64_t g, int s, int c, int64_t tile) {
+    const int r0 = (int)(tile * kTcBM);
+    unsigned char* st = rawst + s * L::STAGE;
+    mbar_expect_tx(&full[s], (uint32_t)L::STAGE);
+    if (c < nchA) tma_load_2d(st, &a.tmA, &full[s], c * 32, r0);
+    else tma_load_2d(st, &a.tmX, &full[s], (c - nchA) * 32, r0);
+    const int kw = c < nchA ? c * 32 : a.KA + (c - nchA) * 32;
+    tma_load_2d(st + L::ZB, &a.tmW, &full[s], kw, 0);
+    tma_load_2d(st + L::ZB + L::WB, &a.tmW, &full[s], kw, RP);
+  };
+  const int npre = (int)(total < kTcNR ? total : kTcNR);
+  if (tid == 128) {
+    for (int s = 0; s < kTcNR; ++s) { mbar_init(&full[s], 1); mbar_init(&rawfree[s], 1); }
+    for (int s = 0; s < kTcNL; ++s) { mbar_init(&lofull[s], 4); mbar_init(&lofree[s], 1); }
+    mbar_init(&accfull, 1);
+    mbar_init(&accfree, 4);
+    mbar_init_fence();
+    int c = 0;
+    int64_t tile = blockIdx.x;
+    for (int g = 0; g < npre; ++g) {               // stages 0 .. npre-1 of the first chunks
+      issue(g, g, c, tile);
+      if (++c == nch) { c = 0; tile += gridDim.x; }
+    }
+    stamp(2);
+  }
+  if (warp == 0) tmem_alloc<L::NCOL>(&tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
 
   if (warp == 4) {
     // ---------------- TMA producer
@@ -105,15 +125,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) row_pass_tc_kernel(const __grid
       int64_t tile = blockIdx.x;
       for (int64_t g = 0; g < total; ++g) {
         if (g >= kTcNR) twait(&rawfree[s], ph ^ 1, w_prod);
-        if (g == 0) stamp(2);
-        const int r0 = (int)(tile * kTcBM);
-        unsigned char* st = rawst + s * L::STAGE;
-        mbar_expect_tx(&full[s], (uint32_t)L::STAGE);
-        if (c < nchA) tma_load_2d(st, &a.tmA, &full[s], c * 32, r0);
-        else tma_load_2d(st, &a.tmX, &full[s], (c - nchA) * 32, r0);
-        const int kw = c < nchA ? c * 32 : a.KA + (c - nchA) * 32;
-        tma_load_2d(st + L::ZB, &a.tmW, &full[s], kw, 0);
-        tma_load_2d(st + L::ZB + L::WB, &a.tmW, &full[s], kw, RP);
+        if (g >= npre) issue(g, s, c, tile);       // the first npre went out before the barrier
         if (++s == kTcNR) { s = 0; ph ^= 1; }
         if (++c == nch) { c = 0; tile += gridDim.x; }
       }

@@ -1,0 +1,54 @@
+"""Diagnostic: GPU timeline of a few bench steps (config 3, CUDA graph + PDL as in bench.py) from
+the CUPTI kernel records of torch.profiler: start offset and duration of every kernel of the step,
+and the gaps between them.  (Profiler timing, not a bench number.)"""
+import json
+import os
+import sys
+import tempfile
+
+sys.path.insert(0, ".")
+import torch
+import synth
+import paper_1703_06303_b200 as w
+
+cfg = synth.CONFIGS[int(sys.argv[1]) if len(sys.argv) > 1 else 3]
+stream = torch.cuda.Stream()
+torch.cuda.set_stream(stream)
+A = torch.from_numpy(synth.make_A(cfg)).cuda()
+h = w.wlr_init(A, cfg.k, cfg.r, None, w1=cfg.w_const or 1.0, stream=stream.cuda_stream)
+w.wlr_row_path(h, True)
+w.wlr_incr_path(h, True)
+flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+w.wlr_iterate_async(h, 20)
+torch.cuda.synchronize()
+marks = []
+from torch.profiler import profile, ProfilerActivity
+with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
+    for i in range(6):
+        flush.fill_(float(i))
+        torch.cuda.synchronize()
+        w.wlr_iterate_async(h, 1)
+        torch.cuda.synchronize()
+path = os.path.join(tempfile.mkdtemp(), "trace.json")
+prof.export_chrome_trace(path)
+ev = json.load(open(path))["traceEvents"]
+ks = [e for e in ev if e.get("cat") == "kernel"]
+ks.sort(key=lambda e: e["ts"])
+# split into steps at the fill kernels
+steps, cur = [], []
+for e in ks:
+    if "fill" in e["name"] or "elementwise" in e["name"].lower():
+        if cur:
+            steps.append(cur)
+        cur = []
+        continue
+    cur.append(e)
+if cur:
+    steps.append(cur)
+for si, st in enumerate(steps[1:], 1):
+    t0 = st[0]["ts"]
+    end = max(e["ts"] + e["dur"] for e in st)
+    print(f"step {si}: span {end - t0:.1f} us")
+    for e in st:
+        nm = e["name"].replace("wlr::", "")[:48]
+        print(f"   {e['ts'] - t0:7.1f} +{e['dur']:6.1f}  end {e['ts'] + e['dur'] - t0:7.1f}  stream {e['args'].get('stream')}  {nm}")
