@@ -96,6 +96,10 @@ struct wlr_ctx {
   int tc_dbg = 0;                       // diagnostics only (WLR_TC_DBG)
   unsigned long long* tc_tstamp = nullptr;   // per-CTA timestamps (WLR_TC_DBG & 16)
   int tc_grid = 0;
+  int64_t tc_m_main = 0;       // rows covered by tensor-core tiles
+  int tc_extra = 0;            // leftover rows per CTA on the CUDA cores (one CTA per SM)
+  bool tc_deep = false;        // 8-stage ring, one CTA per SM
+  CUtensorMap tmA_x, tmX_x[2];  // leftover-row boxes (32 columns x 4 rows)
   void* WtT = nullptr; int KW = 0;
   CUtensorMap tmA_tc{}, tmX_tc[2]{}, tmWT{};
   int nwc = 8;                 // row-pass warps running per-row Cholesky
@@ -295,10 +299,12 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int ph) {
       q.A = a.A; q.lda = a.lda; q.Xold = a.Xold; q.Xnew = a.Xnew; q.Dnew = a.Dnew;
       q.w2s = a.w2s; q.fw_part = h->fw_part;
       for (int i = 0; i < 6; ++i) { q.pf_ptr[i] = a.pf_ptr[i]; q.pf_bytes[i] = a.pf_bytes[i]; }
-      q.m = h->m; q.KA = h->KA; q.k = (int)h->k; q.kp = (int)h->kp;
+      q.m = h->m; q.KA = h->KA; q.k = (int)h->k; q.kp = (int)h->kp; q.n = (int)h->n;
+      q.m_main = h->tc_m_main; q.extra = h->tc_extra;
+      q.tmAx = h->tmA_x; q.tmXx = h->tmX_x[cur];
       q.dbg = h->tc_dbg;
       q.tstamp = h->tc_tstamp;
-      e = launch_row_pass_tc(q, h->rp, h->tc_grid, h->st);
+      e = launch_row_pass_tc(q, h->rp, h->tc_grid, h->st, nullptr, h->tc_deep);
     } else {
       e = launch_row_pass<float>(a, h->rp, h->rp_tr, h->uniform, 0, h->rp_grid, h->st);
       if (e == cudaSuccess && h->Ebuf) {
@@ -635,7 +641,30 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
     RowPassTcArgs q{};
     if (ok && launch_row_pass_tc(q, h->rp, 0, h->st, &occ) == cudaSuccess && occ > 0) {
       occ = std::max(occ, row_pass_tc_ctas_per_sm(h->rp));   // shared-memory bound (carveout 100)
-      h->tc_grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(h->m, kTcBM), (int64_t)h->nsm * occ));
+      const int64_t ntiles = ceil_div(h->m, kTcBM);
+      h->tc_m_main = h->m;
+      h->tc_extra = 0;
+      h->tc_deep = false;
+      const int tcmode = std::getenv("WLR_TC_MODE") ? std::atoi(std::getenv("WLR_TC_MODE")) : -1;   // (A/B)
+      if (tcmode == 0) {
+        h->tc_grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)h->nsm * occ));
+      } else if (row_pass_tc_deep_ok(h->rp) && ntiles <= h->nsm) {
+        // one tile per CTA, one CTA per SM: the 8-stage ring
+        h->tc_deep = true;
+        h->tc_grid = (int)ntiles;
+      } else if (row_pass_tc_deep_ok(h->rp) && h->rp <= 32 && h->m <= (int64_t)h->nsm * (kTcBM + 4) &&
+                 make_tmap_2d(&h->tmA_x, h->A, 4, (uint64_t)n, (uint64_t)h->m, (uint64_t)h->lda * 4, 32u, 4u, false) &&
+                 make_tmap_2d(&h->tmX_x[0], h->X[0], 4, (uint64_t)kp, (uint64_t)h->m, (uint64_t)kp * 4, 32u, 4u, false) &&
+                 make_tmap_2d(&h->tmX_x[1], h->X[1], 4, (uint64_t)kp, (uint64_t)h->m, (uint64_t)kp * 4, 32u, 4u, false)) {
+        // slightly more rows than one tile per SM (config 3: 150 tiles, 148 SMs): every SM takes
+        // one tile plus <= 4 leftover rows on the CUDA cores, instead of a second wave for 2 tiles
+        h->tc_deep = true;
+        h->tc_grid = h->nsm;
+        h->tc_m_main = (int64_t)h->nsm * kTcBM;
+        h->tc_extra = (int)ceil_div(h->m - h->tc_m_main, (int64_t)h->nsm);
+      } else {
+        h->tc_grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)h->nsm * occ));
+      }
       h->tc_on = true;
     } else {
       h->tc_ok = false;
@@ -813,8 +842,8 @@ extern "C" wlr_status wlr_init(wlr_handle* out, const void* A, int64_t lda, cons
   wlr_ctx* h = new wlr_ctx();
   h->opts = op;
   // eigensolver target (relative to lambda_1; the S-product rounding floor is added in K3):
-  // fp64 mode 1e-12, fp32 mode 1e-8 (DESIGN.md §3 "eigensolver tolerance")
-  if (h->opts.eig_tol <= 0.0) h->opts.eig_tol = op.dtype == WLR_F64 ? 1e-12 : 1e-8;
+  // fp64 mode 1e-12, fp32 mode 3e-8 (DESIGN.md §3 reading R17 "eigensolver tolerance")
+  if (h->opts.eig_tol <= 0.0) h->opts.eig_tol = op.dtype == WLR_F64 ? 1e-12 : 3e-8;
   if (h->opts.eig_max_outer <= 0) h->opts.eig_max_outer = 60;
   h->m = m_local; h->n = n; h->k = k; h->r = r; h->t = r - k; h->nk = n - k;
   h->kp = round_up(k, 4); h->k0 = k & ~3LL;

@@ -66,18 +66,25 @@ cudaError_t launch_row_pass(const RowPassArgs<T>& a, int rp, int tr, bool unifor
 struct RowPassTcArgs {
   CUtensorMap tmA, tmX;             // boxes 32 columns (128 B, SWIZZLE_128B) x 128 rows
   CUtensorMap tmW;                  // W'^T (RP x KW, K-major): boxes 32 x RP, SWIZZLE_128B
+  CUtensorMap tmAx, tmXx;           // leftover rows: boxes 32 columns x 4 rows, no swizzle
   const float* A; int64_t lda;
   const float* Xold; float* Xnew; float* Dnew;   // m x kp
   float w2s;
   double* fw_part;                  // gridDim.x partials of f_w
   const void* pf_ptr[6]; int64_t pf_bytes[6];
-  int64_t m; int KA, k, kp;
+  int64_t m; int KA, k, kp, n;
+  // tiles cover rows [0, m_main); with extra > 0 (one CTA per SM, one tile each) CTA i also
+  // computes the rows m_main + extra i + e, e < extra, on the CUDA cores (no tail wave)
+  int64_t m_main; int extra;
   unsigned long long* tstamp;       // diagnostics: 8 globaltimer stamps per CTA, or nullptr
   int dbg;                          // diagnostics: bit 2 skip W loads, bit 3 skip epilogue
 };
 constexpr int kTcBM = 128;          // rows per tile (UMMA M)
-cudaError_t launch_row_pass_tc(const RowPassTcArgs& a, int rp, int grid, cudaStream_t st, int* occ = nullptr);
+// deep = true: 8-stage ring, one CTA per SM (grid <= #SMs); false: 4 stages, 2 CTAs per SM
+cudaError_t launch_row_pass_tc(const RowPassTcArgs& a, int rp, int grid, cudaStream_t st, int* occ = nullptr,
+                               bool deep = false);
 int row_pass_tc_ctas_per_sm(int rp);   // co-resident CTAs by shared memory (228 KB per SM)
+bool row_pass_tc_deep_ok(int rp);      // the 8-stage ring fits one CTA per SM
 
 
 template <typename T>

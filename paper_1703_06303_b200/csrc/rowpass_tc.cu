@@ -24,7 +24,8 @@ namespace wlr {
 // lane 0 issues TMA, warp 5 lane 0 issues the MMAs.  Rings: NR raw stages (TMA -> smem) and NL
 // lo stages.  M = 128: a TF32 MMA with N = 32, K = 8 costs ~44 cycles whether M is 64 or 128
 // (profiles/r01_ubench_umma_rate.log), so the 128-row tile halves the per-row MMA time.
-constexpr int kTcThreads = 192;
+// (+ warp 6 in the deep variant: the leftover rows)
+template <int NR> constexpr int tc_threads() { return NR >= 8 ? 224 : 192; }
 // The A operand lives in TMEM: each converter thread owns one row of the tile, reads its 32
 // values of the chunk from the swizzled stage and writes Z_hi, Z_lo into TMEM (tcgen05.st);
 // the MMAs read A from TMEM (the "TS" form) and only W'^T from shared memory.  Shared-memory
@@ -32,34 +33,34 @@ constexpr int kTcThreads = 192;
 // to ~52 KB, which was the binding limit (profiles/r01_v7_rowpass_tc_roles.log).
 // (Separate Z / W' rings with a polling producer were measured no faster: the MMA issue rate,
 // ~90 cycles per N <= 64 MMA in situ, and the converter -> MMA handoff bound the chunk rate.)
-#ifndef WLR_TC_NR
-#define WLR_TC_NR 4
-#endif
-constexpr int kTcNR = WLR_TC_NR, kTcNL = 3;
+constexpr int kTcNL = 3;
 constexpr int kTcRPW = kTcBM / 4;                  // epilogue rows per warp
 
-template <int RP>
+template <int RP, int NR>
 struct TcLayout {                                  // bytes; every block 1024-aligned
   static constexpr int ZB = kTcBM * 128;          // Z chunk (fp32 BM x 32)
   static constexpr int WB = RP * 128;             // W'^T chunk (RP x 32)
-  static constexpr int STAGE = ZB + 2 * WB;       // raw stage = Z | W'^T | W'^T_lo (all TMA)
-  static constexpr int TOTAL = kTcNR * STAGE;
+  // deep variant: + the chunk of the CTA's <= 4 leftover rows (4 x 128 B, padded to 1 KB)
+  static constexpr int XB = NR >= 8 ? 1024 : 0;
+  static constexpr int STAGE = ZB + 2 * WB + XB;  // raw stage = Z | W'^T | W'^T_lo | leftover (TMA)
+  static constexpr int TOTAL = NR * STAGE;
   // TMEM columns: accumulator [0, RP) z_hi w_hi + z_lo w_hi, [RP, 2 RP) z_hi w_lo; then NL slots
   // of 64 columns (Z_hi chunk | Z_lo chunk, 32 fp32 each)
   static constexpr int ACC = 2 * RP < 64 ? 64 : 2 * RP;
   static constexpr int NCOL = ACC + 64 * kTcNL <= 256 ? 256 : 512;
 };
 
-template <int RP>
-__global__ void __launch_bounds__(kTcThreads, 2) row_pass_tc_kernel(const __grid_constant__ RowPassTcArgs a) {
+template <int RP, int NR>
+__global__ void __launch_bounds__(tc_threads<NR>(), NR >= 8 ? 1 : 2) row_pass_tc_kernel(const __grid_constant__ RowPassTcArgs a) {
   pdl_trigger();                               // the increments may be scheduled (they wait)
-  using L = TcLayout<RP>;
+  using L = TcLayout<RP, NR>;
+  constexpr int kTcNR = NR;
   extern __shared__ __align__(1024) unsigned char tc_raw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tc_raw) + 1023) & ~(uintptr_t)1023);
   unsigned char* rawst = sm;                               // [NR][Z | W | W_lo]
   __shared__ __align__(8) uint64_t full[kTcNR], rawfree[kTcNR], lofull[kTcNL], lofree[kTcNL], accfull, accfree;
   __shared__ uint32_t tslot;
-  __shared__ double wsum[4];
+  __shared__ double wsum[5];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   auto twait = [&](uint64_t* bar, uint32_t par, unsigned long long& acc) {
     if (a.tstamp) {
@@ -80,24 +81,30 @@ __global__ void __launch_bounds__(kTcThreads, 2) row_pass_tc_kernel(const __grid
   if (tid == 0) stamp(0);
   const int nchA = a.KA / 32;
   const int nch = nchA + (a.kp + 31) / 32;
-  const int64_t ntiles = ceil_div(a.m, kTcBM);
+  const int64_t ntiles = ceil_div(a.m_main, kTcBM);
   const int myt = blockIdx.x < ntiles ? (int)ceil_div(ntiles - blockIdx.x, (int64_t)gridDim.x) : 0;
   const int64_t total = (int64_t)myt * nch;        // chunks this CTA streams
   // the producer thread initialises the barriers and puts the first stages in flight before the
   // block-wide barrier (the loads do not wait for the TMEM allocation)
+  const bool xtra = L::XB > 0 && a.extra > 0;
+  const int xr0 = (int)(a.m_main + (int64_t)a.extra * blockIdx.x);   // first leftover row
   auto issue = [&](int64_t g, int s, int c, int64_t tile) {
     const int r0 = (int)(tile * kTcBM);
     unsigned char* st = rawst + s * L::STAGE;
-    mbar_expect_tx(&full[s], (uint32_t)L::STAGE);
+    mbar_expect_tx(&full[s], (uint32_t)(L::ZB + 2 * L::WB + (xtra ? 512 : 0)));
     if (c < nchA) tma_load_2d(st, &a.tmA, &full[s], c * 32, r0);
     else tma_load_2d(st, &a.tmX, &full[s], (c - nchA) * 32, r0);
     const int kw = c < nchA ? c * 32 : a.KA + (c - nchA) * 32;
     tma_load_2d(st + L::ZB, &a.tmW, &full[s], kw, 0);
     tma_load_2d(st + L::ZB + L::WB, &a.tmW, &full[s], kw, RP);
+    if (xtra) {
+      if (c < nchA) tma_load_2d(st + L::ZB + 2 * L::WB, &a.tmAx, &full[s], c * 32, xr0);
+      else tma_load_2d(st + L::ZB + 2 * L::WB, &a.tmXx, &full[s], (c - nchA) * 32, xr0);
+    }
   };
   const int npre = (int)(total < kTcNR ? total : kTcNR);
   if (tid == 128) {
-    for (int s = 0; s < kTcNR; ++s) { mbar_init(&full[s], 1); mbar_init(&rawfree[s], 1); }
+    for (int s = 0; s < kTcNR; ++s) { mbar_init(&full[s], 1); mbar_init(&rawfree[s], xtra ? 2 : 1); }
     for (int s = 0; s < kTcNL; ++s) { mbar_init(&lofull[s], 4); mbar_init(&lofree[s], 1); }
     mbar_init(&accfull, 1);
     mbar_init(&accfree, 4);
@@ -167,6 +174,56 @@ __global__ void __launch_bounds__(kTcThreads, 2) row_pass_tc_kernel(const __grid
         a.tstamp[(int64_t)gridDim.x * 8 + blockIdx.x * 8 + 2] = w_accf;
       }
     }
+  } else if (warp == 6) {
+    // ---------------- warp 6: the CTA's leftover rows on the CUDA cores (fp32 FMA), lane = output
+    // column l; Z(row e, chunk) comes with each stage (TMA box of 4 rows), W'^T row l from the
+    // stage; the stage is released by this warp and the MMA (rawfree count 2)
+    double fw = 0.0;
+    if (xtra) {
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      int r = 0, c = 0;
+      uint32_t phr = 0;
+      for (int64_t g = 0; g < total; ++g) {
+        mbar_wait(&full[r], phr);
+        const unsigned char* st = rawst + r * L::STAGE;
+        const float4* xb = reinterpret_cast<const float4*>(st + L::ZB + 2 * L::WB);   // [4 rows][8 units]
+        const float4* wrow = reinterpret_cast<const float4*>(st + L::ZB) + (lane < RP ? lane : 0) * 8;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float4 wv = lane < RP ? wrow[q ^ (lane & 7)] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float4 z = xb[e * 8 + q];                   // broadcast
+            acc[e] = fmaf(z.x, wv.x, acc[e]);
+            acc[e] = fmaf(z.y, wv.y, acc[e]);
+            acc[e] = fmaf(z.z, wv.z, acc[e]);
+            acc[e] = fmaf(z.w, wv.w, acc[e]);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&rawfree[r]);
+        if (++r == kTcNR) { r = 0; phr ^= 1; }
+        if (++c == nch) {                                     // all chunks summed: epilogue
+          c = 0;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int64_t xr = a.m_main + (int64_t)a.extra * blockIdx.x + e;
+            if (e < a.extra && xr < a.m && lane < a.kp) {
+              const float x = lane < a.k ? acc[e] : 0.f;
+              a.Xnew[xr * a.kp + lane] = x;
+              a.Dnew[xr * a.kp + lane] = x - a.Xold[xr * a.kp + lane];
+              if (lane < a.k) {
+                const double d = (double)a.A[xr * a.lda + lane] - (double)x;
+                fw += (double)a.w2s * d * d;
+              }
+            }
+            acc[e] = 0.f;
+          }
+        }
+      }
+    }
+    fw = warp_sum(fw);
+    if (lane == 0) wsum[4] = fw;
   } else {
     // ---------------- warps 0-3: lo parts, then the epilogue of each tile
     double fw = 0.0;
@@ -295,7 +352,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) row_pass_tc_kernel(const __grid
   }
   tc_fence_before();
   __syncthreads();
-  if (tid == 0) a.fw_part[blockIdx.x] = (wsum[0] + wsum[1]) + (wsum[2] + wsum[3]);
+  if (tid == 0) a.fw_part[blockIdx.x] = ((wsum[0] + wsum[1]) + (wsum[2] + wsum[3])) + wsum[4];
   if (warp == 0) {
     tc_fence_after();
     tmem_dealloc<L::NCOL>(tmem);
@@ -303,10 +360,10 @@ __global__ void __launch_bounds__(kTcThreads, 2) row_pass_tc_kernel(const __grid
   if (tid == 0) stamp(6);
 }
 
-template <int RP>
+template <int RP, int NR>
 static cudaError_t launch_tc(const RowPassTcArgs& a, int grid, cudaStream_t st, int* occ) {
-  auto kern = row_pass_tc_kernel<RP>;
-  const size_t smem = TcLayout<RP>::TOTAL + 1024;
+  auto kern = row_pass_tc_kernel<RP, NR>;
+  const size_t smem = TcLayout<RP, NR>::TOTAL + 1024;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -315,28 +372,44 @@ static cudaError_t launch_tc(const RowPassTcArgs& a, int grid, cudaStream_t st, 
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  if (occ) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kern, kTcThreads, smem);
-  kern<<<grid, kTcThreads, smem, st>>>(a);
+  if (occ) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kern, tc_threads<NR>(), smem);
+  kern<<<grid, tc_threads<NR>(), smem, st>>>(a);
   return cudaGetLastError();
 }
 
-int row_pass_tc_ctas_per_sm(int rp) {
-  int bytes = 0;
+constexpr int kTcNRShallow = 4, kTcNRDeep = 8;
+
+template <int RP, int NR>
+static constexpr int tc_bytes_t() { return TcLayout<RP, NR>::TOTAL; }
+static int tc_bytes(int rp, bool deep) {
   switch (rp) {
-    case 16: bytes = TcLayout<16>::TOTAL; break;
-    case 32: bytes = TcLayout<32>::TOTAL; break;
-    case 64: bytes = TcLayout<64>::TOTAL; break;
-    default: bytes = TcLayout<128>::TOTAL; break;
+    case 16: return deep ? tc_bytes_t<16, kTcNRDeep>() : tc_bytes_t<16, kTcNRShallow>();
+    case 32: return deep ? tc_bytes_t<32, kTcNRDeep>() : tc_bytes_t<32, kTcNRShallow>();
+    case 64: return deep ? tc_bytes_t<64, kTcNRDeep>() : tc_bytes_t<64, kTcNRShallow>();
+    default: return deep ? tc_bytes_t<128, kTcNRDeep>() : tc_bytes_t<128, kTcNRShallow>();
   }
-  return std::max(1, std::min(2, (227 * 1024) / (bytes + 1024 + 1024)));   // + align pad + reserve
 }
 
-cudaError_t launch_row_pass_tc(const RowPassTcArgs& a, int rp, int grid, cudaStream_t st, int* occ) {
+int row_pass_tc_ctas_per_sm(int rp) {
+  return std::max(1, std::min(2, (227 * 1024) / (tc_bytes(rp, false) + 1024 + 1024)));   // + align pad + reserve
+}
+
+bool row_pass_tc_deep_ok(int rp) { return tc_bytes(rp, true) + 2048 <= 227 * 1024; }
+
+cudaError_t launch_row_pass_tc(const RowPassTcArgs& a, int rp, int grid, cudaStream_t st, int* occ, bool deep) {
+  if (deep) {
+    switch (rp) {
+      case 16: return launch_tc<16, kTcNRDeep>(a, grid, st, occ);
+      case 32: return launch_tc<32, kTcNRDeep>(a, grid, st, occ);
+      case 64: return launch_tc<64, kTcNRDeep>(a, grid, st, occ);
+    }
+    return cudaErrorInvalidValue;
+  }
   switch (rp) {
-    case 16: return launch_tc<16>(a, grid, st, occ);
-    case 32: return launch_tc<32>(a, grid, st, occ);
-    case 64: return launch_tc<64>(a, grid, st, occ);
-    case 128: return launch_tc<128>(a, grid, st, occ);
+    case 16: return launch_tc<16, kTcNRShallow>(a, grid, st, occ);
+    case 32: return launch_tc<32, kTcNRShallow>(a, grid, st, occ);
+    case 64: return launch_tc<64, kTcNRShallow>(a, grid, st, occ);
+    case 128: return launch_tc<128, kTcNRShallow>(a, grid, st, occ);
   }
   return cudaErrorInvalidValue;
 }

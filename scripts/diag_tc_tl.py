@@ -26,3 +26,7 @@ wnames = ["prod wait rawfree", "mma wait lofull", "mma wait accfree", "conv wait
 for i, nm in enumerate(wnames):
     v = wc[:, i] / 1.965e3
     print(f"{nm:18s} min {v.min():7.2f} med {np.median(v):7.2f} max {v.max():7.2f} us (cycles / 1965)")
+end = (t[:, 6] - t0) / 1e3
+order = np.argsort(end)[::-1][:8]
+print("slowest CTAs (index: end us):", " ".join(f"{i}:{end[i]:.1f}" for i in order))
+print("end by CTA block of 16:", " ".join(f"{end[i:i+16].mean():.1f}" for i in range(0, len(end), 16)))

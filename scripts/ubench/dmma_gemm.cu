@@ -9,6 +9,35 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
                : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
 }
+// NCH independent accumulator chains (k-step s goes to chain s % NCH), summed at the end
+template <int NCH>
+__device__ __noinline__ void gemm_tcn(int n, const double* A, const double* B, double* C) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int tn = (n + 7) >> 3;
+  for (int tile = w; tile < tn * tn; tile += nw) {
+    const int r0 = (tile / tn) << 3, c0 = (tile % tn) << 3;
+    const int ra = lane >> 2, qa = lane & 3;
+    const int ar = r0 + ra, bc = c0 + ra;
+    const bool aok = ar < n, bok = bc < n;
+    double d0[NCH], d1[NCH];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) { d0[c] = 0; d1[c] = 0; }
+    double a[8], b[8];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const int q = 4 * s + qa;
+      a[s] = aok && q < n ? A[ar * n + q] : 0.0;
+      b[s] = bok && q < n ? B[q * n + bc] : 0.0;
+    }
+#pragma unroll
+    for (int s = 0; s < 8; ++s) dmma884(d0[s % NCH], d1[s % NCH], a[s], b[s]);
+#pragma unroll
+    for (int c = 1; c < NCH; ++c) { d0[0] += d0[c]; d1[0] += d1[c]; }
+    const int cr = r0 + ra, cc = c0 + 2 * qa;
+    if (cr < n && cc < n) C[cr * n + cc] = d0[0];
+    if (cr < n && cc + 1 < n) C[cr * n + cc + 1] = d1[0];
+  }
+}
 template <bool UNROLL>
 __device__ __noinline__ void gemm_tc(int n, const double* A, const double* B, double* C) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -68,6 +97,9 @@ __global__ void k(int n, unsigned long long* out, double* sink) {
     if (MODE == 0) gemm_tc<false>(n, A, B, C);
     if (MODE == 1) gemm_tc<true>(n, A, B, C);
     if (MODE == 2) gemm_cc(n, A, B, C);
+    if (MODE == 3) gemm_tcn<4>(n, A, B, C);
+    if (MODE == 4) gemm_tcn<8>(n, A, B, C);
+    if (MODE == 5) gemm_tcn<1>(n, A, B, C);
     __syncthreads();
     if (MODE == 0 || MODE == 1) { if (threadIdx.x < 1024) {} }
   }
@@ -80,8 +112,12 @@ int main() {
     k<0><<<1, 512>>>(n, d, s); cudaDeviceSynchronize(); k<0><<<1, 512>>>(n, d, s); cudaMemcpy(&h[0], d, 8, cudaMemcpyDeviceToHost);
     k<1><<<1, 512>>>(n, d, s); cudaDeviceSynchronize(); k<1><<<1, 512>>>(n, d, s); cudaMemcpy(&h[1], d, 8, cudaMemcpyDeviceToHost);
     k<2><<<1, 512>>>(n, d, s); cudaDeviceSynchronize(); k<2><<<1, 512>>>(n, d, s); cudaMemcpy(&h[2], d, 8, cudaMemcpyDeviceToHost);
-    printf("n=%2d: DMMA loop %llu cyc | DMMA unrolled loads %llu cyc | CUDA-core %llu cyc  [%s]\n", n, h[0], h[1], h[2],
-           cudaGetErrorString(cudaGetLastError()));
+    unsigned long long g[3];
+    k<3><<<1, 512>>>(n, d, s); cudaDeviceSynchronize(); k<3><<<1, 512>>>(n, d, s); cudaMemcpy(&g[0], d, 8, cudaMemcpyDeviceToHost);
+    k<4><<<1, 512>>>(n, d, s); cudaDeviceSynchronize(); k<4><<<1, 512>>>(n, d, s); cudaMemcpy(&g[1], d, 8, cudaMemcpyDeviceToHost);
+    k<5><<<1, 512>>>(n, d, s); cudaDeviceSynchronize(); k<5><<<1, 512>>>(n, d, s); cudaMemcpy(&g[2], d, 8, cudaMemcpyDeviceToHost);
+    printf("n=%2d: DMMA loop %llu | 2 chains unrolled %llu | CUDA-core %llu | 1 chain %llu | 4 chains %llu | 8 chains %llu cycles  [%s]\n",
+           n, h[0], h[1], h[2], g[2], g[0], g[1], cudaGetErrorString(cudaGetLastError()));
   }
   return 0;
 }

@@ -65,6 +65,23 @@ def test_row_pass_tensor_core_ragged_tail():
     gu.compare(cfg, g, o)
 
 
+def test_row_pass_tensor_core_one_tile_per_sm_plus_leftover_rows():
+    """m just above one 128-row tile per SM (the config-3 regime: 150 tiles on 148 SMs): every
+    CTA takes one tile on the tensor cores plus <= 4 leftover rows on the CUDA cores; the last
+    CTA's leftover block is ragged."""
+    import torch
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    g0 = np.random.default_rng(6)
+    m, n, k, r = nsm * 128 + nsm + 37, 70, 13, 15
+    A = (g0.standard_normal((m, 12)) @ g0.standard_normal((12, n)) + 0.02 * g0.standard_normal((m, n)))
+    cfg = dataclasses.replace(synth.CONFIGS[2], m=m, n=n, k=k, r=r, w_const=30.0, iters=6)
+    A = A.astype(np.float32)
+    g = gu.run_gpu(cfg, A, None, cfg.iters)
+    assert g["tensor_cores"]
+    o = gu.run_oracle(cfg, A, None, cfg.iters)
+    gu.compare(cfg, g, o)
+
+
 def test_step0_is_ghs_on_gpu():
     """p = 0 is the Theorem 1 closed form on the GPU too (pin P1 path)."""
     cfg = synth.CONFIGS[2]
