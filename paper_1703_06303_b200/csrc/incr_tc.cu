@@ -43,7 +43,9 @@ __global__ void __launch_bounds__(kItThreads, 2) incr_tc_kernel(const __grid_con
   // feeds plain FP32 FMAs on the CUDA cores (fp32 sums over 32-row chunks, fp64 across chunks)
   const bool tc = *a.gate != 0;
   extern __shared__ __align__(1024) unsigned char it_raw[];
-  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(it_raw) + 1023) & ~(uintptr_t)1023);
+  // 1024-aligned by pointer arithmetic on the shared array (an integer round trip would turn
+  // every access through sm into a generic load)
+  unsigned char* sm = it_raw + ((1024u - (smem_u32(it_raw) & 1023u)) & 1023u);
   unsigned char* rawst = sm;                               // [NR][Z boxes | Delta]
   unsigned char* bst = sm + kItNR * kItST;                 // [NL][Delta^T hi | Delta^T lo]
   __shared__ __align__(8) uint64_t full[kItNR], rawfree[kItNR], lofull[kItNL], lofree[kItNL], accfull;
@@ -208,16 +210,26 @@ __global__ void __launch_bounds__(kItThreads, 2) incr_tc_kernel(const __grid_con
 #pragma unroll
       for (int q = 0; q < 32; ++q) { v[q] = 0.f; v2[q] = 0.f; }
     }
+    if (a.cs <= 1) {   // straight from the accumulator lanes: row q of the partial, coalesced over c
+      double* out = a.part + (int64_t)blockIdx.y * a.k * a.nz;
+      if (j0 + c < a.nz)
 #pragma unroll
-    for (int q = 0; q < 32; ++q) tile[q * 128 + c] = (double)v[q] + (double)v2[q];
+        for (int q = 0; q < 32; ++q)
+          if (q < a.k) out[(int64_t)q * a.nz + j0 + c] = (double)v[q] + (double)v2[q];
+    } else {
+#pragma unroll
+      for (int q = 0; q < 32; ++q) tile[q * 128 + c] = (double)v[q] + (double)v2[q];
+    }
   }
   tc_fence_before();
   __syncthreads();
   if (a.cs <= 1) {
-    double* out = a.part + (int64_t)blockIdx.y * a.k * a.nz;
-    for (int idx = tid; idx < a.k * 128; idx += kItThreads) {
-      const int q = idx >> 7, c = idx & 127;
-      if (j0 + c < a.nz) out[(int64_t)q * a.nz + j0 + c] = tile[q * 128 + c];
+    if (!tc) {   // CUDA-core path: the fp64 sums went through the tile
+      double* out = a.part + (int64_t)blockIdx.y * a.k * a.nz;
+      for (int idx = tid; idx < a.k * 128; idx += kItThreads) {
+        const int q = idx >> 7, c = idx & 127;
+        if (j0 + c < a.nz) out[(int64_t)q * a.nz + j0 + c] = tile[q * 128 + c];
+      }
     }
   } else {
     cg::cluster_group cl = cg::this_cluster();

@@ -156,7 +156,7 @@ row_pass_kernel(const __grid_constant__ RowPassArgs<T> a) {
   constexpr int RS = BM / TR;                  // row interleave stride
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  T* sm = reinterpret_cast<T*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  T* sm = reinterpret_cast<T*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
   __shared__ __align__(8) uint64_t full[NST];    // stage filled (TMA bytes landed)
   __shared__ __align__(8) uint64_t empty[NST];   // stage drained (one arrival per warp)
   __shared__ __align__(8) uint64_t epb;

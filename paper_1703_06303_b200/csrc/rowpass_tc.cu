@@ -56,7 +56,9 @@ __global__ void __launch_bounds__(tc_threads<NR>(), NR >= 8 ? 1 : 2) row_pass_tc
   using L = TcLayout<RP, NR>;
   constexpr int kTcNR = NR;
   extern __shared__ __align__(1024) unsigned char tc_raw[];
-  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tc_raw) + 1023) & ~(uintptr_t)1023);
+  // 1024-aligned by pointer arithmetic on the shared array (an integer round trip would turn
+  // every access through sm into a generic load)
+  unsigned char* sm = tc_raw + ((1024u - (smem_u32(tc_raw) & 1023u)) & 1023u);
   unsigned char* rawst = sm;                               // [NR][Z | W | W_lo]
   __shared__ __align__(8) uint64_t full[kTcNR], rawfree[kTcNR], lofull[kTcNL], lofree[kTcNL], accfull, accfree;
   __shared__ uint32_t tslot;
