@@ -61,10 +61,15 @@ class ClockSampler:
                  "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi takes a while to start: wait for its first sample, drop it (pre-region)
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 5.0:
+                time.sleep(0.005)
+            self.lines.clear()
         except Exception:
             self.proc = None
         return self
@@ -75,6 +80,10 @@ class ClockSampler:
 
     def __exit__(self, *a):
         if self.proc:
+            # a short timed region may fall between two samples: wait for the next one
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 1.0:
+                time.sleep(0.002)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
