@@ -267,30 +267,29 @@ struct TN {
   double* out;
 };
 template <int ND>
-WLR_NOINL void slice_tn(int nl, const TN (&d)[ND]) {
-  // one combined space of 8 x 8 output tiles over the segments, a tile per warp step
+WLR_DEVI void slice_tn(int nl, const TN (&d)[ND]) {
+  // one combined space of 8 x 8 output tiles over the segments, a tile per warp step; the
+  // segment loop is unrolled so that every descriptor field is a compile-time access (inlined:
+  // the descriptors stay in registers instead of local memory)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  int tot = 0;
+  int base = 0;
 #pragma unroll
-  for (int u = 0; u < ND; ++u) tot += ((d[u].nrow + 7) >> 3) * ((d[u].ncol + 7) >> 3);
-  #pragma unroll 1
-  for (int tile = w; tile < tot; tile += kSSW) {
-    int u = 0, base = 0;
-#pragma unroll
-    for (int q = 0; q < ND - 1; ++q) {
-      const int nt = ((d[u].nrow + 7) >> 3) * ((d[u].ncol + 7) >> 3);
-      if (tile >= base + nt) { base += nt; ++u; }
+  for (int u = 0; u < ND; ++u) {
+    const int tn = (d[u].ncol + 7) >> 3, nt = ((d[u].nrow + 7) >> 3) * tn;
+    int tl = (w - base) % kSSW;
+    if (tl < 0) tl += kSSW;
+    #pragma unroll 1
+    for (; tl < nt; tl += kSSW) {
+      const int r0 = (tl / tn) << 3, c0 = (tl - (tl / tn) * tn) << 3;
+      double v0, v1;
+      tc_tile(d[u].nrow, d[u].ncol, nl, d[u].A, d[u].ars, d[u].ais, d[u].B, d[u].bis, d[u].bcs, r0, c0, v0, v1);
+      const int cr = r0 + (lane >> 2), cc = c0 + 2 * (lane & 3);
+      if (cr < d[u].nrow) {
+        if (cc < d[u].ncol) d[u].out[cr * d[u].ncol + cc] = v0;
+        if (cc + 1 < d[u].ncol) d[u].out[cr * d[u].ncol + cc + 1] = v1;
+      }
     }
-    const TN& g = d[u];
-    const int tn = (g.ncol + 7) >> 3, tl = tile - base;
-    const int r0 = (tl / tn) << 3, c0 = (tl - (tl / tn) * tn) << 3;
-    double v0, v1;
-    tc_tile(g.nrow, g.ncol, nl, g.A, g.ars, g.ais, g.B, g.bis, g.bcs, r0, c0, v0, v1);
-    const int cr = r0 + (lane >> 2), cc = c0 + 2 * (lane & 3);
-    if (cr < g.nrow) {
-      if (cc < g.ncol) g.out[cr * g.ncol + cc] = v0;
-      if (cc + 1 < g.ncol) g.out[cr * g.ncol + cc + 1] = v1;
-    }
+    base += nt;
   }
 }
 
@@ -1067,6 +1066,7 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
         Qt[idx] = v0 + v1;
       }
     __syncthreads();
+    tmark(s, a);                               // (W': U rows, Qt)
     const int RP = a.rp;
     auto put = [&](int64_t row, int l, double v) {
       const int64_t o = row * RP + l;
@@ -1080,12 +1080,22 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
         wt[(int64_t)RP * a.KW] = f - hi;
       }
     };
-    // Wt rows k + rs + c (columns of A2 in this slice): u K^{-1} or u
+    // Wt rows k + rs + c (columns of A2 in this slice): u K^{-1} (FP64 tensor cores, into the free
+    // gathered-operand region) or u; then the stores, each array in its coalesced order
+    const double* Pw = Us;
+    if (a.uniform) {
+      double* scr = p.oXf >= 0 && (int64_t)nk * b >= (int64_t)s.nl * k ? s.sm + p.oXf : nullptr;
+      if (scr) {
+        gemm_tc(s.nl, k, k, Us, k, 1, Xq, k, 1, scr, k, 1.0, false);
+        __syncthreads();
+        Pw = scr;
+      }
+    }
 #pragma unroll 1
     for (int idx = threadIdx.x; idx < s.nl * k; idx += kSST) {
       const int c = idx / k, l = idx - c * k;
       double v;
-      if (a.uniform) {
+      if (a.uniform && Pw == Us) {
         const double* ur = Us + c * k;
         double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
         int q = 0;
@@ -1098,10 +1108,33 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
         for (; q < k; ++q) v0 = fma(ur[q], Xq[q * k + l], v0);
         v = (v0 + v1) + (v2 + v3);
       } else {
-        v = Us[idx];
+        v = Pw[idx];
       }
-      put(k + s.rs + c, l, v);
+      const int64_t o = (int64_t)(k + s.rs + c) * RP + l;      // row-major W' (c-major: coalesced)
+      if (a.dtype) reinterpret_cast<double*>(a.Wt)[o] = v;
+      else reinterpret_cast<float*>(a.Wt)[o] = (float)v;
     }
+    if (a.WtT) {
+      if (a.uniform && Pw == Us) __syncthreads();
+#pragma unroll 1
+      for (int idx = threadIdx.x; idx < s.nl * k; idx += kSST) {   // W'^T (l-major: coalesced)
+        const int l = idx / s.nl, c = idx - l * s.nl;
+        double v;
+        if (Pw != Us || !a.uniform) {
+          v = Pw[c * k + l];
+        } else {   // (no scratch region: recompute u K^{-1})
+          const double* ur = Us + c * k;
+          v = 0.0;
+          for (int q = 0; q < k; ++q) v = fma(ur[q], Xq[q * k + l], v);
+        }
+        const float f = (float)v;
+        const float hi = __uint_as_float(__float_as_uint(f) & 0xFFFFE000u);
+        float* wt = reinterpret_cast<float*>(a.WtT) + (int64_t)l * a.KW + k + s.rs + c;
+        wt[0] = f;
+        wt[(int64_t)RP * a.KW] = f - hi;
+      }
+    }
+    tmark(s, a);                               // (W': A2 rows)
     // A1 rows (uniform: w^2 K^{-1}) and X1_p rows (P K^{-1} = (C'V') Qt, or P = (C'V')(C'V')^T),
     // spread over the cluster: output o of [0, 2 k^2) on CTA o mod CL
 #pragma unroll 1
