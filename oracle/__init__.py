@@ -29,3 +29,4 @@ from .swlr import (  # noqa: F401
     SwlrResult,
 )
 from .als import general_wlra  # noqa: F401
+from . import block_als  # noqa: F401  (R21)
