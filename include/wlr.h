@@ -121,6 +121,22 @@ wlr_status wlr_trace(wlr_handle h, double* out, int32_t cap, int32_t* count);
 wlr_status wlr_result(wlr_handle h, void* X1, int64_t ldx1, void* C, void* B, int64_t ldb,
                       void* D, void* X2, int64_t ldx2);
 
+/* the factorised WLR (X2 = X1 C + B D, B m x (r-k), D (r-k) x (n-k)) as a
+ * one-sweep block ALS (reading R21), starting from the handle's GHS state (p = 0,
+ * before any wlr_iterate).  A sweep is X1 <- the row formula of PAPER.md:184-196 with
+ * D_p := B_p D_p, then C, B and D by least squares.  Runs n_iters sweeps on the handle's stream
+ * and copies the objectives F_0 .. F_N of all states so far (up to cap doubles) into F (host or
+ * device).  With F = NULL the call only enqueues the sweeps (no host synchronisation; errors
+ * surface at the next wlr_sync).  Single rank only.  The sWLR state is consumed: wlr_iterate on the same
+ * handle afterwards returns WLR_EINVAL.  Errors: WLR_EINVAL (p != 0, nranks > 1, k too large
+ * for the small steps), WLR_ERANK (X1^T X1 or B^T B singular), WLR_ECUDA.                    */
+wlr_status wlr_als_iterate(wlr_handle h, int32_t n_iters, double* F, int32_t cap);
+
+/* Block-ALS state (host or device pointers, NULL to skip): X1 m x k (ld ldx1, dtype),
+ * C k x (n-k) double, B m x (r-k) (ld ldb, dtype), D (r-k) x (n-k) double.                   */
+wlr_status wlr_als_result(wlr_handle h, void* X1, int64_t ldx1, void* C, void* B, int64_t ldb,
+                          void* D);
+
 /* Small replicated state for tests: name in {"G","M","C","V","lam","GA"}; copies up to
  * cap doubles to host out, *count = element count.  G = X1^T X1 (k x k), M = X1^T A2
  * (k x (n-k)), C (k x (n-k)), V ((n-k) x (r-k) row-major), lam (r-k), GA (n-k)^2.      */

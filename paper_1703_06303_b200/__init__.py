@@ -170,6 +170,34 @@ def wlr_result(h: Handle, x2: bool = False, b: bool = True):
     return dict(X1=X1, C=C, B=B, D=D, X2=X2)
 
 
+def wlr_als_iterate(h: Handle, n_iters: int) -> np.ndarray:
+    """f3 block ALS (R21) from the GHS state: runs n_iters sweeps and
+    returns the objectives F_0 .. F_N of all states so far."""
+    cap = 1 << 16
+    F = np.zeros(cap, dtype=np.float64)
+    check(lib.wlr_als_iterate(h.raw, int(n_iters), F.ctypes.data, cap), h.raw)
+    h._als_states = getattr(h, "_als_states", 1) + int(n_iters)
+    return F[: h._als_states].copy()
+
+
+def wlr_als_iterate_async(h: Handle, n_iters: int) -> None:
+    """Enqueue n_iters block-ALS sweeps without synchronising (F trace not copied)."""
+    check(lib.wlr_als_iterate(h.raw, int(n_iters), None, 0), h.raw)
+    h._als_states = getattr(h, "_als_states", 1) + int(n_iters)
+
+
+def wlr_als_result(h: Handle):
+    """Host copies of the block-ALS state: X1 (m x k), C (k x (n-k)), B (m x (r-k)), D ((r-k) x (n-k))."""
+    m, n, k, r = h.m, h.n, h.k, h.r
+    dt = h.np_dtype
+    X1 = np.empty((m, k), dtype=dt)
+    C = np.empty((k, n - k), dtype=np.float64)
+    B = np.empty((m, r - k), dtype=dt)
+    D = np.empty((r - k, n - k), dtype=np.float64)
+    check(lib.wlr_als_result(h.raw, X1.ctypes.data, k, C.ctypes.data, B.ctypes.data, r - k, D.ctypes.data), h.raw)
+    return dict(X1=X1, C=C, B=B, D=D)
+
+
 def wlr_row_path(h: Handle, tensor_cores: bool) -> bool:
     """Select the row-pass implementation for uniform-weight fp32 problems: the tcgen05 3xTF32
     kernel (default) or the CUDA-core FP32 kernel.  Returns whether the tensor-core path is

@@ -17,7 +17,7 @@ WLR_INIT_GHS, WLR_INIT_GIVEN = 0, 1
 EXPORTS = ("wlr_opts_default", "wlr_init", "wlr_iterate", "wlr_iterate_async", "wlr_sync",
            "wlr_objective", "wlr_trace", "wlr_result", "wlr_debug_state", "wlr_profile",
            "wlr_nccl_unique_id", "wlr_last_error", "wlr_status_string", "wlr_destroy",
-           "wlr_version")
+           "wlr_version", "wlr_als_iterate", "wlr_als_result")
 
 
 class wlr_opts(ctypes.Structure):
@@ -70,6 +70,8 @@ def _load():
         "wlr_status_string": (ctypes.c_char_p, [i32]),
         "wlr_destroy": (None, [vp]),
         "wlr_version": (i32, []),
+        "wlr_als_iterate": (i32, [vp, i32, vp, i32]),
+        "wlr_als_result": (i32, [vp, vp, i64, vp, vp, i64, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

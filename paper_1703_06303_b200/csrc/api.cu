@@ -72,6 +72,18 @@ struct Profile {
 
 }  // namespace
 
+// f3 block-ALS state (R21; kernels in als.cu)
+struct AlsSt {
+  void* B = nullptr;            // m x kp (first r-k columns), storage dtype
+  void* Wb = nullptr;           // B row map (KA + KX) x rpb
+  double *C[2] = {}, *D[2] = {};
+  double *inc1 = nullptr, *inc2 = nullptr, *scal = nullptr, *F = nullptr;
+  int nF = 0, nrec = 0;         // F capacity, states recorded
+  CUtensorMap tmBx, tmAr, tmXr[2], tmWb;
+  int rpb = 0, x = 0, c = 0;
+  double F0 = 0.0;              // objective of the GHS state (host copy, staged to F[0])
+};
+
 struct wlr_ctx {
   // dimensions
   int64_t m = 0, n = 0, k = 0, r = 0, t = 0, nk = 0, kp = 0, k0 = 0;
@@ -134,6 +146,7 @@ struct wlr_ctx {
   bool own_stream = false;
   int ph = 0;                  // phase of the current state (= p mod 6: X by p mod 2, state by p mod 3)
   int64_t p = 0;               // index of the current canonical state
+  AlsSt* als = nullptr;        // f3 block ALS (consumes the sWLR state)
   cudaGraphExec_t gexec[6][2] = {};   // [phase][deferred pending]
   cudaStream_t st2 = nullptr;  // side stream of the deferred small-step half
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -430,6 +443,7 @@ static wlr_status build_graph(wlr_ctx* h, int ph, int pend) {
 
 static wlr_status launch_iteration(wlr_ctx* h) {
   wlr_status s;
+  if (h->als) return fail(h, WLR_EINVAL, "the handle ran the block-ALS variant (wlr_als_iterate); sWLR state is gone");
   if (h->opts.use_graph && !h->prof) {
     const int pend = h->pending ? 1 : 0;
     if (!h->gexec[h->ph][pend]) {
@@ -1051,6 +1065,204 @@ extern "C" wlr_status wlr_result(wlr_handle h, void* X1, int64_t ldx1, void* C, 
   return WLR_OK;
 }
 
+// ------------------------------------------------------------------ f3: one-sweep block ALS
+// SURVEY.md §8(f3), R21.  Per sweep: W'' (als_w) -> X1 row map over [A | B_p] (the
+// sWLR row pass / per-row solves) -> Grams X1'^T [A2 | B_p | X1'] (increment kernel with
+// Delta := X1') -> C step + B map (als_c) -> B' = [A | X1'] Wb (result-mode row pass) -> Grams
+// B'^T [A2 | X1' | B'] -> D step + objective (als_d).
+template <typename T>
+static cudaError_t als_row_x1(wlr_ctx* h, AlsSt* st) {
+  const int x = st->x, nx = x ^ 1;
+  RowPassArgs<T> a{};
+  a.A = (const T*)h->A; a.lda = h->lda; a.W1 = (const T*)h->W1; a.ldw = h->ldw;
+  a.w2s = (T)(h->w1s * h->w1s);
+  a.Xold = (const T*)st->B; a.Xnew = (T*)h->X[nx]; a.Dnew = (T*)h->Dl; a.nwc = h->nwc;
+  a.Wt = (const T*)h->Wt; a.KA = h->KA; a.Kmat = (const T*)h->Kop;
+  a.tmA = h->tmA; a.tmX = st->tmBx; a.tmW = h->tmW;
+  a.fw_part = h->fw_part; a.flags = h->flags;
+  a.m = h->m; a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.no = (int)h->kp;
+  a.vec_ok = (h->lda % 4 == 0) && ((uintptr_t)h->A % 16 == 0);
+  if constexpr (sizeof(T) == 4) a.Ebuf = (T*)h->Ebuf;
+  cudaError_t e = launch_row_pass<T>(a, h->rp, h->rp_tr, h->uniform, 0, h->rp_grid, h->st);
+  if constexpr (sizeof(T) == 4) {
+    if (e == cudaSuccess && h->Ebuf) {
+      RowSolveArgs q{};
+      q.E = (const float*)h->Ebuf; q.S = (const float*)h->Kop;
+      q.W1 = (const float*)h->W1; q.ldw = h->ldw; q.A = (const float*)h->A; q.lda = h->lda;
+      q.Xold = (const float*)a.Xold; q.Xnew = (float*)a.Xnew; q.Dnew = (float*)a.Dnew; q.fw_part = h->fw_part;
+      q.flags = h->flags; q.m = h->m; q.k = (int)h->k; q.kp = (int)h->kp;
+      e = launch_row_solve(q, h->rs_grid, h->st);
+    }
+  }
+  return e;
+}
+
+// Grams D^T [A(:, k0:n) | Xo | D] of a kp-wide D (rows l < kd) into inc = [D^T A2 | D^T Xo (gk) |
+// D^T D | f_w]
+template <typename T>
+static cudaError_t als_grams(wlr_ctx* h, const void* Xo, const void* Dd, int kd, int gk, double* inc) {
+  IncrArgs<T> a{};
+  a.A = (const T*)h->A; a.lda = h->lda;
+  a.Xold = (const T*)Xo; a.Dnew = (const T*)Dd;
+  a.part = h->inc_part; a.part2 = h->inc_part2; a.cs = h->ics; a.m = h->m; a.rows_per_split = h->rps;
+  a.n = (int)h->n; a.k = kd; a.kp = (int)h->kp; a.k0 = (int)h->k0; a.nz = h->nz; a.nsplit = h->nsplit;
+  a.vec_ok = (h->lda % 4 == 0) && ((uintptr_t)h->A % 16 == 0) && (h->n % 4 == 0);
+  a.gate = nullptr;
+  a.pdl = 0;
+  cudaError_t e = launch_incr<T>(a, h->bm, h->st);
+  if (e != cudaSuccess) return e;
+  const int nfw = h->Ebuf ? h->rs_grid : h->rp_grid;
+  launch_reduce_incr(h->ics > 1 ? h->inc_part2 : h->inc_part, h->ics > 1 ? h->ncl : h->nsplit, kd,
+                     (int)h->nk, h->nz, (int)(h->k - h->k0), (int)(h->n - h->k0), (int)h->kp, h->fw_part,
+                     nfw, inc, h->st, nullptr, ReduceLayout{nullptr, 0, 0, 0, 0}, false, gk);
+  return cudaGetLastError();
+}
+
+// B = [A | X1] Wb (result-mode row pass: b = a2 D^T S^{-1} - x1 C D^T S^{-1})
+template <typename T>
+static cudaError_t als_row_b(wlr_ctx* h, AlsSt* st, int x) {
+  RowPassArgs<T> a{};
+  a.tmA = st->tmAr; a.tmX = st->tmXr[x]; a.tmW = st->tmWb;
+  a.A = (const T*)h->A; a.lda = h->lda; a.W1 = (const T*)h->W1; a.ldw = h->ldw;
+  a.Xold = (const T*)h->X[x]; a.nwc = h->nwc;
+  a.Wt = (const T*)st->Wb; a.KA = h->KA;
+  a.Bout = (T*)st->B; a.ldb = h->kp; a.fw_part = h->fw_part; a.flags = h->flags;
+  a.m = h->m; a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.no = (int)h->t;
+  a.vec_ok = (h->lda % 4 == 0) && ((uintptr_t)h->A % 16 == 0);
+  return launch_row_pass<T>(a, st->rpb, 8, true, 1, h->rp_grid, h->st);
+}
+
+static AlsArgs als_args(wlr_ctx* h, AlsSt* st) {
+  AlsArgs a{};
+  a.k = (int)h->k; a.nk = (int)h->nk; a.t = (int)h->t; a.KA = h->KA; a.rp = h->rp; a.rpb = st->rpb;
+  a.uniform = h->uniform ? 1 : 0; a.w2 = h->w1s * h->w1s; a.a2sq = h->a2sq;
+  a.flags = h->flags; a.scal = st->scal; a.Kop = h->Kop; a.W = h->Wt; a.Wb = st->Wb;
+  return a;
+}
+
+static wlr_status als_setup(wlr_ctx* h) {
+  wlr_status s = check_flags(h);              // flushes the pending half: F_0 in h_scal
+  if (s != WLR_OK) return s;
+  if (h->p != 0) return fail(h, WLR_EINVAL, "wlr_als_iterate starts from the GHS state (p = 0)");
+  if (h->comm) return fail(h, WLR_EINVAL, "block ALS: single rank only");
+  if (!als_ok((int)h->k, (int)h->t)) return fail(h, WLR_EINVAL, "block ALS: k too large for the small steps");
+  AlsSt* st = new AlsSt();
+  h->als = st;
+  const size_t es = h->es;
+  const int64_t kp = h->kp, wt_rows = h->KA + round_up(kp, 32);
+  st->rpb = row_pass_rp((int)h->t);
+  if ((s = dalloc(h, &st->B, (size_t)h->m * kp * es)) != WLR_OK) return s;
+  if ((s = dalloc(h, &st->Wb, (size_t)wt_rows * st->rpb * es)) != WLR_OK) return s;
+  for (int i = 0; i < 2; ++i) {
+    if ((s = dalloc_t(h, &st->C[i], (size_t)(h->k * h->nk))) != WLR_OK) return s;
+    if ((s = dalloc_t(h, &st->D[i], (size_t)(h->t * h->nk))) != WLR_OK) return s;
+  }
+  if ((s = dalloc_t(h, &st->inc1, (size_t)(h->k * h->nk + 2 * h->k * h->k + 1))) != WLR_OK) return s;
+  if ((s = dalloc_t(h, &st->inc2, (size_t)(h->t * h->nk + h->t * h->k + h->t * h->t + 1))) != WLR_OK) return s;
+  if ((s = dalloc_t(h, &st->scal, 8)) != WLR_OK) return s;
+  CUDA_TRY(h, cudaMemsetAsync(st->B, 0, (size_t)h->m * kp * es, h->st));
+  CUDA_TRY(h, cudaMemsetAsync(st->Wb, 0, (size_t)wt_rows * st->rpb * es, h->st));
+  CUDA_TRY(h, cudaMemsetAsync(h->Wt, 0, (size_t)wt_rows * h->rp * es, h->st));   // sWLR operand reused
+  const uint32_t pe = (uint32_t)(128 / es), bm = (uint32_t)row_pass_bm(h->rp, h->rp_tr);
+  const uint32_t bmr = (uint32_t)row_pass_bm(st->rpb, 8);
+  bool ok = make_tmap_2d(&st->tmBx, st->B, (int)es, (uint64_t)kp, (uint64_t)h->m, (uint64_t)kp * es, pe, bm, true) &&
+            make_tmap_2d(&st->tmAr, h->A, (int)es, (uint64_t)h->n, (uint64_t)h->m, (uint64_t)h->lda * es, pe, bmr, true) &&
+            make_tmap_2d(&st->tmWb, st->Wb, (int)es, (uint64_t)st->rpb, (uint64_t)wt_rows, (uint64_t)st->rpb * es,
+                         (uint32_t)st->rpb, 32u, false);
+  for (int i = 0; i < 2 && ok; ++i)
+    ok = make_tmap_2d(&st->tmXr[i], h->X[i], (int)es, (uint64_t)kp, (uint64_t)h->m, (uint64_t)kp * es, pe, bmr, true);
+  if (!ok) return fail(h, WLR_ECUDA, "cuTensorMapEncodeTiled failed (block ALS)");
+  // p = 0: C_0 and V_0 of the GHS state; D_0 = V_0^T; B_0 = (A2 - X1_0 C_0) V_0 (result map)
+  const int cur = h->ph % 3;
+  st->x = h->ph & 1;
+  st->c = 0;
+  CUDA_TRY(h, cudaMemcpyAsync(st->C[0], h->C[cur], (size_t)(h->k * h->nk) * 8, cudaMemcpyDeviceToDevice, h->st));
+  CUDA_TRY(h, launch_als_transpose(h->V[cur], st->D[0], (int)h->nk, (int)h->t, h->st));
+  AlsArgs a = als_args(h, st);
+  a.C = st->C[0]; a.D = st->D[0]; a.c_given = 1;
+  const bool f64 = h->dtype == WLR_F64;
+  CUDA_TRY(h, launch_als(a, 1, f64, h->st));
+  CUDA_TRY(h, f64 ? als_row_b<double>(h, st, st->x) : als_row_b<float>(h, st, st->x));
+  st->F0 = h->h_scal[2];
+  return check_flags(h);
+}
+
+static wlr_status als_sweep(wlr_ctx* h, double* Fdev) {
+  AlsSt* st = h->als;
+  const bool f64 = h->dtype == WLR_F64;
+  const int x = st->x, nx = x ^ 1, c = st->c, nc = c ^ 1;
+  AlsArgs a = als_args(h, st);
+  a.C = st->C[c]; a.D = st->D[c];
+  CUDA_TRY(h, launch_als(a, 0, f64, h->st));                                       // W''
+  CUDA_TRY(h, f64 ? als_row_x1<double>(h, st) : als_row_x1<float>(h, st));          // X1'
+  CUDA_TRY(h, f64 ? als_grams<double>(h, st->B, h->X[nx], (int)h->k, (int)h->k, st->inc1)
+                  : als_grams<float>(h, st->B, h->X[nx], (int)h->k, (int)h->k, st->inc1));
+  a.inc = st->inc1; a.Cout = st->C[nc]; a.c_given = 0;
+  CUDA_TRY(h, launch_als(a, 1, f64, h->st));                                       // C', Wb
+  CUDA_TRY(h, f64 ? als_row_b<double>(h, st, nx) : als_row_b<float>(h, st, nx));    // B'
+  CUDA_TRY(h, f64 ? als_grams<double>(h, h->X[nx], st->B, (int)h->t, (int)h->k, st->inc2)
+                  : als_grams<float>(h, h->X[nx], st->B, (int)h->t, (int)h->k, st->inc2));
+  AlsArgs d = als_args(h, st);
+  d.C = st->C[nc]; d.inc = st->inc2; d.Dout = st->D[nc]; d.Fout = Fdev;
+  CUDA_TRY(h, launch_als(d, 2, f64, h->st));                                       // D', F
+  st->x = nx;
+  st->c = nc;
+  return WLR_OK;
+}
+
+extern "C" wlr_status wlr_als_iterate(wlr_handle h, int32_t n_iters, double* F, int32_t cap) {
+  if (!h) return fail(nullptr, WLR_EINVAL, "null handle");
+  if (n_iters < 0) return fail(h, WLR_EINVAL, "n_iters < 0");
+  wlr_status s;
+  if (!h->als && (s = als_setup(h)) != WLR_OK) return s;
+  AlsSt* st = h->als;
+  if (st->nF < st->nrec + n_iters + 1) {      // device objective trace
+    double* nf = nullptr;
+    const int cap2 = std::max(2 * st->nF, st->nrec + n_iters + 1);
+    if ((s = dalloc_t(h, &nf, (size_t)cap2)) != WLR_OK) return s;
+    if (st->F && st->nrec > 0) CUDA_TRY(h, cudaMemcpyAsync(nf, st->F, (size_t)st->nrec * 8, cudaMemcpyDeviceToDevice, h->st));
+    st->F = nf;
+    st->nF = cap2;
+  }
+  if (st->nrec == 0) {
+    CUDA_TRY(h, cudaMemcpyAsync(st->F, &st->F0, 8, cudaMemcpyHostToDevice, h->st));
+    st->nrec = 1;
+  }
+  for (int32_t i = 0; i < n_iters; ++i) {
+    if ((s = als_sweep(h, st->F + st->nrec)) != WLR_OK) return s;
+    ++st->nrec;
+  }
+  if (!F) return WLR_OK;                       // asynchronous: errors surface at the next sync
+  CUDA_TRY(h, cudaStreamSynchronize(h->st));
+  if ((s = check_flags(h)) != WLR_OK) return s;
+  if (F && cap > 0) {
+    const int n = std::min(cap, st->nrec);
+    CUDA_TRY(h, cudaMemcpy(F, st->F, (size_t)n * 8, is_device_ptr(F) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost));
+  }
+  return WLR_OK;
+}
+
+extern "C" wlr_status wlr_als_result(wlr_handle h, void* X1, int64_t ldx1, void* C, void* B, int64_t ldb, void* D) {
+  if (!h) return fail(nullptr, WLR_EINVAL, "null handle");
+  if (!h->als) return fail(h, WLR_EINVAL, "wlr_als_result before wlr_als_iterate");
+  wlr_status s = check_flags(h);
+  if (s != WLR_OK) return s;
+  AlsSt* st = h->als;
+  const size_t es = h->es;
+  if (X1) {
+    if (ldx1 < h->k) return fail(h, WLR_EINVAL, "ldx1 < k");
+    if ((s = copy_out(h, X1, ldx1, h->X[st->x], h->kp, h->m, h->k, es)) != WLR_OK) return s;
+  }
+  if (C && (s = copy_out(h, C, h->nk, st->C[st->c], h->nk, h->k, h->nk, 8)) != WLR_OK) return s;
+  if (D && (s = copy_out(h, D, h->nk, st->D[st->c], h->nk, h->t, h->nk, 8)) != WLR_OK) return s;
+  if (B) {
+    if (ldb < h->t) return fail(h, WLR_EINVAL, "ldb < r-k");
+    if ((s = copy_out(h, B, ldb, st->B, h->kp, h->m, h->t, es)) != WLR_OK) return s;
+  }
+  CUDA_TRY(h, cudaStreamSynchronize(h->st));
+  return WLR_OK;
+}
+
 extern "C" wlr_status wlr_debug_state(wlr_handle h, const char* name, double* out, int64_t cap,
                                       int64_t* count) {
   if (!h || !name) return fail(h, WLR_EINVAL, "null argument");
@@ -1194,6 +1406,7 @@ extern "C" void wlr_destroy(wlr_handle h) {
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
   if (h->own_stream && h->st) cudaStreamDestroy(h->st);
+  delete h->als;
   delete h;
 }
 

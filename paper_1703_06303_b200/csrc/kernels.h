@@ -137,7 +137,24 @@ struct ReduceLayout { const double* part; int nsplit, nz, nA, kp; };
 void launch_reduce_incr(const double* part, int nsplit, int k, int nk, int nz, int kshift, int nA,
                         int kp, const double* fw_part, int nfw, double* inc, cudaStream_t st,
                         const int* gate = nullptr, ReduceLayout alt = {nullptr, 0, 0, 0, 0},
-                        bool pdl = false);
+                        bool pdl = false, int gk = -1);
+
+// ---------------------------------------------------------------- f3 block ALS (als.cu)
+struct AlsArgs {
+  const double* C; const double* D;     // current C (k x nk), D ((r-k) x nk), fp64
+  double* Cout; double* Dout;           // updated C / D
+  const double* inc;                    // reduced Grams (layout per kernel, see als.cu)
+  double* scal;                         // [f_w, <M', C'>, <C', G' C'>]
+  double* Fout;                         // objective of the new state
+  void* W; void* Wb; void* Kop;         // X1 row map (KA + KX) x rp, B row map x rpb, C C^T
+  int* flags;
+  int k, nk, t, KA, rp, rpb, uniform, c_given;
+  double w2, a2sq;
+};
+// which: 0 = W'' of the X1 row map, 1 = C step + B map, 2 = D step + objective
+cudaError_t launch_als(const AlsArgs& a, int which, bool f64, cudaStream_t st);
+bool als_ok(int k, int t);
+cudaError_t launch_als_transpose(const double* V, double* D, int nk, int t, cudaStream_t st);
 
 // ---------------------------------------------------------------- small step (small_step.cu)
 // Shared-memory plan of the K3 cluster kernel (offsets in doubles; identical in every CTA

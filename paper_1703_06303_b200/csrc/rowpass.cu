@@ -720,7 +720,7 @@ template cudaError_t launch_incr<double>(const IncrArgs<double>&, int, cudaStrea
 __global__ void reduce_incr_kernel(const double* __restrict__ part, int nsplit, int k, int nk,
                                    int nz, int kshift, int nA, int kp,
                                    const double* __restrict__ fw_part, int nfw,
-                                   double* __restrict__ inc, const int* gate, ReduceLayout alt) {
+                                   double* __restrict__ inc, const int* gate, ReduceLayout alt, int gk) {
   pdl_wait();
   pdl_trigger();
   if (gate && *gate) {   // tensor-core partial layout this iteration
@@ -728,8 +728,9 @@ __global__ void reduce_incr_kernel(const double* __restrict__ part, int nsplit, 
   }
   // 8 lanes per output: lane g sums the splits p = g (mod 8) in order, then a fixed
   // shuffle tree combines the 8 sums (deterministic)
-  const int64_t nN = (int64_t)k * nk, nG = (int64_t)k * k;
-  const int64_t tot = nN + 2 * nG;
+  // inc = [N (k x nk) | Gamma (k x gk) | Omega (k x k) | f_w]  (gk = k for the sWLR increments)
+  const int64_t nN = (int64_t)k * nk, nG = (int64_t)k * gk, nO = (int64_t)k * k;
+  const int64_t tot = nN + nG + nO;
   const int64_t stride = (int64_t)k * nz;
   const int g = threadIdx.x & 7;
   const int64_t per_block = blockDim.x / 8;
@@ -739,7 +740,7 @@ __global__ void reduce_incr_kernel(const double* __restrict__ part, int nsplit, 
     if (i < tot) {
       int l, zc;
       if (i < nN) { l = (int)(i / nk); zc = (int)(i % nk) + kshift; }
-      else if (i < nN + nG) { const int64_t q = i - nN; l = (int)(q / k); zc = nA + (int)(q % k); }
+      else if (i < nN + nG) { const int64_t q = i - nN; l = (int)(q / gk); zc = nA + (int)(q % gk); }
       else { const int64_t q = i - nN - nG; l = (int)(q / k); zc = nA + kp + (int)(q % k); }
       const double* src = part + (int64_t)l * nz + zc;
       // batches of 8 splits per lane (64 per output), every load of a batch in flight at once
@@ -769,8 +770,9 @@ __global__ void reduce_incr_kernel(const double* __restrict__ part, int nsplit, 
 
 void launch_reduce_incr(const double* part, int nsplit, int k, int nk, int nz, int kshift, int nA,
                         int kp, const double* fw_part, int nfw, double* inc, cudaStream_t st,
-                        const int* gate, ReduceLayout alt, bool pdl) {
-  const int64_t tot = (int64_t)k * nk + 2LL * k * k;
+                        const int* gate, ReduceLayout alt, bool pdl, int gk) {
+  if (gk < 0) gk = k;
+  const int64_t tot = (int64_t)k * nk + (int64_t)k * gk + (int64_t)k * k;
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(tot, 32), 4096));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(blocks);
@@ -782,7 +784,7 @@ void launch_reduce_incr(const double* part, int nsplit, int k, int nk, int nz, i
   cfg.attrs = at;
   cfg.numAttrs = pdl ? 1 : 0;
   cudaLaunchKernelEx(&cfg, reduce_incr_kernel, part, nsplit, k, nk, nz, kshift, nA, kp, fw_part, nfw, inc,
-                     gate, alt);
+                     gate, alt, gk);
 }
 
 }  // namespace wlr
