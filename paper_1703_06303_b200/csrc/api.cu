@@ -78,6 +78,7 @@ struct AlsSt {
   void* Wb = nullptr;           // B row map (KA + KX) x rpb
   double *C[2] = {}, *D[2] = {};
   double *inc1 = nullptr, *inc2 = nullptr, *scal = nullptr, *F = nullptr;
+  double *cct = nullptr, *dct = nullptr, *part = nullptr;
   int nF = 0, nrec = 0;         // F capacity, states recorded
   CUtensorMap tmBx, tmAr, tmXr[2], tmWb;
   int rpb = 0, x = 0, c = 0;
@@ -1137,6 +1138,7 @@ static AlsArgs als_args(wlr_ctx* h, AlsSt* st) {
   a.k = (int)h->k; a.nk = (int)h->nk; a.t = (int)h->t; a.KA = h->KA; a.rp = h->rp; a.rpb = st->rpb;
   a.uniform = h->uniform ? 1 : 0; a.w2 = h->w1s * h->w1s; a.a2sq = h->a2sq;
   a.flags = h->flags; a.scal = st->scal; a.Kop = h->Kop; a.W = h->Wt; a.Wb = st->Wb;
+  a.cct = st->cct; a.dct = st->dct; a.part = st->part;
   return a;
 }
 
@@ -1160,6 +1162,9 @@ static wlr_status als_setup(wlr_ctx* h) {
   if ((s = dalloc_t(h, &st->inc1, (size_t)(h->k * h->nk + 2 * h->k * h->k + 1))) != WLR_OK) return s;
   if ((s = dalloc_t(h, &st->inc2, (size_t)(h->t * h->nk + h->t * h->k + h->t * h->t + 1))) != WLR_OK) return s;
   if ((s = dalloc_t(h, &st->scal, 8)) != WLR_OK) return s;
+  if ((s = dalloc_t(h, &st->cct, (size_t)(h->k * h->k))) != WLR_OK) return s;
+  if ((s = dalloc_t(h, &st->dct, (size_t)(h->t * h->k))) != WLR_OK) return s;
+  if ((s = dalloc_t(h, &st->part, als_part_doubles((int)h->k, (int)h->t, (int)h->nk))) != WLR_OK) return s;
   CUDA_TRY(h, cudaMemsetAsync(st->B, 0, (size_t)h->m * kp * es, h->st));
   CUDA_TRY(h, cudaMemsetAsync(st->Wb, 0, (size_t)wt_rows * st->rpb * es, h->st));
   CUDA_TRY(h, cudaMemsetAsync(h->Wt, 0, (size_t)wt_rows * h->rp * es, h->st));   // sWLR operand reused
@@ -1204,7 +1209,7 @@ static wlr_status als_sweep(wlr_ctx* h, double* Fdev) {
                   : als_grams<float>(h, h->X[nx], st->B, (int)h->t, (int)h->k, st->inc2));
   AlsArgs d = als_args(h, st);
   d.C = st->C[nc]; d.inc = st->inc2; d.Dout = st->D[nc]; d.Fout = Fdev;
-  CUDA_TRY(h, launch_als(d, 2, f64, h->st));                                       // D', F
+  CUDA_TRY(h, launch_als(d, 2, f64, h->st));                                       // D', F, D'C'^T
   st->x = nx;
   st->c = nc;
   return WLR_OK;

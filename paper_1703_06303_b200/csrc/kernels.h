@@ -147,6 +147,8 @@ struct AlsArgs {
   double* scal;                         // [f_w, <M', C'>, <C', G' C'>]
   double* Fout;                         // objective of the new state
   void* W; void* Wb; void* Kop;         // X1 row map (KA + KX) x rp, B row map x rpb, C C^T
+  double* cct; double* dct;             // C C^T (k x k) and D C^T (t x k) of the current state
+  double* part;                         // per-CTA partials of the column-split kernels
   int* flags;
   int k, nk, t, KA, rp, rpb, uniform, c_given;
   double w2, a2sq;
@@ -154,6 +156,8 @@ struct AlsArgs {
 // which: 0 = W'' of the X1 row map, 1 = C step + B map, 2 = D step + objective
 cudaError_t launch_als(const AlsArgs& a, int which, bool f64, cudaStream_t st);
 bool als_ok(int k, int t);
+int als_blocks(int nk);
+size_t als_part_doubles(int k, int t, int nk);
 cudaError_t launch_als_transpose(const double* V, double* D, int nk, int t, cudaStream_t st);
 
 // ---------------------------------------------------------------- small step (small_step.cu)
