@@ -42,15 +42,20 @@ __global__ void __launch_bounds__(32 * kRsWarps) row_solve_kernel(const __grid_c
   const int64_t nw = (int64_t)gridDim.x * kRsWarps;
   for (int64_t row = (int64_t)blockIdx.x * kRsWarps + warp; row < a.m; row += nw) {
     const float* w1 = a.W1 + row * a.ldw;
+    // the row's W1^2 into the panel buffer first (one coalesced load, not one dependent global
+    // load per diagonal element inside the build loop)
+    float* w2r = reinterpret_cast<float*>(P);
+    for (int l = lane; l < k; l += 32) { const float w = __ldg(w1 + l); w2r[l] = w * w; }
+    for (int l = lane; l < k; l += 32) v[l] = a.E[row * kp + l];
+    __syncwarp();
     // K_i in reverse packed form
     for (int e = lane; e < ntri; e += 32) {
       const int rc = tab[e], r = rc & 255, c = rc >> 8;
       const int i = k - 1 - r, l = k - 1 - c;
       float x = __ldg(S + i * k + l);
-      if (i == l) { const float w = w1[i]; x += w * w; }
+      if (i == l) x += w2r[i];
       Lp[e] = x;
     }
-    for (int l = lane; l < k; l += 32) v[l] = a.E[row * kp + l];
     __syncwarp();
     bool spd = true;
     // blocked right-looking Cholesky: panels of 4 columns, then one rank-4 update of the
@@ -84,7 +89,31 @@ __global__ void __launch_bounds__(32 * kRsWarps) row_solve_kernel(const __grid_c
       }
       __syncwarp();
       const int tt = Mt * (Mt + 1) / 2;
-      for (int e = lane; e < tt; e += 32) {
+      // 4 independent elements per lane per step: their shared-memory loads overlap
+      int e = lane;
+      for (; e + 96 < tt; e += 128) {
+        int rcq[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) rcq[u] = tab[e + 32 * u];
+        float4 pr[4], pc[4];
+        float x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          pr[u] = P[rcq[u] & 255];
+          pc[u] = P[rcq[u] >> 8];
+          x[u] = Lp[e + 32 * u];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          float y = x[u];
+          y = fmaf(-pr[u].x, pc[u].x, y);
+          y = fmaf(-pr[u].y, pc[u].y, y);
+          y = fmaf(-pr[u].z, pc[u].z, y);
+          y = fmaf(-pr[u].w, pc[u].w, y);
+          Lp[e + 32 * u] = y;
+        }
+      }
+      for (; e < tt; e += 32) {
         const int rc = tab[e], r = rc & 255, c = rc >> 8;
         const float4 pr = P[r], pc = P[c];
         float x = Lp[e];
