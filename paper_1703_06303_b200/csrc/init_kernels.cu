@@ -14,7 +14,9 @@ template <typename T>
 __global__ void __launch_bounds__(256) gram64_kernel(const T* __restrict__ L, int64_t ldl, int nl,
                                                      const T* __restrict__ R, int64_t ldr, int nr,
                                                      int64_t m, int64_t rows_per_split,
-                                                     double* __restrict__ part) {
+                                                     double* __restrict__ part, int sym) {
+  // sym (L == R): only the tiles on or above the diagonal; sum_splits mirrors the rest
+  if (sym && blockIdx.x > blockIdx.y) return;
   __shared__ double Ls[16][64];
   __shared__ double Rs[16][64];
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
@@ -61,11 +63,16 @@ __global__ void __launch_bounds__(256) gram64_kernel(const T* __restrict__ L, in
 }
 
 __global__ void sum_splits_kernel(const double* __restrict__ part, int nsplit, int64_t len,
-                                  double* __restrict__ out) {
+                                  double* __restrict__ out, int sym_n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len;
        i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t src = i;
+    if (sym_n > 0) {   // square symmetric product: tiles below the diagonal read their mirror
+      const int64_t r = i / sym_n, c = i - r * sym_n;
+      if (r / 64 > c / 64) src = c * sym_n + r;
+    }
     double s = 0.0;
-    for (int p = 0; p < nsplit; ++p) s += part[(int64_t)p * len + i];   // fixed order
+    for (int p = 0; p < nsplit; ++p) s += part[(int64_t)p * len + src];   // fixed order
     out[i] = s;
   }
 }
@@ -75,10 +82,11 @@ void launch_gram64(const T* L, int64_t ldl, int nl, const T* R, int64_t ldr, int
                    double* part, int nsplit, double* out, cudaStream_t st) {
   const int64_t rps = round_up(ceil_div(m, nsplit), 16);
   dim3 grid((unsigned)ceil_div(nl, 64), (unsigned)ceil_div(nr, 64), (unsigned)nsplit);
-  gram64_kernel<T><<<grid, 256, 0, st>>>(L, ldl, nl, R, ldr, nr, m, rps, part);
+  const int sym = (L == R && ldl == ldr && nl == nr) ? 1 : 0;
+  gram64_kernel<T><<<grid, 256, 0, st>>>(L, ldl, nl, R, ldr, nr, m, rps, part, sym);
   const int64_t len = (int64_t)nl * nr;
   sum_splits_kernel<<<(unsigned)std::min<int64_t>(ceil_div(len, 256), 4096), 256, 0, st>>>(
-      part, nsplit, len, out);
+      part, nsplit, len, out, sym ? nr : 0);
 }
 template void launch_gram64<float>(const float*, int64_t, int, const float*, int64_t, int, int64_t,
                                    double*, int, double*, cudaStream_t);
