@@ -174,8 +174,28 @@ static wlr_status fail(wlr_ctx* h, wlr_status s, const std::string& msg) {
                   std::string(#x) + ": " + cudaGetErrorString(e_));                          \
   } while (0)
 
+// Device buffers come from the device's default stream-ordered memory pool with the release
+// threshold raised, so that a new handle (e.g. one per solve) reuses the memory of a destroyed one
+// instead of paying cudaMalloc / cudaFree (which synchronises the device) every time.
+static cudaMemPool_t wlr_pool() {
+  static cudaMemPool_t pools[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!pools[dev]) {
+    cudaMemPool_t p = nullptr;
+    if (cudaDeviceGetDefaultMemPool(&p, dev) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &thr);
+    pools[dev] = p;
+  }
+  return pools[dev];
+}
+
 static wlr_status dalloc(wlr_ctx* h, void** p, size_t bytes) {
-  cudaError_t e = cudaMalloc(p, bytes ? bytes : 16);
+  cudaMemPool_t pool = wlr_pool();
+  cudaError_t e = pool ? cudaMallocFromPoolAsync(p, bytes ? bytes : 16, pool, h->st)
+                       : cudaMalloc(p, bytes ? bytes : 16);
   if (e != cudaSuccess) {
     cudaGetLastError();
     return fail(h, WLR_ENOMEM, std::string("cudaMalloc failed: ") + cudaGetErrorString(e));
@@ -982,7 +1002,7 @@ extern "C" wlr_status wlr_result(wlr_handle h, void* X1, int64_t ldx1, void* C, 
   }
   if (B || X2) {
     void* Bd = nullptr;
-    CUDA_TRY(h, cudaMalloc(&Bd, (size_t)h->m * h->t * es + 16));
+    CUDA_TRY(h, cudaMallocAsync(&Bd, (size_t)h->m * h->t * es + 16, h->st));
     // B = A2 V - X1 (C V) as the same streaming GEMM: Wb = [0; V; -C V]  (host-built, small)
     const int rpb = row_pass_rp((int)h->t);
     const int64_t wrows = h->KA + round_up(h->kp, 32);
@@ -996,7 +1016,7 @@ extern "C" wlr_status wlr_result(wlr_handle h, void* X1, int64_t ldx1, void* C, 
     for (int64_t q = 0; q < h->k; ++q)
       for (int64_t j = 0; j < h->t; ++j) wb[(size_t)(h->KA + q) * rpb + j] = -cv[(size_t)q * h->t + j];
     void* Wbd = nullptr;
-    CUDA_TRY(h, cudaMalloc(&Wbd, wb.size() * es));
+    CUDA_TRY(h, cudaMallocAsync(&Wbd, wb.size() * es, h->st));
     if (h->dtype == WLR_F32) {
       std::vector<float> wf(wb.begin(), wb.end());
       CUDA_TRY(h, cudaMemcpy(Wbd, wf.data(), wf.size() * 4, cudaMemcpyHostToDevice));
@@ -1009,7 +1029,7 @@ extern "C" wlr_status wlr_result(wlr_handle h, void* X1, int64_t ldx1, void* C, 
     if (!make_tmap_2d(&tmB, Wbd, (int)es, (uint64_t)rpb, (uint64_t)wrows, (uint64_t)rpb * es, (uint32_t)rpb, 32u, false) ||
         !make_tmap_2d(&tmAr, h->A, (int)es, (uint64_t)h->n, (uint64_t)h->m, (uint64_t)h->lda * es, pe, bmr, true) ||
         !make_tmap_2d(&tmXr, h->X[cx], (int)es, (uint64_t)h->kp, (uint64_t)h->m, (uint64_t)h->kp * es, pe, bmr, true)) {
-      cudaFree(Wbd); cudaFree(Bd);
+      cudaFreeAsync(Wbd, h->st); cudaFreeAsync(Bd, h->st);
       return fail(h, WLR_ECUDA, "cuTensorMapEncodeTiled failed (result)");
     }
     cudaError_t e;
@@ -1035,18 +1055,18 @@ extern "C" wlr_status wlr_result(wlr_handle h, void* X1, int64_t ldx1, void* C, 
       e = launch_row_pass<double>(a, rpb, 8, true, 1, h->rp_grid, h->st);
     }
     cudaStreamSynchronize(h->st);
-    cudaFree(Wbd);
-    if (e != cudaSuccess) { cudaFree(Bd); return fail(h, WLR_ECUDA, std::string("result row pass: ") + cudaGetErrorString(e)); }
+    cudaFreeAsync(Wbd, h->st);
+    if (e != cudaSuccess) { cudaFreeAsync(Bd, h->st); return fail(h, WLR_ECUDA, std::string("result row pass: ") + cudaGetErrorString(e)); }
     if (B) {
-      if (ldb < h->t) { cudaFree(Bd); return fail(h, WLR_EINVAL, "ldb < r-k"); }
-      if ((s = copy_out(h, B, ldb, Bd, h->t, h->m, h->t, es)) != WLR_OK) { cudaFree(Bd); return s; }
+      if (ldb < h->t) { cudaFreeAsync(Bd, h->st); return fail(h, WLR_EINVAL, "ldb < r-k"); }
+      if ((s = copy_out(h, B, ldb, Bd, h->t, h->m, h->t, es)) != WLR_OK) { cudaFreeAsync(Bd, h->st); return s; }
     }
     if (X2) {
-      if (ldx2 < h->nk) { cudaFree(Bd); return fail(h, WLR_EINVAL, "ldx2 < n-k"); }
+      if (ldx2 < h->nk) { cudaFreeAsync(Bd, h->st); return fail(h, WLR_EINVAL, "ldx2 < n-k"); }
       void* X2d = nullptr;
       const bool dev = is_device_ptr(X2);
       if (dev) X2d = X2;
-      else if (cudaMalloc(&X2d, (size_t)h->m * h->nk * es) != cudaSuccess) { cudaFree(Bd); return fail(h, WLR_ENOMEM, "X2 staging"); }
+      else if (cudaMallocAsync(&X2d, (size_t)h->m * h->nk * es, h->st) != cudaSuccess) { cudaFreeAsync(Bd, h->st); return fail(h, WLR_ENOMEM, "X2 staging"); }
       const int64_t ldo = dev ? ldx2 : h->nk;
       if (h->dtype == WLR_F32)
         launch_assemble_x2<float>((const float*)h->X[cx], (int)h->kp, (const float*)Bd, h->t, h->C[cur], h->V[cur], h->m, (int)h->k, (int)h->nk, (int)h->t, (float*)X2d, ldo, h->st);
@@ -1055,12 +1075,12 @@ extern "C" wlr_status wlr_result(wlr_handle h, void* X1, int64_t ldx1, void* C, 
       if (!dev) {
         s = copy_out(h, X2, ldx2, X2d, h->nk, h->m, h->nk, es);
         cudaStreamSynchronize(h->st);
-        cudaFree(X2d);
-        if (s != WLR_OK) { cudaFree(Bd); return s; }
+        cudaFreeAsync(X2d, h->st);
+        if (s != WLR_OK) { cudaFreeAsync(Bd, h->st); return s; }
       }
     }
     CUDA_TRY(h, cudaStreamSynchronize(h->st));
-    cudaFree(Bd);
+    cudaFreeAsync(Bd, h->st);
   }
   CUDA_TRY(h, cudaStreamSynchronize(h->st));
   return WLR_OK;
@@ -1403,7 +1423,11 @@ extern "C" void wlr_destroy(wlr_handle h) {
     for (auto& g : gp)
       if (g) cudaGraphExecDestroy(g);
   if (h->comm && g_nccl.commDestroy) g_nccl.commDestroy(h->comm);
-  for (void* p : h->allocs) cudaFree(p);
+  if (h->st2) cudaStreamSynchronize(h->st2);
+  for (void* p : h->allocs) {
+    if (!h->st || cudaFreeAsync(p, h->st) != cudaSuccess) { cudaGetLastError(); cudaFree(p); }
+  }
+  if (h->st) cudaStreamSynchronize(h->st);
   for (auto e : h->pr.pool) cudaEventDestroy(e);
   if (h->h_flags) cudaFreeHost(h->h_flags);
   if (h->h_scal) cudaFreeHost(h->h_scal);
