@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -173,6 +174,30 @@ static wlr_status fail(wlr_ctx* h, wlr_status s, const std::string& msg) {
       return fail(h, e_ == cudaErrorMemoryAllocation ? WLR_ENOMEM : WLR_ECUDA,               \
                   std::string(#x) + ": " + cudaGetErrorString(e_));                          \
   } while (0)
+
+// Pinned 128-byte blocks for the per-handle status words (8 doubles + 8 ints), kept in a
+// process-wide free list.
+static std::mutex g_pin_mu;
+static std::vector<void*> g_pin_free;
+static void* pinned_take() {
+  {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    if (!g_pin_free.empty()) {
+      void* p = g_pin_free.back();
+      g_pin_free.pop_back();
+      std::memset(p, 0, 128);
+      return p;
+    }
+  }
+  void* p = nullptr;
+  if (cudaMallocHost(&p, 128) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+  std::memset(p, 0, 128);
+  return p;
+}
+static void pinned_give(void* p) {
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  g_pin_free.push_back(p);
+}
 
 // Device buffers come from the device's default stream-ordered memory pool with the release
 // threshold raised, so that a new handle (e.g. one per solve) reuses the memory of a destroyed one
@@ -519,8 +544,12 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   int dev = 0;
   CUDA_TRY(h, cudaGetDevice(&dev));
   CUDA_TRY(h, cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, dev));
-  CUDA_TRY(h, cudaMallocHost(&h->h_flags, 8 * sizeof(int)));
-  CUDA_TRY(h, cudaMallocHost(&h->h_scal, 8 * sizeof(double)));
+  {   // pinned status words, recycled across handles (cudaMallocHost costs ~1.5 ms)
+    void* blk = pinned_take();
+    if (!blk) return fail(h, WLR_ENOMEM, "pinned host block");
+    h->h_scal = reinterpret_cast<double*>(blk);
+    h->h_flags = reinterpret_cast<int*>(reinterpret_cast<char*>(blk) + 8 * sizeof(double));
+  }
   wlr_status s;
   // ---- data: borrow device buffers, copy host buffers
   // The streaming kernels read A through TMA: rows must start 16-byte aligned.  A borrowed
@@ -532,8 +561,12 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
     const int64_t ldp = round_up(h->n, (int64_t)(16 / es));
     void* d = nullptr;
     if ((s = dalloc(h, &d, (size_t)h->m * ldp * es)) != WLR_OK) return s;
-    CUDA_TRY(h, cudaMemcpy2DAsync(d, ldp * es, A, h->lda * es, h->n * es, h->m,
+    if (ldp == h->lda)   // contiguous on both sides: one linear copy
+      CUDA_TRY(h, cudaMemcpyAsync(d, A, (size_t)h->m * ldp * es,
                                   dev_a ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->st));
+    else
+      CUDA_TRY(h, cudaMemcpy2DAsync(d, ldp * es, A, h->lda * es, h->n * es, h->m,
+                                    dev_a ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->st));
     h->A = d;
     h->lda = ldp;
   }
@@ -1429,8 +1462,7 @@ extern "C" void wlr_destroy(wlr_handle h) {
   }
   if (h->st) cudaStreamSynchronize(h->st);
   for (auto e : h->pr.pool) cudaEventDestroy(e);
-  if (h->h_flags) cudaFreeHost(h->h_flags);
-  if (h->h_scal) cudaFreeHost(h->h_scal);
+  if (h->h_scal) pinned_give(h->h_scal);
   if (h->st2) { cudaStreamSynchronize(h->st2); cudaStreamDestroy(h->st2); }
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
