@@ -580,15 +580,12 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
       h->ldw = h->k;
     }
   }
-  if ((s = dalloc_t(h, &h->flags, 8)) != WLR_OK) return s;
-  // ---- validation on device: W1 > 0, finite data
+  if ((s = dalloc_t(h, &h->flags, 8)) != WLR_OK) return s;   // (zeroed)
+  // ---- validation on device: W1 > 0, finite data into flags[1]; read
+  // back (first) at the end of the initialisation, so that the host set-up below and the init
+  // Grams overlap it instead of waiting on a synchronisation here
   if (h->dtype == WLR_F32) launch_validate<float>((const float*)h->A, h->lda, h->m, (int)h->n, (const float*)h->W1, h->ldw, (int)h->k, h->flags, h->st);
   else launch_validate<double>((const double*)h->A, h->lda, h->m, (int)h->n, (const double*)h->W1, h->ldw, (int)h->k, h->flags, h->st);
-  CUDA_TRY(h, cudaMemcpyAsync(h->h_flags, h->flags, 8 * sizeof(int), cudaMemcpyDeviceToHost, h->st));
-  CUDA_TRY(h, cudaStreamSynchronize(h->st));
-  if (h->h_flags[1] & 2) return fail(h, WLR_ENONFINITE, "non-finite entry in A or W1");
-  if (h->h_flags[1] & 1) return fail(h, WLR_EINVAL, "W1 must be > 0 (PAPER.md:94)");
-  CUDA_TRY(h, cudaMemsetAsync(h->flags, 0, 8 * sizeof(int), h->st));
 
   // ---- sizes of the per-iteration kernels
   const int64_t k = h->k, n = h->n, nk = h->nk, t = h->t, kp = h->kp;
@@ -798,7 +795,8 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   }
 
   // ---- one-time Grams in fp64 (a0/a1): A^T A (or X1_0^T [X1_0 | A2] and A2^T A2)
-  const int gsplit = (int)std::max<int64_t>(1, std::min<int64_t>(8, ceil_div(h->m, 4096)));
+  // row splits: enough CTAs (tiles x splits) for several per SM -- the tiles are latency-bound
+  const int gsplit = (int)std::max<int64_t>(1, std::min<int64_t>(24, ceil_div(h->m, 1024)));
   double* part = nullptr;
   double* gram = nullptr;
   if ((s = dalloc_t(h, &part, (size_t)gsplit * n * n)) != WLR_OK) return s;
@@ -879,6 +877,10 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   if (e == cudaSuccess) e = launch_deferred(h, sa, h->st);
   if (e != cudaSuccess) return fail(h, WLR_ECUDA, std::string("small step (init): ") + cudaGetErrorString(e));
   h->pr.launches = 0;
+  CUDA_TRY(h, cudaMemcpyAsync(h->h_flags, h->flags, 8 * sizeof(int), cudaMemcpyDeviceToHost, h->st));
+  CUDA_TRY(h, cudaStreamSynchronize(h->st));
+  if (h->h_flags[1] & 2) return fail(h, WLR_ENONFINITE, "non-finite entry in A or W1");
+  if (h->h_flags[1] & 1) return fail(h, WLR_EINVAL, "W1 must be > 0 (PAPER.md:94)");
   s = check_flags(h);
   if (s != WLR_OK) return s;
   h->p = 0;
