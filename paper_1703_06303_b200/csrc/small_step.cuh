@@ -733,29 +733,75 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
     int iY = 0, iZ = 1, iA = 2, iB = 3;        // roles of the four slice buffers
     int nprod = 0;
     // ---------------------------------------------- A: Gram update, G'^{-1}, C', slices
+    if (a.mode) {
+      // rounds of 4 M' elements, 2 G' elements and 2 each of Y, V_p, G^{-1}_p per thread: every
+      // load of a round is issued before its stores (the loops one after the other waited one
+      // L2 round trip each)
+      const int nM = k * s.nl, nY = s.nl * b, nV = s.nl * t;
+      for (int r0 = 0; r0 < nM || r0 < 2 * kk || r0 < 2 * nY; r0 += 4 * kSST) {
+        double mi[4], mn[4], gv[2][5], yv[2], vv[2], xv[2];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int idx = r0 + threadIdx.x + u * kSST;
+          const int q = idx / s.nl, i = idx - q * s.nl;
+          const int64_t gi = (int64_t)q * nk + s.rs + i;
+          mi[u] = idx < nM ? a.M_in[gi] : 0.0;
+          mn[u] = idx < nM ? incN[gi] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int idx = r0 / 2 + threadIdx.x + u * kSST;
+          const int i = idx / k, j = idx - i * k;
+          const bool in = idx < kk;
+          gv[u][0] = in ? a.G_in[idx] : 0.0;
+          gv[u][1] = in ? incGam[i * k + j] : 0.0;
+          gv[u][2] = in ? incGam[j * k + i] : 0.0;
+          gv[u][3] = in ? incOm[i * k + j] : 0.0;
+          gv[u][4] = in ? incOm[j * k + i] : 0.0;
+          xv[u] = in ? a.Gi_in[idx] : 0.0;
+          yv[u] = idx < nY ? a.Y[(int64_t)s.rs * b + idx] : 0.0;
+          vv[u] = idx < nV ? a.V_in[(int64_t)s.rs * t + idx] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int idx = r0 + threadIdx.x + u * kSST;
+          if (idx < nM) {
+            const int q = idx / s.nl, i = idx - q * s.nl;
+            const double mv = mi[u] + mn[u];
+            if (p.oMs >= 0) Ms[q * ldm + i] = mv;
+            a.M_out[(int64_t)q * nk + s.rs + i] = mv;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int idx = r0 / 2 + threadIdx.x + u * kSST;
+          if (idx < kk) {
+            const int i = idx / k, j = idx - i * k;
+            const double g = gv[u][0] + gv[u][1] + gv[u][2] + 0.5 * (gv[u][3] + gv[u][4]);
+            Gq[idx] = g;
+            Xq[idx] = xv[u];
+            if (s.c == 0) a.G_out[idx] = g;
+            if (s.c == 0 && i == j) sm[so.d0 + i] = gv[u][3];      // diag(Omega) for the gate below
+          }
+          if (idx < nY) s.sm[buf[iY] + idx] = yv[u];
+          if (idx < nV) Vp[idx] = vv[u];
+        }
+      }
+    } else {
     for (int idx = threadIdx.x; idx < k * s.nl; idx += kSST) {
       const int q = idx / s.nl, i = idx - q * s.nl;
       const int64_t gi = (int64_t)q * nk + s.rs + i;
-      const double mv = a.mode ? a.M_in[gi] + incN[gi] : a.M_out[gi];
+      const double mv = a.M_out[gi];
       if (p.oMs >= 0) Ms[q * ldm + i] = mv;
-      if (a.mode) a.M_out[gi] = mv;
     }
     for (int idx = threadIdx.x; idx < s.nl * b; idx += kSST) s.sm[buf[iY] + idx] = a.Y[(int64_t)s.rs * b + idx];
-    if (a.mode) {
-      for (int idx = threadIdx.x; idx < s.nl * t; idx += kSST) Vp[idx] = a.V_in[(int64_t)s.rs * t + idx];
-      for (int idx = threadIdx.x; idx < kk; idx += kSST) Xq[idx] = a.Gi_in[idx];
-    }
     for (int idx = threadIdx.x; idx < kk; idx += kSST) {
       const int i = idx / k, j = idx - i * k;
       double g;
-      if (a.mode) {
-        g = a.G_in[idx] + incGam[i * k + j] + incGam[j * k + i] + 0.5 * (incOm[i * k + j] + incOm[j * k + i]);
-        if (s.c == 0) a.G_out[idx] = g;
-        if (s.c == 0 && i == j) sm[so.d0 + i] = incOm[idx];   // diag(Omega) for the gate below
-      } else {
-        g = a.G_out[idx];
-      }
+      (void)i; (void)j;
+      g = a.G_out[idx];
       Gq[idx] = g;
+    }
     }
     __syncthreads();
     if (a.mode && s.c == 0 && threadIdx.x >= kSST - 32) {
