@@ -835,6 +835,9 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
         const int q = idx / s.nl, i = idx - q * s.nl;
         a.C_out[(int64_t)q * nk + s.rs + i] = Cs[q * ldc + i];
       }
+    // K^{-1}_p staged into the free Newton-Schulz scratch now (read at the first Gram exchange)
+    if (a.mode && a.uniform)
+      for (int idx = threadIdx.x; idx < kk; idx += kSST) Pq[idx] = a.Ki[idx];
     tmark(s, a);                               // [2] C'
 
     // ---------------------------------------------- B: eigenpairs of S
@@ -890,7 +893,7 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
               else reinterpret_cast<float*>(a.Kop)[idx] = (float)v;
             }
             Gq[idx] = v + (i == j ? a.w2 : 0.0);
-            if (a.mode && a.uniform) Xq[idx] = a.Ki[idx];
+            if (a.mode && a.uniform) Xq[idx] = Pq[idx];   // K^{-1}_p (staged after C')
           }
           __syncthreads();
         }
@@ -1002,7 +1005,11 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
           }
           part[j] = v;
         }
-        xreduce(s, p, t, rres);
+        // C'V' (k x t) partials ride along: valid at every exit of this loop (it only leaves
+        // right after this exchange), so the operands need no exchange of their own
+        const TN d[1] = {{Cs, ldc, 1, Y, 1, b, k, t, part + t}};
+        slice_tn<1>(s.nl, d);
+        xreduce(s, p, t, rres, kt, rres + t);
       }
       tmark(s, a);                             // residual exchange
       rmax = 0.0;
@@ -1058,18 +1065,14 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
     // Linear row update: Wt = [w^2 K^{-1}; U K^{-1}; P K^{-1}] for uniform W1,
     // [0; U; P] otherwise, with U = C'^T - V' (C'V')^T, P = (C'V')(C'V')^T, K = w^2 I + C'C'^T.
     const double* Y = s.sm + buf[iY];          // V' = Y[:, :t]
-    double* cvs = s.sm + p.oCinE;              // k x t (the residual region is free now)
-    {   // C'V' (k x t): slice partials, cluster sum
-      const TN d[1] = {{Cs, ldc, 1, Y, 1, b, k, t, xpart(s, p)}};
-      slice_tn<1>(s.nl, d);
-    }
+    double* cvs = rres + t;                    // k x t  C'V', summed with the last residuals
     for (int idx = threadIdx.x; idx < s.nl * t; idx += kSST) {
       const int r = idx / t, j = idx - r * t;
       a.V_out[(int64_t)(s.rs + r) * t + j] = Y[r * b + j];
     }
     for (int idx = threadIdx.x; idx < s.nl * b; idx += kSST) a.Y[(int64_t)s.rs * b + idx] = Y[idx];
     tmark(s, a);                               // operand partials
-    xreduce(s, p, kt, cvs);
+    tmark(s, a);                               // (C'V' came with the residual exchange)
     if (s.c == 0)
       for (int idx = threadIdx.x; idx < kt; idx += kSST) a.CV_out[idx] = cvs[idx];
     tmark(s, a);                               // [8a] C'V' summed
