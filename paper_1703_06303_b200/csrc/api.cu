@@ -109,6 +109,7 @@ struct wlr_ctx {
   bool tc_ok = false, tc_on = false;
   int tc_dbg = 0;                       // diagnostics only (WLR_TC_DBG)
   unsigned long long* tc_tstamp = nullptr;   // per-CTA timestamps (WLR_TC_DBG & 16)
+  unsigned long long* itc_tstamp = nullptr;  // increments, per CTA (WLR_TC_DBG & 32)
   int tc_grid = 0;
   int64_t tc_m_main = 0;       // rows covered by tensor-core tiles
   int tc_extra = 0;            // leftover rows per CTA on the CUDA cores (one CTA per SM)
@@ -409,6 +410,7 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int ph) {
       q.k = (int)h->k; q.k0 = (int)h->k0; q.nA32 = h->itc_nA32; q.nz = h->itc_nz;
       q.gate = h->flags + 5;
       q.cs = h->itc_cs;
+      q.tstamp = h->itc_tstamp;
       e = launch_incr_tc(q, h->itc_nsplit, h->st);
     }
   } else {
@@ -690,6 +692,11 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   // tensor-core row pass (uniform W1, fp32): K-major W'^T written by the small step
   h->tc_ok = h->dtype == WLR_F32 && h->uniform;
   if (const char* dbg = std::getenv("WLR_TC_DBG")) h->tc_dbg = std::atoi(dbg);
+  if (h->tc_dbg & 32) {
+    void* p = nullptr;
+    if ((s = dalloc(h, &p, 8 * 8 * 4096)) != WLR_OK) return s;
+    h->itc_tstamp = (unsigned long long*)p;
+  }
   if (h->tc_dbg & 16) {
     void* p = nullptr;
     if ((s = dalloc(h, &p, 8 * 8 * 2048)) != WLR_OK) return s;
@@ -1347,6 +1354,7 @@ extern "C" wlr_status wlr_debug_state(wlr_handle h, const char* name, double* ou
   else if (nm == "GA") { src = h->GA; cnt = h->nk * h->nk; }
   else if (nm == "scal") { src = h->scal; cnt = 8; }
   else if (nm == "ktime") { src = h->tdbg; cnt = 256; }
+  else if (nm == "itctime") { src = (const double*)h->itc_tstamp; cnt = h->itc_tstamp ? 8 * 4096 : 0; }
   else if (nm == "tctime") { src = (const double*)h->tc_tstamp; cnt = h->tc_tstamp ? 16 * h->tc_grid : 0; }
   else if (nm == "ktime_on" || nm == "ktime_off") {   // enable/disable K3 phase timestamps
     h->ktime = nm == "ktime_on";

@@ -37,11 +37,22 @@ constexpr int kItBT = 2 * 32 * 128;     // B operand slot: Delta^T hi | lo (64 r
 constexpr int kItSmem = kItNR * kItST + kItNL * kItBT;
 
 __global__ void __launch_bounds__(kItThreads, 2) incr_tc_kernel(const __grid_constant__ IncrTcArgs a) {
-  pdl_wait();                                     // the row pass
+  // Programmatic dependent launch behind the row pass: only the producer waits for it, and only
+  // before its Delta boxes -- the A and X1_p boxes of the first stages (not written by the row
+  // pass) are requested while the row pass is still finishing.  The gate was written by the small
+  // step before the row pass started.
   pdl_trigger();
   // gate: tensor cores once the X1 step is small; otherwise the same pipeline
   // feeds plain FP32 FMAs on the CUDA cores (fp32 sums over 32-row chunks, fp64 across chunks)
   const bool tc = *a.gate != 0;
+  auto stamp = [&](int i) {
+    if (a.tstamp) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      a.tstamp[((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * 8 + i] = t;
+    }
+  };
+  if (threadIdx.x == 0) stamp(0);
   extern __shared__ __align__(1024) unsigned char it_raw[];
   // 1024-aligned by pointer arithmetic on the shared array (an integer round trip would turn
   // every access through sm into a generic load)
@@ -71,21 +82,32 @@ __global__ void __launch_bounds__(kItThreads, 2) incr_tc_kernel(const __grid_con
 
   if (warp == 4) {
     if (lane == 0) {
-      int s = 0;
-      uint32_t ph = 0;
-      for (int ch = 0; ch < nch; ++ch) {
-        if (ch >= kItNR) mbar_wait(&rawfree[s], ph ^ 1);
+      // boxes of chunk ch in stage s: part 0 = A / X1_p (independent of the row pass), part 1 =
+      // Delta (written by the row pass)
+      auto issue = [&](int ch, int s, int part) {
         unsigned char* st = rawst + s * kItST;
         const int row = (int)(r0 + 32 * ch);
-        mbar_expect_tx(&full[s], (uint32_t)kItST);
+        if (part == 0) mbar_expect_tx(&full[s], (uint32_t)kItST);
         for (int b = 0; b < 4; ++b) {                      // Z column boxes
           const int zc = j0 + 32 * b;
+          const bool dpart = zc >= a.nA32 + 32;
+          if (dpart != (part == 1)) continue;
           if (zc < a.nA32) tma_load_2d(st + b * 4096, &a.tmA, &full[s], a.k0 + zc, row);
           else if (zc < a.nA32 + 32) tma_load_2d(st + b * 4096, &a.tmX, &full[s], 0, row);
-          else if (zc < a.nA32 + 64) tma_load_2d(st + b * 4096, &a.tmD, &full[s], 0, row);
-          else tma_load_2d(st + b * 4096, &a.tmD, &full[s], 0, row);   // beyond nz': ignored lanes
+          else tma_load_2d(st + b * 4096, &a.tmD, &full[s], 0, row);   // Delta (beyond nz': ignored lanes)
         }
-        tma_load_2d(st + kItZB, &a.tmD, &full[s], 0, row);
+        if (part == 1) tma_load_2d(st + kItZB, &a.tmD, &full[s], 0, row);
+      };
+      const int npre = nch < kItNR ? nch : kItNR;
+      for (int ch = 0; ch < npre; ++ch) issue(ch, ch, 0);
+      pdl_wait();                                          // the row pass: Delta is complete
+      for (int ch = 0; ch < npre; ++ch) issue(ch, ch, 1);
+      int s = npre == kItNR ? 0 : npre;
+      uint32_t ph = npre == kItNR ? 1 : 0;
+      for (int ch = npre; ch < nch; ++ch) {
+        if (ch >= kItNR) mbar_wait(&rawfree[s], ph ^ 1);
+        issue(ch, s, 0);
+        issue(ch, s, 1);
         if (++s == kItNR) { s = 0; ph ^= 1; }
       }
     }
@@ -152,6 +174,7 @@ __global__ void __launch_bounds__(kItThreads, 2) incr_tc_kernel(const __grid_con
     uint32_t phr = 0, phl = 0;
     for (int ch = 0; ch < nch; ++ch) {
       mbar_wait(&full[r], phr);
+      if (ch == 0 && tid == 0) stamp(1);
       if (ch >= kItNL) mbar_wait(&lofree[l], phl ^ 1);
       const unsigned char* st = rawst + r * kItST;
       {   // column c: box warp, 16-byte unit (lane / 4) ^ (row & 7), word lane % 4
@@ -201,8 +224,10 @@ __global__ void __launch_bounds__(kItThreads, 2) incr_tc_kernel(const __grid_con
   } else if (warp < 4) {
     const int c = tid;
     float v[32], v2[32];
+    if (tid == 0) stamp(2);                                // converters done
     if (nch > 0) {
       mbar_wait(&accfull, 0);
+      if (tid == 0) stamp(3);                              // accumulator complete
       tc_fence_after();
       tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16), v);
       tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + 32, v2);
@@ -248,6 +273,7 @@ __global__ void __launch_bounds__(kItThreads, 2) incr_tc_kernel(const __grid_con
     tc_fence_after();
     tmem_dealloc<256>(tmem);
   }
+  if (threadIdx.x == 0) stamp(4);
 }
 
 cudaError_t launch_incr_tc(const IncrTcArgs& a, int nsplit, cudaStream_t st) {

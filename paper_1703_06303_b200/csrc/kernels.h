@@ -125,6 +125,7 @@ struct IncrTcArgs {
   int cs;                           // row splits per thread-block cluster (DSMEM pre-reduction)
   int k, k0, nA32, nz;              // nz = nA32 + 64
   const int* gate;                  // runs only when *gate != 0 (set by the small step)
+  unsigned long long* tstamp;       // diagnostics (WLR_TC_DBG bit 32): 8 stamps per CTA, or nullptr
 };
 cudaError_t launch_incr_tc(const IncrTcArgs& a, int nsplit, cudaStream_t st);
 int incr_bm(int kp);
