@@ -683,7 +683,7 @@ WLR_DEVI void s_apply(SS& s, const SmallArgs& a, const double* Cs, int ldc, cons
 //          the library runs it on a second stream concurrently with them.
 template <int BT, int PART>
 __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_constant__ SmallArgs a) {
-  pdl_wait();                                  // part 1: the increments of the reduce kernel
+  if (PART != 1) pdl_wait();                   // (part 1 waits inside its first load round)
   constexpr int PW = BT <= 8 ? BT : (BT <= 16 ? (BT + 1) / 2 : (BT + 3) / 4);
   extern __shared__ __align__(16) double ss_smem[];
   __shared__ double red[8 * kSSW];
@@ -740,27 +740,39 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
       const int nM = k * s.nl, nY = s.nl * b, nV = s.nl * t;
       for (int r0 = 0; r0 < nM || r0 < 2 * kk || r0 < 2 * nY; r0 += 4 * kSST) {
         double mi[4], mn[4], gv[2][5], yv[2], vv[2], xv[2];
+        // the previous state first: it does not depend on the reduce kernel, so under programmatic
+        // dependent launch these loads overlap the reduce's tail
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int idx = r0 + threadIdx.x + u * kSST;
           const int q = idx / s.nl, i = idx - q * s.nl;
-          const int64_t gi = (int64_t)q * nk + s.rs + i;
-          mi[u] = idx < nM ? a.M_in[gi] : 0.0;
-          mn[u] = idx < nM ? incN[gi] : 0.0;
+          mi[u] = idx < nM ? a.M_in[(int64_t)q * nk + s.rs + i] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int idx = r0 / 2 + threadIdx.x + u * kSST;
+          const bool in = idx < kk;
+          gv[u][0] = in ? a.G_in[idx] : 0.0;
+          xv[u] = in ? a.Gi_in[idx] : 0.0;
+          yv[u] = idx < nY ? a.Y[(int64_t)s.rs * b + idx] : 0.0;
+          vv[u] = idx < nV ? a.V_in[(int64_t)s.rs * t + idx] : 0.0;
+        }
+        pdl_wait();                                          // the increments of the reduce kernel
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int idx = r0 + threadIdx.x + u * kSST;
+          const int q = idx / s.nl, i = idx - q * s.nl;
+          mn[u] = idx < nM ? incN[(int64_t)q * nk + s.rs + i] : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
           const int idx = r0 / 2 + threadIdx.x + u * kSST;
           const int i = idx / k, j = idx - i * k;
           const bool in = idx < kk;
-          gv[u][0] = in ? a.G_in[idx] : 0.0;
           gv[u][1] = in ? incGam[i * k + j] : 0.0;
           gv[u][2] = in ? incGam[j * k + i] : 0.0;
           gv[u][3] = in ? incOm[i * k + j] : 0.0;
           gv[u][4] = in ? incOm[j * k + i] : 0.0;
-          xv[u] = in ? a.Gi_in[idx] : 0.0;
-          yv[u] = idx < nY ? a.Y[(int64_t)s.rs * b + idx] : 0.0;
-          vv[u] = idx < nV ? a.V_in[(int64_t)s.rs * t + idx] : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -788,6 +800,7 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
         }
       }
     } else {
+    pdl_wait();
     for (int idx = threadIdx.x; idx < k * s.nl; idx += kSST) {
       const int q = idx / s.nl, i = idx - q * s.nl;
       const int64_t gi = (int64_t)q * nk + s.rs + i;
