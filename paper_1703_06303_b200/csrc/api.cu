@@ -919,8 +919,8 @@ extern "C" wlr_status wlr_init(wlr_handle* out, const void* A, int64_t lda, cons
   wlr_ctx* h = new wlr_ctx();
   h->opts = op;
   // eigensolver target (relative to lambda_1; the S-product rounding floor is added in K3):
-  // fp64 mode 1e-12, fp32 mode 3e-8 (DESIGN.md §3 reading R17 "eigensolver tolerance")
-  if (h->opts.eig_tol <= 0.0) h->opts.eig_tol = op.dtype == WLR_F64 ? 1e-12 : 3e-8;
+  // fp64 mode 1e-12, fp32 mode 1e-7 (DESIGN.md §3 reading R17 "eigensolver tolerance")
+  if (h->opts.eig_tol <= 0.0) h->opts.eig_tol = op.dtype == WLR_F64 ? 1e-12 : 1e-7;
   if (h->opts.eig_max_outer <= 0) h->opts.eig_max_outer = 60;
   h->m = m_local; h->n = n; h->k = k; h->r = r; h->t = r - k; h->nk = n - k;
   h->kp = round_up(k, 4); h->k0 = k & ~3LL;
