@@ -535,13 +535,13 @@ template <int PW>
 WLR_DEVI void s_product_impl(double* smb, int rs, int nl, int SL, int k, int nk, int KS, int JS,
                               int64_t oRed, int64_t oXf, const double* GA, int64_t xoff, int ldx,
                               int w, const double* Wk, const double* Mp, int ldm, double* Z,
-                              int ldz, SS* ms = nullptr, const SmallArgs* ma = nullptr) {
+                              int ldz, SS* ms = nullptr, const SmallArgs* ma = nullptr, bool pre = false) {
   struct { int rs, nl, SL, k, nk; double* sm; } s = {rs, nl, SL, k, nk, smb};
   struct { int KS, JS; } p = {KS, JS};
   cg::cluster_group cl = cg::this_cluster();
   double* Red = s.sm + oRed;
   double* Xf = oXf >= 0 ? s.sm + oXf : nullptr;
-  if (Xf) {
+  if (Xf && !pre) {   // (pre: Xf already holds the whole basis, loaded from global)
     #pragma unroll 1
     for (int idx0 = threadIdx.x; idx0 < s.nk * w; idx0 += 4 * kSST) {
       double v[4];
@@ -650,16 +650,16 @@ WLR_DEVI void s_product_impl(double* smb, int rs, int nl, int SL, int k, int nk,
 
 template <int PW>
 WLR_DEVI void s_product(SS& s, const SmallArgs& a, int64_t xoff, int ldx, int w,
-                        const double* Wk, const double* Mp, int ldm, double* Z, int ldz) {
+                        const double* Wk, const double* Mp, int ldm, double* Z, int ldz, bool pre = false) {
   s_product_impl<PW>(s.sm, s.rs, s.nl, s.SL, s.k, s.nk, a.pl.KS, a.pl.JS, a.pl.oRed, a.pl.oXf,
-                     a.GA, xoff, ldx, w, Wk, Mp, ldm, Z, ldz, &s, &a);
+                     a.GA, xoff, ldx, w, Wk, Mp, ldm, Z, ldz, &s, &a, pre);
 }
 
 // One S-product of the basis X (local slice at offset xoff, width w = row stride):
 // exchange of the C' X partials, then the distributed product into Z (local offset).
 template <int PW>
 WLR_DEVI void s_apply(SS& s, const SmallArgs& a, const double* Cs, int ldc, const double* Ms,
-                      int ldm, int64_t xoff, int w, int64_t zoff, int* nprod) {
+                      int ldm, int64_t xoff, int w, int64_t zoff, int* nprod, bool pre = false) {
   const SSPlan& p = a.pl;
   const double* X = s.sm + xoff;
   double* part = xpart(s, p);
@@ -669,7 +669,7 @@ WLR_DEVI void s_apply(SS& s, const SmallArgs& a, const double* Cs, int ldc, cons
   double* Wk = s.sm + p.oWk;
   xreduce(s, p, s.k * w, Wk);
   tmark(s, a);                                 // [p2] C X exchange
-  s_product<PW>(s, a, xoff, w, w, Wk, Ms, ldm, s.sm + zoff, w);
+  s_product<PW>(s, a, xoff, w, w, Wk, Ms, ldm, s.sm + zoff, w, pre);
   ++*nprod;
 }
 
@@ -733,11 +733,29 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
     int iY = 0, iZ = 1, iA = 2, iB = 3;        // roles of the four slice buffers
     int nprod = 0;
     // ---------------------------------------------- A: Gram update, G'^{-1}, C', slices
+    const bool xf_pre = a.mode && p.oXf >= 0;  // first S-product's operand loaded with the state
     if (a.mode) {
       // rounds of 4 M' elements, 2 G' elements and 2 each of Y, V_p, G^{-1}_p per thread: every
       // load of a round is issued before its stores (the loops one after the other waited one
       // L2 round trip each)
       const int nM = k * s.nl, nY = s.nl * b, nV = s.nl * t;
+      if (xf_pre) {   // the whole warm block Y (n-k x b) into the S-product's gathered operand
+        double* Xf = s.sm + p.oXf;
+        const int nX = nk * b;
+        for (int r0 = 0; r0 < nX; r0 += 8 * kSST) {
+          double v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int idx = r0 + threadIdx.x + u * kSST;
+            v[u] = idx < nX ? a.Y[idx] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int idx = r0 + threadIdx.x + u * kSST;
+            if (idx < nX) Xf[idx] = v[u];
+          }
+        }
+      }
       for (int r0 = 0; r0 < nM || r0 < 2 * kk || r0 < 2 * nY; r0 += 4 * kSST) {
         double mi[4], mn[4], gv[2][5], yv[2], vv[2], xv[2];
         // the previous state first: it does not depend on the reduce kernel, so under programmatic
@@ -863,7 +881,7 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
     bool ortho = !a.cold;                      // Y expected orthonormal (warm Ritz block)
     while (true) {
       // ---- Rayleigh-Ritz on span(Y):  Z = S Y;  Gyy = Y^T Y, Gyz = Y^T Z (generalised RR)
-      s_apply<PW>(s, a, Cs, ldc, Ms, ldm, buf[iY], b, buf[iZ], &nprod);
+      s_apply<PW>(s, a, Cs, ldc, Ms, ldm, buf[iY], b, buf[iZ], &nprod, xf_pre && outer == 0);
       tmark(s, a);                             // product
       {
         const double* Y = s.sm + buf[iY];
