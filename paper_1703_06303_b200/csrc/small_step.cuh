@@ -1302,13 +1302,40 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
     const FinOff fo(k, t);
     double* my = a.xchg + (int64_t)s.c * p.flen;
     {
-      // [0] <M',C'> [1] <C', H C_in> [2] <C', Om C'> [3] <C', Gam dC> [4] <dC, G dC>
+      // [0] <M',C'> [1] <C', H C_in> [2] <C', Om C'> [3] <C', Gam dC> [4] <dC, G dC>, the last
+      // four through k x k slice Grams (FP64 tensor cores): <X, Y Z> over the slice =
+      // sum_{l,q} Y[l][q] (X Z^T)[l][q] with X Z^T = C' C_in^T, C' C'^T, C' dC^T, dC dC^T
       double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
       for (int idx = threadIdx.x; idx < k * s.nl; idx += kSST) {
         const int l = idx / s.nl, i = idx - l * s.nl;
-        const double cn = Cs[(int64_t)l * ldc + i];
-        v[0] = fma(Ms[(int64_t)l * ldm + i], cn, v[0]);
-        if (a.mode) {
+        v[0] = fma(Ms[(int64_t)l * ldm + i], Cs[(int64_t)l * ldc + i], v[0]);
+      }
+      if (a.mode && 4 * kk <= 6 * 1024) {
+        double* dC = s.sm + p.oRed;              // k x nl (the S-product's partials are consumed)
+        for (int idx = threadIdx.x; idx < k * s.nl; idx += kSST) {
+          const int l = idx / s.nl, i = idx - l * s.nl;
+          dC[idx] = Cs[(int64_t)l * ldc + i] - Cin[(int64_t)l * ldci + i];
+        }
+        __syncthreads();
+        double* gr = sm + so.Tb;                  // 4 x k x k (the local RR blocks are free here)
+        const TN d[4] = {{Cs, ldc, 1, Cin, ldci, 1, k, k, gr},
+                         {Cs, ldc, 1, Cs, ldc, 1, k, k, gr + kk},
+                         {Cs, ldc, 1, dC, s.nl, 1, k, k, gr + 2 * kk},
+                         {dC, s.nl, 1, dC, s.nl, 1, k, k, gr + 3 * kk}};
+        slice_tn<4>(s.nl, d);
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < kk; idx += kSST) {
+          const int l = idx / k, q = idx - l * k;
+          const double gm = Gm[idx], gam = Gam[idx];
+          v[1] = fma(gm + gam, gr[idx], v[1]);
+          v[2] = fma(0.5 * (Om[idx] + Om[q * k + l]), gr[kk + idx], v[2]);
+          v[3] = fma(gam, gr[2 * kk + idx], v[3]);
+          v[4] = fma(gm, gr[3 * kk + idx], v[4]);
+        }
+      } else if (a.mode) {   // k > 39: the k x k Grams do not fit the scratch; per-element sums
+        for (int idx = threadIdx.x; idx < k * s.nl; idx += kSST) {
+          const int l = idx / s.nl, i = idx - l * s.nl;
+          const double cn = Cs[(int64_t)l * ldc + i];
           double hc = 0.0, omc = 0.0, gdc = 0.0, ggdc = 0.0;
           for (int q = 0; q < k; ++q) {
             const double co = Cin[(int64_t)q * ldci + i], cq = Cs[(int64_t)q * ldc + i];
