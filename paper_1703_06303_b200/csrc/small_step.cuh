@@ -1403,10 +1403,21 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
     double* ZnV = sm + so.Tb;                  // t x t
     if (threadIdx.x < t * t && a.mode) ZnV[threadIdx.x] = a.k3x[t * t + threadIdx.x];
     __syncthreads();
-    double sum_theta = 0.0;
-    for (int j = 0; j < t; ++j) sum_theta += a.th_out[j];
-    double trG = 0.0;
-    for (int i = 0; i < k; ++i) trG += a.G_out[i * k + i];
+    // sum of the Ritz values, tr(G'), tr(Omega): one warp, lanes over the index (a serial loop
+    // of dependent global loads per thread cost several microseconds here)
+    __shared__ double tr3[3];
+    if (threadIdx.x < 32) {
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+      for (int j = threadIdx.x; j < t; j += 32) s0 += a.th_out[j];
+      for (int i = threadIdx.x; i < k; i += 32) {
+        s1 += a.G_out[i * k + i];
+        if (a.mode) s2 += Om[i * k + i];
+      }
+      s0 = warp_sum(s0); s1 = warp_sum(s1); s2 = warp_sum(s2);
+      if (threadIdx.x == 0) { tr3[0] = s0; tr3[1] = s1; tr3[2] = s2; }
+    }
+    __syncthreads();
+    const double sum_theta = tr3[0], trG = tr3[1];
     const double x2sq_new = R[0] + sum_theta;
     const double F = fw + a.a2sq - R[0] - sum_theta;
     double step = -1.0, rel = -1.0;
@@ -1463,8 +1474,7 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
       }
       block_sum_n<2>(v, red);
       const double cross = R[1] + v[0];
-      double trOm = 0.0;
-      for (int i = 0; i < k; ++i) trOm += Om[i * k + i];
+      const double trOm = tr3[2];
       const double x2sq_old = a.scal[0], xn2_old = a.scal[1];
       const double st2_big = trOm + x2sq_new + x2sq_old - 2.0 * cross;
       const double st2_small = trOm + R[2] + 2.0 * R[3] + R[4] + v[1];
