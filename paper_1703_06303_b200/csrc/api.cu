@@ -278,6 +278,9 @@ static void set_prefetch(wlr_ctx* h, int ph, const void** ptr, int64_t* bytes) {
   ptr[3] = h->Y;        bytes[3] = nk * h->b * 8;
   ptr[4] = h->V[cur];   bytes[4] = nk * h->t * 8;
   ptr[5] = h->Gi[cur];  bytes[5] = k * k * 8;
+  // (prefetching K3b(p-1)'s inputs too -- previous state slot, last increments -- shortened K3b
+  // by ~8 us but slowed the critical K3a by ~2 us: measured and left out)
+  for (int i = 6; i < kPf; ++i) { ptr[i] = nullptr; bytes[i] = 0; }
 }
 
 // Small-step arguments of iteration p (phase ph = p mod 6): state slot p mod 3 -> (p+1) mod 3,
@@ -358,7 +361,7 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int ph) {
       q.tmA = h->tmA_tc; q.tmX = h->tmX_tc[cur]; q.tmW = h->tmWT;
       q.A = a.A; q.lda = a.lda; q.Xold = a.Xold; q.Xnew = a.Xnew; q.Dnew = a.Dnew;
       q.w2s = a.w2s; q.fw_part = h->fw_part;
-      for (int i = 0; i < 6; ++i) { q.pf_ptr[i] = a.pf_ptr[i]; q.pf_bytes[i] = a.pf_bytes[i]; }
+      for (int i = 0; i < kPf; ++i) { q.pf_ptr[i] = a.pf_ptr[i]; q.pf_bytes[i] = a.pf_bytes[i]; }
       q.m = h->m; q.KA = h->KA; q.k = (int)h->k; q.kp = (int)h->kp; q.n = (int)h->n;
       q.m_main = h->tc_m_main; q.extra = h->tc_extra;
       q.tmAx = h->tmA_x; q.tmXx = h->tmX_x[cur];

@@ -23,6 +23,7 @@ void launch_validate(const T* A, int64_t lda, int64_t m, int n, const T* W1, int
                      int* flags, cudaStream_t st);
 
 // ---------------------------------------------------------------- row pass (rowpass.cu)
+constexpr int kPf = 12;             // L2 prefetch slots of the row pass (see api.cu set_prefetch)
 template <typename T>
 struct RowPassArgs {
   // TMA tensor maps (SWIZZLE_128B for A and X1_p boxes of 128 B x BM rows; Wt plain)
@@ -46,7 +47,7 @@ struct RowPassArgs {
   T* Ebuf;                          // non-uniform: write e rows here and skip the per-row solve
   double* fw_part;                  // gridDim.x partials
   int* flags;
-  const void* pf_ptr[6]; int64_t pf_bytes[6];   // L2 prefetch of the next small step's inputs
+  const void* pf_ptr[kPf]; int64_t pf_bytes[kPf];   // L2 prefetch of the next small steps' inputs
   int64_t m; int n, k, kp, no;      // no = output columns (kp, or t for MODE_RESULT)
   int vec_ok;                       // A rows 16-byte aligned at multiples of 4 elements
 };
@@ -71,7 +72,7 @@ struct RowPassTcArgs {
   const float* Xold; float* Xnew; float* Dnew;   // m x kp
   float w2s;
   double* fw_part;                  // gridDim.x partials of f_w
-  const void* pf_ptr[6]; int64_t pf_bytes[6];
+  const void* pf_ptr[kPf]; int64_t pf_bytes[kPf];
   int64_t m; int KA, k, kp, n;
   // tiles cover rows [0, m_main); with extra > 0 (one CTA per SM, one tile each) CTA i also
   // computes the rows m_main + extra i + e, e < extra, on the CUDA cores (no tail wave)

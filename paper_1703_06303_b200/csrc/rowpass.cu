@@ -189,7 +189,7 @@ row_pass_kernel(const __grid_constant__ RowPassArgs<T> a) {
   // The small step that follows is latency-bound and reads G_A and its previous state:
   // pull them into L2 while this pass streams A (bulk L2 prefetch, 64 KB per request).
   if (MODE == 0 && threadIdx.x < 32) {
-    for (int r = 0; r < 6; ++r) {
+    for (int r = 0; r < kPf; ++r) {
       const char* base = reinterpret_cast<const char*>(a.pf_ptr[r]);
       const int64_t nb = a.pf_bytes[r] & ~(int64_t)15;
       if (!base || nb <= 0) continue;

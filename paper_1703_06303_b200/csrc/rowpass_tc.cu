@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(tc_threads<NR>(), NR >= 8 ? 1 : 2) row_pass_tc
     if (lane == 0) wsum[warp] = fw;
     if (warp == 0) {   // the small step that follows reads these: pull them into L2 (not earlier:
                        // bulk prefetches queue behind this CTA's first TMA loads)
-      for (int r = 0; r < 6; ++r) {
+      for (int r = 0; r < kPf; ++r) {
         const char* base = reinterpret_cast<const char*>(a.pf_ptr[r]);
         const int64_t nb = a.pf_bytes[r] & ~(int64_t)15;
         if (!base || nb <= 0) continue;
