@@ -150,6 +150,12 @@ struct wlr_ctx {
   int ph = 0;                  // phase of the current state (= p mod 6: X by p mod 2, state by p mod 3)
   int64_t p = 0;               // index of the current canonical state
   AlsSt* als = nullptr;        // f3 block ALS (consumes the sWLR state)
+  // row-pass timing inside the graph (wlr_debug_state "rptime_on"): external event records around
+  // the row pass only, read after each graph launch (bench.py's roofline pass)
+  bool rp_time = false;
+  cudaEvent_t rp_ev[2] = {};
+  double rp_ms = 0.0;
+  int64_t rp_n = 0;
   cudaGraphExec_t gexec[6][2] = {};   // [phase][deferred pending]
   cudaStream_t st2 = nullptr;  // side stream of the deferred small-step half
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -343,6 +349,8 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int ph) {
     for (int i = 0; i < 8; ++i) ev[i] = prof_event(h);
     cudaEventRecord(ev[0], h->st);
   }
+  const bool rpt = h->rp_time && !prof;
+  if (rpt) CUDA_TRY(h, cudaEventRecordWithFlags(h->rp_ev[0], h->st, cudaEventRecordExternal));
   cudaError_t e;
   if (h->dtype == WLR_F32) {
     RowPassArgs<float> a{};
@@ -394,6 +402,7 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int ph) {
   }
   if (e != cudaSuccess) return fail(h, WLR_ECUDA, std::string("row pass: ") + cudaGetErrorString(e));
   if (prof) cudaEventRecord(ev[1], h->st);
+  if (rpt) CUDA_TRY(h, cudaEventRecordWithFlags(h->rp_ev[1], h->st, cudaEventRecordExternal));
   if (h->dtype == WLR_F32) {
     IncrArgs<float> a{};
     a.A = (const float*)h->A; a.lda = h->lda;
@@ -502,6 +511,13 @@ static wlr_status launch_iteration(wlr_ctx* h) {
       if (s != WLR_OK) return s;
     }
     CUDA_TRY(h, cudaGraphLaunch(h->gexec[h->ph][pend], h->st));
+    if (h->rp_time) {   // (timing pass only: one host synchronisation per iteration)
+      CUDA_TRY(h, cudaEventSynchronize(h->rp_ev[1]));
+      float ms = 0.f;
+      CUDA_TRY(h, cudaEventElapsedTime(&ms, h->rp_ev[0], h->rp_ev[1]));
+      h->rp_ms += ms;
+      h->rp_n++;
+    }
     h->pend = small_args(h, h->ph, 1);
     h->pending = true;
     h->pr.launches += pend ? 5 : 4;
@@ -1357,6 +1373,25 @@ extern "C" wlr_status wlr_debug_state(wlr_handle h, const char* name, double* ou
   else if (nm == "GA") { src = h->GA; cnt = h->nk * h->nk; }
   else if (nm == "scal") { src = h->scal; cnt = 8; }
   else if (nm == "ktime") { src = h->tdbg; cnt = 256; }
+  else if (nm == "rptime_on" || nm == "rptime_off") {   // row-pass events inside the graph
+    h->rp_time = nm == "rptime_on";
+    if (h->rp_time && !h->rp_ev[0]) {
+      CUDA_TRY(h, cudaEventCreate(&h->rp_ev[0]));
+      CUDA_TRY(h, cudaEventCreate(&h->rp_ev[1]));
+    }
+    h->rp_ms = 0.0;
+    h->rp_n = 0;
+    for (auto& gp : h->gexec)
+      for (auto& g : gp)
+        if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+    if (count) *count = 0;
+    return WLR_OK;
+  }
+  else if (nm == "rptime") {
+    if (out && cap >= 2) { out[0] = h->rp_ms; out[1] = (double)h->rp_n; }
+    if (count) *count = 2;
+    return WLR_OK;
+  }
   else if (nm == "itctime") { src = (const double*)h->itc_tstamp; cnt = h->itc_tstamp ? 8 * 4096 : 0; }
   else if (nm == "tctime") { src = (const double*)h->tc_tstamp; cnt = h->tc_tstamp ? 16 * h->tc_grid : 0; }
   else if (nm == "ktime_on" || nm == "ktime_off") {   // enable/disable K3 phase timestamps
@@ -1479,6 +1514,7 @@ extern "C" void wlr_destroy(wlr_handle h) {
   if (h->st2) { cudaStreamSynchronize(h->st2); cudaStreamDestroy(h->st2); }
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
+  for (auto ev : h->rp_ev) if (ev) cudaEventDestroy(ev);
   if (h->own_stream && h->st) cudaStreamDestroy(h->st);
   delete h->als;
   delete h;
