@@ -1269,16 +1269,45 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
     const double* Gam = ms3 ? mats + kk : incGam;
     const double* Om = ms3 ? mats + 2 * kk : incOm;
     const double* CVp = ms3 ? mats + 3 * kk : a.CV_in;
-    for (int idx = threadIdx.x; idx < k * s.nl; idx += kSST) {
-      const int q = idx / s.nl, i = idx - q * s.nl;
-      const int64_t gi = (int64_t)q * nk + s.rs + i;
-      if (p.oCs >= 0) Cs[q * ldc + i] = a.C_out[gi];
-      if (p.oMs >= 0) Ms[q * ldm + i] = a.M_out[gi];
-      if (p.oCin >= 0 && a.mode) s.sm[p.oCin + q * ldci + i] = a.C_in[gi];
+    // slices of C', M', C_in and V', V_p in rounds: every load of a round before its stores
+    for (int r0 = 0; r0 < k * s.nl; r0 += 4 * kSST) {
+      double cv[4], mv[4], ci[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int idx = r0 + threadIdx.x + u * kSST;
+        const int q = idx / s.nl, i = idx - q * s.nl;
+        const int64_t gi = (int64_t)q * nk + s.rs + i;
+        const bool in = idx < k * s.nl;
+        cv[u] = in && p.oCs >= 0 ? a.C_out[gi] : 0.0;
+        mv[u] = in && p.oMs >= 0 ? a.M_out[gi] : 0.0;
+        ci[u] = in && p.oCin >= 0 && a.mode ? a.C_in[gi] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int idx = r0 + threadIdx.x + u * kSST;
+        if (idx >= k * s.nl) continue;
+        const int q = idx / s.nl, i = idx - q * s.nl;
+        if (p.oCs >= 0) Cs[q * ldc + i] = cv[u];
+        if (p.oMs >= 0) Ms[q * ldm + i] = mv[u];
+        if (p.oCin >= 0 && a.mode) s.sm[p.oCin + q * ldci + i] = ci[u];
+      }
     }
-    for (int idx = threadIdx.x; idx < s.nl * t; idx += kSST) {
-      Vn[idx] = a.V_out[(int64_t)s.rs * t + idx];
-      if (a.mode) Vp[idx] = a.V_in[(int64_t)s.rs * t + idx];
+    for (int r0 = 0; r0 < s.nl * t; r0 += 2 * kSST) {
+      double vn[2], vp[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int idx = r0 + threadIdx.x + u * kSST;
+        const bool in = idx < s.nl * t;
+        vn[u] = in ? a.V_out[(int64_t)s.rs * t + idx] : 0.0;
+        vp[u] = in && a.mode ? a.V_in[(int64_t)s.rs * t + idx] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int idx = r0 + threadIdx.x + u * kSST;
+        if (idx >= s.nl * t) continue;
+        Vn[idx] = vn[u];
+        if (a.mode) Vp[idx] = vp[u];
+      }
     }
     if (threadIdx.x < t * t && a.mode) Rt[threadIdx.x] = a.k3x[threadIdx.x];
     __syncthreads();
