@@ -858,17 +858,31 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
       for (int idx = threadIdx.x; idx < kk; idx += kSST) a.Gi_out[idx] = Xq[idx];
     if (threadIdx.x == 0) kok_s = 0;
     tmark(s, a);                               // [1] Gram update + G'^{-1}
+    // K^{-1}_p (read at the first Gram exchange): its loads are issued before the C' product and
+    // stored into the free Newton-Schulz scratch after it
+    const bool ki_stage = a.mode && a.uniform;
+    double kiv[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int idx = threadIdx.x + u * kSST;
+      kiv[u] = ki_stage && idx < kk ? a.Ki[idx] : 0.0;
+    }
     // C'[:, slice] = G'^{-1} M'[:, slice]
     gemm_nn(k, s.nl, k, Xq, k, Ms, ldm, Cs, ldc, 1.0, false);
+    if (ki_stage) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int idx = threadIdx.x + u * kSST;
+        if (idx < kk) Pq[idx] = kiv[u];
+      }
+      for (int idx = threadIdx.x + 2 * kSST; idx < kk; idx += kSST) Pq[idx] = a.Ki[idx];   // k > 32
+    }
     __syncthreads();
     if (p.oCs >= 0)
       for (int idx = threadIdx.x; idx < k * s.nl; idx += kSST) {
         const int q = idx / s.nl, i = idx - q * s.nl;
         a.C_out[(int64_t)q * nk + s.rs + i] = Cs[q * ldc + i];
       }
-    // K^{-1}_p staged into the free Newton-Schulz scratch now (read at the first Gram exchange)
-    if (a.mode && a.uniform)
-      for (int idx = threadIdx.x; idx < kk; idx += kSST) Pq[idx] = a.Ki[idx];
     tmark(s, a);                               // [2] C'
 
     // ---------------------------------------------- B: eigenpairs of S
