@@ -577,7 +577,10 @@ WLR_DEVI void s_product_impl(double* smb, int rs, int nl, int SL, int k, int nk,
   if (wj > 0) {
     const double* gcol = GA + s.rs;
     const int lg = min(l1, s.nk);
-    constexpr int U = 8;                          // G_A loads in flight per lane
+#ifndef WLR_SP_U
+#define WLR_SP_U 8
+#endif
+    constexpr int U = WLR_SP_U;                   // G_A loads in flight per lane (per row half)
     #pragma unroll 1
     for (int lb = l0; lb < lg; lb += U) {
       double g0[U], g1[U];
