@@ -1,6 +1,8 @@
 // small_step.cu -- host side of K3: shared-memory plan, cluster-size choice and dispatch of
 // the cluster kernel (templates in small_step.cuh, one translation unit per eigen-block
 // width BT so the build parallelises).
+#include <cstdlib>
+
 #include "small_step.cuh"
 
 namespace wlr {
@@ -85,7 +87,8 @@ bool small_step_plan(SmallArgs& a, int CL) { return plan_once(a, CL, 1) || plan_
 // which the device can co-schedule.
 int small_step_cluster_size(SmallArgs& a) {
   const int lo = (int)std::max<int64_t>(1, ceil_div(a.nk, 64));
-  const int want = (int)std::max<int64_t>(lo, std::min<int64_t>(16, ceil_div(a.nk, 24)));
+  int want = (int)std::max<int64_t>(lo, std::min<int64_t>(16, ceil_div(a.nk, 24)));
+  if (const char* e = std::getenv("WLR_K3_CL")) want = std::max(lo, std::min(16, std::atoi(e)));   // (A/B)
   for (int CL = want; CL >= lo; --CL) {
     if (!small_step_plan(a, CL)) continue;
     if (max_clusters(bt_of(a.b), CL, (size_t)a.pl.total * 8) >= 1) return CL;
