@@ -732,10 +732,14 @@ __global__ void reduce_incr_kernel(const double* __restrict__ part, int nsplit, 
   const int64_t nN = (int64_t)k * nk, nG = (int64_t)k * gk, nO = (int64_t)k * k;
   const int64_t tot = nN + nG + nO;
   const int64_t stride = (int64_t)k * nz;
-  const int g = threadIdx.x & 7;
-  const int64_t per_block = blockDim.x / 8;
+#ifndef WLR_RED_L
+#define WLR_RED_L 4
+#endif
+  constexpr int RL = WLR_RED_L;          // lanes per output (2 .. 16; same-box A/B: 4 best)
+  const int g = threadIdx.x & (RL - 1);
+  const int64_t per_block = blockDim.x / RL;
   for (int64_t i0 = blockIdx.x * per_block; i0 < tot; i0 += (int64_t)gridDim.x * per_block) {
-    const int64_t i = i0 + threadIdx.x / 8;
+    const int64_t i = i0 + threadIdx.x / RL;
     double s = 0.0;
     if (i < tot) {
       int l, zc;
@@ -744,11 +748,11 @@ __global__ void reduce_incr_kernel(const double* __restrict__ part, int nsplit, 
       else { const int64_t q = i - nN - nG; l = (int)(q / k); zc = nA + kp + (int)(q % k); }
       const double* src = part + (int64_t)l * nz + zc;
       // batches of 8 splits per lane (64 per output), every load of a batch in flight at once
-      for (int p0 = 0; p0 < nsplit; p0 += 64) {
+      for (int p0 = 0; p0 < nsplit; p0 += 8 * RL) {
         double v[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const int p = p0 + g + 8 * j;
+          const int p = p0 + g + RL * j;
           v[j] = p < nsplit ? __ldg(src + (int64_t)p * stride) : 0.0;
         }
 #pragma unroll
@@ -757,7 +761,8 @@ __global__ void reduce_incr_kernel(const double* __restrict__ part, int nsplit, 
     }
     s += __shfl_xor_sync(0xffffffffu, s, 1);
     s += __shfl_xor_sync(0xffffffffu, s, 2);
-    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    if (RL >= 8) s += __shfl_xor_sync(0xffffffffu, s, 4);
+    if (RL >= 16) s += __shfl_xor_sync(0xffffffffu, s, 8);
     if (g == 0 && i < tot) inc[i] = s;
   }
   if (blockIdx.x == 0 && threadIdx.x < 32) {
@@ -773,7 +778,7 @@ void launch_reduce_incr(const double* part, int nsplit, int k, int nk, int nz, i
                         const int* gate, ReduceLayout alt, bool pdl, int gk) {
   if (gk < 0) gk = k;
   const int64_t tot = (int64_t)k * nk + (int64_t)k * gk + (int64_t)k * k;
-  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(tot, 32), 4096));
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(tot, (int64_t)(256 / WLR_RED_L)), 4096));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(blocks);
   cfg.blockDim = dim3(256);
