@@ -65,14 +65,18 @@ typedef struct {
   double w1_scalar;       /* used iff W1 == NULL: uniform weight value (> 0)             */
   double eps;             /* stopping threshold: stop when Error_p < eps or
                              Error_p/||X_p||_F < eps.  0 = run the requested count.      */
-  double eig_tol;         /* eigensolver relative residual target (0 -> 1e-11)          */
-  int32_t eig_block;      /* eigensolver block width b >= r-k (0 -> 2(r-k), min r-k+2)   */
+  double eig_tol;         /* eigensolver relative residual target, relative to lambda_1
+                             (0 -> 1e-12 for WLR_F64, 1e-7 for WLR_F32; R17)   */
+  int32_t eig_block;      /* eigensolver block width b >= r-k (0 -> r-k+2 when r-k <= 4,
+                             else r-k+6; capped at min(32, n-k))                         */
   int32_t eig_max_outer;  /* eigensolver restart budget per (C,D) step (0 -> 60; init x4)*/
   int64_t m_global;       /* total rows over all ranks (0 -> m_local)                    */
   int64_t row_offset;     /* first global row owned by this rank                          */
   int32_t nranks, rank;   /* row sharding over ranks (1, 0 for single GPU)                */
   const void* nccl_id;    /* 128-byte ncclUniqueId shared by all ranks (NULL if nranks==1)*/
-  void* stream;           /* cudaStream_t for all work; NULL = a stream owned by the handle*/
+  void* stream;           /* cudaStream_t for all work; NULL = a BLOCKING stream owned by
+                             the handle (ordered after the legacy default stream).  With a
+                             caller stream, the caller orders device inputs before wlr_init. */
   int32_t use_graph;      /* 1: replay each iteration as a captured CUDA graph (default)  */
   int32_t seed;           /* seed of the eigensolver's cold-start block (host PCG)        */
 } wlr_opts;
@@ -127,7 +131,8 @@ wlr_status wlr_result(wlr_handle h, void* X1, int64_t ldx1, void* C, void* B, in
  * D_p := B_p D_p, then C, B and D by least squares.  Runs n_iters sweeps on the handle's stream
  * and copies the objectives F_0 .. F_N of all states so far (up to cap doubles) into F (host or
  * device).  With F = NULL the call only enqueues the sweeps (no host synchronisation; errors
- * surface at the next wlr_sync).  Single rank only.  The sWLR state is consumed: wlr_iterate on the same
+ * surface at the next wlr_sync).  Single rank only; needs r - k <= round_up(k, 4) (B shares X1's row
+ * layout).  The sWLR state is consumed: wlr_iterate on the same
  * handle afterwards returns WLR_EINVAL.  Errors: WLR_EINVAL (p != 0, nranks > 1, k too large
  * for the small steps), WLR_ERANK (X1^T X1 or B^T B singular), WLR_ECUDA.                    */
 wlr_status wlr_als_iterate(wlr_handle h, int32_t n_iters, double* F, int32_t cap);

@@ -501,6 +501,28 @@ static wlr_status build_graph(wlr_ctx* h, int ph, int pend) {
   return WLR_OK;
 }
 
+// Instantiate (and upload) every per-iteration graph up front, so that no capture or
+// instantiation ever lands inside a timed region or the first iterations of a solve.
+static wlr_status build_all_graphs(wlr_ctx* h) {
+  if (!h->opts.use_graph || h->prof) return WLR_OK;
+  for (int ph = 0; ph < 6; ++ph)
+    for (int pend = 0; pend < 2; ++pend) {
+      if (h->gexec[ph][pend]) continue;
+      wlr_status s = build_graph(h, ph, pend);
+      if (s != WLR_OK) return s;
+      CUDA_TRY(h, cudaGraphUpload(h->gexec[ph][pend], h->st));
+    }
+  return WLR_OK;
+}
+
+static wlr_status reset_graphs(wlr_ctx* h) {   // after a launch-shape switch (diagnostics)
+  CUDA_TRY(h, cudaStreamSynchronize(h->st));
+  for (auto& gp : h->gexec)
+    for (auto& g : gp)
+      if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+  return build_all_graphs(h);
+}
+
 static wlr_status launch_iteration(wlr_ctx* h) {
   wlr_status s;
   if (h->als) return fail(h, WLR_EINVAL, "the handle ran the block-ALS variant (wlr_als_iterate); sWLR state is gone");
@@ -559,7 +581,10 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   // ---- stream
   if (o.stream) h->st = (cudaStream_t)o.stream;
   else {
-    CUDA_TRY(h, cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
+    // a BLOCKING stream: it orders behind work on the legacy default stream, so device inputs a
+    // caller produced there (e.g. a torch tensor on the default stream) are complete before the
+    // handle reads them.  Callers passing their own stream order inputs themselves.
+    CUDA_TRY(h, cudaStreamCreateWithFlags(&h->st, cudaStreamDefault));
     h->own_stream = true;
   }
   int dev = 0;
@@ -911,7 +936,7 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   if (s != WLR_OK) return s;
   h->p = 0;
   h->ph = 0;
-  return WLR_OK;
+  return build_all_graphs(h);
 }
 
 extern "C" wlr_status wlr_init(wlr_handle* out, const void* A, int64_t lda, const void* W1,
@@ -1229,6 +1254,8 @@ static wlr_status als_setup(wlr_ctx* h) {
   if (h->p != 0) return fail(h, WLR_EINVAL, "wlr_als_iterate starts from the GHS state (p = 0)");
   if (h->comm) return fail(h, WLR_EINVAL, "block ALS: single rank only");
   if (!als_ok((int)h->k, (int)h->t)) return fail(h, WLR_EINVAL, "block ALS: k too large for the small steps");
+  // B shares the X1 buffers' kp-wide row layout (row pass, TMA boxes, Gram kernels): r - k must fit
+  if (h->t > h->kp) return fail(h, WLR_EINVAL, "block ALS: needs r - k <= round_up(k, 4)");
   AlsSt* st = new AlsSt();
   h->als = st;
   const size_t es = h->es;
@@ -1381,9 +1408,7 @@ extern "C" wlr_status wlr_debug_state(wlr_handle h, const char* name, double* ou
     }
     h->rp_ms = 0.0;
     h->rp_n = 0;
-    for (auto& gp : h->gexec)
-      for (auto& g : gp)
-        if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+    if ((s = reset_graphs(h)) != WLR_OK) return s;
     if (count) *count = 0;
     return WLR_OK;
   }
@@ -1396,25 +1421,19 @@ extern "C" wlr_status wlr_debug_state(wlr_handle h, const char* name, double* ou
   else if (nm == "tctime") { src = (const double*)h->tc_tstamp; cnt = h->tc_tstamp ? 16 * h->tc_grid : 0; }
   else if (nm == "ktime_on" || nm == "ktime_off") {   // enable/disable K3 phase timestamps
     h->ktime = nm == "ktime_on";
-    for (auto& gp : h->gexec)
-      for (auto& g : gp)
-        if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+    if ((s = reset_graphs(h)) != WLR_OK) return s;
     if (count) *count = 0;
     return WLR_OK;
   }
   else if (nm == "incrtc_on" || nm == "incrtc_off") {   // tensor-core / CUDA-core increments (A/B)
     h->itc_on = h->itc_ok && nm == "incrtc_on";
-    for (auto& gp : h->gexec)
-      for (auto& g : gp)
-        if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+    if ((s = reset_graphs(h)) != WLR_OK) return s;
     if (count) *count = h->itc_on ? 1 : 0;
     return WLR_OK;
   }
   else if (nm == "rowtc_on" || nm == "rowtc_off") {   // tensor-core / CUDA-core row pass (A/B)
     h->tc_on = h->tc_ok && nm == "rowtc_on";
-    for (auto& gp : h->gexec)
-      for (auto& g : gp)
-        if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+    if ((s = reset_graphs(h)) != WLR_OK) return s;
     if (count) *count = h->tc_on ? 1 : 0;
     return WLR_OK;
   }

@@ -735,7 +735,8 @@ __global__ void reduce_incr_kernel(const double* __restrict__ part, int nsplit, 
 #ifndef WLR_RED_L
 #define WLR_RED_L 4
 #endif
-  constexpr int RL = WLR_RED_L;          // lanes per output (2 .. 16; same-box A/B: 4 best)
+  constexpr int RL = WLR_RED_L;          // lanes per output (4, 8 or 16; same-box A/B: 4 best)
+  static_assert(RL == 4 || RL == 8 || RL == 16, "reduce: the shuffle tree assumes 4, 8 or 16 lanes per output");
   const int g = threadIdx.x & (RL - 1);
   const int64_t per_block = blockDim.x / RL;
   for (int64_t i0 = blockIdx.x * per_block; i0 < tot; i0 += (int64_t)gridDim.x * per_block) {

@@ -79,3 +79,16 @@ def test_als_consumes_the_swlr_state():
     with pytest.raises(w.WlrError) as e:
         w.wlr_iterate(g["handle"], 1)
     assert e.value.status == 1
+
+
+def test_als_rejects_r_minus_k_wider_than_x1_rows():
+    """B shares X1's kp-wide row layout: r - k > round_up(k, 4) is rejected with WLR_EINVAL
+    instead of writing past the B buffer."""
+    import torch
+    w = gu.need_gpu()
+    g = np.random.default_rng(5)
+    A = g.standard_normal((200, 30))
+    h = w.wlr_init(torch.from_numpy(A).cuda(), 4, 12, None, w1=10.0)   # r - k = 8 > kp = 4
+    with pytest.raises(w.WlrError) as ei:
+        w.wlr_als_iterate(h, 1)
+    assert "r - k" in str(ei.value)
