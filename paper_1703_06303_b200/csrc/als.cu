@@ -90,7 +90,10 @@ __global__ void __launch_bounds__(kAlsT) als_w_kernel(AlsArgs a) {
       return;
     }
   } else if (blockIdx.x == 0) {   // Kop = C C^T for the per-row solves (diag(W1(i,:)^2) per row)
-    for (int idx = threadIdx.x; idx < k * k; idx += blockDim.x) als_store<T>(a.Kop, idx, a.cct[idx]);
+    for (int idx = threadIdx.x; idx < k * k; idx += blockDim.x) {
+      als_store<T>(a.Kop, idx, a.cct[idx]);
+      if (a.Sop) a.Sop[(idx / k) * ((k + 7) & ~7) + idx % k] = (float)a.cct[idx];
+    }
   }
   const int RP = a.rp;
   if (blockIdx.x == 0) {

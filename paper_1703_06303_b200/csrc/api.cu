@@ -119,6 +119,7 @@ struct wlr_ctx {
   CUtensorMap tmA_tc{}, tmX_tc[2]{}, tmWT{};
   int nwc = 8;                 // row-pass warps running per-row Cholesky
   void *Wt = nullptr, *CVop = nullptr, *Kop = nullptr;
+  float* Sop = nullptr;        // fp32 C C^T, ld round_up(k, 8): per-row solves (non-uniform fp32)
   double *inc_part = nullptr, *inc_part2 = nullptr, *fw_part = nullptr, *fw0 = nullptr;
   int ics = 1, ncl = 0;        // increment row splits per cluster, cluster partials
   // tensor-core increments (fp32, kp <= 32): own column layout (A part padded to 32)
@@ -306,7 +307,7 @@ static SmallArgs small_args(wlr_ctx* h, int ph, int mode) {
   s.Gi_in = h->Gi[cur]; s.Gi_out = h->Gi[nxt]; s.Ki = h->Ki; s.gws = h->gws;
   s.xchg = h->xchg; s.red = h->red; s.scal = h->scal;
   s.trace = h->trace; s.trace_cap = h->trace_cap;
-  s.Wt = h->Wt; s.CVop = h->CVop; s.Kop = h->Kop; s.flags = h->flags;
+  s.Wt = h->Wt; s.CVop = h->CVop; s.Kop = h->Kop; s.Sop = h->Sop; s.flags = h->flags;
   s.WtT = h->WtT; s.KW = h->KW;
   s.eps = h->opts.eps; s.tol = h->opts.eig_tol; s.max_outer = h->opts.eig_max_outer; s.max_deg = 16;
   s.cold = 0;
@@ -380,7 +381,7 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int ph) {
       e = launch_row_pass<float>(a, h->rp, h->rp_tr, h->uniform, 0, h->rp_grid, h->st);
       if (e == cudaSuccess && h->Ebuf) {
         RowSolveArgs q{};
-        q.E = (const float*)h->Ebuf; q.S = (const float*)h->Kop;
+        q.E = (const float*)h->Ebuf; q.S = h->Sop;
         q.W1 = (const float*)h->W1; q.ldw = h->ldw; q.A = (const float*)h->A; q.lda = h->lda;
         q.Xold = a.Xold; q.Xnew = a.Xnew; q.Dnew = a.Dnew; q.fw_part = h->fw_part; q.flags = h->flags;
         q.m = h->m; q.k = (int)h->k; q.kp = (int)h->kp;
@@ -720,8 +721,9 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   if ((s = dalloc(h, &h->X[1], (size_t)h->m * kp * es)) != WLR_OK) return s;
   if ((s = dalloc(h, &h->Dl, (size_t)h->m * kp * es)) != WLR_OK) return s;
   if (h->dtype == WLR_F32 && !h->uniform && row_solve_ok((int)k)) {
-    if ((s = dalloc(h, &h->Ebuf, (size_t)h->m * kp * es)) != WLR_OK) return s;
-    h->rs_grid = row_solve_grid((int)k, h->nsm);
+    if ((s = dalloc(h, &h->Ebuf, (size_t)h->m * kp * es + 64)) != WLR_OK) return s;   // (8-float over-read)
+    if ((s = dalloc_t(h, &h->Sop, (size_t)k * round_up(k, (int64_t)8))) != WLR_OK) return s;
+    h->rs_grid = (int)std::max<int64_t>(1, std::min<int64_t>(row_solve_grid((int)k, h->nsm), h->m));
   }
   if ((s = dalloc(h, &h->Wt, (size_t)wt_rows * h->rp * es)) != WLR_OK) return s;
   {   // TMA tensor maps: 128-byte x BM boxes (SWIZZLE_128B) of A and X1, 32-row boxes of Wt
@@ -798,7 +800,7 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   if ((s = dalloc_t(h, &h->inc_part, std::max((size_t)h->nsplit * k * h->nz,
                                                 (size_t)h->itc_nsplit * k * h->itc_nz))) != WLR_OK) return s;
   if ((s = dalloc_t(h, &h->inc_part2, (size_t)h->ncl * k * h->nz)) != WLR_OK) return s;
-  if ((s = dalloc_t(h, &h->fw_part, (size_t)std::max(h->rp_grid, 1184))) != WLR_OK) return s;
+  if ((s = dalloc_t(h, &h->fw_part, (size_t)std::max({h->rp_grid, h->rs_grid, h->tc_grid, 1184}))) != WLR_OK) return s;
   for (int i = 0; i < 2; ++i)
     if ((s = dalloc_t(h, &h->inc[i], (size_t)(k * nk + 2 * k * k + 1))) != WLR_OK) return s;
   if ((s = dalloc_t(h, &h->fw0, 2)) != WLR_OK) return s;
@@ -1194,7 +1196,7 @@ static cudaError_t als_row_x1(wlr_ctx* h, AlsSt* st) {
   if constexpr (sizeof(T) == 4) {
     if (e == cudaSuccess && h->Ebuf) {
       RowSolveArgs q{};
-      q.E = (const float*)h->Ebuf; q.S = (const float*)h->Kop;
+      q.E = (const float*)h->Ebuf; q.S = h->Sop;
       q.W1 = (const float*)h->W1; q.ldw = h->ldw; q.A = (const float*)h->A; q.lda = h->lda;
       q.Xold = (const float*)a.Xold; q.Xnew = (float*)a.Xnew; q.Dnew = (float*)a.Dnew; q.fw_part = h->fw_part;
       q.flags = h->flags; q.m = h->m; q.k = (int)h->k; q.kp = (int)h->kp;
@@ -1243,7 +1245,7 @@ static AlsArgs als_args(wlr_ctx* h, AlsSt* st) {
   AlsArgs a{};
   a.k = (int)h->k; a.nk = (int)h->nk; a.t = (int)h->t; a.KA = h->KA; a.rp = h->rp; a.rpb = st->rpb;
   a.uniform = h->uniform ? 1 : 0; a.w2 = h->w1s * h->w1s; a.a2sq = h->a2sq;
-  a.flags = h->flags; a.scal = st->scal; a.Kop = h->Kop; a.W = h->Wt; a.Wb = st->Wb;
+  a.flags = h->flags; a.scal = st->scal; a.Kop = h->Kop; a.Sop = h->Sop; a.W = h->Wt; a.Wb = st->Wb;
   a.cct = st->cct; a.dct = st->dct; a.part = st->part;
   return a;
 }

@@ -104,8 +104,8 @@ struct IncrArgs {
 // per-row SPD solves of the non-uniform X1 half-step (rowsolve.cu), fp32: warp per row,
 // reverse-packed shared-memory Cholesky
 struct RowSolveArgs {
-  const float* E;                   // m x kp  e_i (written by the row pass)
-  const float* S;                   // k x k   C C^T
+  const float* E;                   // m x kp  e_i (written by the row pass; >= 8 floats of slack after)
+  const float* S;                   // k x k8  C C^T, ld k8 = round_up(k, 8), zero columns k..k8-1
   const float* W1; int64_t ldw;
   const float* A; int64_t lda;      // A1 = A(:, 0:k) for f_w
   const float* Xold; float* Xnew; float* Dnew;   // m x kp
@@ -149,6 +149,7 @@ struct AlsArgs {
   double* scal;                         // [f_w, <M', C'>, <C', G' C'>]
   double* Fout;                         // objective of the new state
   void* W; void* Wb; void* Kop;         // X1 row map (KA + KX) x rp, B row map x rpb, C C^T
+  float* Sop;                           // fp32 C C^T with ld round_up(k, 8) for the per-row solves (or null)
   double* cct; double* dct;             // C C^T (k x k) and D C^T (t x k) of the current state
   double* part;                         // per-CTA partials of the column-split kernels
   int* flags;
@@ -205,6 +206,7 @@ struct SmallArgs {
   double* scal;                     // persistent scalars (see small_step.cuh)
   double* trace; int trace_cap;     // trace ring (4 doubles per state)
   void* Wt; void* CVop; void* Kop;  // row-pass operands (dtype)
+  float* Sop;                       // fp32 C C^T, ld round_up(k, 8), zero padding (per-row solves; or null)
   int* flags;
   double eps, tol; int max_outer, max_deg;
   int cold;                         // 1: Y holds a random block (no Ritz values yet)

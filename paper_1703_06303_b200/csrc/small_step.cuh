@@ -939,6 +939,7 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
             if (!a.uniform && s.c == 0) {
               if (a.dtype) reinterpret_cast<double*>(a.Kop)[idx] = v;
               else reinterpret_cast<float*>(a.Kop)[idx] = (float)v;
+              if (a.Sop) a.Sop[i * ((k + 7) & ~7) + j] = (float)v;
             }
             Gq[idx] = v + (i == j ? a.w2 : 0.0);
             if (a.mode && a.uniform) Xq[idx] = Pq[idx];   // K^{-1}_p (staged after C')
