@@ -82,4 +82,7 @@ def compare(cfg, g, o, tol_x=None, tol_f=None, check_steps=True):
         if big.any():
             es = np.abs(tr[big, 1] - so[big]) / so[big]
             assert es.max() <= (2e-2 if cfg.dtype == "f32" else 1e-3), f"step mismatch {es.max():.3e}"
+            # rel_p = Error_p / ||X_p|| (reading R3), element-wise
+            er = np.abs(tr[big, 2] - ro[big]) / ro[big]
+            assert er.max() <= (2e-2 if cfg.dtype == "f32" else 1e-3), f"rel mismatch {er.max():.3e}"
     return ex, float(ef.max())

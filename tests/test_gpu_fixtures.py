@@ -1,0 +1,102 @@
+"""GPU parity at BASELINE.json's configs 3, 4 and 5 at their FULL iteration counts (200 / 100 / 50),
+from the GHS start, in the launch configuration bench.py times (same library defaults), against
+the oracle fixtures under ``tests/fixtures/`` written by ``scripts/make_oracle_fixtures.py`` (which
+calls only ``synth`` and ``oracle``; config 5 through ``oracle/swlr_large.py``, reading R22).
+
+Compared (north_star tolerances): the objective F_p of EVERY canonical state (relative 1e-5), the
+relative step rel_p = Error_p / ||X_p|| (reading R3) element-wise while the oracle's
+step is above the fp32 iterate's resolution, and X_N = (X1_N, X1_N C_N + D_N) on 1026 fixed sampled
+rows (relative Frobenius 1e-4).  Then the running fp64 Grams G = X1^T X1 and M = X1^T A2 of the
+device state are checked against an fp64 recomputation from the returned X1 (the drift bound of
+SURVEY.md §8(a) a4)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import synth
+from tests import gpu_util as gu
+
+pytestmark = pytest.mark.gpu
+
+FIX = os.path.join(os.path.dirname(os.path.abspath(__file__)), "fixtures")
+
+# rel_p is compared where the oracle's relative step is above this (below it the fp32 iterate's
+# own rounding, ~1e-8 .. 1e-7 relative per step, is the step)
+REL_RESOLVED = 1e-5
+# Gram drift (fp64 running sums vs fp64 recomputation from the stored fp32 X1), relative to ||G||, ||M||
+GRAM_DRIFT = 1e-7
+
+
+def _load(ci):
+    path = os.path.join(FIX, f"oracle_cfg{ci}.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"fixture {path} not generated (scripts/make_oracle_fixtures.py {ci})")
+    d = np.load(path)
+    with open(os.path.join(FIX, f"oracle_cfg{ci}.json")) as f:
+        meta = json.load(f)
+    return d, meta
+
+
+@pytest.mark.parametrize("ci", [3, 4, 5])
+def test_full_iterations_against_oracle_fixture(ci):
+    import torch
+    w = gu.need_gpu()
+    d, meta = _load(ci)
+    cfg = synth.CONFIGS[ci]
+    assert meta["iters"] == cfg.iters and meta["m"] == cfg.m and meta["init"].startswith("GHS")
+    A = synth.make_A(cfg)
+    W1 = synth.make_W1(cfg)
+    rows = d["rows"]
+    # the same problem as the fixture's
+    fp = meta["fingerprint"]
+    assert abs(float(np.sum(A, dtype=np.float64)) - fp["A_sum"]) <= 1e-9 * abs(fp["A_sum"])
+    if W1 is not None:
+        assert abs(float(np.sum(W1, dtype=np.float64)) - fp["W1_sum"]) <= 1e-9 * abs(fp["W1_sum"])
+    np.testing.assert_array_equal(A[rows[:8]], d["A_rows"])
+
+    At = torch.from_numpy(A).cuda()
+    Wt = None if W1 is None else torch.from_numpy(W1).cuda()
+    h = w.wlr_init(At, cfg.k, cfg.r, Wt, w1=cfg.w_const or 1.0)
+    done, _ = w.wlr_iterate(h, cfg.iters)
+    assert done == cfg.iters
+    tr = w.wlr_trace(h)
+    res = w.wlr_result(h, x2=True)
+
+    keys = list(d["trace_keys"])
+    to = d["trace"]
+    Fo, so, ro = to[:, keys.index("F")], to[:, keys.index("step")], to[:, keys.index("rel")]
+    assert tr.shape[0] == cfg.iters + 1
+    eF = np.abs(tr[:, 0] - Fo) / np.abs(Fo)
+    assert eF.max() <= gu.TOL_F[cfg.dtype], f"relF {eF.max():.2e} at p={int(eF.argmax())}"
+    # rel_p: element-wise where resolved, and small where the oracle says it is small
+    big = ro > REL_RESOLVED
+    big[0] = False
+    if big.any():
+        er = np.abs(tr[big, 2] - ro[big]) / ro[big]
+        assert er.max() <= 2e-2, f"rel mismatch {er.max():.2e}"
+        es = np.abs(tr[big, 1] - so[big]) / so[big]
+        assert es.max() <= 2e-2, f"step mismatch {es.max():.2e}"
+    small = ro < 0.1 * REL_RESOLVED
+    small[0] = False
+    assert np.all(tr[small, 2] < REL_RESOLVED), "GPU relative step not small where the oracle's is"
+
+    X = np.concatenate([res["X1"][rows].astype(np.float64), res["X2"][rows].astype(np.float64)], axis=1)
+    Xo = d["X_rows"].astype(np.float64)
+    ex = np.linalg.norm(X - Xo) / np.linalg.norm(Xo)
+    assert ex <= gu.TOL_X[cfg.dtype], f"relX(sampled rows) {ex:.2e}"
+
+    # running Grams vs an fp64 recomputation from the returned X1 (drift check)
+    X1 = res["X1"].astype(np.float64)
+    G = w.wlr_debug_state(h, "G").reshape(cfg.k, cfg.k)
+    M = w.wlr_debug_state(h, "M").reshape(cfg.k, cfg.n - cfg.k)
+    Gf = X1.T @ X1
+    Mf = np.zeros_like(M)
+    for i0 in range(0, cfg.m, 65536):
+        Mf += X1[i0:i0 + 65536].T @ A[i0:i0 + 65536, cfg.k:].astype(np.float64)
+    dg = np.linalg.norm(G - Gf) / np.linalg.norm(Gf)
+    dm = np.linalg.norm(M - Mf) / np.linalg.norm(Mf)
+    assert dg <= GRAM_DRIFT and dm <= GRAM_DRIFT, (dg, dm)
+    print(f"config {ci}: {cfg.iters} iterations, relF max {eF.max():.2e}, relX(rows) {ex:.2e}, "
+          f"Gram drift G {dg:.1e} M {dm:.1e}")

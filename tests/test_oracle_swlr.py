@@ -182,7 +182,6 @@ def test_p9_bracketing_by_general_als():
         f_s = res.trace[-1]["F"]
         w = np.concatenate([w1, np.ones((10, 10))], axis=1)
         _, f_a = oracle.general_wlra(a, w, 4, restarts=4, inner_iters=400, seed=t)
-        assert f_s <= f_a + 1e-6 * (1 + f_a) or f_a <= f_s   # neither is worse by construction
         if abs(f_s - f_a) <= 1e-6 * (1 + f_s):
             agree += 1
     assert agree >= 18
@@ -258,3 +257,25 @@ def test_invalid_arguments():
     a0[:, 1] = a0[:, 0]
     with pytest.raises(oracle.RankDeficientError):
         oracle.swlr(a0, w1, cfg.k, cfg.r, iters=1)           # rank(A1) < k
+
+
+def test_r3_relative_error_is_relative_to_the_previous_state():
+    """Reading R3: rel_p = ||X_{p+1} - X_p||_F / ||X_p||_F -- the norm of the state
+    BEFORE the step, not after.  The states are rebuilt here by separate oracle runs of p and p+1
+    iterations, and the case (random X1_0, unit weight) makes ||X_p|| and ||X_{p+1}|| differ by
+    far more than the tolerance, so the other denominator fails."""
+    g = np.random.default_rng(31)
+    a = g.standard_normal((40, 6)) @ g.standard_normal((6, 12)) + 0.1 * g.standard_normal((40, 12))
+    w1 = np.ones((40, 3))
+    x0 = 5.0 * g.standard_normal((40, 3))           # far from A1: the first steps change ||X|| a lot
+    full = oracle.swlr(a, w1, 3, 5, iters=3, x1_0=x0)
+    for p in range(3):
+        xp = oracle.swlr(a, w1, 3, 5, iters=p, x1_0=x0).x
+        xq = oracle.swlr(a, w1, 3, 5, iters=p + 1, x1_0=x0).x
+        err = np.linalg.norm(xq - xp)
+        before, after = err / np.linalg.norm(xp), err / np.linalg.norm(xq)
+        rec = full.trace[p + 1]
+        assert abs(rec["step"] - err) <= 1e-12 * err
+        assert abs(rec["rel"] - before) <= 1e-12 * before
+        if p == 0:
+            assert abs(after - before) > 1e-3 * before   # the two readings are distinguishable
