@@ -16,7 +16,7 @@ CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libwlr.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["api.cu", "init_kernels.cu", "rowpass.cu", "small_step.cu", "result.cu", "tma_host.cu", "rowpass_tc.cu", "incr_tc.cu", "rowsolve.cu", "als.cu"] + [
+SOURCES = ["api.cu", "init_kernels.cu", "rowpass.cu", "small_step.cu", "result.cu", "tma_host.cu", "rowpass_tc.cu", "incr_tc.cu", "rowsolve.cu", "als.cu", "prop.cu"] + [
     f"small_step_bt{b}.cu" for b in (4, 8, 12, 16, 24, 32)]
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # WLR_NVCC_EXTRA: extra nvcc flags for experiments (e.g. "-DWLR_IT_NR=4"); empty in normal builds

@@ -119,6 +119,18 @@ struct wlr_ctx {
   CUtensorMap tmA_tc{}, tmX_tc[2]{}, tmWT{};
   int nwc = 8;                 // row-pass warps running per-row Cholesky
   void *Wt = nullptr, *CVop = nullptr, *Kop = nullptr;
+  // W' double-buffered by iteration parity: row pass(p) and prop(p) read W'_p while K3a(p) writes
+  // W'_{p+1} (buffer 0 is Wt / WtT / tmW / tmWT, also used by the block ALS)
+  void *Wt1 = nullptr, *WtT1 = nullptr;
+  CUtensorMap tmW1{}, tmWT1{};
+  // Gram propagation (uniform W1, prop.cu): A^T A, Q_p = A^T X1_p (by parity), scratch
+  bool prop = false;
+  double *AtA = nullptr, *Qg[2] = {nullptr, nullptr}, *Hs = nullptr, *dgs = nullptr;
+  int* pcnt = nullptr;
+  double a1sq = 0.0;
+  cudaStream_t st3 = nullptr;  // row-pass branch of a propagation iteration
+  cudaStream_t st4 = nullptr;  // critical chain (prop -> K3a) of a propagation iteration, high priority
+  cudaEvent_t ev_f3 = nullptr, ev_j3 = nullptr, ev_j4 = nullptr;
   float* Sop = nullptr;        // fp32 C C^T, ld round_up(k, 8): per-row solves (non-uniform fp32)
   double *inc_part = nullptr, *inc_part2 = nullptr, *fw_part = nullptr, *fw0 = nullptr;
   int ics = 1, ncl = 0;        // increment row splits per cluster, cluster partials
@@ -307,8 +319,9 @@ static SmallArgs small_args(wlr_ctx* h, int ph, int mode) {
   s.Gi_in = h->Gi[cur]; s.Gi_out = h->Gi[nxt]; s.Ki = h->Ki; s.gws = h->gws;
   s.xchg = h->xchg; s.red = h->red; s.scal = h->scal;
   s.trace = h->trace; s.trace_cap = h->trace_cap;
-  s.Wt = h->Wt; s.CVop = h->CVop; s.Kop = h->Kop; s.Sop = h->Sop; s.flags = h->flags;
-  s.WtT = h->WtT; s.KW = h->KW;
+  const bool wb1 = ((ph + 1) & 1) != 0;     // K3(p) writes W'_{p+1}
+  s.Wt = wb1 ? h->Wt1 : h->Wt; s.CVop = h->CVop; s.Kop = h->Kop; s.Sop = h->Sop; s.flags = h->flags;
+  s.WtT = wb1 ? h->WtT1 : h->WtT; s.KW = h->KW;
   s.eps = h->opts.eps; s.tol = h->opts.eig_tol; s.max_outer = h->opts.eig_max_outer; s.max_deg = 16;
   s.cold = 0;
   s.tdbg = h->ktime ? h->tdbg : nullptr;
@@ -341,7 +354,134 @@ static wlr_status flush_pending(wlr_ctx* h) {
 // (=> programmatic dependent launch: the row pass overlaps K3b(p-1), the objective / step
 // norm of the previous state; K3b only reads state the row pass does not write, and the
 // increments, which wait for both, are where K3b's inputs get rewritten.)
+// Row pass of iteration p (phase ph) on stream st: X1_{p+1} from [A | X1_p] and W'_p.  light: the
+// tensor-core pass writes X1_{p+1} only (Gram-propagation mode needs no Delta / f_w partials).
+static cudaError_t launch_row_pass_iter(wlr_ctx* h, int ph, cudaStream_t st, bool light, bool pdl = false) {
+  const int cur = ph & 1, nxt = cur ^ 1;      // X1 buffers
+  const bool wb = cur != 0;                   // W'_p buffer
+  cudaError_t e;
+  if (h->dtype == WLR_F32) {
+    RowPassArgs<float> a{};
+    a.A = (const float*)h->A; a.lda = h->lda; a.W1 = (const float*)h->W1; a.ldw = h->ldw;
+    a.w2s = (float)(h->w1s * h->w1s);
+    a.Xold = (const float*)h->X[cur]; a.Xnew = (float*)h->X[nxt]; a.Dnew = (float*)h->Dl; a.nwc = h->nwc;
+    a.Wt = (const float*)(wb ? h->Wt1 : h->Wt); a.KA = h->KA; a.Kmat = (const float*)h->Kop;
+    a.tmA = h->tmA; a.tmX = h->tmX[cur]; a.tmW = wb ? h->tmW1 : h->tmW;
+    a.fw_part = h->fw_part; a.flags = h->flags;
+    a.m = h->m; a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.no = (int)h->kp;
+    a.vec_ok = (h->lda % 4 == 0) && ((uintptr_t)h->A % 16 == 0);
+    a.Ebuf = (float*)h->Ebuf;
+    set_prefetch(h, ph, a.pf_ptr, a.pf_bytes);
+    if (h->tc_on) {
+      RowPassTcArgs q{};
+      q.tmA = h->tmA_tc; q.tmX = h->tmX_tc[cur]; q.tmW = wb ? h->tmWT1 : h->tmWT;
+      q.A = a.A; q.lda = a.lda; q.Xold = a.Xold; q.Xnew = a.Xnew; q.Dnew = light ? nullptr : a.Dnew;
+      q.w2s = a.w2s; q.fw_part = h->fw_part;
+      for (int i = 0; i < kPf; ++i) { q.pf_ptr[i] = a.pf_ptr[i]; q.pf_bytes[i] = a.pf_bytes[i]; }
+      q.m = h->m; q.KA = h->KA; q.k = (int)h->k; q.kp = (int)h->kp; q.n = (int)h->n;
+      q.m_main = h->tc_m_main; q.extra = h->tc_extra;
+      q.tmAx = h->tmA_x; q.tmXx = h->tmX_x[cur];
+      q.dbg = h->tc_dbg;
+      q.tstamp = h->tc_tstamp;
+      q.pdl = pdl ? 1 : 0;
+      e = launch_row_pass_tc(q, h->rp, h->tc_grid, st, nullptr, h->tc_deep);
+    } else {
+      e = launch_row_pass<float>(a, h->rp, h->rp_tr, h->uniform, 0, h->rp_grid, st);
+      if (e == cudaSuccess && h->Ebuf) {
+        RowSolveArgs q{};
+        q.E = (const float*)h->Ebuf; q.S = h->Sop;
+        q.W1 = (const float*)h->W1; q.ldw = h->ldw; q.A = (const float*)h->A; q.lda = h->lda;
+        q.Xold = a.Xold; q.Xnew = a.Xnew; q.Dnew = a.Dnew; q.fw_part = h->fw_part; q.flags = h->flags;
+        q.m = h->m; q.k = (int)h->k; q.kp = (int)h->kp;
+        e = launch_row_solve(q, h->rs_grid, st);
+      }
+    }
+  } else {
+    RowPassArgs<double> a{};
+    a.A = (const double*)h->A; a.lda = h->lda; a.W1 = (const double*)h->W1; a.ldw = h->ldw;
+    a.w2s = h->w1s * h->w1s;
+    a.Xold = (const double*)h->X[cur]; a.Xnew = (double*)h->X[nxt]; a.Dnew = (double*)h->Dl; a.nwc = h->nwc;
+    a.Wt = (const double*)(wb ? h->Wt1 : h->Wt); a.KA = h->KA; a.Kmat = (const double*)h->Kop;
+    a.tmA = h->tmA; a.tmX = h->tmX[cur]; a.tmW = wb ? h->tmW1 : h->tmW;
+    a.fw_part = h->fw_part; a.flags = h->flags;
+    a.m = h->m; a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.no = (int)h->kp;
+    a.vec_ok = (h->lda % 4 == 0) && ((uintptr_t)h->A % 16 == 0);
+    set_prefetch(h, ph, a.pf_ptr, a.pf_bytes);
+    e = launch_row_pass<double>(a, h->rp, h->rp_tr, h->uniform, 0, h->rp_grid, st);
+  }
+  return e;
+}
+
+// One iteration in Gram-propagation mode (uniform W1):
+//   st : prop1(p) -> prop2(p) -> K3a(p)                   (the critical chain, m-independent)
+//   st3:   row pass(p)  (X1_{p+1} materialised beside it; joined at the end of the iteration)
+//   st2:   K3b(p-1)     (deferred objective / step norm of the previous state)
+static wlr_status enqueue_prop_iteration(wlr_ctx* h, int ph) {
+  const int cur = ph & 1, nxt = cur ^ 1, slot = ph % 3;
+  const bool prof = h->prof, pend = h->pending;
+  PropArgs pa{};
+  pa.AtA = h->AtA; pa.Wt = cur ? h->Wt1 : h->Wt; pa.RP = h->rp; pa.KA = h->KA;
+  pa.Qp = h->Qg[cur]; pa.Qn = h->Qg[nxt]; pa.Gp = h->G[slot]; pa.part = h->Hs;
+  pa.inc = h->inc[cur];
+  pa.n = (int)h->n; pa.k = (int)h->k;
+  SmallArgs sa = small_args(h, ph, 1);
+  const int nfw = h->tc_on ? h->tc_grid : h->rp_grid;
+  double* fw_dst = h->inc[cur] + (h->k * h->nk + 2 * h->k * h->k);   // f_w(X1_{p+1}), read by K3b(p)
+  cudaError_t e;
+  if (prof) {   // eager profiling pass: everything serial on st, one event group per kernel kind
+    cudaEvent_t ev[8];
+    for (int i = 0; i < 8; ++i) ev[i] = prof_event(h);
+    cudaEventRecord(ev[0], h->st);
+    if ((e = launch_row_pass_iter(h, ph, h->st, true)) != cudaSuccess) return fail(h, WLR_ECUDA, std::string("row pass: ") + cudaGetErrorString(e));
+    launch_reduce_incr(h->inc_part, 0, 0, 0, 1, 0, 0, 0, h->fw_part, nfw, fw_dst, h->st);
+    cudaEventRecord(ev[1], h->st);
+    if ((e = launch_prop(pa, false, 0, h->st)) != cudaSuccess) return fail(h, WLR_ECUDA, std::string("Gram propagation: ") + cudaGetErrorString(e));
+    cudaEventRecord(ev[2], h->st);
+    cudaEventRecord(ev[3], h->st);
+    cudaEventRecord(ev[4], h->st);
+    sa.pdl = 0;
+    h->last_ss = sa;
+    if ((e = launch_small_step(sa, 1, h->st)) != cudaSuccess) return fail(h, WLR_ECUDA, std::string("small step: ") + cudaGetErrorString(e));
+    cudaEventRecord(ev[5], h->st);
+    if (pend) {
+      cudaEventRecord(ev[6], h->st);
+      if ((e = launch_deferred(h, h->pend, h->st)) != cudaSuccess) return fail(h, WLR_ECUDA, std::string("small step (deferred): ") + cudaGetErrorString(e));
+      cudaEventRecord(ev[7], h->st);
+    }
+    h->pr.iters++;
+    h->pr.groups.push_back(pend ? 1 : 0);
+  } else {
+    // critical chain on the high-priority st4: prop1 -> prop2 -> K3a, and the row pass as K3a's
+    // programmatic dependent: K3a holds its cluster's SMs before the streaming pass fills the rest
+    // of the GPU beside it.  K3b(p-1) on st2 once prop1 is done (it only needs to end with K3a).
+    CUDA_TRY(h, cudaEventRecord(h->ev_fork, h->st));
+    CUDA_TRY(h, cudaStreamWaitEvent(h->st4, h->ev_fork, 0));
+    if ((e = launch_prop(pa, false, 0, h->st4, h->ev_f3)) != cudaSuccess) return fail(h, WLR_ECUDA, std::string("Gram propagation: ") + cudaGetErrorString(e));
+    if (pend) {
+      CUDA_TRY(h, cudaStreamWaitEvent(h->st2, h->ev_f3, 0));
+      if ((e = launch_deferred(h, h->pend, h->st2)) != cudaSuccess) return fail(h, WLR_ECUDA, std::string("small step (deferred): ") + cudaGetErrorString(e));
+      CUDA_TRY(h, cudaEventRecord(h->ev_join, h->st2));
+    }
+    sa.pdl = 1;                                // right behind prop2
+    h->last_ss = sa;
+    if ((e = launch_small_step(sa, 1, h->st4)) != cudaSuccess) return fail(h, WLR_ECUDA, std::string("small step: ") + cudaGetErrorString(e));
+    const bool rpt = h->rp_time;
+    if (rpt) CUDA_TRY(h, cudaEventRecordWithFlags(h->rp_ev[0], h->st4, cudaEventRecordExternal));
+    if ((e = launch_row_pass_iter(h, ph, h->st4, true, !rpt)) != cudaSuccess) return fail(h, WLR_ECUDA, std::string("row pass: ") + cudaGetErrorString(e));
+    if (rpt) CUDA_TRY(h, cudaEventRecordWithFlags(h->rp_ev[1], h->st4, cudaEventRecordExternal));
+    launch_reduce_incr(h->inc_part, 0, 0, 0, 1, 0, 0, 0, h->fw_part, nfw, fw_dst, h->st4);
+    CUDA_TRY(h, cudaEventRecord(h->ev_j4, h->st4));
+    CUDA_TRY(h, cudaStreamWaitEvent(h->st, h->ev_j4, 0));
+    if (pend) CUDA_TRY(h, cudaStreamWaitEvent(h->st, h->ev_join, 0));
+  }
+  h->pend = sa;
+  h->pending = true;
+  h->pr.launches += pend ? 6 : 5;
+  return WLR_OK;
+}
+
 static wlr_status enqueue_iteration(wlr_ctx* h, int ph) {
+  if (h->prop) return enqueue_prop_iteration(h, ph);
   const int cur = ph & 1, nxt = cur ^ 1;      // X1 buffers
   cudaEvent_t ev[8] = {};
   const bool prof = h->prof;
@@ -352,55 +492,7 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int ph) {
   }
   const bool rpt = h->rp_time && !prof;
   if (rpt) CUDA_TRY(h, cudaEventRecordWithFlags(h->rp_ev[0], h->st, cudaEventRecordExternal));
-  cudaError_t e;
-  if (h->dtype == WLR_F32) {
-    RowPassArgs<float> a{};
-    a.A = (const float*)h->A; a.lda = h->lda; a.W1 = (const float*)h->W1; a.ldw = h->ldw;
-    a.w2s = (float)(h->w1s * h->w1s);
-    a.Xold = (const float*)h->X[cur]; a.Xnew = (float*)h->X[nxt]; a.Dnew = (float*)h->Dl; a.nwc = h->nwc;
-    a.Wt = (const float*)h->Wt; a.KA = h->KA; a.Kmat = (const float*)h->Kop;
-    a.tmA = h->tmA; a.tmX = h->tmX[cur]; a.tmW = h->tmW;
-    a.fw_part = h->fw_part; a.flags = h->flags;
-    a.m = h->m; a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.no = (int)h->kp;
-    a.vec_ok = (h->lda % 4 == 0) && ((uintptr_t)h->A % 16 == 0);
-    a.Ebuf = (float*)h->Ebuf;
-    set_prefetch(h, ph, a.pf_ptr, a.pf_bytes);
-    if (h->tc_on) {
-      RowPassTcArgs q{};
-      q.tmA = h->tmA_tc; q.tmX = h->tmX_tc[cur]; q.tmW = h->tmWT;
-      q.A = a.A; q.lda = a.lda; q.Xold = a.Xold; q.Xnew = a.Xnew; q.Dnew = a.Dnew;
-      q.w2s = a.w2s; q.fw_part = h->fw_part;
-      for (int i = 0; i < kPf; ++i) { q.pf_ptr[i] = a.pf_ptr[i]; q.pf_bytes[i] = a.pf_bytes[i]; }
-      q.m = h->m; q.KA = h->KA; q.k = (int)h->k; q.kp = (int)h->kp; q.n = (int)h->n;
-      q.m_main = h->tc_m_main; q.extra = h->tc_extra;
-      q.tmAx = h->tmA_x; q.tmXx = h->tmX_x[cur];
-      q.dbg = h->tc_dbg;
-      q.tstamp = h->tc_tstamp;
-      e = launch_row_pass_tc(q, h->rp, h->tc_grid, h->st, nullptr, h->tc_deep);
-    } else {
-      e = launch_row_pass<float>(a, h->rp, h->rp_tr, h->uniform, 0, h->rp_grid, h->st);
-      if (e == cudaSuccess && h->Ebuf) {
-        RowSolveArgs q{};
-        q.E = (const float*)h->Ebuf; q.S = h->Sop;
-        q.W1 = (const float*)h->W1; q.ldw = h->ldw; q.A = (const float*)h->A; q.lda = h->lda;
-        q.Xold = a.Xold; q.Xnew = a.Xnew; q.Dnew = a.Dnew; q.fw_part = h->fw_part; q.flags = h->flags;
-        q.m = h->m; q.k = (int)h->k; q.kp = (int)h->kp;
-        e = launch_row_solve(q, h->rs_grid, h->st);
-      }
-    }
-  } else {
-    RowPassArgs<double> a{};
-    a.A = (const double*)h->A; a.lda = h->lda; a.W1 = (const double*)h->W1; a.ldw = h->ldw;
-    a.w2s = h->w1s * h->w1s;
-    a.Xold = (const double*)h->X[cur]; a.Xnew = (double*)h->X[nxt]; a.Dnew = (double*)h->Dl; a.nwc = h->nwc;
-    a.Wt = (const double*)h->Wt; a.KA = h->KA; a.Kmat = (const double*)h->Kop;
-    a.tmA = h->tmA; a.tmX = h->tmX[cur]; a.tmW = h->tmW;
-    a.fw_part = h->fw_part; a.flags = h->flags;
-    a.m = h->m; a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.no = (int)h->kp;
-    a.vec_ok = (h->lda % 4 == 0) && ((uintptr_t)h->A % 16 == 0);
-    set_prefetch(h, ph, a.pf_ptr, a.pf_bytes);
-    e = launch_row_pass<double>(a, h->rp, h->rp_tr, h->uniform, 0, h->rp_grid, h->st);
-  }
+  cudaError_t e = launch_row_pass_iter(h, ph, h->st, false);
   if (e != cudaSuccess) return fail(h, WLR_ECUDA, std::string("row pass: ") + cudaGetErrorString(e));
   if (prof) cudaEventRecord(ev[1], h->st);
   if (rpt) CUDA_TRY(h, cudaEventRecordWithFlags(h->rp_ev[1], h->st, cudaEventRecordExternal));
@@ -543,7 +635,7 @@ static wlr_status launch_iteration(wlr_ctx* h) {
     }
     h->pend = small_args(h, h->ph, 1);
     h->pending = true;
-    h->pr.launches += pend ? 5 : 4;
+    h->pr.launches += (pend ? 5 : 4) + (h->prop ? 1 : 0);
   } else {
     s = enqueue_iteration(h, h->ph);
     if (s != WLR_OK) return s;
@@ -726,12 +818,15 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
     h->rs_grid = (int)std::max<int64_t>(1, std::min<int64_t>(row_solve_grid((int)k, h->nsm), h->m));
   }
   if ((s = dalloc(h, &h->Wt, (size_t)wt_rows * h->rp * es)) != WLR_OK) return s;
+  if ((s = dalloc(h, &h->Wt1, (size_t)wt_rows * h->rp * es)) != WLR_OK) return s;
   {   // TMA tensor maps: 128-byte x BM boxes (SWIZZLE_128B) of A and X1, 32-row boxes of Wt
     const uint32_t pe = (uint32_t)(128 / es), bm = (uint32_t)row_pass_bm(h->rp, h->rp_tr);
     bool ok = make_tmap_2d(&h->tmA, h->A, (int)es, (uint64_t)n, (uint64_t)h->m, (uint64_t)h->lda * es, pe, bm, true);
     for (int i = 0; i < 2; ++i)
       ok = ok && make_tmap_2d(&h->tmX[i], h->X[i], (int)es, (uint64_t)kp, (uint64_t)h->m, (uint64_t)kp * es, pe, bm, true);
     ok = ok && make_tmap_2d(&h->tmW, h->Wt, (int)es, (uint64_t)h->rp, (uint64_t)wt_rows, (uint64_t)h->rp * es,
+                            (uint32_t)h->rp, 32u, false);
+    ok = ok && make_tmap_2d(&h->tmW1, h->Wt1, (int)es, (uint64_t)h->rp, (uint64_t)wt_rows, (uint64_t)h->rp * es,
                             (uint32_t)h->rp, 32u, false);
     if (!ok) return fail(h, WLR_ECUDA, "cuTensorMapEncodeTiled failed (TMA descriptors)");
   }
@@ -751,10 +846,12 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   if (h->tc_ok) {
     h->KW = (int)wt_rows;
     if ((s = dalloc(h, &h->WtT, (size_t)2 * h->rp * wt_rows * es)) != WLR_OK) return s;   // W'^T | W'^T_lo
+    if ((s = dalloc(h, &h->WtT1, (size_t)2 * h->rp * wt_rows * es)) != WLR_OK) return s;
     bool ok = make_tmap_2d(&h->tmA_tc, h->A, 4, (uint64_t)n, (uint64_t)h->m, (uint64_t)h->lda * 4, 32u, (uint32_t)kTcBM, true);
     for (int i = 0; i < 2; ++i)
       ok = ok && make_tmap_2d(&h->tmX_tc[i], h->X[i], 4, (uint64_t)kp, (uint64_t)h->m, (uint64_t)kp * 4, 32u, (uint32_t)kTcBM, true);
     ok = ok && make_tmap_2d(&h->tmWT, h->WtT, 4, (uint64_t)wt_rows, (uint64_t)(2 * h->rp), (uint64_t)wt_rows * 4, 32u, (uint32_t)h->rp, true);
+    ok = ok && make_tmap_2d(&h->tmWT1, h->WtT1, 4, (uint64_t)wt_rows, (uint64_t)(2 * h->rp), (uint64_t)wt_rows * 4, 32u, (uint32_t)h->rp, true);
     int occ = 0;
     RowPassTcArgs q{};
     if (ok && launch_row_pass_tc(q, h->rp, 0, h->st, &occ) == cudaSuccess && occ > 0) {
@@ -803,6 +900,16 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   if ((s = dalloc_t(h, &h->fw_part, (size_t)std::max({h->rp_grid, h->rs_grid, h->tc_grid, 1184}))) != WLR_OK) return s;
   for (int i = 0; i < 2; ++i)
     if ((s = dalloc_t(h, &h->inc[i], (size_t)(k * nk + 2 * k * k + 1))) != WLR_OK) return s;
+  {   // Gram propagation for the linear (uniform-W1) X1 half-step (prop.cu; WLR_PROP=0 disables, A/B)
+    const char* pe = std::getenv("WLR_PROP");
+    h->prop = h->uniform && h->dtype == WLR_F32 && (!pe || std::atoi(pe) != 0) && prop1_smem((int)n, (int)k) <= 220 * 1024 &&
+              16 * k * k <= 200 * 1024;
+  }
+  if (h->prop) {
+    for (int i = 0; i < 2; ++i)
+      if ((s = dalloc_t(h, &h->Qg[i], (size_t)n * k)) != WLR_OK) return s;
+    if ((s = dalloc_t(h, &h->Hs, prop_part_doubles((int)n, (int)k))) != WLR_OK) return s;
+  }
   if ((s = dalloc_t(h, &h->fw0, 2)) != WLR_OK) return s;
   if ((s = dalloc_t(h, &h->GA, (size_t)nk * nk)) != WLR_OK) return s;
   for (int i = 0; i < 3; ++i) {
@@ -826,6 +933,11 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
     int lo = 0, hi = 0;
     CUDA_TRY(h, cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CUDA_TRY(h, cudaStreamCreateWithPriority(&h->st2, cudaStreamNonBlocking, hi));
+    CUDA_TRY(h, cudaStreamCreateWithPriority(&h->st3, cudaStreamNonBlocking, lo));   // row pass branch
+    CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_f3, cudaEventDisableTiming));
+    CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_j3, cudaEventDisableTiming));
+    CUDA_TRY(h, cudaStreamCreateWithPriority(&h->st4, cudaStreamNonBlocking, hi));
+    CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_j4, cudaEventDisableTiming));
     CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
     CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
   }
@@ -875,8 +987,14 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
     run_gram(h->X[0], kp, (int)k, A2, h->lda, (int)nk, tmp);                 // k x nk
     CUDA_TRY(h, cudaMemcpy2DAsync(gram + k, n * 8, tmp, nk * 8, nk * 8, k, cudaMemcpyDeviceToDevice, h->st));
     run_gram(A2, h->lda, (int)nk, A2, h->lda, (int)nk, h->GA);               // nk x nk
+    if (h->prop) {   // the full A^T A and Q_0 = A^T X1_0 for the propagation
+      if ((s = dalloc_t(h, &h->AtA, (size_t)n * n)) != WLR_OK) return s;
+      run_gram(h->A, h->lda, (int)n, h->A, h->lda, (int)n, h->AtA);
+      run_gram(h->A, h->lda, (int)n, h->X[0], kp, (int)k, h->Qg[0]);
+    }
   } else {
     run_gram(h->A, h->lda, (int)n, h->A, h->lda, (int)n, gram);
+    h->AtA = gram;
   }
   if (h->comm) {
     // sum the per-rank Grams (rows are sharded, Grams are additive over rows)
@@ -885,12 +1003,27 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
     if (o.init == WLR_INIT_GIVEN) {
       nr = g_nccl.allReduce(h->GA, h->GA, (size_t)nk * nk, ncclFloat64, ncclSum, h->comm, h->st);
       if (nr != ncclSuccess) return fail(h, WLR_ENCCL, "ncclAllReduce(init GA)");
+      if (h->prop) {
+        nr = g_nccl.allReduce(h->AtA, h->AtA, (size_t)n * n, ncclFloat64, ncclSum, h->comm, h->st);
+        if (nr == ncclSuccess) nr = g_nccl.allReduce(h->Qg[0], h->Qg[0], (size_t)n * k, ncclFloat64, ncclSum, h->comm, h->st);
+        if (nr != ncclSuccess) return fail(h, WLR_ENCCL, "ncclAllReduce(init A^T A, Q_0)");
+      }
     }
   }
   CUDA_TRY(h, cudaMemcpy2DAsync(h->G[0], k * 8, gram, n * 8, k * 8, k, cudaMemcpyDeviceToDevice, h->st));
   CUDA_TRY(h, cudaMemcpy2DAsync(h->M[0], nk * 8, gram + k, n * 8, nk * 8, k, cudaMemcpyDeviceToDevice, h->st));
   if (o.init != WLR_INIT_GIVEN)
     CUDA_TRY(h, cudaMemcpy2DAsync(h->GA, nk * 8, gram + k * n + k, n * 8, nk * 8, nk, cudaMemcpyDeviceToDevice, h->st));
+  if (h->prop && o.init != WLR_INIT_GIVEN)   // X1_0 = A1: Q_0 = A^T A1, the first k columns of A^T A
+    CUDA_TRY(h, cudaMemcpy2DAsync(h->Qg[0], k * 8, h->AtA, n * 8, k * 8, n, cudaMemcpyDeviceToDevice, h->st));
+  if (h->prop) {   // ||A1||_F^2 = tr(A^T A)(0:k, 0:k)
+    std::vector<double> diag(k);
+    CUDA_TRY(h, cudaMemcpy2DAsync(diag.data(), 8, h->AtA, (n + 1) * 8, 8, k, cudaMemcpyDeviceToHost, h->st));
+    CUDA_TRY(h, cudaStreamSynchronize(h->st));
+    double a1 = 0.0;
+    for (double v : diag) a1 += v;
+    h->a1sq = a1;
+  }
   // ||A2||_F^2 = tr(G_A)
   {
     std::vector<double> diag(nk);
@@ -1533,6 +1666,11 @@ extern "C" void wlr_destroy(wlr_handle h) {
   for (auto e : h->pr.pool) cudaEventDestroy(e);
   if (h->h_scal) pinned_give(h->h_scal);
   if (h->st2) { cudaStreamSynchronize(h->st2); cudaStreamDestroy(h->st2); }
+  if (h->st3) { cudaStreamSynchronize(h->st3); cudaStreamDestroy(h->st3); }
+  if (h->ev_f3) cudaEventDestroy(h->ev_f3);
+  if (h->ev_j3) cudaEventDestroy(h->ev_j3);
+  if (h->st4) { cudaStreamSynchronize(h->st4); cudaStreamDestroy(h->st4); }
+  if (h->ev_j4) cudaEventDestroy(h->ev_j4);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
   for (auto ev : h->rp_ev) if (ev) cudaEventDestroy(ev);

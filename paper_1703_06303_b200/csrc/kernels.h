@@ -79,6 +79,7 @@ struct RowPassTcArgs {
   int64_t m_main; int extra;
   unsigned long long* tstamp;       // diagnostics: 8 globaltimer stamps per CTA, or nullptr
   int dbg;                          // diagnostics: bit 2 skip W loads, bit 3 skip epilogue
+  int pdl;                          // host: launch as a programmatic dependent (no griddepcontrol.wait inside)
 };
 constexpr int kTcBM = 128;          // rows per tile (UMMA M)
 // deep = true: 8-stage ring, one CTA per SM (grid <= #SMs); false: 4 stages, 2 CTAs per SM
@@ -103,6 +104,22 @@ struct IncrArgs {
 };
 // per-row SPD solves of the non-uniform X1 half-step (rowsolve.cu), fp32: warp per row,
 // reverse-packed shared-memory Cholesky
+// Gram propagation (prop.cu): uniform W1, the linear X1 half-step's Grams from A^T A
+struct PropArgs {
+  const double* AtA;                // n x n fp64 (once, at init)
+  const void* Wt;                   // W' (KA + KX) x RP row-major, storage dtype (A rows 0..n-1, X rows KA..)
+  int RP, KA;
+  const double* Qp; double* Qn;     // n x k  A^T X1_p, A^T X1_{p+1}
+  const double* Gp;                 // k x k  X1_p^T X1_p (small-step state)
+  double* part;                     // ceil(n/8) x 2 x k x k per-block partials (scratch)
+  double* inc;                      // packed [N | Gamma | Omega | f_w] for the small step (f_w not written)
+  int n, k;
+};
+size_t prop1_smem(int n);
+size_t prop1_smem(int n, int k);
+size_t prop_part_doubles(int n, int k);
+cudaError_t launch_prop(const PropArgs& a, bool f64, int pdl, cudaStream_t st, cudaEvent_t after1 = nullptr);
+
 struct RowSolveArgs {
   const float* E;                   // m x kp  e_i (written by the row pass; >= 8 floats of slack after)
   const float* S;                   // k x k8  C C^T, ld k8 = round_up(k, 8), zero columns k..k8-1

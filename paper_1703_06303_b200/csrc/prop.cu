@@ -1,0 +1,319 @@
+// prop.cu -- Gram propagation for the LINEAR X1 half-step (uniform W1).
+//
+// With uniform W1 every row of the X1 half-step (Algorithm 1 lines 7-9) is the
+// same linear map of z = [A(i,:) | X1_p(i,:)]:  X1_{p+1} = A W'_A + X1_p W'_X  (W' built by K3).
+// The small step only needs Grams of X1_{p+1}, and those follow EXACTLY from the n x n Gram
+// A^T A (fp64, computed once at init) and the running Q_p = A^T X1_p, G_p = X1_p^T X1_p:
+//     Q_{p+1} = A^T A W'_A + Q_p W'_X                          (n x k)
+//     H       = X1_{p+1}^T X1_p = W'_A^T Q_p + W'_X^T G_p       (k x k)
+//     G_{p+1} = Q_{p+1}^T W'_A + H W'_X                         (k x k)
+//     M_{p+1} = X1_{p+1}^T A2 = Q_{p+1}(k:n, :)^T
+// They are written in the packed increment format the small step consumes
+// [N = M_{p+1} - M_p | Gamma = H - G_p | Omega = G_{p+1} - H - H^T + G_p | (f_w)], so K3 is
+// unchanged and no pass over the m rows is on its path (the row pass materialises X1_{p+1}
+// beside it and supplies f_w = sum W1^2 (A1 - X1_{p+1})^2 from the stored rows: the closed form
+// w^2 (||A1||^2 - 2 tr Q + tr G) cancels to ~1e-16 ||A1||^2 / ||A1 - X1||^2, too coarse in fp64 mode).
+// W' is read in the storage dtype the row pass uses (fp32 in fp32 mode), upcast exactly.
+//
+// prop1: CTA b owns the 8 rows [8b, 8b + 8) of the n index: Q_{p+1} rows (A^T A rows and all of
+//        W' staged in shared memory), N columns, and the per-block partials
+//        Hp[b] = W'_A(rows)^T Q_p(rows), Gp[b] = Q_{p+1}(rows)^T W'_A(rows)   (k x k each).
+// prop2: CTA a sums row a (and column a) of the partials in block order and adds the k x k terms:
+//        row a of H, of H^T, of G_{p+1}; writes row a of Gamma and Omega.
+// fp64 throughout; every sum has a fixed order (replicas and reruns bitwise identical).
+#include "kernels.h"
+
+namespace wlr {
+
+constexpr int kPropT = 256;        // prop2 threads
+constexpr int kPropT1 = 256;       // prop1 threads: 32 lanes (columns l) x 8 groups (j ranges)
+constexpr int kPropG = kPropT1 / 32;
+constexpr int kPropRB = 4;         // n-index rows per prop1 CTA
+
+template <typename T>
+WLR_DEVI double wld(const void* W, int64_t i) { return (double)reinterpret_cast<const T*>(W)[i]; }
+
+// shared layout of prop1: AtA rows (8 x n doubles) | reduction (8 x 8 x 32 doubles) | Q_p, Q_{p+1}
+// rows (8 x k doubles each) | W'_A rows 0..n-1 and W'_X rows (k), RP elements each in the storage
+// dtype, bulk-copied (fp32: RP = 32 for k <= 32, so W' is 80 KB) | mbarrier
+// reduction slots x columns of prop1 (the shuffle path when k rounds to 8 column blocks)
+__host__ __device__ inline int prop1_slots(int k) {   // (slots x 4 ncb doubles per row)
+  const int ncb = (k + 3) / 4;
+  return ncb == 8 ? (kPropT1 / 32) * 32 : (kPropT1 / ncb) * 4 * ncb;
+}
+static size_t prop1_wbytes(int n, int k, int RP, int es) { return (size_t)(n + k) * RP * es; }
+size_t prop1_smem(int n, int k, int RP, int es) {
+  return sizeof(double) * ((size_t)kPropRB * n + (size_t)kPropRB * prop1_slots(k) + 2 * kPropRB * k) +
+         prop1_wbytes(n, k, RP, es) + 32;
+}
+size_t prop1_smem(int n) { return prop1_smem(n, 32, 32, 4); }
+size_t prop1_smem(int n, int k) { return prop1_smem(n, k, (k + 31) / 32 * 32, 4); }
+
+template <typename T>
+__global__ void __launch_bounds__(kPropT1) prop1_kernel(const __grid_constant__ PropArgs a) {
+  extern __shared__ __align__(16) double pr_sm[];
+  const int n = a.n, k = a.k, nk = n - k, RP = a.RP, kk = k * k;
+  const int tid = threadIdx.x, lane = tid & 31, grp = tid >> 5;     // kPropG groups split the j sum
+  const int b = blockIdx.x, i0 = b * kPropRB, nr = min(kPropRB, n - i0);
+  double* rows = pr_sm;                                  // nr x n rows of A^T A
+  double* red = rows + kPropRB * n;                      // kPropG groups x kPropRB rows x 32
+  double* Qps = red + kPropRB * prop1_slots(k);                  // nr x k  Q_p rows
+  double* Qns = Qps + kPropRB * k;                       // nr x k  Q_{p+1} rows
+  T* Wr = reinterpret_cast<T*>(Qns + kPropRB * k);       // (n + k) x RP  [W'_A ; W'_X], storage dtype
+  uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(Wr) + (size_t)(n + k) * RP * sizeof(T));
+  const uint32_t wa_bytes = (uint32_t)((size_t)n * RP * sizeof(T)), wx_bytes = (uint32_t)((size_t)k * RP * sizeof(T));
+  const bool bulk_rows = ((size_t)n * 8) % 16 == 0;      // A^T A rows by bulk copy when 16-byte aligned
+  // two barriers, each used for ONE phase: a parity wait on a barrier that has since moved two
+  // phases on (rows, then W') would wait for a phase that never completes
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+    mbar_init_fence();
+    if (bulk_rows) {                                     // (init data: before the dependency wait)
+      mbar_expect_tx(bar + 1, (uint32_t)(nr * n * 8));
+      bulk_load_1d(rows, a.AtA + (int64_t)i0 * n, (uint32_t)(nr * n * 8), bar + 1);
+    }
+  }
+  if (!bulk_rows) {
+    for (int r0 = 0; r0 < nr * n; r0 += 8 * kPropT1) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int idx = r0 + u * kPropT1 + tid;
+        v[u] = idx < nr * n ? a.AtA[(int64_t)i0 * n + idx] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int idx = r0 + u * kPropT1 + tid;
+        if (idx < nr * n) rows[idx] = v[u];
+      }
+    }
+  }
+  __syncthreads();
+  pdl_wait();                                            // W' (K3) and Q_p (previous prop)
+  if (tid == 0) {                                        // W' rows by two bulk copies
+    mbar_expect_tx(bar, wa_bytes + wx_bytes);
+    bulk_load_1d(Wr, a.Wt, wa_bytes, bar);
+    bulk_load_1d(Wr + (size_t)n * RP, reinterpret_cast<const T*>(a.Wt) + (size_t)a.KA * RP, wx_bytes, bar);
+  }
+  for (int idx = tid; idx < nr * k; idx += kPropT1) Qps[idx] = a.Qp[(int64_t)i0 * k + idx];
+  if (bulk_rows) mbar_wait(bar + 1, 0);                  // the A^T A rows
+  mbar_wait(bar, 0);                                     // W'
+  __syncthreads();
+#define Ws(j, l) ((double)Wr[(int64_t)(j) * RP + (l)])
+  // Q_{p+1} rows: thread = (column block cb of 4 columns, j group jg); 4 rows x 4 columns of
+  // accumulators; the j groups are summed through shared memory in a fixed order
+  {
+    const int ncb = (k + 3) / 4, njg = kPropT1 / ncb;      // (k <= 128: ncb <= 32, njg >= 8)
+    const int cb = tid % ncb, jg = tid / ncb;
+    double acc[kPropRB][4];
+#pragma unroll
+    for (int r = 0; r < kPropRB; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
+    if (jg < njg) {
+      const int jlo = (int)((int64_t)n * jg / njg), jhi = (int)((int64_t)n * (jg + 1) / njg);
+#pragma unroll 2
+      for (int j = jlo; j < jhi; ++j) {
+        double wv[4];
+        if constexpr (sizeof(T) == 4) {
+          const float4 w4 = *reinterpret_cast<const float4*>(Wr + (int64_t)j * RP + 4 * cb);
+          wv[0] = w4.x; wv[1] = w4.y; wv[2] = w4.z; wv[3] = w4.w;
+        } else {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) wv[c] = (double)Wr[(int64_t)j * RP + 4 * cb + c];
+        }
+#pragma unroll
+        for (int r = 0; r < kPropRB; ++r) {
+          const double av = rows[r * n + j];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[r][c] = fma(av, wv[c], acc[r][c]);
+        }
+      }
+      if (jg == njg - 1)                                 // + Q_p W'_X
+        for (int q = 0; q < k; ++q) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const double wv = (double)Wr[(int64_t)(n + q) * RP + 4 * cb + c];
+#pragma unroll
+            for (int r = 0; r < kPropRB; ++r) acc[r][c] = fma(Qps[r * k + q], wv, acc[r][c]);
+          }
+        }
+    }
+    // fixed-order sum over the j groups: within a warp by shuffles (ncb = 8: 4 j groups per warp),
+    // then over the warps through shared memory, slots [warp][r][4 cb + c]
+    double* red2 = red;                                  // 8 warps x kPropRB x (4 ncb) doubles
+    const int w4 = 4 * ncb;
+    const bool shfl = ncb == 8;
+    if (shfl) {
+#pragma unroll
+      for (int r = 0; r < kPropRB; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          acc[r][c] += __shfl_xor_sync(0xffffffffu, acc[r][c], 8);
+          acc[r][c] += __shfl_xor_sync(0xffffffffu, acc[r][c], 16);
+        }
+    }
+    const int nslot = shfl ? kPropT1 / 32 : njg, slot = shfl ? tid / 32 : jg;
+    if (jg < njg && (!shfl || (tid & 31) < 8))
+#pragma unroll
+      for (int r = 0; r < kPropRB; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) red2[((int64_t)slot * kPropRB + r) * w4 + 4 * cb + c] = acc[r][c];
+    __syncthreads();
+    for (int o = tid; o < kPropRB * w4; o += kPropT1) {
+      const int r = o / w4, ll = o - r * w4;
+      if (r < nr && ll < k) {
+        double v = 0.0;
+        for (int g = 0; g < nslot; ++g) v += red2[((int64_t)g * kPropRB + r) * w4 + ll];
+        const int i = i0 + r;
+        Qns[r * k + ll] = v;
+        a.Qn[(int64_t)i * k + ll] = v;
+        if (i >= k) a.inc[(int64_t)ll * nk + (i - k)] = v - Qps[r * k + ll];   // N = M_{p+1} - M_p
+      }
+    }
+    __syncthreads();
+  }
+  // per-block partials of H and of Q_{p+1}^T W'_A over the block's rows
+  double* hp = a.part + (int64_t)b * 2 * kk;
+  for (int idx = tid; idx < kk; idx += kPropT1) {
+    const int ar = idx / k, l = idx - ar * k;
+    double h = 0.0, g = 0.0;
+    for (int r = 0; r < nr; ++r) {
+      h = fma(Ws(i0 + r, ar), Qps[r * k + l], h);
+      g = fma(Qns[r * k + ar], Ws(i0 + r, l), g);
+    }
+    hp[idx] = h;
+    hp[kk + idx] = g;
+  }
+#undef Ws
+  pdl_trigger();
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kPropT) prop2_kernel(const __grid_constant__ PropArgs a) {
+  __shared__ double hrow[128], hcol[128], grow[128];
+  extern __shared__ __align__(16) double p2_sm[];
+  const int n = a.n, k = a.k, nk = n - k, RP = a.RP, kk = k * k;
+  const int tid = threadIdx.x;
+  const int ar = blockIdx.x;                               // row a
+  const int nb = (n + kPropRB - 1) / kPropRB;
+  double* Wx = p2_sm;                                      // k x k   W'_X
+  double* Gs = Wx + kk;                                    // k x k   G_p
+  for (int r0 = 0; r0 < kk; r0 += 4 * kPropT) {           // (G_p: not written by prop1)
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { const int idx = r0 + u * kPropT + tid; v[u] = idx < kk ? a.Gp[idx] : 0.0; }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { const int idx = r0 + u * kPropT + tid; if (idx < kk) Gs[idx] = v[u]; }
+  }
+  for (int r0 = 0; r0 < kk; r0 += 4 * kPropT) {
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int idx = r0 + u * kPropT + tid, q = idx / k;
+      v[u] = idx < kk ? wld<T>(a.Wt, (int64_t)(a.KA + q) * RP + (idx - q * k)) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { const int idx = r0 + u * kPropT + tid; if (idx < kk) Wx[idx] = v[u]; }
+  }
+  pdl_wait();
+  // block sums (fixed order) + the k x k terms
+  // 8 threads per output: thread g of an output sums the blocks b = g (mod 8) (16 loads in flight),
+  // then a fixed shuffle tree; outputs: row a of H, column a of H, row a of Q_{p+1}^T W'_A
+  const int g = tid & 7;
+  for (int o0 = 0; o0 < 3 * k; o0 += kPropT / 8) {
+    const int o = o0 + tid / 8;
+    const int which = o < 3 * k ? o / k : 0, c = o < 3 * k ? o - which * k : 0;
+    const int64_t off = which == 0 ? ar * k + c : which == 1 ? c * k + ar : kk + ar * k + c;
+    double v = 0.0;
+    if (o < 3 * k) {
+      for (int b0 = 0; b0 < nb; b0 += 128) {
+        double x[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int bb = b0 + g + 8 * u;
+          x[u] = bb < nb ? a.part[(int64_t)bb * 2 * kk + off] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v += x[u];
+      }
+    }
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    v += __shfl_xor_sync(0xffffffffu, v, 4);
+    if (g == 0 && o < 3 * k) {
+      if (which == 0) hrow[c] = v;
+      else if (which == 1) hcol[c] = v;
+      else grow[c] = v;
+    }
+  }
+  __syncthreads();
+  for (int o = tid; o < 2 * k; o += kPropT) {    // + W'_X^T G_p terms of H (row a) and H^T (column a)
+    const int c = o < k ? o : o - k;
+    double v = 0.0;
+    if (o < k) {
+      for (int q = 0; q < k; ++q) v = fma(Wx[q * k + ar], Gs[q * k + c], v);
+      hrow[c] += v;
+    } else {
+      for (int q = 0; q < k; ++q) v = fma(Wx[q * k + c], Gs[q * k + ar], v);
+      hcol[c] += v;
+    }
+  }
+  __syncthreads();
+  double* gam = a.inc + (int64_t)k * nk;
+  double* om = gam + (int64_t)kk;
+  for (int c = tid; c < k; c += kPropT) {
+    double g = grow[c];                                    // G_{p+1}[a][c] = ... + (H W'_X)[a][c]
+    for (int q = 0; q < k; ++q) g = fma(hrow[q], Wx[q * k + c], g);
+    const double gp = Gs[ar * k + c];
+    gam[ar * k + c] = hrow[c] - gp;
+    om[ar * k + c] = g - hrow[c] - hcol[c] + gp;
+  }
+  pdl_trigger();
+}
+
+cudaError_t launch_prop(const PropArgs& a, bool f64, int pdl, cudaStream_t st, cudaEvent_t after1) {
+  const size_t sm1 = prop1_smem(a.n, a.k, a.RP, f64 ? 8 : 4);
+  const size_t sm2 = sizeof(double) * 2 * (size_t)a.k * a.k;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cudaLaunchConfig_t c1{};
+  c1.gridDim = dim3((a.n + kPropRB - 1) / kPropRB);
+  c1.blockDim = dim3(kPropT1);
+  c1.dynamicSmemBytes = sm1;
+  c1.stream = st;
+  c1.attrs = at;
+  c1.numAttrs = 1;
+  cudaError_t e;
+  if (f64) {
+    cudaFuncSetAttribute(prop1_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
+    e = cudaLaunchKernelEx(&c1, prop1_kernel<double>, a);
+  } else {
+    cudaFuncSetAttribute(prop1_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
+    e = cudaLaunchKernelEx(&c1, prop1_kernel<float>, a);
+  }
+  if (e != cudaSuccess) return e;
+  if (after1 && (e = cudaEventRecord(after1, st)) != cudaSuccess) return e;   // (prop1 done)
+  cudaLaunchAttribute at2[1];
+  at2[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at2[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t c2{};
+  c2.gridDim = dim3(a.k);
+  c2.blockDim = dim3(kPropT);
+  c2.dynamicSmemBytes = sm2;
+  c2.stream = st;
+  c2.attrs = at2;
+  c2.numAttrs = 1;
+  if (f64) {
+    cudaFuncSetAttribute(prop2_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+    return cudaLaunchKernelEx(&c2, prop2_kernel<double>, a);
+  }
+  cudaFuncSetAttribute(prop2_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+  return cudaLaunchKernelEx(&c2, prop2_kernel<float>, a);
+}
+
+size_t prop_part_doubles(int n, int k) { return (size_t)((n + kPropRB - 1) / kPropRB) * 2 * k * k; }
+
+}  // namespace wlr

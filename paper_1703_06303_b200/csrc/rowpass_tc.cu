@@ -90,7 +90,12 @@ __global__ void __launch_bounds__(tc_threads<NR>(), NR >= 8 ? 1 : 2) row_pass_tc
   // block-wide barrier (the loads do not wait for the TMEM allocation)
   const bool xtra = L::XB > 0 && a.extra > 0;
   const int xr0 = (int)(a.m_main + (int64_t)a.extra * blockIdx.x);   // first leftover row
-  auto issue = [&](int64_t g, int s, int c, int64_t tile) {
+  auto issue = [&](int64_t g, int s, int lc, int64_t tile) {
+    // chunk order 1, 2, ..., nch - 1, 0: the A1 chunk (whose w^2 K^{-1} term carries most of
+    // x' in magnitude) is accumulated LAST, so the tensor core's fp32 accumulator holds only the
+    // small terms while the other ~600 products are added (each MMA rounds its sum into the
+    // accumulator: with the large term first, ~250 roundings at |x'| gave ~5e-6 relative error)
+    const int c = lc + 1 == nch ? 0 : lc + 1;
     const int r0 = (int)(tile * kTcBM);
     unsigned char* st = rawst + s * L::STAGE;
     mbar_expect_tx(&full[s], (uint32_t)(L::ZB + 2 * L::WB + (xtra ? 512 : 0)));
@@ -190,9 +195,14 @@ __global__ void __launch_bounds__(tc_threads<NR>(), NR >= 8 ? 1 : 2) row_pass_tc
         const unsigned char* st = rawst + r * L::STAGE;
         const float4* xb = reinterpret_cast<const float4*>(st + L::ZB + 2 * L::WB);   // [4 rows][8 units]
         const float4* wrow = reinterpret_cast<const float4*>(st + L::ZB) + (lane < RP ? lane : 0) * 8;
+        const float4* wlow = reinterpret_cast<const float4*>(st + L::ZB + L::WB) + (lane < RP ? lane : 0) * 8;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          const float4 wv = lane < RP ? wrow[q ^ (lane & 7)] : make_float4(0.f, 0.f, 0.f, 0.f);
+          float4 wv = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (lane < RP) {                                    // W' = hi + lo (the 3xTF32 pair)
+            const float4 h4 = wrow[q ^ (lane & 7)], l4 = wlow[q ^ (lane & 7)];
+            wv = make_float4(h4.x + l4.x, h4.y + l4.y, h4.z + l4.z, h4.w + l4.w);
+          }
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const float4 z = xb[e * 8 + q];                   // broadcast
@@ -213,7 +223,7 @@ __global__ void __launch_bounds__(tc_threads<NR>(), NR >= 8 ? 1 : 2) row_pass_tc
             if (e < a.extra && xr < a.m && lane < a.kp) {
               const float x = lane < a.k ? acc[e] : 0.f;
               a.Xnew[xr * a.kp + lane] = x;
-              a.Dnew[xr * a.kp + lane] = x - a.Xold[xr * a.kp + lane];
+              if (a.Dnew) a.Dnew[xr * a.kp + lane] = x - a.Xold[xr * a.kp + lane];
               if (lane < a.k) {
                 const double d = (double)a.A[xr * a.lda + lane] - (double)x;
                 fw += (double)a.w2s * d * d;
@@ -239,6 +249,7 @@ __global__ void __launch_bounds__(tc_threads<NR>(), NR >= 8 ? 1 : 2) row_pass_tc
       if (g == 0 && tid == 0) stamp(1);
       if (g >= kTcNL) twait(&lofree[l], phl ^ 1, w_lofree);
       const unsigned long long tc0 = a.tstamp ? clock64() : 0;
+      const int pc = c + 1 == nch ? 0 : c + 1;      // physical chunk of logical chunk c (see issue)
       {   // this thread's row (32 warp + lane) of the chunk: 8 swizzled 16-byte units
         const int rr = 32 * warp + lane;
         const float4* src = reinterpret_cast<const float4*>(rawst + r * L::STAGE) + rr * 8;
@@ -246,8 +257,8 @@ __global__ void __launch_bounds__(tc_threads<NR>(), NR >= 8 ? 1 : 2) row_pass_tc
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const float4 v = src[q ^ (rr & 7)];
-          if (RP <= 32 && c == 0) a1r[q] = v;            // A1 (epilogue operand)
-          if (RP <= 32 && c == nchA) xor_[q] = v;        // X1_p
+          if (RP <= 32 && pc == 0) a1r[q] = v;           // A1 (epilogue operand)
+          if (RP <= 32 && pc == nchA) xor_[q] = v;       // X1_p
           tf32_split(v.x, hi[4 * q], lo[4 * q]);
           tf32_split(v.y, hi[4 * q + 1], lo[4 * q + 1]);
           tf32_split(v.z, hi[4 * q + 2], lo[4 * q + 2]);
@@ -286,7 +297,10 @@ __global__ void __launch_bounds__(tc_threads<NR>(), NR >= 8 ? 1 : 2) row_pass_tc
             const float4* ap = reinterpret_cast<const float4*>(a.A + row * a.lda + c0);
 #pragma unroll
             for (int q = 0; q < 8; ++q)
-              if (q < nv) { xo[q] = __ldg(xp + q); ar[q] = __ldg(ap + q); }
+              if (q < nv) {
+                ar[q] = __ldg(ap + q);
+                if (a.Dnew) xo[q] = __ldg(xp + q);   // (Gram-propagation mode: no Delta)
+              }
           }
           float v[32];
           {
@@ -317,7 +331,7 @@ __global__ void __launch_bounds__(tc_threads<NR>(), NR >= 8 ? 1 : 2) row_pass_tc
                   }
                 }
                 xn[q] = make_float4(xq[0], xq[1], xq[2], xq[3]);
-                dn[q] = make_float4(dq[0], dq[1], dq[2], dq[3]);
+                if (a.Dnew) dn[q] = make_float4(dq[0], dq[1], dq[2], dq[3]);
               }
             }
           }
@@ -375,6 +389,19 @@ static cudaError_t launch_tc(const RowPassTcArgs& a, int grid, cudaStream_t st, 
     configured = true;
   }
   if (occ) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kern, tc_threads<NR>(), smem);
+  if (a.pdl) {   // programmatic dependent of the kernel before it on st (it never waits on that one)
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t c{};
+    c.gridDim = dim3(grid);
+    c.blockDim = dim3(tc_threads<NR>());
+    c.dynamicSmemBytes = smem;
+    c.stream = st;
+    c.attrs = at;
+    c.numAttrs = 1;
+    return cudaLaunchKernelEx(&c, kern, a);
+  }
   kern<<<grid, tc_threads<NR>(), smem, st>>>(a);
   return cudaGetLastError();
 }

@@ -29,6 +29,7 @@
 #include <cooperative_groups.h>
 
 #include "kernels.h"
+#include "umma.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -687,6 +688,9 @@ WLR_DEVI void s_apply(SS& s, const SmallArgs& a, const double* Cs, int ldc, cons
 template <int BT, int PART>
 __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_constant__ SmallArgs a) {
   if (PART != 1) pdl_wait();                   // (part 1 waits inside its first load round)
+  // a programmatic dependent may start now: the only one is the propagation iteration's row pass,
+  // which reads W'_p / X1_p (never this kernel's outputs) and never waits on it
+  if (PART == 1) pdl_trigger();
   constexpr int PW = BT <= 8 ? BT : (BT <= 16 ? (BT + 1) / 2 : (BT + 3) / 4);
   extern __shared__ __align__(16) double ss_smem[];
   __shared__ double red[8 * kSSW];
@@ -1171,11 +1175,11 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
       if (a.dtype) reinterpret_cast<double*>(a.Wt)[o] = v;
       else reinterpret_cast<float*>(a.Wt)[o] = (float)v;
       if (a.WtT) {   // K-major fp32 copy W'^T and its 3xTF32 low part (tensor-core row pass)
-        const float f = (float)v;
-        const float hi = __uint_as_float(__float_as_uint(f) & 0xFFFFE000u);
+        float hi, lo;
+        tf32_split((float)v, hi, lo);          // 3xTF32 operand pair (umma.cuh)
         float* wt = reinterpret_cast<float*>(a.WtT) + (int64_t)l * a.KW + row;
-        wt[0] = f;
-        wt[(int64_t)RP * a.KW] = f - hi;
+        wt[0] = hi;
+        wt[(int64_t)RP * a.KW] = lo;
       }
     };
     // Wt rows k + rs + c (columns of A2 in this slice): u K^{-1} (FP64 tensor cores, into the free
@@ -1225,11 +1229,11 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
           v = 0.0;
           for (int q = 0; q < k; ++q) v = fma(ur[q], Xq[q * k + l], v);
         }
-        const float f = (float)v;
-        const float hi = __uint_as_float(__float_as_uint(f) & 0xFFFFE000u);
+        float hi, lo;
+        tf32_split((float)v, hi, lo);
         float* wt = reinterpret_cast<float*>(a.WtT) + (int64_t)l * a.KW + k + s.rs + c;
-        wt[0] = f;
-        wt[(int64_t)RP * a.KW] = f - hi;
+        wt[0] = hi;
+        wt[(int64_t)RP * a.KW] = lo;
       }
     }
     tmark(s, a);                               // (W': A2 rows)

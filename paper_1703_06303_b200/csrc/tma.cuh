@@ -58,6 +58,15 @@ WLR_DEVI void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int 
       : "memory");
 }
 
+// 1-D bulk copy global -> shared (bytes % 16 == 0, both addresses 16-byte aligned), completion
+// signalled on bar (complete_tx bytes)
+WLR_DEVI void bulk_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // element offset of (row r, column c) in a [rows][PE] panel written by TMA with
 // SWIZZLE_128B (PE = 128 / sizeof(T) elements per row; 16-byte chunks XOR row % 8)
 template <typename T>

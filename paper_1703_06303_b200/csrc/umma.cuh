@@ -102,10 +102,21 @@ WLR_DEVI void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// 3xTF32 split: hi = x with the 13 low mantissa bits cleared (exact TF32), lo = x - hi (exact)
+// x rounded to the nearest TF32 value (10 explicit mantissa bits; the low 13 bits come out zero,
+// so the tensor core's truncation of its operands leaves it unchanged)
+WLR_DEVI float tf32_rn(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// 3xTF32 split: hi = RN_tf32(x), lo = RN_tf32(x - hi) (x - hi is exact in fp32).  Rounding both
+// parts to nearest (instead of truncating them) makes the split's error ~2^-22 |x| and UNBIASED:
+// truncation biases every product toward zero, and the bias accumulated to ~6e-6 relative in X1
+// over a 630-term row update (measured, scripts/diag_drift.py).
 WLR_DEVI void tf32_split(float x, float& hi, float& lo) {
-  hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
-  lo = x - hi;
+  hi = tf32_rn(x);
+  lo = tf32_rn(x - hi);
 }
 
 }  // namespace wlr

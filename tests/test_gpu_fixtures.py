@@ -25,8 +25,12 @@ FIX = os.path.join(os.path.dirname(os.path.abspath(__file__)), "fixtures")
 # rel_p is compared where the oracle's relative step is above this (below it the fp32 iterate's
 # own rounding, ~1e-8 .. 1e-7 relative per step, is the step)
 REL_RESOLVED = 1e-5
-# Gram drift (fp64 running sums vs fp64 recomputation from the stored fp32 X1), relative to ||G||, ||M||
-GRAM_DRIFT = 1e-7
+# Gram drift (fp64 running sums vs fp64 recomputation from the stored fp32 X1), relative to ||G||, ||M||.
+# Incremental Grams (non-uniform W1) accumulate fp32 increments of the stored rows: measured
+# 1e-13 .. 4e-11.  Gram propagation (uniform fp32 W1) follows the exact-arithmetic
+# iterate of the fp32 maps, and the stored X1 differs from it by its own fp32 rounding (2^-24 per
+# entry) plus the row pass's 3xTF32 error: ||G - X1^T X1|| / ||G|| ~ 1.1e-7 measured at config 3.
+GRAM_DRIFT = 5e-7
 
 
 def _load(ci):
