@@ -79,7 +79,22 @@ typedef struct {
                              caller stream, the caller orders device inputs before wlr_init. */
   int32_t use_graph;      /* 1: replay each iteration as a captured CUDA graph (default)  */
   int32_t seed;           /* seed of the eigensolver's cold-start block (host PCG)        */
+  void* vgroup;           /* wlr_vgroup (see wlr_vgroup_create) or NULL: virtual ranks      */
 } wlr_opts;
+
+/* Virtual ranks (validation hook for the row-sharded path on ONE GPU).  A group of G members:
+ * member g is a handle created with opts.vgroup = group, opts.nranks = G, opts.rank = g,
+ * opts.m_global / opts.row_offset of its contiguous row shard, each handle
+ * driven by its own host thread (like one process per GPU).  Every sum that the NCCL path
+ * all-reduces over ranks (the init Grams; per iteration, the Gram increments [N, Gamma, Omega,
+ * f_w] of non-uniform W1 -- uniform W1 exchanges nothing per iteration) is formed
+ * instead by a fixed-order device sum over the members' buffers, so the replicated small-step state
+ * (C, V, F) must come out bitwise identical on every member.  Graph capture is disabled for
+ * members.  Every member must make the same sequence of calls; a member that fails leaves the
+ * others waiting (test use only).  Errors: WLR_EINVAL (G < 1), WLR_ENOMEM.                    */
+typedef struct wlr_vgroup_s* wlr_vgroup;
+wlr_status wlr_vgroup_create(int32_t G, wlr_vgroup* out);
+void wlr_vgroup_destroy(wlr_vgroup g);
 
 /* Fill *o with defaults (dtype F32, GHS init, eps 0, single rank, graphs on). */
 void wlr_opts_default(wlr_opts* o);

@@ -19,7 +19,7 @@ from ._lib import (WLR_F32, WLR_F64, WLR_INIT_GHS, WLR_INIT_GIVEN, WlrError, che
 
 __all__ = ["wlr_init", "wlr_iterate", "wlr_iterate_async", "wlr_sync", "wlr_objective",
            "wlr_trace", "wlr_result", "wlr_debug_state", "wlr_profile", "wlr_nccl_unique_id",
-           "wlr_destroy", "wlr_version", "Handle", "WlrError", "LIB_PATH"]
+           "wlr_destroy", "wlr_version", "wlr_vgroup_create", "Handle", "VGroup", "WlrError", "LIB_PATH"]
 
 LIB_PATH = _lib.LIB_PATH
 
@@ -78,7 +78,7 @@ def wlr_init(A, k: int, r: int, W1=None, *, w1: float = 1.0, init: str = "ghs", 
              eps: float = 0.0, eig_tol: float = 0.0, eig_block: int = 0, eig_max_outer: int = 0,
              m_global: int = 0, row_offset: int = 0, nranks: int = 1, rank: int = 0,
              nccl_id: Optional[bytes] = None, stream: Optional[int] = None, use_graph: bool = True,
-             seed: int = 0) -> Handle:
+             seed: int = 0, vgroup: Optional["VGroup"] = None) -> Handle:
     """wlr_init: PAPER.md Algorithm 1 lines 1-2 plus the first (C, D) half-step.
     ``W1=None`` uses the uniform weight ``w1``.  ``stream`` is a raw cudaStream_t (e.g.
     ``torch.cuda.current_stream().cuda_stream``); None lets the handle own a stream."""
@@ -116,11 +116,35 @@ def wlr_init(A, k: int, r: int, W1=None, *, w1: float = 1.0, init: str = "ghs", 
         o.nccl_id = ctypes.cast(idbuf, ctypes.c_void_p)
     if stream is not None:
         o.stream = int(stream)
+    if vgroup is not None:
+        o.vgroup = vgroup.raw
     raw = ctypes.c_void_p()
     st = lib.wlr_init(ctypes.byref(raw), pa, A.shape[1] if A.ndim == 2 else n, pw,
                       (W1.shape[1] if W1 is not None else 0), m, n, int(k), int(r), ctypes.byref(o))
     check(st)
     return Handle(raw, (m, n, int(k), int(r)), code, (ka, kw, kx, idbuf))
+
+
+class VGroup:
+    """wlr_vgroup: G virtual ranks on one GPU (include/wlr.h); members are handles created with
+    ``vgroup=``, ``nranks=G``, ``rank=g`` and driven from G host threads."""
+
+    def __init__(self, G: int):
+        self.raw = ctypes.c_void_p()
+        self.G = int(G)
+        check(lib.wlr_vgroup_create(self.G, ctypes.byref(self.raw)))
+
+    def __del__(self):
+        try:
+            if getattr(self, "raw", None) and lib is not None:
+                lib.wlr_vgroup_destroy(self.raw)
+                self.raw = None
+        except Exception:  # interpreter shutdown
+            pass
+
+
+def wlr_vgroup_create(G: int) -> VGroup:
+    return VGroup(G)
 
 
 def wlr_iterate(h: Handle, max_iters: int):

@@ -17,7 +17,7 @@ WLR_INIT_GHS, WLR_INIT_GIVEN = 0, 1
 EXPORTS = ("wlr_opts_default", "wlr_init", "wlr_iterate", "wlr_iterate_async", "wlr_sync",
            "wlr_objective", "wlr_trace", "wlr_result", "wlr_debug_state", "wlr_profile",
            "wlr_nccl_unique_id", "wlr_last_error", "wlr_status_string", "wlr_destroy",
-           "wlr_version", "wlr_als_iterate", "wlr_als_result")
+           "wlr_version", "wlr_als_iterate", "wlr_als_result", "wlr_vgroup_create", "wlr_vgroup_destroy")
 
 
 class wlr_opts(ctypes.Structure):
@@ -38,6 +38,7 @@ class wlr_opts(ctypes.Structure):
         ("stream", ctypes.c_void_p),
         ("use_graph", ctypes.c_int32),
         ("seed", ctypes.c_int32),
+        ("vgroup", ctypes.c_void_p),
     ]
 
 
@@ -49,7 +50,7 @@ class WlrError(RuntimeError):
 
 def _load():
     if not os.path.exists(LIB_PATH):
-        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_1703_06303_b200.build` "
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python paper_1703_06303_b200/build.py` "
                           "(there is no CPU fallback)")
     lib = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
     vp, i32, i64, dbl = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
@@ -72,6 +73,8 @@ def _load():
         "wlr_version": (i32, []),
         "wlr_als_iterate": (i32, [vp, i32, vp, i32]),
         "wlr_als_result": (i32, [vp, vp, i64, vp, vp, i64, vp]),
+        "wlr_vgroup_create": (i32, [i32, P(vp)]),
+        "wlr_vgroup_destroy": (None, [vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

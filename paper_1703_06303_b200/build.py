@@ -1,6 +1,6 @@
 """Build libwlr.so in-tree for sm_100a (nvcc, static cudart, NCCL loaded with dlopen).
 
-    python -m paper_1703_06303_b200.build [--verbose-ptxas] [--force]
+    python paper_1703_06303_b200/build.py [--verbose-ptxas] [--force]
 """
 from __future__ import annotations
 

@@ -13,6 +13,8 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <condition_variable>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -72,6 +74,32 @@ struct Profile {
 };
 
 }  // namespace
+
+// Virtual ranks on one GPU (include/wlr.h wlr_vgroup): a host barrier between the members' threads,
+// per-slot staging buffers and events; the sum is a fixed-order device reduce (vsum_kernel).
+struct wlr_vgroup_s {
+  int G = 1;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  int64_t gen = 0;
+  double* buf[2] = {nullptr, nullptr};   // slot s: G x cap doubles
+  size_t cap = 0;
+  std::vector<cudaEvent_t> ready, done[2];
+  std::vector<char> done_valid[2];
+  void barrier(const std::function<void()>& last = nullptr) {
+    std::unique_lock<std::mutex> lk(mu);
+    const int64_t my = gen;
+    if (++arrived == G) {
+      if (last) last();
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != my; });
+    }
+  }
+};
 
 // f3 block-ALS state (R21; kernels in als.cu)
 struct AlsSt {
@@ -175,6 +203,8 @@ struct wlr_ctx {
   bool pending = false;        // deferred half of the last small step not launched yet
   SmallArgs pend{};
   ncclComm_t comm = nullptr;
+  wlr_vgroup_s* vg = nullptr;  // virtual ranks (test hook), instead of comm
+  int64_t vcalls = 0;
   bool prof = false;
   Profile pr;
   std::string err;
@@ -253,6 +283,64 @@ static wlr_status dalloc(wlr_ctx* h, void** p, size_t bytes) {
 template <typename P>
 static wlr_status dalloc_t(wlr_ctx* h, P** p, size_t count) {
   return dalloc(h, reinterpret_cast<void**>(p), count * sizeof(P));
+}
+
+// Sum of buf (count fp64 values) over the ranks, in place, ordered on st: NCCL across GPUs, or the
+// virtual group's fixed-order device sum; a no-op on one rank.
+static wlr_status group_allreduce(wlr_ctx* h, double* buf, size_t count, cudaStream_t st, const char* what) {
+  if (h->comm) {
+    ncclResult_t nr = g_nccl.allReduce(buf, buf, count, ncclFloat64, ncclSum, h->comm, st);
+    if (nr != ncclSuccess) return fail(h, WLR_ENCCL, std::string("ncclAllReduce(") + what + "): " + g_nccl.errStr(nr));
+    return WLR_OK;
+  }
+  wlr_vgroup_s* g = h->vg;
+  if (!g) return WLR_OK;
+  const int r = h->opts.rank, slot = (int)(h->vcalls++ & 1);
+  cudaError_t ae = cudaSuccess;
+  g->barrier([&] {                           // the last member to arrive sizes the staging buffers
+    if (count > g->cap) {
+      cudaDeviceSynchronize();
+      for (auto& b : g->buf) { if (b) cudaFree(b); b = nullptr; }
+      for (auto& b : g->buf)
+        if (ae == cudaSuccess) ae = cudaMalloc(&b, (size_t)g->G * count * sizeof(double));
+      g->cap = ae == cudaSuccess ? count : 0;
+    }
+  });
+  if (ae != cudaSuccess || !g->buf[slot]) return fail(h, WLR_ENOMEM, "virtual group staging buffers");
+  for (int j = 0; j < g->G; ++j)             // the previous use of this slot has been summed everywhere
+    if (g->done_valid[slot][j]) CUDA_TRY(h, cudaStreamWaitEvent(st, g->done[slot][j], 0));
+  CUDA_TRY(h, cudaMemcpyAsync(g->buf[slot] + (size_t)r * g->cap, buf, count * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(h, cudaEventRecord(g->ready[r], st));
+  g->barrier();
+  for (int j = 0; j < g->G; ++j) CUDA_TRY(h, cudaStreamWaitEvent(st, g->ready[j], 0));
+  CUDA_TRY(h, launch_vsum(buf, g->buf[slot], g->G, g->cap, count, st));
+  CUDA_TRY(h, cudaEventRecord(g->done[slot][r], st));
+  g->done_valid[slot][r] = 1;
+  return WLR_OK;
+}
+
+extern "C" wlr_status wlr_vgroup_create(int32_t G, wlr_vgroup* out) {
+  if (!out || G < 1) return fail(nullptr, WLR_EINVAL, "wlr_vgroup_create: need G >= 1");
+  wlr_vgroup_s* g = new wlr_vgroup_s();
+  g->G = G;
+  g->ready.resize(G);
+  for (int s = 0; s < 2; ++s) { g->done[s].resize(G); g->done_valid[s].assign(G, 0); }
+  for (int j = 0; j < G; ++j) {
+    bool ok = cudaEventCreateWithFlags(&g->ready[j], cudaEventDisableTiming) == cudaSuccess;
+    for (int s = 0; s < 2; ++s) ok = ok && cudaEventCreateWithFlags(&g->done[s][j], cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) { cudaGetLastError(); wlr_vgroup_destroy(g); return fail(nullptr, WLR_ECUDA, "wlr_vgroup_create: events"); }
+  }
+  *out = g;
+  return WLR_OK;
+}
+
+extern "C" void wlr_vgroup_destroy(wlr_vgroup g) {
+  if (!g) return;
+  cudaDeviceSynchronize();
+  for (auto e : g->ready) if (e) cudaEventDestroy(e);
+  for (auto& v : g->done) for (auto e : v) if (e) cudaEventDestroy(e);
+  for (auto b : g->buf) if (b) cudaFree(b);
+  delete g;
 }
 
 static wlr_status flush_pending(wlr_ctx* h);
@@ -422,18 +510,16 @@ static wlr_status enqueue_prop_iteration(wlr_ctx* h, int ph) {
   PropArgs pa{};
   pa.AtA = h->AtA; pa.Wt = cur ? h->Wt1 : h->Wt; pa.RP = h->rp; pa.KA = h->KA;
   pa.Qp = h->Qg[cur]; pa.Qn = h->Qg[nxt]; pa.Gp = h->G[slot]; pa.part = h->Hs;
-  pa.inc = h->inc[cur];
+  pa.inc = h->inc[cur]; pa.dg = h->dgs; pa.counter = h->pcnt;
+  pa.w2 = h->w1s * h->w1s; pa.a1sq = h->a1sq;
   pa.n = (int)h->n; pa.k = (int)h->k;
   SmallArgs sa = small_args(h, ph, 1);
-  const int nfw = h->tc_on ? h->tc_grid : h->rp_grid;
-  double* fw_dst = h->inc[cur] + (h->k * h->nk + 2 * h->k * h->k);   // f_w(X1_{p+1}), read by K3b(p)
   cudaError_t e;
   if (prof) {   // eager profiling pass: everything serial on st, one event group per kernel kind
     cudaEvent_t ev[8];
     for (int i = 0; i < 8; ++i) ev[i] = prof_event(h);
     cudaEventRecord(ev[0], h->st);
     if ((e = launch_row_pass_iter(h, ph, h->st, true)) != cudaSuccess) return fail(h, WLR_ECUDA, std::string("row pass: ") + cudaGetErrorString(e));
-    launch_reduce_incr(h->inc_part, 0, 0, 0, 1, 0, 0, 0, h->fw_part, nfw, fw_dst, h->st);
     cudaEventRecord(ev[1], h->st);
     if ((e = launch_prop(pa, false, 0, h->st)) != cudaSuccess) return fail(h, WLR_ECUDA, std::string("Gram propagation: ") + cudaGetErrorString(e));
     cudaEventRecord(ev[2], h->st);
@@ -469,14 +555,13 @@ static wlr_status enqueue_prop_iteration(wlr_ctx* h, int ph) {
     if (rpt) CUDA_TRY(h, cudaEventRecordWithFlags(h->rp_ev[0], h->st4, cudaEventRecordExternal));
     if ((e = launch_row_pass_iter(h, ph, h->st4, true, !rpt)) != cudaSuccess) return fail(h, WLR_ECUDA, std::string("row pass: ") + cudaGetErrorString(e));
     if (rpt) CUDA_TRY(h, cudaEventRecordWithFlags(h->rp_ev[1], h->st4, cudaEventRecordExternal));
-    launch_reduce_incr(h->inc_part, 0, 0, 0, 1, 0, 0, 0, h->fw_part, nfw, fw_dst, h->st4);
     CUDA_TRY(h, cudaEventRecord(h->ev_j4, h->st4));
     CUDA_TRY(h, cudaStreamWaitEvent(h->st, h->ev_j4, 0));
     if (pend) CUDA_TRY(h, cudaStreamWaitEvent(h->st, h->ev_join, 0));
   }
   h->pend = sa;
   h->pending = true;
-  h->pr.launches += pend ? 6 : 5;
+  h->pr.launches += pend ? 5 : 4;
   return WLR_OK;
 }
 
@@ -551,14 +636,13 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int ph) {
                        (int)h->nk, h->nz, (int)(h->k - h->k0), (int)(h->n - h->k0), (int)h->kp, h->fw_part,
                        nfw, h->inc[cur], h->st, nullptr, ReduceLayout{nullptr, 0, 0, 0, 0}, !prof && !pend);
   if (prof) cudaEventRecord(ev[3], h->st);
-  if (h->comm) {
-    const size_t cnt = (size_t)(h->k * h->nk + 2 * h->k * h->k + 1);
-    ncclResult_t nr = g_nccl.allReduce(h->inc[cur], h->inc[cur], cnt, ncclFloat64, ncclSum, h->comm, h->st);
-    if (nr != ncclSuccess) return fail(h, WLR_ENCCL, std::string("ncclAllReduce: ") + g_nccl.errStr(nr));
+  {
+    wlr_status gs = group_allreduce(h, h->inc[cur], (size_t)(h->k * h->nk + 2 * h->k * h->k + 1), h->st, "increments");
+    if (gs != WLR_OK) return gs;
   }
   if (prof) cudaEventRecord(ev[4], h->st);
   SmallArgs s = small_args(h, ph, 1);
-  s.pdl = (!h->comm && !prof) ? 1 : 0;   // right behind the reduce kernel (no allreduce between)
+  s.pdl = (!h->comm && !h->vg && !prof) ? 1 : 0;   // right behind the reduce kernel (no allreduce between)
   h->last_ss = s;
   e = launch_small_step(s, 1, h->st);
   if (e != cudaSuccess) return fail(h, WLR_ECUDA, std::string("small step: ") + cudaGetErrorString(e));
@@ -635,7 +719,7 @@ static wlr_status launch_iteration(wlr_ctx* h) {
     }
     h->pend = small_args(h, h->ph, 1);
     h->pending = true;
-    h->pr.launches += (pend ? 5 : 4) + (h->prop ? 1 : 0);
+    h->pr.launches += pend ? 5 : 4;
   } else {
     s = enqueue_iteration(h, h->ph);
     if (s != WLR_OK) return s;
@@ -909,6 +993,8 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
     for (int i = 0; i < 2; ++i)
       if ((s = dalloc_t(h, &h->Qg[i], (size_t)n * k)) != WLR_OK) return s;
     if ((s = dalloc_t(h, &h->Hs, prop_part_doubles((int)n, (int)k))) != WLR_OK) return s;
+    if ((s = dalloc_t(h, &h->dgs, (size_t)k)) != WLR_OK) return s;
+    if ((s = dalloc_t(h, &h->pcnt, 1)) != WLR_OK) return s;
   }
   if ((s = dalloc_t(h, &h->fw0, 2)) != WLR_OK) return s;
   if ((s = dalloc_t(h, &h->GA, (size_t)nk * nk)) != WLR_OK) return s;
@@ -948,8 +1034,11 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   if ((s = dalloc_t(h, &h->tdbg, 256)) != WLR_OK) return s;   // K3a marks, K3b marks, exchange stamps
   if ((s = dalloc_t(h, &h->trace, (size_t)h->trace_cap * 4)) != WLR_OK) return s;
 
-  // ---- NCCL communicator (rows sharded over ranks)
-  if (o.nranks > 1) {
+  // ---- NCCL communicator (rows sharded over ranks), or the virtual group (one GPU, test hook)
+  if (o.vgroup) {
+    h->vg = reinterpret_cast<wlr_vgroup_s*>(o.vgroup);
+    if (h->vg->G != o.nranks) return fail(h, WLR_EINVAL, "opts.nranks must equal the virtual group's size");
+  } else if (o.nranks > 1) {
     if (!o.nccl_id) return fail(h, WLR_EINVAL, "nranks > 1 needs opts.nccl_id");
     std::string e;
     if (!g_nccl.load(e)) return fail(h, WLR_ENCCL, e);
@@ -996,18 +1085,13 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
     run_gram(h->A, h->lda, (int)n, h->A, h->lda, (int)n, gram);
     h->AtA = gram;
   }
-  if (h->comm) {
-    // sum the per-rank Grams (rows are sharded, Grams are additive over rows)
-    ncclResult_t nr = g_nccl.allReduce(gram, gram, (size_t)n * n, ncclFloat64, ncclSum, h->comm, h->st);
-    if (nr != ncclSuccess) return fail(h, WLR_ENCCL, "ncclAllReduce(init gram)");
-    if (o.init == WLR_INIT_GIVEN) {
-      nr = g_nccl.allReduce(h->GA, h->GA, (size_t)nk * nk, ncclFloat64, ncclSum, h->comm, h->st);
-      if (nr != ncclSuccess) return fail(h, WLR_ENCCL, "ncclAllReduce(init GA)");
-      if (h->prop) {
-        nr = g_nccl.allReduce(h->AtA, h->AtA, (size_t)n * n, ncclFloat64, ncclSum, h->comm, h->st);
-        if (nr == ncclSuccess) nr = g_nccl.allReduce(h->Qg[0], h->Qg[0], (size_t)n * k, ncclFloat64, ncclSum, h->comm, h->st);
-        if (nr != ncclSuccess) return fail(h, WLR_ENCCL, "ncclAllReduce(init A^T A, Q_0)");
-      }
+  // sum the per-rank Grams (rows are sharded, Grams are additive over rows)
+  if ((s = group_allreduce(h, gram, (size_t)n * n, h->st, "init gram")) != WLR_OK) return s;
+  if (o.init == WLR_INIT_GIVEN) {
+    if ((s = group_allreduce(h, h->GA, (size_t)nk * nk, h->st, "init GA")) != WLR_OK) return s;
+    if (h->prop) {
+      if ((s = group_allreduce(h, h->AtA, (size_t)n * n, h->st, "init A^T A")) != WLR_OK) return s;
+      if ((s = group_allreduce(h, h->Qg[0], (size_t)n * k, h->st, "init Q_0")) != WLR_OK) return s;
     }
   }
   CUDA_TRY(h, cudaMemcpy2DAsync(h->G[0], k * 8, gram, n * 8, k * 8, k, cudaMemcpyDeviceToDevice, h->st));
@@ -1038,10 +1122,7 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
     if (h->dtype == WLR_F32) launch_fw<float>((const float*)h->A, h->lda, (const float*)h->W1, h->ldw, h->w1s * h->w1s, (const float*)h->X[0], (int)kp, h->m, (int)k, h->fw_part, 1184, h->st);
     else launch_fw<double>((const double*)h->A, h->lda, (const double*)h->W1, h->ldw, h->w1s * h->w1s, (const double*)h->X[0], (int)kp, h->m, (int)k, h->fw_part, 1184, h->st);
     launch_reduce_incr(h->inc_part, 0, 0, 0, 1, 0, 0, 0, h->fw_part, 1184, h->fw0, h->st);
-    if (h->comm) {
-      ncclResult_t nr = g_nccl.allReduce(h->fw0, h->fw0, 1, ncclFloat64, ncclSum, h->comm, h->st);
-      if (nr != ncclSuccess) return fail(h, WLR_ENCCL, "ncclAllReduce(fw0)");
-    }
+    if ((s = group_allreduce(h, h->fw0, 1, h->st, "fw0")) != WLR_OK) return s;
   }
   // cold-start block of the eigensolver: deterministic host PRNG (identical on all ranks)
   {
@@ -1097,6 +1178,7 @@ extern "C" wlr_status wlr_init(wlr_handle* out, const void* A, int64_t lda, cons
   if (m_local < k && op.nranks == 1) return fail(nullptr, WLR_EINVAL, "need m >= k");
   wlr_ctx* h = new wlr_ctx();
   h->opts = op;
+  if (op.vgroup) h->opts.use_graph = 0;      // (cross-member event waits cannot be captured)
   // eigensolver target (relative to lambda_1; the S-product rounding floor is added in K3):
   // fp64 mode 1e-12, fp32 mode 1e-7 (DESIGN.md §3 reading R17 "eigensolver tolerance")
   if (h->opts.eig_tol <= 0.0) h->opts.eig_tol = op.dtype == WLR_F64 ? 1e-12 : 1e-7;
@@ -1387,7 +1469,7 @@ static wlr_status als_setup(wlr_ctx* h) {
   wlr_status s = check_flags(h);              // flushes the pending half: F_0 in h_scal
   if (s != WLR_OK) return s;
   if (h->p != 0) return fail(h, WLR_EINVAL, "wlr_als_iterate starts from the GHS state (p = 0)");
-  if (h->comm) return fail(h, WLR_EINVAL, "block ALS: single rank only");
+  if (h->comm || h->vg) return fail(h, WLR_EINVAL, "block ALS: single rank only");
   if (!als_ok((int)h->k, (int)h->t)) return fail(h, WLR_EINVAL, "block ALS: k too large for the small steps");
   // B shares the X1 buffers' kp-wide row layout (row pass, TMA boxes, Gram kernels): r - k must fit
   if (h->t > h->kp) return fail(h, WLR_EINVAL, "block ALS: needs r - k <= round_up(k, 4)");

@@ -111,13 +111,18 @@ struct PropArgs {
   int RP, KA;
   const double* Qp; double* Qn;     // n x k  A^T X1_p, A^T X1_{p+1}
   const double* Gp;                 // k x k  X1_p^T X1_p (small-step state)
-  double* part;                     // ceil(n/8) x 2 x k x k per-block partials (scratch)
-  double* inc;                      // packed [N | Gamma | Omega | f_w] for the small step (f_w not written)
+  double* part;                     // ceil(n/RB) x 2 x k x k per-block partials (scratch)
+  double* inc;                      // packed [N | Gamma | Omega | f_w] for the small step
+  double* dg;                       // k scratch: f_w's diagonal terms
+  int* counter;                     // zero-initialised; prop2's last CTA resets it
+  double w2, a1sq;                  // w^2, ||A1||_F^2
   int n, k;
 };
 size_t prop1_smem(int n);
 size_t prop1_smem(int n, int k);
 size_t prop_part_doubles(int n, int k);
+// virtual-group sum: out[i] = sum_{g < G} in[g * stride + i], g in order (fixed, deterministic)
+cudaError_t launch_vsum(double* out, const double* in, int G, size_t stride, size_t count, cudaStream_t st);
 cudaError_t launch_prop(const PropArgs& a, bool f64, int pdl, cudaStream_t st, cudaEvent_t after1 = nullptr);
 
 struct RowSolveArgs {

@@ -269,6 +269,22 @@ __global__ void __launch_bounds__(kPropT) prop2_kernel(const __grid_constant__ P
     const double gp = Gs[ar * k + c];
     gam[ar * k + c] = hrow[c] - gp;
     om[ar * k + c] = g - hrow[c] - hcol[c] + gp;
+    if (c == ar) a.dg[ar] = g - 2.0 * a.Qn[(int64_t)ar * k + ar];   // f_w's diagonal terms
+  }
+  // f_w = w^2 ||A1 - X1_{p+1}||^2 = w^2 (||A1||^2 + sum_a (G_{p+1} - 2 A1^T X1_{p+1})[a][a]) by the
+  // last CTA, in a fixed order (fp32 mode only: the cancellation costs ~1e-16 w^2 ||A1||^2 absolute,
+  // ~1e-12 of F at configs 2-3), so that no per-iteration quantity depends on the row shards
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last = atomicAdd(a.counter, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (last && tid == 0) {
+    __threadfence();
+    double sd = 0.0;
+    for (int q = 0; q < k; ++q) sd += __ldcg(a.dg + q);
+    om[(int64_t)kk] = a.w2 * (a.a1sq + sd);
+    *a.counter = 0;
   }
   pdl_trigger();
 }
@@ -312,6 +328,20 @@ cudaError_t launch_prop(const PropArgs& a, bool f64, int pdl, cudaStream_t st, c
   }
   cudaFuncSetAttribute(prop2_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
   return cudaLaunchKernelEx(&c2, prop2_kernel<float>, a);
+}
+
+__global__ void vsum_kernel(double* __restrict__ out, const double* __restrict__ in, int G, size_t stride, size_t count) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int g = 0; g < G; ++g) s += in[(size_t)g * stride + i];
+    out[i] = s;
+  }
+}
+
+cudaError_t launch_vsum(double* out, const double* in, int G, size_t stride, size_t count, cudaStream_t st) {
+  const int blocks = (int)std::min<size_t>(1024, (count + 255) / 256);
+  vsum_kernel<<<blocks > 0 ? blocks : 1, 256, 0, st>>>(out, in, G, stride, count);
+  return cudaGetLastError();
 }
 
 size_t prop_part_doubles(int n, int k) { return (size_t)((n + kPropRB - 1) / kPropRB) * 2 * k * k; }
