@@ -21,7 +21,11 @@
 // prop2: CTA a sums row a (and column a) of the partials in block order and adds the k x k terms:
 //        row a of H, of H^T, of G_{p+1}; writes row a of Gamma and Omega.
 // fp64 throughout; every sum has a fixed order (replicas and reruns bitwise identical).
+#include <cooperative_groups.h>
+
 #include "kernels.h"
+
+namespace cg = cooperative_groups;
 
 namespace wlr {
 
@@ -174,8 +178,9 @@ __global__ void __launch_bounds__(kPropT1) prop1_kernel(const __grid_constant__ 
     }
     __syncthreads();
   }
-  // per-block partials of H and of Q_{p+1}^T W'_A over the block's rows
-  double* hp = a.part + (int64_t)b * 2 * kk;
+  // per-block partials of H and of Q_{p+1}^T W'_A over the block's rows, stored for prop2's CTA a
+  // as three contiguous [nb][k] panels: row a of Hp, column a of Hp, row a of Gp
+  const int nb = (n + kPropRB - 1) / kPropRB;
   for (int idx = tid; idx < kk; idx += kPropT1) {
     const int ar = idx / k, l = idx - ar * k;
     double h = 0.0, g = 0.0;
@@ -183,72 +188,80 @@ __global__ void __launch_bounds__(kPropT1) prop1_kernel(const __grid_constant__ 
       h = fma(Ws(i0 + r, ar), Qps[r * k + l], h);
       g = fma(Qns[r * k + ar], Ws(i0 + r, l), g);
     }
-    hp[idx] = h;
-    hp[kk + idx] = g;
+    a.part[(((int64_t)ar * 3 + 0) * nb + b) * k + l] = h;     // H row ar
+    a.part[(((int64_t)l * 3 + 1) * nb + b) * k + ar] = h;     // H column l (entry ar)
+    a.part[(((int64_t)ar * 3 + 2) * nb + b) * k + l] = g;     // Gp row ar
   }
 #undef Ws
   pdl_trigger();
 }
 
+// prop2: one 3-CTA cluster per row a: rank 0 sums row a of the H partials, rank 1 column a of
+// them, rank 2 row a of the Gp partials (each a contiguous [nb][k] panel, 8 warps over the block
+// range); rank 0 gathers the other two sums through distributed shared memory and finishes row a.
 template <typename T>
-__global__ void __launch_bounds__(kPropT) prop2_kernel(const __grid_constant__ PropArgs a) {
+__global__ void __cluster_dims__(3, 1, 1) __launch_bounds__(kPropT) prop2_kernel(const __grid_constant__ PropArgs a) {
+  __shared__ double vrow[128];
   __shared__ double hrow[128], hcol[128], grow[128];
+  __shared__ double wred[8][128];
   extern __shared__ __align__(16) double p2_sm[];
+  cg::cluster_group cl = cg::this_cluster();
   const int n = a.n, k = a.k, nk = n - k, RP = a.RP, kk = k * k;
   const int tid = threadIdx.x;
-  const int ar = blockIdx.x;                               // row a
+  const int ar = blockIdx.x / 3, which = (int)cl.block_rank();
   const int nb = (n + kPropRB - 1) / kPropRB;
-  double* Wx = p2_sm;                                      // k x k   W'_X
-  double* Gs = Wx + kk;                                    // k x k   G_p
-  for (int r0 = 0; r0 < kk; r0 += 4 * kPropT) {           // (G_p: not written by prop1)
-    double v[4];
+  double* Wx = p2_sm;                                      // k x k   W'_X      (rank 0)
+  double* Gs = Wx + kk;                                    // k x k   G_p       (rank 0)
+  if (which == 0) {
+    for (int r0 = 0; r0 < kk; r0 += 4 * kPropT) {         // (G_p, W': not written by prop1)
+      double v[4], x[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) { const int idx = r0 + u * kPropT + tid; v[u] = idx < kk ? a.Gp[idx] : 0.0; }
+      for (int u = 0; u < 4; ++u) {
+        const int idx = r0 + u * kPropT + tid, q = idx / k;
+        v[u] = idx < kk ? a.Gp[idx] : 0.0;
+        x[u] = idx < kk ? wld<T>(a.Wt, (int64_t)(a.KA + q) * RP + (idx - q * k)) : 0.0;
+      }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) { const int idx = r0 + u * kPropT + tid; if (idx < kk) Gs[idx] = v[u]; }
-  }
-  for (int r0 = 0; r0 < kk; r0 += 4 * kPropT) {
-    double v[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int idx = r0 + u * kPropT + tid, q = idx / k;
-      v[u] = idx < kk ? wld<T>(a.Wt, (int64_t)(a.KA + q) * RP + (idx - q * k)) : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) { const int idx = r0 + u * kPropT + tid; if (idx < kk) Wx[idx] = v[u]; }
-  }
-  pdl_wait();
-  // block sums (fixed order) + the k x k terms
-  // 8 threads per output: thread g of an output sums the blocks b = g (mod 8) (16 loads in flight),
-  // then a fixed shuffle tree; outputs: row a of H, column a of H, row a of Q_{p+1}^T W'_A
-  const int g = tid & 7;
-  for (int o0 = 0; o0 < 3 * k; o0 += kPropT / 8) {
-    const int o = o0 + tid / 8;
-    const int which = o < 3 * k ? o / k : 0, c = o < 3 * k ? o - which * k : 0;
-    const int64_t off = which == 0 ? ar * k + c : which == 1 ? c * k + ar : kk + ar * k + c;
-    double v = 0.0;
-    if (o < 3 * k) {
-      for (int b0 = 0; b0 < nb; b0 += 128) {
-        double x[16];
-#pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          const int bb = b0 + g + 8 * u;
-          x[u] = bb < nb ? a.part[(int64_t)bb * 2 * kk + off] : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < 16; ++u) v += x[u];
+      for (int u = 0; u < 4; ++u) {
+        const int idx = r0 + u * kPropT + tid;
+        if (idx < kk) { Gs[idx] = v[u]; Wx[idx] = x[u]; }
       }
     }
-    v += __shfl_xor_sync(0xffffffffu, v, 1);
-    v += __shfl_xor_sync(0xffffffffu, v, 2);
-    v += __shfl_xor_sync(0xffffffffu, v, 4);
-    if (g == 0 && o < 3 * k) {
-      if (which == 0) hrow[c] = v;
-      else if (which == 1) hcol[c] = v;
-      else grow[c] = v;
+  }
+  pdl_wait();
+  {
+    const int w = tid >> 5, lane = tid & 31;
+    const int b0 = (int)((int64_t)nb * w / 8), b1 = (int)((int64_t)nb * (w + 1) / 8);
+    const double* P = a.part + ((int64_t)ar * 3 + which) * nb * k;
+    for (int c0 = 0; c0 < k; c0 += 32) {
+      const int c = c0 + lane;
+      double v = 0.0;
+      if (c < k) {
+        for (int bb = b0; bb < b1; bb += 16) {
+          double x[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) x[u] = bb + u < b1 ? P[(int64_t)(bb + u) * k + c] : 0.0;
+#pragma unroll
+          for (int u = 0; u < 16; ++u) v += x[u];
+        }
+        wred[w][c] = v;
+      }
     }
   }
   __syncthreads();
+  for (int c = tid; c < k; c += kPropT) {
+    double v = 0.0;
+    for (int w = 0; w < 8; ++w) v += wred[w][c];
+    vrow[c] = v;
+  }
+  cl.sync();
+  if (which == 0) {
+    const double* v1 = cl.map_shared_rank(vrow, 1);
+    const double* v2 = cl.map_shared_rank(vrow, 2);
+    for (int c = tid; c < k; c += kPropT) { hrow[c] = vrow[c]; hcol[c] = v1[c]; grow[c] = v2[c]; }
+  }
+  cl.sync();                                   // (ranks 1, 2 keep their shared memory until read)
+  if (which != 0) return;
   for (int o = tid; o < 2 * k; o += kPropT) {    // + W'_X^T G_p terms of H (row a) and H^T (column a)
     const int c = o < k ? o : o - k;
     double v = 0.0;
@@ -272,19 +285,24 @@ __global__ void __launch_bounds__(kPropT) prop2_kernel(const __grid_constant__ P
     if (c == ar) a.dg[ar] = g - 2.0 * a.Qn[(int64_t)ar * k + ar];   // f_w's diagonal terms
   }
   // f_w = w^2 ||A1 - X1_{p+1}||^2 = w^2 (||A1||^2 + sum_a (G_{p+1} - 2 A1^T X1_{p+1})[a][a]) by the
-  // last CTA, in a fixed order (fp32 mode only: the cancellation costs ~1e-16 w^2 ||A1||^2 absolute,
-  // ~1e-12 of F at configs 2-3), so that no per-iteration quantity depends on the row shards
+  // last row to finish, in a fixed order (fp32 mode only: the cancellation costs ~1e-16 w^2 ||A1||^2
+  // absolute, ~1e-12 of F at configs 2-3), so that no per-iteration quantity depends on the shards
   __shared__ bool last;
   __threadfence();
   __syncthreads();
-  if (tid == 0) last = atomicAdd(a.counter, 1) == (int)gridDim.x - 1;
+  if (tid == 0) last = atomicAdd(a.counter, 1) == (int)gridDim.x / 3 - 1;
   __syncthreads();
-  if (last && tid == 0) {
-    __threadfence();
-    double sd = 0.0;
-    for (int q = 0; q < k; ++q) sd += __ldcg(a.dg + q);
-    om[(int64_t)kk] = a.w2 * (a.a1sq + sd);
-    *a.counter = 0;
+  if (last) {                                  // (loads in parallel: a serial load->add chain costs
+    __threadfence();                           //  one L2 round trip per term)
+    __shared__ double dsum[128];
+    for (int q = tid; q < k; q += kPropT) dsum[q] = __ldcg(a.dg + q);
+    __syncthreads();
+    if (tid == 0) {
+      double sd = 0.0;
+      for (int q = 0; q < k; ++q) sd += dsum[q];
+      om[(int64_t)kk] = a.w2 * (a.a1sq + sd);
+      *a.counter = 0;
+    }
   }
   pdl_trigger();
 }
@@ -316,7 +334,7 @@ cudaError_t launch_prop(const PropArgs& a, bool f64, int pdl, cudaStream_t st, c
   at2[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at2[0].val.programmaticStreamSerializationAllowed = 1;
   cudaLaunchConfig_t c2{};
-  c2.gridDim = dim3(a.k);
+  c2.gridDim = dim3(3 * a.k);                  // 3-CTA clusters (__cluster_dims__)
   c2.blockDim = dim3(kPropT);
   c2.dynamicSmemBytes = sm2;
   c2.stream = st;
@@ -344,6 +362,6 @@ cudaError_t launch_vsum(double* out, const double* in, int G, size_t stride, siz
   return cudaGetLastError();
 }
 
-size_t prop_part_doubles(int n, int k) { return (size_t)((n + kPropRB - 1) / kPropRB) * 2 * k * k; }
+size_t prop_part_doubles(int n, int k) { return (size_t)((n + kPropRB - 1) / kPropRB) * 3 * k * k; }
 
 }  // namespace wlr

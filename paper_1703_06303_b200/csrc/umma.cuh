@@ -110,13 +110,13 @@ WLR_DEVI float tf32_rn(float x) {
   return __uint_as_float(r);
 }
 
-// 3xTF32 split: hi = RN_tf32(x), lo = RN_tf32(x - hi) (x - hi is exact in fp32).  Rounding both
-// parts to nearest (instead of truncating them) makes the split's error ~2^-22 |x| and UNBIASED:
-// truncation biases every product toward zero, and the bias accumulated to ~6e-6 relative in X1
-// over a 630-term row update (measured, scripts/diag_drift.py).
+// 3xTF32 split: hi = x rounded to TF32 (nearest, ties away: add half an ulp of the 13 dropped bits
+// to the bit pattern, then clear them; two integer ops), lo = x - hi (exact in fp32, |lo| <= 2^-11
+// |x|; the tensor core truncates it to TF32, an error <= 2^-21 |x| on the small side).  Rounding hi
+// to nearest instead of truncating it halves the split error and removes its sign bias.
 WLR_DEVI void tf32_split(float x, float& hi, float& lo) {
-  hi = tf32_rn(x);
-  lo = tf32_rn(x - hi);
+  hi = __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+  lo = x - hi;
 }
 
 }  // namespace wlr
