@@ -48,6 +48,60 @@ WLR_DEVI float lds1(uint32_t addr) {
   return v;
 }
 
+// (a0, a1) -= (x, x) * (b0, b1) as ONE packed FFMA2 (sm_100a): half the issue slots of two FFMAs
+WLR_DEVI void ffma2_neg(float& a0, float& a1, float x, float b0, float b1) {
+  unsigned long long A, X, B;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(A) : "f"(a0), "f"(a1));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(X) : "f"(-x));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(B) : "f"(b0), "f"(b1));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(A) : "l"(X), "l"(B));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(A));
+}
+
+template <int NQ, int NA>
+WLR_DEVI void rs_fma4(float (&acc)[NQ][8], const float4 (&b)[8], const float (&o)[NA][4]) {
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const float bb[8] = {b[2 * u].x, b[2 * u].y, b[2 * u].z, b[2 * u].w,
+                         b[2 * u + 1].x, b[2 * u + 1].y, b[2 * u + 1].z, b[2 * u + 1].w};
+#pragma unroll
+    for (int q = 0; q < NA; ++q)
+#pragma unroll
+      for (int jj = 0; jj < 8; jj += 2) ffma2_neg(acc[q][jj], acc[q][jj + 1], o[q][u], bb[jj], bb[jj + 1]);
+  }
+}
+
+template <int NA>
+WLR_DEVI void rs_ld4(float4 (&b)[8], float (&o)[NA][4], uint32_t ob, const uint32_t* sa, uint32_t oa) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) b[i] = lds4(ob + 16 * i);
+#pragma unroll
+  for (int q = 0; q < NA; ++q)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) o[q][u] = lds1(sa[q] + oa + 32 * u);
+}
+
+// panel GEMM: acc[q][jj] -= sum_{t < J0} L[a_q, t] L[J0 + jj, t] for the NA first q-blocks.
+// J0 is a multiple of 8: eight t per loop trip in two register stages of four (no copies), 32-bit
+// shared addresses, the loads of one stage issued before the packed FMAs (FFMA2) of the other (the
+// last trip over-reads four columns inside the factor storage; those values are never used).
+template <int NQ, int NA>
+WLR_DEVI void rs_gemm8(float (&acc)[NQ][8], const uint32_t (&sa)[NQ], uint32_t sb, int J0) {
+  float4 b0[8], b1[8];
+  float o0[NA][4], o1[NA][4];
+  rs_ld4<NA>(b0, o0, sb, sa, 0);
+  uint32_t oa = 0;
+#pragma unroll 1
+  for (int t = 0; t < J0; t += 8) {
+    rs_ld4<NA>(b1, o1, sb + 128, sa, oa + 128);
+    rs_fma4<NQ, NA>(acc, b0, o0);
+    rs_ld4<NA>(b0, o0, sb + 256, sa, oa + 256);
+    rs_fma4<NQ, NA>(acc, b1, o1);
+    sb += 256;
+    oa += 256;
+  }
+}
+
 template <int NQ, int NA>
 WLR_DEVI void rs_fma2(float (&acc)[NQ][8], const float4 (&b)[4], const float (&o)[NA][2]) {
 #pragma unroll
@@ -57,7 +111,7 @@ WLR_DEVI void rs_fma2(float (&acc)[NQ][8], const float4 (&b)[4], const float (&o
 #pragma unroll
     for (int q = 0; q < NA; ++q)
 #pragma unroll
-      for (int jj = 0; jj < 8; ++jj) acc[q][jj] = fmaf(-o[q][u], bb[jj], acc[q][jj]);
+      for (int jj = 0; jj < 8; jj += 2) ffma2_neg(acc[q][jj], acc[q][jj + 1], o[q][u], bb[jj], bb[jj + 1]);
   }
 }
 
@@ -69,12 +123,10 @@ WLR_DEVI void rs_ld2(float4 (&b)[4], float (&o)[NA][2], uint32_t ob, const uint3
   for (int q = 0; q < NA; ++q) { o[q][0] = lds1(sa[q] + oa); o[q][1] = lds1(sa[q] + oa + 32); }
 }
 
-// panel GEMM: acc[q][jj] -= sum_{t < J0} L[a_q, t] L[J0 + jj, t] for the NA first q-blocks.
-// J0 is a multiple of 8: four t per loop trip in two register stages (no copies), 32-bit shared
-// addresses, the loads of one stage issued before the FMAs of the other (the last trip
-// over-reads two columns inside the factor storage; those values are never used).
+// the same with four t per trip in two stages of two (fewer registers: the k <= 95 kernels, which
+// run more warps per SM, are faster with it; measured at configs 4 / 5)
 template <int NQ, int NA>
-WLR_DEVI void rs_gemm(float (&acc)[NQ][8], const uint32_t (&sa)[NQ], uint32_t sb, int J0) {
+WLR_DEVI void rs_gemm4(float (&acc)[NQ][8], const uint32_t (&sa)[NQ], uint32_t sb, int J0) {
   float4 b0[4], b1[4];
   float o0[NA][2], o1[NA][2];
   rs_ld2<NA>(b0, o0, sb, sa, 0);
@@ -88,6 +140,12 @@ WLR_DEVI void rs_gemm(float (&acc)[NQ][8], const uint32_t (&sa)[NQ], uint32_t sb
     sb += 128;
     oa += 128;
   }
+}
+
+template <int NQ, int NA>
+WLR_DEVI void rs_gemm(float (&acc)[NQ][8], const uint32_t (&sa)[NQ], uint32_t sb, int J0) {
+  if constexpr (NQ >= 4) rs_gemm8<NQ, NA>(acc, sa, sb, J0);
+  else rs_gemm4<NQ, NA>(acc, sa, sb, J0);
 }
 
 // K entries of panel P for the own rows (rows of S = C C^T, ld k8 with zero padding, or e_i for
