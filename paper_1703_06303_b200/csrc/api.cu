@@ -462,6 +462,7 @@ static cudaError_t launch_row_pass_iter(wlr_ctx* h, int ph, cudaStream_t st, boo
     set_prefetch(h, ph, a.pf_ptr, a.pf_bytes);
     if (h->tc_on) {
       RowPassTcArgs q{};
+      q.E = (float*)h->Ebuf; q.W1 = (const float*)h->W1; q.ldw = h->ldw;   // (non-uniform: e rows)
       q.tmA = h->tmA_tc; q.tmX = h->tmX_tc[cur]; q.tmW = wb ? h->tmWT1 : h->tmWT;
       q.A = a.A; q.lda = a.lda; q.Xold = a.Xold; q.Xnew = a.Xnew; q.Dnew = light ? nullptr : a.Dnew;
       q.w2s = a.w2s; q.fw_part = h->fw_part;
@@ -475,6 +476,8 @@ static cudaError_t launch_row_pass_iter(wlr_ctx* h, int ph, cudaStream_t st, boo
       e = launch_row_pass_tc(q, h->rp, h->tc_grid, st, nullptr, h->tc_deep);
     } else {
       e = launch_row_pass<float>(a, h->rp, h->rp_tr, h->uniform, 0, h->rp_grid, st);
+    }
+    {
       if (e == cudaSuccess && h->Ebuf) {
         RowSolveArgs q{};
         q.E = (const float*)h->Ebuf; q.S = h->Sop;
@@ -626,7 +629,7 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int ph) {
     if (prof) cudaEventRecord(ev[7], h->st2);
     CUDA_TRY(h, cudaEventRecord(h->ev_join, h->st2));
   }
-  const int nfw = h->tc_on ? h->tc_grid : (h->Ebuf ? h->rs_grid : h->rp_grid);
+  const int nfw = h->Ebuf ? h->rs_grid : (h->tc_on ? h->tc_grid : h->rp_grid);   // (the solver writes f_w)
   if (h->itc_on)   // tensor-core layout: A part padded to nA32, kp' = 32
     launch_reduce_incr(h->inc_part, (int)ceil_div(h->itc_nsplit, h->itc_cs), (int)h->k, (int)h->nk, h->itc_nz,
                        (int)(h->k - h->k0), h->itc_nA32, 32, h->fw_part, nfw, h->inc[cur], h->st, nullptr,
@@ -915,7 +918,9 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
     if (!ok) return fail(h, WLR_ECUDA, "cuTensorMapEncodeTiled failed (TMA descriptors)");
   }
   // tensor-core row pass (uniform W1, fp32): K-major W'^T written by the small step
-  h->tc_ok = h->dtype == WLR_F32 && h->uniform;
+  // tensor-core row pass: fp32, uniform W1 (X1_{p+1} directly) or non-uniform with the per-row
+  // solver (E mode: the tile result plus A1 . W1^2 goes to the e rows)
+  h->tc_ok = h->dtype == WLR_F32 && (h->uniform || h->Ebuf != nullptr);
   if (const char* dbg = std::getenv("WLR_TC_DBG")) h->tc_dbg = std::atoi(dbg);
   if (h->tc_dbg & 32) {
     void* p = nullptr;
@@ -951,7 +956,7 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
         // one tile per CTA, one CTA per SM: the 8-stage ring
         h->tc_deep = true;
         h->tc_grid = (int)ntiles;
-      } else if (row_pass_tc_deep_ok(h->rp) && h->rp <= 32 && h->m <= (int64_t)h->nsm * (kTcBM + 4) &&
+      } else if (row_pass_tc_deep_ok(h->rp) && h->rp <= 32 && h->uniform && h->m <= (int64_t)h->nsm * (kTcBM + 4) &&
                  make_tmap_2d(&h->tmA_x, h->A, 4, (uint64_t)n, (uint64_t)h->m, (uint64_t)h->lda * 4, 32u, 4u, false) &&
                  make_tmap_2d(&h->tmX_x[0], h->X[0], 4, (uint64_t)kp, (uint64_t)h->m, (uint64_t)kp * 4, 32u, 4u, false) &&
                  make_tmap_2d(&h->tmX_x[1], h->X[1], 4, (uint64_t)kp, (uint64_t)h->m, (uint64_t)kp * 4, 32u, 4u, false)) {

@@ -72,6 +72,10 @@ struct RowPassTcArgs {
   const float* Xold; float* Xnew; float* Dnew;   // m x kp
   float w2s;
   double* fw_part;                  // gridDim.x partials of f_w
+  // non-uniform W1 (E mode, E != nullptr): the tile result is E - A1 . W1^2 (the linear part of E,
+  // W'' = [0; U; P]); the epilogue writes e = result + A1 . W1^2 rows (m x kp) for the per-row
+  // solves instead of X1_{p+1} / Delta / f_w
+  float* E; const float* W1; int64_t ldw;
   const void* pf_ptr[kPf]; int64_t pf_bytes[kPf];
   int64_t m; int KA, k, kp, n;
   // tiles cover rows [0, m_main); with extra > 0 (one CTA per SM, one tile each) CTA i also

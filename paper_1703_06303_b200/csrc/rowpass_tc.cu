@@ -310,7 +310,25 @@ __global__ void __launch_bounds__(tc_threads<NR>(), NR >= 8 ? 1 : 2) row_pass_tc
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] += vl[j];
           }
-          if (live) {
+          if (live && a.E) {               // non-uniform: e = (E - A1 . W1^2) + A1 . W1^2
+            float4* en = reinterpret_cast<float4*>(a.E + row * a.kp + c0);
+            const float* w1r = a.W1 + row * a.ldw;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              if (q < nv) {
+                const float* av = reinterpret_cast<const float*>(&ar[q]);
+                float eq[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const int ll = c0 + 4 * q + e;
+                  float w = 0.f;
+                  if (ll < a.k) w = __ldg(w1r + ll);
+                  eq[e] = ll < a.k ? fmaf(av[e] * w, w, v[4 * q + e]) : 0.f;
+                }
+                en[q] = make_float4(eq[0], eq[1], eq[2], eq[3]);
+              }
+            }
+          } else if (live) {
             float4* xn = reinterpret_cast<float4*>(a.Xnew + row * a.kp + c0);
             float4* dn = reinterpret_cast<float4*>(a.Dnew + row * a.kp + c0);
 #pragma unroll
