@@ -164,7 +164,7 @@ struct wlr_ctx {
   int ics = 1, ncl = 0;        // increment row splits per cluster, cluster partials
   // tensor-core increments (fp32, kp <= 32): own column layout (A part padded to 32)
   bool itc_ok = false, itc_on = false;
-  int itc_nsplit = 0, itc_nA32 = 0, itc_nz = 0, itc_cs = 1;
+  int itc_nsplit = 0, itc_nA32 = 0, itc_nz = 0, itc_cs = 1, itc_kpd = 32;
   // non-uniform fp32: e rows -> warp-per-row shared-memory Cholesky (rowsolve.cu)
   void* Ebuf = nullptr; int rs_grid = 0;
   int64_t itc_rps = 0;
@@ -595,12 +595,13 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int ph) {
     // whether its pipeline feeds the tensor cores (small X1 step) or CUDA-core FMAs
     a.gate = nullptr;
     a.pdl = prof ? 0 : 1;
-    if (!h->itc_on) e = launch_incr<float>(a, h->bm, h->st);
-    else {
+    if (h->itc_on && h->itc_kpd > 32) a.gate = h->flags + 5;   // (it computes only while the gate is off)
+    if (!h->itc_on || h->itc_kpd > 32) e = launch_incr<float>(a, h->bm, h->st);
+    if (h->itc_on && e == cudaSuccess) {
       IncrTcArgs q{};
       q.tmA = h->tmA32; q.tmX = h->tmX32[cur]; q.tmD = h->tmD32;
       q.part = h->inc_part; q.m = h->m; q.rows_per_split = h->itc_rps;
-      q.k = (int)h->k; q.k0 = (int)h->k0; q.nA32 = h->itc_nA32; q.nz = h->itc_nz;
+      q.k = (int)h->k; q.k0 = (int)h->k0; q.nA32 = h->itc_nA32; q.nz = h->itc_nz; q.kpd = h->itc_kpd;
       q.gate = h->flags + 5;
       q.cs = h->itc_cs;
       q.tstamp = h->itc_tstamp;
@@ -630,10 +631,15 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int ph) {
     CUDA_TRY(h, cudaEventRecord(h->ev_join, h->st2));
   }
   const int nfw = h->Ebuf ? h->rs_grid : (h->tc_on ? h->tc_grid : h->rp_grid);   // (the solver writes f_w)
-  if (h->itc_on)   // tensor-core layout: A part padded to nA32, kp' = 32
+  if (h->itc_on && h->itc_kpd == 32)   // tensor-core layout: A part padded to nA32, kp' = 32
     launch_reduce_incr(h->inc_part, (int)ceil_div(h->itc_nsplit, h->itc_cs), (int)h->k, (int)h->nk, h->itc_nz,
                        (int)(h->k - h->k0), h->itc_nA32, 32, h->fw_part, nfw, h->inc[cur], h->st, nullptr,
                        ReduceLayout{nullptr, 0, 0, 0, 0}, !prof && !pend);
+  else if (h->itc_on)   // KPD > 32: the CUDA-core layout while the gate is off, the tensor-core one after
+    launch_reduce_incr(h->ics > 1 ? h->inc_part2 : h->inc_part, h->ics > 1 ? h->ncl : h->nsplit, (int)h->k,
+                       (int)h->nk, h->nz, (int)(h->k - h->k0), (int)(h->n - h->k0), (int)h->kp, h->fw_part,
+                       nfw, h->inc[cur], h->st, h->flags + 5,
+                       ReduceLayout{h->inc_part, h->itc_nsplit, h->itc_nz, h->itc_nA32, h->itc_kpd}, !prof && !pend);
   else
     launch_reduce_incr(h->ics > 1 ? h->inc_part2 : h->inc_part, h->ics > 1 ? h->ncl : h->nsplit, (int)h->k,
                        (int)h->nk, h->nz, (int)(h->k - h->k0), (int)(h->n - h->k0), (int)h->kp, h->fw_part,
@@ -865,13 +871,14 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   h->ics = h->nsplit >= 8 && incr_cluster_ok() ? 8 : 1;
   h->ncl = (int)ceil_div(h->nsplit, h->ics);
   // tensor-core increments: 128-column blocks x row splits, one wave at 2 CTAs/SM
-  h->itc_ok = h->dtype == WLR_F32 && kp <= 32;
+  h->itc_kpd = incr_tc_kpd((int)kp);
+  h->itc_ok = h->dtype == WLR_F32 && h->itc_kpd > 0;
   if (h->itc_ok) {
     h->itc_nA32 = (int)round_up(n - h->k0, 32);
-    h->itc_nz = h->itc_nA32 + 64;
+    h->itc_nz = h->itc_nA32 + 2 * h->itc_kpd;
     const int64_t ncb = ceil_div(h->itc_nz, 128);
     const char* cps_env = getenv("WLR_ITC_CPS");    // (experiments: CTAs per SM of the split grid)
-    const int cps = cps_env ? std::max(1, atoi(cps_env)) : 2;
+    const int cps = cps_env ? std::max(1, atoi(cps_env)) : (h->itc_kpd > 32 ? 1 : 2);   // (smem: 1 CTA/SM above 32)
     const int64_t want = std::max<int64_t>(1, (cps * h->nsm) / ncb);
     h->itc_rps = round_up(ceil_div(h->m, want), 32);
     h->itc_nsplit = (int)ceil_div(h->m, h->itc_rps);

@@ -1,4 +1,4 @@
-// incr_tc.cu -- K2b on the 5th-generation tensor cores (fp32 data, kp <= 32).
+// incr_tc.cu -- K2b on the 5th-generation tensor cores (fp32 data, kp <= 128).
 //
 // The Gram increments are one contraction over the pixel rows:
 //     [N | Gamma | Omega](l, j) = sum_i Delta(i, l) Z(i, j),   Z = [A(:, k0:n) | X1_p | Delta]
@@ -12,8 +12,11 @@
 //   warp 5 (lane 0): per 8-row k-step, Z_hi x [Delta_hi; Delta_lo] (N = 64) and
 //     Z_lo x Delta_hi (N = 32) into the TMEM accumulator
 // Epilogue: thread c reads its accumulator lane and writes the fp64 partial of column c for all
-// l < k.  The column layout pads the A part to a multiple of 32 (nA32) so that no 32-column TMA
-// box straddles two sources; the reduce kernel reads that layout (nz' = nA32 + 64, kp' = 32).
+// l < k.  The column layout pads the A part to a multiple of 32 (nA32) and the X1_p and Delta
+// parts to KPD = kp rounded up to 32, so that no 32-column TMA box straddles two sources; the
+// reduce kernel reads that layout (nz' = nA32 + 2 KPD, kp' = KPD).  KPD = 64 .. 128 (k > 32,
+// configs 4-5): the Delta^T operand is N = 2 KPD <= 256 wide, the accumulator 2 KPD TMEM columns;
+// while the tensor-core gate is off those widths leave the chunk to the CUDA-core kernel.
 #include "kernels.h"
 #include "umma.cuh"
 
@@ -31,12 +34,19 @@ constexpr int kItThreads = 192;
 #endif
 constexpr int kItNR = WLR_IT_NR, kItNL = WLR_IT_NL;
 constexpr int kItZB = 4 * 32 * 128;     // Z chunk: 4 boxes of 32 rows x 128 B (16 KB)
-constexpr int kItDB = 32 * 128;         // Delta chunk: 32 rows x 32 fp32 (4 KB)
-constexpr int kItST = kItZB + kItDB;    // raw stage
-constexpr int kItBT = 2 * 32 * 128;     // B operand slot: Delta^T hi | lo (64 rows x 128 B)
-constexpr int kItSmem = kItNR * kItST + kItNL * kItBT;
+template <int KPD> struct ItLayout {
+  static constexpr int DB = KPD * 128;                 // Delta chunk: 32 rows x KPD fp32 (KPD/32 boxes)
+  static constexpr int ST = kItZB + DB;                // raw stage
+  static constexpr int BT = 2 * KPD * 128;             // B operand slot: Delta^T hi | lo (2 KPD rows x 128 B)
+  static constexpr int SMEM = kItNR * ST + kItNL * BT;
+  static constexpr int ACC = 2 * KPD;                  // accumulator columns
+  static constexpr int NCOL = ACC + 64 * kItNL <= 256 ? 256 : 512;
+};
 
-__global__ void __launch_bounds__(kItThreads, 2) incr_tc_kernel(const __grid_constant__ IncrTcArgs a) {
+template <int KPD>
+__global__ void __launch_bounds__(kItThreads, KPD <= 32 ? 2 : 1) incr_tc_kernel(const __grid_constant__ IncrTcArgs a) {
+  using L = ItLayout<KPD>;
+  constexpr int kItST = L::ST, kItBT = L::BT;
   // Programmatic dependent launch behind the row pass: only the producer waits for it, and only
   // before its Delta boxes -- the A and X1_p boxes of the first stages (not written by the row
   // pass) are requested while the row pass is still finishing.  The gate was written by the small
@@ -45,6 +55,10 @@ __global__ void __launch_bounds__(kItThreads, 2) incr_tc_kernel(const __grid_con
   // gate: tensor cores once the X1 step is small; otherwise the same pipeline
   // feeds plain FP32 FMAs on the CUDA cores (fp32 sums over 32-row chunks, fp64 across chunks)
   const bool tc = *a.gate != 0;
+  if (KPD > 32 && !tc) {                       // (gate off: the CUDA-core kernel computed this iteration;
+    pdl_wait();                                //  complete only after it, for the reduce that follows)
+    return;
+  }
   auto stamp = [&](int i) {
     if (a.tstamp) {
       unsigned long long t;
@@ -62,8 +76,8 @@ __global__ void __launch_bounds__(kItThreads, 2) incr_tc_kernel(const __grid_con
   __shared__ __align__(8) uint64_t full[kItNR], rawfree[kItNR], lofull[kItNL], lofree[kItNL], accfull;
   __shared__ uint32_t tslot;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  constexpr int ACC = 64;                                  // accumulator columns
-  if (warp == 0) tmem_alloc<256>(&tslot);                  // ACC + NL x 64 (Z_hi | Z_lo) <= 256
+  constexpr int ACC = L::ACC;                              // accumulator columns
+  if (warp == 0) tmem_alloc<L::NCOL>(&tslot);              // ACC + NL x 64 (Z_hi | Z_lo)
   if (tid == 32) {
     for (int s = 0; s < kItNR; ++s) { mbar_init(&full[s], 1); mbar_init(&rawfree[s], tc ? 1 : 4); }
     for (int s = 0; s < kItNL; ++s) { mbar_init(&lofull[s], 4); mbar_init(&lofree[s], 1); }
@@ -90,13 +104,14 @@ __global__ void __launch_bounds__(kItThreads, 2) incr_tc_kernel(const __grid_con
         if (part == 0) mbar_expect_tx(&full[s], (uint32_t)kItST);
         for (int b = 0; b < 4; ++b) {                      // Z column boxes
           const int zc = j0 + 32 * b;
-          const bool dpart = zc >= a.nA32 + 32;
+          const bool dpart = zc >= a.nA32 + KPD;
           if (dpart != (part == 1)) continue;
           if (zc < a.nA32) tma_load_2d(st + b * 4096, &a.tmA, &full[s], a.k0 + zc, row);
-          else if (zc < a.nA32 + 32) tma_load_2d(st + b * 4096, &a.tmX, &full[s], 0, row);
-          else tma_load_2d(st + b * 4096, &a.tmD, &full[s], 0, row);   // Delta (beyond nz': ignored lanes)
+          else if (zc < a.nA32 + KPD) tma_load_2d(st + b * 4096, &a.tmX, &full[s], zc - a.nA32, row);
+          else tma_load_2d(st + b * 4096, &a.tmD, &full[s], zc - a.nA32 - KPD < KPD ? zc - a.nA32 - KPD : 0, row);
         }
-        if (part == 1) tma_load_2d(st + kItZB, &a.tmD, &full[s], 0, row);
+        if (part == 1)
+          for (int db = 0; db < KPD / 32; ++db) tma_load_2d(st + kItZB + db * 4096, &a.tmD, &full[s], 32 * db, row);
       };
       const int npre = nch < kItNR ? nch : kItNR;
       for (int ch = 0; ch < npre; ++ch) issue(ch, ch, 0);
@@ -113,7 +128,7 @@ __global__ void __launch_bounds__(kItThreads, 2) incr_tc_kernel(const __grid_con
     }
   } else if (warp == 5) {
     if (lane == 0 && tc) {
-      const uint32_t id2 = umma_idesc_tf32<128, 64>(), id1 = umma_idesc_tf32<128, 32>();
+      const uint32_t id2 = umma_idesc_tf32<128, 2 * KPD>(), id1 = umma_idesc_tf32<128, KPD>();
       int r = 0, l = 0;
       uint32_t phl = 0;
       for (int ch = 0; ch < nch; ++ch) {
@@ -123,7 +138,7 @@ __global__ void __launch_bounds__(kItThreads, 2) incr_tc_kernel(const __grid_con
         const uint32_t bs = smem_u32(bst + l * kItBT);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
-          const uint64_t db = umma_desc_k_sw128(bs + kk * 32);   // [Delta_hi^T; Delta_lo^T], N = 64
+          const uint64_t db = umma_desc_k_sw128(bs + kk * 32);   // [Delta_hi^T; Delta_lo^T], N = 2 KPD
           umma_tf32_ts(tmem, ta + 8 * kk, db, id2, ch > 0 || kk > 0);
           umma_tf32_ts(tmem, ta + 32 + 8 * kk, db, id1, true);
         }
@@ -190,19 +205,21 @@ __global__ void __launch_bounds__(kItThreads, 2) incr_tc_kernel(const __grid_con
         tmem_st32(ta + 32, lo);
         tmem_st_wait();
       }
-      {   // Delta^T hi (rows 0-31) | lo (rows 32-63) of the B slot: element (n, k) = Delta(k, n)
+      {   // Delta^T hi (rows 0..KPD-1) | lo (rows KPD..) of the B slot: element (n, k) = Delta(k, n)
         const float* dl = reinterpret_cast<const float*>(st + kItZB);
         float* bt = reinterpret_cast<float*>(bst + l * kItBT);
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int e = tid + 128 * q;                    // 1024 elements
-          const int k = e >> 5, n = e & 31;               // read row k of Delta (coalesced)
-          const float v = dl[k * 32 + ((((n >> 2) ^ (k & 7)) << 2) | (n & 3))];
+        for (int q = 0; q < KPD / 4; ++q) {
+          const int e = tid + 128 * q;                    // 32 x KPD elements
+          const int k = e / KPD, n = e % KPD;             // read row k of Delta (coalesced)
+          const float* box = dl + (n >> 5) * 1024;        // 32-column box of the chunk
+          const int nn = n & 31;
+          const float v = box[k * 32 + ((((nn >> 2) ^ (k & 7)) << 2) | (nn & 3))];
           float h, lo;
           tf32_split(v, h, lo);
           const int off = n * 32 + ((((k >> 2) ^ (n & 7)) << 2) | (k & 3));
           bt[off] = h;
-          bt[32 * 32 + off] = lo;                         // rows 32.. : (n + 32) & 7 == n & 7
+          bt[KPD * 32 + off] = lo;                        // rows KPD.. : (n + KPD) & 7 == n & 7
         }
       }
       fence_proxy_async();
@@ -223,27 +240,32 @@ __global__ void __launch_bounds__(kItThreads, 2) incr_tc_kernel(const __grid_con
       for (int q = 0; q < 32; ++q) tile[q * 128 + tid] = acc64[q];
   } else if (warp < 4) {
     const int c = tid;
-    float v[32], v2[32];
     if (tid == 0) stamp(2);                                // converters done
     if (nch > 0) {
       mbar_wait(&accfull, 0);
       if (tid == 0) stamp(3);                              // accumulator complete
       tc_fence_after();
-      tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16), v);
-      tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + 32, v2);
-    } else {
-#pragma unroll
-      for (int q = 0; q < 32; ++q) { v[q] = 0.f; v2[q] = 0.f; }
     }
-    if (a.cs <= 1) {   // straight from the accumulator lanes: row q of the partial, coalesced over c
-      double* out = a.part + (int64_t)blockIdx.y * a.k * a.nz;
-      if (j0 + c < a.nz)
+#pragma unroll 1
+    for (int s0 = 0; s0 < KPD; s0 += 32) {                 // 32 Delta columns per TMEM load
+      float v[32], v2[32];
+      if (nch > 0) {
+        tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)s0, v);
+        tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(KPD + s0), v2);
+      } else {
 #pragma unroll
-        for (int q = 0; q < 32; ++q)
-          if (q < a.k) out[(int64_t)q * a.nz + j0 + c] = (double)v[q] + (double)v2[q];
-    } else {
+        for (int q = 0; q < 32; ++q) { v[q] = 0.f; v2[q] = 0.f; }
+      }
+      if (a.cs <= 1) {   // straight from the accumulator lanes: row q of the partial, coalesced over c
+        double* out = a.part + (int64_t)blockIdx.y * a.k * a.nz;
+        if (j0 + c < a.nz)
 #pragma unroll
-      for (int q = 0; q < 32; ++q) tile[q * 128 + c] = (double)v[q] + (double)v2[q];
+          for (int q = 0; q < 32; ++q)
+            if (s0 + q < a.k) out[(int64_t)(s0 + q) * a.nz + j0 + c] = (double)v[q] + (double)v2[q];
+      } else {           // (clusters: KPD = 32 only)
+#pragma unroll
+        for (int q = 0; q < 32; ++q) tile[q * 128 + c] = (double)v[q] + (double)v2[q];
+      }
     }
   }
   tc_fence_before();
@@ -271,25 +293,28 @@ __global__ void __launch_bounds__(kItThreads, 2) incr_tc_kernel(const __grid_con
   }
   if (warp == 0) {
     tc_fence_after();
-    tmem_dealloc<256>(tmem);
+    tmem_dealloc<L::NCOL>(tmem);
   }
   if (threadIdx.x == 0) stamp(4);
 }
 
-cudaError_t launch_incr_tc(const IncrTcArgs& a, int nsplit, cudaStream_t st) {
+template <int KPD>
+static cudaError_t launch_incr_tc_t(const IncrTcArgs& a, int nsplit, cudaStream_t st) {
+  using L = ItLayout<KPD>;
+  auto kern = incr_tc_kernel<KPD>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(incr_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kItSmem + 1024);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM + 1024);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(incr_tc_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  const int cs = a.cs > 1 ? a.cs : 1;
+  const int cs = (a.cs > 1 && KPD == 32) ? a.cs : 1;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)ceil_div(a.nz, 128), (unsigned)(ceil_div(nsplit, cs) * cs));
   cfg.blockDim = dim3(kItThreads);
-  cfg.dynamicSmemBytes = kItSmem + 1024;
+  cfg.dynamicSmemBytes = L::SMEM + 1024;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -301,7 +326,19 @@ cudaError_t launch_incr_tc(const IncrTcArgs& a, int nsplit, cudaStream_t st) {
   ++na;
   cfg.attrs = atp;
   cfg.numAttrs = na;
-  return cudaLaunchKernelEx(&cfg, incr_tc_kernel, a);
+  return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
+int incr_tc_kpd(int kp) { return kp <= 32 ? 32 : kp <= 64 ? 64 : kp <= 96 ? 96 : kp <= 128 ? 128 : -1; }
+
+cudaError_t launch_incr_tc(const IncrTcArgs& a, int nsplit, cudaStream_t st) {
+  switch (a.kpd) {
+    case 32: return launch_incr_tc_t<32>(a, nsplit, st);
+    case 64: return launch_incr_tc_t<64>(a, nsplit, st);
+    case 96: return launch_incr_tc_t<96>(a, nsplit, st);
+    case 128: return launch_incr_tc_t<128>(a, nsplit, st);
+  }
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace wlr

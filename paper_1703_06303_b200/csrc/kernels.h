@@ -150,11 +150,13 @@ struct IncrTcArgs {
   double* part;                     // nsplit x k x nz' (cs == 1) or (nsplit / cs) x k x nz' (clusters)
   int64_t m, rows_per_split;
   int cs;                           // row splits per thread-block cluster (DSMEM pre-reduction)
-  int k, k0, nA32, nz;              // nz = nA32 + 64
+  int k, k0, nA32, nz;              // nz = nA32 + 2 kpd
+  int kpd;                          // Delta / X1_p width in the layout: kp rounded up to 32 (<= 128)
   const int* gate;                  // runs only when *gate != 0 (set by the small step)
   unsigned long long* tstamp;       // diagnostics (WLR_TC_DBG bit 32): 8 stamps per CTA, or nullptr
 };
 cudaError_t launch_incr_tc(const IncrTcArgs& a, int nsplit, cudaStream_t st);
+int incr_tc_kpd(int kp);           // 32 / 64 / 96 / 128, or -1
 int incr_bm(int kp);
 inline bool incr_cluster_ok() { return true; }   // 8-CTA clusters of 128-512 threads (portable)
 int incr_bn(int bm, int elem_bytes);   // columns per CTA
