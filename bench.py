@@ -141,14 +141,16 @@ def iteration_bytes(cfg):
     return s * cfg.m * (cfg.n + 2 * cfg.k + (0 if cfg.uniform_w else cfg.k))
 
 
-def ncu_traffic(kernel_key):
+def ncu_traffic(kernel_key, config):
+    """DRAM bytes per launch of the kernel from the committed ncu --set full summary of this round
+    (profiles/ncu_summary.json, keyed by config), or None."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if not os.path.exists(p):
         return None
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get(kernel_key, {}).get("dram_bytes_per_launch")
+        return d.get(f"config{config}", {}).get(kernel_key, {}).get("dram_bytes_per_launch")
     except Exception:
         return None
 
@@ -330,49 +332,65 @@ def main():
     value = 1e3 / ms_per_step
     F, step_norm, rel = w.wlr_objective(h)
 
-    # per-kernel rooflines; the roofline object is the dominant m-scaled (streaming) kernel
+    # per-kernel rooflines; the roofline object is the dominant m-scaled kernel
     iters = max(prof["iters"], 1)
-    kern_ms = {"row_pass": prof["row_pass"] / iters, "increments": prof["increments"] / iters,
-               "reduce": prof["reduce"] / iters, "small_step": prof["small_step"] / iters,
-               "deferred_small_step": prof["deferred"] / iters}
+    prop_mode = cfg.uniform_w and cfg.dtype == "f32" and os.environ.get("WLR_PROP", "1") != "0"
+    kern_ms = {"row_pass": prof["row_pass"] / iters, "row_solve": prof["row_solve"] / iters,
+               "increments": prof["increments"] / iters, "reduce": prof["reduce"] / iters,
+               "small_step": prof["small_step"] / iters, "deferred_small_step": prof["deferred"] / iters}
+    if prop_mode:   # uniform fp32: the Gram propagation replaces the increments + reduce
+        kern_ms["gram_propagation"] = kern_ms.pop("increments")
+        kern_ms.pop("reduce")
+    if cfg.uniform_w:
+        kern_ms.pop("row_solve")
     cfg_local = dataclasses.replace(cfg, m=r1 - r0)
     peaks, peak_kind = measured_peaks()
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     kernels = {}
     if tensor_cores:
-        a = row_pass_bytes(cfg_local) / (kern_ms["row_pass"] * 1e-3) / 1e9
+        a = iteration_bytes(cfg_local) / (kern_ms["row_pass"] * 1e-3) / 1e9
         kernels["row_pass"] = {"bound": "hbm", "achieved": a, "peak": hbm_peak, "unit": "GB/s",
                                "frac": a / hbm_peak, "impl": "tcgen05 3xTF32",
-                               "per_unit": "4 (n + 3 kp) bytes per pixel row"}
+                               "per_unit": "SURVEY.md 8(d): 4 (n + 2 k) bytes per pixel row (+ 4 k for W1)"}
     else:
         a = row_pass_flops(cfg_local) / (kern_ms["row_pass"] * 1e-3) / 1e12
         kernels["row_pass"] = {"bound": "alu", "achieved": a, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
                                "frac": a / FP32_PEAK_TFLOPS, "impl": "CUDA-core FP32"}
-    if incr_tc:
-        a = incr_bytes(cfg_local) / (kern_ms["increments"] * 1e-3) / 1e9
-        kernels["increments"] = {"bound": "hbm", "achieved": a, "peak": hbm_peak, "unit": "GB/s",
-                                 "frac": a / hbm_peak, "impl": "tcgen05 3xTF32 (one kernel; CUDA-core FMAs "
-                                 "on the same pipeline while the X1 step is large)",
-                                 "per_unit": "4 (n - k0 + 2 kp) bytes per pixel row"}
+    if "row_solve" in kern_ms:
+        k = cfg.k
+        a = cfg_local.m * (k ** 3 / 3 + 2 * k * k) / (kern_ms["row_solve"] * 1e-3) / 1e12
+        kernels["row_solve"] = {"bound": "alu", "achieved": a, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
+                                "frac": a / FP32_PEAK_TFLOPS, "impl": "CUDA-core FP32 (FFMA2), warp per row",
+                                "per_unit": "k^3/3 + 2 k^2 flops per pixel row (Cholesky + two triangular solves)"}
+    if "increments" in kern_ms:
+        if incr_tc:
+            a = incr_bytes(cfg_local) / (kern_ms["increments"] * 1e-3) / 1e9
+            kernels["increments"] = {"bound": "hbm", "achieved": a, "peak": hbm_peak, "unit": "GB/s",
+                                     "frac": a / hbm_peak, "impl": "tcgen05 3xTF32 (CUDA-core FMAs while the "
+                                     "X1 step is large)", "per_unit": "4 (n - k0 + 2 kp) bytes per pixel row"}
+        else:
+            a = incr_flops(cfg_local) / (kern_ms["increments"] * 1e-3) / 1e12
+            kernels["increments"] = {"bound": "alu", "achieved": a, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
+                                     "frac": a / FP32_PEAK_TFLOPS, "impl": "CUDA-core FP32",
+                                     "per_unit": "2 k (n - k + 2 k) flops per pixel row"}
     else:
-        a = incr_flops(cfg_local) / (kern_ms["increments"] * 1e-3) / 1e12
-        kernels["increments"] = {"bound": "alu", "achieved": a, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
-                                 "frac": a / FP32_PEAK_TFLOPS, "impl": "CUDA-core FP32",
-                                 "per_unit": "2 k (n - k + 2 k) flops per pixel row"}
+        kernels["gram_propagation"] = {"bound": "latency", "ms": kern_ms["gram_propagation"],
+                                       "note": "m-independent: Grams of X1_{p+1} from A^T A (DESIGN.md 5.3)"}
     kernels["small_step"] = {"bound": "latency", "ms": kern_ms["small_step"],
-                             "note": "one 16-CTA cluster, fp64, dependent chain (DESIGN.md §5.2)"}
-    dom = max(("row_pass", "increments"), key=lambda kk: kern_ms[kk])
+                             "note": "one 16-CTA cluster, fp64, dependent chain (DESIGN.md 5.2)"}
+    mscaled = [kk for kk in ("row_pass", "row_solve", "increments") if kk in kern_ms]
+    dom = max(mscaled, key=lambda kk: kern_ms[kk])
     roof = dict(kernels[dom])
     roof.update({"kernel": dom,
                  "peak_source": (f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, burst)" if roof["unit"] == "GB/s"
-                                 else "derived CUDA-core FP32: 148 SM x 128 lanes x 2 x 1.965 GHz (DESIGN.md §6)"),
-                 "traffic": ncu_traffic(dom),
+                                 else "derived CUDA-core FP32: 148 SM x 128 lanes x 2 x 1.965 GHz (DESIGN.md 6)"),
+                 "traffic": ncu_traffic(dom, args.config),
                  "kernel_ms": kern_ms,
                  "kernel_share_of_step": {kk: v / prof_step_ms for kk, v in kern_ms.items()},
-                 "kernel_timing": ("CUDA events around every kernel in a second pass of %d steps (eager "
-                                   "launches: %.4f ms per step there; the metric's pass runs the CUDA "
-                                   "graph with programmatic dependent launch)" % (K2, prof_step_ms)),
-                 "dominant_of_step": max(("row_pass", "increments", "small_step"), key=lambda kk: kern_ms[kk]),
+                 "kernel_timing": ("CUDA events around every kernel in a second pass of %d steps (eager, "
+                                   "serial launches: %.4f ms per step there; the metric's pass runs the CUDA "
+                                   "graph, where the uniform-W1 row pass overlaps the small step)" % (K2, prof_step_ms)),
+                 "dominant_of_step": max(kern_ms, key=lambda kk: kern_ms[kk]),
                  "kernels": kernels})
     alg_gbs = iteration_bytes(cfg_local) / (ms_per_step * 1e-3) / 1e9
 
@@ -443,8 +461,9 @@ def main():
             "steps": K, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32" if cfg.dtype == "f32" else "f64",
             "data": "synthetic (seeded scene generator, synth/)",
-            "config": {"workload": f"{cfg.name} (BASELINE configs[2]): m={cfg.m} (120x160), n={cfg.n}, "
-                                   f"k={cfg.k}, r={cfg.r}, W1={cfg.w_const}, GHS init",
+            "config": {"workload": f"{cfg.name} (BASELINE configs[{args.config - 1}]): m={cfg.m}" + (f" ({cfg.H}x{cfg.W})" if cfg.H else "") + ", "
+                                   f"n={cfg.n}, k={cfg.k}, r={cfg.r}, W1=" +
+                                   (f"{cfg.w_const}" if cfg.uniform_w else f"log-U{list(cfg.w_logu)}") + ", GHS init",
                        "l2": ("flushed before every timed step (256 MB write, then a read of it: no dirty lines left); "
                               "steps timed individually" if args.flush == "clean" else
                               "flushed before every timed step (256 MB write); steps timed individually"),

@@ -163,10 +163,11 @@ wlr_status wlr_als_result(wlr_handle h, void* X1, int64_t ldx1, void* C, void* B
 wlr_status wlr_debug_state(wlr_handle h, const char* name, double* out, int64_t cap,
                            int64_t* count);
 
-/* Per-kernel device time accumulated (CUDA events on the handle's streams) while
- * profiling is on.  Order of ms[] (nms <= 5): row pass, increment GEMM, reduce, small step
- * (critical half), deferred small-step half (objective / step norm, which runs on a side
- * stream concurrently with the next iteration's row pass).
+/* Per-kernel device time accumulated (CUDA events on the handle's stream) while profiling is
+ * on; profiling runs every kernel of an iteration serially (no graph, no overlap).  Order of
+ * ms[] (nms <= 6): row pass, increment GEMM (uniform W1: the Gram propagation), reduce, small
+ * step (critical half), deferred small-step half (objective / step norm), per-row solves
+ * (non-uniform W1; included in neither the row pass nor the increments).
  * launches = number of library kernel launches since the last reset.                 */
 wlr_status wlr_profile(wlr_handle h, int32_t enable, int32_t reset, double* ms, int32_t nms,
                        int64_t* launches, int64_t* timed_iters);

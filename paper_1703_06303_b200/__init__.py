@@ -268,13 +268,13 @@ def wlr_profile(h: Handle, enable: bool, reset: bool = False):
     """Per-kernel device time (ms, CUDA events on the handle's streams) accumulated while
     profiling was enabled: row pass, increment GEMM, reduce, small step (critical half K3a)
     and the deferred small-step half (K3b, overlapped with the next row pass)."""
-    ms = (ctypes.c_double * 5)()
+    ms = (ctypes.c_double * 6)()
     la = ctypes.c_int64()
     it = ctypes.c_int64()
-    check(lib.wlr_profile(h.raw, 1 if enable else 0, 1 if reset else 0, ms, 5, ctypes.byref(la),
+    check(lib.wlr_profile(h.raw, 1 if enable else 0, 1 if reset else 0, ms, 6, ctypes.byref(la),
                           ctypes.byref(it)), h.raw)
     return dict(row_pass=ms[0], increments=ms[1], reduce=ms[2], small_step=ms[3], deferred=ms[4],
-                launches=la.value, iters=it.value)
+                row_solve=ms[5], launches=la.value, iters=it.value)
 
 
 def wlr_nccl_unique_id() -> bytes:

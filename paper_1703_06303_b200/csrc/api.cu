@@ -68,7 +68,7 @@ bool is_device_ptr(const void* p) {
 struct Profile {
   std::vector<cudaEvent_t> pool;
   size_t used = 0;
-  double ms[5] = {0, 0, 0, 0, 0};   // row pass, increments, reduce, small step (K3a), deferred K3b
+  double ms[6] = {0, 0, 0, 0, 0, 0};   // row pass, increments (or Gram propagation), reduce, K3a, K3b, row solves
   int64_t launches = 0, iters = 0;
   std::vector<int> groups;           // per profiled iteration: 1 if it launched a deferred K3b
 };
@@ -444,7 +444,8 @@ static wlr_status flush_pending(wlr_ctx* h) {
 // increments, which wait for both, are where K3b's inputs get rewritten.)
 // Row pass of iteration p (phase ph) on stream st: X1_{p+1} from [A | X1_p] and W'_p.  light: the
 // tensor-core pass writes X1_{p+1} only (Gram-propagation mode needs no Delta / f_w partials).
-static cudaError_t launch_row_pass_iter(wlr_ctx* h, int ph, cudaStream_t st, bool light, bool pdl = false) {
+static cudaError_t launch_row_pass_iter(wlr_ctx* h, int ph, cudaStream_t st, bool light, bool pdl = false,
+                                        cudaEvent_t mid = nullptr) {
   const int cur = ph & 1, nxt = cur ^ 1;      // X1 buffers
   const bool wb = cur != 0;                   // W'_p buffer
   cudaError_t e;
@@ -477,6 +478,7 @@ static cudaError_t launch_row_pass_iter(wlr_ctx* h, int ph, cudaStream_t st, boo
     } else {
       e = launch_row_pass<float>(a, h->rp, h->rp_tr, h->uniform, 0, h->rp_grid, st);
     }
+    if (mid) cudaEventRecord(mid, st);           // (profiling: the row pass / per-row solve boundary)
     {
       if (e == cudaSuccess && h->Ebuf) {
         RowSolveArgs q{};
@@ -499,6 +501,7 @@ static cudaError_t launch_row_pass_iter(wlr_ctx* h, int ph, cudaStream_t st, boo
     a.vec_ok = (h->lda % 4 == 0) && ((uintptr_t)h->A % 16 == 0);
     set_prefetch(h, ph, a.pf_ptr, a.pf_bytes);
     e = launch_row_pass<double>(a, h->rp, h->rp_tr, h->uniform, 0, h->rp_grid, st);
+    if (mid) cudaEventRecord(mid, st);           // (fp64: the solves run inside the row pass)
   }
   return e;
 }
@@ -519,10 +522,10 @@ static wlr_status enqueue_prop_iteration(wlr_ctx* h, int ph) {
   SmallArgs sa = small_args(h, ph, 1);
   cudaError_t e;
   if (prof) {   // eager profiling pass: everything serial on st, one event group per kernel kind
-    cudaEvent_t ev[8];
-    for (int i = 0; i < 8; ++i) ev[i] = prof_event(h);
+    cudaEvent_t ev[9];
+    for (int i = 0; i < 9; ++i) ev[i] = prof_event(h);
     cudaEventRecord(ev[0], h->st);
-    if ((e = launch_row_pass_iter(h, ph, h->st, true)) != cudaSuccess) return fail(h, WLR_ECUDA, std::string("row pass: ") + cudaGetErrorString(e));
+    if ((e = launch_row_pass_iter(h, ph, h->st, true, false, ev[8])) != cudaSuccess) return fail(h, WLR_ECUDA, std::string("row pass: ") + cudaGetErrorString(e));
     cudaEventRecord(ev[1], h->st);
     if ((e = launch_prop(pa, false, 0, h->st)) != cudaSuccess) return fail(h, WLR_ECUDA, std::string("Gram propagation: ") + cudaGetErrorString(e));
     cudaEventRecord(ev[2], h->st);
@@ -571,16 +574,16 @@ static wlr_status enqueue_prop_iteration(wlr_ctx* h, int ph) {
 static wlr_status enqueue_iteration(wlr_ctx* h, int ph) {
   if (h->prop) return enqueue_prop_iteration(h, ph);
   const int cur = ph & 1, nxt = cur ^ 1;      // X1 buffers
-  cudaEvent_t ev[8] = {};
+  cudaEvent_t ev[9] = {};
   const bool prof = h->prof;
   const bool pend = h->pending;
   if (prof) {
-    for (int i = 0; i < 8; ++i) ev[i] = prof_event(h);
+    for (int i = 0; i < 9; ++i) ev[i] = prof_event(h);
     cudaEventRecord(ev[0], h->st);
   }
   const bool rpt = h->rp_time && !prof;
   if (rpt) CUDA_TRY(h, cudaEventRecordWithFlags(h->rp_ev[0], h->st, cudaEventRecordExternal));
-  cudaError_t e = launch_row_pass_iter(h, ph, h->st, false);
+  cudaError_t e = launch_row_pass_iter(h, ph, h->st, false, false, prof ? ev[8] : nullptr);
   if (e != cudaSuccess) return fail(h, WLR_ECUDA, std::string("row pass: ") + cudaGetErrorString(e));
   if (prof) cudaEventRecord(ev[1], h->st);
   if (rpt) CUDA_TRY(h, cudaEventRecordWithFlags(h->rp_ev[1], h->st, cudaEventRecordExternal));
@@ -1692,20 +1695,23 @@ extern "C" wlr_status wlr_profile(wlr_handle h, int32_t enable, int32_t reset, d
                                   int32_t nms, int64_t* launches, int64_t* timed_iters) {
   if (!h) return fail(nullptr, WLR_EINVAL, "null handle");
   CUDA_TRY(h, cudaStreamSynchronize(h->st));
-  // fold recorded event groups (8 per iteration; 6, 7 = deferred K3b on the side stream)
-  for (size_t g = 0, it = 0; g + 8 <= h->pr.used; g += 8, ++it) {
-    float t01 = 0, t12 = 0, t23 = 0, t45 = 0, t67 = 0;
-    cudaEventElapsedTime(&t01, h->pr.pool[g], h->pr.pool[g + 1]);
+  // fold recorded event groups (9 per iteration; 6, 7 = deferred K3b on the side stream; 8 = the
+  // row pass / row solve boundary inside [0, 1])
+  for (size_t g = 0, it = 0; g + 9 <= h->pr.used; g += 9, ++it) {
+    float t01 = 0, t12 = 0, t23 = 0, t45 = 0, t67 = 0, t81 = 0;
+    cudaEventElapsedTime(&t01, h->pr.pool[g], h->pr.pool[g + 8]);
+    cudaEventElapsedTime(&t81, h->pr.pool[g + 8], h->pr.pool[g + 1]);
     cudaEventElapsedTime(&t12, h->pr.pool[g + 1], h->pr.pool[g + 2]);
     cudaEventElapsedTime(&t23, h->pr.pool[g + 2], h->pr.pool[g + 3]);
     cudaEventElapsedTime(&t45, h->pr.pool[g + 4], h->pr.pool[g + 5]);
     if (it < h->pr.groups.size() && h->pr.groups[it]) cudaEventElapsedTime(&t67, h->pr.pool[g + 6], h->pr.pool[g + 7]);
     h->pr.ms[0] += t01; h->pr.ms[1] += t12; h->pr.ms[2] += t23; h->pr.ms[3] += t45; h->pr.ms[4] += t67;
+    h->pr.ms[5] += t81;
   }
   h->pr.groups.clear();
   h->pr.used = 0;
   if (ms)
-    for (int i = 0; i < nms && i < 5; ++i) ms[i] = h->pr.ms[i];
+    for (int i = 0; i < nms && i < 6; ++i) ms[i] = h->pr.ms[i];
   if (launches) *launches = h->pr.launches;
   if (timed_iters) *timed_iters = h->pr.iters;
   if (reset) {

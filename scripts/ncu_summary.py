@@ -3,7 +3,7 @@ family, duration and DRAM bytes (read + write) per launch, achieved DRAM GB/s an
 utilisations.  Usage: ncu -i rep --page raw --csv > raw.csv; python scripts/ncu_summary.py raw.csv out.json"""
 import csv, json, sys
 
-UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "us": 1e-6, "usecond": 1e-6,
+UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0, "usecond": 1e-6,
         "msecond": 1e-3, "nsecond": 1e-9}
 rows = list(csv.reader(open(sys.argv[1])))
 hdr, units = rows[0], rows[1]
@@ -19,6 +19,10 @@ def val(d, name):
 
 
 def family(name):
+    if "row_solve_kernel" in name:
+        return "row_solve"
+    if "prop1_kernel" in name or "prop2_kernel" in name:
+        return "gram_propagation_" + ("1" if "prop1" in name else "2")
     if "reduce_incr_kernel" in name:
         return "reduce"
     if "incr_tc_kernel" in name:
