@@ -80,6 +80,10 @@ typedef struct {
   int32_t use_graph;      /* 1: replay each iteration as a captured CUDA graph (default)  */
   int32_t seed;           /* seed of the eigensolver's cold-start block (host PCG)        */
   void* vgroup;           /* wlr_vgroup (see wlr_vgroup_create) or NULL: virtual ranks      */
+  int32_t check_every;    /* eps > 0: host checks the stop flag every this many iterations
+                             (0 -> 8).  The stopping rule itself is applied on the device: the
+                             iterations launched after the converged state do no work, so the
+                             result is the converged state whatever this value              */
 } wlr_opts;
 
 /* Virtual ranks (validation hook for the row-sharded path on ONE GPU).  A group of G members:
@@ -112,7 +116,8 @@ wlr_status wlr_init(wlr_handle* h, const void* A, int64_t lda, const void* W1, i
 
 /* Run up to max_iters iterations (each = X1 half-step, then (C,D)
  * half-step).  Stops early when opts.eps > 0 and the stopping rule
- * holds (R3).  *iters_done / *converged may be NULL.  Synchronises the stream. */
+ * holds (R3): the state is then the first one that satisfies it, and later calls
+ * do not move it.  *iters_done / *converged may be NULL.  Synchronises the stream.       */
 wlr_status wlr_iterate(wlr_handle h, int32_t max_iters, int32_t* iters_done, int32_t* converged);
 
 /* Enqueue exactly n_iters iterations on the stream WITHOUT synchronising and without

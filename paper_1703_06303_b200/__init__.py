@@ -78,7 +78,7 @@ def wlr_init(A, k: int, r: int, W1=None, *, w1: float = 1.0, init: str = "ghs", 
              eps: float = 0.0, eig_tol: float = 0.0, eig_block: int = 0, eig_max_outer: int = 0,
              m_global: int = 0, row_offset: int = 0, nranks: int = 1, rank: int = 0,
              nccl_id: Optional[bytes] = None, stream: Optional[int] = None, use_graph: bool = True,
-             seed: int = 0, vgroup: Optional["VGroup"] = None) -> Handle:
+             seed: int = 0, vgroup: Optional["VGroup"] = None, check_every: int = 0) -> Handle:
     """wlr_init: PAPER.md Algorithm 1 lines 1-2 plus the first (C, D) half-step.
     ``W1=None`` uses the uniform weight ``w1``.  ``stream`` is a raw cudaStream_t (e.g.
     ``torch.cuda.current_stream().cuda_stream``); None lets the handle own a stream."""
@@ -101,6 +101,7 @@ def wlr_init(A, k: int, r: int, W1=None, *, w1: float = 1.0, init: str = "ghs", 
     o.rank = int(rank)
     o.use_graph = 1 if use_graph else 0
     o.seed = int(seed)
+    o.check_every = int(check_every)
     kx = None
     if init == "given":
         px, xcode, _, kx = _ptr(x1_0)

@@ -39,6 +39,7 @@ class wlr_opts(ctypes.Structure):
         ("use_graph", ctypes.c_int32),
         ("seed", ctypes.c_int32),
         ("vgroup", ctypes.c_void_p),
+        ("check_every", ctypes.c_int32),
     ]
 
 

@@ -411,6 +411,7 @@ static SmallArgs small_args(wlr_ctx* h, int ph, int mode) {
   s.Wt = wb1 ? h->Wt1 : h->Wt; s.CVop = h->CVop; s.Kop = h->Kop; s.Sop = h->Sop; s.flags = h->flags;
   s.WtT = wb1 ? h->WtT1 : h->WtT; s.KW = h->KW;
   s.eps = h->opts.eps; s.tol = h->opts.eig_tol; s.max_outer = h->opts.eig_max_outer; s.max_deg = 16;
+  s.stop = (mode != 0 && h->opts.eps > 0.0) ? h->flags + 6 : nullptr;   // eps mode: latched stop flag
   s.cold = 0;
   s.tdbg = h->ktime ? h->tdbg : nullptr;
   s.pl = h->spl;
@@ -430,7 +431,10 @@ static cudaError_t launch_deferred(wlr_ctx* h, const SmallArgs& a, cudaStream_t 
 
 static wlr_status flush_pending(wlr_ctx* h) {
   if (!h->pending) return WLR_OK;
-  cudaError_t e = launch_deferred(h, h->pend, h->st);
+  // eps mode: re-latch, so that a convergence decided inside the last launched iteration also
+  // stops this deferred half (the state stays at the converged one)
+  cudaError_t e = h->opts.eps > 0.0 ? launch_stop_latch(h->flags, h->st) : cudaSuccess;
+  if (e == cudaSuccess) e = launch_deferred(h, h->pend, h->st);
   if (e != cudaSuccess) return fail(h, WLR_ECUDA, std::string("small step (deferred): ") + cudaGetErrorString(e));
   h->pending = false;
   h->pr.launches += 1;
@@ -448,6 +452,7 @@ static cudaError_t launch_row_pass_iter(wlr_ctx* h, int ph, cudaStream_t st, boo
                                         cudaEvent_t mid = nullptr) {
   const int cur = ph & 1, nxt = cur ^ 1;      // X1 buffers
   const bool wb = cur != 0;                   // W'_p buffer
+  const int* stop = h->opts.eps > 0.0 ? h->flags + 6 : nullptr;
   cudaError_t e;
   if (h->dtype == WLR_F32) {
     RowPassArgs<float> a{};
@@ -460,6 +465,7 @@ static cudaError_t launch_row_pass_iter(wlr_ctx* h, int ph, cudaStream_t st, boo
     a.m = h->m; a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.no = (int)h->kp;
     a.vec_ok = (h->lda % 4 == 0) && ((uintptr_t)h->A % 16 == 0);
     a.Ebuf = (float*)h->Ebuf;
+    a.stop = stop;
     set_prefetch(h, ph, a.pf_ptr, a.pf_bytes);
     if (h->tc_on) {
       RowPassTcArgs q{};
@@ -467,13 +473,14 @@ static cudaError_t launch_row_pass_iter(wlr_ctx* h, int ph, cudaStream_t st, boo
       q.tmA = h->tmA_tc; q.tmX = h->tmX_tc[cur]; q.tmW = wb ? h->tmWT1 : h->tmWT;
       q.A = a.A; q.lda = a.lda; q.Xold = a.Xold; q.Xnew = a.Xnew; q.Dnew = light ? nullptr : a.Dnew;
       q.w2s = a.w2s; q.fw_part = h->fw_part;
-      for (int i = 0; i < kPf; ++i) { q.pf_ptr[i] = a.pf_ptr[i]; q.pf_bytes[i] = a.pf_bytes[i]; }
+      for (int i = 0; i < kPf; ++i) { q.pf_ptr[i] = light ? nullptr : a.pf_ptr[i]; q.pf_bytes[i] = light ? 0 : a.pf_bytes[i]; }
       q.m = h->m; q.KA = h->KA; q.k = (int)h->k; q.kp = (int)h->kp; q.n = (int)h->n;
       q.m_main = h->tc_m_main; q.extra = h->tc_extra;
       q.tmAx = h->tmA_x; q.tmXx = h->tmX_x[cur];
       q.dbg = h->tc_dbg;
       q.tstamp = h->tc_tstamp;
       q.pdl = pdl ? 1 : 0;
+      q.stop = stop;
       e = launch_row_pass_tc(q, h->rp, h->tc_grid, st, nullptr, h->tc_deep);
     } else {
       e = launch_row_pass<float>(a, h->rp, h->rp_tr, h->uniform, 0, h->rp_grid, st);
@@ -486,6 +493,7 @@ static cudaError_t launch_row_pass_iter(wlr_ctx* h, int ph, cudaStream_t st, boo
         q.W1 = (const float*)h->W1; q.ldw = h->ldw; q.A = (const float*)h->A; q.lda = h->lda;
         q.Xold = a.Xold; q.Xnew = a.Xnew; q.Dnew = a.Dnew; q.fw_part = h->fw_part; q.flags = h->flags;
         q.m = h->m; q.k = (int)h->k; q.kp = (int)h->kp;
+        q.stop = stop;
         e = launch_row_solve(q, h->rs_grid, st);
       }
     }
@@ -499,6 +507,7 @@ static cudaError_t launch_row_pass_iter(wlr_ctx* h, int ph, cudaStream_t st, boo
     a.fw_part = h->fw_part; a.flags = h->flags;
     a.m = h->m; a.n = (int)h->n; a.k = (int)h->k; a.kp = (int)h->kp; a.no = (int)h->kp;
     a.vec_ok = (h->lda % 4 == 0) && ((uintptr_t)h->A % 16 == 0);
+    a.stop = stop;
     set_prefetch(h, ph, a.pf_ptr, a.pf_bytes);
     e = launch_row_pass<double>(a, h->rp, h->rp_tr, h->uniform, 0, h->rp_grid, st);
     if (mid) cudaEventRecord(mid, st);           // (fp64: the solves run inside the row pass)
@@ -519,6 +528,8 @@ static wlr_status enqueue_prop_iteration(wlr_ctx* h, int ph) {
   pa.inc = h->inc[cur]; pa.dg = h->dgs; pa.counter = h->pcnt;
   pa.w2 = h->w1s * h->w1s; pa.a1sq = h->a1sq;
   pa.n = (int)h->n; pa.k = (int)h->k;
+  set_prefetch(h, ph, pa.pf_ptr, pa.pf_bytes);   // K3a(p)'s inputs, issued at prop1's entry
+  pa.stop = h->opts.eps > 0.0 ? h->flags + 6 : nullptr;
   SmallArgs sa = small_args(h, ph, 1);
   cudaError_t e;
   if (prof) {   // eager profiling pass: everything serial on st, one event group per kernel kind
@@ -572,6 +583,11 @@ static wlr_status enqueue_prop_iteration(wlr_ctx* h, int ph) {
 }
 
 static wlr_status enqueue_iteration(wlr_ctx* h, int ph) {
+  if (h->opts.eps > 0.0) {                     // eps mode: latch the converged flag for this iteration
+    cudaError_t le = launch_stop_latch(h->flags, h->st);
+    if (le != cudaSuccess) return fail(h, WLR_ECUDA, std::string("stop latch: ") + cudaGetErrorString(le));
+    h->pr.launches += 1;
+  }
   if (h->prop) return enqueue_prop_iteration(h, ph);
   const int cur = ph & 1, nxt = cur ^ 1;      // X1 buffers
   cudaEvent_t ev[9] = {};
@@ -1243,7 +1259,9 @@ extern "C" wlr_status wlr_iterate(wlr_handle h, int32_t max_iters, int32_t* iter
   const int64_t p0 = h->p;
   wlr_status s = WLR_OK;
   int done = 0;
-  const int chunk = h->opts.eps > 0.0 ? 1 : 64;
+  // eps mode: the stopping rule is applied on the device (kernels of every iteration after the
+  // converged state skip their work), so the host only checks every check_every iterations
+  const int chunk = h->opts.eps > 0.0 ? (h->opts.check_every > 0 ? h->opts.check_every : 8) : 64;
   while (done < max_iters) {
     const int n = std::min(chunk, max_iters - done);
     s = wlr_iterate_async(h, n);

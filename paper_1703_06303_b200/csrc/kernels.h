@@ -50,6 +50,7 @@ struct RowPassArgs {
   const void* pf_ptr[kPf]; int64_t pf_bytes[kPf];   // L2 prefetch of the next small steps' inputs
   int64_t m; int n, k, kp, no;      // no = output columns (kp, or t for MODE_RESULT)
   int vec_ok;                       // A rows 16-byte aligned at multiples of 4 elements
+  const int* stop;                  // eps mode: the iteration's latched stop flag (skip all work), or nullptr
 };
 int row_pass_rp(int r);
 bool row_pass_tr_ok(int rp, int tr);     // rows per thread TR available for this width
@@ -84,6 +85,7 @@ struct RowPassTcArgs {
   unsigned long long* tstamp;       // diagnostics: 8 globaltimer stamps per CTA, or nullptr
   int dbg;                          // diagnostics: bit 2 skip W loads, bit 3 skip epilogue
   int pdl;                          // host: launch as a programmatic dependent (no griddepcontrol.wait inside)
+  const int* stop;                  // eps mode: the iteration's latched stop flag, or nullptr
 };
 constexpr int kTcBM = 128;          // rows per tile (UMMA M)
 // deep = true: 8-stage ring, one CTA per SM (grid <= #SMs); false: 4 stages, 2 CTAs per SM
@@ -121,11 +123,16 @@ struct PropArgs {
   int* counter;                     // zero-initialised; prop2's last CTA resets it
   double w2, a1sq;                  // w^2, ||A1||_F^2
   int n, k;
+  const void* pf_ptr[kPf]; int64_t pf_bytes[kPf];   // L2 prefetch of the small step's inputs (prop1 entry)
+  const int* stop;                  // eps mode: the iteration's latched stop flag, or nullptr
 };
 size_t prop1_smem(int n);
 size_t prop1_smem(int n, int k);
 size_t prop_part_doubles(int n, int k);
 // virtual-group sum: out[i] = sum_{g < G} in[g * stride + i], g in order (fixed, deterministic)
+// eps mode: flags[6] = flags[2] (the converged flag) at the start of an iteration, one thread, so that
+// every kernel of the iteration (clusters included) sees one consistent value
+cudaError_t launch_stop_latch(int* flags, cudaStream_t st);
 cudaError_t launch_vsum(double* out, const double* in, int G, size_t stride, size_t count, cudaStream_t st);
 cudaError_t launch_prop(const PropArgs& a, bool f64, int pdl, cudaStream_t st, cudaEvent_t after1 = nullptr);
 
@@ -138,6 +145,7 @@ struct RowSolveArgs {
   double* fw_part;                  // gridDim.x partials of f_w
   int* flags;
   int64_t m; int k, kp;
+  const int* stop;                  // eps mode: the iteration's latched stop flag, or nullptr
 };
 bool row_solve_ok(int k);
 size_t row_solve_smem(int k);
@@ -211,6 +219,7 @@ struct SSPlan {
 struct SmallArgs {
   int k, nk, t, b, kp, k0, rp;      // dims; b = eigen block width (t <= b <= 32)
   int pdl;                          // host only: launch as a programmatic dependent (part 1)
+  const int* stop;                  // eps mode: the iteration's latched stop flag (skip the step), or nullptr
   int KA;                           // row offset of the X1_p block of the row-pass Wt
   void* WtT; int KW;                // fp32 W'^T (RP x KW, K-major) for the tensor-core row pass
   int mode;                         // 0: init (G, M given), 1: iteration (apply increments)

@@ -34,6 +34,8 @@ constexpr int kPropT1 = 256;       // prop1 threads: 32 lanes (columns l) x 8 gr
 constexpr int kPropG = kPropT1 / 32;
 constexpr int kPropRB = 4;         // n-index rows per prop1 CTA
 
+WLR_DEVI int warp_id_prop1(int tid) { return tid >> 5; }
+
 template <typename T>
 WLR_DEVI double wld(const void* W, int64_t i) { return (double)reinterpret_cast<const T*>(W)[i]; }
 
@@ -55,6 +57,7 @@ size_t prop1_smem(int n, int k) { return prop1_smem(n, k, (k + 31) / 32 * 32, 4)
 
 template <typename T>
 __global__ void __launch_bounds__(kPropT1) prop1_kernel(const __grid_constant__ PropArgs a) {
+  if (a.stop && *a.stop) return;               // (eps mode: converged before this iteration)
   extern __shared__ __align__(16) double pr_sm[];
   const int n = a.n, k = a.k, nk = n - k, RP = a.RP, kk = k * k;
   const int tid = threadIdx.x, lane = tid & 31, grp = tid >> 5;     // kPropG groups split the j sum
@@ -66,6 +69,19 @@ __global__ void __launch_bounds__(kPropT1) prop1_kernel(const __grid_constant__ 
   T* Wr = reinterpret_cast<T*>(Qns + kPropRB * k);       // (n + k) x RP  [W'_A ; W'_X], storage dtype
   uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(Wr) + (size_t)(n + k) * RP * sizeof(T));
   const uint32_t wa_bytes = (uint32_t)((size_t)n * RP * sizeof(T)), wx_bytes = (uint32_t)((size_t)k * RP * sizeof(T));
+  if (warp_id_prop1(tid) == 7) {   // the small step (K3a) that follows reads these: pull them into L2
+    for (int r = 0; r < kPf; ++r) {                // now (the bench flushes L2 before every iteration)
+      const char* base = reinterpret_cast<const char*>(a.pf_ptr[r]);
+      const int64_t nb = a.pf_bytes[r] & ~(int64_t)15;
+      if (!base || nb <= 0) continue;
+      const int64_t chunk = 8192, nchunk = (nb + chunk - 1) / chunk;   // spread over all CTAs
+      for (int64_t c = blockIdx.x + (int64_t)gridDim.x * (tid & 31); c < nchunk; c += (int64_t)gridDim.x * 32) {
+        const int64_t off = c * chunk;
+        const unsigned sz = (unsigned)(nb - off < chunk ? nb - off : chunk);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(base + off), "r"(sz) : "memory");
+      }
+    }
+  }
   const bool bulk_rows = ((size_t)n * 8) % 16 == 0;      // A^T A rows by bulk copy when 16-byte aligned
   // two barriers, each used for ONE phase: a parity wait on a barrier that has since moved two
   // phases on (rows, then W') would wait for a phase that never completes
@@ -201,6 +217,7 @@ __global__ void __launch_bounds__(kPropT1) prop1_kernel(const __grid_constant__ 
 // range); rank 0 gathers the other two sums through distributed shared memory and finishes row a.
 template <typename T>
 __global__ void __cluster_dims__(3, 1, 1) __launch_bounds__(kPropT) prop2_kernel(const __grid_constant__ PropArgs a) {
+  if (a.stop && *a.stop) return;               // (consistent for the whole cluster: latched flag)
   __shared__ double vrow[128];
   __shared__ double hrow[128], hcol[128], grow[128];
   __shared__ double wred[8][128];
@@ -346,6 +363,13 @@ cudaError_t launch_prop(const PropArgs& a, bool f64, int pdl, cudaStream_t st, c
   }
   cudaFuncSetAttribute(prop2_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
   return cudaLaunchKernelEx(&c2, prop2_kernel<float>, a);
+}
+
+__global__ void stop_latch_kernel(int* flags) { flags[6] = flags[2]; }
+
+cudaError_t launch_stop_latch(int* flags, cudaStream_t st) {
+  stop_latch_kernel<<<1, 1, 0, st>>>(flags);
+  return cudaGetLastError();
 }
 
 __global__ void vsum_kernel(double* __restrict__ out, const double* __restrict__ in, int G, size_t stride, size_t count) {

@@ -144,6 +144,7 @@ int row_pass_nwc(bool uniform, int k, int kp) {
 template <typename T, int RP, int TR, bool UNIFORM, int MODE>
 __global__ void __launch_bounds__(kRowThreads, RP <= 32 ? 3 : 1)
 row_pass_kernel(const __grid_constant__ RowPassArgs<T> a) {
+  if (a.stop && *a.stop) return;               // (eps mode: converged before this iteration)
   pdl_trigger();                               // the increments may be scheduled (they wait)
   using S = RowPassShape<RP>;
   using L = RowPassLayout<T, RP, TR>;

@@ -52,6 +52,7 @@ struct TcLayout {                                  // bytes; every block 1024-al
 
 template <int RP, int NR>
 __global__ void __launch_bounds__(tc_threads<NR>(), NR >= 8 ? 1 : 2) row_pass_tc_kernel(const __grid_constant__ RowPassTcArgs a) {
+  if (a.stop && *a.stop) return;               // (eps mode: converged before this iteration)
   pdl_trigger();                               // the increments may be scheduled (they wait)
   using L = TcLayout<RP, NR>;
   constexpr int kTcNR = NR;

@@ -169,6 +169,7 @@ WLR_DEVI void rs_fetch(float (&sn)[NQ][8], const int (&arow)[NQ], const float* _
 
 template <int NQ>
 __global__ void __launch_bounds__(32) row_solve_kernel(const __grid_constant__ RowSolveArgs a) {
+  if (a.stop && *a.stop) return;               // (eps mode: converged before this iteration)
   extern __shared__ __align__(16) float rs_sm[];
   const int k = a.k, kp = a.kp, k8 = rs_k8(k);
   const int lane = threadIdx.x;

@@ -687,6 +687,8 @@ WLR_DEVI void s_apply(SS& s, const SmallArgs& a, const double* Cs, int ldc, cons
 //          the library runs it on a second stream concurrently with them.
 template <int BT, int PART>
 __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_constant__ SmallArgs a) {
+  if (a.stop && *a.stop) return;               // (eps mode: latched before the iteration; every CTA of the
+                                               //  cluster reads the same value, so none waits at a barrier)
   if (PART != 1) pdl_wait();                   // (part 1 waits inside its first load round)
   // a programmatic dependent may start now: the only one is the propagation iteration's row pass,
   // which reads W'_p / X1_p (never this kernel's outputs) and never waits on it

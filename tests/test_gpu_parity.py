@@ -173,4 +173,31 @@ def test_stopping_rule_eps():
     done, conv = w.wlr_iterate(h, 100)
     o = oracle.swlr(A, synth.dense_W1(cfg, W1, cfg.m), cfg.k, cfg.r, iters=100, eps=eps)
     assert conv and o.converged
-    assert abs(done - (len(o.trace) - 1)) <= 1
+    assert done == len(o.trace) - 1, (done, len(o.trace) - 1)
+
+
+@pytest.mark.parametrize("ci,check_every", [(1, 1), (1, 8), (3, 8), (2, 3)])
+def test_stopping_rule_on_device(ci, check_every):
+    """eps > 0: the stopping rule (R3) is applied on the device -- the iterations
+    launched after the first state that satisfies it do no work -- so the returned state is that
+    state whatever the host's check period, and further wlr_iterate calls leave it unchanged."""
+    import torch
+    w = gu.need_gpu()
+    cfg = synth.CONFIGS[ci]
+    A, W1 = gu.inputs(cfg)
+    eps = 1e-7
+    h = w.wlr_init(torch.from_numpy(A).cuda(), cfg.k, cfg.r, None, w1=cfg.w_const, eps=eps,
+                   check_every=check_every)
+    done, conv = w.wlr_iterate(h, 100)
+    o = oracle.swlr(A.astype(np.float64), synth.dense_W1(cfg, W1, cfg.m), cfg.k, cfg.r, iters=100, eps=eps)
+    assert conv and o.converged
+    assert done == len(o.trace) - 1, (done, len(o.trace) - 1)
+    tr = w.wlr_trace(h)
+    assert tr.shape[0] == done + 1
+    F = w.wlr_objective(h)[0]
+    X1 = w.wlr_result(h)["X1"].copy()
+    more, conv2 = w.wlr_iterate(h, 10)
+    assert more == 0 and conv2
+    assert w.wlr_objective(h)[0] == F
+    np.testing.assert_array_equal(w.wlr_result(h)["X1"], X1)
+    assert abs(F - o.trace[-1]["F"]) <= gu.TOL_F[cfg.dtype] * abs(o.trace[-1]["F"])
