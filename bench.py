@@ -155,6 +155,22 @@ def ncu_traffic(kernel_key, config):
         return None
 
 
+def oracle_crossing(config, eps):
+    """The fp64 oracle's stopping iteration for the same start (GHS) and eps (R3),
+    read from the committed oracle fixture's trace (tests/fixtures, written by
+    scripts/make_oracle_fixtures.py from oracle/ only), or None."""
+    p = os.path.join(ROOT, "tests", "fixtures", f"oracle_cfg{config}.npz")
+    if not os.path.exists(p):
+        return None
+    d = np.load(p)
+    keys = list(d["trace_keys"])
+    tr = d["trace"]
+    for q in range(1, tr.shape[0]):
+        if tr[q, keys.index("rel")] < eps or tr[q, keys.index("step")] < eps:
+            return q
+    return None
+
+
 # ------------------------------------------------------------------------ reference arm
 def run_reference(args, cfg, world, rank):
     if rank != 0:
@@ -245,6 +261,8 @@ def main():
         os.execv(sys.executable, cmd)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")   # (the communicator lines show the N ranks)
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
@@ -449,7 +467,8 @@ def main():
         Ft, st_, rl_ = w.wlr_objective(ht)
         w.wlr_destroy(ht)
         ttt = {"eps": 1e-7, "iters": done, "converged": conv, "ms": (t2 - t1) * 1e3,
-               "ms_incl_init": (t2 - t0) * 1e3, "final_rel_step": rl_}
+               "ms_incl_init": (t2 - t0) * 1e3, "final_rel_step": rl_,
+               "oracle_iters": oracle_crossing(args.config, 1e-7)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
