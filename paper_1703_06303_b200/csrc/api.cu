@@ -153,7 +153,7 @@ struct wlr_ctx {
   CUtensorMap tmW1{}, tmWT1{};
   // Gram propagation (uniform W1, prop.cu): A^T A, Q_p = A^T X1_p (by parity), scratch
   bool prop = false;
-  double *AtA = nullptr, *Qg[2] = {nullptr, nullptr}, *Hs = nullptr, *dgs = nullptr;
+  double *AtA = nullptr, *Qg[2] = {nullptr, nullptr}, *Hs = nullptr, *dgs = nullptr, *GAY = nullptr;
   int* pcnt = nullptr;
   double a1sq = 0.0;
   cudaStream_t st3 = nullptr;  // row-pass branch of a propagation iteration
@@ -392,6 +392,11 @@ static void set_prefetch(wlr_ctx* h, int ph, const void** ptr, int64_t* bytes) {
 
 // Small-step arguments of iteration p (phase ph = p mod 6): state slot p mod 3 -> (p+1) mod 3,
 // increments / exchange block by p mod 2.
+// prop1 stages the warm block Y ((n-k) x b doubles) in its W' area ((n+k) x rp fp32 values)
+static bool gay_fits(const wlr_ctx* h) {
+  return h->b <= 32 && (size_t)(h->n - h->k) * h->b * 8 <= (size_t)(h->n + h->k) * h->rp * 4;
+}
+
 static SmallArgs small_args(wlr_ctx* h, int ph, int mode) {
   const int cur = ph % 3, nxt = (ph + 1) % 3, par = ph & 1;
   SmallArgs s{};
@@ -412,6 +417,7 @@ static SmallArgs small_args(wlr_ctx* h, int ph, int mode) {
   s.WtT = wb1 ? h->WtT1 : h->WtT; s.KW = h->KW;
   s.eps = h->opts.eps; s.tol = h->opts.eig_tol; s.max_outer = h->opts.eig_max_outer; s.max_deg = 16;
   s.stop = (mode != 0 && h->opts.eps > 0.0) ? h->flags + 6 : nullptr;   // eps mode: latched stop flag
+  s.GAY = (mode != 0 && h->prop && gay_fits(h)) ? h->GAY : nullptr;                      // (computed by prop1)
   s.cold = 0;
   s.tdbg = h->ktime ? h->tdbg : nullptr;
   s.pl = h->spl;
@@ -530,6 +536,7 @@ static wlr_status enqueue_prop_iteration(wlr_ctx* h, int ph) {
   pa.n = (int)h->n; pa.k = (int)h->k;
   set_prefetch(h, ph, pa.pf_ptr, pa.pf_bytes);   // K3a(p)'s inputs, issued at prop1's entry
   pa.stop = h->opts.eps > 0.0 ? h->flags + 6 : nullptr;
+  pa.Y = h->Y; pa.GAY = gay_fits(h) ? h->GAY : nullptr; pa.b = h->b;   // G_A Y of the warm block for K3a(p)'s first S-product
   SmallArgs sa = small_args(h, ph, 1);
   cudaError_t e;
   if (prof) {   // eager profiling pass: everything serial on st, one event group per kernel kind
@@ -1025,6 +1032,7 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
       if ((s = dalloc_t(h, &h->Qg[i], (size_t)n * k)) != WLR_OK) return s;
     if ((s = dalloc_t(h, &h->Hs, prop_part_doubles((int)n, (int)k))) != WLR_OK) return s;
     if ((s = dalloc_t(h, &h->dgs, (size_t)k)) != WLR_OK) return s;
+    if ((s = dalloc_t(h, &h->GAY, (size_t)nk * 32)) != WLR_OK) return s;   // (n-k) x b, b <= 32
     if ((s = dalloc_t(h, &h->pcnt, 1)) != WLR_OK) return s;
   }
   if ((s = dalloc_t(h, &h->fw0, 2)) != WLR_OK) return s;

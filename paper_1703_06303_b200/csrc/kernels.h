@@ -125,6 +125,8 @@ struct PropArgs {
   int n, k;
   const void* pf_ptr[kPf]; int64_t pf_bytes[kPf];   // L2 prefetch of the small step's inputs (prop1 entry)
   const int* stop;                  // eps mode: the iteration's latched stop flag, or nullptr
+  const double* Y; double* GAY;     // warm Ritz block Y ((n-k) x b) -> G_A Y for the small step's first S-product
+  int b;
 };
 size_t prop1_smem(int n);
 size_t prop1_smem(int n, int k);
@@ -220,6 +222,7 @@ struct SmallArgs {
   int k, nk, t, b, kp, k0, rp;      // dims; b = eigen block width (t <= b <= 32)
   int pdl;                          // host only: launch as a programmatic dependent (part 1)
   const int* stop;                  // eps mode: the iteration's latched stop flag (skip the step), or nullptr
+  const double* GAY;                // G_A Y of the warm block, precomputed (Gram propagation), or nullptr
   int KA;                           // row offset of the X1_p block of the row-pass Wt
   void* WtT; int KW;                // fp32 W'^T (RP x KW, K-major) for the tensor-core row pass
   int mode;                         // 0: init (G, M given), 1: iteration (apply increments)

@@ -208,6 +208,36 @@ __global__ void __launch_bounds__(kPropT1) prop1_kernel(const __grid_constant__ 
     a.part[(((int64_t)l * 3 + 1) * nb + b) * k + ar] = h;     // H column l (entry ar)
     a.part[(((int64_t)ar * 3 + 2) * nb + b) * k + l] = g;     // Gp row ar
   }
+  // G_A Y for the small step's first S-product (Y = the warm Ritz block K3a(p-1) left; G_A = the
+  // A2 block of A^T A, whose rows are staged here): rows i >= k of the block, (n-k) x b.  Y is staged
+  // in the W' area (free once the partials above are done).
+  if (a.GAY) {
+    const int bw = a.b, ny = nk * bw;
+    double* Ys = reinterpret_cast<double*>(Wr);
+    __syncthreads();                                   // (the partials' last reads of W')
+    for (int r0 = 0; r0 < ny; r0 += 8 * kPropT1) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) { const int idx = r0 + u * kPropT1 + tid; v[u] = idx < ny ? a.Y[idx] : 0.0; }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) { const int idx = r0 + u * kPropT1 + tid; if (idx < ny) Ys[idx] = v[u]; }
+    }
+    __syncthreads();
+    const int nout = nr * bw;
+    int tpo = kPropT1 / (nout > 0 ? nout : 1);          // threads per output (power of 2, <= 32)
+    tpo = tpo >= 32 ? 32 : tpo >= 16 ? 16 : tpo >= 8 ? 8 : tpo >= 4 ? 4 : tpo >= 2 ? 2 : 1;
+    for (int o0 = 0; o0 < nout; o0 += kPropT1 / tpo) {
+      const int o = o0 + tid / tpo, g = tid % tpo;
+      const int r = o / bw, j = o - r * bw;
+      double v = 0.0;
+      if (o < nout && i0 + r >= k) {
+        const double* ar = rows + r * n + k;
+        for (int l = g; l < nk; l += tpo) v = fma(ar[l], Ys[l * bw + j], v);
+      }
+      for (int sft = tpo >> 1; sft > 0; sft >>= 1) v += __shfl_xor_sync(0xffffffffu, v, sft);
+      if (g == 0 && o < nout && i0 + r >= k) a.GAY[(int64_t)(i0 + r - k) * bw + j] = v;
+    }
+  }
 #undef Ws
   pdl_trigger();
 }

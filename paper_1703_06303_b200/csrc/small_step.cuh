@@ -536,7 +536,8 @@ template <int PW>
 WLR_DEVI void s_product_impl(double* smb, int rs, int nl, int SL, int k, int nk, int KS, int JS,
                               int64_t oRed, int64_t oXf, const double* GA, int64_t xoff, int ldx,
                               int w, const double* Wk, const double* Mp, int ldm, double* Z,
-                              int ldz, SS* ms = nullptr, const SmallArgs* ma = nullptr, bool pre = false) {
+                              int ldz, SS* ms = nullptr, const SmallArgs* ma = nullptr, bool pre = false,
+                              const double* gay = nullptr) {
   struct { int rs, nl, SL, k, nk; double* sm; } s = {rs, nl, SL, k, nk, smb};
   struct { int KS, JS; } p = {KS, JS};
   cg::cluster_group cl = cg::this_cluster();
@@ -575,9 +576,18 @@ WLR_DEVI void s_product_impl(double* smb, int rs, int nl, int SL, int k, int nk,
   double acc0[PW], acc1[PW];
 #pragma unroll
   for (int j = 0; j < PW; ++j) { acc0[j] = 0.0; acc1[j] = 0.0; }
+  if (wj > 0 && gay) {   // G_A X precomputed (the propagation kernel, X = the warm block): its slice
+    if (ks == 0)
+#pragma unroll
+      for (int j = 0; j < PW; ++j)
+        if (j < wj) {
+          acc0[j] = has0 ? gay[(int64_t)(s.rs + lane) * w + j0 + j] : 0.0;
+          acc1[j] = has1 ? gay[(int64_t)(s.rs + lane + 32) * w + j0 + j] : 0.0;
+        }
+  }
   if (wj > 0) {
     const double* gcol = GA + s.rs;
-    const int lg = min(l1, s.nk);
+    const int lg = gay ? 0 : min(l1, s.nk);
 #ifndef WLR_SP_U
 #define WLR_SP_U 8
 #endif
@@ -654,16 +664,18 @@ WLR_DEVI void s_product_impl(double* smb, int rs, int nl, int SL, int k, int nk,
 
 template <int PW>
 WLR_DEVI void s_product(SS& s, const SmallArgs& a, int64_t xoff, int ldx, int w,
-                        const double* Wk, const double* Mp, int ldm, double* Z, int ldz, bool pre = false) {
+                        const double* Wk, const double* Mp, int ldm, double* Z, int ldz, bool pre = false,
+                        const double* gay = nullptr) {
   s_product_impl<PW>(s.sm, s.rs, s.nl, s.SL, s.k, s.nk, a.pl.KS, a.pl.JS, a.pl.oRed, a.pl.oXf,
-                     a.GA, xoff, ldx, w, Wk, Mp, ldm, Z, ldz, &s, &a, pre);
+                     a.GA, xoff, ldx, w, Wk, Mp, ldm, Z, ldz, &s, &a, pre, gay);
 }
 
 // One S-product of the basis X (local slice at offset xoff, width w = row stride):
 // exchange of the C' X partials, then the distributed product into Z (local offset).
 template <int PW>
 WLR_DEVI void s_apply(SS& s, const SmallArgs& a, const double* Cs, int ldc, const double* Ms,
-                      int ldm, int64_t xoff, int w, int64_t zoff, int* nprod, bool pre = false) {
+                      int ldm, int64_t xoff, int w, int64_t zoff, int* nprod, bool pre = false,
+                      const double* gay = nullptr) {
   const SSPlan& p = a.pl;
   const double* X = s.sm + xoff;
   double* part = xpart(s, p);
@@ -673,7 +685,7 @@ WLR_DEVI void s_apply(SS& s, const SmallArgs& a, const double* Cs, int ldc, cons
   double* Wk = s.sm + p.oWk;
   xreduce(s, p, s.k * w, Wk);
   tmark(s, a);                                 // [p2] C X exchange
-  s_product<PW>(s, a, xoff, w, w, Wk, Ms, ldm, s.sm + zoff, w, pre);
+  s_product<PW>(s, a, xoff, w, w, Wk, Ms, ldm, s.sm + zoff, w, pre, gay);
   ++*nprod;
 }
 
@@ -904,7 +916,8 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
     bool ortho = !a.cold;                      // Y expected orthonormal (warm Ritz block)
     while (true) {
       // ---- Rayleigh-Ritz on span(Y):  Z = S Y;  Gyy = Y^T Y, Gyz = Y^T Z (generalised RR)
-      s_apply<PW>(s, a, Cs, ldc, Ms, ldm, buf[iY], b, buf[iZ], &nprod, xf_pre && outer == 0);
+      s_apply<PW>(s, a, Cs, ldc, Ms, ldm, buf[iY], b, buf[iZ], &nprod, xf_pre && outer == 0,
+                  xf_pre && outer == 0 ? a.GAY : nullptr);
       tmark(s, a);                             // product
       {
         const double* Y = s.sm + buf[iY];

@@ -8,7 +8,9 @@ import torch
 import synth
 import paper_1703_06303_b200 as w
 
-def run(ci, warm=8, H=None, Wd=None):
+FLUSH = torch.empty(0)
+
+def run(ci, warm=8, H=None, Wd=None, flush=False):
     cfg = synth.CONFIGS[ci]
     if H:
         cfg = synth.scaled(cfg, H, Wd)
@@ -18,7 +20,10 @@ def run(ci, warm=8, H=None, Wd=None):
     h = w.wlr_init(A, cfg.k, cfg.r, W1, w1=cfg.w_const or 1.0)
     w.wlr_iterate(h, warm)
     w.wlr_debug_state(h, "ktime_on")
-    for rep in range(2):
+    for rep in range(3):
+        if flush:
+            FLUSH.fill_(float(rep))
+            torch.cuda.synchronize()
         w.wlr_iterate_async(h, 1)
         torch.cuda.synchronize()
         kt = w.wlr_debug_state(h, "ktime")   # [0:64] K3a(p), [64:128] K3b(p-1) (ran beside it)
@@ -30,7 +35,7 @@ def run(ci, warm=8, H=None, Wd=None):
                 continue
             d = np.diff(ts) / 1e3
             mhz = (ck[-1] - ck[0]) / max(ts[-1] - ts[0], 1) * 1e3
-            print(f"cfg{ci} {name} total={(ts[-1]-ts[0])/1e3:.1f}us clk={mhz:.0f}MHz phases(us)=" + " ".join(f"{x:.1f}" for x in d))
+            print(f"cfg{ci}{'F' if flush else ''} {name} total={(ts[-1]-ts[0])/1e3:.1f}us clk={mhz:.0f}MHz phases(us)=" + " ".join(f"{x:.1f}" for x in d))
             xb = kt[128 + off: 128 + off + 32]
             xb = xb[xb > 0]
             if len(xb):
@@ -45,6 +50,10 @@ def run(ci, warm=8, H=None, Wd=None):
 
 
 for c in (sys.argv[1:] or ["1", "2", "3", "4"]):
+    if c.startswith("F"):               # "F3": flush L2 (256 MB write) before each iteration, as bench.py does
+        FLUSH = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+        run(int(c[1:]), flush=True)
+        continue
     if c == "4":
         run(4, H=120, Wd=160)
     else:
