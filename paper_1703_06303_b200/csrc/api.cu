@@ -154,7 +154,6 @@ struct wlr_ctx {
   // Gram propagation (uniform W1, prop.cu): A^T A, Q_p = A^T X1_p (by parity), scratch
   bool prop = false;
   double *AtA = nullptr, *Qg[2] = {nullptr, nullptr}, *Hs = nullptr, *dgs = nullptr, *GAY = nullptr;
-  int* pcnt = nullptr;
   double a1sq = 0.0;
   cudaStream_t st3 = nullptr;  // row-pass branch of a propagation iteration
   cudaStream_t st4 = nullptr;  // critical chain (prop -> K3a) of a propagation iteration, high priority
@@ -180,6 +179,9 @@ struct wlr_ctx {
   double *Y = nullptr, *k3x[2] = {nullptr, nullptr};
   double *xchg = nullptr, *xchg2 = nullptr, *red = nullptr, *scal = nullptr, *trace = nullptr;
   double* tdbg = nullptr;      // K3 phase timestamps (wlr_debug_state "ktime")
+  int prop_nb = 0;             // prop1 CTAs (min(n, #SMs))
+  unsigned long long* prop_ts = nullptr;   // (diagnostics: WLR_PROP_TS=1, prop1 phase stamps)
+  bool k3b_early = true;       // K3b(p-1) forks at the iteration start (WLR_K3B_EARLY=0: after prop1)
   SmallArgs last_ss{};         // arguments of the last small-step launch (diagnostics)
   bool ktime = false;
   int trace_cap = 4096;
@@ -392,10 +394,8 @@ static void set_prefetch(wlr_ctx* h, int ph, const void** ptr, int64_t* bytes) {
 
 // Small-step arguments of iteration p (phase ph = p mod 6): state slot p mod 3 -> (p+1) mod 3,
 // increments / exchange block by p mod 2.
-// prop1 stages the warm block Y ((n-k) x b doubles) in its W' area ((n+k) x rp fp32 values)
-static bool gay_fits(const wlr_ctx* h) {
-  return h->b <= 32 && (size_t)(h->n - h->k) * h->b * 8 <= (size_t)(h->n + h->k) * h->rp * 4;
-}
+// prop1 computes G_A Y of the warm block (Y fragments in registers: b <= 8, n - k <= 768)
+static bool gay_fits(const wlr_ctx* h) { return prop_gay_ok((int)h->n, (int)h->k, h->b, h->nsm); }
 
 static SmallArgs small_args(wlr_ctx* h, int ph, int mode) {
   const int cur = ph % 3, nxt = (ph + 1) % 3, par = ph & 1;
@@ -417,7 +417,9 @@ static SmallArgs small_args(wlr_ctx* h, int ph, int mode) {
   s.WtT = wb1 ? h->WtT1 : h->WtT; s.KW = h->KW;
   s.eps = h->opts.eps; s.tol = h->opts.eig_tol; s.max_outer = h->opts.eig_max_outer; s.max_deg = 16;
   s.stop = (mode != 0 && h->opts.eps > 0.0) ? h->flags + 6 : nullptr;   // eps mode: latched stop flag
-  s.GAY = (mode != 0 && h->prop && gay_fits(h)) ? h->GAY : nullptr;                      // (computed by prop1)
+  s.GAY = (mode != 0 && h->prop && gay_fits(h)) ? h->GAY : nullptr;
+  s.dg = (mode != 0 && h->prop) ? h->dgs : nullptr;   // f_w from prop2's diagonal terms
+  s.a1sq = h->a1sq;                      // (computed by prop1)
   s.cold = 0;
   s.tdbg = h->ktime ? h->tdbg : nullptr;
   s.pl = h->spl;
@@ -531,12 +533,14 @@ static wlr_status enqueue_prop_iteration(wlr_ctx* h, int ph) {
   PropArgs pa{};
   pa.AtA = h->AtA; pa.Wt = cur ? h->Wt1 : h->Wt; pa.RP = h->rp; pa.KA = h->KA;
   pa.Qp = h->Qg[cur]; pa.Qn = h->Qg[nxt]; pa.Gp = h->G[slot]; pa.part = h->Hs;
-  pa.inc = h->inc[cur]; pa.dg = h->dgs; pa.counter = h->pcnt;
+  pa.inc = h->inc[cur]; pa.dg = h->dgs;
   pa.w2 = h->w1s * h->w1s; pa.a1sq = h->a1sq;
   pa.n = (int)h->n; pa.k = (int)h->k;
   set_prefetch(h, ph, pa.pf_ptr, pa.pf_bytes);   // K3a(p)'s inputs, issued at prop1's entry
   pa.stop = h->opts.eps > 0.0 ? h->flags + 6 : nullptr;
   pa.Y = h->Y; pa.GAY = gay_fits(h) ? h->GAY : nullptr; pa.b = h->b;   // G_A Y of the warm block for K3a(p)'s first S-product
+  pa.ts = h->prop_ts;
+  pa.nb = h->prop_nb;
   SmallArgs sa = small_args(h, ph, 1);
   cudaError_t e;
   if (prof) {   // eager profiling pass: everything serial on st, one event group per kernel kind
@@ -568,7 +572,7 @@ static wlr_status enqueue_prop_iteration(wlr_ctx* h, int ph) {
     CUDA_TRY(h, cudaStreamWaitEvent(h->st4, h->ev_fork, 0));
     if ((e = launch_prop(pa, false, 0, h->st4, h->ev_f3)) != cudaSuccess) return fail(h, WLR_ECUDA, std::string("Gram propagation: ") + cudaGetErrorString(e));
     if (pend) {
-      CUDA_TRY(h, cudaStreamWaitEvent(h->st2, h->ev_f3, 0));
+      CUDA_TRY(h, cudaStreamWaitEvent(h->st2, h->k3b_early ? h->ev_fork : h->ev_f3, 0));
       if ((e = launch_deferred(h, h->pend, h->st2)) != cudaSuccess) return fail(h, WLR_ECUDA, std::string("small step (deferred): ") + cudaGetErrorString(e));
       CUDA_TRY(h, cudaEventRecord(h->ev_join, h->st2));
     }
@@ -1024,16 +1028,22 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
     if ((s = dalloc_t(h, &h->inc[i], (size_t)(k * nk + 2 * k * k + 1))) != WLR_OK) return s;
   {   // Gram propagation for the linear (uniform-W1) X1 half-step (prop.cu; WLR_PROP=0 disables, A/B)
     const char* pe = std::getenv("WLR_PROP");
-    h->prop = h->uniform && h->dtype == WLR_F32 && (!pe || std::atoi(pe) != 0) && prop1_smem((int)n, (int)k) <= 220 * 1024 &&
-              16 * k * k <= 200 * 1024;
+    if (const char* ke = std::getenv("WLR_K3B_EARLY")) h->k3b_early = std::atoi(ke) != 0;
+    h->prop = h->uniform && h->dtype == WLR_F32 && (!pe || std::atoi(pe) != 0) && prop1_smem((int)n, (int)k, h->nsm, h->b) <= 227 * 1024 &&
+              prop1_rb((int)n, h->nsm) <= 8 && 16 * k * k <= 200 * 1024;
+    h->prop_nb = (int)std::min<int64_t>(n, h->nsm);
   }
   if (h->prop) {
     for (int i = 0; i < 2; ++i)
       if ((s = dalloc_t(h, &h->Qg[i], (size_t)n * k)) != WLR_OK) return s;
-    if ((s = dalloc_t(h, &h->Hs, prop_part_doubles((int)n, (int)k))) != WLR_OK) return s;
+    if ((s = dalloc_t(h, &h->Hs, prop_part_doubles(h->prop_nb, (int)k))) != WLR_OK) return s;
     if ((s = dalloc_t(h, &h->dgs, (size_t)k)) != WLR_OK) return s;
+    if (const char* pt = std::getenv("WLR_PROP_TS"); pt && std::atoi(pt)) {
+      void* q = nullptr;
+      if ((s = dalloc(h, &q, (size_t)8 * 8 * h->prop_nb)) != WLR_OK) return s;
+      h->prop_ts = (unsigned long long*)q;
+    }
     if ((s = dalloc_t(h, &h->GAY, (size_t)nk * 32)) != WLR_OK) return s;   // (n-k) x b, b <= 32
-    if ((s = dalloc_t(h, &h->pcnt, 1)) != WLR_OK) return s;
   }
   if ((s = dalloc_t(h, &h->fw0, 2)) != WLR_OK) return s;
   if ((s = dalloc_t(h, &h->GA, (size_t)nk * nk)) != WLR_OK) return s;
@@ -1676,6 +1686,7 @@ extern "C" wlr_status wlr_debug_state(wlr_handle h, const char* name, double* ou
     return WLR_OK;
   }
   else if (nm == "itctime") { src = (const double*)h->itc_tstamp; cnt = h->itc_tstamp ? 8 * 4096 : 0; }
+  else if (nm == "proptime") { src = (const double*)h->prop_ts; cnt = h->prop_ts ? 8 * h->prop_nb : 0; }
   else if (nm == "tctime") { src = (const double*)h->tc_tstamp; cnt = h->tc_tstamp ? 16 * h->tc_grid : 0; }
   else if (nm == "ktime_on" || nm == "ktime_off") {   // enable/disable K3 phase timestamps
     h->ktime = nm == "ktime_on";

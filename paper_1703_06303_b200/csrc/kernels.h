@@ -120,17 +120,19 @@ struct PropArgs {
   double* part;                     // ceil(n/RB) x 2 x k x k per-block partials (scratch)
   double* inc;                      // packed [N | Gamma | Omega | f_w] for the small step
   double* dg;                       // k scratch: f_w's diagonal terms
-  int* counter;                     // zero-initialised; prop2's last CTA resets it
   double w2, a1sq;                  // w^2, ||A1||_F^2
   int n, k;
   const void* pf_ptr[kPf]; int64_t pf_bytes[kPf];   // L2 prefetch of the small step's inputs (prop1 entry)
   const int* stop;                  // eps mode: the iteration's latched stop flag, or nullptr
   const double* Y; double* GAY;     // warm Ritz block Y ((n-k) x b) -> G_A Y for the small step's first S-product
   int b;
+  int nb;                           // prop1 CTAs (= blocks of the partials): min(n, #SMs)
+  unsigned long long* ts;           // (diagnostics, or nullptr) prop1 phase %globaltimer stamps, 8 per CTA
 };
-size_t prop1_smem(int n);
-size_t prop1_smem(int n, int k);
-size_t prop_part_doubles(int n, int k);
+size_t prop1_smem(int n, int k, int nsm, int b);   // dynamic shared memory of prop1 (one CTA per SM)
+int prop1_rb(int n, int nsm);               // rows per prop1 CTA (<= 8 supported)
+size_t prop_part_doubles(int nb, int k);
+bool prop_gay_ok(int n, int k, int b, int nsm);   // prop1 computes G_A Y of the warm block (Y fits in smem)
 // virtual-group sum: out[i] = sum_{g < G} in[g * stride + i], g in order (fixed, deterministic)
 // eps mode: flags[6] = flags[2] (the converged flag) at the start of an iteration, one thread, so that
 // every kernel of the iteration (clusters included) sees one consistent value
@@ -223,6 +225,8 @@ struct SmallArgs {
   int pdl;                          // host only: launch as a programmatic dependent (part 1)
   const int* stop;                  // eps mode: the iteration's latched stop flag (skip the step), or nullptr
   const double* GAY;                // G_A Y of the warm block, precomputed (Gram propagation), or nullptr
+  const double* dg;                 // Gram propagation: prop2's diagonal terms of f_w (k), or nullptr
+  double a1sq;                      //   and ||A1||_F^2: CTA 0 writes f_w for the deferred half
   int KA;                           // row offset of the X1_p block of the row-pass Wt
   void* WtT; int KW;                // fp32 W'^T (RP x KW, K-major) for the tensor-core row pass
   int mode;                         // 0: init (G, M given), 1: iteration (apply increments)

@@ -15,9 +15,10 @@
 // w^2 (||A1||^2 - 2 tr Q + tr G) cancels to ~1e-16 ||A1||^2 / ||A1 - X1||^2, too coarse in fp64 mode).
 // W' is read in the storage dtype the row pass uses (fp32 in fp32 mode), upcast exactly.
 //
-// prop1: CTA b owns the 8 rows [8b, 8b + 8) of the n index: Q_{p+1} rows (A^T A rows and all of
-//        W' staged in shared memory), N columns, and the per-block partials
-//        Hp[b] = W'_A(rows)^T Q_p(rows), Gp[b] = Q_{p+1}(rows)^T W'_A(rows)   (k x k each).
+// prop1: CTA b of nb = min(n, #SMs) owns RB = ceil(n / nb) (or RB - 1) consecutive rows of the n
+//        index: Q_{p+1} rows (A^T A rows and all of W' staged in shared memory), N columns, the
+//        per-block partials Hp[b] = W'_A(rows)^T Q_p(rows), Gp[b] = Q_{p+1}(rows)^T W'_A(rows)
+//        (k x k each), and G_A Y of the warm Ritz block for the small step's first S-product.
 // prop2: CTA a sums row a (and column a) of the partials in block order and adds the k x k terms:
 //        row a of H, of H^T, of G_{p+1}; writes row a of Gamma and Omega.
 // fp64 throughout; every sum has a fixed order (replicas and reruns bitwise identical).
@@ -30,59 +31,105 @@ namespace cg = cooperative_groups;
 namespace wlr {
 
 constexpr int kPropT = 256;        // prop2 threads
-constexpr int kPropT1 = 256;       // prop1 threads: 32 lanes (columns l) x 8 groups (j ranges)
-constexpr int kPropG = kPropT1 / 32;
-constexpr int kPropRB = 4;         // n-index rows per prop1 CTA
-
-WLR_DEVI int warp_id_prop1(int tid) { return tid >> 5; }
+constexpr int kPropT1 = 512;       // prop1 threads (16 warps: one CTA per SM)
+constexpr int kPropRBmax = 8;      // max n-index rows per prop1 CTA (the grid is min(n, #SMs) CTAs)
 
 template <typename T>
 WLR_DEVI double wld(const void* W, int64_t i) { return (double)reinterpret_cast<const T*>(W)[i]; }
 
-// shared layout of prop1: AtA rows (8 x n doubles) | reduction (8 x 8 x 32 doubles) | Q_p, Q_{p+1}
-// rows (8 x k doubles each) | W'_A rows 0..n-1 and W'_X rows (k), RP elements each in the storage
-// dtype, bulk-copied (fp32: RP = 32 for k <= 32, so W' is 80 KB) | mbarrier
-// reduction slots x columns of prop1 (the shuffle path when k rounds to 8 column blocks)
-__host__ __device__ inline int prop1_slots(int k) {   // (slots x 4 ncb doubles per row)
-  const int ncb = (k + 3) / 4;
-  return ncb == 8 ? (kPropT1 / 32) * 32 : (kPropT1 / ncb) * 4 * ncb;
+WLR_DEVI void pstamp(const PropArgs& a, int i) {   // (diagnostics: wlr_debug_state "proptime")
+  if (a.ts && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.ts[blockIdx.x * 8 + i] = t;
+  }
 }
+
+// rows of prop1 CTA b of nb: n = nb * base + ext, the first ext CTAs take base + 1 rows
+WLR_DEVI void prop1_rows(int n, int nb, int b, int& i0, int& nr) {
+  const int base = n / nb, ext = n - base * nb;
+  i0 = b * base + min(b, ext);
+  nr = base + (b < ext ? 1 : 0);
+}
+// Q column blocks of 4, rounded up to a power of 2 (lanes of one column block are reduced by shuffles)
+__host__ __device__ inline int prop1_ncbp(int k) {
+  const int ncb = (k + 3) / 4;
+  int p = 1;
+  while (p < ncb) p *= 2;
+  return p;
+}
+// G_A Y in prop1: thread (output o = (row, column), lane g of tpo threads per output) sums
+// l = g, g + tpo, ... < n - k
+__host__ __device__ inline int prop1_gay_tpo(int nout) {
+  int t = kPropT1 / (nout > 0 ? nout : 1);
+  return t >= 32 ? 32 : t >= 16 ? 16 : t >= 8 ? 8 : t >= 4 ? 4 : t >= 2 ? 2 : 1;
+}
+int prop1_rb(int n, int nsm) { return (n + std::min(n, nsm) - 1) / std::min(n, nsm); }
+
+// shared layout of prop1 (RB rows): A^T A rows (RB x n doubles; reused for the j-group reduction,
+// 16 warps x RB x 4 ncbp doubles, once the rows are consumed) | Q_p, Q_{p+1} rows (RB x k each) |
+// Y ((n - k) x b doubles, when G_A Y is computed here) | W'_A rows 0..n-1 and W'_X rows (k), RP
+// elements each in the storage dtype, bulk-copied (fp32: RP = 32 for k <= 32, so W' is 80 KB at
+// config 3) | mbarriers
 static size_t prop1_wbytes(int n, int k, int RP, int es) { return (size_t)(n + k) * RP * es; }
-size_t prop1_smem(int n, int k, int RP, int es) {
-  return sizeof(double) * ((size_t)kPropRB * n + (size_t)kPropRB * prop1_slots(k) + 2 * kPropRB * k) +
+__host__ __device__ inline int prop1_even(int x) { return (x + 1) & ~1; }   // (16-byte region starts)
+__host__ __device__ inline int prop1_rows_doubles(int n, int k, int rb) {
+  return prop1_even(rb * (n > (kPropT1 / 32) * 4 * prop1_ncbp(k) ? n : (kPropT1 / 32) * 4 * prop1_ncbp(k)));
+}
+size_t prop1_smem(int n, int k, int RP, int es, int rb, int ys) {
+  return sizeof(double) * ((size_t)prop1_rows_doubles(n, k, rb) + prop1_even(2 * rb * k) + prop1_even(ys)) +
          prop1_wbytes(n, k, RP, es) + 32;
 }
-size_t prop1_smem(int n) { return prop1_smem(n, 32, 32, 4); }
-size_t prop1_smem(int n, int k) { return prop1_smem(n, k, (k + 31) / 32 * 32, 4); }
+// with G_A Y (the warm block Y, (n - k) x b doubles, staged in shared memory) when it fits
+size_t prop1_smem(int n, int k, int nsm, int b) {
+  const int RP = (k + 31) / 32 * 32, rb = prop1_rb(n, nsm);
+  const size_t with = prop1_smem(n, k, RP, 4, rb, (n - k) * b);
+  return with <= 227 * 1024 ? with : prop1_smem(n, k, RP, 4, rb, 0);
+}
+bool prop_gay_ok(int n, int k, int b, int nsm) {
+  const int RP = (k + 31) / 32 * 32, rb = prop1_rb(n, nsm);
+  return b >= 1 && rb * b <= kPropT1 && prop1_smem(n, k, RP, 4, rb, (n - k) * b) <= 227 * 1024;
+}
 
-template <typename T>
-__global__ void __launch_bounds__(kPropT1) prop1_kernel(const __grid_constant__ PropArgs a) {
+// prop1: CTA b owns RB (or RB - 1) consecutive rows i0.. of the n index (FP64 CUDA cores; the
+// m8n8k4 DMMA chain measured 3x slower for these shapes, profiles/r02_prop_dmma.log):
+//   G_A Y rows (the small step's first S-product operand; needs only the A^T A rows, so it runs
+//   while W' is still in flight), Q_{p+1} rows = [A^T A rows | Q_p rows] . [W'_A ; W'_X], N columns,
+//   and the per-block partials Hp = W'_A(rows)^T Q_p(rows), Gp = Q_{p+1}(rows)^T W'_A(rows).
+template <typename T, int RB>
+__global__ void __launch_bounds__(kPropT1, 1) prop1_kernel(const __grid_constant__ PropArgs a) {
   if (a.stop && *a.stop) return;               // (eps mode: converged before this iteration)
+  pstamp(a, 0);
   extern __shared__ __align__(16) double pr_sm[];
   const int n = a.n, k = a.k, nk = n - k, RP = a.RP, kk = k * k;
-  const int tid = threadIdx.x, lane = tid & 31, grp = tid >> 5;     // kPropG groups split the j sum
-  const int b = blockIdx.x, i0 = b * kPropRB, nr = min(kPropRB, n - i0);
-  double* rows = pr_sm;                                  // nr x n rows of A^T A
-  double* red = rows + kPropRB * n;                      // kPropG groups x kPropRB rows x 32
-  double* Qps = red + kPropRB * prop1_slots(k);                  // nr x k  Q_p rows
-  double* Qns = Qps + kPropRB * k;                       // nr x k  Q_{p+1} rows
-  T* Wr = reinterpret_cast<T*>(Qns + kPropRB * k);       // (n + k) x RP  [W'_A ; W'_X], storage dtype
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int b = blockIdx.x;
+  int i0, nr;
+  prop1_rows(n, a.nb, b, i0, nr);
+  const int ncbp = prop1_ncbp(k), ncb = (k + 3) / 4;
+  double* rows = pr_sm;                                  // nr x n rows of A^T A (then the reduction)
+  double* Qps = rows + prop1_rows_doubles(n, k, RB);     // RB x k  Q_p rows
+  double* Qns = Qps + RB * k;                            // RB x k  Q_{p+1} rows
+  double* Ys = Qps + prop1_even(2 * RB * k);             // (n - k) x b  Y (G_A Y only)
+  T* Wr = reinterpret_cast<T*>(Ys + prop1_even(a.GAY ? nk * a.b : 0));   // (n + k) x RP  [W'_A ; W'_X], storage dtype
   uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(Wr) + (size_t)(n + k) * RP * sizeof(T));
   const uint32_t wa_bytes = (uint32_t)((size_t)n * RP * sizeof(T)), wx_bytes = (uint32_t)((size_t)k * RP * sizeof(T));
-  if (warp_id_prop1(tid) == 7) {   // the small step (K3a) that follows reads these: pull them into L2
-    for (int r = 0; r < kPf; ++r) {                // now (the bench flushes L2 before every iteration)
-      const char* base = reinterpret_cast<const char*>(a.pf_ptr[r]);
-      const int64_t nb = a.pf_bytes[r] & ~(int64_t)15;
-      if (!base || nb <= 0) continue;
-      const int64_t chunk = 8192, nchunk = (nb + chunk - 1) / chunk;   // spread over all CTAs
-      for (int64_t c = blockIdx.x + (int64_t)gridDim.x * (tid & 31); c < nchunk; c += (int64_t)gridDim.x * 32) {
-        const int64_t off = c * chunk;
-        const unsigned sz = (unsigned)(nb - off < chunk ? nb - off : chunk);
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(base + off), "r"(sz) : "memory");
-      }
+  // G_A Y for the small step's first S-product (Y = the warm Ritz block K3a(p-1) left, complete
+  // before this kernel starts; G_A = the A2 block of A^T A, whose rows this CTA stages): rows i >= k
+  // of the block, (n-k) x b.  Y is staged in shared memory now (coalesced, rounds of 8 loads in
+  // flight); the sums run while W' is still in flight.
+  const int gbw = a.b, gnout = a.GAY ? nr * gbw : 0, gtpo = prop1_gay_tpo(gnout);
+  if (gnout > 0) {
+    const int ny = nk * gbw;
+    for (int r0 = 0; r0 < ny; r0 += 8 * kPropT1) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) { const int idx = r0 + u * kPropT1 + tid; v[u] = idx < ny ? a.Y[idx] : 0.0; }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) { const int idx = r0 + u * kPropT1 + tid; if (idx < ny) Ys[idx] = v[u]; }
     }
   }
-  const bool bulk_rows = ((size_t)n * 8) % 16 == 0;      // A^T A rows by bulk copy when 16-byte aligned
+  const bool bulk_rows = ((size_t)n * 8) % 16 == 0 && ((size_t)i0 * n * 8) % 16 == 0;   // 16-byte aligned
   // two barriers, each used for ONE phase: a parity wait on a barrier that has since moved two
   // phases on (rows, then W') would wait for a phase that never completes
   if (tid == 0) {
@@ -110,135 +157,142 @@ __global__ void __launch_bounds__(kPropT1) prop1_kernel(const __grid_constant__ 
     }
   }
   __syncthreads();
+  pstamp(a, 1);
   pdl_wait();                                            // W' (K3) and Q_p (previous prop)
+  pstamp(a, 2);
   if (tid == 0) {                                        // W' rows by two bulk copies
     mbar_expect_tx(bar, wa_bytes + wx_bytes);
     bulk_load_1d(Wr, a.Wt, wa_bytes, bar);
     bulk_load_1d(Wr + (size_t)n * RP, reinterpret_cast<const T*>(a.Wt) + (size_t)a.KA * RP, wx_bytes, bar);
   }
-  for (int idx = tid; idx < nr * k; idx += kPropT1) Qps[idx] = a.Qp[(int64_t)i0 * k + idx];
+  for (int idx = tid; idx < RB * k; idx += kPropT1) Qps[idx] = idx < nr * k ? a.Qp[(int64_t)i0 * k + idx] : 0.0;
+  if (w == 15) {   // the small step (K3a) that follows reads these: pull them into L2 now (the
+    for (int r = 0; r < kPf; ++r) {              // bench flushes L2 before every iteration)
+      const char* base = reinterpret_cast<const char*>(a.pf_ptr[r]);
+      const int64_t nbt = a.pf_bytes[r] & ~(int64_t)15;
+      if (!base || nbt <= 0) continue;
+      const int64_t chunk = 8192, nchunk = (nbt + chunk - 1) / chunk;   // spread over all CTAs
+#pragma unroll 1
+      for (int64_t c = blockIdx.x + (int64_t)gridDim.x * lane; c < nchunk; c += (int64_t)gridDim.x * 32) {
+        const int64_t off = c * chunk;
+        const unsigned sz = (unsigned)(nbt - off < chunk ? nbt - off : chunk);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(base + off), "r"(sz) : "memory");
+      }
+    }
+  }
   if (bulk_rows) mbar_wait(bar + 1, 0);                  // the A^T A rows
+  if (gnout > 0) {
+    for (int o0 = 0; o0 < gnout; o0 += kPropT1 / gtpo) {
+      const int o = o0 + tid / gtpo, g = tid % gtpo, r = o / gbw, j = o - r * gbw;
+      const bool valid = o < gnout && i0 + r >= k;
+      double v4[4] = {0.0, 0.0, 0.0, 0.0};
+      if (valid) {
+        const double* ar = rows + r * n + k;
+        int l = g;
+        for (; l + 3 * gtpo < nk; l += 4 * gtpo) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) v4[q] = fma(ar[l + q * gtpo], Ys[(l + q * gtpo) * gbw + j], v4[q]);
+        }
+        for (; l < nk; l += gtpo) v4[0] = fma(ar[l], Ys[l * gbw + j], v4[0]);
+      }
+      double v = (v4[0] + v4[1]) + (v4[2] + v4[3]);
+      for (int sft = gtpo >> 1; sft > 0; sft >>= 1) v += __shfl_xor_sync(0xffffffffu, v, sft);
+      if (g == 0 && valid) a.GAY[(int64_t)(i0 + r - k) * gbw + j] = v;
+    }
+  }
+  pstamp(a, 3);
   mbar_wait(bar, 0);                                     // W'
   __syncthreads();
-#define Ws(j, l) ((double)Wr[(int64_t)(j) * RP + (l)])
-  // Q_{p+1} rows: thread = (column block cb of 4 columns, j group jg); 4 rows x 4 columns of
-  // accumulators; the j groups are summed through shared memory in a fixed order
+  pstamp(a, 4);
+  // Q_{p+1} rows: thread = (column block cb of 4 columns, j group jg); RB rows x 4 columns of
+  // accumulators.  The j groups split the combined sum over [A^T A rows | Q_p rows] . [W'_A ; W'_X]
+  // (n + k terms) evenly; they are summed in a fixed order: within a warp by shuffles (the lanes
+  // of one column block), then over the 16 warps through shared memory (in the rows' place).
   {
-    const int ncb = (k + 3) / 4, njg = kPropT1 / ncb;      // (k <= 128: ncb <= 32, njg >= 8)
-    const int cb = tid % ncb, jg = tid / ncb;
-    double acc[kPropRB][4];
+    const int njg = kPropT1 / ncbp;                      // (ncbp <= 32: 16 or more j groups)
+    const int cb = tid % ncbp, jg = tid / ncbp;
+    double acc[RB][4];
 #pragma unroll
-    for (int r = 0; r < kPropRB; ++r)
+    for (int r = 0; r < RB; ++r)
 #pragma unroll
       for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
-    if (jg < njg) {
-      const int jlo = (int)((int64_t)n * jg / njg), jhi = (int)((int64_t)n * (jg + 1) / njg);
+    if (cb < ncb) {
+      const int nj = n + k;
+      const int jlo = (int)((int64_t)nj * jg / njg), jhi = (int)((int64_t)nj * (jg + 1) / njg);
+      const int jae = min(jhi, n);
 #pragma unroll 2
-      for (int j = jlo; j < jhi; ++j) {
+      for (int j = jlo; j < jae; ++j) {
         double wv[4];
-        if constexpr (sizeof(T) == 4) {
-          const float4 w4 = *reinterpret_cast<const float4*>(Wr + (int64_t)j * RP + 4 * cb);
-          wv[0] = w4.x; wv[1] = w4.y; wv[2] = w4.z; wv[3] = w4.w;
-        } else {
+        const float4 w4 = *reinterpret_cast<const float4*>(Wr + (int64_t)j * RP + 4 * cb);
+        wv[0] = w4.x; wv[1] = w4.y; wv[2] = w4.z; wv[3] = w4.w;
 #pragma unroll
-          for (int c = 0; c < 4; ++c) wv[c] = (double)Wr[(int64_t)j * RP + 4 * cb + c];
-        }
-#pragma unroll
-        for (int r = 0; r < kPropRB; ++r) {
+        for (int r = 0; r < RB; ++r) {
           const double av = rows[r * n + j];
 #pragma unroll
           for (int c = 0; c < 4; ++c) acc[r][c] = fma(av, wv[c], acc[r][c]);
         }
       }
-      if (jg == njg - 1)                                 // + Q_p W'_X
-        for (int q = 0; q < k; ++q) {
+      for (int j = max(jlo, n); j < jhi; ++j) {          // + Q_p W'_X (rows n.. of W')
+        const int q = j - n;
+        double wv[4];
+        const float4 w4 = *reinterpret_cast<const float4*>(Wr + (int64_t)j * RP + 4 * cb);
+        wv[0] = w4.x; wv[1] = w4.y; wv[2] = w4.z; wv[3] = w4.w;
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const double wv = (double)Wr[(int64_t)(n + q) * RP + 4 * cb + c];
+        for (int r = 0; r < RB; ++r) {
+          const double qv = Qps[r * k + q];
 #pragma unroll
-            for (int r = 0; r < kPropRB; ++r) acc[r][c] = fma(Qps[r * k + q], wv, acc[r][c]);
-          }
+          for (int c = 0; c < 4; ++c) acc[r][c] = fma(qv, wv[c], acc[r][c]);
         }
+      }
     }
-    // fixed-order sum over the j groups: within a warp by shuffles (ncb = 8: 4 j groups per warp),
-    // then over the warps through shared memory, slots [warp][r][4 cb + c]
-    double* red2 = red;                                  // 8 warps x kPropRB x (4 ncb) doubles
-    const int w4 = 4 * ncb;
-    const bool shfl = ncb == 8;
-    if (shfl) {
+    for (int sft = ncbp; sft < 32; sft *= 2)
 #pragma unroll
-      for (int r = 0; r < kPropRB; ++r)
+      for (int r = 0; r < RB; ++r)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          acc[r][c] += __shfl_xor_sync(0xffffffffu, acc[r][c], 8);
-          acc[r][c] += __shfl_xor_sync(0xffffffffu, acc[r][c], 16);
-        }
-    }
-    const int nslot = shfl ? kPropT1 / 32 : njg, slot = shfl ? tid / 32 : jg;
-    if (jg < njg && (!shfl || (tid & 31) < 8))
+        for (int c = 0; c < 4; ++c) acc[r][c] += __shfl_xor_sync(0xffffffffu, acc[r][c], sft);
+    const int w4n = 4 * ncbp, nsl = kPropT1 / 32;
+    __syncthreads();                                     // (every warp is done with the rows)
+    double* red = rows;                                  // [warp][r][4 ncbp]
+    if (lane < ncbp)
 #pragma unroll
-      for (int r = 0; r < kPropRB; ++r)
+      for (int r = 0; r < RB; ++r)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) red2[((int64_t)slot * kPropRB + r) * w4 + 4 * cb + c] = acc[r][c];
+        for (int c = 0; c < 4; ++c) red[((int64_t)w * RB + r) * w4n + 4 * cb + c] = acc[r][c];
     __syncthreads();
-    for (int o = tid; o < kPropRB * w4; o += kPropT1) {
-      const int r = o / w4, ll = o - r * w4;
-      if (r < nr && ll < k) {
-        double v = 0.0;
-        for (int g = 0; g < nslot; ++g) v += red2[((int64_t)g * kPropRB + r) * w4 + ll];
+    for (int o = tid; o < RB * k; o += kPropT1) {
+      const int r = o / k, ll = o - r * k;
+      double v = 0.0;
+      for (int g = 0; g < nsl; ++g) v += red[((int64_t)g * RB + r) * w4n + ll];
+      Qns[o] = v;
+      if (r < nr) {
         const int i = i0 + r;
-        Qns[r * k + ll] = v;
         a.Qn[(int64_t)i * k + ll] = v;
-        if (i >= k) a.inc[(int64_t)ll * nk + (i - k)] = v - Qps[r * k + ll];   // N = M_{p+1} - M_p
+        if (i >= k) a.inc[(int64_t)ll * nk + (i - k)] = v - Qps[o];   // N = M_{p+1} - M_p
       }
     }
     __syncthreads();
   }
+  pstamp(a, 5);
   // per-block partials of H and of Q_{p+1}^T W'_A over the block's rows, stored for prop2's CTA a
   // as three contiguous [nb][k] panels: row a of Hp, column a of Hp, row a of Gp
-  const int nb = (n + kPropRB - 1) / kPropRB;
+  const int nb = a.nb;
+#define Ws(j, l) ((double)Wr[(int64_t)(j) * RP + (l)])
   for (int idx = tid; idx < kk; idx += kPropT1) {
     const int ar = idx / k, l = idx - ar * k;
     double h = 0.0, g = 0.0;
-    for (int r = 0; r < nr; ++r) {
-      h = fma(Ws(i0 + r, ar), Qps[r * k + l], h);
-      g = fma(Qns[r * k + ar], Ws(i0 + r, l), g);
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      if (r < nr) {
+        h = fma(Ws(i0 + r, ar), Qps[r * k + l], h);
+        g = fma(Qns[r * k + ar], Ws(i0 + r, l), g);
+      }
     }
     a.part[(((int64_t)ar * 3 + 0) * nb + b) * k + l] = h;     // H row ar
     a.part[(((int64_t)l * 3 + 1) * nb + b) * k + ar] = h;     // H column l (entry ar)
     a.part[(((int64_t)ar * 3 + 2) * nb + b) * k + l] = g;     // Gp row ar
   }
-  // G_A Y for the small step's first S-product (Y = the warm Ritz block K3a(p-1) left; G_A = the
-  // A2 block of A^T A, whose rows are staged here): rows i >= k of the block, (n-k) x b.  Y is staged
-  // in the W' area (free once the partials above are done).
-  if (a.GAY) {
-    const int bw = a.b, ny = nk * bw;
-    double* Ys = reinterpret_cast<double*>(Wr);
-    __syncthreads();                                   // (the partials' last reads of W')
-    for (int r0 = 0; r0 < ny; r0 += 8 * kPropT1) {
-      double v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) { const int idx = r0 + u * kPropT1 + tid; v[u] = idx < ny ? a.Y[idx] : 0.0; }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) { const int idx = r0 + u * kPropT1 + tid; if (idx < ny) Ys[idx] = v[u]; }
-    }
-    __syncthreads();
-    const int nout = nr * bw;
-    int tpo = kPropT1 / (nout > 0 ? nout : 1);          // threads per output (power of 2, <= 32)
-    tpo = tpo >= 32 ? 32 : tpo >= 16 ? 16 : tpo >= 8 ? 8 : tpo >= 4 ? 4 : tpo >= 2 ? 2 : 1;
-    for (int o0 = 0; o0 < nout; o0 += kPropT1 / tpo) {
-      const int o = o0 + tid / tpo, g = tid % tpo;
-      const int r = o / bw, j = o - r * bw;
-      double v = 0.0;
-      if (o < nout && i0 + r >= k) {
-        const double* ar = rows + r * n + k;
-        for (int l = g; l < nk; l += tpo) v = fma(ar[l], Ys[l * bw + j], v);
-      }
-      for (int sft = tpo >> 1; sft > 0; sft >>= 1) v += __shfl_xor_sync(0xffffffffu, v, sft);
-      if (g == 0 && o < nout && i0 + r >= k) a.GAY[(int64_t)(i0 + r - k) * bw + j] = v;
-    }
-  }
 #undef Ws
+  pstamp(a, 6);
   pdl_trigger();
 }
 
@@ -256,7 +310,7 @@ __global__ void __cluster_dims__(3, 1, 1) __launch_bounds__(kPropT) prop2_kernel
   const int n = a.n, k = a.k, nk = n - k, RP = a.RP, kk = k * k;
   const int tid = threadIdx.x;
   const int ar = blockIdx.x / 3, which = (int)cl.block_rank();
-  const int nb = (n + kPropRB - 1) / kPropRB;
+  const int nb = a.nb;
   double* Wx = p2_sm;                                      // k x k   W'_X      (rank 0)
   double* Gs = Wx + kk;                                    // k x k   G_p       (rank 0)
   if (which == 0) {
@@ -331,49 +385,40 @@ __global__ void __cluster_dims__(3, 1, 1) __launch_bounds__(kPropT) prop2_kernel
     om[ar * k + c] = g - hrow[c] - hcol[c] + gp;
     if (c == ar) a.dg[ar] = g - 2.0 * a.Qn[(int64_t)ar * k + ar];   // f_w's diagonal terms
   }
-  // f_w = w^2 ||A1 - X1_{p+1}||^2 = w^2 (||A1||^2 + sum_a (G_{p+1} - 2 A1^T X1_{p+1})[a][a]) by the
-  // last row to finish, in a fixed order (fp32 mode only: the cancellation costs ~1e-16 w^2 ||A1||^2
-  // absolute, ~1e-12 of F at configs 2-3), so that no per-iteration quantity depends on the shards
-  __shared__ bool last;
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) last = atomicAdd(a.counter, 1) == (int)gridDim.x / 3 - 1;
-  __syncthreads();
-  if (last) {                                  // (loads in parallel: a serial load->add chain costs
-    __threadfence();                           //  one L2 round trip per term)
-    __shared__ double dsum[128];
-    for (int q = tid; q < k; q += kPropT) dsum[q] = __ldcg(a.dg + q);
-    __syncthreads();
-    if (tid == 0) {
-      double sd = 0.0;
-      for (int q = 0; q < k; ++q) sd += dsum[q];
-      om[(int64_t)kk] = a.w2 * (a.a1sq + sd);
-      *a.counter = 0;
-    }
-  }
+  // (f_w = w^2 (||A1||^2 + sum_a dg[a]) is summed by the small step's CTA 0, which runs next)
   pdl_trigger();
 }
 
 cudaError_t launch_prop(const PropArgs& a, bool f64, int pdl, cudaStream_t st, cudaEvent_t after1) {
-  const size_t sm1 = prop1_smem(a.n, a.k, a.RP, f64 ? 8 : 4);
+  if (f64) return cudaErrorNotSupported;       // (Gram propagation is the fp32 path, api.cu)
+  const int rb = (a.n + a.nb - 1) / a.nb;
+  if (rb < 1 || rb > kPropRBmax) return cudaErrorInvalidValue;
+  const size_t sm1 = prop1_smem(a.n, a.k, a.RP, 4, rb, a.GAY ? (a.n - a.k) * a.b : 0);
   const size_t sm2 = sizeof(double) * 2 * (size_t)a.k * a.k;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cudaLaunchConfig_t c1{};
-  c1.gridDim = dim3((a.n + kPropRB - 1) / kPropRB);
+  c1.gridDim = dim3(a.nb);
   c1.blockDim = dim3(kPropT1);
   c1.dynamicSmemBytes = sm1;
   c1.stream = st;
   c1.attrs = at;
   c1.numAttrs = 1;
   cudaError_t e;
-  if (f64) {
-    cudaFuncSetAttribute(prop1_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
-    e = cudaLaunchKernelEx(&c1, prop1_kernel<double>, a);
-  } else {
-    cudaFuncSetAttribute(prop1_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
-    e = cudaLaunchKernelEx(&c1, prop1_kernel<float>, a);
+  auto go1 = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
+    return cudaLaunchKernelEx(&c1, kern, a);
+  };
+  switch (rb) {
+    case 1: e = go1(prop1_kernel<float, 1>); break;
+    case 2: e = go1(prop1_kernel<float, 2>); break;
+    case 3: e = go1(prop1_kernel<float, 3>); break;
+    case 4: e = go1(prop1_kernel<float, 4>); break;
+    case 5: e = go1(prop1_kernel<float, 5>); break;
+    case 6: e = go1(prop1_kernel<float, 6>); break;
+    case 7: e = go1(prop1_kernel<float, 7>); break;
+    default: e = go1(prop1_kernel<float, 8>); break;
   }
   if (e != cudaSuccess) return e;
   if (after1 && (e = cudaEventRecord(after1, st)) != cudaSuccess) return e;   // (prop1 done)
@@ -387,10 +432,6 @@ cudaError_t launch_prop(const PropArgs& a, bool f64, int pdl, cudaStream_t st, c
   c2.stream = st;
   c2.attrs = at2;
   c2.numAttrs = 1;
-  if (f64) {
-    cudaFuncSetAttribute(prop2_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
-    return cudaLaunchKernelEx(&c2, prop2_kernel<double>, a);
-  }
   cudaFuncSetAttribute(prop2_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
   return cudaLaunchKernelEx(&c2, prop2_kernel<float>, a);
 }
@@ -416,6 +457,6 @@ cudaError_t launch_vsum(double* out, const double* in, int G, size_t stride, siz
   return cudaGetLastError();
 }
 
-size_t prop_part_doubles(int n, int k) { return (size_t)((n + kPropRB - 1) / kPropRB) * 3 * k * k; }
+size_t prop_part_doubles(int nb, int k) { return (size_t)nb * 3 * k * k; }
 
 }  // namespace wlr

@@ -864,6 +864,13 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
       tom = warp_sum(tom);
       tg = warp_sum(tg);
       if ((threadIdx.x & 31) == 0) a.flags[5] = tom <= 1e-6 * tg ? 1 : 0;
+      if (a.dg) {   // Gram propagation: f_w = w^2 ||A1 - X1_{p+1}||^2 = w^2 (||A1||^2 + sum_a dg[a]),
+                    // dg[a] = (G_{p+1} - 2 A1^T X1_{p+1})[a][a] from prop2 (fixed-order warp sum)
+        double sd = 0.0;
+        for (int q = threadIdx.x & 31; q < k; q += 32) sd += __ldcg(a.dg + q);
+        sd = warp_sum(sd);
+        if ((threadIdx.x & 31) == 0) const_cast<double*>(incOm)[(int64_t)kk] = a.w2 * (a.a1sq + sd);
+      }
     }
     tmark(s, a);                               // [1a] Gram update loads
     bool okinv = a.mode ? ns_inverse(Gq, Xq, Rq, Pq, k, red) : false;
