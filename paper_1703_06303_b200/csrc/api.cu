@@ -1040,7 +1040,7 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
     if ((s = dalloc_t(h, &h->dgs, (size_t)k)) != WLR_OK) return s;
     if (const char* pt = std::getenv("WLR_PROP_TS"); pt && std::atoi(pt)) {
       void* q = nullptr;
-      if ((s = dalloc(h, &q, (size_t)8 * 8 * h->prop_nb)) != WLR_OK) return s;
+      if ((s = dalloc(h, &q, (size_t)8 * 8 * (h->prop_nb + 3 * k))) != WLR_OK) return s;
       h->prop_ts = (unsigned long long*)q;
     }
     if ((s = dalloc_t(h, &h->GAY, (size_t)nk * 32)) != WLR_OK) return s;   // (n-k) x b, b <= 32
@@ -1686,7 +1686,7 @@ extern "C" wlr_status wlr_debug_state(wlr_handle h, const char* name, double* ou
     return WLR_OK;
   }
   else if (nm == "itctime") { src = (const double*)h->itc_tstamp; cnt = h->itc_tstamp ? 8 * 4096 : 0; }
-  else if (nm == "proptime") { src = (const double*)h->prop_ts; cnt = h->prop_ts ? 8 * h->prop_nb : 0; }
+  else if (nm == "proptime") { src = (const double*)h->prop_ts; cnt = h->prop_ts ? 8 * (h->prop_nb + 3 * h->k) : 0; }
   else if (nm == "tctime") { src = (const double*)h->tc_tstamp; cnt = h->tc_tstamp ? 16 * h->tc_grid : 0; }
   else if (nm == "ktime_on" || nm == "ktime_off") {   // enable/disable K3 phase timestamps
     h->ktime = nm == "ktime_on";

@@ -37,11 +37,11 @@ constexpr int kPropRBmax = 8;      // max n-index rows per prop1 CTA (the grid i
 template <typename T>
 WLR_DEVI double wld(const void* W, int64_t i) { return (double)reinterpret_cast<const T*>(W)[i]; }
 
-WLR_DEVI void pstamp(const PropArgs& a, int i) {   // (diagnostics: wlr_debug_state "proptime")
+WLR_DEVI void pstamp(const PropArgs& a, int i, int base = 0) {   // (diagnostics: wlr_debug_state "proptime")
   if (a.ts && threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    a.ts[blockIdx.x * 8 + i] = t;
+    a.ts[(base + blockIdx.x) * 8 + i] = t;
   }
 }
 
@@ -296,97 +296,107 @@ __global__ void __launch_bounds__(kPropT1, 1) prop1_kernel(const __grid_constant
   pdl_trigger();
 }
 
-// prop2: one 3-CTA cluster per row a: rank 0 sums row a of the H partials, rank 1 column a of
-// them, rank 2 row a of the Gp partials (each a contiguous [nb][k] panel, 8 warps over the block
-// range); rank 0 gathers the other two sums through distributed shared memory and finishes row a.
+// prop2: CTA a (of k) finishes row a: 15 warps sum the three [nb][k] partial panels of row a (row a
+// of Hp, column a of Hp, row a of Gp; 5 warps per panel over the block range, one round of loads),
+// then the k x k terms: row a of H, of H^T and of G_{p+1}; writes row a of Gamma and Omega.
+constexpr int kPropT2 = 512;
+constexpr int kP2Sub = 5;                      // warps per panel
 template <typename T>
-__global__ void __cluster_dims__(3, 1, 1) __launch_bounds__(kPropT) prop2_kernel(const __grid_constant__ PropArgs a) {
-  if (a.stop && *a.stop) return;               // (consistent for the whole cluster: latched flag)
-  __shared__ double vrow[128];
+__global__ void __launch_bounds__(kPropT2) prop2_kernel(const __grid_constant__ PropArgs a) {
+  if (a.stop && *a.stop) return;
+  pstamp(a, 0, a.nb);
   __shared__ double hrow[128], hcol[128], grow[128];
-  __shared__ double wred[8][128];
   extern __shared__ __align__(16) double p2_sm[];
-  cg::cluster_group cl = cg::this_cluster();
   const int n = a.n, k = a.k, nk = n - k, RP = a.RP, kk = k * k;
-  const int tid = threadIdx.x;
-  const int ar = blockIdx.x / 3, which = (int)cl.block_rank();
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const int ar = blockIdx.x;
   const int nb = a.nb;
-  double* Wx = p2_sm;                                      // k x k   W'_X      (rank 0)
-  double* Gs = Wx + kk;                                    // k x k   G_p       (rank 0)
-  if (which == 0) {
-    for (int r0 = 0; r0 < kk; r0 += 4 * kPropT) {         // (G_p, W': not written by prop1)
-      double v[4], x[4];
+  double* Wx = p2_sm;                                      // k x k   W'_X
+  double* Gs = Wx + kk;                                    // k x k   G_p
+  double* wred = Gs + kk;                                  // 3 x kP2Sub x k  panel partial sums
+  for (int r0 = 0; r0 < kk; r0 += 2 * kPropT2) {          // (G_p, W': not written by prop1)
+    double v[2], x[2];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int idx = r0 + u * kPropT + tid, q = idx / k;
-        v[u] = idx < kk ? a.Gp[idx] : 0.0;
-        x[u] = idx < kk ? wld<T>(a.Wt, (int64_t)(a.KA + q) * RP + (idx - q * k)) : 0.0;
-      }
+    for (int u = 0; u < 2; ++u) {
+      const int idx = r0 + u * kPropT2 + tid, q = idx / k;
+      v[u] = idx < kk ? a.Gp[idx] : 0.0;
+      x[u] = idx < kk ? wld<T>(a.Wt, (int64_t)(a.KA + q) * RP + (idx - q * k)) : 0.0;
+    }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int idx = r0 + u * kPropT + tid;
-        if (idx < kk) { Gs[idx] = v[u]; Wx[idx] = x[u]; }
-      }
+    for (int u = 0; u < 2; ++u) {
+      const int idx = r0 + u * kPropT2 + tid;
+      if (idx < kk) { Gs[idx] = v[u]; Wx[idx] = x[u]; }
     }
   }
+  pstamp(a, 1, a.nb);
   pdl_wait();
-  {
-    const int w = tid >> 5, lane = tid & 31;
-    const int b0 = (int)((int64_t)nb * w / 8), b1 = (int)((int64_t)nb * (w + 1) / 8);
-    const double* P = a.part + ((int64_t)ar * 3 + which) * nb * k;
+  pstamp(a, 2, a.nb);
+  if (w < 3 * kP2Sub) {
+    const int pn = w / kP2Sub, sub = w - pn * kP2Sub;
+    const int b0 = (int)((int64_t)nb * sub / kP2Sub), b1 = (int)((int64_t)nb * (sub + 1) / kP2Sub);
+    const double* P = a.part + ((int64_t)ar * 3 + pn) * nb * k;
     for (int c0 = 0; c0 < k; c0 += 32) {
       const int c = c0 + lane;
       double v = 0.0;
       if (c < k) {
-        for (int bb = b0; bb < b1; bb += 16) {
-          double x[16];
+        for (int bb = b0; bb < b1; bb += 32) {           // (nb <= 160: one round)
+          double x[32];
 #pragma unroll
-          for (int u = 0; u < 16; ++u) x[u] = bb + u < b1 ? P[(int64_t)(bb + u) * k + c] : 0.0;
+          for (int u = 0; u < 32; ++u) x[u] = bb + u < b1 ? __ldcg(P + (int64_t)(bb + u) * k + c) : 0.0;
 #pragma unroll
-          for (int u = 0; u < 16; ++u) v += x[u];
+          for (int u = 0; u < 32; ++u) v += x[u];
         }
-        wred[w][c] = v;
+        wred[(pn * kP2Sub + sub) * k + c] = v;
       }
     }
   }
   __syncthreads();
-  for (int c = tid; c < k; c += kPropT) {
+  pstamp(a, 3, a.nb);
+  for (int o = tid; o < 3 * k; o += kPropT2) {             // fixed-order sums over the sub-ranges
+    const int pn = o / k, c = o - pn * k;
     double v = 0.0;
-    for (int w = 0; w < 8; ++w) v += wred[w][c];
-    vrow[c] = v;
-  }
-  cl.sync();
-  if (which == 0) {
-    const double* v1 = cl.map_shared_rank(vrow, 1);
-    const double* v2 = cl.map_shared_rank(vrow, 2);
-    for (int c = tid; c < k; c += kPropT) { hrow[c] = vrow[c]; hcol[c] = v1[c]; grow[c] = v2[c]; }
-  }
-  cl.sync();                                   // (ranks 1, 2 keep their shared memory until read)
-  if (which != 0) return;
-  for (int o = tid; o < 2 * k; o += kPropT) {    // + W'_X^T G_p terms of H (row a) and H^T (column a)
-    const int c = o < k ? o : o - k;
-    double v = 0.0;
-    if (o < k) {
-      for (int q = 0; q < k; ++q) v = fma(Wx[q * k + ar], Gs[q * k + c], v);
-      hrow[c] += v;
-    } else {
-      for (int q = 0; q < k; ++q) v = fma(Wx[q * k + c], Gs[q * k + ar], v);
-      hcol[c] += v;
-    }
+    for (int sub = 0; sub < kP2Sub; ++sub) v += wred[(pn * kP2Sub + sub) * k + c];
+    (pn == 0 ? hrow : pn == 1 ? hcol : grow)[c] = v;
   }
   __syncthreads();
+  pstamp(a, 4, a.nb);
+  // + W'_X^T G_p terms of H (row a) and H^T (column a): 8 lanes per output, q split, shuffle sum
+  for (int o0 = 0; o0 < 2 * k; o0 += kPropT2 / 8) {
+    const int o = o0 + tid / 8, g = tid & 7;
+    const int c = o < k ? o : o - k;
+    double v = 0.0;
+    if (o < 2 * k) {
+      if (o < k) for (int q = g; q < k; q += 8) v = fma(Wx[q * k + ar], Gs[q * k + c], v);
+      else       for (int q = g; q < k; q += 8) v = fma(Wx[q * k + c], Gs[q * k + ar], v);
+    }
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    v += __shfl_xor_sync(0xffffffffu, v, 4);
+    if (o < 2 * k && g == 0) (o < k ? hrow : hcol)[c] += v;
+  }
+  __syncthreads();
+  pstamp(a, 5, a.nb);
   double* gam = a.inc + (int64_t)k * nk;
   double* om = gam + (int64_t)kk;
-  for (int c = tid; c < k; c += kPropT) {
-    double g = grow[c];                                    // G_{p+1}[a][c] = ... + (H W'_X)[a][c]
-    for (int q = 0; q < k; ++q) g = fma(hrow[q], Wx[q * k + c], g);
-    const double gp = Gs[ar * k + c];
-    gam[ar * k + c] = hrow[c] - gp;
-    om[ar * k + c] = g - hrow[c] - hcol[c] + gp;
-    if (c == ar) a.dg[ar] = g - 2.0 * a.Qn[(int64_t)ar * k + ar];   // f_w's diagonal terms
+  for (int c0 = 0; c0 < k; c0 += kPropT2 / 8) {
+    const int c = c0 + tid / 8, g = tid & 7;
+    double v = 0.0;                                        // (H W'_X)[a][c]
+    if (c < k)
+      for (int q = g; q < k; q += 8) v = fma(hrow[q], Wx[q * k + c], v);
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    v += __shfl_xor_sync(0xffffffffu, v, 4);
+    if (c < k && g == 0) {
+      const double gv = grow[c] + v;                       // G_{p+1}[a][c]
+      const double gp = Gs[ar * k + c];
+      gam[ar * k + c] = hrow[c] - gp;
+      om[ar * k + c] = gv - hrow[c] - hcol[c] + gp;
+      if (c == ar) a.dg[ar] = gv - 2.0 * a.Qn[(int64_t)ar * k + ar];   // f_w's diagonal terms
+    }
   }
   // (f_w = w^2 (||A1||^2 + sum_a dg[a]) is summed by the small step's CTA 0, which runs next)
   pdl_trigger();
+  pstamp(a, 6, a.nb);
 }
 
 cudaError_t launch_prop(const PropArgs& a, bool f64, int pdl, cudaStream_t st, cudaEvent_t after1) {
@@ -394,7 +404,7 @@ cudaError_t launch_prop(const PropArgs& a, bool f64, int pdl, cudaStream_t st, c
   const int rb = (a.n + a.nb - 1) / a.nb;
   if (rb < 1 || rb > kPropRBmax) return cudaErrorInvalidValue;
   const size_t sm1 = prop1_smem(a.n, a.k, a.RP, 4, rb, a.GAY ? (a.n - a.k) * a.b : 0);
-  const size_t sm2 = sizeof(double) * 2 * (size_t)a.k * a.k;
+  const size_t sm2 = sizeof(double) * (2 * (size_t)a.k * a.k + 3 * kP2Sub * (size_t)a.k);
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
@@ -426,8 +436,8 @@ cudaError_t launch_prop(const PropArgs& a, bool f64, int pdl, cudaStream_t st, c
   at2[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at2[0].val.programmaticStreamSerializationAllowed = 1;
   cudaLaunchConfig_t c2{};
-  c2.gridDim = dim3(3 * a.k);                  // 3-CTA clusters (__cluster_dims__)
-  c2.blockDim = dim3(kPropT);
+  c2.gridDim = dim3(a.k);
+  c2.blockDim = dim3(kPropT2);
   c2.dynamicSmemBytes = sm2;
   c2.stream = st;
   c2.attrs = at2;
