@@ -86,6 +86,35 @@ __device__ __noinline__ void gemm_cc(int n, const double* A, const double* B, do
     C[o] = (v0 + v1) + (v2 + v3);
   }
 }
+// register-blocked CUDA-core: thread = RR x CC block of outputs, q loop unrolled by 2
+template <int RR, int CC>
+__device__ __noinline__ void gemm_rb(int n, const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C) {
+  const int nbr = (n + RR - 1) / RR, nbc = (n + CC - 1) / CC;
+  for (int o = threadIdx.x; o < nbr * nbc; o += blockDim.x) {
+    const int r0 = (o / nbc) * RR, c0 = (o % nbc) * CC;
+    double acc[RR][CC];
+#pragma unroll
+    for (int i = 0; i < RR; ++i)
+#pragma unroll
+      for (int j = 0; j < CC; ++j) acc[i][j] = 0.0;
+#pragma unroll 2
+    for (int q = 0; q < n; ++q) {
+      double a[RR], b[CC];
+#pragma unroll
+      for (int i = 0; i < RR; ++i) a[i] = r0 + i < n ? A[(r0 + i) * n + q] : 0.0;
+#pragma unroll
+      for (int j = 0; j < CC; ++j) b[j] = c0 + j < n ? B[q * n + c0 + j] : 0.0;
+#pragma unroll
+      for (int i = 0; i < RR; ++i)
+#pragma unroll
+        for (int j = 0; j < CC; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+#pragma unroll
+    for (int i = 0; i < RR; ++i)
+#pragma unroll
+      for (int j = 0; j < CC; ++j) if (r0 + i < n && c0 + j < n) C[(r0 + i) * n + c0 + j] = acc[i][j];
+  }
+}
 template <int MODE>
 __global__ void k(int n, unsigned long long* out, double* sink) {
   __shared__ double A[1024], B[1024], C[1024];
@@ -100,6 +129,9 @@ __global__ void k(int n, unsigned long long* out, double* sink) {
     if (MODE == 3) gemm_tcn<4>(n, A, B, C);
     if (MODE == 4) gemm_tcn<8>(n, A, B, C);
     if (MODE == 5) gemm_tcn<1>(n, A, B, C);
+    if (MODE == 6) gemm_rb<1, 2>(n, A, B, C);
+    if (MODE == 7) gemm_rb<2, 2>(n, A, B, C);
+    if (MODE == 8) gemm_rb<1, 1>(n, A, B, C);
     __syncthreads();
     if (MODE == 0 || MODE == 1) { if (threadIdx.x < 1024) {} }
   }
@@ -116,6 +148,11 @@ int main() {
     k<3><<<1, 512>>>(n, d, s); cudaDeviceSynchronize(); k<3><<<1, 512>>>(n, d, s); cudaMemcpy(&g[0], d, 8, cudaMemcpyDeviceToHost);
     k<4><<<1, 512>>>(n, d, s); cudaDeviceSynchronize(); k<4><<<1, 512>>>(n, d, s); cudaMemcpy(&g[1], d, 8, cudaMemcpyDeviceToHost);
     k<5><<<1, 512>>>(n, d, s); cudaDeviceSynchronize(); k<5><<<1, 512>>>(n, d, s); cudaMemcpy(&g[2], d, 8, cudaMemcpyDeviceToHost);
+    unsigned long long q[3];
+    k<6><<<1, 512>>>(n, d, s); cudaDeviceSynchronize(); k<6><<<1, 512>>>(n, d, s); cudaMemcpy(&q[0], d, 8, cudaMemcpyDeviceToHost);
+    k<7><<<1, 512>>>(n, d, s); cudaDeviceSynchronize(); k<7><<<1, 512>>>(n, d, s); cudaMemcpy(&q[1], d, 8, cudaMemcpyDeviceToHost);
+    k<8><<<1, 512>>>(n, d, s); cudaDeviceSynchronize(); k<8><<<1, 512>>>(n, d, s); cudaMemcpy(&q[2], d, 8, cudaMemcpyDeviceToHost);
+    printf("n=%2d: register-blocked CUDA-core 1x2 %llu | 2x2 %llu | 1x1 %llu cycles\n", n, q[0], q[1], q[2]);
     printf("n=%2d: DMMA loop %llu | 2 chains unrolled %llu | CUDA-core %llu | 1 chain %llu | 4 chains %llu | 8 chains %llu cycles  [%s]\n",
            n, h[0], h[1], h[2], g[2], g[0], g[1], cudaGetErrorString(cudaGetLastError()));
   }
