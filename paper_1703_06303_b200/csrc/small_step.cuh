@@ -423,20 +423,25 @@ WLR_NOINL void tri_inverse(const double* L, const double* dinv, int n, double* L
 // on exit th = eigenvalues in DESCENDING order and U (ld 32) the matching orthonormal
 // eigenvectors (columns).  b/2 disjoint rotations per round, b-1 rounds per sweep; stops
 // when every off-diagonal is at rounding level.  Deterministic.
-WLR_NOINL void jacobi_par(double* T, double* U, double* th, double* cs, int b) {
-  {   // warp 0 only (the caller branches); no block barrier inside
+// Threads [0, nt) of the CTA (nt = 32: warp 0 alone, beside the K^{-1} refinement on the other
+// warps; nt = kSST: the whole CTA, synchronised by barrier 0).  The arithmetic of every element
+// is the same for any nt (bitwise identical results).
+WLR_NOINL void jacobi_par(double* T, double* U, double* th, double* cs, int b, int nt, int* flag) {
+  {
     const int lane = threadIdx.x;
+    auto sync = [&]() { if (nt == 32) __syncwarp(); else __syncthreads(); };
     const int nb = (b + 1) & ~1;
     const int np = nb / 2;
     #pragma unroll 1
-    for (int i = lane; i < b; i += 32)
-      #pragma unroll 1
-      for (int j = 0; j < b; ++j) U[i * 32 + j] = (i == j) ? 1.0 : 0.0;
+    for (int idx = lane; idx < b * b; idx += nt) {
+      const int i = idx / b, j = idx - i * b;
+      U[i * 32 + j] = (i == j) ? 1.0 : 0.0;
+    }
     double dmax = 0.0;
     #pragma unroll 1
     for (int i = 0; i < b; ++i) dmax = fmax(dmax, fabs(T[i * 32 + i]));
     const double tabs = 2e-15 * dmax;
-    __syncwarp();
+    sync();
     #pragma unroll 1
     for (int sweep = 0; sweep < 30 && nb > 1; ++sweep) {
       #pragma unroll 1
@@ -460,10 +465,10 @@ WLR_NOINL void jacobi_par(double* T, double* U, double* th, double* cs, int b) {
           cs[4 * lane + 0] = c; cs[4 * lane + 1] = sn;
           cs[4 * lane + 2] = (double)p; cs[4 * lane + 3] = (double)(q < b && sn != 0.0 ? q : -1);
         }
-        __syncwarp();
+        sync();
         // rows:  T <- J^T T
         #pragma unroll 1
-        for (int idx = lane; idx < np * b; idx += 32) {
+        for (int idx = lane; idx < np * b; idx += nt) {
           const int kq = idx / b, j = idx - kq * b;
           const int q = (int)cs[4 * kq + 3];
           if (q >= 0) {
@@ -474,10 +479,10 @@ WLR_NOINL void jacobi_par(double* T, double* U, double* th, double* cs, int b) {
             T[q * 32 + j] = sn * tp + c * tq;
           }
         }
-        __syncwarp();
+        sync();
         // columns: T <- T J, U <- U J
         #pragma unroll 1
-        for (int idx = lane; idx < np * b; idx += 32) {
+        for (int idx = lane; idx < np * b; idx += nt) {
           const int kq = idx / b, i = idx - kq * b;
           const int q = (int)cs[4 * kq + 3];
           if (q >= 0) {
@@ -491,20 +496,31 @@ WLR_NOINL void jacobi_par(double* T, double* U, double* th, double* cs, int b) {
             U[i * 32 + q] = sn * up + c * uq;
           }
         }
-        __syncwarp();
+        sync();
       }
       // converged when every off-diagonal is at rounding level
       bool big = false;
       #pragma unroll 1
-      for (int idx = lane; idx < b * b; idx += 32) {
+      for (int idx = lane; idx < b * b; idx += nt) {
         const int i = idx / b, j = idx - i * b;
         if (i != j) {
           const double v = fabs(T[i * 32 + j]);
           big = big || (v > tabs && v > 1e-16 * sqrt(fabs(T[i * 32 + i] * T[j * 32 + j])));
         }
       }
-      if (!__any_sync(0xffffffffu, big)) break;
+      if (nt == 32) {
+        if (!__any_sync(0xffffffffu, big)) break;
+      } else {
+        if (lane == 0) *flag = 0;
+        __syncthreads();
+        if (__any_sync(0xffffffffu, big) && (lane & 31) == 0) *flag = 1;
+        __syncthreads();
+        const bool more = *flag != 0;
+        __syncthreads();
+        if (!more) break;
+      }
     }
+    if (lane >= 32) return;                   // (nt = kSST: warp 0 sorts; the caller's barrier follows)
     // sort descending (stable by index) and permute U's columns
     double wj = lane < b ? T[lane * 32 + lane] : 0.0;
     int rk = 0;
@@ -710,6 +726,7 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
   __shared__ double red[8 * kSSW];
   __shared__ int ok_s;
   __shared__ int kok_s;                        // K^{-1} refined during the first Rayleigh-Ritz
+  __shared__ int jflag_s;                      // (Jacobi convergence flag, whole-CTA form)
   const SSPlan& p = a.pl;
   SS s;
   s.CL = p.CL;
@@ -753,6 +770,8 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
   if constexpr (PART == 1) {
     int iY = 0, iZ = 1, iA = 2, iB = 3;        // roles of the four slice buffers
     int nprod = 0;
+    long long cyc_jac = 0, cyc_cheb = 0;       // (diagnostics, a.tdbg: cycles in the Jacobi / filter products)
+    int n_jac = 0;
     // ---------------------------------------------- A: Gram update, G'^{-1}, C', slices
     const bool xf_pre = a.mode && p.oXf >= 0;  // first S-product's operand loaded with the state
     if (a.mode) {
@@ -1034,15 +1053,20 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
           }
         }
         __syncthreads();
-        // warp 0: Jacobi; warps 1..: K^{-1} by Newton-Schulz from the previous one (first pass)
-        if (threadIdx.x < 32) {
-          jacobi_par(Tb, Ub, th, sm + so.cs, b);
-        } else if (outer == 0 && a.uniform && a.mode) {
+        const long long tj0 = a.tdbg ? clock64() : 0;
+        // warp 0: Jacobi; warps 1..: K^{-1} by Newton-Schulz from the previous one (first pass);
+        // otherwise the whole CTA runs the Jacobi
+        const bool ki_side = outer == 0 && a.uniform && a.mode;
+        const int jnt = ki_side || b <= 4 ? 32 : kSST;
+        if (threadIdx.x < jnt) {
+          jacobi_par(Tb, Ub, th, sm + so.cs, b, jnt, &jflag_s);
+        } else if (ki_side) {
           // warps 1..: K^{-1} by Newton-Schulz from the previous one
           const bool okk = ns_inverse(Gq, Xq, Rq, Pq, k, red + 32, 32, kSST - 32, 1);
           if (threadIdx.x == 32) kok_s = okk ? 1 : 0;
         }
         __syncthreads();
+        if (a.tdbg) { cyc_jac += clock64() - tj0; ++n_jac; }
         tmark(s, a);                           // (RR: Jacobi || K^{-1})
         for (int idx = threadIdx.x; idx < b * b; idx += kSST) {     // Qb = D (Li^T U) or D U
           const int i = idx / b, j = idx - i * b;
@@ -1119,7 +1143,9 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
         __syncthreads();
       }
       for (int j = 2; j <= d; ++j) {
+        const long long tc0 = a.tdbg ? clock64() : 0;
         s_apply<PW>(s, a, Cs, ldc, Ms, ldm, buf[i1], b, buf[iz], &nprod);
+        if (a.tdbg) cyc_cheb += clock64() - tc0;
         double* pn = s.sm + buf[i0];           // P2 = 2 (S P1 - c P1)/e - P0, in place of P0
         const double* pz = s.sm + buf[iz];
         const double* p1 = s.sm + buf[i1];
@@ -1290,6 +1316,10 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
     }
     for (int j = threadIdx.x; j < b; j += kSST) a.th_out[j] = th[j];
     if (threadIdx.x == 0) {
+      if (a.tdbg) {
+        a.tdbg[240] = (double)cyc_jac; a.tdbg[241] = (double)n_jac; a.tdbg[242] = (double)cyc_cheb;
+        a.tdbg[243] = (double)nprod; a.tdbg[244] = (double)outer;
+      }
       a.scal[6] = rmax / fabs(th[0]);
       a.scal[7] = (double)nprod;
       a.flags[3] = outer;

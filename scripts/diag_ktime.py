@@ -42,6 +42,10 @@ def run(ci, warm=8, H=None, Wd=None, flush=False):
                 print(f"   {name} exchange barrier releases (us from start): " +
                       " ".join(f"{(x - ts[0]) / 1e3:.1f}" for x in xb) +
                       " | marks: " + " ".join(f"{(x - ts[0]) / 1e3:.1f}" for x in ts))
+        if name == "K3a" or True:
+            pass
+        print(f"   K3a: Jacobi {kt[240] / 1.9e3:.1f} us in {kt[241]:.0f} calls, filter products {kt[242] / 1.9e3:.1f} us, "
+              f"S-products {kt[243]:.0f}, outer {kt[244]:.0f}  (cycles / 1.9 GHz)")
         if kt[167] > 0:
             print("   EXP NS#1 start %.1f end %.1f restore %.1f (us from K3a start)" % tuple((kt[i] - kt[1]) / 1e3 for i in (167, 168, 169)))
         t0a, t0b = kt[1], kt[65]
@@ -56,5 +60,7 @@ for c in (sys.argv[1:] or ["1", "2", "3", "4"]):
         continue
     if c == "4":
         run(4, H=120, Wd=160)
+    elif c in ("4f", "5f"):                 # full-size configs 4 / 5
+        run(int(c[0]))
     else:
         run(int(c))

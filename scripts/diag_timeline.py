@@ -16,7 +16,9 @@ NOFLUSH = "noflush" in sys.argv[2:]          # warm L2 (kernel durations without
 stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
 A = torch.from_numpy(synth.make_A(cfg)).cuda()
-h = w.wlr_init(A, cfg.k, cfg.r, None, w1=cfg.w_const or 1.0, stream=stream.cuda_stream)
+W1n = synth.make_W1(cfg)
+W1 = None if W1n is None else torch.from_numpy(W1n).cuda()
+h = w.wlr_init(A, cfg.k, cfg.r, W1, w1=cfg.w_const or 1.0, stream=stream.cuda_stream)
 w.wlr_row_path(h, True)
 w.wlr_incr_path(h, True)
 flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
