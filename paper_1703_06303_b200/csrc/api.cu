@@ -925,7 +925,7 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   // small-step (K3) cluster plan: depends on the dimensions only
   {
     SmallArgs pa{};
-    pa.k = (int)k; pa.nk = (int)nk; pa.t = (int)t; pa.b = b;
+    pa.k = (int)k; pa.nk = (int)nk; pa.t = (int)t; pa.b = b; pa.uniform = h->uniform ? 1 : 0;
     if (small_step_cluster_size(pa) <= 0)
       return fail(h, WLR_ECUDA, "no schedulable cluster configuration for the small step");
     h->spl = pa.pl;

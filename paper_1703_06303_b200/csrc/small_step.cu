@@ -35,7 +35,8 @@ static constexpr int64_t kSmemLimit = 227 * 1024 / 8;   // doubles per CTA
 
 // Lay out the shared memory of one CTA for cluster size CL.  Required regions first, then
 // optional ones greedily in priority order (C' slice, Newton-Schulz mats, M' slice, gathered
-// S-product operand, staged G/Gamma/Omega, C_in slice, CTA-0 tail staging); an optional
+// S-product operand -- for non-uniform W1: C' and M' slices, gathered operand, Newton-Schulz
+// mats --, staged G/Gamma/Omega, C_in slice, CTA-0 tail staging); an optional
 // region that does not fit gets offset -1 (the kernel then uses the global copy).
 static bool plan_once(SmallArgs& a, int CL, int ccx) {
   SSPlan& p = a.pl;
@@ -70,9 +71,15 @@ static bool plan_once(SmallArgs& a, int CL, int ccx) {
     return take(n);
   };
   p.oCs = opt((int64_t)k * (SL | 1));
-  p.oGsq = opt(4 * kk);
-  p.oMs = opt((int64_t)k * (SL | 1));
-  p.oXf = opt((int64_t)nk * b);
+  if (a.uniform) {       // (the K^{-1} refinement runs on the staged Newton-Schulz matrices every call)
+    p.oGsq = opt(4 * kk);
+    p.oMs = opt((int64_t)k * (SL | 1));
+    p.oXf = opt((int64_t)nk * b);
+  } else {               // (narrow gaps: many filter products per call, each gathers X)
+    p.oMs = opt((int64_t)k * (SL | 1));
+    p.oXf = opt((int64_t)nk * b);
+    p.oGsq = opt(4 * kk);
+  }
   p.oMat3 = opt(3 * kk + kt);
   p.oCin = opt((int64_t)k * (SL | 1));
   p.oTail = opt(p.flen + 3 * kt);
@@ -81,7 +88,13 @@ static bool plan_once(SmallArgs& a, int CL, int ccx) {
   return true;
 }
 
-bool small_step_plan(SmallArgs& a, int CL) { return plan_once(a, CL, 1) || plan_once(a, CL, 0); }
+// C'C'^T in the exchange bank (ccx) serves the uniform K^{-1}; for non-uniform W1 the bank space
+// goes to the staged Newton-Schulz matrices first (C'C'^T is then summed through global memory,
+// each CTA storing its share of the row solves' operand)
+bool small_step_plan(SmallArgs& a, int CL) {
+  if (!a.uniform) return plan_once(a, CL, 0) || plan_once(a, CL, 1);
+  return plan_once(a, CL, 1) || plan_once(a, CL, 0);
+}
 
 // Largest cluster (<= 16 CTAs, >= 24 columns per CTA where possible) whose plan fits and
 // which the device can co-schedule.

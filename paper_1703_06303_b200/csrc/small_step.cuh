@@ -963,7 +963,22 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
         tmark(s, a);                           // [4a] Gram partials
         xreduce(s, p, lg, Gx, p.ccx ? kc * k : 0, Gq);
         tmark(s, a);                           // [4b] exchange
-        if (kc) {
+        if (kc && !p.ccx && !a.uniform) {
+          // non-uniform W1: C'C'^T (the row solves' K = C'C'^T + diag(W1^2), next iteration) is only
+          // stored: every CTA sums its share of the entries over the cluster's global partials
+          // (fixed order), no CTA needs the whole matrix here
+          const int e0 = (int)((int64_t)kk * s.c / s.CL), e1 = (int)((int64_t)kk * (s.c + 1) / s.CL);
+          #pragma unroll 1
+          for (int idx = e0 + threadIdx.x; idx < e1; idx += kSST) {
+            const int i = idx / k, j = idx - i * k;
+            double v = 0.0;
+            for (int c = 0; c < s.CL; ++c)
+              v += 0.5 * (__ldcg(a.xchg + (int64_t)c * p.flen + idx) + __ldcg(a.xchg + (int64_t)c * p.flen + j * k + i));
+            if (a.dtype) reinterpret_cast<double*>(a.Kop)[idx] = v;
+            else reinterpret_cast<float*>(a.Kop)[idx] = (float)v;
+            if (a.Sop) a.Sop[i * ((k + 7) & ~7) + j] = (float)v;
+          }
+        } else if (kc) {
           #pragma unroll 1
           for (int idx = threadIdx.x; idx < kk; idx += kSST) {
             const int i = idx / k, j = idx - i * k;
