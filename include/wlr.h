@@ -67,8 +67,8 @@ typedef struct {
                              Error_p/||X_p||_F < eps.  0 = run the requested count.      */
   double eig_tol;         /* eigensolver relative residual target, relative to lambda_1
                              (0 -> 1e-12 for WLR_F64, 1e-7 for WLR_F32; R17)   */
-  int32_t eig_block;      /* eigensolver block width b >= r-k (0 -> r-k+2 when r-k <= 4,
-                             else r-k+6; capped at min(32, n-k))                         */
+  int32_t eig_block;      /* eigensolver block width b >= r-k (0 -> r-k+2; capped at
+                             min(32, n-k))                                               */
   int32_t eig_max_outer;  /* eigensolver restart budget per (C,D) step (0 -> 60; init x4)*/
   int64_t m_global;       /* total rows over all ranks (0 -> m_local)                    */
   int64_t row_offset;     /* first global row owned by this rank                          */

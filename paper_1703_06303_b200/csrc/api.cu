@@ -915,9 +915,10 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
     // (2/4/8-CTA clusters pre-reducing the partials were measured no faster: profiles/r01_v10_itc_cs.log)
   }
   // eigen block width b
-  // warm block: 2 spare Ritz vectors for r-k <= 4 (one product per iteration at steady state,
-  // profiles/r01_v7_eigblock.log), 6 otherwise (narrow gaps at configs 4-5)
-  int b = o.eig_block > 0 ? o.eig_block : (int)(t + (t <= 4 ? 2 : 6));
+  // warm block: 2 spare Ritz vectors (one product per iteration at steady state at config 3,
+  // profiles/r01_v7_eigblock.log; at config 4's narrow gaps a wider block saves few filter products
+  // but makes each one dearer: b = 6..11 -> 1243..1400 us per iteration, profiles/r02_eigblock.log)
+  int b = o.eig_block > 0 ? o.eig_block : (int)(t + 2);
   b = (int)std::min<int64_t>(std::max<int64_t>(b, t), nk);
   if (b > 32) b = 32;
   if (b < t) return fail(h, WLR_EINVAL, "r-k > 32 is not supported by this build");
