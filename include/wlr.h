@@ -43,7 +43,8 @@ typedef struct wlr_ctx* wlr_handle;
 typedef enum {
   WLR_OK = 0,
   WLR_EINVAL = 1,      /* bad argument: k<1, k>=n, r<=k (Theorem 2 needs r>k),
-                          r>min(m,n), W1<=0, ld < cols, bad pointer       */
+                          r>min(m,n), W1<=0, ld < cols, bad pointer;
+                          build limits: n-k > 1024, r-k > 32                            */
   WLR_ERANK = 2,       /* X1 numerically rank deficient: Cholesky of X1^T X1 failed
                           (PAPER.md:133 assumes rank(X1)=k)                  */
   WLR_EEIG = 3,        /* top-(r-k) eigensolver exceeded its iteration budget            */

@@ -927,6 +927,7 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   {
     SmallArgs pa{};
     pa.k = (int)k; pa.nk = (int)nk; pa.t = (int)t; pa.b = b; pa.uniform = h->uniform ? 1 : 0;
+    if (nk > 1024) return fail(h, WLR_EINVAL, "n - k > 1024 is not supported by this build (small step: one cluster of <= 16 CTAs x 64 columns)");
     if (small_step_cluster_size(pa) <= 0)
       return fail(h, WLR_ECUDA, "no schedulable cluster configuration for the small step");
     h->spl = pa.pl;
@@ -1679,6 +1680,13 @@ extern "C" wlr_status wlr_debug_state(wlr_handle h, const char* name, double* ou
     h->rp_n = 0;
     if ((s = reset_graphs(h)) != WLR_OK) return s;
     if (count) *count = 0;
+    return WLR_OK;
+  }
+  else if (nm == "prop") {   // Gram-propagation path: [active, prop1 CTAs, rows per CTA, G_A Y in prop1]
+    const double v[4] = {h->prop ? 1.0 : 0.0, (double)h->prop_nb,
+                         h->prop ? (double)prop1_rb((int)h->n, h->nsm) : 0.0, h->prop && gay_fits(h) ? 1.0 : 0.0};
+    for (int i = 0; i < 4 && out && i < cap; ++i) out[i] = v[i];
+    if (count) *count = 4;
     return WLR_OK;
   }
   else if (nm == "rptime") {

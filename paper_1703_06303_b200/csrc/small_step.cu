@@ -100,6 +100,7 @@ bool small_step_plan(SmallArgs& a, int CL) {
 // which the device can co-schedule.
 int small_step_cluster_size(SmallArgs& a) {
   const int lo = (int)std::max<int64_t>(1, ceil_div(a.nk, 64));
+  if (lo > 16) return 0;                       // (n - k > 16 x 64: no cluster holds the slices)
   int want = (int)std::max<int64_t>(lo, std::min<int64_t>(16, ceil_div(a.nk, 24)));
   if (const char* e = std::getenv("WLR_K3_CL")) want = std::max(lo, std::min(16, std::atoi(e)));   // (A/B)
   for (int CL = want; CL >= lo; --CL) {
