@@ -773,7 +773,10 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
     long long cyc_jac = 0, cyc_cheb = 0;       // (diagnostics, a.tdbg: cycles in the Jacobi / filter products)
     int n_jac = 0;
     // ---------------------------------------------- A: Gram update, G'^{-1}, C', slices
-    const bool xf_pre = a.mode && p.oXf >= 0;  // first S-product's operand loaded with the state
+    // G_A Y of the warm block precomputed by the propagation kernel: the first S-product needs no
+    // gathered operand at all; otherwise that operand (the whole Y) is loaded with the state
+    const bool use_gay = a.mode && a.GAY != nullptr;
+    const bool xf_pre = a.mode && p.oXf >= 0 && !use_gay;
     if (a.mode) {
       // rounds of 4 M' elements, 2 G' elements and 2 each of Y, V_p, G^{-1}_p per thread: every
       // load of a round is issued before its stores (the loops one after the other waited one
@@ -942,8 +945,8 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
     bool ortho = !a.cold;                      // Y expected orthonormal (warm Ritz block)
     while (true) {
       // ---- Rayleigh-Ritz on span(Y):  Z = S Y;  Gyy = Y^T Y, Gyz = Y^T Z (generalised RR)
-      s_apply<PW>(s, a, Cs, ldc, Ms, ldm, buf[iY], b, buf[iZ], &nprod, xf_pre && outer == 0,
-                  xf_pre && outer == 0 ? a.GAY : nullptr);
+      s_apply<PW>(s, a, Cs, ldc, Ms, ldm, buf[iY], b, buf[iZ], &nprod, (xf_pre || use_gay) && outer == 0,
+                  use_gay && outer == 0 ? a.GAY : nullptr);
       tmark(s, a);                             // product
       {
         const double* Y = s.sm + buf[iY];
