@@ -74,7 +74,8 @@ typedef struct {
   int64_t m_global;       /* total rows over all ranks (0 -> m_local)                    */
   int64_t row_offset;     /* first global row owned by this rank                          */
   int32_t nranks, rank;   /* row sharding over ranks (1, 0 for single GPU)                */
-  const void* nccl_id;    /* 128-byte ncclUniqueId shared by all ranks (NULL if nranks==1)*/
+  const void* nccl_id;    /* 128-byte ncclUniqueId shared by all ranks (NULL if nranks==1;
+                             with nranks==1 a one-rank communicator: tests the NCCL path)  */
   void* stream;           /* cudaStream_t for all work; NULL = a BLOCKING stream owned by
                              the handle (ordered after the legacy default stream).  With a
                              caller stream, the caller orders device inputs before wlr_init. */

@@ -1089,7 +1089,7 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   if (o.vgroup) {
     h->vg = reinterpret_cast<wlr_vgroup_s*>(o.vgroup);
     if (h->vg->G != o.nranks) return fail(h, WLR_EINVAL, "opts.nranks must equal the virtual group's size");
-  } else if (o.nranks > 1) {
+  } else if (o.nranks > 1 || o.nccl_id) {   // (nranks = 1 with an id: a one-rank communicator, test hook)
     if (!o.nccl_id) return fail(h, WLR_EINVAL, "nranks > 1 needs opts.nccl_id");
     std::string e;
     if (!g_nccl.load(e)) return fail(h, WLR_ENCCL, e);
