@@ -585,9 +585,11 @@ WLR_DEVI void s_product_impl(double* smb, int rs, int nl, int SL, int k, int nk,
   const int cw = (w + p.JS - 1) / p.JS;
   const int j0 = js * cw;
   const int wj = min(w - j0, cw);                 // columns of this warp (may be <= 0)
-  const int KT = s.nk + s.k;
-  const int kc = (KT + p.KS - 1) / p.KS;
-  const int l0 = ks * kc, l1 = min(KT, l0 + kc);
+  // contraction index l over [G_A rows (n-k) | M' rows (k)]; with G_A X given only the M' rows
+  // remain, spread over all the k-split warps
+  const int KT = s.nk + s.k, LB = gay ? s.nk : 0;
+  const int kc = (KT - LB + p.KS - 1) / p.KS;
+  const int l0 = LB + ks * kc, l1 = min(KT, l0 + kc);
   const bool has0 = lane < s.nl, has1 = lane + 32 < s.nl;
   double acc0[PW], acc1[PW];
 #pragma unroll
@@ -666,7 +668,7 @@ WLR_DEVI void s_product_impl(double* smb, int rs, int nl, int SL, int k, int nk,
     }
   }
   __syncthreads();
-  const int nks = (KT + kc - 1) / kc;             // chunks that exist (ks >= nks are empty)
+  const int nks = (KT - LB + kc - 1) / kc;        // chunks that exist (ks >= nks are empty)
   #pragma unroll 1
   for (int idx = threadIdx.x; idx < s.nl * w; idx += kSST) {
     const int i = idx / w, j = idx - i * w;
