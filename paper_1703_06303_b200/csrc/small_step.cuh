@@ -1080,10 +1080,12 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
         const int jnt = ki_side || b <= 4 ? 32 : kSST;
         if (threadIdx.x < jnt) {
           jacobi_par(Tb, Ub, th, sm + so.cs, b, jnt, &jflag_s);
+          if (a.tdbg && threadIdx.x == 0 && s.c == 0) a.tdbg[245] = (double)(clock64() - tj0);
         } else if (ki_side) {
           // warps 1..: K^{-1} by Newton-Schulz from the previous one
           const bool okk = ns_inverse(Gq, Xq, Rq, Pq, k, red + 32, 32, kSST - 32, 1);
           if (threadIdx.x == 32) kok_s = okk ? 1 : 0;
+          if (a.tdbg && threadIdx.x == 32 && s.c == 0) a.tdbg[246] = (double)(clock64() - tj0);
         }
         __syncthreads();
         if (a.tdbg) { cyc_jac += clock64() - tj0; ++n_jac; }

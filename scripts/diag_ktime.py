@@ -45,7 +45,8 @@ def run(ci, warm=8, H=None, Wd=None, flush=False):
         if name == "K3a" or True:
             pass
         print(f"   K3a: Jacobi {kt[240] / 1.9e3:.1f} us in {kt[241]:.0f} calls, filter products {kt[242] / 1.9e3:.1f} us, "
-              f"S-products {kt[243]:.0f}, outer {kt[244]:.0f}  (cycles / 1.9 GHz)")
+              f"S-products {kt[243]:.0f}, outer {kt[244]:.0f}  (cycles / 1.9 GHz); Jacobi warp alone {kt[245] / 1.9e3:.1f} us, "
+              f"K^-1 warps {kt[246] / 1.9e3:.1f} us (last call)")
         if kt[167] > 0:
             print("   EXP NS#1 start %.1f end %.1f restore %.1f (us from K3a start)" % tuple((kt[i] - kt[1]) / 1e3 for i in (167, 168, 169)))
         t0a, t0b = kt[1], kt[65]
