@@ -233,10 +233,54 @@ WLR_DEVI void tc_tile(int m, int n, int kk, const double* A, int ars, int aqs, c
 // B(q, c) = B[q*bqs + c*bcs], C(r, c) = C[r*ldc + c]: one 8 x 8 output tile per warp step, on
 // the warps of the threads [t0, t0 + nt) (whole warps; no barrier inside).  C must not alias
 // A or B.
+// Two horizontally adjacent 8 x 8 tiles (c0, c0 + 8) sharing the A fragments: one accumulator
+// chain each (used when the tiles outnumber the warps, so that no warp runs two tiles in a row)
+WLR_DEVI void tc_tile_pair(int m, int n, int kk, const double* A, int ars, int aqs, const double* B, int bqs,
+                           int bcs, int r0, int c0, double (&v)[4]) {
+  const int lane = threadIdx.x & 31, ra = lane >> 2, qa = lane & 3;
+  const int ar = r0 + ra, bc = c0 + ra;
+  const bool aok = ar < m, bok0 = bc < n, bok1 = bc + 8 < n;
+  const double* pa = A + (int64_t)ar * ars + (int64_t)qa * aqs;
+  const double* pb = B + (int64_t)bc * bcs + (int64_t)qa * bqs;
+  const int64_t sa = 4LL * aqs, sb = 4LL * bqs, b8 = 8LL * bcs;
+  double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
+  #pragma unroll 2
+  for (int q = 0; q < kk; q += 4) {
+    const bool kin = q + qa < kk;
+    const double a0 = aok && kin ? pa[0] : 0.0;
+    const double b0 = bok0 && kin ? pb[0] : 0.0, b1 = bok1 && kin ? pb[b8] : 0.0;
+    dmma884(d0, d1, a0, b0);
+    dmma884(e0, e1, a0, b1);
+    pa += sa; pb += sb;
+  }
+  v[0] = d0; v[1] = d1; v[2] = e0; v[3] = e1;
+}
+
 WLR_NOINL void gemm_tc(int m, int n, int kk, const double* A, int ars, int aqs, const double* B, int bqs, int bcs,
                        double* C, int ldc, double alpha, bool addI, int t0 = 0, int nt = kSST) {
   const int lane = threadIdx.x & 31, w = (threadIdx.x - t0) >> 5, nw = nt >> 5;
   const int tn = (n + 7) >> 3, tt = ((m + 7) >> 3) * tn;
+  if (tt > nw) {   // more tiles than warps: pairs of column tiles (one round instead of two)
+    const int tn2 = (tn + 1) >> 1, tt2 = ((m + 7) >> 3) * tn2;
+    #pragma unroll 1
+    for (int tile = w; tile < tt2; tile += nw) {
+      const int r0 = (tile / tn2) << 3, c0 = (tile - (tile / tn2) * tn2) << 4;
+      double v[4];
+      tc_tile_pair(m, n, kk, A, ars, aqs, B, bqs, bcs, r0, c0, v);
+      const int cr = r0 + (lane >> 2);
+      if (cr < m) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int cc = c0 + 8 * h + 2 * (lane & 3);
+          double v0 = v[2 * h] * alpha, v1 = v[2 * h + 1] * alpha;
+          if (addI) { if (cr == cc) v0 += 1.0; if (cr == cc + 1) v1 += 1.0; }
+          if (cc < n) C[(int64_t)cr * ldc + cc] = v0;
+          if (cc + 1 < n) C[(int64_t)cr * ldc + cc + 1] = v1;
+        }
+      }
+    }
+    return;
+  }
   #pragma unroll 1
   for (int tile = w; tile < tt; tile += nw) {
     const int r0 = (tile / tn) << 3, c0 = (tile - (tile / tn) * tn) << 3;
