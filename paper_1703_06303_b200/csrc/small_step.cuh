@@ -467,6 +467,104 @@ WLR_NOINL void tri_inverse(const double* L, const double* dinv, int n, double* L
 // on exit th = eigenvalues in DESCENDING order and U (ld 32) the matching orthonormal
 // eigenvectors (columns).  b/2 disjoint rotations per round, b-1 rounds per sweep; stops
 // when every off-diagonal is at rounding level.  Deterministic.
+// One-warp form (warp 0, beside the K^{-1} refinement): the same round-robin rotations, each round
+// applied as ONE update T' = J^T T J, U' = U J from the previous buffers into the other pair
+// (T, U) <-> (T2, U2) -- two warp barriers per round instead of three.  pi / pc / ps: for every
+// index x its partner in the round and the coefficients of new_row_x = pc x + ps partner.
+WLR_NOINL void jacobi_warp(double* T, double* U, double* T2, double* U2, double* th, double* scr, int b) {
+  const int lane = threadIdx.x & 31;
+  const int nb = (b + 1) & ~1, np = nb / 2;
+  double* const Uo = U;                        // (the caller's U: the sorted eigenvectors go here)
+  double* pcoef = scr;                         // [32] self coefficient, [32..64) partner coefficient
+  int* pidx = reinterpret_cast<int*>(scr + 64);   // [32] partner index (-1: no rotation)
+  #pragma unroll 1
+  for (int idx = lane; idx < b * b; idx += 32) {
+    const int i = idx / b, j = idx - i * b;
+    U[i * 32 + j] = (i == j) ? 1.0 : 0.0;
+  }
+  double dmax = 0.0;
+  #pragma unroll 1
+  for (int i = 0; i < b; ++i) dmax = fmax(dmax, fabs(T[i * 32 + i]));
+  const double tabs = 2e-15 * dmax;
+  __syncwarp();
+  #pragma unroll 1
+  for (int sweep = 0; sweep < 30 && nb > 1; ++sweep) {
+    #pragma unroll 1
+    for (int rnd = 0; rnd < nb - 1; ++rnd) {
+      if (lane < np) {
+        int p, q;
+        if (lane == 0) { p = rnd; q = nb - 1; }
+        else { p = (rnd + lane) % (nb - 1); q = (rnd - lane + nb - 1) % (nb - 1); }
+        if (p > q) { const int x = p; p = q; q = x; }
+        double c = 1.0, sn = 0.0;
+        if (q < b) {
+          const double apq = T[p * 32 + q], app = T[p * 32 + p], aqq = T[q * 32 + q];
+          if (fabs(apq) > tabs && fabs(apq) > 1e-16 * sqrt(fabs(app * aqq))) {
+            const double tau = (aqq - app) / (2.0 * apq);
+            const double tt = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+            c = rsqrt(1.0 + tt * tt);
+            sn = tt * c;
+          }
+        }
+        const bool rot = q < b && sn != 0.0;
+        pcoef[p] = rot ? c : 1.0; pcoef[32 + p] = rot ? -sn : 0.0; pidx[p] = rot ? q : -1;
+        if (q < b) { pcoef[q] = rot ? c : 1.0; pcoef[32 + q] = rot ? sn : 0.0; pidx[q] = rot ? p : -1; }
+      }
+      __syncwarp();
+      #pragma unroll 1
+      for (int idx = lane; idx < b * b; idx += 32) {
+        const int i = idx / b, j = idx - i * b;
+        const int pi = pidx[i], pj = pidx[j];
+        const double ci = pcoef[i], si = pcoef[32 + i], cj = pcoef[j], sj = pcoef[32 + j];
+        // rows first (new row i = ci T_i + si T_pi), then columns (new col j = cj . + sj .pj)
+        const double rij = ci * T[i * 32 + j] + (pi >= 0 ? si * T[pi * 32 + j] : 0.0);
+        double v = cj * rij;
+        if (pj >= 0) v += sj * (ci * T[i * 32 + pj] + (pi >= 0 ? si * T[pi * 32 + pj] : 0.0));
+        T2[i * 32 + j] = v;
+        U2[i * 32 + j] = cj * U[i * 32 + j] + (pj >= 0 ? sj * U[i * 32 + pj] : 0.0);
+      }
+      __syncwarp();
+      { double* x = T; T = T2; T2 = x; x = U; U = U2; U2 = x; }
+    }
+    bool big = false;
+    #pragma unroll 1
+    for (int idx = lane; idx < b * b; idx += 32) {
+      const int i = idx / b, j = idx - i * b;
+      if (i != j) {
+        const double v = fabs(T[i * 32 + j]);
+        big = big || (v > tabs && v > 1e-16 * sqrt(fabs(T[i * 32 + i] * T[j * 32 + j])));
+      }
+    }
+    if (!__any_sync(0xffffffffu, big)) break;
+  }
+  // sort descending (stable by index)
+  double wj = lane < b ? T[lane * 32 + lane] : 0.0;
+  int rk = 0;
+  #pragma unroll 1
+  for (int i = 0; i < b; ++i) {
+    const double wi = T[i * 32 + i];
+    if (wi > wj || (wi == wj && i < lane)) ++rk;
+  }
+  __syncwarp();
+  if (lane < b) th[rk] = wj;
+  // U holds the current eigenvectors: permuted into the caller's buffer (through the other one
+  // when that is U itself)
+  const double* src = U;
+  if (U == Uo) {
+    #pragma unroll 1
+    for (int idx = lane; idx < b * b; idx += 32) {
+      const int i = idx / b, j = idx - i * b;
+      U2[i * 32 + j] = U[i * 32 + j];
+    }
+    __syncwarp();
+    src = U2;
+  }
+  if (lane < b)
+    #pragma unroll 1
+    for (int i = 0; i < b; ++i) Uo[i * 32 + rk] = src[i * 32 + lane];
+  __syncwarp();
+}
+
 // Threads [0, nt) of the CTA (nt = 32: warp 0 alone, beside the K^{-1} refinement on the other
 // warps; nt = kSST: the whole CTA, synchronised by barrier 0).  The arithmetic of every element
 // is the same for any nt (bitwise identical results).
@@ -1123,7 +1221,8 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
         const bool ki_side = outer == 0 && a.uniform && a.mode;
         const int jnt = ki_side || b <= 4 ? 32 : kSST;
         if (threadIdx.x < jnt) {
-          jacobi_par(Tb, Ub, th, sm + so.cs, b, jnt, &jflag_s);
+          if (jnt == 32) jacobi_warp(Tb, Ub, Wb, sm + so.Qb, th, sm + so.Lb, b);   // (Wb, Qb, Lb free here)
+          else jacobi_par(Tb, Ub, th, sm + so.cs, b, jnt, &jflag_s);
           if (a.tdbg && threadIdx.x == 0 && s.c == 0) a.tdbg[245] = (double)(clock64() - tj0);
         } else if (ki_side) {
           // warps 1..: K^{-1} by Newton-Schulz from the previous one
