@@ -500,8 +500,11 @@ WLR_NOINL void jacobi_warp(double* T, double* U, double* T2, double* U2, double*
         if (q < b) {
           const double apq = T[p * 32 + q], app = T[p * 32 + p], aqq = T[q * 32 + q];
           if (fabs(apq) > tabs && fabs(apq) > 1e-16 * sqrt(fabs(app * aqq))) {
-            const double tau = (aqq - app) / (2.0 * apq);
-            const double tt = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+            // the angle's tangent in fp32 (short-latency MUFU ops; |tau| < 1e15 by the thresholds):
+            // c, s from the same fp64 t keep the rotation orthogonal to fp64 rounding, only the
+            // angle is fp32-accurate (apq drops to ~1e-7 of itself; the next sweep removes the rest)
+            const float tauf = (float)((aqq - app) / (2.0 * apq));
+            const double tt = (double)(copysignf(1.0f, tauf) / (fabsf(tauf) + sqrtf(fmaf(tauf, tauf, 1.0f))));
             c = rsqrt(1.0 + tt * tt);
             sn = tt * c;
           }
