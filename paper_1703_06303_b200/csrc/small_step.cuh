@@ -1264,13 +1264,18 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
         const double* Y = s.sm + buf[iY];
         const double* Z = s.sm + buf[iZ];
         double* part = xpart(s, p);
-        for (int j = threadIdx.x; j < t; j += kSST) {
-          double v = 0.0;
-          for (int r = 0; r < s.nl; ++r) {
-            const double d = Z[r * b + j] - th[j] * Y[r * b + j];
-            v = fma(d, d, v);
+        {   // one warp per wanted pair (the last warps: the C'V' tiles below start on the first ones)
+          const int wq = kSSW - 1 - (threadIdx.x >> 5), ln = threadIdx.x & 31;
+          #pragma unroll 1
+          for (int j = wq; j < t; j += kSSW) {
+            double v = 0.0;
+            for (int r = ln; r < s.nl; r += 32) {
+              const double d = Z[r * b + j] - th[j] * Y[r * b + j];
+              v = fma(d, d, v);
+            }
+            v = warp_sum(v);
+            if (ln == 0) part[j] = v;
           }
-          part[j] = v;
         }
         // C'V' (k x t) partials ride along: valid at every exit of this loop (it only leaves
         // right after this exchange), so the operands need no exchange of their own
