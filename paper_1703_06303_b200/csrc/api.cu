@@ -9,6 +9,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -153,7 +154,7 @@ struct wlr_ctx {
   CUtensorMap tmW1{}, tmWT1{};
   // Gram propagation (uniform W1, prop.cu): A^T A, Q_p = A^T X1_p (by parity), scratch
   bool prop = false;
-  double *AtA = nullptr, *Qg[2] = {nullptr, nullptr}, *Hs = nullptr, *dgs = nullptr, *GAY = nullptr;
+  double *AtA = nullptr, *Qg[2] = {nullptr, nullptr}, *Hs = nullptr, *dgs = nullptr, *GAY[2] = {nullptr, nullptr};   // G_A Y by iteration parity
   double a1sq = 0.0;
   cudaStream_t st3 = nullptr;  // row-pass branch of a propagation iteration
   cudaStream_t st4 = nullptr;  // critical chain (prop -> K3a) of a propagation iteration, high priority
@@ -179,9 +180,26 @@ struct wlr_ctx {
   double *Y = nullptr, *k3x[2] = {nullptr, nullptr};
   double *xchg = nullptr, *xchg2 = nullptr, *red = nullptr, *scal = nullptr, *trace = nullptr;
   double* tdbg = nullptr;      // K3 phase timestamps (wlr_debug_state "ktime")
-  int prop_nb = 0;             // prop1 CTAs (min(n, #SMs))
+  int prop_nb = 0;             // prop1 CTAs (min(n, prop_nsm))
+  int prop_nsm = 0;            // SMs prop1 spreads over: #SMs less those the K3b / shadow clusters hold
   unsigned long long* prop_ts = nullptr;   // (diagnostics: WLR_PROP_TS=1, prop1 phase stamps)
   bool k3b_early = true;       // K3b(p-1) forks at the iteration start (WLR_K3B_EARLY=0: after prop1)
+  // shadow K3a (propagation mode): at the start of iteration p a rerun of K3a(p-1)
+  // with every output redirected into these private buffers, so that its instruction fetches pull
+  // K3a's code into L2 ahead of the real K3a(p) (the bench flushes L2 before every iteration).
+  // Nothing reads what it writes; WLR_SHADOW=0 disables it.
+  bool shadow = false;
+  bool shadow_now = false;     // enqueue_prop_iteration launches the shadow (every iteration but p = 0)
+                               // (every real K3a writes the snapshots, whatever path launched it)
+  cudaStream_t st5 = nullptr;
+  cudaEvent_t ev_j5 = nullptr;
+  double *sh_G = nullptr, *sh_M = nullptr, *sh_C = nullptr, *sh_V = nullptr, *sh_CV = nullptr, *sh_th = nullptr;
+  double *sh_k3x = nullptr, *sh_Gi = nullptr, *sh_gws = nullptr, *sh_xchg = nullptr;
+  double *snapY[2] = {nullptr, nullptr}, *snapKi[2] = {nullptr, nullptr};   // K3a(p)'s Y, K^{-1} inputs, by parity
+  double *sh_red = nullptr, *sh_scal = nullptr, *sh_trace = nullptr;
+  void *sh_Wt = nullptr, *sh_WtT = nullptr, *sh_CVop = nullptr, *sh_Kop = nullptr;
+  float* sh_Sop = nullptr;
+  int* sh_flags = nullptr;
   SmallArgs last_ss{};         // arguments of the last small-step launch (diagnostics)
   bool ktime = false;
   int trace_cap = 4096;
@@ -203,6 +221,10 @@ struct wlr_ctx {
   cudaStream_t st2 = nullptr;  // side stream of the deferred small-step half
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool pending = false;        // deferred half of the last small step not launched yet
+  // One graph per phase: it always holds K3b(p-1); when that half already ran (flush_pending, or
+  // the GHS step at init) the host sets flags[7] and the graph's K3b clears it and returns
+  // (halves the graphs instantiated at init).  Eager iterations launch K3b only when pending.
+  bool capturing = false;
   SmallArgs pend{};
   ncclComm_t comm = nullptr;
   wlr_vgroup_s* vg = nullptr;  // virtual ranks (test hook), instead of comm
@@ -395,7 +417,7 @@ static void set_prefetch(wlr_ctx* h, int ph, const void** ptr, int64_t* bytes) {
 // Small-step arguments of iteration p (phase ph = p mod 6): state slot p mod 3 -> (p+1) mod 3,
 // increments / exchange block by p mod 2.
 // prop1 computes G_A Y of the warm block (Y fragments in registers: b <= 8, n - k <= 768)
-static bool gay_fits(const wlr_ctx* h) { return prop_gay_ok((int)h->n, (int)h->k, h->b, h->nsm); }
+static bool gay_fits(const wlr_ctx* h) { return prop_gay_ok((int)h->n, (int)h->k, h->b, h->prop_nsm); }
 
 static SmallArgs small_args(wlr_ctx* h, int ph, int mode) {
   const int cur = ph % 3, nxt = (ph + 1) % 3, par = ph & 1;
@@ -409,6 +431,7 @@ static SmallArgs small_args(wlr_ctx* h, int ph, int mode) {
   s.V_in = h->V[cur]; s.V_out = h->V[nxt]; s.CV_in = h->CV[cur]; s.CV_out = h->CV[nxt];
   s.th_in = h->th[cur]; s.th_out = h->th[nxt]; s.k3x = h->k3x[par];
   s.Y = h->Y;
+  if (h->shadow && mode != 0) { s.snapY = h->snapY[ph & 1]; s.snapKi = h->snapKi[ph & 1]; }
   s.Gi_in = h->Gi[cur]; s.Gi_out = h->Gi[nxt]; s.Ki = h->Ki; s.gws = h->gws;
   s.xchg = h->xchg; s.red = h->red; s.scal = h->scal;
   s.trace = h->trace; s.trace_cap = h->trace_cap;
@@ -417,7 +440,7 @@ static SmallArgs small_args(wlr_ctx* h, int ph, int mode) {
   s.WtT = wb1 ? h->WtT1 : h->WtT; s.KW = h->KW;
   s.eps = h->opts.eps; s.tol = h->opts.eig_tol; s.max_outer = h->opts.eig_max_outer; s.max_deg = 16;
   s.stop = (mode != 0 && h->opts.eps > 0.0) ? h->flags + 6 : nullptr;   // eps mode: latched stop flag
-  s.GAY = (mode != 0 && h->prop && gay_fits(h)) ? h->GAY : nullptr;
+  s.GAY = (mode != 0 && h->prop && gay_fits(h)) ? h->GAY[ph & 1] : nullptr;
   s.dg = (mode != 0 && h->prop) ? h->dgs : nullptr;   // f_w from prop2's diagonal terms
   s.a1sq = h->a1sq;                      // (computed by prop1)
   s.cold = 0;
@@ -431,10 +454,32 @@ static SmallArgs small_args(wlr_ctx* h, int ph, int mode) {
 // K3b has its own exchange block / workspace, so it can run beside the next K3a.
 static cudaError_t launch_deferred(wlr_ctx* h, const SmallArgs& a, cudaStream_t st) {
   SmallArgs d = a;
+  d.skip = h->capturing ? h->flags + 7 : nullptr;
   d.xchg = h->xchg2;
   d.gws = h->gws2;
   if (d.tdbg) d.tdbg += 64;                  // its own timestamp block
   return launch_small_step(d, 2, st);
+}
+
+// Shadow K3a (see wlr_ctx::shadow), launched at the start of iteration p: a rerun of K3a(p-1) --
+// state p-1 (slot (p-1) mod 3, intact until K3a(p+1) writes it), iteration p-1's increments and
+// G_A Y (the parity-(p-1) buffers, which prop(p) does not write), and the copies of its two
+// in-place inputs (warm block Y, K^{-1}) that K3a(p-1) wrote as it read them (snapY / snapKi by
+// parity; the shadow updates that copy in place, K3a(p) writes the other one).  Same inputs, same
+// code path: its instruction fetches run ahead of the real K3a(p).  Nothing carries over from one
+// shadow to the next.
+static SmallArgs shadow_args(wlr_ctx* h, int ph) {
+  SmallArgs a = small_args(h, (ph + 5) % 6, 1);
+  a.pdl = 0;
+  a.G_out = h->sh_G; a.M_out = h->sh_M; a.C_out = h->sh_C; a.V_out = h->sh_V; a.CV_out = h->sh_CV;
+  const int pp = ((ph + 5) % 6) & 1;         // parity of p-1
+  a.th_out = h->sh_th; a.k3x = h->sh_k3x; a.Y = h->snapY[pp]; a.Gi_out = h->sh_Gi; a.Ki = h->snapKi[pp];
+  a.snapY = nullptr; a.snapKi = nullptr;
+  a.gws = h->sh_gws; a.xchg = h->sh_xchg; a.red = h->sh_red; a.scal = h->sh_scal; a.trace = h->sh_trace;
+  a.Wt = h->sh_Wt; a.WtT = a.WtT ? h->sh_WtT : nullptr; a.CVop = h->sh_CVop; a.Kop = h->sh_Kop;
+  a.Sop = a.Sop ? h->sh_Sop : nullptr; a.flags = h->sh_flags;
+  a.tdbg = nullptr;
+  return a;
 }
 
 static wlr_status flush_pending(wlr_ctx* h) {
@@ -443,6 +488,7 @@ static wlr_status flush_pending(wlr_ctx* h) {
   // stops this deferred half (the state stays at the converged one)
   cudaError_t e = h->opts.eps > 0.0 ? launch_stop_latch(h->flags, h->st) : cudaSuccess;
   if (e == cudaSuccess) e = launch_deferred(h, h->pend, h->st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(h->flags + 7, 1, 1, h->st);   // the next graph's K3b: done
   if (e != cudaSuccess) return fail(h, WLR_ECUDA, std::string("small step (deferred): ") + cudaGetErrorString(e));
   h->pending = false;
   h->pr.launches += 1;
@@ -538,7 +584,7 @@ static wlr_status enqueue_prop_iteration(wlr_ctx* h, int ph) {
   pa.n = (int)h->n; pa.k = (int)h->k;
   set_prefetch(h, ph, pa.pf_ptr, pa.pf_bytes);   // K3a(p)'s inputs, issued at prop1's entry
   pa.stop = h->opts.eps > 0.0 ? h->flags + 6 : nullptr;
-  pa.Y = h->Y; pa.GAY = gay_fits(h) ? h->GAY : nullptr; pa.b = h->b;   // G_A Y of the warm block for K3a(p)'s first S-product
+  pa.Y = h->Y; pa.GAY = gay_fits(h) ? h->GAY[cur] : nullptr; pa.b = h->b;   // G_A Y of the warm block for K3a(p)'s first S-product
   pa.ts = h->prop_ts;
   pa.nb = h->prop_nb;
   SmallArgs sa = small_args(h, ph, 1);
@@ -570,8 +616,23 @@ static wlr_status enqueue_prop_iteration(wlr_ctx* h, int ph) {
     // of the GPU beside it.  K3b(p-1) on st2 once prop1 is done (it only needs to end with K3a).
     CUDA_TRY(h, cudaEventRecord(h->ev_fork, h->st));
     CUDA_TRY(h, cudaStreamWaitEvent(h->st4, h->ev_fork, 0));
+    const bool shadow = h->shadow && h->shadow_now;   // (K3a(p-1) exists: p >= 1)
+    if (shadow) {
+      // K3b(p-1) and the shadow are clusters of whole SMs of one GPC: they must be resident before
+      // prop1's CTAs spread over every GPC (prop1 leaves them prop_nsm's room), so they are
+      // launched first and prop1 follows an empty kernel on st4 (its launch latency is the head start)
+      if (pend) {
+        CUDA_TRY(h, cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
+        if ((e = launch_deferred(h, h->pend, h->st2)) != cudaSuccess) return fail(h, WLR_ECUDA, std::string("small step (deferred): ") + cudaGetErrorString(e));
+        CUDA_TRY(h, cudaEventRecord(h->ev_join, h->st2));
+      }
+      CUDA_TRY(h, cudaStreamWaitEvent(h->st5, h->ev_fork, 0));
+      if ((e = launch_small_step(shadow_args(h, ph), 1, h->st5)) != cudaSuccess) return fail(h, WLR_ECUDA, std::string("small step (shadow): ") + cudaGetErrorString(e));
+      CUDA_TRY(h, cudaEventRecord(h->ev_j5, h->st5));
+      if ((e = launch_noop(h->st4)) != cudaSuccess) return fail(h, WLR_ECUDA, std::string("no-op: ") + cudaGetErrorString(e));
+    }
     if ((e = launch_prop(pa, false, 0, h->st4, h->ev_f3)) != cudaSuccess) return fail(h, WLR_ECUDA, std::string("Gram propagation: ") + cudaGetErrorString(e));
-    if (pend) {
+    if (pend && !shadow) {
       CUDA_TRY(h, cudaStreamWaitEvent(h->st2, h->k3b_early ? h->ev_fork : h->ev_f3, 0));
       if ((e = launch_deferred(h, h->pend, h->st2)) != cudaSuccess) return fail(h, WLR_ECUDA, std::string("small step (deferred): ") + cudaGetErrorString(e));
       CUDA_TRY(h, cudaEventRecord(h->ev_join, h->st2));
@@ -586,10 +647,12 @@ static wlr_status enqueue_prop_iteration(wlr_ctx* h, int ph) {
     CUDA_TRY(h, cudaEventRecord(h->ev_j4, h->st4));
     CUDA_TRY(h, cudaStreamWaitEvent(h->st, h->ev_j4, 0));
     if (pend) CUDA_TRY(h, cudaStreamWaitEvent(h->st, h->ev_join, 0));
+    if (shadow) CUDA_TRY(h, cudaStreamWaitEvent(h->st, h->ev_j5, 0));
   }
+  if (!pend && !h->capturing) CUDA_TRY(h, cudaMemsetAsync(h->flags + 7, 0, 1, h->st));   // (now pending)
   h->pend = sa;
   h->pending = true;
-  h->pr.launches += pend ? 5 : 4;
+  h->pr.launches += (pend ? 5 : 4) + (h->shadow && h->shadow_now && !prof ? 2 : 0);   // (+ shadow, no-op)
   return WLR_OK;
 }
 
@@ -691,27 +754,39 @@ static wlr_status enqueue_iteration(wlr_ctx* h, int ph) {
     h->pr.iters++;
     h->pr.groups.push_back(pend ? 1 : 0);
   }
+  if (!pend && !h->capturing) CUDA_TRY(h, cudaMemsetAsync(h->flags + 7, 0, 1, h->st));   // (now pending)
   h->pend = s;
   h->pending = true;
   h->pr.launches += pend ? 5 : 4;
   return WLR_OK;
 }
 
-static wlr_status build_graph(wlr_ctx* h, int ph, int pend) {
-  cudaGraph_t g;
+// Capture one iteration (phase ph, deferred half pending or not) into *out.
+static wlr_status capture_graph(wlr_ctx* h, int ph, int pend, cudaGraph_t* out) {
   const bool keep_pend = h->pending;
   const SmallArgs keep_args = h->pend;
   h->pending = pend != 0;
   if (pend) h->pend = small_args(h, (ph + 5) % 6, 1);   // the previous iteration's step
+  h->capturing = true;
   CUDA_TRY(h, cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
   const int64_t l0 = h->pr.launches;
+  h->shadow_now = h->shadow;                 // graphs serve p >= 1 (p = 0 launches eagerly with a shadow)
   wlr_status s = enqueue_iteration(h, ph);
+  h->shadow_now = false;
   h->pr.launches = l0;
-  cudaError_t e = cudaStreamEndCapture(h->st, &g);
+  cudaError_t e = cudaStreamEndCapture(h->st, out);
+  h->capturing = false;
   h->pending = keep_pend;
   h->pend = keep_args;
   if (s != WLR_OK) return s;
   CUDA_TRY(h, e);
+  return WLR_OK;
+}
+
+static wlr_status build_graph(wlr_ctx* h, int ph, int pend) {
+  cudaGraph_t g;
+  wlr_status s = capture_graph(h, ph, pend, &g);
+  if (s != WLR_OK) return s;
   CUDA_TRY(h, cudaGraphInstantiate(&h->gexec[ph][pend], g, 0));
   cudaGraphDestroy(g);
   return WLR_OK;
@@ -719,15 +794,19 @@ static wlr_status build_graph(wlr_ctx* h, int ph, int pend) {
 
 // Instantiate (and upload) every per-iteration graph up front, so that no capture or
 // instantiation ever lands inside a timed region or the first iterations of a solve.
+// (Instantiating on 6 host threads was measured slower: 1.9-2.0 ms against 1.3 ms serial.)
 static wlr_status build_all_graphs(wlr_ctx* h) {
   if (!h->opts.use_graph || h->prof) return WLR_OK;
-  for (int ph = 0; ph < 6; ++ph)
-    for (int pend = 0; pend < 2; ++pend) {
-      if (h->gexec[ph][pend]) continue;
-      wlr_status s = build_graph(h, ph, pend);
-      if (s != WLR_OK) return s;
-      CUDA_TRY(h, cudaGraphUpload(h->gexec[ph][pend], h->st));
-    }
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int ph = 0; ph < 6; ++ph) {
+    if (h->gexec[ph][1]) continue;
+    wlr_status s = build_graph(h, ph, 1);
+    if (s != WLR_OK) return s;
+    CUDA_TRY(h, cudaGraphUpload(h->gexec[ph][1], h->st));
+  }
+  if (std::getenv("WLR_INIT_TIMES"))   // (diagnostics: host time of the graph builds)
+    std::fprintf(stderr, "[wlr] graphs %.3f ms\n",
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
   return WLR_OK;
 }
 
@@ -742,8 +821,8 @@ static wlr_status reset_graphs(wlr_ctx* h) {   // after a launch-shape switch (d
 static wlr_status launch_iteration(wlr_ctx* h) {
   wlr_status s;
   if (h->als) return fail(h, WLR_EINVAL, "the handle ran the block-ALS variant (wlr_als_iterate); sWLR state is gone");
-  if (h->opts.use_graph && !h->prof) {
-    const int pend = h->pending ? 1 : 0;
+  if (h->opts.use_graph && !h->prof && !(h->shadow && h->p == 0)) {
+    const int pend = 1;                       // (K3b(p-1) skips itself when not pending, flags[7])
     if (!h->gexec[h->ph][pend]) {
       s = build_graph(h, h->ph, pend);
       if (s != WLR_OK) return s;
@@ -758,9 +837,11 @@ static wlr_status launch_iteration(wlr_ctx* h) {
     }
     h->pend = small_args(h, h->ph, 1);
     h->pending = true;
-    h->pr.launches += pend ? 5 : 4;
+    h->pr.launches += 5 + (h->shadow ? 2 : 0);
   } else {
+    h->shadow_now = h->p > 0;                 // (the first iteration has no K3a(p-1) to rerun)
     s = enqueue_iteration(h, h->ph);
+    h->shadow_now = false;
     if (s != WLR_OK) return s;
   }
   h->ph = (h->ph + 1) % 6;
@@ -1031,9 +1112,20 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   {   // Gram propagation for the linear (uniform-W1) X1 half-step (prop.cu; WLR_PROP=0 disables, A/B)
     const char* pe = std::getenv("WLR_PROP");
     if (const char* ke = std::getenv("WLR_K3B_EARLY")) h->k3b_early = std::atoi(ke) != 0;
-    h->prop = h->uniform && h->dtype == WLR_F32 && (!pe || std::atoi(pe) != 0) && prop1_smem((int)n, (int)k, h->nsm, h->b) <= 227 * 1024 &&
-              prop1_rb((int)n, h->nsm) <= 8 && 16 * k * k <= 200 * 1024;
-    h->prop_nb = (int)std::min<int64_t>(n, h->nsm);
+    // prop1 runs one CTA per SM; K3b(p-1) and the shadow K3a start beside it at the iteration start,
+    // each a cluster of CL whole SMs, so prop1 leaves them room (WLR_PROP_RSV: SMs left out, A/B)
+    const char* se = std::getenv("WLR_SHADOW");
+    const bool want_shadow = !se || std::atoi(se) != 0;
+    int rsv = (want_shadow ? 2 : 1) * h->spl.CL;
+    if (const char* re = std::getenv("WLR_PROP_RSV")) rsv = std::atoi(re);
+    h->prop_nsm = std::max(1, h->nsm - std::max(0, rsv));
+    auto prop_fits = [&](int nsm) {
+      return prop1_smem((int)n, (int)k, nsm, h->b) <= 227 * 1024 && prop1_rb((int)n, nsm) <= 8;
+    };
+    if (!prop_fits(h->prop_nsm)) h->prop_nsm = h->nsm;
+    h->prop = h->uniform && h->dtype == WLR_F32 && (!pe || std::atoi(pe) != 0) && prop_fits(h->prop_nsm) &&
+              16 * k * k <= 200 * 1024;
+    h->prop_nb = (int)std::min<int64_t>(n, h->prop_nsm);
   }
   if (h->prop) {
     for (int i = 0; i < 2; ++i)
@@ -1045,7 +1137,8 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
       if ((s = dalloc(h, &q, (size_t)8 * 8 * (h->prop_nb + 3 * k))) != WLR_OK) return s;
       h->prop_ts = (unsigned long long*)q;
     }
-    if ((s = dalloc_t(h, &h->GAY, (size_t)nk * 32)) != WLR_OK) return s;   // (n-k) x b, b <= 32
+    for (int i = 0; i < 2; ++i)
+      if ((s = dalloc_t(h, &h->GAY[i], (size_t)nk * 32)) != WLR_OK) return s;   // (n-k) x b, b <= 32
   }
   if ((s = dalloc_t(h, &h->fw0, 2)) != WLR_OK) return s;
   if ((s = dalloc_t(h, &h->GA, (size_t)nk * nk)) != WLR_OK) return s;
@@ -1084,6 +1177,40 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   if ((s = dalloc_t(h, &h->scal, 8)) != WLR_OK) return s;
   if ((s = dalloc_t(h, &h->tdbg, 256)) != WLR_OK) return s;   // K3a marks, K3b marks, exchange stamps
   if ((s = dalloc_t(h, &h->trace, (size_t)h->trace_cap * 4)) != WLR_OK) return s;
+  if (h->prop) {   // shadow K3a buffers (same shapes as the real outputs)
+    const char* se = std::getenv("WLR_SHADOW");
+    h->shadow = !se || std::atoi(se) != 0;
+  }
+  if (h->shadow) {
+    const int64_t wt_rows = h->KA + round_up(kp, 32);
+    if ((s = dalloc_t(h, &h->sh_G, (size_t)k * k)) != WLR_OK) return s;
+    if ((s = dalloc_t(h, &h->sh_M, (size_t)k * nk)) != WLR_OK) return s;
+    if ((s = dalloc_t(h, &h->sh_C, (size_t)k * nk)) != WLR_OK) return s;
+    if ((s = dalloc_t(h, &h->sh_V, (size_t)nk * t)) != WLR_OK) return s;
+    if ((s = dalloc_t(h, &h->sh_CV, (size_t)k * t)) != WLR_OK) return s;
+    if ((s = dalloc_t(h, &h->sh_th, 32)) != WLR_OK) return s;
+    if ((s = dalloc_t(h, &h->sh_k3x, (size_t)2 * t * t + 8)) != WLR_OK) return s;
+    if ((s = dalloc_t(h, &h->sh_Gi, (size_t)k * k)) != WLR_OK) return s;
+    for (int i = 0; i < 2; ++i) {
+      if ((s = dalloc_t(h, &h->snapY[i], (size_t)nk * b)) != WLR_OK) return s;
+      if ((s = dalloc_t(h, &h->snapKi[i], (size_t)k * k)) != WLR_OK) return s;
+    }
+    if ((s = dalloc_t(h, &h->sh_gws, (size_t)std::max<int64_t>(1, h->spl.CL * h->spl.gws_stride))) != WLR_OK) return s;
+    if ((s = dalloc_t(h, &h->sh_xchg, (size_t)h->spl.CL * h->spl.flen)) != WLR_OK) return s;
+    if ((s = dalloc_t(h, &h->sh_red, (size_t)h->spl.flen + 3 * k * t + 64)) != WLR_OK) return s;
+    if ((s = dalloc_t(h, &h->sh_scal, 8)) != WLR_OK) return s;
+    if ((s = dalloc_t(h, &h->sh_trace, (size_t)h->trace_cap * 4)) != WLR_OK) return s;
+    if ((s = dalloc(h, &h->sh_Wt, (size_t)wt_rows * h->rp * h->es)) != WLR_OK) return s;
+    if ((s = dalloc(h, &h->sh_WtT, (size_t)2 * h->rp * wt_rows * h->es)) != WLR_OK) return s;
+    if ((s = dalloc(h, &h->sh_CVop, (size_t)std::max<int64_t>(k * t, 1) * h->es)) != WLR_OK) return s;
+    if ((s = dalloc(h, &h->sh_Kop, (size_t)k * k * h->es)) != WLR_OK) return s;
+    if (h->Sop && (s = dalloc_t(h, &h->sh_Sop, (size_t)k * round_up(k, (int64_t)8))) != WLR_OK) return s;
+    if ((s = dalloc_t(h, &h->sh_flags, 8)) != WLR_OK) return s;
+    int lo = 0, hi = 0;
+    CUDA_TRY(h, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CUDA_TRY(h, cudaStreamCreateWithPriority(&h->st5, cudaStreamNonBlocking, hi));
+    CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_j5, cudaEventDisableTiming));
+  }
 
   // ---- NCCL communicator (rows sharded over ranks), or the virtual group (one GPU, test hook)
   if (o.vgroup) {
@@ -1193,6 +1320,7 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   sa.tdbg = h->tdbg;
   cudaError_t e = launch_small_step(sa, 1, h->st);
   if (e == cudaSuccess) e = launch_deferred(h, sa, h->st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(h->flags + 7, 1, 1, h->st);   // (no deferred half pending)
   if (e != cudaSuccess) return fail(h, WLR_ECUDA, std::string("small step (init): ") + cudaGetErrorString(e));
   h->pr.launches = 0;
   CUDA_TRY(h, cudaMemcpyAsync(h->h_flags, h->flags, 8 * sizeof(int), cudaMemcpyDeviceToHost, h->st));
@@ -1682,11 +1810,13 @@ extern "C" wlr_status wlr_debug_state(wlr_handle h, const char* name, double* ou
     if (count) *count = 0;
     return WLR_OK;
   }
-  else if (nm == "prop") {   // Gram-propagation path: [active, prop1 CTAs, rows per CTA, G_A Y in prop1]
-    const double v[4] = {h->prop ? 1.0 : 0.0, (double)h->prop_nb,
-                         h->prop ? (double)prop1_rb((int)h->n, h->nsm) : 0.0, h->prop && gay_fits(h) ? 1.0 : 0.0};
-    for (int i = 0; i < 4 && out && i < cap; ++i) out[i] = v[i];
-    if (count) *count = 4;
+  else if (nm == "prop") {   // Gram-propagation path: [active, prop1 CTAs, rows per CTA, G_A Y in prop1,
+                             //  SMs prop1 spreads over, shadow K3a on]
+    const double v[6] = {h->prop ? 1.0 : 0.0, (double)h->prop_nb,
+                         h->prop ? (double)prop1_rb((int)h->n, h->prop_nsm) : 0.0, h->prop && gay_fits(h) ? 1.0 : 0.0,
+                         (double)h->prop_nsm, h->shadow ? 1.0 : 0.0};
+    for (int i = 0; i < 6 && out && i < cap; ++i) out[i] = v[i];
+    if (count) *count = 6;
     return WLR_OK;
   }
   else if (nm == "rptime") {
@@ -1816,6 +1946,8 @@ extern "C" void wlr_destroy(wlr_handle h) {
   if (h->ev_f3) cudaEventDestroy(h->ev_f3);
   if (h->ev_j3) cudaEventDestroy(h->ev_j3);
   if (h->st4) { cudaStreamSynchronize(h->st4); cudaStreamDestroy(h->st4); }
+  if (h->st5) { cudaStreamSynchronize(h->st5); cudaStreamDestroy(h->st5); }
+  if (h->ev_j5) cudaEventDestroy(h->ev_j5);
   if (h->ev_j4) cudaEventDestroy(h->ev_j4);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);

@@ -137,6 +137,7 @@ bool prop_gay_ok(int n, int k, int b, int nsm);   // prop1 computes G_A Y of the
 // eps mode: flags[6] = flags[2] (the converged flag) at the start of an iteration, one thread, so that
 // every kernel of the iteration (clusters included) sees one consistent value
 cudaError_t launch_stop_latch(int* flags, cudaStream_t st);
+cudaError_t launch_noop(cudaStream_t st);    // an empty kernel (launch ordering, api.cu)
 cudaError_t launch_vsum(double* out, const double* in, int G, size_t stride, size_t count, cudaStream_t st);
 cudaError_t launch_prop(const PropArgs& a, bool f64, int pdl, cudaStream_t st, cudaEvent_t after1 = nullptr);
 
@@ -242,6 +243,9 @@ struct SmallArgs {
   const double* th_in; double* th_out;   // b       Ritz values of S_p / S_{p+1}
   double* k3x;                      // small results K3a -> K3b: R (t x t), ZnV (t x t)
   double* Y;                        // nk x b  warm-start Ritz block (updated)
+  int* skip;                        // part 2 in a graph: *skip != 0 -> this deferred half already ran
+                                    // (flushed by the host or never needed): clear it and return
+  double* snapY; double* snapKi;    // part 1: copies of its Y and K^{-1} inputs as read (for the shadow K3a), or nullptr
   const double* Gi_in; double* Gi_out;   // k x k  G^{-1} of the previous / current state
   double* Ki;                       // k x k  (w^2 I + C C^T)^{-1} (uniform W1; updated)
   double* gws;                      // CL x gws_stride global workspace

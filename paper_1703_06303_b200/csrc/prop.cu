@@ -448,6 +448,12 @@ cudaError_t launch_prop(const PropArgs& a, bool f64, int pdl, cudaStream_t st, c
 
 __global__ void stop_latch_kernel(int* flags) { flags[6] = flags[2]; }
 
+__global__ void noop_kernel() {}
+cudaError_t launch_noop(cudaStream_t st) {
+  noop_kernel<<<1, 32, 0, st>>>();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_stop_latch(int* flags, cudaStream_t st) {
   stop_latch_kernel<<<1, 1, 0, st>>>(flags);
   return cudaGetLastError();

@@ -864,6 +864,11 @@ template <int BT, int PART>
 __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_constant__ SmallArgs a) {
   if (a.stop && *a.stop) return;               // (eps mode: latched before the iteration; every CTA of the
                                                //  cluster reads the same value, so none waits at a barrier)
+  if (PART == 2 && a.skip && *a.skip) {        // (graph node of a deferred half that already ran)
+    cg::this_cluster().sync();                 // every CTA has read the flag
+    if (cg::this_cluster().block_rank() == 0 && threadIdx.x == 0) *a.skip = 0;
+    return;
+  }
   if (PART != 1) pdl_wait();                   // (part 1 waits inside its first load round)
   // a programmatic dependent may start now: the only one is the propagation iteration's row pass,
   // which reads W'_p / X1_p (never this kernel's outputs) and never waits on it
@@ -965,6 +970,13 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
           yv[u] = idx < nY ? a.Y[(int64_t)s.rs * b + idx] : 0.0;
           vv[u] = idx < nV ? a.V_in[(int64_t)s.rs * t + idx] : 0.0;
         }
+        if (a.snapY) {                                       // (each CTA its slice: all of Y once)
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int idx = r0 / 2 + threadIdx.x + u * kSST;
+            if (idx < nY) a.snapY[(int64_t)s.rs * b + idx] = yv[u];
+          }
+        }
         pdl_wait();                                          // the increments of the reduce kernel
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -1063,6 +1075,7 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
     for (int u = 0; u < 2; ++u) {
       const int idx = threadIdx.x + u * kSST;
       kiv[u] = ki_stage && idx < kk ? a.Ki[idx] : 0.0;
+      if (ki_stage && a.snapKi && s.c == 0 && idx < kk) a.snapKi[idx] = kiv[u];
     }
     // C'[:, slice] = G'^{-1} M'[:, slice]
     gemm_nn(k, s.nl, k, Xq, k, Ms, ldm, Cs, ldc, 1.0, false);
@@ -1072,7 +1085,10 @@ __global__ void __launch_bounds__(kSST, 1) small_step_kernel(const __grid_consta
         const int idx = threadIdx.x + u * kSST;
         if (idx < kk) Pq[idx] = kiv[u];
       }
-      for (int idx = threadIdx.x + 2 * kSST; idx < kk; idx += kSST) Pq[idx] = a.Ki[idx];   // k > 32
+      for (int idx = threadIdx.x + 2 * kSST; idx < kk; idx += kSST) {   // k > 32
+        Pq[idx] = a.Ki[idx];
+        if (a.snapKi && s.c == 0) a.snapKi[idx] = Pq[idx];
+      }
     }
     __syncthreads();
     if (p.oCs >= 0)

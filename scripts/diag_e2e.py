@@ -9,7 +9,7 @@ import paper_1703_06303_b200 as w
 cfg = synth.CONFIGS[3]
 stream = torch.cuda.Stream(); torch.cuda.set_stream(stream)
 Ah = torch.from_numpy(synth.make_A(cfg)).pin_memory()
-for rep in range(3):
+for rep in range(int(sys.argv[1]) if len(sys.argv) > 1 else 3):
     torch.cuda.synchronize(); t0 = time.perf_counter()
     h = w.wlr_init(Ah, cfg.k, cfg.r, None, w1=cfg.w_const, stream=stream.cuda_stream)
     torch.cuda.synchronize(); t1 = time.perf_counter()

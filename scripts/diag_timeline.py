@@ -13,6 +13,7 @@ import paper_1703_06303_b200 as w
 
 cfg = synth.CONFIGS[int(sys.argv[1]) if len(sys.argv) > 1 else 3]
 NOFLUSH = "noflush" in sys.argv[2:]          # warm L2 (kernel durations without the cold-cache cost)
+NOSYNC = "nosync" in sys.argv[2:]            # as bench.py: no host synchronisation between flush and step
 stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
 A = torch.from_numpy(synth.make_A(cfg)).cuda()
@@ -32,21 +33,25 @@ with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
             flush.fill_(float(i))
         else:
             flush[:1].fill_(float(i))      # (a step marker kernel only)
-        torch.cuda.synchronize()
+        if not NOSYNC:
+            torch.cuda.synchronize()
         w.wlr_iterate_async(h, 1)
-        torch.cuda.synchronize()
+        if not NOSYNC:
+            torch.cuda.synchronize()
+    torch.cuda.synchronize()
 path = os.path.join(tempfile.mkdtemp(), "trace.json")
 prof.export_chrome_trace(path)
 ev = json.load(open(path))["traceEvents"]
 ks = [e for e in ev if e.get("cat") == "kernel"]
 ks.sort(key=lambda e: e["ts"])
 # split into steps at the fill kernels
-steps, cur = [], []
+steps, cur, fills = [], [], []
 for e in ks:
     if "fill" in e["name"] or "elementwise" in e["name"].lower():
         if cur:
             steps.append(cur)
         cur = []
+        fills.append(e)
         continue
     cur.append(e)
 if cur:
@@ -54,7 +59,8 @@ if cur:
 for si, st in enumerate(steps[1:], 1):
     t0 = st[0]["ts"]
     end = max(e["ts"] + e["dur"] for e in st)
-    print(f"step {si}: span {end - t0:.1f} us")
+    fe = fills[si]["ts"] + fills[si]["dur"] if si < len(fills) else t0
+    print(f"step {si}: span {end - t0:.1f} us (flush end -> first kernel {t0 - fe:.1f} us)")
     for e in st:
         nm = e["name"].replace("wlr::", "")[:48]
         print(f"   {e['ts'] - t0:7.1f} +{e['dur']:6.1f}  end {e['ts'] + e['dur'] - t0:7.1f}  stream {e['args'].get('stream')}  {nm}")

@@ -1,5 +1,5 @@
 """GPU parity of the Gram-propagation path (uniform W1, fp32: prop1 / prop2) at
-shapes that exercise its variants: rows per prop1 CTA RB = ceil(n / min(n, #SMs)) from 1 to 8
+shapes that exercise its variants: rows per prop1 CTA RB = ceil(n / min(n, #SMs less the K3b / shadow clusters)) from 1 to 8
 (uneven row splits), Q column blocks rounded to 2 / 8 / 16 (k = 8, 20..30, 36), r - k = 1..5, and
 G_A Y computed in prop1 or left to the small step (Y not fitting in prop1's shared memory).
 Against the fp64 oracle (literal Algorithm 1) on the same seeded inputs and iteration count."""
@@ -39,7 +39,9 @@ def test_gram_propagation_shapes(m, n, k, r):
     info = w.wlr_debug_state(g["handle"], "prop")
     nsm = torch.cuda.get_device_properties(0).multi_processor_count
     assert info[0] == 1.0, "Gram propagation not active"
-    assert info[1] == min(n, nsm) and info[2] == -(-n // min(n, nsm))
+    nsp = int(info[4])                        # SMs left to prop1 beside the K3b / shadow clusters
+    assert 1 <= nsp <= nsm and info[5] == 1.0
+    assert info[1] == min(n, nsp) and info[2] == -(-n // min(n, nsp))
     if n == 1030 and nsm == 148:
         assert info[3] == 0.0                  # (the G_A Y fallback inside the small step)
     o = gu.run_oracle(cfg, A, None, cfg.iters)
@@ -54,3 +56,28 @@ def test_n_minus_k_beyond_the_cluster_is_rejected():
     with pytest.raises(w.WlrError) as e:
         w.wlr_init(A, 16, 18, None, w1=30.0)
     assert "n - k > 1024" in str(e.value)
+
+
+@pytest.mark.parametrize("cfg_id", [2, 3])
+def test_shadow_small_step_is_bitwise_neutral(cfg_id, monkeypatch):
+    """The shadow K3a (a rerun of K3a(p-1) into private buffers at the start of iteration p, which
+    warms K3a's code in L2) changes nothing: trace and result bitwise identical with
+    it off, at the same prop1 grid (WLR_PROP_RSV fixed), over iterations that cross the graph phases
+    and a host synchronisation (the eager p = 0 iteration and the shadow's own state chain)."""
+    w = gu.need_gpu()
+    import torch
+    cfg = synth.CONFIGS[cfg_id]
+    A = torch.from_numpy(synth.make_A(cfg)).cuda()
+    out = {}
+    for sh in ("0", "1"):
+        monkeypatch.setenv("WLR_SHADOW", sh)
+        monkeypatch.setenv("WLR_PROP_RSV", "32")
+        h = w.wlr_init(A, cfg.k, cfg.r, None, w1=cfg.w_const)
+        assert w.wlr_debug_state(h, "prop")[5] == float(sh)
+        w.wlr_iterate(h, 7)
+        w.wlr_iterate(h, 13)
+        r = w.wlr_result(h, x2=False)
+        out[sh] = (np.asarray(w.wlr_trace(h)).copy(), {k_: np.asarray(v).copy() for k_, v in r.items() if v is not None})
+    assert np.array_equal(out["0"][0], out["1"][0])
+    for k_ in out["0"][1]:
+        assert np.array_equal(out["0"][1][k_], out["1"][1][k_]), k_
