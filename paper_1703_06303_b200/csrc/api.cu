@@ -548,6 +548,7 @@ static cudaError_t launch_row_pass_iter(wlr_ctx* h, int ph, cudaStream_t st, boo
         q.Xold = a.Xold; q.Xnew = a.Xnew; q.Dnew = a.Dnew; q.fw_part = h->fw_part; q.flags = h->flags;
         q.m = h->m; q.k = (int)h->k; q.kp = (int)h->kp;
         q.stop = stop;
+        q.e_lin = h->tc_on ? 1 : 0;              // (the tensor-core row pass writes the linear part)
         e = launch_row_solve(q, h->rs_grid, st);
       }
     }

@@ -74,8 +74,8 @@ struct RowPassTcArgs {
   float w2s;
   double* fw_part;                  // gridDim.x partials of f_w
   // non-uniform W1 (E mode, E != nullptr): the tile result is E - A1 . W1^2 (the linear part of E,
-  // W'' = [0; U; P]); the epilogue writes e = result + A1 . W1^2 rows (m x kp) for the per-row
-  // solves instead of X1_{p+1} / Delta / f_w
+  // W'' = [0; U; P]); the epilogue writes those rows (m x kp) for the per-row solves, which add
+  // A1 . W1^2 (RowSolveArgs::e_lin), instead of X1_{p+1} / Delta / f_w
   float* E; const float* W1; int64_t ldw;
   const void* pf_ptr[kPf]; int64_t pf_bytes[kPf];
   int64_t m; int KA, k, kp, n;
@@ -151,6 +151,8 @@ struct RowSolveArgs {
   int* flags;
   int64_t m; int k, kp;
   const int* stop;                  // eps mode: the iteration's latched stop flag, or nullptr
+  int e_lin;                        // 1: E holds only the linear part [A | X1_p] W'' (the tensor-core row
+                                    //    pass); the solver adds A1 . W1^2 (it reads both rows anyway)
 };
 bool row_solve_ok(int k);
 size_t row_solve_smem(int k);

@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(tc_threads<NR>(), NR >= 8 ? 1 : 2) row_pass_tc
           if (RP <= 32) {
 #pragma unroll
             for (int q = 0; q < 8; ++q) { xo[q] = xor_[q]; ar[q] = a1r[q]; }
-          } else if (live) {
+          } else if (live && !a.E) {
             const float4* xp = reinterpret_cast<const float4*>(a.Xold + row * a.kp + c0);
             const float4* ap = reinterpret_cast<const float4*>(a.A + row * a.lda + c0);
 #pragma unroll
@@ -311,21 +311,14 @@ __global__ void __launch_bounds__(tc_threads<NR>(), NR >= 8 ? 1 : 2) row_pass_tc
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] += vl[j];
           }
-          if (live && a.E) {               // non-uniform: e = (E - A1 . W1^2) + A1 . W1^2
-            float4* en = reinterpret_cast<float4*>(a.E + row * a.kp + c0);
-            const float* w1r = a.W1 + row * a.ldw;
-#pragma unroll
+          if (live && a.E) {               // non-uniform: the linear part e - A1 . W1^2 (the per-row
+            float4* en = reinterpret_cast<float4*>(a.E + row * a.kp + c0);   // solver adds A1 . W1^2:
+#pragma unroll                                                           // no loads in this epilogue)
             for (int q = 0; q < 8; ++q) {
               if (q < nv) {
-                const float* av = reinterpret_cast<const float*>(&ar[q]);
                 float eq[4];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  const int ll = c0 + 4 * q + e;
-                  float w = 0.f;
-                  if (ll < a.k) w = __ldg(w1r + ll);
-                  eq[e] = ll < a.k ? fmaf(av[e] * w, w, v[4 * q + e]) : 0.f;
-                }
+                for (int e = 0; e < 4; ++e) eq[e] = c0 + 4 * q + e < a.k ? v[4 * q + e] : 0.f;
                 en[q] = make_float4(eq[0], eq[1], eq[2], eq[3]);
               }
             }

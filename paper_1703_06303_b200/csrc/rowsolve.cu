@@ -189,6 +189,8 @@ __global__ void __launch_bounds__(32) row_solve_kernel(const __grid_constant__ R
     sa[q] = (uint32_t)__cvta_generic_to_shared(Lwr[q]);
   }
   float* w2s = xo + rs_k8(k);                       // W1(i,:)^2 of the row (the panel diagonals)
+  float* ecor = xo;                                 // A1(i,:) . W1(i,:)^2 (e_lin: added to the bordered row
+                                                    // during the factorisation; xo is written only after it)
   const float* Lk = Lw + rs_base(k >> 3) + (k & 7);   // row k: z = e L^{-T}
   const int npan = (k + 7) / 8;
   double fw = 0.0;
@@ -199,6 +201,15 @@ __global__ void __launch_bounds__(32) row_solve_kernel(const __grid_constant__ R
   for (; row < a.m; row += gridDim.x) {
     const float* w1 = a.W1 + row * a.ldw;
     const float* er = a.E + row * kp;
+    if (lane < 3 && row + gridDim.x < a.m) {         // the next row's W1, A1 and X1_p rows into L2 (read at
+      const int64_t rn = row + gridDim.x;             // its start, where their latency is exposed)
+      const char* src = lane == 0 ? reinterpret_cast<const char*>(a.W1 + rn * a.ldw)
+                      : lane == 1 ? reinterpret_cast<const char*>(a.A + rn * a.lda)
+                                  : reinterpret_cast<const char*>(a.Xold + rn * kp);
+      const unsigned nb = (unsigned)((lane == 2 ? kp : k) * 4);
+      if ((((uintptr_t)src) & 15) == 0 && (nb & 15) == 0)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(nb) : "memory");
+    }
     // the output epilogue's inputs, loaded now so that their latency hides behind the solve
     float xold[NQ], a1v[NQ], w1v[NQ];
 #pragma unroll
@@ -208,6 +219,7 @@ __global__ void __launch_bounds__(32) row_solve_kernel(const __grid_constant__ R
       a1v[q] = l < k ? __ldg(a.A + row * a.lda + l) : 0.f;
       w1v[q] = l < k ? __ldg(w1 + l) : 0.f;
       if (l < k) w2s[l] = w1v[q] * w1v[q];
+      if (a.e_lin && l < rs_k8(k)) ecor[l] = l < k ? a1v[q] * (w1v[q] * w1v[q]) : 0.f;
     }
     __syncwarp();
     // ---------------------------------------------------------------- factorisation
@@ -218,6 +230,11 @@ __global__ void __launch_bounds__(32) row_solve_kernel(const __grid_constant__ R
       for (int q = 0; q < NQ; ++q)
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj) acc[q][jj] = sn[q][jj];
+      if (a.e_lin && lane == 0) {                    // (row k = the bordered row e: lane 0 of q-block 0)
+        const float4 c0 = reinterpret_cast<const float4*>(ecor + J0)[0], c1 = reinterpret_cast<const float4*>(ecor + J0)[1];
+        acc[0][0] += c0.x; acc[0][1] += c0.y; acc[0][2] += c0.z; acc[0][3] += c0.w;
+        acc[0][4] += c1.x; acc[0][5] += c1.y; acc[0][6] += c1.z; acc[0][7] += c1.w;
+      }
       {   // the next panel's K entries (or panel 0 of this warp's next row)
         const int64_t rn = P + 1 < npan ? row : row + gridDim.x;
         if (rn < a.m) rs_fetch<NQ>(sn, arow, S, a.E + rn * kp, k, k8, P + 1 < npan ? P + 1 : 0);

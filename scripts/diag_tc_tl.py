@@ -1,14 +1,16 @@
-"""Timeline of the tensor-core row pass: per-CTA globaltimer stamps (WLR_TC_DBG=16)."""
+"""Timeline of the tensor-core row pass: per-CTA globaltimer stamps (WLR_TC_DBG=16).  Usage: [config]"""
 import sys
 import numpy as np
 sys.path.insert(0, ".")
 import torch
 import synth
 import paper_1703_06303_b200 as w
-cfg = synth.CONFIGS[3]
+cfg = synth.CONFIGS[int(sys.argv[1]) if len(sys.argv) > 1 else 3]
 A = torch.from_numpy(synth.make_A(cfg)).cuda()
+W1n = synth.make_W1(cfg)
+W1 = None if W1n is None else torch.from_numpy(W1n).cuda()
 flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
-h = w.wlr_init(A, cfg.k, cfg.r, None, w1=cfg.w_const)
+h = w.wlr_init(A, cfg.k, cfg.r, W1, w1=cfg.w_const or 1.0)
 w.wlr_iterate(h, 5)
 flush.fill_(1.0)
 w.wlr_iterate_async(h, 1)
