@@ -198,26 +198,29 @@ __global__ void __launch_bounds__(32) row_solve_kernel(const __grid_constant__ R
   float sn[NQ][8];
   int64_t row = blockIdx.x;
   if (row < a.m) rs_fetch<NQ>(sn, arow, S, a.E + row * kp, k, k8, 0);
-  for (; row < a.m; row += gridDim.x) {
-    const float* w1 = a.W1 + row * a.ldw;
-    const float* er = a.E + row * kp;
-    if (lane < 3 && row + gridDim.x < a.m) {         // the next row's W1, A1 and X1_p rows into L2 (read at
-      const int64_t rn = row + gridDim.x;             // its start, where their latency is exposed)
-      const char* src = lane == 0 ? reinterpret_cast<const char*>(a.W1 + rn * a.ldw)
-                      : lane == 1 ? reinterpret_cast<const char*>(a.A + rn * a.lda)
-                                  : reinterpret_cast<const char*>(a.Xold + rn * kp);
-      const unsigned nb = (unsigned)((lane == 2 ? kp : k) * 4);
-      if ((((uintptr_t)src) & 15) == 0 && (nb & 15) == 0)
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(nb) : "memory");
-    }
-    // the output epilogue's inputs, loaded now so that their latency hides behind the solve
-    float xold[NQ], a1v[NQ], w1v[NQ];
+  // the row's X1_p, A1 and W1 values (lane + 32 q), software-pipelined one row ahead: W1^2 (the panel
+  // diagonals) and A1 . W1^2 (e_lin) are needed at the start of a row, where a fresh load's DRAM
+  // latency would be exposed; X1_p and A1 again at its end (Delta, f_w)
+  float xon[NQ], a1n[NQ], w1n[NQ];
+  auto load_row = [&](int64_t r) {
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
       const int l = lane + 32 * q;
-      xold[q] = l < kp ? a.Xold[row * kp + l] : 0.f;
-      a1v[q] = l < k ? __ldg(a.A + row * a.lda + l) : 0.f;
-      w1v[q] = l < k ? __ldg(w1 + l) : 0.f;
+      xon[q] = r < a.m && l < kp ? a.Xold[r * kp + l] : 0.f;
+      a1n[q] = r < a.m && l < k ? __ldg(a.A + r * a.lda + l) : 0.f;
+      w1n[q] = r < a.m && l < k ? __ldg(a.W1 + r * a.ldw + l) : 0.f;
+    }
+  };
+  load_row(row);
+  for (; row < a.m; row += gridDim.x) {
+    const float* er = a.E + row * kp;
+    float xold[NQ], a1v[NQ], w1v[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) { xold[q] = xon[q]; a1v[q] = a1n[q]; w1v[q] = w1n[q]; }
+    load_row(row + gridDim.x);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int l = lane + 32 * q;
       if (l < k) w2s[l] = w1v[q] * w1v[q];
       if (a.e_lin && l < rs_k8(k)) ecor[l] = l < k ? a1v[q] * (w1v[q] * w1v[q]) : 0.f;
     }
@@ -230,10 +233,13 @@ __global__ void __launch_bounds__(32) row_solve_kernel(const __grid_constant__ R
       for (int q = 0; q < NQ; ++q)
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj) acc[q][jj] = sn[q][jj];
-      if (a.e_lin && lane == 0) {                    // (row k = the bordered row e: lane 0 of q-block 0)
+      if (a.e_lin) {                                 // row k = the bordered row e: lane 0 of q-block 0
         const float4 c0 = reinterpret_cast<const float4*>(ecor + J0)[0], c1 = reinterpret_cast<const float4*>(ecor + J0)[1];
-        acc[0][0] += c0.x; acc[0][1] += c0.y; acc[0][2] += c0.z; acc[0][3] += c0.w;
-        acc[0][4] += c1.x; acc[0][5] += c1.y; acc[0][6] += c1.z; acc[0][7] += c1.w;
+        const float m0 = lane == 0 ? 1.f : 0.f;      // (no divergent branch: a broadcast and 8 FMAs)
+        acc[0][0] = fmaf(m0, c0.x, acc[0][0]); acc[0][1] = fmaf(m0, c0.y, acc[0][1]);
+        acc[0][2] = fmaf(m0, c0.z, acc[0][2]); acc[0][3] = fmaf(m0, c0.w, acc[0][3]);
+        acc[0][4] = fmaf(m0, c1.x, acc[0][4]); acc[0][5] = fmaf(m0, c1.y, acc[0][5]);
+        acc[0][6] = fmaf(m0, c1.z, acc[0][6]); acc[0][7] = fmaf(m0, c1.w, acc[0][7]);
       }
       {   // the next panel's K entries (or panel 0 of this warp's next row)
         const int64_t rn = P + 1 < npan ? row : row + gridDim.x;
