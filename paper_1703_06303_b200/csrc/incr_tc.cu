@@ -205,21 +205,38 @@ __global__ void __launch_bounds__(kItThreads, KPD <= 32 ? 2 : 1) incr_tc_kernel(
         tmem_st32(ta + 32, lo);
         tmem_st_wait();
       }
-      {   // Delta^T hi (rows 0..KPD-1) | lo (rows KPD..) of the B slot: element (n, k) = Delta(k, n)
-        const float* dl = reinterpret_cast<const float*>(st + kItZB);
-        float* bt = reinterpret_cast<float*>(bst + l * kItBT);
+      {   // Delta^T hi (rows 0..KPD-1) | lo (rows KPD..) of the B slot: element (n, k) = Delta(k, n).
+          // Task t = (kb, nb): the 4 x 4 block k = 4 kb.., n = 4 nb.. -- four 16-byte reads (one per
+          // k row of the SWIZZLE_128B box), a register transpose, four 16-byte hi and four lo writes
+          // (one per n row of the K-major SWIZZLE_128B operand); lanes spread over kb = t & 7 and 4
+          // consecutive nb, so every access is at its minimum of 4 wavefronts per warp
+        const unsigned char* dl = st + kItZB;
+        unsigned char* bt = bst + l * kItBT;
 #pragma unroll
-        for (int q = 0; q < KPD / 4; ++q) {
-          const int e = tid + 128 * q;                    // 32 x KPD elements
-          const int k = e / KPD, n = e % KPD;             // read row k of Delta (coalesced)
-          const float* box = dl + (n >> 5) * 1024;        // 32-column box of the chunk
-          const int nn = n & 31;
-          const float v = box[k * 32 + ((((nn >> 2) ^ (k & 7)) << 2) | (nn & 3))];
-          float h, lo;
-          tf32_split(v, h, lo);
-          const int off = n * 32 + ((((k >> 2) ^ (n & 7)) << 2) | (k & 3));
-          bt[off] = h;
-          bt[KPD * 32 + off] = lo;                        // rows KPD.. : (n + KPD) & 7 == n & 7
+        for (int t = tid; t < 2 * KPD; t += 128) {
+          const int kb = t & 7, nb = t >> 3;
+          const unsigned char* box = dl + (nb >> 3) * 4096;   // 32-column box of the chunk
+          const int u = nb & 7;                               // 16-byte unit of n within the box row
+          float4 r[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int k = 4 * kb + i;
+            r[i] = *reinterpret_cast<const float4*>(box + k * 128 + ((u ^ (k & 7)) << 4));
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int n = 4 * nb + j;
+            const float c[4] = {j == 0 ? r[0].x : j == 1 ? r[0].y : j == 2 ? r[0].z : r[0].w,
+                                j == 0 ? r[1].x : j == 1 ? r[1].y : j == 2 ? r[1].z : r[1].w,
+                                j == 0 ? r[2].x : j == 1 ? r[2].y : j == 2 ? r[2].z : r[2].w,
+                                j == 0 ? r[3].x : j == 1 ? r[3].y : j == 2 ? r[3].z : r[3].w};
+            float h[4], lo[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) tf32_split(c[i], h[i], lo[i]);
+            const int pos = (kb ^ (n & 7)) << 4;                // (KPD + n) & 7 == n & 7
+            *reinterpret_cast<float4*>(bt + n * 128 + pos) = make_float4(h[0], h[1], h[2], h[3]);
+            *reinterpret_cast<float4*>(bt + (KPD + n) * 128 + pos) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+          }
         }
       }
       fence_proxy_async();
