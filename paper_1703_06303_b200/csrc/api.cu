@@ -1811,6 +1811,15 @@ extern "C" wlr_status wlr_debug_state(wlr_handle h, const char* name, double* ou
     if (count) *count = 0;
     return WLR_OK;
   }
+  else if (nm == "gate") {   // [tensor-core increments enabled, gate (flags[5]: on once the X1 step is small), KPD]
+    int f = 0;
+    CUDA_TRY(h, cudaStreamSynchronize(h->st));
+    CUDA_TRY(h, cudaMemcpy(&f, h->flags + 5, sizeof(int), cudaMemcpyDeviceToHost));
+    const double v[3] = {h->itc_on ? 1.0 : 0.0, (double)f, (double)h->itc_kpd};
+    for (int i = 0; i < 3 && out && i < cap; ++i) out[i] = v[i];
+    if (count) *count = 3;
+    return WLR_OK;
+  }
   else if (nm == "prop") {   // Gram-propagation path: [active, prop1 CTAs, rows per CTA, G_A Y in prop1,
                              //  SMs prop1 spreads over, shadow K3a on]
     const double v[6] = {h->prop ? 1.0 : 0.0, (double)h->prop_nb,

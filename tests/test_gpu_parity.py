@@ -201,3 +201,29 @@ def test_stopping_rule_on_device(ci, check_every):
     assert w.wlr_objective(h)[0] == F
     np.testing.assert_array_equal(w.wlr_result(h)["X1"], X1)
     assert abs(F - o.trace[-1]["F"]) <= gu.TOL_F[cfg.dtype] * abs(o.trace[-1]["F"])
+
+
+@pytest.mark.parametrize("m,n,k,r", [
+    (2049, 110, 40, 44),     # KPD 64
+    (2517, 130, 70, 73),     # KPD 96, r - k = 3
+    (3037, 150, 90, 94),     # KPD 96, ragged m
+])
+def test_nonuniform_tensor_core_increments(m, n, k, r):
+    """Non-uniform fp32 W1 (log-uniform) at k = 40..90: the tcgen05 E-mode row pass
+    (linear part, the per-row solver adds A1 . W1^2), the warp-per-row Cholesky and the tcgen05
+    increments with a KPD = 64 / 96 wide Delta^T operand (4 x 4 register-block transpose) once the
+    X1 step is small (the gate); against the fp64 oracle over 20 iterations."""
+    w = gu.need_gpu()
+    g0 = np.random.default_rng(3 + k)
+    # rank r - 1 plus noise: the iteration settles within a few steps (relative X1 step ~3e-5), so the
+    # gate (||Delta||^2 <= 1e-6 ||X1||^2) opens and most iterations run the tensor-core increments
+    A = (g0.standard_normal((m, r - 1)) @ g0.standard_normal((r - 1, n)) + 0.1 * g0.standard_normal((m, n)))
+    W1 = np.exp(g0.uniform(0.0, np.log(30.0), size=(m, k)))
+    A, W1 = A.astype(np.float32), W1.astype(np.float32)
+    cfg = synth.Config("nonuniform_tc", m, n, k, r, "f32", 20, "lowrank", w_const=None, w_logu=(1, 30))
+    g = gu.run_gpu(cfg, A, W1, 20)
+    gate = w.wlr_debug_state(g["handle"], "gate")
+    assert g["tensor_cores"] and gate[0] == 1.0 and gate[2] == (64 if k <= 64 else 96)
+    assert gate[1] == 1.0, "the tensor-core increments never engaged (X1 step never small)"
+    o = gu.run_oracle(cfg, A.astype(np.float64), W1.astype(np.float64), 20)
+    gu.compare(cfg, g, o)
