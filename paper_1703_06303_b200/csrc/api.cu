@@ -203,6 +203,11 @@ struct wlr_ctx {
   SmallArgs last_ss{};         // arguments of the last small-step launch (diagnostics)
   bool ktime = false;
   int trace_cap = 4096;
+  // device flags (8 ints): [0] first error (DevFlag), [1] input validation bits (1: W1 <= 0, 2: non-
+  // finite), [2] converged (eps rule), [3] eigensolver restarts of the last small step (diagnostics),
+  // [4] (spare), [5] tensor-core increments gate (X1
+  // step small), [6] the iteration's latched stop flag (eps mode), [7] K3b(p-1) of the next graph
+  // already ran (set by flush_pending / init, cleared by that K3b)
   int* flags = nullptr;
   int* h_flags = nullptr;
   double* h_scal = nullptr;
