@@ -208,15 +208,18 @@ __global__ void __launch_bounds__(kItThreads, KPD <= 32 ? 2 : 1) incr_tc_kernel(
       {   // Delta^T hi (rows 0..KPD-1) | lo (rows KPD..) of the B slot: element (n, k) = Delta(k, n).
           // Task t = (kb, nb): the 4 x 4 block k = 4 kb.., n = 4 nb.. -- four 16-byte reads (one per
           // k row of the SWIZZLE_128B box), a register transpose, four 16-byte hi and four lo writes
-          // (one per n row of the K-major SWIZZLE_128B operand); lanes spread over kb = t & 7 and 4
-          // consecutive nb, so every access is at its minimum of 4 wavefronts per warp
+          // (one per n row of the K-major SWIZZLE_128B operand).  A 128-bit access is served 8 lanes
+          // at a time, so each 8-lane group takes u = lane % 8 and kb = (u + s) % 8 (s = the group):
+          // the read position u ^ (k % 8) and the write position kb ^ (n % 8) are then 8 distinct
+          // 16-byte units in every group, one wavefront each (lanes with kb = lane % 8 and a shared u
+          // per group read with 4-way conflicts: 16 wavefronts per warp instead of 4, ncu source page)
         const unsigned char* dl = st + kItZB;
         unsigned char* bt = bst + l * kItBT;
 #pragma unroll
         for (int t = tid; t < 2 * KPD; t += 128) {
-          const int kb = t & 7, nb = t >> 3;
-          const unsigned char* box = dl + (nb >> 3) * 4096;   // 32-column box of the chunk
-          const int u = nb & 7;                               // 16-byte unit of n within the box row
+          const int u = t & 7, kb = (u + (t >> 3)) & 7, bx = t >> 6;   // 16-byte unit of n, row block
+          const int nb = 8 * bx + u;
+          const unsigned char* box = dl + bx * 4096;          // 32-column box of the chunk
           float4 r[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
