@@ -16,6 +16,7 @@
 #include <cstdlib>
 #include <condition_variable>
 #include <functional>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -789,10 +790,48 @@ static wlr_status capture_graph(wlr_ctx* h, int ph, int pend, cudaGraph_t* out) 
   return WLR_OK;
 }
 
+// Instantiated iteration graphs outlive their handle (process-wide pool, keyed by device, shape and
+// launch-path choices): a later handle of the same shape captures its graphs and updates a pooled
+// executable in place (cudaGraphExecUpdate) instead of instantiating one -- instantiation is ~0.1 ms
+// of host time per graph, the largest part of wlr_init for repeated solves.  An update that the
+// driver rejects (another topology) falls back to instantiation.  Not for NCCL / virtual-group
+// handles (their graphs hold communicator state).
+static std::mutex g_gpool_mu;
+static std::map<std::string, std::vector<cudaGraphExec_t>> g_gpool;
+static std::string gpool_key(const wlr_ctx* h, int ph, int pend) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  char b[256];
+  std::snprintf(b, sizeof b, "%d:%lld:%lld:%lld:%lld:%d:%d:%d:%d:%d:%d:%d:%d:%d", dev, (long long)h->m,
+                (long long)h->n, (long long)h->k, (long long)h->r, h->dtype, h->uniform ? 1 : 0,
+                h->prop ? 1 : 0, h->shadow ? 1 : 0, h->tc_on ? 1 : 0, h->itc_on ? 1 : 0,
+                h->opts.eps > 0.0 ? 1 : 0, ph, pend);
+  return b;
+}
+static bool gpool_ok(const wlr_ctx* h) { return !h->comm && !h->vg && !h->rp_time; }
+
 static wlr_status build_graph(wlr_ctx* h, int ph, int pend) {
   cudaGraph_t g;
   wlr_status s = capture_graph(h, ph, pend, &g);
   if (s != WLR_OK) return s;
+  if (gpool_ok(h)) {
+    cudaGraphExec_t ex = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(g_gpool_mu);
+      auto it = g_gpool.find(gpool_key(h, ph, pend));
+      if (it != g_gpool.end() && !it->second.empty()) { ex = it->second.back(); it->second.pop_back(); }
+    }
+    if (ex) {
+      cudaGraphExecUpdateResultInfo info{};
+      if (cudaGraphExecUpdate(ex, g, &info) == cudaSuccess) {
+        h->gexec[ph][pend] = ex;
+        cudaGraphDestroy(g);
+        return WLR_OK;
+      }
+      cudaGetLastError();
+      cudaGraphExecDestroy(ex);
+    }
+  }
   CUDA_TRY(h, cudaGraphInstantiate(&h->gexec[ph][pend], g, 0));
   cudaGraphDestroy(g);
   return WLR_OK;
@@ -1945,9 +1984,18 @@ extern "C" const char* wlr_status_string(int32_t s) {
 extern "C" void wlr_destroy(wlr_handle h) {
   if (!h) return;
   if (h->st) cudaStreamSynchronize(h->st);
-  for (auto& gp : h->gexec)
-    for (auto& g : gp)
-      if (g) cudaGraphExecDestroy(g);
+  for (int ph = 0; ph < 6; ++ph)
+    for (int pend = 0; pend < 2; ++pend) {
+      cudaGraphExec_t g = h->gexec[ph][pend];
+      if (!g) continue;
+      bool kept = false;
+      if (gpool_ok(h)) {                           // (see build_graph: a later handle updates it)
+        std::lock_guard<std::mutex> lk(g_gpool_mu);
+        auto& v = g_gpool[gpool_key(h, ph, pend)];
+        if (v.size() < 4) { v.push_back(g); kept = true; }
+      }
+      if (!kept) cudaGraphExecDestroy(g);
+    }
   if (h->comm && g_nccl.commDestroy) g_nccl.commDestroy(h->comm);
   if (h->st2) cudaStreamSynchronize(h->st2);
   for (void* p : h->allocs) {
