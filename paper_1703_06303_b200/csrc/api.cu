@@ -226,6 +226,8 @@ struct wlr_ctx {
   cudaGraphExec_t gexec[6][2] = {};   // [phase][deferred pending]
   cudaStream_t st2 = nullptr;  // side stream of the deferred small-step half
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool zero_defer = false;     // dalloc defers its zeroing to flush_zero (init allocation block)
+  std::vector<std::pair<void*, int64_t>> zero_list;
   bool pending = false;        // deferred half of the last small step not launched yet
   // One graph per phase: it always holds K3b(p-1); when that half already ran (flush_pending, or
   // the GHS step at init) the host sets flags[7] and the graph's K3b clears it and returns
@@ -306,8 +308,26 @@ static wlr_status dalloc(wlr_ctx* h, void** p, size_t bytes) {
     return fail(h, WLR_ENOMEM, std::string("cudaMalloc failed: ") + cudaGetErrorString(e));
   }
   h->allocs.push_back(*p);
+  if (h->zero_defer) {                         // (init: zeroed together by flush_zero)
+    h->zero_list.push_back({*p, (int64_t)(bytes ? bytes : 16)});
+    return WLR_OK;
+  }
   e = cudaMemsetAsync(*p, 0, bytes ? bytes : 16, h->st);
   if (e != cudaSuccess) return fail(h, WLR_ECUDA, cudaGetErrorString(e));
+  return WLR_OK;
+}
+// Zero every allocation deferred since zero_defer was set, with one kernel per 64 buffers (the
+// initialisation allocates ~80 buffers between its first kernels; one memset each cost ~0.3 ms of
+// launch-bound host time)
+static wlr_status flush_zero(wlr_ctx* h) {
+  h->zero_defer = false;
+  for (size_t i = 0; i < h->zero_list.size(); i += kZeroList) {
+    ZeroList z{};
+    z.n = (int)std::min<size_t>(kZeroList, h->zero_list.size() - i);
+    for (int j = 0; j < z.n; ++j) { z.ptr[j] = h->zero_list[i + j].first; z.bytes[j] = h->zero_list[i + j].second; }
+    CUDA_TRY(h, launch_zero_list(z, h->st));
+  }
+  h->zero_list.clear();
   return WLR_OK;
 }
 template <typename P>
@@ -974,6 +994,8 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   // Grams overlap it instead of waiting on a synchronisation here
   if (h->dtype == WLR_F32) launch_validate<float>((const float*)h->A, h->lda, h->m, (int)h->n, (const float*)h->W1, h->ldw, (int)h->k, h->flags, h->st);
   else launch_validate<double>((const double*)h->A, h->lda, h->m, (int)h->n, (const double*)h->W1, h->ldw, (int)h->k, h->flags, h->st);
+  h->zero_defer = true;                        // the allocations below are zeroed by flush_zero, before
+                                               // the first kernel that reads them (init_x1 below)
 
   // ---- sizes of the per-iteration kernels
   const int64_t k = h->k, n = h->n, nk = h->nk, t = h->t, kp = h->kp;
@@ -1279,6 +1301,7 @@ static wlr_status do_init(wlr_ctx* h, const void* A, const void* W1) {
   if ((s = dalloc_t(h, &part, (size_t)gsplit * n * n)) != WLR_OK) return s;
   if ((s = dalloc_t(h, &gram, (size_t)n * n)) != WLR_OK) return s;
   const char* A2 = (const char*)h->A + k * es;
+  if ((s = flush_zero(h)) != WLR_OK) return s;
   if (h->dtype == WLR_F32) {
     if (o.init == WLR_INIT_GIVEN) launch_init_x1<float>((const float*)h->opts.x1_0, k, h->m, (int)k, (int)kp, (float*)h->X[0], h->st);
     else launch_init_x1<float>((const float*)h->A, h->lda, h->m, (int)k, (int)kp, (float*)h->X[0], h->st);

@@ -93,6 +93,24 @@ template void launch_gram64<float>(const float*, int64_t, int, const float*, int
 template void launch_gram64<double>(const double*, int64_t, int, const double*, int64_t, int,
                                     int64_t, double*, int, double*, cudaStream_t);
 
+// Zero a list of buffers (pool allocations: 256-byte aligned): every thread of the grid strides
+// over each buffer in turn in 16-byte stores, the tail bytes singly
+__global__ void zero_list_kernel(const __grid_constant__ ZeroList z) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+  for (int j = 0; j < z.n; ++j) {
+    const int64_t nb = z.bytes[j], n16 = nb / 16;
+    int4* p = reinterpret_cast<int4*>(z.ptr[j]);
+    for (int64_t i = tid; i < n16; i += nt) p[i] = make_int4(0, 0, 0, 0);
+    char* c = reinterpret_cast<char*>(z.ptr[j]);
+    for (int64_t i = 16 * n16 + tid; i < nb; i += nt) c[i] = 0;
+  }
+}
+cudaError_t launch_zero_list(const ZeroList& z, cudaStream_t st) {
+  if (z.n <= 0) return cudaSuccess;
+  zero_list_kernel<<<1184, 256, 0, st>>>(z);
+  return cudaGetLastError();
+}
+
 // X1 buffer (m x kp, zero padded) := first k columns of src (ld lds)
 template <typename T>
 __global__ void init_x1_kernel(const T* __restrict__ src, int64_t lds, int64_t m, int k, int kp,

@@ -137,6 +137,9 @@ bool prop_gay_ok(int n, int k, int b, int nsm);   // prop1 computes G_A Y of the
 // eps mode: flags[6] = flags[2] (the converged flag) at the start of an iteration, one thread, so that
 // every kernel of the iteration (clusters included) sees one consistent value
 cudaError_t launch_stop_latch(int* flags, cudaStream_t st);
+constexpr int kZeroList = 64;
+struct ZeroList { void* ptr[kZeroList]; int64_t bytes[kZeroList]; int n; };
+cudaError_t launch_zero_list(const ZeroList& z, cudaStream_t st);   // zero n buffers in one launch
 cudaError_t launch_noop(cudaStream_t st);    // an empty kernel (launch ordering, api.cu)
 cudaError_t launch_vsum(double* out, const double* in, int G, size_t stride, size_t count, cudaStream_t st);
 cudaError_t launch_prop(const PropArgs& a, bool f64, int pdl, cudaStream_t st, cudaEvent_t after1 = nullptr);
