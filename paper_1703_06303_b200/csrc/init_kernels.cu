@@ -24,17 +24,30 @@ __global__ void __launch_bounds__(256) gram64_kernel(const T* __restrict__ L, in
   const int64_t rb0 = (int64_t)blockIdx.z * rows_per_split;
   const int64_t re = rb0 + rows_per_split < m ? rb0 + rows_per_split : m;
   double acc[4][4] = {};
-  for (int64_t rb = rb0; rb < re; rb += 16) {
+  // the next 16 rows' operands are loaded into registers while this step computes (software
+  // pipelined: the step's global-load latency was exposed once per 16 rows)
+  T lv[4], rv[4];
+  auto fetch = [&](int64_t rb) {
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int idx = threadIdx.x + e * 256;
       const int rr = idx / 64, cc = idx % 64;
       const int64_t row = rb + rr;
       const bool ok = row < re;
-      Ls[rr][cc] = (ok && i0 + cc < nl) ? (double)L[row * ldl + i0 + cc] : 0.0;
-      Rs[rr][cc] = (ok && j0 + cc < nr) ? (double)R[row * ldr + j0 + cc] : 0.0;
+      lv[e] = (ok && i0 + cc < nl) ? L[row * ldl + i0 + cc] : T(0);
+      rv[e] = (ok && j0 + cc < nr) ? R[row * ldr + j0 + cc] : T(0);
+    }
+  };
+  if (rb0 < re) fetch(rb0);
+  for (int64_t rb = rb0; rb < re; rb += 16) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int idx = threadIdx.x + e * 256;
+      Ls[idx / 64][idx % 64] = (double)lv[e];
+      Rs[idx / 64][idx % 64] = (double)rv[e];
     }
     __syncthreads();
+    if (rb + 16 < re) fetch(rb + 16);
 #pragma unroll
     for (int kk = 0; kk < 16; ++kk) {
       double a[4], b[4];
