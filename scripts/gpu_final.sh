@@ -2,7 +2,7 @@
 # Final measurement session (one GPU): GPU tests, bench lines for configs 3/4/5, the ncu launch
 # list of the config-3 bench command, one ncu --set full capture of the config-3 and config-4
 # kernels at steady state, CUPTI timelines.  Outputs under gpurun_out/final/.
-O=gpurun_out/final5
+O=gpurun_out/final
 mkdir -p $O
 nvidia-smi > $O/nvidia_smi.txt 2>&1
 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $O/pytest_gpu.log
