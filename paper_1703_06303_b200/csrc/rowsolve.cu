@@ -21,7 +21,8 @@
 //     L[a, J] = T[a, J] L_JJ^{-T} (36 FMAs per row) and store their 8 entries.
 //   * Back substitution x L = z by 8-column blocks from the right: the block's z values are
 //     published through shared memory, x_B = z_B L_BB^{-1} redundantly per lane, and every own
-//     row b < 8P subtracts sum_i x_i L[8P + i, b] (one float4 pair per row).
+//     row b < 8P subtracts sum_i x_i L[8P + i, b] (one float4 pair per row; full blocks as two
+//     packed FFMA2 chains of four).
 // Storage per warp: the factor in 8-row blocks, block J = rows [8J, 8J + 8) stored [t][8]
 // (t < 8J + 8; upper parts unused), block base 32 J (J + 1) + 8 J floats, so that any 32
 // consecutive rows hit 32 distinct banks for a fixed column t; plus an 8 x 8 scratch, 1/L_jj
@@ -53,6 +54,16 @@ WLR_DEVI void ffma2_neg(float& a0, float& a1, float x, float b0, float b1) {
   unsigned long long A, X, B;
   asm("mov.b64 %0, {%1, %2};" : "=l"(A) : "f"(a0), "f"(a1));
   asm("mov.b64 %0, {%1, %1};" : "=l"(X) : "f"(-x));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(B) : "f"(b0), "f"(b1));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(A) : "l"(X), "l"(B));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(A));
+}
+
+// (a0, a1) += (x0, x1) * (b0, b1) as ONE packed FFMA2 (both operands per element)
+WLR_DEVI void ffma2_vv(float& a0, float& a1, float x0, float x1, float b0, float b1) {
+  unsigned long long A, X, B;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(A) : "f"(a0), "f"(a1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(X) : "f"(x0), "f"(x1));
   asm("mov.b64 %0, {%1, %2};" : "=l"(B) : "f"(b0), "f"(b1));
   asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(A) : "l"(X), "l"(B));
   asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(A));
@@ -152,8 +163,8 @@ WLR_DEVI void rs_gemm(float (&acc)[NQ][8], const uint32_t (&sa)[NQ], uint32_t sb
 // the bordered row k), issued one panel ahead so that their L1 / L2 latency hides behind the
 // current panel.  Rows below 8P are finished: nothing to load.
 template <int NQ>
-WLR_DEVI void rs_fetch(float (&sn)[NQ][8], const int (&arow)[NQ], const float* __restrict__ S,
-                       const float* __restrict__ er, int k, int k8, int P) {
+WLR_DEVI void rs_fetch_rc(float (&sn)[NQ][8], const int (&arow)[NQ], const float* __restrict__ S,
+                          const float* __restrict__ er, int k, int k8, int P) {
   const int J0 = 8 * P;
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
@@ -166,6 +177,29 @@ WLR_DEVI void rs_fetch(float (&sn)[NQ][8], const int (&arow)[NQ], const float* _
     }
   }
 }
+
+// the same from per-pixel-row resolved row pointers (measured faster at NQ >= 4, slower at NQ = 2)
+// src[q]: the own row's K row (row r of S, or e_i for r = k), resolved once per pixel row
+template <int NQ>
+WLR_DEVI void rs_fetch(float (&sn)[NQ][8], const int (&arow)[NQ], const float* const (&src)[NQ], int P) {
+  const int J0 = 8 * P;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    if (arow[q] >= J0) {
+      const float4* s4 = reinterpret_cast<const float4*>(src[q] + J0);
+      const float4 u0 = __ldg(s4), u1 = __ldg(s4 + 1);
+      sn[q][0] = u0.x; sn[q][1] = u0.y; sn[q][2] = u0.z; sn[q][3] = u0.w;
+      sn[q][4] = u1.x; sn[q][5] = u1.y; sn[q][6] = u1.z; sn[q][7] = u1.w;
+    }
+  }
+}
+
+#ifndef WLR_RS_BS2_NQ
+#define WLR_RS_BS2_NQ 1     // packed back substitution (measured faster at k = 50 and k = 100)
+#endif
+#ifndef WLR_RS_SROW_NQ
+#define WLR_RS_SROW_NQ 4    // K-row pointers resolved once per pixel row
+#endif
 
 template <int NQ>
 __global__ void __launch_bounds__(32) row_solve_kernel(const __grid_constant__ RowSolveArgs a) {
@@ -197,7 +231,16 @@ __global__ void __launch_bounds__(32) row_solve_kernel(const __grid_constant__ R
   bool spd = true;
   float sn[NQ][8];
   int64_t row = blockIdx.x;
-  if (row < a.m) rs_fetch<NQ>(sn, arow, S, a.E + row * kp, k, k8, 0);
+  // own K rows: rows of S are fixed; the bordered row k points at e_i of the current / next pixel row
+  const float* srow[NQ];
+  const float* snext[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) srow[q] = arow[q] < k ? S + (int64_t)max(arow[q], 0) * k8 : a.E + row * kp;
+  constexpr bool kSrow = NQ >= WLR_RS_SROW_NQ;
+  if (row < a.m) {
+    if constexpr (kSrow) rs_fetch<NQ>(sn, arow, srow, 0);
+    else rs_fetch_rc<NQ>(sn, arow, S, a.E + row * kp, k, k8, 0);
+  }
   // the row's X1_p, A1 and W1 values (lane + 32 q), software-pipelined one row ahead: W1^2 (the panel
   // diagonals) and A1 . W1^2 (e_lin) are needed at the start of a row, where a fresh load's DRAM
   // latency would be exposed; X1_p and A1 again at its end (Delta, f_w)
@@ -213,7 +256,8 @@ __global__ void __launch_bounds__(32) row_solve_kernel(const __grid_constant__ R
   };
   load_row(row);
   for (; row < a.m; row += gridDim.x) {
-    const float* er = a.E + row * kp;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) snext[q] = arow[q] < k ? srow[q] : a.E + (row + gridDim.x) * kp;
     float xold[NQ], a1v[NQ], w1v[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) { xold[q] = xon[q]; a1v[q] = a1n[q]; w1v[q] = w1n[q]; }
@@ -242,8 +286,13 @@ __global__ void __launch_bounds__(32) row_solve_kernel(const __grid_constant__ R
         acc[0][6] = fmaf(m0, c1.z, acc[0][6]); acc[0][7] = fmaf(m0, c1.w, acc[0][7]);
       }
       {   // the next panel's K entries (or panel 0 of this warp's next row)
-        const int64_t rn = P + 1 < npan ? row : row + gridDim.x;
-        if (rn < a.m) rs_fetch<NQ>(sn, arow, S, a.E + rn * kp, k, k8, P + 1 < npan ? P + 1 : 0);
+        if constexpr (kSrow) {
+          if (P + 1 < npan) rs_fetch<NQ>(sn, arow, srow, P + 1);
+          else if (row + gridDim.x < a.m) rs_fetch<NQ>(sn, arow, snext, 0);
+        } else {
+          const int64_t rn = P + 1 < npan ? row : row + gridDim.x;
+          if (rn < a.m) rs_fetch_rc<NQ>(sn, arow, S, a.E + rn * kp, k, k8, P + 1 < npan ? P + 1 : 0);
+        }
       }
       const uint32_t sb = (uint32_t)__cvta_generic_to_shared(Lw + rs_base(P));
       const int nqa = min(NQ, (k - J0) / 32 + 1);  // q-blocks holding a row >= J0
@@ -395,18 +444,38 @@ __global__ void __launch_bounds__(32) row_solve_kernel(const __grid_constant__ R
             if (i < nb) xo[J0 + i] = x[i];
         }
       }
+      if (NQ >= WLR_RS_BS2_NQ && nb == 8) {          // full block: two packed chains of four FFMA2
+        float nx[8];
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) {
-        const int r = arow[q];
-        if (r >= 0 && r < J0) {
-          const float4 c0 = reinterpret_cast<const float4*>(Lb + 8 * r)[0];            // L[J0 + i, r]
-          const float4 c1 = reinterpret_cast<const float4*>(Lb + 8 * r)[1];
-          const float cc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-          float v = zr[q];
+        for (int i = 0; i < 8; ++i) nx[i] = -x[i];
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
-            if (i < nb) v = fmaf(-x[i], cc[i], v);
-          zr[q] = v;
+        for (int q = 0; q < NQ; ++q) {
+          const int r = arow[q];
+          if (r >= 0 && r < J0) {
+            const float4 c0 = reinterpret_cast<const float4*>(Lb + 8 * r)[0];          // L[J0 + i, r]
+            const float4 c1 = reinterpret_cast<const float4*>(Lb + 8 * r)[1];
+            float v0 = zr[q], v1 = 0.f;
+            ffma2_vv(v0, v1, nx[0], nx[1], c0.x, c0.y);
+            ffma2_vv(v0, v1, nx[2], nx[3], c0.z, c0.w);
+            ffma2_vv(v0, v1, nx[4], nx[5], c1.x, c1.y);
+            ffma2_vv(v0, v1, nx[6], nx[7], c1.z, c1.w);
+            zr[q] = v0 + v1;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const int r = arow[q];
+          if (r >= 0 && r < J0) {
+            const float4 c0 = reinterpret_cast<const float4*>(Lb + 8 * r)[0];
+            const float4 c1 = reinterpret_cast<const float4*>(Lb + 8 * r)[1];
+            const float cc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+            float v = zr[q];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (i < nb) v = fmaf(-x[i], cc[i], v);   // (entries beyond k in the last block: never set)
+            zr[q] = v;
+          }
         }
       }
       __syncwarp();
@@ -424,6 +493,8 @@ __global__ void __launch_bounds__(32) row_solve_kernel(const __grid_constant__ R
         fw += w * w * dd * dd;
       }
     }
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) srow[q] = snext[q];
     __syncwarp();
   }
   if (!spd) raise_flag(a.flags, DF_ROWSPD);
