@@ -503,6 +503,9 @@ def main():
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "init_ms": t_init * 1e3,
+            # distribution of the K individually timed steps on this rank (value = their mean)
+            "step_ms_stats": {"median": statistics.median(step_ms), "min": min(step_ms), "max": max(step_ms),
+                              "p90": sorted(step_ms)[min(len(step_ms) - 1, int(0.9 * len(step_ms)))]},
             "final": {"F": F, "step": step_norm, "rel": rel},
             "peaks_source": peak_kind,
         }
